@@ -1,0 +1,33 @@
+"""CPU oracle for the single-pass randomized ID ingest path (arxiv 2405.16076).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import anything
+in this package.  The product path (``paper_2405_16076_b200``) never imports it
+and shares no code with it: the oracle re-implements the Philox stream, the
+Gauss-256 sketch entries, the selection draws and every arithmetic step on its
+own, in plain numpy fp64, following the paper step by step.
+
+Citation tags: ``P:n`` = line n of the paper's LaTeX source;
+readings R1..R14 are listed in DESIGN.md section 3.
+
+Parity-pin status per function:
+  philox4x32_10        pinned (Random123 / cuRAND known-answer vectors)
+  gauss256_table       pinned (symmetry, independent erfc bisection, moments)
+  sketch / ingest      pinned (identity sketch, slab additivity, JL statistics)
+  ridge scores         pinned (exact leverage at lambda=0, closed form at lambda>0,
+                       hand case A=I2, Lemma 1 direction)
+  selection            pinned (C1 block 1 forced admissions, MC frequencies)
+  Alg 4 coefficients   pinned (exact recovery, self-representation, identity sketch)
+  NA-Hutch++ estimate  pinned (P=0 case, exactness, unbiasedness over seeds)
+  ridge scores at lambda>0 with Gaussian sketch / Bernoulli trajectories on
+  C2-C5 are "parity unpinned" beyond the above.
+"""
+
+from .philox import philox4x32_10, uniform24
+from .gauss256 import gauss256_table, gauss256_scale, omega_rows
+from .oid import OracleParams, OracleOID, ridge_scores, hutchpp_estimate, alg4_coefficients
+
+__all__ = [
+    "philox4x32_10", "uniform24", "gauss256_table", "gauss256_scale", "omega_rows",
+    "OracleParams", "OracleOID", "ridge_scores", "hutchpp_estimate", "alg4_coefficients",
+]

@@ -1,0 +1,372 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix (not against itself).
+
+Each test names the passage it follows.  P:n = PAPER.md line n, S:n = SPEC.md line n.
+"""
+
+import itertools
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import philox4x32_10, uniform24, gauss256_table, gauss256_scale, omega_rows
+from oracle.oid import (OracleParams, OracleOID, ridge_scores, ridge_lambda, eig_gram, select,
+                        alg4_coefficients, hutchpp_estimate, sketch)
+from synth import c1_matrix, low_rank_matrix
+
+
+def _params(m, k, ell, lam, seed=0, split=None, **kw):
+    if split is None:
+        a, b = ell // 6, ell // 3
+        split = (a, b, ell - a - b)
+    return OracleParams(m=m, k=k, ell=ell, ell1=split[0], ell2=split[1], ell3=split[2], lam=lam, seed=seed, **kw)
+
+
+# ------------------------------------------------------------------ Philox (reading R1)
+
+def test_philox_known_answer_vectors(golden_dir):
+    rows = [l.split() for l in open(os.path.join(golden_dir, "philox4x32_10_kat.txt")) if l.strip() and not l.startswith("#")]
+    assert len(rows) == 6
+    for r in rows:
+        c0, c1, c2, c3, k0, k1 = (int(x, 16) for x in r[:6])
+        want = [int(x, 16) for x in r[6:]]
+        got = [int(x) for x in philox4x32_10(c0, c1, c2, c3, k0, k1)]
+        assert got == want
+
+
+def test_uniform24_grid_and_range():
+    u = uniform24(12345, np.arange(5000), 3, 7)
+    assert np.all(u >= 0) and np.all(u < 1)
+    assert np.all(u * 2 ** 24 == np.floor(u * 2 ** 24))
+    assert abs(u.mean() - 0.5) < 4 * math.sqrt(1 / 12 / u.size)
+
+
+# ------------------------------------------------------------------ Gauss-256 (reading R2)
+
+def _inv_norm_bisect(p):
+    """Independent inverse normal CDF: bisection on 0.5*erfc(-x/sqrt 2) (stdlib libm)."""
+    lo, hi = -10.0, 10.0
+    for _ in range(200):
+        mid = 0.5 * (lo + hi)
+        if 0.5 * math.erfc(-mid / math.sqrt(2.0)) < p:
+            lo = mid
+        else:
+            hi = mid
+    return 0.5 * (lo + hi)
+
+
+def test_gauss256_table_independent_construction():
+    q = gauss256_table()
+    want = [round(44.0 * _inv_norm_bisect((u + 0.5) / 256.0)) for u in range(256)]
+    assert list(q) == want
+    assert np.all(q == -q[::-1])                  # odd about u = 127.5 -> mean exactly 0
+    assert q.min() == -127 and q.max() == 127     # fits int8
+    assert np.all(np.diff(q) >= 0)
+
+
+def test_gauss256_unit_variance_and_shape():
+    q = gauss256_table().astype(np.float64)
+    s = gauss256_scale()
+    assert abs(s * s * np.mean(q * q) - 1.0) < 4e-16
+    z = s * q
+    # discretised N(0,1): KS distance of the equiprobable 256-point law is ~1/256
+    from scipy.stats import norm
+    ks = np.max(np.abs((np.arange(1, 257) - 0.5) / 256 - norm.cdf(z)))
+    assert ks < 0.006
+    kurt = np.mean(z ** 4)
+    assert 2.85 < kurt < 3.0
+
+
+def test_omega_bytes_uniform_and_moments():
+    Z = omega_rows(7, np.arange(64), 0, 1 << 14).astype(np.float64) * gauss256_scale()
+    n = Z.size
+    assert abs(Z.mean()) < 4 / math.sqrt(n)
+    assert abs(Z.var() - 1.0) < 4 * math.sqrt(2.0 / n)
+    # rows independent: empirical correlation of two sketch rows ~ 0
+    c = np.corrcoef(Z[0], Z[1])[0, 1]
+    assert abs(c) < 4 / math.sqrt(Z.shape[1])
+
+
+def test_omega_rows_offsets_consistent():
+    full = omega_rows(3, np.arange(5), 0, 200)
+    part = omega_rows(3, np.arange(5), 37, 133)
+    assert np.array_equal(full[:, 37:133], part)
+
+
+# ------------------------------------------------------------------ sketch
+
+def test_sketch_slab_additivity():
+    """Philox is keyed on GLOBAL rows, so shard sketches sum to the full sketch."""
+    X = np.random.default_rng(0).standard_normal((1000, 7))
+    p = _params(1000, 4, 12, 0.0, seed=9)
+    Y = sketch(p, X)
+    cut = 377
+    p1 = _params(1000, 4, 12, 0.0, seed=9, row_begin=0, row_end=cut)
+    p2 = _params(1000, 4, 12, 0.0, seed=9, row_begin=cut, row_end=1000)
+    Ys = sketch(p1, X[:cut]) + sketch(p2, X[cut:])
+    assert np.allclose(Y, Ys, rtol=1e-13, atol=1e-13)
+
+
+def test_sketch_identity_mode():
+    """Identity sketch (Omega = I, l = m) makes S = A exactly."""
+    X = np.random.default_rng(1).standard_normal((40, 5))
+    p = _params(40, 4, 40, 0.0)
+    Y = sketch(p, X, Qcache=np.eye(40) / gauss256_scale())
+    assert np.allclose(Y, X, rtol=1e-15, atol=1e-15)
+
+
+def test_sketch_jl_norm_statistic():
+    """E ||Omega a||^2 = l ||a||^2 for unit-variance i.i.d. entries."""
+    rng = np.random.default_rng(2)
+    X = rng.standard_normal((2000, 200))
+    X /= np.linalg.norm(X, axis=0)
+    p = _params(2000, 4, 32, 0.0, seed=5)
+    Y = sketch(p, X)
+    r = np.sum(Y * Y, axis=0) / 32
+    assert abs(r.mean() - 1.0) < 4 * math.sqrt(2 / 32 / 200) + 0.01
+
+
+def test_gram_and_frob_invariants():
+    """SS^T accumulated column block by block equals S S^T; ||A_obs||^2 equals direct sum."""
+    A = np.random.default_rng(3).standard_normal((500, 48))
+    o = OracleOID(_params(500, 6, 24, 0.0, seed=1))
+    for b in range(6):
+        o.ingest_block(A[:, 8 * b:8 * b + 8])
+    assert np.allclose(o.gram, o.S @ o.S.T, rtol=1e-12, atol=1e-10)
+    assert math.isclose(o.frob2, float(np.sum(A * A)), rel_tol=1e-13)
+    assert o.n_obs == 48 and o.S.shape == (24, 48)
+
+
+# ------------------------------------------------------------------ ridge lambda / scores
+
+def test_topk_energy_worked_example():
+    """Gram = diag(4, 1), k = 1 -> E_k = 4."""
+    mu, W = eig_gram(np.diag([4.0, 1.0]))
+    p = _params(2, 1, 2, -2.0, split=(0, 1, 1))
+    lam, Ek = ridge_lambda(p, mu, 0.0, 5.0)
+    assert Ek == 4.0
+    assert lam == pytest.approx((5.0 - 4.0) / (2 * 1))
+
+
+def test_scores_lambda0_equal_exact_leverage():
+    """At lam = 0 and l >= rank(A): sketched scores equal exact leverage ||V(j,:)||^2 and sum to rank."""
+    A = low_rank_matrix(11, 300, 80, 7)
+    p = _params(300, 4, 20, 0.0, seed=4)
+    Y = sketch(p, A)
+    mu, W = eig_gram(Y @ Y.T)
+    tau = ridge_scores(mu, W, 0.0, Y)
+    U, s, Vt = np.linalg.svd(A, full_matrices=False)
+    lev = np.sum(Vt[:7] ** 2, axis=0)
+    assert np.max(np.abs(tau - lev)) < 1e-9
+    assert abs(tau.sum() - 7.0) < 1e-9
+
+
+def test_scores_closed_form_identity_sketch():
+    """Identity sketch: tau_j = sum_q sigma_q^2/(sigma_q^2 + lam) V_jq^2 (eq:ridge-leverage-score)."""
+    A = np.random.default_rng(5).standard_normal((30, 12))
+    lam = 0.7
+    mu, W = eig_gram(A @ A.T)
+    tau = ridge_scores(mu, W, lam, A)
+    U, s, Vt = np.linalg.svd(A, full_matrices=False)
+    want = np.sum((s ** 2 / (s ** 2 + lam))[:, None] * Vt ** 2, axis=0)
+    assert np.allclose(tau, want, rtol=1e-11, atol=1e-13)
+
+
+def test_scores_hand_case(golden_dir):
+    """A = I_2, k = 1 -> lam = ||A - A_1||^2/1 = 1, tau = 0.5 each."""
+    A = np.eye(2)
+    mu, W = eig_gram(A @ A.T)
+    tau = ridge_scores(mu, W, 1.0, A)
+    assert np.allclose(tau, [0.5, 0.5], atol=1e-15)
+
+
+def test_scaled_unscaled_equivalence():
+    """Reading R3: (Y/sqrt l)^T (YY^T/l + lam I)^-1 (Y/sqrt l) == y^T (YY^T + l lam I)^+ y."""
+    rng = np.random.default_rng(6)
+    Y = rng.standard_normal((16, 40))
+    l, lam = 16, 0.3
+    S = Y / math.sqrt(l)
+    want = np.sum(S * np.linalg.solve(S @ S.T + lam * np.eye(l), S), axis=0)
+    mu, W = eig_gram(Y @ Y.T)
+    got = ridge_scores(mu, W, l * lam, Y)
+    assert np.allclose(got, want, rtol=1e-11)
+
+
+def test_lemma1_scores_decrease_when_columns_added():
+    """Lemma 1, reading R13: with lam fixed, tau_j([A b]) <= tau_j(A)."""
+    rng = np.random.default_rng(7)
+    worst = -np.inf
+    for _ in range(100):
+        m, n = rng.integers(3, 12), rng.integers(1, 10)
+        A = rng.standard_normal((m, n))
+        b = rng.standard_normal((m, 1)) * rng.uniform(0.1, 3)
+        lam = rng.uniform(0.01, 2)
+        mu, W = eig_gram(A @ A.T)
+        t0 = ridge_scores(mu, W, lam, A)
+        Ab = np.hstack([A, b])
+        mu, W = eig_gram(Ab @ Ab.T)
+        t1 = ridge_scores(mu, W, lam, A)
+        worst = max(worst, float(np.max(t1 - t0)))
+    assert worst <= 1e-12
+
+
+# ------------------------------------------------------------------ selection
+
+def test_c1_first_block_forced_admissions():
+    """On C1 block 1 every admission probability clamps to 1 (tau f >= 1), so J = 0..15 regardless of u."""
+    A = c1_matrix()
+    k = 20
+    s = np.linalg.svd(A, compute_uv=False)
+    lam = float(np.sum(s[k:] ** 2) / k)
+    o = OracleOID(_params(4096, 20, 48, lam, split=(16, 16, 16), seed=0))
+    lg = o.ingest_block(A[:, :16])
+    assert list(lg.J[:16]) == list(range(16)) and np.all(lg.J[16:] == -1)
+    assert np.all(lg.tau_cand * o.p.admission_factor() >= 1.0)
+    assert np.array_equal(o.C[:, :16], A[:, :16])      # bit-exact copies
+
+
+def test_no_eviction_when_scores_unchanged():
+    """tau_i == tau_old_i gives eviction probability 0."""
+    J = np.arange(5)
+    tau_old = np.full(5, 0.4)
+    for e in range(200):
+        J2, t2, adm, _ = select(1, e, J, tau_old, tau_old.copy(), np.array([0.9]), np.array([False]), 2.0, 100)
+        assert np.array_equal(J2, J) and not adm
+
+
+def test_admission_frequency_matches_probability():
+    """a single vacant slot admits with probability min(1, tau f)."""
+    trials = 4000
+    tau, f = 0.3, 1.0
+    hits = 0
+    for e in range(trials):
+        J2, _, adm, _ = select(77, e, np.array([-1]), np.ones(1), np.zeros(1), np.array([tau]), np.array([False]), f, 0)
+        hits += len(adm)
+    freq = hits / trials
+    assert abs(freq - tau) < 4 * math.sqrt(tau * (1 - tau) / trials)
+
+
+def test_first_success_and_consumption():
+    """Reading R4: first success wins, admitted candidates are consumed, zero columns skipped."""
+    J2, t2, adm, _ = select(5, 0, np.full(3, -1), np.ones(3), np.zeros(3),
+                            np.array([0.0, 1.0, 1.0, 1.0]), np.array([True, False, False, False]), 10.0, 50)
+    assert list(J2) == [51, 52, 53] and adm == [(0, 1), (1, 2), (2, 3)]
+    assert list(t2) == [1.0, 1.0, 1.0]
+
+
+# ------------------------------------------------------------------ Alg 4
+
+def _stream(A, params, b):
+    o = OracleOID(params)
+    for j in range(0, A.shape[1], b):
+        o.ingest_block(A[:, j:j + b])
+    return o
+
+
+def test_alg4_exact_recovery_rank_deficient():
+    """Exactly rank-r data, k >= r, l >= r => ||A - A_J P|| / ||A|| <= 1e-12 once rank(A_J) = r."""
+    A = low_rank_matrix(21, 200, 60, 5)
+    o = _stream(A, _params(200, 8, 24, 0.0, seed=3), 10)
+    err = np.linalg.norm(A - o.C @ o.P) / np.linalg.norm(A)
+    assert np.linalg.matrix_rank(o.C) == 5
+    assert err < 1e-12
+
+
+def test_alg4_self_representation():
+    """With S_J of full column rank, P(:, J_i) = e_i."""
+    A = np.random.default_rng(8).standard_normal((150, 40))
+    o = _stream(A, _params(150, 6, 20, 0.0, seed=2), 8)
+    occ = np.nonzero(o.J >= 0)[0]
+    sub = o.P[np.ix_(occ, o.J[occ])]
+    assert np.allclose(sub, np.eye(occ.size), atol=1e-12)
+
+
+def test_alg4_identity_sketch_is_least_squares():
+    """Identity sketch: Alg 4 equals the exact LS coefficients argmin ||A_J X - A|| (eq:coeff_ID1)."""
+    rng = np.random.default_rng(9)
+    A = rng.standard_normal((25, 30))
+    J = np.array([3, -1, 7, 12])
+    P, _ = alg4_coefficients(A, J)
+    X, *_ = np.linalg.lstsq(A[:, [3, 7, 12]], A, rcond=None)
+    assert np.allclose(P[[0, 2, 3]], X, atol=1e-12)
+    assert np.all(P[1] == 0.0)
+
+
+# ------------------------------------------------------------------ NA-Hutch++ 
+
+def test_hutchpp_p_zero_gives_frob():
+    """P = 0 => estimate^2 == ||A_obs||^2 exactly."""
+    rng = np.random.default_rng(10)
+    S = rng.standard_normal((24, 30))
+    out = hutchpp_estimate(S, rng.standard_normal((24, 5)), np.zeros((5, 30)), np.eye(5), 3.5, 4, 8, 12)
+    assert out["e2"] == 3.5 and out["T"] == 0.0
+
+
+def test_hutchpp_exact_when_reconstruction_exact():
+    """A = A_J P exactly => the NA-Hutch++ cross trace equals tr(A (A_J P)^T) (B~ exact when rank <= c1 l)."""
+    A = low_rank_matrix(12, 120, 40, 4)
+    p = _params(120, 6, 24, 0.0, seed=11, split=(6, 8, 10))
+    o = _stream(A, p, 8)
+    out = o.error_estimate()
+    T_true = float(np.trace(A.T @ (o.C @ o.P)))
+    assert abs(out["T"] - T_true) / np.sum(A * A) < 1e-10
+    assert abs(out["e2"]) / np.sum(A * A) < 1e-10
+
+
+def test_hutchpp_unbiased_over_sketch_seeds():
+    """NA-Hutch++ is unbiased for tr(A (A_J P)^T) given P: mean over seeds within 3 s.e."""
+    rng = np.random.default_rng(13)
+    m, n, t, ell = 150, 40, 5, 30
+    A = rng.standard_normal((m, n)) @ np.diag(np.linspace(2, 0.2, n))
+    J = np.arange(t)
+    P = rng.standard_normal((t, n)) * 0.3
+    G = A[:, J].T @ A[:, J]
+    T_true = float(np.trace(A @ (A[:, J] @ P).T))
+    diffs = []
+    for seed in range(300):
+        p = _params(m, t, ell, 0.0, seed=seed, split=(5, 10, 15))
+        S = sketch(p, A)
+        out = hutchpp_estimate(S, S[:, J], P, G, float(np.sum(A * A)), 5, 10, 15)
+        diffs.append((out["T"] - T_true) / np.sum(A * A))
+    d = np.array(diffs)
+    assert abs(d.mean()) < 3 * d.std(ddof=1) / math.sqrt(d.size)
+
+
+def test_hutchpp_estimate_quality_moderate_error():
+    """Error estimates are informative when ||E||^2/||A||^2 >= 1e-2 (S:439 style): |e^ - e|/e <= 0.5 in >= 80% of seeds."""
+    rng = np.random.default_rng(14)
+    A = low_rank_matrix(15, 300, 60, 6) + 0.3 * rng.standard_normal((300, 60))
+    ok = 0
+    runs = 20
+    for seed in range(runs):
+        o = _stream(A, _params(300, 6, 36, -1.0, seed=seed), 12)
+        e = np.linalg.norm(A - o.C @ o.P)
+        est = o.error_estimate()["est_abs"]
+        ok += abs(est - e) / e <= 0.5
+    assert ok >= 0.8 * runs
+
+
+# ------------------------------------------------------------------ whole-run bounds
+
+def test_brute_force_subset_lower_bound():
+    """min over all k-subsets of ||A - A_J A_J^+ A|| <= oracle error; truncated SVD error <= that."""
+    rng = np.random.default_rng(16)
+    A = low_rank_matrix(17, 40, 14, 4) + 0.05 * rng.standard_normal((40, 14))
+    o = _stream(A, _params(40, 3, 12, -1.0, seed=1), 7)
+    err = np.linalg.norm(A - o.C @ o.P)
+    best = min(np.linalg.norm(A - A[:, list(S)] @ np.linalg.pinv(A[:, list(S)]) @ A)
+               for S in itertools.combinations(range(14), 3))
+    s = np.linalg.svd(A, compute_uv=False)
+    assert math.sqrt(np.sum(s[3:] ** 2)) <= best + 1e-12
+    assert best <= err + 1e-12
+
+
+def test_exact_rank_stream_selects_full_rank_basis():
+    """rank-5 stream, t = 8 => selected basis has numerical rank 5 in >= 18/20 seeds."""
+    good = 0
+    for seed in range(20):
+        A = low_rank_matrix(100 + seed, 120, 48, 5)
+        o = _stream(A, _params(120, 8, 24, -1.0, seed=seed), 8)
+        good += np.linalg.matrix_rank(o.C, tol=1e-8 * np.linalg.norm(A)) == 5
+    assert good >= 18
