@@ -1,0 +1,173 @@
+/*
+ * oid.h — C ABI of liboid.so, the B200 (sm_100a) hot path of the single-pass online
+ * randomized interpolative decomposition with NA-Hutch++ error estimation
+ * (Li, Becker, Doostan, arxiv 2405.16076).  Citations: P:n = line n of the paper's LaTeX
+ * source; readings R1..R14 are in DESIGN.md section 3.
+ *
+ * Problem: A = [a_1 .. a_n] (m x n) arrives column by column; the library keeps a
+ * sketch S = Omega A_obs, a basis of t = k selected columns A_J and coefficients P with
+ * A_obs ~ A_J P (eqn:id), following Algorithm 3 with Algorithm 4
+ * coefficients and Algorithm 8 error estimates.
+ *
+ * Conventions for every entry point
+ *   - All matrices are column-major.  Device pointers are CUDA global memory on the context's
+ *     device; "stream" is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Every call returns an oid_status.  Parameters are validated before any data is touched
+ *     (OID_EINVAL / OID_ESHAPE); call order is checked (OID_ESTATE).  CUDA launch failures
+ *     return OID_ECUDA.  oid_last_error(ctx) returns a message for the last failure.
+ *   - Numerical degradation that is not an error (non-finite input, rank-deficient S_J,
+ *     negative estimated ||E||^2) is reported in flag bits (OID_FLAG_*), never silently.
+ *   - Ingest calls are asynchronous: nothing is copied to the host and the host never waits.
+ *   - Determinism: identical parameters and data give bitwise-identical J, P and estimates.
+ *   - The context is single-threaded.  With several row shards, all ranks make the same calls
+ *     in the same order (collective semantics) and reduce the exposed partial buffers between
+ *     the *_sketch/_begin and *_commit/_end halves (sum, fp64), e.g. with an NCCL all-reduce.
+ */
+#ifndef OID_H_
+#define OID_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct oid_ctx_s* oid_ctx;
+
+typedef enum {
+  OID_OK = 0,
+  OID_EINVAL = -1,   /* bad parameter values                                               */
+  OID_ESHAPE = -2,   /* ncols > b_max, ld < m_loc, capacity n_cap exceeded, small workspace */
+  OID_ENOMEM = -3,   /* host allocation failed                                              */
+  OID_ECUDA = -4,    /* CUDA error (launch, copy, no device / unsupported arch)             */
+  OID_ENCCL = -5,    /* reserved: collective failure reported by the caller's reducer       */
+  OID_ENUMERIC = -6, /* reserved                                                            */
+  OID_ESTATE = -7    /* call out of order (e.g. commit without sketch)                      */
+} oid_status;
+
+typedef enum { OID_F32 = 0, OID_F64 = 1 } oid_dtype;
+
+/* K1 (fused ingest) implementation.  Both are exact to fp64 rounding. */
+typedef enum {
+  OID_K1_AUTO = 0,      /* tensor-core path when available for the shape, else SIMT       */
+  OID_K1_SIMT_F64 = 1,  /* CUDA-core DFMA, Omega generated in registers                    */
+  OID_K1_TC_INT8 = 2    /* tcgen05 kind::i8, Omega bytes generated into shared memory,
+                           data split into exact int8 digits (sm_100a)                     */
+} oid_k1_mode;
+
+/* flag bits (oid_stats.flags, estimate out[6]) */
+#define OID_FLAG_NONFINITE_INPUT 1u   /* a block contained NaN/Inf (column norm not finite)   */
+#define OID_FLAG_SJ_RANK_DEFICIENT 2u /* S_J had singular values below the 1e-12 cutoff (R9)   */
+#define OID_FLAG_E2_NEGATIVE 4u       /* NA-Hutch++ ||E||^2 estimate < 0, clamped (R13 / S:434) */
+#define OID_FLAG_K1_RECOMPUTED 8u     /* tensor-core K1 re-ran a slab with exact exponents     */
+
+typedef struct {
+  int64_t m;          /* global rows (spatial points of one snapshot)              */
+  int64_t row_begin;  /* this shard's global rows [row_begin, row_end); Omega is keyed   */
+  int64_t row_end;    /*   on GLOBAL rows so the sketch is independent of the sharding   */
+  int64_t n_cap;      /* max columns ever ingested (sizes S: ell x n_cap, P: k x n_cap)  */
+  int32_t k;          /* target rank = basis size t (k = t)                        */
+  int32_t ell;        /* sketch rows l = k + p; 1 <= ell <= 1024                  */
+  int32_t b_max;      /* max columns per ingest call, 1..64                              */
+  int32_t ell1, ell2, ell3; /* NA-Hutch++ contiguous row split, sum = ell (R11)    */
+  double lambda;      /* >= 0 fixed ridge; -1 streaming surrogate;
+                         -2 sketch-tail surrogate (R8)                                   */
+  double eps, delta;  /* accuracy / failure probability of the admission rate    */
+  double c;           /* admission constant (R5: 1)                                      */
+  uint64_t seed;      /* Philox key (R1): tag 0 sketch entries, tag 1 selection draws    */
+  int32_t dtype;      /* oid_dtype of the snapshot data and of the stored basis          */
+  int32_t k1_mode;    /* oid_k1_mode                                                     */
+  int32_t profile;    /* 1: time K1 and the other kernel groups with CUDA events          */
+  int32_t device;     /* CUDA device ordinal the workspace lives on                      */
+} oid_params;
+
+typedef struct {
+  int64_t n_obs;          /* columns ingested so far                                    */
+  int64_t epochs;         /* non-empty ingest calls                                     */
+  int64_t launches;       /* kernels launched by this context                          */
+  int64_t k1_launches;    /* launches of the fused ingest kernel                        */
+  double k1_ms;           /* summed CUDA-event time of K1 (profile = 1), launch stream   */
+  double post_ms;         /* summed CUDA-event time of the post-pass (commit)           */
+  double est_ms;          /* summed CUDA-event time of error estimates                  */
+  uint32_t flags;         /* OR of OID_FLAG_* seen so far (read at this call; syncs)     */
+  int32_t k1_mode_used;   /* oid_k1_mode actually used by the last ingest               */
+} oid_stats_t;
+
+/* Size in bytes of the device workspace oid_init needs for these parameters.
+   Errors: OID_EINVAL on invalid parameters. */
+oid_status oid_workspace_query(const oid_params* p, size_t* bytes);
+
+/* Create a context.  workspace: caller-owned device buffer of >= oid_workspace_query bytes
+   (256-byte aligned), kept alive and untouched until oid_destroy.  stream: used for the
+   initial clears.  Errors: OID_EINVAL, OID_ESHAPE (workspace too small), OID_ECUDA. */
+oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* stream, oid_ctx* out);
+
+/* Single-shard ingest of one block = one epoch (R4): Alg 3 steps 9-27 for ncols columns,
+   then Alg 4.  X: device, m_loc x ncols, leading dimension ld >= m_loc, dtype p->dtype,
+   read by kernels enqueued on `stream`; X must stay valid until those kernels complete
+   (the caller may record an event after this call).  Global column indices continue from
+   the previous call (0-based).  ncols == 0 is a no-op.
+   Errors: OID_ESHAPE (ncols > b_max, ld < m_loc, n_obs + ncols > n_cap), OID_ECUDA. */
+oid_status oid_ingest_block(oid_ctx ctx, const void* X, int64_t ld, int32_t ncols, void* stream);
+
+/* Multi-shard ingest, first half: K1 on this shard's rows.  Afterwards the partial buffer
+   (oid_partials, which = 0) holds [Y (ell x ncols, col-major); n (ncols)] for this shard's rows;
+   the caller sums it over shards in place before oid_ingest_commit. */
+oid_status oid_ingest_sketch(oid_ctx ctx, const void* X, int64_t ld, int32_t ncols, void* stream);
+
+/* Multi-shard ingest, second half: Gram, ridge scores, selection, basis copy of this shard's
+   rows of the admitted columns (reads X again, admitted columns only), Alg 4.
+   Same X, ld, ncols as the preceding oid_ingest_sketch.  Errors: OID_ESTATE if no sketch. */
+oid_status oid_ingest_commit(oid_ctx ctx, const void* X, int64_t ld, int32_t ncols, void* stream);
+
+/* Device pointer and element count (fp64) of a partial buffer to be summed over shards:
+   which = 0: ingest partials ((ell + 1) * ncols of the last sketch);
+   which = 1: basis-Gram partials (k * k) of the last oid_estimate_begin. */
+oid_status oid_partials(oid_ctx ctx, int32_t which, double** dev_ptr, int64_t* count);
+
+/* NA-Hutch++ estimate of ||A_obs - A_J P||_F for the current J and P (Alg 8).
+   _begin computes this shard's part of G = A_J^T A_J; after the caller's reduction
+   _end evaluates eq:NAhutchPP_2nd_term and eq:NAhutchPP_expansion.
+   out_dev: device array of 8 doubles receiving
+     [0] ||E||^2 estimate (unclamped), [1] T = estimate of tr(A (A_J P)^T), [2] tr(G P P^T),
+     [3] ||A_obs||_F^2, [4] ||E||_F estimate (clamped at 0), [5] relative estimate,
+     [6] flags (as double), [7] kappa(S_J).  Errors: OID_ESTATE before the first block. */
+oid_status oid_estimate_begin(oid_ctx ctx, void* stream);
+oid_status oid_estimate_end(oid_ctx ctx, double* out_dev, void* stream);
+
+/* Single-shard convenience: begin + end, then copies the 8 values to host memory out_host
+   (synchronizes `stream`). */
+oid_status oid_error_estimate(oid_ctx ctx, double* out_host, void* stream);
+
+/* Final outputs: J (k int64 to host memory, slot order, -1 = vacant) and
+   P (k x n_obs, column-major, ld = k) to device memory (P_on_device = 1) or host memory
+   (0); basis_dev (may be NULL): device m_loc x k buffer (ld = m_loc, dtype) receiving the
+   basis slab A_J (vacant columns zero).  Synchronizes `stream`.  The context stays usable. */
+oid_status oid_finalize(oid_ctx ctx, int64_t* J_host, double* P, int32_t P_on_device,
+                        void* basis_dev, void* stream);
+
+/* Copy internal state to host memory (synchronizes `stream`), for tests and diagnostics.
+   field: 0 J (k int64), 1 tau_old (k), 2 S (ell x n_obs), 3 Gram (ell x ell),
+          4 scalars [frob2, lambda_eff, E_k, shift, trace, dmax, min_margin, kappa],
+          5 last scores (k + ncols: basis slots then candidates), 6 eigenvalues of Gram (ell),
+          7 last ingest partials ((ell+1) * ncols), 8 S_J^+ (k x ell). */
+oid_status oid_get(oid_ctx ctx, int32_t field, void* host_dst, size_t bytes, void* stream);
+
+/* Counters and CUDA-event timings (synchronizes the context's recorded events).
+   oid_stats_reset clears the launch counters and the recorded timings. */
+oid_status oid_stats(oid_ctx ctx, oid_stats_t* out);
+oid_status oid_stats_reset(oid_ctx ctx);
+
+/* Host-only: the Gauss-256 sketch-entry table q[0..255] and scale s (reading R2,
+   Omega = s * q[u]); needs no GPU. */
+oid_status oid_sketch_table(int32_t q[256], double* scale);
+
+void oid_destroy(oid_ctx ctx);
+const char* oid_last_error(oid_ctx ctx);
+const char* oid_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OID_H_ */

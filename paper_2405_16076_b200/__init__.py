@@ -1,0 +1,249 @@
+"""Python binding of liboid.so (include/oid.h): argument marshalling only.
+
+Every step of the ingest path runs in the library's CUDA kernels; PyTorch supplies device
+memory (the workspace and the snapshot blocks), streams and, for row-sharded runs,
+torch.distributed for the all-reduce of the exposed partial buffers.  There is no CPU
+fallback: importing fails if liboid.so has not been built (``python
+paper_2405_16076_b200/build.py`` or ``__graft_entry__.build()``).
+"""
+
+import ctypes
+import math
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liboid.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python {_HERE}/build.py` "
+                      "(the product path has no CPU fallback)")
+_lib = ctypes.CDLL(LIB_PATH)
+
+OID_OK, OID_EINVAL, OID_ESHAPE, OID_ENOMEM, OID_ECUDA, OID_ENCCL, OID_ENUMERIC, OID_ESTATE = 0, -1, -2, -3, -4, -5, -6, -7
+_STATUS = {0: "OID_OK", -1: "OID_EINVAL", -2: "OID_ESHAPE", -3: "OID_ENOMEM", -4: "OID_ECUDA", -5: "OID_ENCCL",
+           -6: "OID_ENUMERIC", -7: "OID_ESTATE"}
+OID_F32, OID_F64 = 0, 1
+K1_AUTO, K1_SIMT_F64, K1_TC_INT8 = 0, 1, 2
+FLAG_NONFINITE_INPUT, FLAG_SJ_RANK_DEFICIENT, FLAG_E2_NEGATIVE, FLAG_K1_RECOMPUTED = 1, 2, 4, 8
+
+EXPORTED = ["oid_workspace_query", "oid_init", "oid_ingest_block", "oid_ingest_sketch", "oid_ingest_commit",
+            "oid_partials", "oid_estimate_begin", "oid_estimate_end", "oid_error_estimate", "oid_finalize", "oid_get",
+            "oid_stats", "oid_stats_reset", "oid_sketch_table", "oid_destroy", "oid_last_error", "oid_version"]
+
+
+class OidParams(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_int64), ("row_begin", ctypes.c_int64), ("row_end", ctypes.c_int64),
+                ("n_cap", ctypes.c_int64), ("k", ctypes.c_int32), ("ell", ctypes.c_int32), ("b_max", ctypes.c_int32),
+                ("ell1", ctypes.c_int32), ("ell2", ctypes.c_int32), ("ell3", ctypes.c_int32),
+                ("lam", ctypes.c_double), ("eps", ctypes.c_double), ("delta", ctypes.c_double), ("c", ctypes.c_double),
+                ("seed", ctypes.c_uint64), ("dtype", ctypes.c_int32), ("k1_mode", ctypes.c_int32),
+                ("profile", ctypes.c_int32), ("device", ctypes.c_int32)]
+
+
+class OidStats(ctypes.Structure):
+    _fields_ = [("n_obs", ctypes.c_int64), ("epochs", ctypes.c_int64), ("launches", ctypes.c_int64),
+                ("k1_launches", ctypes.c_int64), ("k1_ms", ctypes.c_double), ("post_ms", ctypes.c_double),
+                ("est_ms", ctypes.c_double), ("flags", ctypes.c_uint32), ("k1_mode_used", ctypes.c_int32)]
+
+
+_vp, _i64, _i32, _dp = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_double)
+_sig = {
+    "oid_workspace_query": [ctypes.POINTER(OidParams), ctypes.POINTER(ctypes.c_size_t)],
+    "oid_init": [ctypes.POINTER(OidParams), _vp, ctypes.c_size_t, _vp, ctypes.POINTER(_vp)],
+    "oid_ingest_block": [_vp, _vp, _i64, _i32, _vp],
+    "oid_ingest_sketch": [_vp, _vp, _i64, _i32, _vp],
+    "oid_ingest_commit": [_vp, _vp, _i64, _i32, _vp],
+    "oid_partials": [_vp, _i32, ctypes.POINTER(_dp), ctypes.POINTER(_i64)],
+    "oid_estimate_begin": [_vp, _vp],
+    "oid_estimate_end": [_vp, _vp, _vp],
+    "oid_error_estimate": [_vp, _dp, _vp],
+    "oid_finalize": [_vp, _vp, _vp, _i32, _vp, _vp],
+    "oid_get": [_vp, _i32, _vp, ctypes.c_size_t, _vp],
+    "oid_stats": [_vp, ctypes.POINTER(OidStats)],
+    "oid_stats_reset": [_vp],
+    "oid_sketch_table": [ctypes.POINTER(ctypes.c_int32), _dp],
+}
+for _n, _a in _sig.items():
+    getattr(_lib, _n).argtypes = _a
+    getattr(_lib, _n).restype = ctypes.c_int
+_lib.oid_destroy.argtypes = [_vp]
+_lib.oid_destroy.restype = None
+_lib.oid_last_error.argtypes = [_vp]
+_lib.oid_last_error.restype = ctypes.c_char_p
+_lib.oid_version.argtypes = []
+_lib.oid_version.restype = ctypes.c_char_p
+
+
+class OidError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def lib():
+    return _lib
+
+
+def version():
+    return _lib.oid_version().decode()
+
+
+def sketch_table():
+    """Host-only: (q[256] int32, scale) of the Gauss-256 sketch entries (reading R2)."""
+    q = (ctypes.c_int32 * 256)()
+    s = ctypes.c_double()
+    st = _lib.oid_sketch_table(q, ctypes.byref(s))
+    if st != OID_OK:
+        raise OidError(st, "oid_sketch_table")
+    return np.frombuffer(q, dtype=np.int32).copy(), s.value
+
+
+def hutch_split(ell):
+    a, b = ell // 6, ell // 3
+    return (a, b, ell - a - b)
+
+
+def make_params(m, k, ell, b_max, n_cap, lam, split=None, eps=0.5, delta=0.05, c=1.0, seed=0, dtype="f64",
+                row_begin=0, row_end=None, k1_mode=K1_AUTO, profile=False, device=0):
+    split = hutch_split(ell) if split is None else split
+    return OidParams(m=m, row_begin=row_begin, row_end=m if row_end is None else row_end, n_cap=n_cap, k=k, ell=ell,
+                     b_max=b_max, ell1=split[0], ell2=split[1], ell3=split[2], lam=lam, eps=eps, delta=delta, c=c,
+                     seed=seed, dtype=OID_F64 if dtype in ("f64", "float64") else OID_F32, k1_mode=k1_mode,
+                     profile=int(bool(profile)), device=device)
+
+
+def workspace_bytes(params):
+    n = ctypes.c_size_t()
+    st = _lib.oid_workspace_query(ctypes.byref(params), ctypes.byref(n))
+    if st != OID_OK:
+        raise OidError(st, "invalid parameters")
+    return n.value
+
+
+class Engine:
+    """One oid context on one CUDA device (C ABI calls with torch-owned memory)."""
+
+    def __init__(self, params, stream=None):
+        import torch
+        self._torch = torch
+        self.p = params
+        self.device = torch.device("cuda", params.device)
+        self.m_loc = params.row_end - params.row_begin
+        self.ws_bytes = workspace_bytes(params)
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        h = ctypes.c_void_p()
+        st = _lib.oid_init(ctypes.byref(params), ctypes.c_void_p(self.ws.data_ptr()), self.ws_bytes,
+                           self._st(), ctypes.byref(h))
+        if st != OID_OK:
+            raise OidError(st, "oid_init failed")
+        self.h = h
+        self.dtype = torch.float64 if params.dtype == OID_F64 else torch.float32
+
+    def _st(self):
+        return ctypes.c_void_p(self.stream.cuda_stream)
+
+    def _check(self, st, what):
+        if st != OID_OK:
+            raise OidError(st, f"{what}: {_lib.oid_last_error(self.h).decode()}")
+
+    def _block(self, X):
+        """X: device tensor (m_loc, ncols) with unit row stride (column-major) -> (ptr, ld, ncols)."""
+        if X.device != self.device or X.dtype != self.dtype:
+            raise ValueError(f"block must be a {self.dtype} tensor on {self.device}")
+        if X.dim() != 2 or X.shape[0] != self.m_loc:
+            raise ValueError(f"block must have shape (m_loc={self.m_loc}, ncols)")
+        ncols = X.shape[1]
+        if ncols > 1 and X.stride(0) != 1:
+            raise ValueError("block must be column-major (X.stride(0) == 1); pass Xt.T for a (ncols, m) tensor")
+        ld = X.stride(1) if ncols > 1 else self.m_loc
+        return ctypes.c_void_p(X.data_ptr()), ld, ncols
+
+    def ingest_block(self, X):
+        ptr, ld, nc = self._block(X)
+        self._check(_lib.oid_ingest_block(self.h, ptr, ld, nc, self._st()), "oid_ingest_block")
+
+    def ingest_sketch(self, X):
+        ptr, ld, nc = self._block(X)
+        self._check(_lib.oid_ingest_sketch(self.h, ptr, ld, nc, self._st()), "oid_ingest_sketch")
+
+    def ingest_commit(self, X):
+        ptr, ld, nc = self._block(X)
+        self._check(_lib.oid_ingest_commit(self.h, ptr, ld, nc, self._st()), "oid_ingest_commit")
+
+    def partials(self, which=0):
+        """fp64 torch view (aliasing the workspace) of the buffer to be summed over shards."""
+        p = _dp()
+        n = _i64()
+        self._check(_lib.oid_partials(self.h, which, ctypes.byref(p), ctypes.byref(n)), "oid_partials")
+        off = ctypes.cast(p, ctypes.c_void_p).value - self.ws.data_ptr()
+        return self.ws[off:off + 8 * n.value].view(self._torch.float64)
+
+    def estimate_begin(self):
+        self._check(_lib.oid_estimate_begin(self.h, self._st()), "oid_estimate_begin")
+
+    def estimate_end(self, out=None):
+        ptr = ctypes.c_void_p(out.data_ptr()) if out is not None else ctypes.c_void_p()
+        self._check(_lib.oid_estimate_end(self.h, ptr, self._st()), "oid_estimate_end")
+
+    def error_estimate(self):
+        out = (ctypes.c_double * 8)()
+        self._check(_lib.oid_error_estimate(self.h, out, self._st()), "oid_error_estimate")
+        v = list(out)
+        return dict(e2=v[0], T=v[1], gpp=v[2], frob2=v[3], est_abs=v[4], est_rel=v[5], flags=int(v[6]), kappa=v[7])
+
+    def finalize(self, basis=False):
+        torch = self._torch
+        t = self.p.k
+        J = np.empty(t, dtype=np.int64)
+        n_obs = self.stats()["n_obs"]
+        P = torch.empty((n_obs, t), dtype=torch.float64, device=self.device)   # column-major t x n_obs
+        B = torch.empty((t, self.m_loc), dtype=self.dtype, device=self.device) if basis else None
+        self._check(_lib.oid_finalize(self.h, ctypes.c_void_p(J.ctypes.data), ctypes.c_void_p(P.data_ptr()), 1,
+                                      ctypes.c_void_p(B.data_ptr()) if basis else ctypes.c_void_p(), self._st()),
+                    "oid_finalize")
+        out = dict(J=J, P=P.T)
+        if basis:
+            out["basis"] = B.T
+        return out
+
+    def get(self, field):
+        ell, t, bm = self.p.ell, self.p.k, self.p.b_max
+        n_obs = self.stats()["n_obs"] if field == 2 else 0
+        shapes = {0: ((t,), np.int64), 1: ((t,), np.float64), 2: ((n_obs, ell), np.float64),
+                  3: ((ell, ell), np.float64), 4: ((8,), np.float64), 5: ((t + bm,), np.float64),
+                  6: ((ell,), np.float64), 7: (((ell + 1) * bm,), np.float64), 8: ((ell, t), np.float64)}
+        shape, dt = shapes[field]
+        a = np.empty(shape, dtype=dt)
+        self._check(_lib.oid_get(self.h, field, ctypes.c_void_p(a.ctypes.data), a.nbytes, self._st()), "oid_get")
+        if field in (2, 3, 8):
+            a = a.T   # stored column-major
+        return a
+
+    def J(self):
+        return self.get(0)
+
+    def scalars(self):
+        v = self.get(4)
+        return dict(frob2=v[0], lam=v[1], Ek=v[2], shift=v[3], trace=v[4], dmax=v[5], min_margin=v[6], kappa=v[7])
+
+    def stats(self):
+        s = OidStats()
+        self._check(_lib.oid_stats(self.h, ctypes.byref(s)), "oid_stats")
+        return {f: getattr(s, f) for f, _ in OidStats._fields_}
+
+    def stats_reset(self):
+        self._check(_lib.oid_stats_reset(self.h), "oid_stats_reset")
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.oid_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

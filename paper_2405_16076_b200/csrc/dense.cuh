@@ -1,0 +1,204 @@
+// Small dense fp64 kernels of the post-pass (Gram, GEMM, one-sided Jacobi SVD / eigen,
+// traces).  All reductions run in a fixed order, so results are bitwise reproducible.
+#pragma once
+#include <cooperative_groups.h>
+#include "common.cuh"
+
+namespace oid {
+namespace cg = cooperative_groups;
+
+// C (M x N, ldc) = alpha * op(A) * op(B) + beta * C, column-major, op = transpose if T*.
+// 32x32 output tile per CTA, 256 threads x 4 outputs, K staged in 16-wide smem panels.
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(256) dgemm_kernel(int M, int N, int K, double alpha, const double* __restrict__ A,
+                                                    int64_t lda, const double* __restrict__ B, int64_t ldb, double beta,
+                                                    double* __restrict__ C, int64_t ldc) {
+  __shared__ double As[16][33];
+  __shared__ double Bs[16][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // ty: 0..7
+  const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    for (int e = threadIdx.x; e < 16 * 32; e += 256) {
+      const int kk = e >> 5, ii = e & 31;
+      const int i = i0 + ii, k = k0 + kk;
+      double a = 0.0;
+      if (i < M && k < K) a = TA ? A[k + static_cast<int64_t>(i) * lda] : A[i + static_cast<int64_t>(k) * lda];
+      As[kk][ii] = a;
+      const int j = j0 + ii;
+      double b = 0.0;
+      if (j < N && k < K) b = TB ? B[j + static_cast<int64_t>(k) * ldb] : B[k + static_cast<int64_t>(j) * ldb];
+      Bs[kk][ii] = b;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      const double a = As[kk][tx];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] = fma(a, Bs[kk][ty + 8 * q], acc[q]);
+    }
+    __syncthreads();
+  }
+  const int i = i0 + tx;
+  if (i < M) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = j0 + ty + 8 * q;
+      if (j < N) {
+        double* c = C + i + static_cast<int64_t>(j) * ldc;
+        *c = (beta == 0.0) ? alpha * acc[q] : fma(beta, *c, alpha * acc[q]);
+      }
+    }
+  }
+}
+
+// Gram += Y Y^T (ell x ell), S(:, n0:n0+nc) = Y, frob2 += sum n_j  (Alg 3 steps 10-13).
+__global__ void gram_update_kernel(const double* __restrict__ Yp, int ell, int nc, double* __restrict__ gram,
+                                   double* __restrict__ S, int64_t n0, double* __restrict__ scal) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nn = static_cast<int64_t>(ell) * ell;
+  if (idx < nn) {
+    const int r = static_cast<int>(idx % ell), c = static_cast<int>(idx / ell);
+    double s = gram[idx];
+    for (int j = 0; j < nc; ++j) s = fma(Yp[r + static_cast<int64_t>(j) * ell], Yp[c + static_cast<int64_t>(j) * ell], s);
+    gram[idx] = s;
+  }
+  const int64_t ny = static_cast<int64_t>(ell) * nc;
+  if (idx < ny) S[n0 * ell + idx] = Yp[idx];
+  if (idx == 0) {
+    double f = scal[0];
+    for (int j = 0; j < nc; ++j) f += Yp[ny + j];
+    scal[0] = f;
+  }
+}
+
+// One-sided (Hestenes) Jacobi: orthogonalise the n columns of B (L x n) by plane rotations
+// accumulated in V (n x n, initialised by the caller).  Round-robin pair ordering, one
+// pair per CTA per round, one grid-wide barrier per round.  Sweeps stop when a sweep
+// applies no rotation (|b_p.b_q| <= tol sqrt(|b_p|^2 |b_q|^2)).  Cooperative launch.
+__global__ void __launch_bounds__(256) jacobi_svd_kernel(double* __restrict__ B, int L, int n, double* __restrict__ V,
+                                                         int* __restrict__ counters, int max_sweeps, double tol) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[3][8];
+  const int nn = n + (n & 1);
+  const int npairs = nn / 2;
+  const int m1 = nn - 1;
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    for (int k = 0; k < m1; ++k) {
+      for (int pi = blockIdx.x; pi < npairs; pi += gridDim.x) {
+        int a, b;
+        if (pi == 0) { a = m1; b = k; } else { a = (k + pi) % m1; b = (k - pi + m1) % m1; }
+        const int p = min(a, b), q = max(a, b);
+        if (q >= n) continue;
+        double* bp = B + static_cast<int64_t>(p) * L;
+        double* bq = B + static_cast<int64_t>(q) * L;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int i = threadIdx.x; i < L; i += blockDim.x) {
+          const double x = bp[i], y = bq[i];
+          al = fma(x, x, al); be = fma(y, y, be); ga = fma(x, y, ga);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        const int w = threadIdx.x >> 5;
+        if ((threadIdx.x & 31) == 0) { red[0][w] = al; red[1][w] = be; red[2][w] = ga; }
+        __syncthreads();
+        al = 0.0; be = 0.0; ga = 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { al += red[0][i]; be += red[1][i]; ga += red[2][i]; }
+        __syncthreads();
+        if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
+          const double zeta = (be - al) / (2.0 * ga);
+          double t;
+          if (fabs(zeta) > 1e150) t = 0.5 / zeta;
+          else t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+          const double c = 1.0 / sqrt(fma(t, t, 1.0)), s = c * t;
+          for (int i = threadIdx.x; i < L; i += blockDim.x) {
+            const double x = bp[i], y = bq[i];
+            bp[i] = c * x - s * y;
+            bq[i] = s * x + c * y;
+          }
+          double* vp = V + static_cast<int64_t>(p) * n;
+          double* vq = V + static_cast<int64_t>(q) * n;
+          for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const double x = vp[i], y = vq[i];
+            vp[i] = c * x - s * y;
+            vq[i] = s * x + c * y;
+          }
+          if (threadIdx.x == 0) atomicAdd(&counters[sweep], 1);
+        }
+      }
+      grid.sync();
+    }
+    const int rotated = atomicAdd(&counters[sweep], 0);
+    if (rotated == 0) break;
+  }
+}
+
+// col_norm[i] = ||B(:, i)||_2 (fixed order), one CTA per column.
+__global__ void col_norms_kernel(const double* __restrict__ B, int L, int n, double* __restrict__ out) {
+  __shared__ double red[8];
+  const int i = blockIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int r = threadIdx.x; r < L; r += blockDim.x) { const double v = B[static_cast<int64_t>(i) * L + r]; s = fma(v, v, s); }
+  s = block_sum<256>(s, red);
+  if (threadIdx.x == 0) out[i] = sqrt(s);
+}
+
+__global__ void set_identity_kernel(double* __restrict__ V, int n) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx < static_cast<int64_t>(n) * n) V[idx] = (idx % n == idx / n) ? 1.0 : 0.0;
+}
+
+// Z(i, r) = w_i * B(r, i) with w_i = 1/sigma_i^2 if sigma_i > rcond * max sigma else 0
+// (pseudo-inverse assembly pinv = V Z, reading R9).  Z is n x L.  One CTA.
+__global__ void pinv_weights_kernel(const double* __restrict__ sig, int n, double rcond, double* __restrict__ w,
+                                    double* __restrict__ kappa_out, unsigned* __restrict__ flags, unsigned flagbit) {
+  __shared__ double red[8];
+  double mx = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) mx = fmax(mx, sig[i]);
+  mx = block_max<256>(mx, red);
+  double mn = INFINITY;
+  int cut = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double s = sig[i];
+    const bool keep = mx > 0.0 && s > rcond * mx;
+    w[i] = keep ? 1.0 / (s * s) : 0.0;
+    if (keep) mn = fmin(mn, s); else if (s > 0.0) cut = 1;
+  }
+  mn = -block_max<256>(-mn, red);
+  const double anycut = block_max<256>(static_cast<double>(cut), red);
+  if (threadIdx.x == 0) {
+    if (kappa_out) *kappa_out = (mx > 0.0) ? mx / mn : 1.0;
+    if (flags && anycut > 0.0) atomicOr(flags, flagbit);
+  }
+}
+
+__global__ void scale_transpose_kernel(const double* __restrict__ B, int L, int n, const double* __restrict__ w,
+                                       double* __restrict__ Z) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<int64_t>(L) * n) return;
+  const int i = static_cast<int>(idx % n), r = static_cast<int>(idx / n);   // Z(i, r), ld = n
+  Z[idx] = w[i] * B[static_cast<int64_t>(i) * L + r];
+}
+
+// sum_{i < rows, j < cols} A(i, j) * B(i, j)  (fixed order), written to *out (one CTA).
+__global__ void frob_dot_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ B, int64_t ldb,
+                                int rows, int64_t cols, double* __restrict__ out) {
+  __shared__ double red[8];
+  double s = 0.0;
+  const int64_t total = static_cast<int64_t>(rows) * cols;
+  for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
+    const int64_t j = e / rows;
+    const int i = static_cast<int>(e % rows);
+    s = fma(A[i + j * lda], B[i + j * ldb], s);
+  }
+  s = block_sum<256>(s, red);
+  if (threadIdx.x == 0) *out = s;
+}
+
+}  // namespace oid

@@ -1,0 +1,741 @@
+// liboid: host engine and C ABI (include/oid.h) of the B200 ingest hot path of the
+// single-pass randomized ID (arxiv 2405.16076, Alg 3 / Alg 4 / Alg 8).
+//
+// The caller owns all device memory (one workspace buffer, sized by oid_workspace_query);
+// every step runs in the kernels below on the caller's stream; the host never waits during
+// ingest.  See DESIGN.md sections 1 and 6 for the kernel list and the data layout.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/oid.h"
+#include "common.cuh"
+#include "dense.cuh"
+#include "k1_simt.cuh"
+#include "k1_tc.cuh"
+#include "path.cuh"
+
+using namespace oid;
+
+namespace {
+
+constexpr int kK1MaxCtas = 1024;
+constexpr int kGramChunks = 96;
+constexpr int kMaxSweeps = 48;
+constexpr int kNumJacobiUses = 3;
+
+// ------------------------------------------------------------------ Gauss-256 (reading R2)
+// Inverse normal CDF: Acklam's rational approximation refined by one Halley step on erfc.
+double inv_norm_cdf(double p) {
+  static const double a[] = {-3.969683028665376e+01, 2.209460984245205e+02, -2.759285104469687e+02,
+                             1.383577518672690e+02, -3.066479806614716e+01, 2.506628277459239e+00};
+  static const double b[] = {-5.447609879822406e+01, 1.615858368580409e+02, -1.556989798598866e+02,
+                             6.680131188771972e+01, -1.328068155288572e+01};
+  static const double c[] = {-7.784894002430293e-03, -3.223964580411365e-01, -2.400758277161838e+00,
+                             -2.549732539343734e+00, 4.374664141464968e+00, 2.938163982698783e+00};
+  static const double d[] = {7.784695709041462e-03, 3.224671290700398e-01, 2.445134137142996e+00,
+                             3.754408661907416e+00};
+  double x;
+  if (p < 0.02425) {
+    const double q = std::sqrt(-2.0 * std::log(p));
+    x = (((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) /
+        ((((d[0] * q + d[1]) * q + d[2]) * q + d[3]) * q + 1.0);
+  } else if (p <= 1.0 - 0.02425) {
+    const double q = p - 0.5, r = q * q;
+    x = (((((a[0] * r + a[1]) * r + a[2]) * r + a[3]) * r + a[4]) * r + a[5]) * q /
+        (((((b[0] * r + b[1]) * r + b[2]) * r + b[3]) * r + b[4]) * r + 1.0);
+  } else {
+    const double q = std::sqrt(-2.0 * std::log(1.0 - p));
+    x = -(((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) /
+        ((((d[0] * q + d[1]) * q + d[2]) * q + d[3]) * q + 1.0);
+  }
+  for (int it = 0; it < 2; ++it) {
+    const double e = 0.5 * std::erfc(-x / std::sqrt(2.0)) - p;
+    const double u = e * std::sqrt(2.0 * M_PI) * std::exp(0.5 * x * x);
+    x = x - u / (1.0 + 0.5 * x * u);
+  }
+  return x;
+}
+
+void gauss256(int32_t q[256], double* scale) {
+  long long sum2 = 0;
+  for (int u = 0; u < 256; ++u) {
+    q[u] = static_cast<int32_t>(std::lround(44.0 * inv_norm_cdf((u + 0.5) / 256.0)));
+    sum2 += static_cast<long long>(q[u]) * q[u];
+  }
+  *scale = 16.0 / std::sqrt(static_cast<double>(sum2));
+}
+
+// ------------------------------------------------------------------ workspace layout
+struct Bump {
+  size_t off = 0;
+  size_t take(size_t bytes) {
+    const size_t o = off;
+    off = (off + bytes + 255) & ~static_cast<size_t>(255);
+    return o;
+  }
+};
+
+struct Layout {
+  size_t S, gram, Ypart, k1part, k1npart, gB, gV, mu, mu_sorted, Yc, Tsc, tau, scal, J, tau_old, admit, counts,
+      flags, counters, C, SJ, sjB, sjV, sjsig, sjw, sjZ, Sjpinv, Pexp, AJP, G, Gsum, Gpart, cB, cV, csig, cw, cZ, M,
+      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, total;
+};
+
+int64_t m_local(const oid_params& p) { return p.row_end - p.row_begin; }
+size_t dsize(const oid_params& p) { return p.dtype == OID_F64 ? 8 : 4; }
+
+Layout make_layout(const oid_params& p) {
+  Layout L{};
+  Bump b;
+  const size_t d = sizeof(double);
+  const size_t ell = p.ell, t = p.k, bm = p.b_max, n = p.n_cap;
+  const size_t ncb = 64;
+  L.S = b.take(ell * n * d);
+  L.gram = b.take(ell * ell * d);
+  L.Ypart = b.take((ell + 1) * bm * d);
+  L.k1part = b.take(static_cast<size_t>(kK1MaxCtas) * ell * ncb * d);
+  L.k1npart = b.take(static_cast<size_t>(kK1MaxCtas) * ncb * d);
+  L.gB = b.take(ell * ell * d);
+  L.gV = b.take(ell * ell * d);
+  L.mu = b.take(ell * d);
+  L.mu_sorted = b.take(ell * d);
+  L.Yc = b.take(ell * (t + bm) * d);
+  L.Tsc = b.take(ell * (t + bm) * d);
+  L.tau = b.take((t + bm) * d);
+  L.scal = b.take(SC_COUNT * d);
+  L.J = b.take(t * sizeof(int64_t));
+  L.tau_old = b.take(t * d);
+  L.admit = b.take(2 * (t + bm) * sizeof(int));
+  L.counts = b.take(4 * sizeof(int));
+  L.flags = b.take(4 * sizeof(unsigned));
+  L.counters = b.take(kNumJacobiUses * kMaxSweeps * sizeof(int));
+  L.C = b.take(static_cast<size_t>(m_local(p)) * t * dsize(p));
+  L.SJ = b.take(ell * t * d);
+  L.sjB = b.take(ell * t * d);
+  L.sjV = b.take(t * t * d);
+  L.sjsig = b.take(t * d);
+  L.sjw = b.take(t * d);
+  L.sjZ = b.take(t * ell * d);
+  L.Sjpinv = b.take(t * ell * d);
+  L.Pexp = b.take(t * n * d);
+  L.AJP = b.take(ell * n * d);
+  L.G = b.take(t * t * d);
+  L.Gsum = b.take(t * t * d);
+  L.Gpart = b.take(static_cast<size_t>(kGramChunks) * t * t * d);
+  const size_t l1 = p.ell1, l2 = p.ell2, l3 = p.ell3;
+  L.cB = b.take(std::max<size_t>(1, l1 * l2) * d);
+  L.cV = b.take(std::max<size_t>(1, l2 * l2) * d);
+  L.csig = b.take(std::max<size_t>(1, l2) * d);
+  L.cw = b.take(std::max<size_t>(1, l2) * d);
+  L.cZ = b.take(std::max<size_t>(1, l2 * l1) * d);
+  L.M = b.take(std::max<size_t>(1, l2 * l1) * d);
+  L.X1 = b.take(std::max<size_t>(1, l1 * t) * d);
+  L.X2 = b.take(std::max<size_t>(1, l2 * t) * d);
+  L.Q1 = b.take(std::max<size_t>(1, l2 * t) * d);
+  L.Q2 = b.take(std::max<size_t>(1, l2 * t) * d);
+  L.R1 = b.take(std::max<size_t>(1, l3 * l2) * d);
+  L.R2t = b.take(std::max<size_t>(1, l3 * l1) * d);
+  L.R3 = b.take(std::max<size_t>(1, l3 * l1) * d);
+  L.PPt = b.take(t * t * d);
+  L.est = b.take(8 * d);
+  L.tc = b.take(k1tc_workspace_bytes(p.ell, p.b_max, m_local(p), p.dtype == OID_F64));
+  L.total = b.off;
+  return L;
+}
+
+const char* validate(const oid_params* p) {
+  if (!p) return "null params";
+  if (p->m <= 0) return "m must be > 0";
+  if (p->row_begin < 0 || p->row_end > p->m || p->row_begin >= p->row_end) return "need 0 <= row_begin < row_end <= m";
+  if (p->k < 1) return "k must be >= 1";
+  if (p->ell < 1 || p->ell > 1024) return "ell must be in [1, 1024]";
+  if (p->k > p->ell) return "k must be <= ell";
+  if (p->b_max < 1 || p->b_max > 64) return "b_max must be in [1, 64]";
+  if (p->n_cap < 1) return "n_cap must be >= 1";
+  if (p->ell1 < 0 || p->ell2 < 0 || p->ell3 < 0 || p->ell1 + p->ell2 + p->ell3 != p->ell)
+    return "ell1 + ell2 + ell3 must equal ell (all >= 0)";
+  if (!(p->lambda >= 0.0 || p->lambda == -1.0 || p->lambda == -2.0)) return "lambda must be >= 0, -1 or -2";
+  if (!(p->eps > 0.0) || !(p->delta > 0.0 && p->delta < 1.0) || !(p->c > 0.0)) return "need eps > 0, 0 < delta < 1, c > 0";
+  if (p->dtype != OID_F32 && p->dtype != OID_F64) return "dtype must be OID_F32 or OID_F64";
+  if (p->k1_mode < 0 || p->k1_mode > 2) return "bad k1_mode";
+  if (p->m / 16 >= (int64_t(1) << 32)) return "m too large for the 32-bit Philox row counter";
+  return nullptr;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ context
+struct oid_ctx_s {
+  oid_params p{};
+  Layout L{};
+  char* ws = nullptr;
+  int64_t m_loc = 0;
+  int t = 0;
+  int num_sms = 0;
+  int coop_max = 0;   // max co-resident CTAs of the Jacobi kernel
+  int k1_ctas_per_sm = 1;
+  double qscale = 0.0;
+  double factor = 0.0;
+  uint32_t key0 = 0, key1 = 0;
+  int64_t n_obs = 0, epoch = 0;
+  int pending_nc = -1;        // ncols of a sketch awaiting commit
+  bool estimate_ready = false;
+  int64_t launches = 0, k1_launches = 0;
+  int k1_mode_used = 0;
+  bool tc_ok = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_k1, ev_post, ev_est;
+  char err[512] = {0};
+
+  template <typename T> T* ptr(size_t off) const { return reinterpret_cast<T*>(ws + off); }
+  double* d(size_t off) const { return ptr<double>(off); }
+
+  oid_status fail(oid_status s, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(err, sizeof(err), fmt, ap);
+    va_end(ap);
+    return s;
+  }
+};
+
+#define CK(expr)                                                                                   \
+  do {                                                                                             \
+    cudaError_t e_ = (expr);                                                                       \
+    if (e_ != cudaSuccess) return ctx->fail(OID_ECUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+#define CKL()                                                                                      \
+  do {                                                                                             \
+    ++ctx->launches;                                                                               \
+    cudaError_t e_ = cudaGetLastError();                                                           \
+    if (e_ != cudaSuccess) return ctx->fail(OID_ECUDA, "launch: %s (%s:%d)", cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+namespace {
+
+unsigned blocks_for(int64_t n, int threads = 256) { return static_cast<unsigned>((n + threads - 1) / threads); }
+
+// C = alpha op(A) op(B) + beta C (column-major)
+oid_status gemm(oid_ctx ctx, cudaStream_t st, bool ta, bool tb, int M, int N, int K, double alpha, const double* A,
+                int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
+  if (M <= 0 || N <= 0) return OID_OK;
+  dim3 grid((M + 31) / 32, (N + 31) / 32);
+  if (!ta && !tb) dgemm_kernel<false, false><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else if (!ta && tb) dgemm_kernel<false, true><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else if (ta && !tb) dgemm_kernel<true, false><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else dgemm_kernel<true, true><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  CKL();
+  return OID_OK;
+}
+
+// One-sided Jacobi SVD of B (L x n) in place, V (n x n) set to I first; sig = column norms.
+oid_status jacobi(oid_ctx ctx, cudaStream_t st, double* B, int L, int n, double* V, double* sig, int use) {
+  if (n <= 0) return OID_OK;
+  set_identity_kernel<<<blocks_for(int64_t(n) * n), 256, 0, st>>>(V, n);
+  CKL();
+  int* counters = ctx->ptr<int>(ctx->L.counters) + use * kMaxSweeps;
+  CK(cudaMemsetAsync(counters, 0, kMaxSweeps * sizeof(int), st));
+  if (n > 1) {
+    const int npairs = (n + (n & 1)) / 2;
+    const int grid = std::max(1, std::min(npairs, ctx->coop_max));
+    int Li = L, ni = n, ms = kMaxSweeps;
+    double tol = 1e-15 * std::max(1.0, std::sqrt(static_cast<double>(L)));
+    void* args[] = {&B, &Li, &ni, &V, &counters, &ms, &tol};
+    CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(jacobi_svd_kernel), dim3(grid), dim3(256), args, 0, st));
+    CKL();
+  }
+  col_norms_kernel<<<n, 256, 0, st>>>(B, L, n, sig);
+  CKL();
+  return OID_OK;
+}
+
+// pinv(A) for A = B_orig (L x n) given the Jacobi result (B, V, sig): out (n x L) = V diag(w) B^T
+oid_status pinv_assemble(oid_ctx ctx, cudaStream_t st, const double* B, int L, int n, const double* V,
+                         const double* sig, double* w, double* Z, double* out, double* kappa, unsigned flagbit) {
+  if (n <= 0 || L <= 0) return OID_OK;
+  pinv_weights_kernel<<<1, 256, 0, st>>>(sig, n, 1e-12, w, kappa, flagbit ? ctx->ptr<unsigned>(ctx->L.flags) : nullptr,
+                                         flagbit);
+  CKL();
+  scale_transpose_kernel<<<blocks_for(int64_t(L) * n), 256, 0, st>>>(B, L, n, w, Z);
+  CKL();
+  return gemm(ctx, st, false, false, n, L, n, 1.0, V, n, Z, n, 0.0, out, n);
+}
+
+struct EvScope {
+  oid_ctx ctx;
+  cudaStream_t st;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* v;
+  cudaEvent_t b = nullptr, e = nullptr;
+  EvScope(oid_ctx c, cudaStream_t s, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* vec) : ctx(c), st(s), v(vec) {
+    if (!ctx->p.profile) return;
+    cudaEventCreate(&b);
+    cudaEventCreate(&e);
+    cudaEventRecord(b, st);
+  }
+  ~EvScope() {
+    if (!ctx->p.profile) return;
+    cudaEventRecord(e, st);
+    v->emplace_back(b, e);
+  }
+};
+
+template <typename T>
+oid_status launch_k1_simt(oid_ctx ctx, cudaStream_t st, const T* X, int64_t ld, int nc) {
+  const oid_params& p = ctx->p;
+  const int ncb = nc <= 16 ? 16 : (nc <= 32 ? 32 : 64);
+  const int rpt = ncb <= 32 ? 2 : 1;
+  const int ysplit = (p.ell + 256 * rpt - 1) / (256 * rpt);
+  const int64_t g_begin = p.row_begin / 16, g_end = (p.row_end + 15) / 16;
+  const int64_t ngroups = g_end - g_begin;
+  int64_t want = std::max<int64_t>(1, (int64_t(ctx->num_sms) * ctx->k1_ctas_per_sm) / ysplit);
+  want = std::min<int64_t>(want, std::min<int64_t>(ngroups, kK1MaxCtas));
+  const int64_t per = (ngroups + want - 1) / want;
+  const int gx = static_cast<int>((ngroups + per - 1) / per);
+  dim3 grid(gx, ysplit);
+  double* part = ctx->d(ctx->L.k1part);
+  double* npart = ctx->d(ctx->L.k1npart);
+  {
+    EvScope ev(ctx, st, &ctx->ev_k1);
+#define K1_LAUNCH(NCB, RPT)                                                                              \
+  k1_simt_kernel<T, NCB, RPT><<<grid, kThreads, 0, st>>>(X, ld, nc, p.row_begin, p.row_end, g_begin, g_end, per, \
+                                                         p.ell, ctx->key0, ctx->key1, part, npart)
+    if (ncb == 16) K1_LAUNCH(16, 2);
+    else if (ncb == 32) K1_LAUNCH(32, 2);
+    else K1_LAUNCH(64, 1);
+#undef K1_LAUNCH
+    CKL();
+    ++ctx->k1_launches;
+  }
+  const int64_t nout = int64_t(p.ell) * nc + nc;
+  k1_reduce_kernel<<<blocks_for(nout), 256, 0, st>>>(part, npart, gx, ncb, p.ell, nc, ctx->qscale, ctx->d(ctx->L.Ypart),
+                                                    ctx->ptr<unsigned>(ctx->L.flags));
+  CKL();
+  ctx->k1_mode_used = OID_K1_SIMT_F64;
+  return OID_OK;
+}
+
+oid_status do_sketch(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_t st) {
+  const oid_params& p = ctx->p;
+  const bool want_tc = (p.k1_mode == OID_K1_TC_INT8) || (p.k1_mode == OID_K1_AUTO && ctx->tc_ok);
+  if (want_tc) {
+    if (!ctx->tc_ok) return ctx->fail(OID_EINVAL, "tensor-core K1 unavailable for this device/shape");
+    K1TcArgs a{};
+    a.X = X; a.ld = ld; a.ncols = nc; a.row_begin = p.row_begin; a.row_end = p.row_end; a.ell = p.ell;
+    a.key0 = ctx->key0; a.key1 = ctx->key1; a.scale = ctx->qscale; a.f64 = p.dtype == OID_F64;
+    a.ws = ctx->ws + ctx->L.tc; a.out = ctx->d(ctx->L.Ypart); a.flags = ctx->ptr<unsigned>(ctx->L.flags);
+    a.num_sms = ctx->num_sms;
+    int nl = 0;
+    cudaError_t e;
+    {
+      EvScope ev(ctx, st, &ctx->ev_k1);
+      e = k1tc_launch(a, st, &nl);
+    }
+    ctx->launches += nl;
+    ctx->k1_launches += 1;
+    if (e != cudaSuccess) return ctx->fail(OID_ECUDA, "k1 tc: %s", cudaGetErrorString(e));
+    ctx->k1_mode_used = OID_K1_TC_INT8;
+    return OID_OK;
+  }
+  if (p.dtype == OID_F64) return launch_k1_simt<double>(ctx, st, static_cast<const double*>(X), ld, nc);
+  return launch_k1_simt<float>(ctx, st, static_cast<const float*>(X), ld, nc);
+}
+
+oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_t st) {
+  const oid_params& p = ctx->p;
+  const Layout& L = ctx->L;
+  const int ell = p.ell, t = ctx->t;
+  double* Yp = ctx->d(L.Ypart);
+  double* scal = ctx->d(L.scal);
+  EvScope ev(ctx, st, &ctx->ev_post);
+  // A3: S <- [S, Y], SS^T += YY^T, ||A_obs||^2 += sum n_j
+  gram_update_kernel<<<blocks_for(int64_t(ell) * ell), 256, 0, st>>>(Yp, ell, nc, ctx->d(L.gram), ctx->d(L.S), ctx->n_obs,
+                                                                    scal);
+  CKL();
+  // A4: eigen-decomposition of the Gram (one-sided Jacobi on a copy), lambda
+  CK(cudaMemcpyAsync(ctx->d(L.gB), ctx->d(L.gram), sizeof(double) * ell * ell, cudaMemcpyDeviceToDevice, st));
+  oid_status s = jacobi(ctx, st, ctx->d(L.gB), ell, ell, ctx->d(L.gV), ctx->d(L.mu), 0);
+  if (s != OID_OK) return s;
+  lambda_kernel<<<1, 256, 0, st>>>(ctx->d(L.mu), ell, p.k, ctx->d(L.gram), p.lambda, ell, scal, ctx->d(L.mu_sorted));
+  CKL();
+  // A5: ridge scores of the basis slots and the candidates
+  gather_scored_kernel<<<blocks_for(int64_t(ell) * (t + nc)), 256, 0, st>>>(ctx->d(L.S), ctx->ptr<int64_t>(L.J), t, Yp, nc,
+                                                                           ell, ctx->d(L.Yc));
+  CKL();
+  s = gemm(ctx, st, true, false, ell, t + nc, ell, 1.0, ctx->d(L.gV), ell, ctx->d(L.Yc), ell, 0.0, ctx->d(L.Tsc), ell);
+  if (s != OID_OK) return s;
+  scores_kernel<<<t + nc, 256, 0, st>>>(ctx->d(L.Tsc), ctx->d(L.mu), ell, t + nc, scal, ctx->d(L.tau));
+  CKL();
+  // A6: selection / replacement
+  select_kernel<<<1, 32, 0, st>>>(ctx->ptr<int64_t>(L.J), ctx->d(L.tau_old), ctx->d(L.tau), Yp + int64_t(ell) * nc, t, nc,
+                                  ctx->factor, static_cast<uint32_t>(ctx->epoch), ctx->n_obs, ctx->key0, ctx->key1,
+                                  ctx->ptr<int>(L.admit), ctx->ptr<int>(L.counts), scal);
+  CKL();
+  // A7: basis copy of this shard's rows
+  {
+    dim3 grid(std::max(1u, std::min(blocks_for(ctx->m_loc), 2048u)), nc + t);
+    if (p.dtype == OID_F64)
+      basis_copy_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(X), ld, ctx->ptr<double>(L.C), ctx->m_loc,
+                                                      ctx->ptr<int>(L.admit), ctx->ptr<int>(L.counts), nc, t);
+    else
+      basis_copy_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(X), ld, ctx->ptr<float>(L.C), ctx->m_loc,
+                                                     ctx->ptr<int>(L.admit), ctx->ptr<int>(L.counts), nc, t);
+    CKL();
+  }
+  ctx->n_obs += nc;
+  // A8: Alg 4 kept implicit: S_J^+ = V diag(1/sigma^2) B^T from the SVD of S_J
+  gather_sj_kernel<<<blocks_for(int64_t(ell) * t), 256, 0, st>>>(ctx->d(L.S), ctx->ptr<int64_t>(L.J), t, ell, ctx->d(L.SJ));
+  CKL();
+  CK(cudaMemcpyAsync(ctx->d(L.sjB), ctx->d(L.SJ), sizeof(double) * ell * t, cudaMemcpyDeviceToDevice, st));
+  s = jacobi(ctx, st, ctx->d(L.sjB), ell, t, ctx->d(L.sjV), ctx->d(L.sjsig), 1);
+  if (s != OID_OK) return s;
+  s = pinv_assemble(ctx, st, ctx->d(L.sjB), ell, t, ctx->d(L.sjV), ctx->d(L.sjsig), ctx->d(L.sjw), ctx->d(L.sjZ),
+                    ctx->d(L.Sjpinv), scal + SC_KAPPA, OID_FLAG_SJ_RANK_DEFICIENT);
+  if (s != OID_OK) return s;
+  ctx->epoch += 1;
+  ctx->estimate_ready = true;
+  return OID_OK;
+}
+
+oid_status check_block(oid_ctx ctx, const void* X, int64_t ld, int32_t nc) {
+  if (nc < 0 || nc > ctx->p.b_max) return ctx->fail(OID_ESHAPE, "ncols=%d outside [0, b_max=%d]", nc, ctx->p.b_max);
+  if (nc > 0 && X == nullptr) return ctx->fail(OID_EINVAL, "X is NULL");
+  if (nc > 0 && ld < ctx->m_loc) return ctx->fail(OID_ESHAPE, "ld=%lld < m_loc=%lld", (long long)ld, (long long)ctx->m_loc);
+  if (ctx->n_obs + nc > ctx->p.n_cap)
+    return ctx->fail(OID_ESHAPE, "n_obs + ncols = %lld exceeds n_cap = %lld", (long long)(ctx->n_obs + nc),
+                     (long long)ctx->p.n_cap);
+  if (ctx->n_obs + nc >= (int64_t(1) << 31)) return ctx->fail(OID_ESHAPE, "too many columns");
+  return OID_OK;
+}
+
+oid_status explicit_P(oid_ctx ctx, cudaStream_t st) {
+  const Layout& L = ctx->L;
+  return gemm(ctx, st, false, false, ctx->t, static_cast<int>(ctx->n_obs), ctx->p.ell, 1.0, ctx->d(L.Sjpinv), ctx->t,
+              ctx->d(L.S), ctx->p.ell, 0.0, ctx->d(L.Pexp), ctx->t);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ C ABI
+extern "C" {
+
+const char* oid_version(void) { return "liboid 0.1 (sm_100a)"; }
+
+const char* oid_last_error(oid_ctx ctx) { return ctx ? ctx->err : "null context"; }
+
+oid_status oid_workspace_query(const oid_params* p, size_t* bytes) {
+  if (!bytes || validate(p)) return OID_EINVAL;
+  *bytes = make_layout(*p).total;
+  return OID_OK;
+}
+
+oid_status oid_sketch_table(int32_t q[256], double* scale) {
+  if (!q || !scale) return OID_EINVAL;
+  gauss256(q, scale);
+  return OID_OK;
+}
+
+oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* stream, oid_ctx* out) {
+  if (!out) return OID_EINVAL;
+  *out = nullptr;
+  if (validate(p)) return OID_EINVAL;
+  oid_ctx ctx = new (std::nothrow) oid_ctx_s();
+  if (!ctx) return OID_ENOMEM;
+  ctx->p = *p;
+  ctx->L = make_layout(*p);
+  if (!workspace || bytes < ctx->L.total || (reinterpret_cast<uintptr_t>(workspace) & 255)) {
+    delete ctx;
+    return OID_ESHAPE;
+  }
+  ctx->ws = static_cast<char*>(workspace);
+  ctx->m_loc = m_local(*p);
+  ctx->t = p->k;
+  ctx->key0 = static_cast<uint32_t>(p->seed & 0xffffffffu);
+  ctx->key1 = static_cast<uint32_t>(p->seed >> 32);
+  const double k = p->k;
+  ctx->factor = p->c * (k * std::log(k) + k * std::log(1.0 / p->delta) / p->eps) / ctx->t;
+  int32_t q[256];
+  gauss256(q, &ctx->qscale);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  auto bad = [&](cudaError_t e) {
+    snprintf(ctx->err, sizeof(ctx->err), "init: %s", cudaGetErrorString(e));
+    delete ctx;
+    return OID_ECUDA;
+  };
+  cudaError_t e = cudaSetDevice(p->device);
+  if (e != cudaSuccess) return bad(e);
+  cudaDeviceProp prop;
+  if ((e = cudaGetDeviceProperties(&prop, p->device)) != cudaSuccess) return bad(e);
+  ctx->num_sms = prop.multiProcessorCount;
+  int per_sm = 0;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_svd_kernel, 256, 0)) != cudaSuccess) return bad(e);
+  ctx->coop_max = std::max(1, per_sm * ctx->num_sms);
+  ctx->k1_ctas_per_sm = 1;
+  ctx->tc_ok = (prop.major == 10 && prop.minor == 0) && k1tc_supported(p->ell, p->b_max, p->dtype == OID_F64);
+  double qd[256];
+  for (int i = 0; i < 256; ++i) qd[i] = q[i];
+  if ((e = cudaMemcpyToSymbolAsync(c_qtab_f64, qd, sizeof(qd), 0, cudaMemcpyHostToDevice, st)) != cudaSuccess) return bad(e);
+  if ((e = k1tc_init_tables(q, st)) != cudaSuccess) return bad(e);
+  // state: J = -1, tau_old = 1, Gram = 0, S = 0, scalars, flags
+  const Layout& L = ctx->L;
+  if ((e = cudaMemsetAsync(ctx->ws + L.J, 0xff, sizeof(int64_t) * ctx->t, st)) != cudaSuccess) return bad(e);
+  std::vector<double> ones(ctx->t, 1.0);
+  if ((e = cudaMemcpyAsync(ctx->ws + L.tau_old, ones.data(), sizeof(double) * ctx->t, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    return bad(e);
+  if ((e = cudaMemsetAsync(ctx->ws + L.gram, 0, sizeof(double) * p->ell * p->ell, st)) != cudaSuccess) return bad(e);
+  double sc[SC_COUNT] = {0};
+  sc[SC_MINMARGIN] = INFINITY;
+  sc[SC_KAPPA] = 1.0;
+  if ((e = cudaMemcpyAsync(ctx->ws + L.scal, sc, sizeof(sc), cudaMemcpyHostToDevice, st)) != cudaSuccess) return bad(e);
+  if ((e = cudaMemsetAsync(ctx->ws + L.flags, 0, 4 * sizeof(unsigned), st)) != cudaSuccess) return bad(e);
+  if ((e = cudaMemsetAsync(ctx->ws + L.C, 0, static_cast<size_t>(ctx->m_loc) * ctx->t * dsize(*p), st)) != cudaSuccess) return bad(e);
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return bad(e);   // host arrays above go out of scope
+  *out = ctx;
+  return OID_OK;
+}
+
+oid_status oid_ingest_sketch(oid_ctx ctx, const void* X, int64_t ld, int32_t ncols, void* stream) {
+  if (!ctx) return OID_EINVAL;
+  oid_status s = check_block(ctx, X, ld, ncols);
+  if (s != OID_OK) return s;
+  ctx->pending_nc = ncols;
+  if (ncols == 0) return OID_OK;
+  return do_sketch(ctx, X, ld, ncols, static_cast<cudaStream_t>(stream));
+}
+
+oid_status oid_ingest_commit(oid_ctx ctx, const void* X, int64_t ld, int32_t ncols, void* stream) {
+  if (!ctx) return OID_EINVAL;
+  if (ctx->pending_nc < 0 || ctx->pending_nc != ncols)
+    return ctx->fail(OID_ESTATE, "commit without a matching sketch (pending ncols %d, got %d)", ctx->pending_nc, ncols);
+  oid_status s = check_block(ctx, X, ld, ncols);
+  if (s != OID_OK) return s;
+  ctx->pending_nc = -1;
+  if (ncols == 0) return OID_OK;
+  return do_commit(ctx, X, ld, ncols, static_cast<cudaStream_t>(stream));
+}
+
+oid_status oid_ingest_block(oid_ctx ctx, const void* X, int64_t ld, int32_t ncols, void* stream) {
+  if (!ctx) return OID_EINVAL;
+  if (ctx->p.row_begin != 0 || ctx->p.row_end != ctx->p.m)
+    return ctx->fail(OID_ESTATE, "sharded context: use oid_ingest_sketch / reduce / oid_ingest_commit");
+  oid_status s = oid_ingest_sketch(ctx, X, ld, ncols, stream);
+  if (s != OID_OK) return s;
+  return oid_ingest_commit(ctx, X, ld, ncols, stream);
+}
+
+oid_status oid_partials(oid_ctx ctx, int32_t which, double** dev_ptr, int64_t* count) {
+  if (!ctx || !dev_ptr || !count) return OID_EINVAL;
+  if (which == 0) {
+    *dev_ptr = ctx->d(ctx->L.Ypart);
+    *count = int64_t(ctx->p.ell + 1) * std::max(0, ctx->pending_nc);
+  } else if (which == 1) {
+    *dev_ptr = ctx->d(ctx->L.Gsum);
+    *count = int64_t(ctx->t) * ctx->t;
+  } else {
+    return OID_EINVAL;
+  }
+  return OID_OK;
+}
+
+oid_status oid_estimate_begin(oid_ctx ctx, void* stream) {
+  if (!ctx) return OID_EINVAL;
+  if (!ctx->estimate_ready) return ctx->fail(OID_ESTATE, "no block ingested yet");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const Layout& L = ctx->L;
+  const int t = ctx->t;
+  EvScope ev(ctx, st, &ctx->ev_est);
+  // A9: exact basis Gram G = A_J^T A_J over this shard's rows
+  const int ntile = (t + 31) / 32;
+  const int npair = ntile * (ntile + 1) / 2;
+  int chunks = static_cast<int>(std::min<int64_t>(kGramChunks, (ctx->m_loc + 4095) / 4096));
+  chunks = std::max(1, chunks);
+  int64_t per = (ctx->m_loc + chunks - 1) / chunks;
+  per = (per + 31) / 32 * 32;
+  chunks = static_cast<int>((ctx->m_loc + per - 1) / per);
+  dim3 grid(chunks, npair);
+  if (ctx->p.dtype == OID_F64)
+    basis_gram_kernel<double><<<grid, 256, 0, st>>>(ctx->ptr<double>(L.C), ctx->m_loc, t, per, ctx->d(L.Gpart));
+  else
+    basis_gram_kernel<float><<<grid, 256, 0, st>>>(ctx->ptr<float>(L.C), ctx->m_loc, t, per, ctx->d(L.Gpart));
+  CKL();
+  sum_chunks_kernel<<<blocks_for(int64_t(t) * t), 256, 0, st>>>(ctx->d(L.Gpart), chunks, int64_t(t) * t, ctx->d(L.Gsum));
+  CKL();
+  return OID_OK;
+}
+
+oid_status oid_estimate_end(oid_ctx ctx, double* out_dev, void* stream) {
+  if (!ctx) return OID_EINVAL;
+  if (!ctx->estimate_ready) return ctx->fail(OID_ESTATE, "no block ingested yet");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const Layout& L = ctx->L;
+  const oid_params& p = ctx->p;
+  const int t = ctx->t, ell = p.ell, l1 = p.ell1, l2 = p.ell2, l3 = p.ell3;
+  const int n = static_cast<int>(ctx->n_obs);
+  double* S = ctx->d(L.S);
+  double* scal = ctx->d(L.scal);
+  EvScope ev(ctx, st, &ctx->ev_est);
+  CK(cudaMemcpyAsync(ctx->d(L.G), ctx->d(L.Gsum), sizeof(double) * t * t, cudaMemcpyDeviceToDevice, st));
+  mask_gram_kernel<<<blocks_for(int64_t(t) * t), 256, 0, st>>>(ctx->d(L.G), ctx->ptr<int64_t>(L.J), t);
+  CKL();
+  oid_status s = explicit_P(ctx, st);                                                 // P = S_J^+ S
+  if (s != OID_OK) return s;
+  double* P = ctx->d(L.Pexp);
+  double* AJP = ctx->d(L.AJP);
+  s = gemm(ctx, st, false, false, ell, n, t, 1.0, ctx->d(L.SJ), ell, P, t, 0.0, AJP, ell);   // Omega A_J P
+  if (s != OID_OK) return s;
+  CK(cudaMemsetAsync(scal + SC_T1, 0, 4 * sizeof(double), st));
+  if (l1 > 0 && l2 > 0) {
+    // M = (Omega1 A (Omega2 A_J P)^T)^+   
+    s = gemm(ctx, st, false, true, l1, l2, n, 1.0, S, ell, AJP + l1, ell, 0.0, ctx->d(L.cB), l1);
+    if (s != OID_OK) return s;
+    s = jacobi(ctx, st, ctx->d(L.cB), l1, l2, ctx->d(L.cV), ctx->d(L.csig), 2);
+    if (s != OID_OK) return s;
+    s = pinv_assemble(ctx, st, ctx->d(L.cB), l1, l2, ctx->d(L.cV), ctx->d(L.csig), ctx->d(L.cw), ctx->d(L.cZ), ctx->d(L.M),
+                      nullptr, 0);
+    if (s != OID_OK) return s;
+    // term1 = tr(M (Omega1 A P^T) G (Omega2 A P^T)^T)
+    s = gemm(ctx, st, false, true, l1, t, n, 1.0, S, ell, P, t, 0.0, ctx->d(L.X1), l1);
+    if (s != OID_OK) return s;
+    s = gemm(ctx, st, false, true, l2, t, n, 1.0, S + l1, ell, P, t, 0.0, ctx->d(L.X2), l2);
+    if (s != OID_OK) return s;
+    s = gemm(ctx, st, false, false, l2, t, l1, 1.0, ctx->d(L.M), l2, ctx->d(L.X1), l1, 0.0, ctx->d(L.Q1), l2);
+    if (s != OID_OK) return s;
+    s = gemm(ctx, st, false, false, l2, t, t, 1.0, ctx->d(L.Q1), l2, ctx->d(L.G), t, 0.0, ctx->d(L.Q2), l2);
+    if (s != OID_OK) return s;
+    frob_dot_kernel<<<1, 256, 0, st>>>(ctx->d(L.Q2), l2, ctx->d(L.X2), l2, l2, t, scal + SC_T1);
+    CKL();
+  }
+  if (l3 > 0) {
+    // t3a = tr((Omega3 A)(Omega3 A_J P)^T)
+    frob_dot_kernel<<<1, 256, 0, st>>>(S + l1 + l2, ell, AJP + l1 + l2, ell, l3, n, scal + SC_T3A);
+    CKL();
+    if (l1 > 0 && l2 > 0) {
+      // t3b = tr((Omega3 A_J P)(Omega2 A)^T M (Omega1 A)(Omega3 A_J P)^T)
+      s = gemm(ctx, st, false, true, l3, l2, n, 1.0, AJP + l1 + l2, ell, S + l1, ell, 0.0, ctx->d(L.R1), l3);
+      if (s != OID_OK) return s;
+      s = gemm(ctx, st, false, true, l3, l1, n, 1.0, AJP + l1 + l2, ell, S, ell, 0.0, ctx->d(L.R2t), l3);
+      if (s != OID_OK) return s;
+      s = gemm(ctx, st, false, false, l3, l1, l2, 1.0, ctx->d(L.R1), l3, ctx->d(L.M), l2, 0.0, ctx->d(L.R3), l3);
+      if (s != OID_OK) return s;
+      frob_dot_kernel<<<1, 256, 0, st>>>(ctx->d(L.R3), l3, ctx->d(L.R2t), l3, l3, l1, scal + SC_T3B);
+      CKL();
+    }
+  }
+  // tr(G P P^T) = ||A_J P||_F^2
+  s = gemm(ctx, st, false, true, t, t, n, 1.0, P, t, P, t, 0.0, ctx->d(L.PPt), t);
+  if (s != OID_OK) return s;
+  frob_dot_kernel<<<1, 256, 0, st>>>(ctx->d(L.G), t, ctx->d(L.PPt), t, t, t, scal + SC_GPP);
+  CKL();
+  hutch_final_kernel<<<1, 32, 0, st>>>(scal, l3, ctx->ptr<unsigned>(L.flags), ctx->d(L.est));
+  CKL();
+  if (out_dev) CK(cudaMemcpyAsync(out_dev, ctx->d(L.est), 8 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  return OID_OK;
+}
+
+oid_status oid_error_estimate(oid_ctx ctx, double* out_host, void* stream) {
+  if (!ctx || !out_host) return OID_EINVAL;
+  oid_status s = oid_estimate_begin(ctx, stream);
+  if (s != OID_OK) return s;
+  s = oid_estimate_end(ctx, nullptr, stream);
+  if (s != OID_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CK(cudaMemcpyAsync(out_host, ctx->d(ctx->L.est), 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return OID_OK;
+}
+
+oid_status oid_finalize(oid_ctx ctx, int64_t* J_host, double* P, int32_t P_on_device, void* basis_dev, void* stream) {
+  if (!ctx) return OID_EINVAL;
+  if (ctx->pending_nc >= 0) return ctx->fail(OID_ESTATE, "a sketch is pending commit");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const Layout& L = ctx->L;
+  const int t = ctx->t;
+  if (ctx->n_obs > 0 && P) {
+    oid_status s = explicit_P(ctx, st);
+    if (s != OID_OK) return s;
+    CK(cudaMemcpyAsync(P, ctx->d(L.Pexp), sizeof(double) * t * ctx->n_obs,
+                       P_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+  }
+  if (J_host) CK(cudaMemcpyAsync(J_host, ctx->ws + L.J, sizeof(int64_t) * t, cudaMemcpyDeviceToHost, st));
+  if (basis_dev)
+    CK(cudaMemcpyAsync(basis_dev, ctx->ws + L.C, static_cast<size_t>(ctx->m_loc) * t * dsize(ctx->p), cudaMemcpyDeviceToDevice, st));
+  CK(cudaStreamSynchronize(st));
+  return OID_OK;
+}
+
+oid_status oid_get(oid_ctx ctx, int32_t field, void* host_dst, size_t bytes, void* stream) {
+  if (!ctx || !host_dst) return OID_EINVAL;
+  const Layout& L = ctx->L;
+  const oid_params& p = ctx->p;
+  size_t off = 0, need = 0;
+  switch (field) {
+    case 0: off = L.J; need = sizeof(int64_t) * ctx->t; break;
+    case 1: off = L.tau_old; need = sizeof(double) * ctx->t; break;
+    case 2: off = L.S; need = sizeof(double) * p.ell * ctx->n_obs; break;
+    case 3: off = L.gram; need = sizeof(double) * p.ell * p.ell; break;
+    case 4: off = L.scal; need = sizeof(double) * 8; break;
+    case 5: off = L.tau; need = sizeof(double) * (ctx->t + p.b_max); break;
+    case 6: off = L.mu; need = sizeof(double) * p.ell; break;
+    case 7: off = L.Ypart; need = sizeof(double) * (p.ell + 1) * p.b_max; break;
+    case 8: off = L.Sjpinv; need = sizeof(double) * ctx->t * p.ell; break;
+    default: return ctx->fail(OID_EINVAL, "unknown field %d", field);
+  }
+  if (bytes < need) return ctx->fail(OID_ESHAPE, "field %d needs %zu bytes", field, need);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (need) CK(cudaMemcpyAsync(host_dst, ctx->ws + off, need, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return OID_OK;
+}
+
+oid_status oid_stats(oid_ctx ctx, oid_stats_t* out) {
+  if (!ctx || !out) return OID_EINVAL;
+  std::memset(out, 0, sizeof(*out));
+  out->n_obs = ctx->n_obs;
+  out->epochs = ctx->epoch;
+  out->launches = ctx->launches;
+  out->k1_launches = ctx->k1_launches;
+  out->k1_mode_used = ctx->k1_mode_used;
+  auto sum = [&](std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v, double* dst) -> cudaError_t {
+    double s = 0.0;
+    for (auto& pr : v) {
+      cudaError_t e = cudaEventSynchronize(pr.second);
+      if (e != cudaSuccess) return e;
+      float ms = 0.f;
+      e = cudaEventElapsedTime(&ms, pr.first, pr.second);
+      if (e != cudaSuccess) return e;
+      s += ms;
+    }
+    *dst = s;
+    return cudaSuccess;
+  };
+  CK(sum(ctx->ev_k1, &out->k1_ms));
+  CK(sum(ctx->ev_post, &out->post_ms));
+  CK(sum(ctx->ev_est, &out->est_ms));
+  unsigned f = 0;
+  CK(cudaMemcpy(&f, ctx->ws + ctx->L.flags, sizeof(unsigned), cudaMemcpyDeviceToHost));
+  out->flags = f;
+  return OID_OK;
+}
+
+oid_status oid_stats_reset(oid_ctx ctx) {
+  if (!ctx) return OID_EINVAL;
+  for (auto* v : {&ctx->ev_k1, &ctx->ev_post, &ctx->ev_est}) {
+    for (auto& pr : *v) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+    v->clear();
+  }
+  ctx->launches = 0;
+  ctx->k1_launches = 0;
+  return OID_OK;
+}
+
+void oid_destroy(oid_ctx ctx) {
+  if (!ctx) return;
+  oid_stats_reset(ctx);
+  delete ctx;
+}
+
+}  // extern "C"

@@ -1,0 +1,247 @@
+// Post-pass kernels specific to Algorithm 3: ridge regulariser, ridge scores, selection,
+// basis copy, S_J gather, NA-Hutch++ final combination.
+#pragma once
+#include "common.cuh"
+
+namespace oid {
+
+// scalars layout (device double array)
+enum Scal : int {
+  SC_FROB2 = 0, SC_LAM = 1, SC_EK = 2, SC_SHIFT = 3, SC_TRACE = 4, SC_DMAX = 5, SC_MINMARGIN = 6, SC_KAPPA = 7,
+  SC_T1 = 8, SC_T3A = 9, SC_T3B = 10, SC_GPP = 11, SC_COUNT = 16
+};
+
+// Ridge regulariser (reading R8): eigenvalues mu of the unscaled Gram, E_k = sum of the k
+// largest (descending order), lambda per mode, shift = ell * lambda (reading R3),
+// dmax = max(mu) + shift.  One CTA (n <= 1024): rank sort, then sequential sums.
+__global__ void lambda_kernel(const double* __restrict__ mu, int n, int k, const double* __restrict__ gram,
+                              double lam_param, int ell, double* __restrict__ scal, double* __restrict__ sorted) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double v = mu[i];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) {
+      const double u = mu[j];
+      rank += (u > v) || (u == v && j < i);
+    }
+    sorted[rank] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double Ek = 0.0;
+    for (int i = 0; i < k && i < n; ++i) Ek += sorted[i];
+    double tr = 0.0;
+    for (int i = 0; i < ell; ++i) tr += gram[static_cast<int64_t>(i) * ell + i];
+    const double frob2 = scal[SC_FROB2];
+    double lam;
+    if (lam_param >= 0.0) lam = lam_param;
+    else if (lam_param == -1.0) lam = fmax(0.0, (frob2 - Ek / ell) / k);
+    else lam = fmax(0.0, (tr - Ek) / (static_cast<double>(ell) * k));
+    const double shift = ell * lam;
+    scal[SC_LAM] = lam;
+    scal[SC_EK] = Ek;
+    scal[SC_SHIFT] = shift;
+    scal[SC_TRACE] = tr;
+    scal[SC_DMAX] = (n > 0 ? sorted[0] : 0.0) + shift;
+  }
+}
+
+// Yc = [S(:, J_i) for slots (zero if vacant) | Y_block]  (ell x (t + nc))
+__global__ void gather_scored_kernel(const double* __restrict__ S, const int64_t* __restrict__ J, int t,
+                                     const double* __restrict__ Yp, int nc, int ell, double* __restrict__ Yc) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t total = static_cast<int64_t>(ell) * (t + nc);
+  if (idx >= total) return;
+  const int col = static_cast<int>(idx / ell), r = static_cast<int>(idx % ell);
+  double v = 0.0;
+  if (col < t) {
+    const int64_t j = J[col];
+    if (j >= 0) v = S[j * ell + r];
+  } else {
+    v = Yp[static_cast<int64_t>(col - t) * ell + r];
+  }
+  Yc[idx] = v;
+}
+
+// tau_j = sum_{i: mu_i + shift > 1e-12 dmax} T(i, j)^2 / (mu_i + shift), T = W^T Yc
+// (eq:sketch_ridge_leverage_score; readings R3, R9).  One CTA per column.
+__global__ void scores_kernel(const double* __restrict__ T, const double* __restrict__ mu, int ell, int ncol,
+                              const double* __restrict__ scal, double* __restrict__ tau) {
+  __shared__ double red[8];
+  const int j = blockIdx.x;
+  if (j >= ncol) return;
+  const double shift = scal[SC_SHIFT], dmax = scal[SC_DMAX];
+  double s = 0.0;
+  if (dmax > 0.0) {
+    for (int i = threadIdx.x; i < ell; i += blockDim.x) {
+      const double d = mu[i] + shift;
+      if (d > 1e-12 * dmax) { const double x = T[static_cast<int64_t>(j) * ell + i]; s += x * x / d; }
+    }
+  }
+  s = block_sum<256>(s, red);
+  if (threadIdx.x == 0) tau[j] = s;
+}
+
+// Alg 3 steps 15-27, readings R4-R7, R14.  Single thread (sequential by nature:
+// slot i+1 sees the candidates consumed by slot i).
+// tau: [t slot scores | nc candidate scores]; nrm: candidate norms (zero columns skipped).
+// Outputs: admit list (slot, r) pairs, count; zero list (slots vacated, not refilled).
+__global__ void select_kernel(int64_t* __restrict__ J, double* __restrict__ tau_old, const double* __restrict__ tau,
+                              const double* __restrict__ nrm, int t, int nc, double factor, uint32_t epoch,
+                              int64_t base, uint32_t key0, uint32_t key1, int* __restrict__ admit,
+                              int* __restrict__ counts, double* __restrict__ scal) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  unsigned consumed[2] = {0u, 0u};   // nc <= 64
+  int na = 0, nz = 0;
+  double minm = scal[SC_MINMARGIN];
+  for (int i = 0; i < t; ++i) {
+    bool occupied = J[i] >= 0;
+    bool evicted = false;
+    if (occupied) {
+      const double told = tau_old[i];
+      const double ti = fmin(told, tau[i]);
+      const double rho = told > 0.0 ? ti / told : 1.0;
+      const double pev = 1.0 - rho;
+      const double u = select_uniform(epoch, static_cast<uint32_t>(i), 0xFFFFFFFFu, key0, key1);
+      minm = fmin(minm, fabs(u - pev) / fmax(rho, 0x1p-24));
+      if (u < pev) { J[i] = -1; tau_old[i] = 1.0; occupied = false; evicted = true; }
+      else tau_old[i] = ti;
+    }
+    if (!occupied) {
+      bool filled = false;
+      for (int r = 0; r < nc; ++r) {
+        if ((consumed[r >> 5] >> (r & 31)) & 1u) continue;
+        if (nrm[r] == 0.0) continue;
+        const double praw = tau[t + r] * factor;
+        const double p = fmin(1.0, praw);
+        const double u = select_uniform(epoch, static_cast<uint32_t>(i), static_cast<uint32_t>(r), key0, key1);
+        minm = fmin(minm, fabs(u - praw) / fmax(praw, 0x1p-24));
+        if (u < p) {
+          J[i] = base + r;
+          tau_old[i] = tau[t + r];
+          consumed[r >> 5] |= 1u << (r & 31);
+          admit[2 * na] = i;
+          admit[2 * na + 1] = r;
+          ++na;
+          filled = true;
+          break;
+        }
+      }
+      if (evicted && !filled) { admit[2 * (nc + t) - 2 - 2 * nz] = i; ++nz; }
+    }
+  }
+  counts[0] = na;
+  counts[1] = nz;
+  scal[SC_MINMARGIN] = minm;
+}
+
+// C(:, slot) <- X(:, r) for admissions, C(:, slot) <- 0 for vacated slots.
+template <typename T>
+__global__ void basis_copy_kernel(const T* __restrict__ X, int64_t ld, T* __restrict__ C, int64_t m_loc,
+                                  const int* __restrict__ admit, const int* __restrict__ counts, int nc, int t) {
+  const int a = blockIdx.y;
+  const int na = counts[0], nz = counts[1];
+  int slot, r = -1;
+  if (a < na) { slot = admit[2 * a]; r = admit[2 * a + 1]; }
+  else if (a - na < nz) { slot = admit[2 * (nc + t) - 2 - 2 * (a - na)]; }
+  else return;
+  T* dst = C + static_cast<int64_t>(slot) * m_loc;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  if (r >= 0) {
+    const T* src = X + static_cast<int64_t>(r) * ld;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < m_loc; i += stride) dst[i] = src[i];
+  } else {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < m_loc; i += stride) dst[i] = T(0);
+  }
+}
+
+// S_J = S(:, J) with zero columns for vacant slots (ell x t)
+__global__ void gather_sj_kernel(const double* __restrict__ S, const int64_t* __restrict__ J, int t, int ell,
+                                 double* __restrict__ SJ) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<int64_t>(ell) * t) return;
+  const int col = static_cast<int>(idx / ell), r = static_cast<int>(idx % ell);
+  const int64_t j = J[col];
+  SJ[idx] = j >= 0 ? S[j * ell + r] : 0.0;
+}
+
+// G(i, j) masked to occupied slots: G <- G .* [J_i >= 0][J_j >= 0]
+__global__ void mask_gram_kernel(double* __restrict__ G, const int64_t* __restrict__ J, int t) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= t * t) return;
+  const int i = idx % t, j = idx / t;
+  if (J[i] < 0 || J[j] < 0) G[idx] = 0.0;
+}
+
+// Final combination of Alg 8: T = term1 + (t3a - t3b)/ell3;
+// e2 = frob2 - 2T + tr(G P P^T).  out[8] as documented in oid.h.
+__global__ void hutch_final_kernel(const double* __restrict__ scal, int ell3, const unsigned* __restrict__ flags,
+                                   double* __restrict__ out) {
+  if (threadIdx.x != 0) return;
+  const double term1 = scal[SC_T1];
+  const double T = ell3 > 0 ? term1 + (scal[SC_T3A] - scal[SC_T3B]) / ell3 : term1;
+  const double gpp = scal[SC_GPP];
+  const double frob2 = scal[SC_FROB2];
+  const double e2 = frob2 - 2.0 * T + gpp;
+  unsigned f = *flags;
+  if (e2 < 0.0) f |= 4u;
+  const double est = sqrt(fmax(e2, 0.0));
+  out[0] = e2; out[1] = T; out[2] = gpp; out[3] = frob2; out[4] = est;
+  out[5] = frob2 > 0.0 ? est / sqrt(frob2) : 0.0;
+  out[6] = static_cast<double>(f);
+  out[7] = scal[SC_KAPPA];
+}
+
+// Partial basis Gram over this shard's rows: Gp(i, j) = sum_rows C(r, i) C(r, j) (upper tiles
+// mirrored).  grid: (row chunks, tile pairs); tile 32 x 32; fp64 accumulation.
+template <typename T>
+__global__ void __launch_bounds__(256) basis_gram_kernel(const T* __restrict__ C, int64_t m_loc, int t,
+                                                         int64_t rows_per_chunk, double* __restrict__ part) {
+  __shared__ double Ai[32][33];
+  __shared__ double Aj[32][33];
+  const int ntile = (t + 31) / 32;
+  // decode upper-triangular tile pair (ti <= tj) from blockIdx.y
+  int p = blockIdx.y, ti = 0;
+  while (p >= ntile - ti) { p -= ntile - ti; ++ti; }
+  const int tj = ti + p;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * rows_per_chunk;
+  const int64_t r1 = min(m_loc, r0 + rows_per_chunk);
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t rb = r0; rb < r1; rb += 32) {
+    for (int e = threadIdx.x; e < 32 * 32; e += 256) {
+      const int rr = e & 31, cc = e >> 5;
+      const int64_t r = rb + rr;
+      const int ci = ti * 32 + cc, cj = tj * 32 + cc;
+      Ai[rr][cc] = (r < r1 && ci < t) ? static_cast<double>(C[static_cast<int64_t>(ci) * m_loc + r]) : 0.0;
+      Aj[rr][cc] = (r < r1 && cj < t) ? static_cast<double>(C[static_cast<int64_t>(cj) * m_loc + r]) : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int rr = 0; rr < 32; ++rr) {
+      const double a = Ai[rr][tx];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] = fma(a, Aj[rr][ty + 8 * q], acc[q]);
+    }
+    __syncthreads();
+  }
+  double* out = part + static_cast<int64_t>(blockIdx.x) * t * t;
+  const int i = ti * 32 + tx;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int j = tj * 32 + ty + 8 * q;
+    if (i < t && j < t) {
+      out[i + static_cast<int64_t>(j) * t] = acc[q];
+      out[j + static_cast<int64_t>(i) * t] = acc[q];
+    }
+  }
+}
+
+__global__ void sum_chunks_kernel(const double* __restrict__ part, int nchunks, int64_t n, double* __restrict__ out) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= n) return;
+  double s = 0.0;
+  for (int c = 0; c < nchunks; ++c) s += part[static_cast<int64_t>(c) * n + idx];
+  out[idx] = s;
+}
+
+}  // namespace oid

@@ -1,0 +1,67 @@
+"""CPU-side checks of the C ABI: the library loads, exports every symbol include/oid.h declares,
+validates parameters, and its Gauss-256 table equals the oracle's (built independently)."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def oid():
+    from __graft_entry__ import build
+    build()
+    import paper_2405_16076_b200 as oid
+    return oid
+
+
+def _declared_functions():
+    src = open(os.path.join(ROOT, "include", "oid.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(oid_[a-z_]+)\s*\(", src)))
+
+
+def test_header_symbols_exported(oid):
+    names = _declared_functions()
+    assert len(names) >= 17
+    lib = oid.lib()
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(oid.EXPORTED)
+
+
+def test_version(oid):
+    assert "sm_100a" in oid.version()
+
+
+def test_sketch_table_matches_oracle(oid):
+    from oracle import gauss256_table, gauss256_scale
+    q, s = oid.sketch_table()
+    assert np.array_equal(q, gauss256_table())
+    assert s == gauss256_scale()
+
+
+def test_workspace_query_validates(oid):
+    good = oid.make_params(m=4096, k=20, ell=48, b_max=16, n_cap=512, lam=1e-7, split=(16, 16, 16))
+    assert oid.workspace_bytes(good) > 0
+    bad_cases = [
+        dict(m=4096, k=60, ell=48, b_max=16, n_cap=512, lam=0.0),                  # k > ell
+        dict(m=4096, k=20, ell=48, b_max=65, n_cap=512, lam=0.0),                  # b_max > 64
+        dict(m=4096, k=20, ell=48, b_max=16, n_cap=512, lam=-3.0),                 # bad lambda mode
+        dict(m=4096, k=20, ell=48, b_max=16, n_cap=512, lam=0.0, split=(10, 10, 10)),
+        dict(m=4096, k=20, ell=48, b_max=16, n_cap=512, lam=0.0, row_begin=100, row_end=50),
+        dict(m=4096, k=20, ell=2000, b_max=16, n_cap=512, lam=0.0),                # ell > 1024
+    ]
+    for kw in bad_cases:
+        with pytest.raises(oid.OidError):
+            oid.workspace_bytes(oid.make_params(**kw))
+
+
+def test_struct_layout_matches_header(oid):
+    # oid_params: 4 int64 + 6 int32 + 4 double + uint64 + 4 int32 = 32 + 24 + 32 + 8 + 16 = 112 bytes
+    assert ctypes.sizeof(oid.OidParams) == 112
+    assert ctypes.sizeof(oid.OidStats) == 4 * 8 + 3 * 8 + 8
