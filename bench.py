@@ -1,0 +1,364 @@
+"""Snapshot-ingest benchmark of the B200 single-pass randomized ID path (BASELINE.json metric:
+"snapshot ingest GB/s (sketch+CSS+Hutch++) at 1/2/4/8 B200; % of roofline").
+
+One step = one block of b snapshots through the whole hot path:
+oid_ingest_block (fused sketch incl. the NA-Hutch++ row blocks + norms, [all-reduce], Gram,
+ridge regulariser, ridge scores, selection, basis copy, Alg 4) followed by the Alg 8 error
+estimate (basis Gram + NA-Hutch++), i.e. Alg 3 steps 9-32 with Alg 4 only.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C3] [--impl reference]
+
+N > 1 is launched by torchrun: rows are sharded (strong scaling, fixed m), one NCCL
+all-reduce of the (l+1) x b partial sketch per block and one of the t x t basis-Gram
+partials per estimate.  Prints ONE JSON line on rank 0.
+"""
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (grid, b, k, ell, dtype, description)
+    "C3": ((192, 129, 192), 32, 200, 512, "f64",
+           "C3 channel-flow stand-in: 3 components on 192x129x192 (m=14,266,368) fp64, b=32, k=200, l=512"),
+    "C3r": ((48, 33, 48), 32, 200, 512, "f64", "C3r: C3 on a 48x33x48 grid (m=228,096)"),
+}
+METRIC = "snapshot ingest GB/s (sketch+CSS+Hutch++) at 1/2/4/8 B200; % of roofline"
+FP64_NOMINAL_TF, BF16_NOMINAL_TF = 40.0, 2250.0    # B200 datasheet ratio used to derive the fp64 peak
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=8)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--workload", default="C3", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--k1-mode", type=int, default=0)
+    ap.add_argument("--no-estimate", action="store_true", help="ingest only (estimate not in the step)")
+    ap.add_argument("--cpu-sample-rows", type=int, default=1 << 18)
+    ap.add_argument("--skip-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mp = json.load(f)
+        return mp["hbm_gbs"], mp["bf16_tflops"], mp.get("bf16_tflops_sustained", mp["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.proc = None
+        self.idx = gpu_index
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "-i", str(self.idx),
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------ CPU oracle legs
+def oracle_sample(workload, rows, steps=1, warmup=0):
+    """Time the CPU oracle (as it stands) on row-sampled blocks of the workload.
+
+    Each step = OracleOID.ingest_block + error_estimate on rows [0, rows) of one fresh block.
+    Returns (GB/s over the timed steps, seconds per step, BLAS threads, sample description).
+    """
+    from oracle import OracleParams, OracleOID
+    from synth import ChannelFlow
+    grid, b, k, ell, dt, _ = WORKLOADS[workload]
+    gen = ChannelFlow(*grid, seed=1003)
+    m = gen.m
+    rows = min(rows, m)
+    sp = (ell // 6, ell // 3, ell - ell // 6 - ell // 3)
+    o = OracleOID(OracleParams(m=m, k=k, ell=ell, ell1=sp[0], ell2=sp[1], ell3=sp[2], lam=-1.0, seed=0,
+                               row_begin=0, row_end=rows), cache_omega=False)
+    blocks = [_host_rows(gen, s * b, (s + 1) * b, rows) for s in range(warmup + steps)]
+    for X in blocks[:warmup]:
+        o.ingest_block(X)
+        o.error_estimate()
+    t0 = time.perf_counter()
+    for X in blocks[warmup:]:
+        o.ingest_block(X)
+        o.error_estimate()
+    dt_s = time.perf_counter() - t0
+    try:
+        from threadpoolctl import threadpool_info
+        thr = max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
+    except Exception:
+        thr = 1
+    gbs = steps * rows * b * 8 / dt_s / 1e9
+    sample = (f"{workload} rows [0,{rows}) of {m} x {b} snapshots per block, all {ell} sketch rows, "
+              f"{steps} timed block(s) after {warmup} warm-up: oracle ingest_block + error_estimate")
+    return gbs, dt_s / steps, thr, sample
+
+
+def _host_rows(gen, t0, t1, rows):
+    """Rows [0, rows) of a ChannelFlow block on the host (numpy), same formula as synth.ChannelFlow.block."""
+    import numpy as np
+    plane = gen.ny * gen.nx
+    nz_needed = (rows + plane - 1) // plane
+    a = gen._coeff(t0, t1)
+    ex = np.exp(1j * gen.alpha[None, :] * gen.x[:, None] / 4)
+    ez = np.exp(1j * 2 * gen.beta[None, :] * gen.z[:, None] / 3)
+    out = np.empty((nz_needed * plane, t1 - t0))
+    for zi in range(nz_needed):
+        F = (ez[zi][None, None, :] * gen.g[:, None, :] * ex[None, :, :]).reshape(-1, gen.NMODE)
+        out[zi * plane:(zi + 1) * plane] = (F @ a[0]).real + (1 - gen.y ** 2).repeat(gen.nx)[:, None]
+    out = out[:rows]
+    for j, t in enumerate(range(t0, t1)):
+        out[:, j] += gen.noise * np.random.default_rng([gen.seed, t]).standard_normal(rows)
+    return out
+
+
+def run_reference(args, rank, world):
+    """Reference arm = the CPU oracle (no runnable reference implementation exists)."""
+    if rank != 0:
+        return
+    steps = max(1, args.steps)
+    rows = min(args.cpu_sample_rows, 1 << 16)
+    gbs, secs, thr, sample = oracle_sample(args.workload, rows, steps=steps, warmup=min(args.warmup, 1))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus, "steps": steps,
+        "warmup": args.warmup, "ms_per_step": secs * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.workload][5], "sample_rows": rows},
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": thr, "kind": "oracle", "sample": sample},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ B200 arm
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from __graft_entry__ import build
+    build()
+    import paper_2405_16076_b200 as oid
+    from synth import ChannelFlow
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    grid, b, k, ell, dt, desc = WORKLOADS[args.workload]
+    gen = ChannelFlow(*grid, seed=1003)
+    m = gen.m
+    rb, re = (m * rank) // world, (m * (rank + 1)) // world
+    m_loc = re - rb
+    W, K, E = args.warmup, args.steps, args.e2e_steps
+    nblk = W + K + E
+    n_cap = max(1000, nblk * b)
+    split = (ell // 6, ell // 3, ell - ell // 6 - ell // 3)
+    p = oid.make_params(m=m, k=k, ell=ell, b_max=b, n_cap=n_cap, lam=-1.0, split=split, seed=0, dtype=dt,
+                        row_begin=rb, row_end=re, k1_mode=args.k1_mode, profile=True, device=local)
+    eng = oid.Engine(p)
+    stream = eng.stream
+
+    # synthetic blocks, generated on the device outside any timed region (inputs >> L2)
+    blocks = []
+    for s in range(W + K):
+        blocks.append(gen.block_torch(s * b, (s + 1) * b, dev, row_begin=rb, row_end=re).T)   # (m_loc, b) col-major
+    torch.cuda.synchronize()
+    est_out = torch.empty(8, dtype=torch.float64, device=dev)
+    sharded = world > 1
+
+    def step(X):
+        if sharded:
+            eng.ingest_sketch(X)
+            dist.all_reduce(eng.partials(0))
+            eng.ingest_commit(X)
+        else:
+            eng.ingest_block(X)
+        if not args.no_estimate:
+            eng.estimate_begin()
+            if sharded:
+                dist.all_reduce(eng.partials(1))
+            eng.estimate_end(est_out)
+
+    for s in range(W):
+        step(blocks[s])
+    torch.cuda.synchronize()
+    eng.stats_reset()
+    if sharded:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for s in range(W, W + K):
+        step(blocks[s])
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if sharded:
+        dist.barrier()
+    clocks = clk.stop()
+    ms = ev0.elapsed_time(ev1)
+    st = eng.stats()
+    if sharded:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    dsz = 8 if dt == "f64" else 4
+    block_bytes = m * b * dsz                       # all ranks together
+    value = K * block_bytes / (ms * 1e-3) / 1e9
+    est_val = est_out.cpu().tolist()
+
+    # roofline of the dominant kernel (K1, fused ingest) on this rank
+    hbm, bf16, bf16_sus, src = peaks()
+    k1_avg_ms = st["k1_ms"] / max(1, st["k1_launches"])
+    k1_bytes = m_loc * b * dsz
+    k1_flops = 2.0 * ell * m_loc * b
+    mode = st["k1_mode_used"]
+    achieved_gbs = k1_bytes / (k1_avg_ms * 1e-3) / 1e9
+    if mode == oid.K1_TC_INT8:
+        pipe_peak = 2 * bf16_sus * 1e12                   # int8 dense = 2x bf16 (nominal ratio)
+        slices = 8 if dt == "f64" else 4
+        pipe_time = slices * k1_flops / pipe_peak
+    else:
+        pipe_peak = bf16_sus * FP64_NOMINAL_TF / BF16_NOMINAL_TF * 1e12
+        pipe_time = k1_flops / pipe_peak
+    hbm_time = k1_bytes / (hbm * 1e9)
+    if hbm_time >= pipe_time:
+        roof = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s", "frac": achieved_gbs / hbm}
+    else:
+        ach = (k1_flops if mode != oid.K1_TC_INT8 else slices * k1_flops) / (k1_avg_ms * 1e-3) / 1e12
+        roof = {"bound": "tensor" if mode == oid.K1_TC_INT8 else "fp64",
+                "achieved": ach, "peak": pipe_peak / 1e12, "unit": "TFLOP/s", "frac": ach * 1e12 / pipe_peak}
+    roof["peak_source"] = src
+    roof["kernel"] = "k1_tc_int8" if mode == oid.K1_TC_INT8 else "k1_simt_kernel"
+    roof["traffic"] = _traffic_from_profiles(args.workload, mode)
+    roof["k1_ms"] = k1_avg_ms
+
+    # e2e through the public API with HOST buffers (pinned), H2D + D2H inside the timed region
+    e2e = None
+    if E > 0:
+        host = []
+        for s in range(E):
+            t0_ = (W + K + s) * b
+            hb = torch.empty((b, m_loc), dtype=blocks[0].dtype, pin_memory=True)
+            hb.copy_(gen.block_torch(t0_, t0_ + b, dev, row_begin=rb, row_end=re).cpu())
+            host.append(hb)
+        dbuf = torch.empty((b, m_loc), dtype=blocks[0].dtype, device=dev)
+        est_host = torch.empty(8, dtype=torch.float64, pin_memory=True)
+        del blocks
+        torch.cuda.synchronize()
+        if sharded:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for hb in host:
+            dbuf.copy_(hb, non_blocking=True)
+            step(dbuf.T)
+            est_host.copy_(est_out, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if sharded:
+            t = torch.tensor([ems], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = t.item()
+        e2e = {"value": E * block_bytes / (ems * 1e-3) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": block_bytes, "d2h_bytes_per_step": 8 * 8, "steps": E}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.skip_cpu_baseline:
+        gbs, secs, thr, sample = oracle_sample(args.workload, args.cpu_sample_rows)
+        cpu = {"value": gbs, "unit": "GB/s", "cores": thr, "kind": "oracle", "sample": sample, "seconds": secs}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong" if world > 1 else "strong",
+            "vs_baseline": None, "dtype": dt, "data": "synthetic",
+            "config": {"workload": desc, "m": m, "b": b, "k": k, "ell": ell, "lambda": "paper surrogate (-1)",
+                       "step": "ingest_block + error_estimate" if not args.no_estimate else "ingest_block",
+                       "l2": "inputs larger than L2 (each block %.2f GB, fresh block per step)" % (block_bytes / 1e9),
+                       "parallelism": f"rows sharded over {world} GPU(s)"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clocks,
+            "gpu_launches": st["launches"],
+            "breakdown_ms_per_step": {"k1": st["k1_ms"] / K, "post": st["post_ms"] / K, "estimate": st["est_ms"] / K},
+            "last_estimate": {"est_rel": est_val[5], "e2": est_val[0], "flags": int(est_val[6])},
+            "k1_mode": "tc_int8" if mode == oid.K1_TC_INT8 else "simt_f64",
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if sharded:
+        dist.destroy_process_group()
+
+
+def _traffic_from_profiles(workload, mode):
+    """dram bytes per K1 launch from the committed ncu capture, when it matches this workload/kernel."""
+    path = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        key = f"{workload}:{'tc' if mode == 2 else 'simt'}"
+        return d.get(key)
+    except Exception:
+        return None
+
+
+if __name__ == "__main__":
+    main()
