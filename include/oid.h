@@ -151,7 +151,8 @@ oid_status oid_finalize(oid_ctx ctx, int64_t* J_host, double* P, int32_t P_on_de
    field: 0 J (k int64), 1 tau_old (k), 2 S (ell x n_obs), 3 Gram (ell x ell),
           4 scalars [frob2, lambda_eff, E_k, shift, trace, dmax, min_margin, kappa],
           5 last scores (k + ncols: basis slots then candidates), 6 eigenvalues of Gram (ell),
-          7 last ingest partials ((ell+1) * ncols), 8 S_J^+ (k x ell). */
+          7 last ingest partials ((ell+1) * ncols), 8 S_J^+ (k x ell),
+          9 Jacobi rotation counts per sweep (3 x 48 int32: Gram, S_J, NA-Hutch++ core). */
 oid_status oid_get(oid_ctx ctx, int32_t field, void* host_dst, size_t bytes, void* stream);
 
 /* Counters and CUDA-event timings (synchronizes the context's recorded events).
@@ -164,7 +165,7 @@ oid_status oid_stats_reset(oid_ctx ctx);
 oid_status oid_sketch_table(int32_t q[256], double* scale);
 
 void oid_destroy(oid_ctx ctx);
-const char* oid_last_error(oid_ctx ctx);
+const char* oid_last_error(oid_ctx ctx);   /* ctx == NULL: last oid_init failure (this thread) */
 const char* oid_version(void);
 
 #ifdef __cplusplus

@@ -138,7 +138,7 @@ class Engine:
         st = _lib.oid_init(ctypes.byref(params), ctypes.c_void_p(self.ws.data_ptr()), self.ws_bytes,
                            self._st(), ctypes.byref(h))
         if st != OID_OK:
-            raise OidError(st, "oid_init failed")
+            raise OidError(st, "oid_init failed: " + _lib.oid_last_error(None).decode())
         self.h = h
         self.dtype = torch.float64 if params.dtype == OID_F64 else torch.float32
 
@@ -214,7 +214,8 @@ class Engine:
         n_obs = self.stats()["n_obs"] if field == 2 else 0
         shapes = {0: ((t,), np.int64), 1: ((t,), np.float64), 2: ((n_obs, ell), np.float64),
                   3: ((ell, ell), np.float64), 4: ((8,), np.float64), 5: ((t + bm,), np.float64),
-                  6: ((ell,), np.float64), 7: (((ell + 1) * bm,), np.float64), 8: ((ell, t), np.float64)}
+                  6: ((ell,), np.float64), 7: (((ell + 1) * bm,), np.float64), 8: ((ell, t), np.float64),
+                  9: ((3, 48), np.int32)}
         shape, dt = shapes[field]
         a = np.empty(shape, dtype=dt)
         self._check(_lib.oid_get(self.h, field, ctypes.c_void_p(a.ctypes.data), a.nbytes, self._st()), "oid_get")

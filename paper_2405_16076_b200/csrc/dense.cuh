@@ -7,6 +7,21 @@
 namespace oid {
 namespace cg = cooperative_groups;
 
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// out = ||A||_F^2 over len doubles (one CTA, fixed order)
+__global__ void fro2_kernel(const double* __restrict__ A, int64_t len, double* __restrict__ out) {
+  __shared__ double red[8];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < len; i += blockDim.x) s = fma(A[i], A[i], s);
+  s = block_sum<256>(s, red);
+  if (threadIdx.x == 0) *out = s;
+}
+
 // C (M x N, ldc) = alpha * op(A) * op(B) + beta * C, column-major, op = transpose if T*.
 // 32x32 output tile per CTA, 256 threads x 4 outputs, K staged in 16-wide smem panels.
 template <bool TA, bool TB>
@@ -130,6 +145,121 @@ __global__ void __launch_bounds__(256) jacobi_svd_kernel(double* __restrict__ B,
           }
           if (threadIdx.x == 0) atomicAdd(&counters[sweep], 1);
         }
+      }
+      grid.sync();
+    }
+    const int rotated = atomicAdd(&counters[sweep], 0);
+    if (rotated == 0) break;
+  }
+}
+
+// Block one-sided Jacobi: the n columns of B (L x n) are cut into blocks of W columns; each
+// outer round pairs blocks round-robin and one CTA (W warps) orthogonalises the 2W columns of
+// its block pair with one inner cyclic sweep held in shared memory (B and V columns staged),
+// one warp per column pair, warp-shuffle dot products.  One grid-wide barrier per outer round;
+// outer sweeps stop when a sweep applies no rotation.  V (n x n) must hold the initial
+// orthogonal matrix (identity or a warm start) and B = A V on entry.  Cooperative launch,
+// dynamic smem = 2W (L + n) doubles.
+template <int W>
+__global__ void __launch_bounds__(32 * W) bjacobi_kernel(double* __restrict__ B, int L, int n, double* __restrict__ V,
+                                                         int* __restrict__ counters, int max_sweeps, double tol,
+                                                         const double* __restrict__ fro2) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double sm[];
+  double* Bs = sm;                       // [2W][L]
+  double* Vs = sm + 2 * W * L;           // [2W][n]
+  __shared__ int gcol[2 * W];
+  __shared__ int nrot;
+  const int nb = (n + W - 1) / W;
+  const int nbb = nb + (nb & 1);
+  const int npairs = nbb / 2;
+  const int m1 = nbb - 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double floor2 = 1e-28 * (*fro2);
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    for (int k = 0; k < max(m1, 1); ++k) {
+      for (int pi = blockIdx.x; pi < npairs; pi += gridDim.x) {
+        int a, b;
+        if (pi == 0) { a = m1; b = k; } else { a = (k + pi) % m1; b = (k - pi + m1) % m1; }
+        if (m1 == 0) { a = 0; b = 1; }
+        const int P = min(a, b), Q = max(a, b);
+        if (P >= nb) continue;
+        if (threadIdx.x < 2 * W) {
+          const int c = threadIdx.x;
+          const int blk = c < W ? P : Q;
+          const int g = blk * W + (c % W);
+          gcol[c] = (blk < nb && g < n) ? g : -1;
+        }
+        if (threadIdx.x == 0) nrot = 0;
+        __syncthreads();
+        // stage the 2W columns of B and V with asynchronous 8-byte copies (all in flight at once)
+        for (int e = threadIdx.x; e < 2 * W * L; e += blockDim.x) {
+          const int c = e / L, i = e - c * L;
+          const int g = gcol[c];
+          if (g >= 0) cp_async8(Bs + e, B + static_cast<int64_t>(g) * L + i);
+        }
+        for (int e = threadIdx.x; e < 2 * W * n; e += blockDim.x) {
+          const int c = e / n, i = e - c * n;
+          const int g = gcol[c];
+          if (g >= 0) cp_async8(Vs + e, V + static_cast<int64_t>(g) * n + i);
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        const int m2 = 2 * W - 1;
+        for (int r = 0; r < m2; ++r) {
+          int p, q;
+          if (warp == 0) { p = m2; q = r; } else { p = (r + warp) % m2; q = (r - warp + m2) % m2; }
+          if (p > q) { const int tmp = p; p = q; q = tmp; }
+          if (gcol[p] >= 0 && gcol[q] >= 0) {
+            double* bp = Bs + p * L;
+            double* bq = Bs + q * L;
+            double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll 4
+            for (int i = lane; i < L; i += 32) {
+              const double x = bp[i], y = bq[i];
+              al = fma(x, x, al); be = fma(y, y, be); ga = fma(x, y, ga);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              al += __shfl_xor_sync(0xffffffffu, al, o);
+              be += __shfl_xor_sync(0xffffffffu, be, o);
+              ga += __shfl_xor_sync(0xffffffffu, ga, o);
+            }
+            // columns at the rounding-noise level of B (||b||^2 <= (1e-14 ||B||_F)^2) are not rotated:
+            // they carry no information and would never satisfy the relative test.
+            if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be) && fmin(al, be) > floor2) {
+              const double zeta = (be - al) / (2.0 * ga);
+              double t;
+              if (fabs(zeta) > 1e150) t = 0.5 / zeta;
+              else t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+              const double cs = 1.0 / sqrt(fma(t, t, 1.0)), sn = cs * t;
+#pragma unroll 4
+              for (int i = lane; i < L; i += 32) {
+                const double x = bp[i], y = bq[i];
+                bp[i] = cs * x - sn * y;
+                bq[i] = sn * x + cs * y;
+              }
+              double* vp = Vs + p * n;
+              double* vq = Vs + q * n;
+#pragma unroll 4
+              for (int i = lane; i < n; i += 32) {
+                const double x = vp[i], y = vq[i];
+                vp[i] = cs * x - sn * y;
+                vq[i] = sn * x + cs * y;
+              }
+              if (lane == 0) atomicAdd(&nrot, 1);
+            }
+          }
+          __syncthreads();
+        }
+        for (int c = 0; c < 2 * W; ++c) {
+          const int g = gcol[c];
+          if (g < 0) continue;
+          for (int i = threadIdx.x; i < L; i += blockDim.x) B[static_cast<int64_t>(g) * L + i] = Bs[c * L + i];
+          for (int i = threadIdx.x; i < n; i += blockDim.x) V[static_cast<int64_t>(g) * n + i] = Vs[c * n + i];
+        }
+        if (threadIdx.x == 0 && nrot) atomicAdd(&counters[sweep], nrot);
+        __syncthreads();
       }
       grid.sync();
     }

@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -25,7 +26,8 @@ using namespace oid;
 namespace {
 
 constexpr int kK1MaxCtas = 1024;
-constexpr int kGramChunks = 96;
+thread_local char g_init_err[512] = "no error";
+constexpr int kGramChunks = 296;
 constexpr int kMaxSweeps = 48;
 constexpr int kNumJacobiUses = 3;
 
@@ -84,7 +86,7 @@ struct Bump {
 struct Layout {
   size_t S, gram, Ypart, k1part, k1npart, gB, gV, mu, mu_sorted, Yc, Tsc, tau, scal, J, tau_old, admit, counts,
       flags, counters, C, SJ, sjB, sjV, sjsig, sjw, sjZ, Sjpinv, Pexp, AJP, G, Gsum, Gpart, cB, cV, csig, cw, cZ, M,
-      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, total;
+      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, total;
 };
 
 int64_t m_local(const oid_params& p) { return p.row_end - p.row_begin; }
@@ -144,6 +146,10 @@ Layout make_layout(const oid_params& p) {
   L.R3 = b.take(std::max<size_t>(1, l3 * l1) * d);
   L.PPt = b.take(t * t * d);
   L.est = b.take(8 * d);
+  L.Gfull = b.take(t * t * d);
+  L.dirty = b.take(t * sizeof(int));
+  L.dlist = b.take(t * sizeof(int));
+  L.jfro2 = b.take(kNumJacobiUses * d);
   L.tc = b.take(k1tc_workspace_bytes(p.ell, p.b_max, m_local(p), p.dtype == OID_F64));
   L.total = b.off;
   return L;
@@ -189,6 +195,7 @@ struct oid_ctx_s {
   int64_t launches = 0, k1_launches = 0;
   int k1_mode_used = 0;
   bool tc_ok = false;
+  bool cold_jacobi = false;   // diagnostics: OID_JACOBI_COLD=1 disables the warm starts
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_k1, ev_post, ev_est;
   char err[512] = {0};
 
@@ -233,20 +240,35 @@ oid_status gemm(oid_ctx ctx, cudaStream_t st, bool ta, bool tb, int M, int N, in
   return OID_OK;
 }
 
-// One-sided Jacobi SVD of B (L x n) in place, V (n x n) set to I first; sig = column norms.
-oid_status jacobi(oid_ctx ctx, cudaStream_t st, double* B, int L, int n, double* V, double* sig, int use) {
+// Block one-sided Jacobi SVD of B (L x n) in place.  warm = false: V <- I first (B = A);
+// warm = true: V holds an orthogonal start and the caller has set B = A V.  sig = column norms.
+oid_status jacobi(oid_ctx ctx, cudaStream_t st, double* B, int L, int n, double* V, double* sig, int use,
+                  bool warm = false) {
   if (n <= 0) return OID_OK;
-  set_identity_kernel<<<blocks_for(int64_t(n) * n), 256, 0, st>>>(V, n);
-  CKL();
+  if (!warm) {
+    set_identity_kernel<<<blocks_for(int64_t(n) * n), 256, 0, st>>>(V, n);
+    CKL();
+  }
   int* counters = ctx->ptr<int>(ctx->L.counters) + use * kMaxSweeps;
   CK(cudaMemsetAsync(counters, 0, kMaxSweeps * sizeof(int), st));
   if (n > 1) {
-    const int npairs = (n + (n & 1)) / 2;
-    const int grid = std::max(1, std::min(npairs, ctx->coop_max));
+    const bool w8 = (L + n) <= 1600;
+    const int Wd = w8 ? 8 : 4;
+    const size_t smem = sizeof(double) * 2 * Wd * (L + n);
+    const void* fn = w8 ? reinterpret_cast<const void*>(bjacobi_kernel<8>) : reinterpret_cast<const void*>(bjacobi_kernel<4>);
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * Wd, smem));
+    const int nb = (n + Wd - 1) / Wd;
+    const int npairs = (nb + (nb & 1)) / 2;
+    const int grid = std::max(1, std::min(npairs, std::max(1, per_sm) * ctx->num_sms));
+    double* fro2 = ctx->d(ctx->L.jfro2) + use;
+    fro2_kernel<<<1, 256, 0, st>>>(B, int64_t(L) * n, fro2);
+    CKL();
     int Li = L, ni = n, ms = kMaxSweeps;
-    double tol = 1e-15 * std::max(1.0, std::sqrt(static_cast<double>(L)));
-    void* args[] = {&B, &Li, &ni, &V, &counters, &ms, &tol};
-    CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(jacobi_svd_kernel), dim3(grid), dim3(256), args, 0, st));
+    // relative orthogonality target: well above the dot-product rounding level (~L eps)
+    double tol = 4e-14 * std::max(1.0, std::sqrt(static_cast<double>(L) / 16.0));
+    void* args[] = {&B, &Li, &ni, &V, &counters, &ms, &tol, &fro2};
+    CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(32 * Wd), args, smem, st));
     CKL();
   }
   col_norms_kernel<<<n, 256, 0, st>>>(B, L, n, sig);
@@ -322,13 +344,15 @@ oid_status launch_k1_simt(oid_ctx ctx, cudaStream_t st, const T* X, int64_t ld, 
 oid_status do_sketch(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_t st) {
   const oid_params& p = ctx->p;
   const bool want_tc = (p.k1_mode == OID_K1_TC_INT8) || (p.k1_mode == OID_K1_AUTO && ctx->tc_ok);
-  if (want_tc) {
-    if (!ctx->tc_ok) return ctx->fail(OID_EINVAL, "tensor-core K1 unavailable for this device/shape");
-    K1TcArgs a{};
-    a.X = X; a.ld = ld; a.ncols = nc; a.row_begin = p.row_begin; a.row_end = p.row_end; a.ell = p.ell;
-    a.key0 = ctx->key0; a.key1 = ctx->key1; a.scale = ctx->qscale; a.f64 = p.dtype == OID_F64;
-    a.ws = ctx->ws + ctx->L.tc; a.out = ctx->d(ctx->L.Ypart); a.flags = ctx->ptr<unsigned>(ctx->L.flags);
-    a.num_sms = ctx->num_sms;
+  K1TcArgs a{};
+  a.X = X; a.ld = ld; a.ncols = nc; a.row_begin = p.row_begin; a.row_end = p.row_end; a.ell = p.ell;
+  a.key0 = ctx->key0; a.key1 = ctx->key1; a.scale = ctx->qscale; a.f64 = p.dtype == OID_F64;
+  a.ws = ctx->ws + ctx->L.tc; a.out = ctx->d(ctx->L.Ypart); a.flags = ctx->ptr<unsigned>(ctx->L.flags);
+  a.num_sms = ctx->num_sms;
+  const bool tc_call = want_tc && ctx->tc_ok && k1tc_call_ok(a);
+  if (p.k1_mode == OID_K1_TC_INT8 && !tc_call)
+    return ctx->fail(OID_EINVAL, "tensor-core K1 unavailable for this device/shape/alignment");
+  if (tc_call) {
     int nl = 0;
     cudaError_t e;
     {
@@ -357,8 +381,15 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
                                                                     scal);
   CKL();
   // A4: eigen-decomposition of the Gram (one-sided Jacobi on a copy), lambda
-  CK(cudaMemcpyAsync(ctx->d(L.gB), ctx->d(L.gram), sizeof(double) * ell * ell, cudaMemcpyDeviceToDevice, st));
-  oid_status s = jacobi(ctx, st, ctx->d(L.gB), ell, ell, ctx->d(L.gV), ctx->d(L.mu), 0);
+  oid_status s;
+  if (ctx->epoch == 0 || ctx->cold_jacobi) {
+    CK(cudaMemcpyAsync(ctx->d(L.gB), ctx->d(L.gram), sizeof(double) * ell * ell, cudaMemcpyDeviceToDevice, st));
+    s = jacobi(ctx, st, ctx->d(L.gB), ell, ell, ctx->d(L.gV), ctx->d(L.mu), 0);
+  } else {   // warm start from the previous eigenvectors: B = Gram V_prev
+    s = gemm(ctx, st, false, false, ell, ell, ell, 1.0, ctx->d(L.gram), ell, ctx->d(L.gV), ell, 0.0, ctx->d(L.gB), ell);
+    if (s != OID_OK) return s;
+    s = jacobi(ctx, st, ctx->d(L.gB), ell, ell, ctx->d(L.gV), ctx->d(L.mu), 0, true);
+  }
   if (s != OID_OK) return s;
   lambda_kernel<<<1, 256, 0, st>>>(ctx->d(L.mu), ell, p.k, ctx->d(L.gram), p.lambda, ell, scal, ctx->d(L.mu_sorted));
   CKL();
@@ -373,7 +404,7 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   // A6: selection / replacement
   select_kernel<<<1, 32, 0, st>>>(ctx->ptr<int64_t>(L.J), ctx->d(L.tau_old), ctx->d(L.tau), Yp + int64_t(ell) * nc, t, nc,
                                   ctx->factor, static_cast<uint32_t>(ctx->epoch), ctx->n_obs, ctx->key0, ctx->key1,
-                                  ctx->ptr<int>(L.admit), ctx->ptr<int>(L.counts), scal);
+                                  ctx->ptr<int>(L.admit), ctx->ptr<int>(L.counts), scal, ctx->ptr<int>(L.dirty));
   CKL();
   // A7: basis copy of this shard's rows
   {
@@ -390,8 +421,14 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   // A8: Alg 4 kept implicit: S_J^+ = V diag(1/sigma^2) B^T from the SVD of S_J
   gather_sj_kernel<<<blocks_for(int64_t(ell) * t), 256, 0, st>>>(ctx->d(L.S), ctx->ptr<int64_t>(L.J), t, ell, ctx->d(L.SJ));
   CKL();
-  CK(cudaMemcpyAsync(ctx->d(L.sjB), ctx->d(L.SJ), sizeof(double) * ell * t, cudaMemcpyDeviceToDevice, st));
-  s = jacobi(ctx, st, ctx->d(L.sjB), ell, t, ctx->d(L.sjV), ctx->d(L.sjsig), 1);
+  if (ctx->epoch == 0 || ctx->cold_jacobi) {
+    CK(cudaMemcpyAsync(ctx->d(L.sjB), ctx->d(L.SJ), sizeof(double) * ell * t, cudaMemcpyDeviceToDevice, st));
+    s = jacobi(ctx, st, ctx->d(L.sjB), ell, t, ctx->d(L.sjV), ctx->d(L.sjsig), 1);
+  } else {   // warm start: B = S_J V_prev
+    s = gemm(ctx, st, false, false, ell, t, t, 1.0, ctx->d(L.SJ), ell, ctx->d(L.sjV), t, 0.0, ctx->d(L.sjB), ell);
+    if (s != OID_OK) return s;
+    s = jacobi(ctx, st, ctx->d(L.sjB), ell, t, ctx->d(L.sjV), ctx->d(L.sjsig), 1, true);
+  }
   if (s != OID_OK) return s;
   s = pinv_assemble(ctx, st, ctx->d(L.sjB), ell, t, ctx->d(L.sjV), ctx->d(L.sjsig), ctx->d(L.sjw), ctx->d(L.sjZ),
                     ctx->d(L.Sjpinv), scal + SC_KAPPA, OID_FLAG_SJ_RANK_DEFICIENT);
@@ -425,7 +462,7 @@ extern "C" {
 
 const char* oid_version(void) { return "liboid 0.1 (sm_100a)"; }
 
-const char* oid_last_error(oid_ctx ctx) { return ctx ? ctx->err : "null context"; }
+const char* oid_last_error(oid_ctx ctx) { return ctx ? ctx->err : g_init_err; }
 
 oid_status oid_workspace_query(const oid_params* p, size_t* bytes) {
   if (!bytes || validate(p)) return OID_EINVAL;
@@ -462,7 +499,7 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
   gauss256(q, &ctx->qscale);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   auto bad = [&](cudaError_t e) {
-    snprintf(ctx->err, sizeof(ctx->err), "init: %s", cudaGetErrorString(e));
+    snprintf(g_init_err, sizeof(g_init_err), "init: %s", cudaGetErrorString(e));
     delete ctx;
     return OID_ECUDA;
   };
@@ -474,7 +511,18 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
   int per_sm = 0;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_svd_kernel, 256, 0)) != cudaSuccess) return bad(e);
   ctx->coop_max = std::max(1, per_sm * ctx->num_sms);
+  {
+    const int big = static_cast<int>(prop.sharedMemPerBlockOptin) - 2048;
+    if ((e = cudaFuncSetAttribute(bjacobi_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big)) != cudaSuccess) return bad(e);
+    if ((e = cudaFuncSetAttribute(bjacobi_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big)) != cudaSuccess) return bad(e);
+#define BG_ATTR(TT, JC, DQ) \
+    if ((e = cudaFuncSetAttribute(basis_gram_dirty_kernel<TT, JC, DQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, big)) != cudaSuccess) return bad(e)
+    BG_ATTR(double, 1, 32); BG_ATTR(double, 2, 32); BG_ATTR(double, 3, 16); BG_ATTR(double, 4, 16);
+    BG_ATTR(float, 1, 32); BG_ATTR(float, 2, 32); BG_ATTR(float, 3, 16); BG_ATTR(float, 4, 16);
+#undef BG_ATTR
+  }
   ctx->k1_ctas_per_sm = 1;
+  ctx->cold_jacobi = getenv("OID_JACOBI_COLD") && atoi(getenv("OID_JACOBI_COLD")) != 0;
   ctx->tc_ok = (prop.major == 10 && prop.minor == 0) && k1tc_supported(p->ell, p->b_max, p->dtype == OID_F64);
   double qd[256];
   for (int i = 0; i < 256; ++i) qd[i] = q[i];
@@ -492,6 +540,9 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
   sc[SC_KAPPA] = 1.0;
   if ((e = cudaMemcpyAsync(ctx->ws + L.scal, sc, sizeof(sc), cudaMemcpyHostToDevice, st)) != cudaSuccess) return bad(e);
   if ((e = cudaMemsetAsync(ctx->ws + L.flags, 0, 4 * sizeof(unsigned), st)) != cudaSuccess) return bad(e);
+  if ((e = cudaMemsetAsync(ctx->ws + L.Gfull, 0, sizeof(double) * ctx->t * ctx->t, st)) != cudaSuccess) return bad(e);
+  if ((e = cudaMemsetAsync(ctx->ws + L.dirty, 0, sizeof(int) * ctx->t, st)) != cudaSuccess) return bad(e);
+  if ((e = cudaMemsetAsync(ctx->ws + L.counts, 0, 4 * sizeof(int), st)) != cudaSuccess) return bad(e);
   if ((e = cudaMemsetAsync(ctx->ws + L.C, 0, static_cast<size_t>(ctx->m_loc) * ctx->t * dsize(*p), st)) != cudaSuccess) return bad(e);
   if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return bad(e);   // host arrays above go out of scope
   *out = ctx;
@@ -548,19 +599,29 @@ oid_status oid_estimate_begin(oid_ctx ctx, void* stream) {
   const Layout& L = ctx->L;
   const int t = ctx->t;
   EvScope ev(ctx, st, &ctx->ev_est);
-  // A9: exact basis Gram G = A_J^T A_J over this shard's rows
-  const int ntile = (t + 31) / 32;
-  const int npair = ntile * (ntile + 1) / 2;
-  int chunks = static_cast<int>(std::min<int64_t>(kGramChunks, (ctx->m_loc + 4095) / 4096));
+  // A9: exact basis Gram G = A_J^T A_J, incremental: only the rows/columns of
+  // slots admitted since the last estimate are recomputed, over this shard's rows.
+  dirty_compact_kernel<<<1, 32, 0, st>>>(ctx->ptr<int>(L.dirty), t, ctx->ptr<int>(L.dlist), ctx->ptr<int>(L.counts));
+  CKL();
+  int chunks = static_cast<int>(std::min<int64_t>(std::min(2 * ctx->num_sms, kGramChunks), (ctx->m_loc + 1023) / 1024));
   chunks = std::max(1, chunks);
   int64_t per = (ctx->m_loc + chunks - 1) / chunks;
-  per = (per + 31) / 32 * 32;
+  per = (per + 15) / 16 * 16;
   chunks = static_cast<int>((ctx->m_loc + per - 1) / per);
-  dim3 grid(chunks, npair);
-  if (ctx->p.dtype == OID_F64)
-    basis_gram_kernel<double><<<grid, 256, 0, st>>>(ctx->ptr<double>(L.C), ctx->m_loc, t, per, ctx->d(L.Gpart));
-  else
-    basis_gram_kernel<float><<<grid, 256, 0, st>>>(ctx->ptr<float>(L.C), ctx->m_loc, t, per, ctx->d(L.Gpart));
+  const size_t smem = sizeof(double) * 16 * t;
+  const int jc = (t + 255) / 256;
+#define BG_LAUNCH(TT, JC, DQ)                                                                                   \
+  basis_gram_dirty_kernel<TT, JC, DQ><<<chunks, 256, smem, st>>>(ctx->ptr<TT>(L.C), ctx->m_loc, t, per,           \
+                                                                 ctx->ptr<int>(L.dlist), ctx->ptr<int>(L.counts), \
+                                                                 ctx->d(L.Gpart))
+#define BG_DISPATCH(TT)                          \
+  if (jc == 1) BG_LAUNCH(TT, 1, 32);              \
+  else if (jc == 2) BG_LAUNCH(TT, 2, 32);         \
+  else if (jc == 3) BG_LAUNCH(TT, 3, 16);         \
+  else BG_LAUNCH(TT, 4, 16)
+  if (ctx->p.dtype == OID_F64) { BG_DISPATCH(double); } else { BG_DISPATCH(float); }
+#undef BG_DISPATCH
+#undef BG_LAUNCH
   CKL();
   sum_chunks_kernel<<<blocks_for(int64_t(t) * t), 256, 0, st>>>(ctx->d(L.Gpart), chunks, int64_t(t) * t, ctx->d(L.Gsum));
   CKL();
@@ -578,7 +639,10 @@ oid_status oid_estimate_end(oid_ctx ctx, double* out_dev, void* stream) {
   double* S = ctx->d(L.S);
   double* scal = ctx->d(L.scal);
   EvScope ev(ctx, st, &ctx->ev_est);
-  CK(cudaMemcpyAsync(ctx->d(L.G), ctx->d(L.Gsum), sizeof(double) * t * t, cudaMemcpyDeviceToDevice, st));
+  gram_scatter_kernel<<<blocks_for(int64_t(t) * t), 256, 0, st>>>(ctx->d(L.Gsum), ctx->ptr<int>(L.dlist),
+                                                                  ctx->ptr<int>(L.counts), t, ctx->d(L.Gfull));
+  CKL();
+  CK(cudaMemcpyAsync(ctx->d(L.G), ctx->d(L.Gfull), sizeof(double) * t * t, cudaMemcpyDeviceToDevice, st));
   mask_gram_kernel<<<blocks_for(int64_t(t) * t), 256, 0, st>>>(ctx->d(L.G), ctx->ptr<int64_t>(L.J), t);
   CKL();
   oid_status s = explicit_P(ctx, st);                                                 // P = S_J^+ S
@@ -682,6 +746,7 @@ oid_status oid_get(oid_ctx ctx, int32_t field, void* host_dst, size_t bytes, voi
     case 6: off = L.mu; need = sizeof(double) * p.ell; break;
     case 7: off = L.Ypart; need = sizeof(double) * (p.ell + 1) * p.b_max; break;
     case 8: off = L.Sjpinv; need = sizeof(double) * ctx->t * p.ell; break;
+    case 9: off = L.counters; need = sizeof(int) * kNumJacobiUses * kMaxSweeps; break;
     default: return ctx->fail(OID_EINVAL, "unknown field %d", field);
   }
   if (bytes < need) return ctx->fail(OID_ESHAPE, "field %d needs %zu bytes", field, need);

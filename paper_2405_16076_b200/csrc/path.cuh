@@ -88,7 +88,7 @@ __global__ void scores_kernel(const double* __restrict__ T, const double* __rest
 __global__ void select_kernel(int64_t* __restrict__ J, double* __restrict__ tau_old, const double* __restrict__ tau,
                               const double* __restrict__ nrm, int t, int nc, double factor, uint32_t epoch,
                               int64_t base, uint32_t key0, uint32_t key1, int* __restrict__ admit,
-                              int* __restrict__ counts, double* __restrict__ scal) {
+                              int* __restrict__ counts, double* __restrict__ scal, int* __restrict__ dirty) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   unsigned consumed[2] = {0u, 0u};   // nc <= 64
   int na = 0, nz = 0;
@@ -121,6 +121,7 @@ __global__ void select_kernel(int64_t* __restrict__ J, double* __restrict__ tau_
           consumed[r >> 5] |= 1u << (r & 31);
           admit[2 * na] = i;
           admit[2 * na + 1] = r;
+          dirty[i] = 1;
           ++na;
           filled = true;
           break;
@@ -191,49 +192,85 @@ __global__ void hutch_final_kernel(const double* __restrict__ scal, int ell3, co
   out[7] = scal[SC_KAPPA];
 }
 
-// Partial basis Gram over this shard's rows: Gp(i, j) = sum_rows C(r, i) C(r, j) (upper tiles
-// mirrored).  grid: (row chunks, tile pairs); tile 32 x 32; fp64 accumulation.
-template <typename T>
-__global__ void __launch_bounds__(256) basis_gram_kernel(const T* __restrict__ C, int64_t m_loc, int t,
-                                                         int64_t rows_per_chunk, double* __restrict__ part) {
-  __shared__ double Ai[32][33];
-  __shared__ double Aj[32][33];
-  const int ntile = (t + 31) / 32;
-  // decode upper-triangular tile pair (ti <= tj) from blockIdx.y
-  int p = blockIdx.y, ti = 0;
-  while (p >= ntile - ti) { p -= ntile - ti; ++ti; }
-  const int tj = ti + p;
+// Slots admitted since the last estimate (dirty flags set by select_kernel), compacted in
+// slot order; flags cleared.  counts[2] = number of dirty slots.
+__global__ void dirty_compact_kernel(int* __restrict__ dirty, int t, int* __restrict__ list, int* __restrict__ counts) {
+  if (threadIdx.x != 0) return;
+  int c = 0;
+  for (int i = 0; i < t; ++i)
+    if (dirty[i]) { list[c++] = i; dirty[i] = 0; }
+  counts[2] = c;
+}
+
+// Incremental exact basis Gram (A9): Dpart[chunk](q, j) = sum_{rows in chunk} C(r, d_q) C(r, j)
+// for the dirty slots d_q.  Each CTA streams its row chunk of the basis once per
+// group of DQ dirty slots (one group in steady state).  Rows staged 16 at a time in smem.
+template <typename T, int JC, int DQ>
+__global__ void __launch_bounds__(256) basis_gram_dirty_kernel(const T* __restrict__ C, int64_t m_loc, int t,
+                                                               int64_t rows_per_chunk, const int* __restrict__ list,
+                                                               const int* __restrict__ counts,
+                                                               double* __restrict__ part) {
+  extern __shared__ double tile[];   // [16][t]
+  const int nd = counts[2];
+  if (nd == 0) return;
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * rows_per_chunk;
   const int64_t r1 = min(m_loc, r0 + rows_per_chunk);
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int64_t rb = r0; rb < r1; rb += 32) {
-    for (int e = threadIdx.x; e < 32 * 32; e += 256) {
-      const int rr = e & 31, cc = e >> 5;
-      const int64_t r = rb + rr;
-      const int ci = ti * 32 + cc, cj = tj * 32 + cc;
-      Ai[rr][cc] = (r < r1 && ci < t) ? static_cast<double>(C[static_cast<int64_t>(ci) * m_loc + r]) : 0.0;
-      Aj[rr][cc] = (r < r1 && cj < t) ? static_cast<double>(C[static_cast<int64_t>(cj) * m_loc + r]) : 0.0;
-    }
-    __syncthreads();
-#pragma unroll 8
-    for (int rr = 0; rr < 32; ++rr) {
-      const double a = Ai[rr][tx];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc[q] = fma(a, Aj[rr][ty + 8 * q], acc[q]);
-    }
-    __syncthreads();
-  }
   double* out = part + static_cast<int64_t>(blockIdx.x) * t * t;
-  const int i = ti * 32 + tx;
+  for (int q0 = 0; q0 < nd; q0 += DQ) {
+    int dq[DQ];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int j = tj * 32 + ty + 8 * q;
-    if (i < t && j < t) {
-      out[i + static_cast<int64_t>(j) * t] = acc[q];
-      out[j + static_cast<int64_t>(i) * t] = acc[q];
+    for (int q = 0; q < DQ; ++q) dq[q] = (q0 + q < nd) ? list[q0 + q] : 0;
+    double acc[JC][DQ];
+#pragma unroll
+    for (int c = 0; c < JC; ++c)
+#pragma unroll
+      for (int q = 0; q < DQ; ++q) acc[c][q] = 0.0;
+    for (int64_t rb = r0; rb < r1; rb += 16) {
+      __syncthreads();
+      for (int e = threadIdx.x; e < 16 * t; e += 256) {
+        const int rr = e & 15, col = e >> 4;
+        const int64_t r = rb + rr;
+        tile[rr * t + col] = r < r1 ? static_cast<double>(C[static_cast<int64_t>(col) * m_loc + r]) : 0.0;
+      }
+      __syncthreads();
+#pragma unroll 4
+      for (int rr = 0; rr < 16; ++rr) {
+        const double* row = tile + rr * t;
+        double dv[DQ];
+#pragma unroll
+        for (int q = 0; q < DQ; ++q) dv[q] = row[dq[q]];
+#pragma unroll
+        for (int c = 0; c < JC; ++c) {
+          const int j = threadIdx.x + 256 * c;
+          const double xj = j < t ? row[j] : 0.0;
+#pragma unroll
+          for (int q = 0; q < DQ; ++q) acc[c][q] = fma(dv[q], xj, acc[c][q]);
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < JC; ++c) {
+      const int j = threadIdx.x + 256 * c;
+      if (j < t) {
+#pragma unroll
+        for (int q = 0; q < DQ; ++q)
+          if (q0 + q < nd) out[(q0 + q) + static_cast<int64_t>(j) * t] = acc[c][q];
+      }
     }
   }
+}
+
+// G(d_q, j) = G(j, d_q) = D(q, j) for the dirty slots (after the cross-shard reduction).
+__global__ void gram_scatter_kernel(const double* __restrict__ D, const int* __restrict__ list,
+                                    const int* __restrict__ counts, int t, double* __restrict__ G) {
+  const int nd = counts[2];
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<int64_t>(nd) * t) return;
+  const int q = static_cast<int>(idx % nd), j = static_cast<int>(idx / nd);
+  const int d = list[q];
+  const double v = D[q + static_cast<int64_t>(j) * t];
+  G[d + static_cast<int64_t>(j) * t] = v;
+  G[j + static_cast<int64_t>(d) * t] = v;
 }
 
 __global__ void sum_chunks_kernel(const double* __restrict__ part, int nchunks, int64_t n, double* __restrict__ out) {

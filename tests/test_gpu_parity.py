@@ -69,14 +69,19 @@ def _lam_exact(A, k):
 
 # ----------------------------------------------------------------------------- sketch (K1)
 
-@pytest.mark.parametrize("m,nc,ell,dtype", [(4096, 16, 48, np.float64), (5000, 7, 24, np.float64),
-                                            (12345, 33, 96, np.float64), (777, 1, 8, np.float64),
-                                            (5120, 64, 256, np.float32), (70001, 32, 512, np.float64),
-                                            (3001, 64, 1024, np.float32)])
-def test_sketch_parity(oid, m, nc, ell, dtype):
+SKETCH_CASES = [(4096, 16, 48, np.float64), (5000, 7, 24, np.float64), (12346, 33, 96, np.float64),
+                (777, 1, 8, np.float64), (5120, 64, 256, np.float32), (70001, 32, 512, np.float64),
+                (3001, 64, 1024, np.float32), (100000, 64, 512, np.float64), (20000, 20, 300, np.float32)]
+
+
+@pytest.mark.parametrize("k1_mode", [1, 0])
+@pytest.mark.parametrize("m,nc,ell,dtype", SKETCH_CASES)
+def test_sketch_parity(oid, m, nc, ell, dtype, k1_mode):
     rng = np.random.default_rng(m + nc)
     X = rng.standard_normal((m, nc)).astype(dtype) * rng.uniform(0.1, 10, nc).astype(dtype)
-    eng, o = _pair(oid, m, min(8, ell), ell, 64, 256, 0.0, seed=12345, dtype="f64" if dtype == np.float64 else "f32")
+    X[rng.integers(0, m, 5), 0] *= 1e5          # late large values force accumulator flushes in the TC kernel
+    eng, o = _pair(oid, m, min(8, ell), ell, 64, 256, 0.0, seed=12345, dtype="f64" if dtype == np.float64 else "f32",
+                   k1_mode=k1_mode)
     eng.ingest_sketch(_dev(X, dtype))
     part = eng.partials(0).cpu().numpy()
     Yg = part[:ell * nc].reshape(nc, ell).T
@@ -86,6 +91,10 @@ def test_sketch_parity(oid, m, nc, ell, dtype):
     scale = np.max(np.abs(Y), axis=0)
     assert np.max(np.abs(Yg - Y) / scale) < 1e-12
     assert np.allclose(ng, nrm, rtol=1e-13)
+    if k1_mode == 0:
+        mode = eng.stats()["k1_mode_used"]
+        aligned = (m % (2 if dtype == np.float64 else 4) == 0)
+        assert mode == (oid.K1_TC_INT8 if aligned else oid.K1_SIMT_F64), mode
 
 
 def test_sketch_shard_additivity(oid):
