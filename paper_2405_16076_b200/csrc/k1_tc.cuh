@@ -1,22 +1,24 @@
 // K1, tensor-core variant for sm_100a: Y_part = Z(:, slab) * X_blk and n_j = ||x_j||^2 in one
-// read of X (Alg 3 steps 10 and 13), exactly.
+// read of X (Alg 3 steps 10 and 13), exact to fp64 rounding.
 //
 // Why exact: the sketch entries are Gauss-256 integers q in [-127, 127] (reading R2), so
-// Z = s * Q with Q int8.  Each snapshot value x is cut into S two's-complement 8-bit digits of a
-// per-column fixed-point integer x_int = round(x * 2^F_j) (S = 8 digit planes, 64-bit fixed point),
-// and Q * X_digit_s runs on the 5th-generation tensor cores as tcgen05.mma kind::i8 with exact
-// int32 accumulation in TMEM.  Y = s * sum_s 2^(8 s - F_j) * D_s is assembled in fp64.
+// Z = s * Q with Q int8.  Each snapshot value x is cut into S = 7 two's-complement 8-bit digit
+// planes of a per-column fixed-point integer x_int = round(x * 2^F_j) (56-bit fixed point; the
+// column exponent F_j leaves kHeadroom bits above the first tile's maximum), and Q * X_digit
+// runs on the 5th-generation tensor cores as tcgen05.mma kind::i8 with exact int32 accumulation
+// in TMEM.  Y = s * sum_p 2^(8p - F_j) * D_p is assembled in fp64.
 //
-// CTA organisation (one CTA per SM, 16 warps, persistent over one work unit = row slab x
-// slice of 128*T_M sketch rows):
-//   warp 0      TMA producer: cp.async.bulk.tensor 2D boxes of X (64 rows x b) into a ring
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2-3   digit slicer: X stage -> per-column exponent check -> int8 digit planes (B op.)
-//   warps 4-7   epilogue: tcgen05.ld of the int32 accumulators, fp64 assembly, partial out
-//   warps 8-15  sketch generator: Philox4x32-10 -> Gauss-256 bytes -> A operand in smem
-// Per-column exponents start from the first tile of the unit plus 16 bits of headroom; if a
-// later tile exceeds them the accumulators are flushed to fp64 (exactly) and accumulation
-// restarts with a larger exponent ("accumulation epochs"), so X is still read once.
+// CTA organisation (one CTA per SM, 14 warps; one work unit = row slab x 128*TM sketch rows):
+//   warp 0        TMA producer: cp.async.bulk.tensor 2D boxes (128 B x BPAD, 128B swizzle) of X
+//   warp 1        TMEM allocator + single-thread tcgen05.mma issuer (A from TMEM, B from smem)
+//   warps 2-5     digit slicer: X stage -> per-column exponent check -> int8 digit planes (B op.);
+//                 also the epilogue at accumulation-epoch ends (tcgen05.ld of the int32
+//                 accumulators, fp64 assembly, partial out)
+//   warps 6-13    sketch generator: Philox4x32-10 -> Gauss-256 bytes -> tcgen05.st into TMEM (A op.)
+// Per-column exponents start from the first tile of the unit plus kHeadroom bits; if a later
+// tile exceeds them, or 1024 tiles have accumulated (int32 overflow bound: 65536 rows x 255 x
+// 127 < 2^31), the accumulators are flushed to fp64 (exactly) and accumulation restarts
+// ("accumulation epochs"), so X is still read once.
 #pragma once
 #include <cstddef>
 #include <cstdint>
@@ -45,23 +47,27 @@ __constant__ int8_t c_qtab_i8[256];
 
 namespace k1tc {
 
-constexpr int kThreads = 512;
+constexpr int kWarps = 14;
+constexpr int kThreads = 32 * kWarps;
 constexpr int kKTile = 64;          // data rows per pipeline stage
-constexpr int kNumStages = 3;
-constexpr int kHeadroom = 16;       // exponent headroom bits
+constexpr int kS = 7;               // digit planes (56-bit fixed point)
+constexpr int kTop = 55;            // |x_int| < 2^55
+constexpr int kHeadroom = 8;        // exponent headroom bits over the first tile
 constexpr int kEmin = -900;         // exponents are clamped here (data below 2^-900 lose bits)
 constexpr int kNone = -100000;      // "no nonzero seen yet" exponent
+constexpr int kMaxEpochTiles = 1024;
+constexpr int kMaxStages = 4;
+constexpr int kSlicer0 = 2, kGen0 = 6;   // first warp of each role
+constexpr int kQtabBytes = 256 * 32 * 4;
 
 struct Geom {
   int bpad;      // padded block width (16, 32, 64)
-  int S;         // digit planes (8 fp64, 6 fp32)
   int TM;        // M tiles (of 128 sketch rows) per CTA
   int rows;      // 128 * TM
-  int ntot;      // bpad * S accumulator columns per M tile
-  int tmem_cols; // allocation (power of two)
-  int a_bytes, b_bytes, x_bytes;   // per stage
+  int ntot;      // bpad * kS accumulator columns per M tile
+  int x_bytes, b_bytes;   // per stage
+  int nst;       // pipeline stages of X / B
   int smem;      // dynamic smem bytes
-  int nst;       // pipeline stages (2 or 3)
   int nhalves;   // sketch-row slices
   int nslabs;
   int64_t rows_per_slab;
@@ -70,18 +76,15 @@ struct Geom {
 inline Geom make_geom(int ell, int ncols, int64_t m_loc, bool f64, int num_sms) {
   Geom g{};
   g.bpad = ncols <= 16 ? 16 : (ncols <= 32 ? 32 : 64);
-  g.S = 8;   // 64-bit fixed point for both fp64 and fp32 data
-  g.ntot = g.bpad * g.S;
-  g.TM = (2 * g.ntot <= 512) ? 2 : 1;
+  g.ntot = g.bpad * kS;
+  // TMEM: TM accumulators of ntot columns + 2 A stages of TM x 16 columns <= 512
+  g.TM = (ell > 128 && 2 * g.ntot + 64 <= 512) ? 2 : 1;
   g.rows = 128 * g.TM;
-  const int need = g.TM * g.ntot;
-  g.tmem_cols = need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
-  g.a_bytes = g.rows * kKTile;
-  g.b_bytes = g.ntot * kKTile;
   g.x_bytes = kKTile * g.bpad * (f64 ? 8 : 4);
-  g.nst = kNumStages;
-  while (g.nst > 2 && g.nst * (g.a_bytes + g.b_bytes + g.x_bytes) + 256 * 32 * 4 + 4096 > 220 * 1024) --g.nst;
-  g.smem = g.nst * (g.a_bytes + g.b_bytes + g.x_bytes) + 256 * 32 * 4 + 4096;
+  g.b_bytes = g.ntot * kKTile;
+  g.nst = kMaxStages;
+  while (g.nst > 2 && g.nst * (g.x_bytes + g.b_bytes) + kQtabBytes + 1024 > 225 * 1024) --g.nst;
+  g.smem = g.nst * (g.x_bytes + g.b_bytes) + kQtabBytes + 1024;
   g.nhalves = (ell + g.rows - 1) / g.rows;
   g.nslabs = std::max(1, num_sms / g.nhalves);
   int64_t per = (m_loc + g.nslabs - 1) / g.nslabs;
@@ -116,6 +119,19 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+// named barrier with an OR reduction of one predicate over the participating threads
+__device__ __forceinline__ int named_bar_or(int id, int n, int v) {
+  int out;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.s32 p, %1, 0;\n\t"
+      "bar.red.or.pred q, %2, %3, p;\n\t"
+      "selp.s32 %0, 1, 0, q;\n\t}"
+      : "=r"(out)
+      : "r"(v), "r"(id), "r"(n)
+      : "memory");
+  return out;
+}
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
   asm volatile(
@@ -147,12 +163,13 @@ __device__ __forceinline__ uint32_t idesc_i8(int n, bool b_signed) {
   return d;
 }
 
-__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+// D[tmem] (+)= A[tmem] * B[smem]
+__device__ __forceinline__ void mma_i8_ta(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc)
       : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -160,15 +177,27 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
-#define OID_TMEM_LD32(taddr, r)                                                                                   \
+#define OID_TMEM_LD16(taddr, r)                                                                                   \
   asm volatile(                                                                                                   \
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, " \
-      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"              \
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, " \
+      "%15}, [%16];"                                                                                              \
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),          \
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),     \
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),   \
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])    \
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])      \
       : "r"(taddr))
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   uint32_t d;
@@ -176,58 +205,122 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   return d;
 }
 
-// exponent e with |v| < 2^e for finite v > 0 (frexp exponent); kNone for v == 0
-__device__ __forceinline__ int exp_bound(double v) {
-  if (!(v > 0.0)) return kNone;
-  const long long bits = __double_as_longlong(v);
-  int e = static_cast<int>((bits >> 52) & 0x7ff);
-  if (e == 0) return -1021;    // subnormal
-  if (e == 0x7ff) return 1024; // inf/nan: force a (harmless) raise; the norm flags it
-  return e - 1022;
+// Value bits of one element: x = (-1)^neg * m * 2^e2 (m < 2^53), plus the frexp-style exponent
+// key (biased exponent field, 0 for zero).
+template <typename T> struct Bits;
+template <> struct Bits<double> {
+  static constexpr int kPer16 = 8;   // 16-byte chunks per 16 rows
+  __device__ static __forceinline__ uint32_t key(uint32_t hi) { return hi & 0x7FFFFFFFu; }
+  // exponent bound e (|x| < 2^e) from the max key of a group; kNone if all zero
+  __device__ static __forceinline__ int ebound(uint32_t k) {
+    const int E = static_cast<int>(k >> 20);
+    return E ? E - 1022 : (k ? -1021 : kNone);
+  }
+};
+template <> struct Bits<float> {
+  static constexpr int kPer16 = 4;
+  __device__ static __forceinline__ uint32_t key(uint32_t b) { return b & 0x7FFFFFFFu; }
+  __device__ static __forceinline__ int ebound(uint32_t k) {
+    const int E = static_cast<int>(k >> 23);
+    return E ? E - 126 : (k ? -125 : kNone);
+  }
+};
+
+// x_int = round_half_away(x * 2^F) as a 64-bit two's-complement integer, for |x| < 2^(55 - F).
+__device__ __forceinline__ uint64_t fixpt64(uint32_t lo, uint32_t hi, int F) {
+  const int E = static_cast<int>((hi >> 20) & 0x7FF);
+  const uint64_t m = (static_cast<uint64_t>((hi & 0xFFFFFu) | (E ? 0x100000u : 0u)) << 32) | lo;
+  const int sh = max(E, 1) - 1075 + F;         // x * 2^F = m * 2^sh
+  uint64_t u;
+  if (sh >= 0) u = m << min(sh, 63);
+  else if (sh > -64) u = (m + (1ull << (-sh - 1))) >> (-sh);
+  else u = 0;
+  return (hi & 0x80000000u) ? (0ull - u) : u;
+}
+__device__ __forceinline__ uint64_t fixpt32(uint32_t b, int F) {
+  const int E = static_cast<int>((b >> 23) & 0xFF);
+  const uint64_t m = static_cast<uint64_t>((b & 0x7FFFFFu) | (E ? 0x800000u : 0u));
+  const int sh = max(E, 1) - 150 + F;
+  uint64_t u;
+  if (sh >= 0) u = m << min(sh, 63);
+  else if (sh > -64) u = (m + (1ull << (-sh - 1))) >> (-sh);
+  else u = 0;
+  return (b & 0x80000000u) ? (0ull - u) : u;
 }
 
 struct Shared {
-  uint64_t x_full[kNumStages], x_empty[kNumStages];
-  uint64_t a_full[kNumStages], b_full[kNumStages], ab_empty[kNumStages];
+  uint64_t x_full[kMaxStages], x_empty[kMaxStages];
+  uint64_t b_full[kMaxStages], b_empty[kMaxStages];
+  uint64_t a_full[2], a_empty[2];
   uint64_t d_full, d_empty;
   uint32_t tmem_base;
-  int bflags[kNumStages];
-  int flush_final[2];
+  int bflags[kMaxStages];
   int ecur[64];
   int ehist[2][64];
-  double colmax[128];
-  double nrm[64][2];
+  int emax[4][64];
+  double nrm[128];
 };
 
-template <typename T>
+// Load the 16 values (rows 16 c16 .. +15) of column j from a 128B-swizzled X stage as raw bits.
+template <typename T, int BPAD>
+__device__ __forceinline__ void load_unit(const uint8_t* xs, int j, int c16, uint32_t (&w)[2 * Bits<T>::kPer16 * 2]) {
+  if constexpr (sizeof(T) == 8) {
+    const uint8_t* base = xs + (c16 * BPAD + j) * 128;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint4 v = *reinterpret_cast<const uint4*>(base + ((q ^ (j & 7)) << 4));
+      w[4 * q + 0] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+    }
+  } else {
+    const uint8_t* base = xs + ((c16 >> 1) * BPAD + j) * 128;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int qq = (c16 & 1) * 4 + q;
+      const uint4 v = *reinterpret_cast<const uint4*>(base + ((qq ^ (j & 7)) << 4));
+      w[4 * q + 0] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+    }
+  }
+}
+
+template <typename T, int BPAD, int TM>
 __global__ void __launch_bounds__(kThreads, 1)
 k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_begin, int64_t m_loc, int ell,
              uint32_t key0, uint32_t key1, Geom g, double* __restrict__ part, double* __restrict__ npart) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  extern __shared__ uint8_t smem_raw[];
   __shared__ Shared sh;
   constexpr bool kF64 = sizeof(T) == 8;
-  constexpr int S = 8;
+  constexpr int NTOT = BPAD * kS;
+  constexpr int ROWS = 128 * TM;
+  constexpr int ACOL0 = TM * NTOT;                 // first TMEM column of the A stages
+  constexpr int BOX_ROWS = 128 / sizeof(T);
+  constexpr int NBOX = kKTile / BOX_ROWS;
+  constexpr int NUNITS = 4 * BPAD;                 // (column, 16-row chunk) units per tile
+  constexpr int U = (NUNITS + 127) / 128;          // units per slicer thread
+  constexpr int NW = kF64 ? 32 : 16;               // 32-bit words per unit
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int unit = blockIdx.x;
   const int slab = unit / g.nhalves, half = unit % g.nhalves;
   const int64_t r0 = static_cast<int64_t>(slab) * g.rows_per_slab;
   const int64_t r1 = min(m_loc, r0 + g.rows_per_slab);
   const int ntiles = static_cast<int>((r1 - r0 + kKTile - 1) / kKTile);
-  const int bpad = g.bpad;
   const int NS = g.nst;
 
-  uint8_t* abuf = smem_raw;
-  uint8_t* bbuf = abuf + NS * g.a_bytes;
-  uint8_t* xbuf = bbuf + NS * g.b_bytes;
-  uint32_t* qtab = reinterpret_cast<uint32_t*>(xbuf + NS * g.x_bytes);   // [256][32]
+  // dynamic smem: [X stages (1024-aligned, 128B-swizzled)] [B stages] [Gauss-256 table x 32 lanes]
+  uint8_t* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint8_t* xbuf = base;
+  uint8_t* bbuf = xbuf + NS * g.x_bytes;
+  uint32_t* qtab = reinterpret_cast<uint32_t*>(bbuf + NS * g.b_bytes);   // [256][32]
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&sh.x_full[s], 1);
-      mbar_init(&sh.x_empty[s], 2);
-      mbar_init(&sh.a_full[s], 8);
+      mbar_init(&sh.x_empty[s], 4);
       mbar_init(&sh.b_full[s], 1);
-      mbar_init(&sh.ab_empty[s], 1);
+      mbar_init(&sh.b_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&sh.a_full[s], 8);
+      mbar_init(&sh.a_empty[s], 1);
     }
     mbar_init(&sh.d_full, 2);
     mbar_init(&sh.d_empty, 4);
@@ -236,7 +329,7 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
   for (int i = threadIdx.x; i < 256 * 32; i += kThreads) qtab[i] = static_cast<uint32_t>(c_qtab_i8[i >> 5]) & 0xFFu;
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sh.tmem_base)),
-                 "r"(g.tmem_cols));
+                 "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -251,24 +344,27 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
         const int s = t % NS;
         if (t >= NS) mbar_wait(&sh.x_empty[s], ((t / NS) - 1) & 1);
         mbar_arrive_expect_tx(&sh.x_full[s], g.x_bytes);
-        tma_load_2d(xbuf + s * g.x_bytes, &tmap, &sh.x_full[s], static_cast<int>(r0 + int64_t(t) * kKTile), 0);
+        uint8_t* dst = xbuf + s * g.x_bytes;
+#pragma unroll
+        for (int bx = 0; bx < NBOX; ++bx)
+          tma_load_2d(dst + bx * BPAD * 128, &tmap, &sh.x_full[s], static_cast<int>(r0 + int64_t(t) * kKTile + bx * BOX_ROWS),
+                      0);
       }
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
     if (lane == 0) {
-      const int chA = g.rows / 8 * 128;      // bytes per 16-byte K chunk of the A stage
-      const int chB = g.ntot / 8 * 128;
+      constexpr int chB = NTOT / 8 * 128;      // bytes per 16-byte K chunk of the B stage
+      constexpr int NU = (kS - 1) * BPAD;      // unsigned digit planes 0 .. S-2
+      constexpr int NUC = NU > 256 ? NU / 2 : NU;
       int q = 0;
       bool first = true;
       for (int t = 0; t < ntiles; ++t) {
-        const int s = t % NS;
-        const uint32_t ph = (t / NS) & 1;
-        mbar_wait(&sh.a_full[s], ph);
-        mbar_wait(&sh.b_full[s], ph);
+        const int s = t % NS, sa = t & 1;
+        mbar_wait(&sh.a_full[sa], (t >> 1) & 1);
+        mbar_wait(&sh.b_full[s], (t / NS) & 1);
         tc_fence_after();
         if (sh.bflags[s] && t > 0) {           // close accumulation epoch q: flush D to fp64
-          sh.flush_final[q & 1] = 0;
           mma_commit(&sh.d_full);
           mbar_arrive(&sh.d_full);
           mbar_wait(&sh.d_empty, q & 1);
@@ -276,97 +372,157 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
           ++q;
           first = true;
         }
-        const uint32_t abase = smem_u32(abuf + s * g.a_bytes);
         const uint32_t bbase = smem_u32(bbuf + s * g.b_bytes);
 #pragma unroll
         for (int ks = 0; ks < kKTile / 32; ++ks) {
-          for (int tm = 0; tm < g.TM; ++tm) {
-            const uint64_t ad = umma_desc(abase + 2 * ks * chA + tm * 16 * 128, chA, 128);
+#pragma unroll
+          for (int tm = 0; tm < TM; ++tm) {
+            const uint32_t at = tmem + ACOL0 + (sa * TM + tm) * 16 + ks * 8;
             const uint32_t acc = (first && ks == 0) ? 0u : 1u;
-            const uint32_t dcol = tmem + tm * g.ntot;
-            // unsigned digit planes 0 .. S-2 (columns [0, (S-1) bpad)), chunks of <= 256
-            const int nu = (S - 1) * bpad;
-            for (int n0 = 0; n0 < nu; n0 += 256) {
-              const int nn = min(256, nu - n0);
+            const uint32_t dcol = tmem + tm * NTOT;
+#pragma unroll
+            for (int n0 = 0; n0 < NU; n0 += NUC) {
               const uint64_t bd = umma_desc(bbase + 2 * ks * chB + (n0 / 8) * 128, chB, 128);
-              mma_i8(dcol + n0, ad, bd, idesc_i8(nn, false), acc);
+              mma_i8_ta(dcol + n0, at, bd, idesc_i8(NUC, false), acc);
             }
-            // signed top plane
-            const uint64_t bd = umma_desc(bbase + 2 * ks * chB + (nu / 8) * 128, chB, 128);
-            mma_i8(dcol + nu, ad, bd, idesc_i8(bpad, true), acc);
+            const uint64_t bd = umma_desc(bbase + 2 * ks * chB + (NU / 8) * 128, chB, 128);
+            mma_i8_ta(dcol + NU, at, bd, idesc_i8(BPAD, true), acc);
           }
         }
         first = false;
-        mma_commit(&sh.ab_empty[s]);
+        mma_commit(&sh.a_empty[sa]);
+        mma_commit(&sh.b_empty[s]);
       }
-      sh.flush_final[q & 1] = 1;
       mma_commit(&sh.d_full);
       mbar_arrive(&sh.d_full);
     }
-  } else if (warp < 4) {
-    // ---------------------------------------------------------------- digit slicer (64 threads)
-    const int st = threadIdx.x - 64;                 // 0..63
-    const int per = 64 / bpad;                       // threads per column
-    const int j = st % bpad;                         // this thread's column
-    const int base = 62;                             // |x_int| < 2^62 for |x| < 2^E
-    const int chB = g.ntot / 8 * 128;
+  } else if (warp < kGen0) {
+    // ---------------------------------------------------------------- digit slicer (128 threads)
+    const int st = threadIdx.x - 32 * kSlicer0;     // 0..127
+    const int j = st % BPAD;                         // this thread's column (all its units)
+    constexpr int chB = NTOT / 8 * 128;
+    // epilogue of accumulation epoch qe: D (int32, TMEM) -> fp64 partial sums
+    const int quarter = warp & 3;                    // TMEM lane quarter this warp may access
+    auto epilogue = [&](int qe) {
+      mbar_wait(&sh.d_full, qe & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int tm = 0; tm < TM; ++tm) {
+        const int rl = tm * 128 + 32 * quarter + lane;
+        const int r = half * ROWS + rl;
+#pragma unroll 1
+        for (int jb = 0; jb < BPAD; jb += 16) {
+          double acc[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) acc[k] = 0.0;
+#pragma unroll 1
+          for (int p = kS - 1; p >= 0; --p) {
+            uint32_t v[16];
+            const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * quarter) << 16) + tm * NTOT + p * BPAD + jb;
+            OID_TMEM_LD16(taddr, v);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            const double wgt = __longlong_as_double(static_cast<long long>(8 * p + 1023) << 52);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) acc[k] = fma(static_cast<double>(static_cast<int>(v[k])), wgt, acc[k]);
+          }
+          if (r < ell) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              const int jj = jb + k;
+              if (jj >= ncols) continue;
+              const int e = sh.ehist[qe & 1][jj];
+              const double val =
+                  (e == kNone) ? 0.0 : acc[k] * __longlong_as_double(static_cast<long long>(e - kTop + 1023) << 52);
+              double* dst = part + (static_cast<int64_t>(unit) * BPAD + jj) * ROWS + rl;
+              *dst = (qe == 0) ? val : *dst + val;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.d_empty);
+    };
     double nacc = 0.0;
-    int q = 0;
+    int q = 0, tacc = 0;
     for (int t = 0; t < ntiles; ++t) {
       const int s = t % NS;
       const uint32_t ph = (t / NS) & 1;
       mbar_wait(&sh.x_full[s], ph);
-      const T* xs = reinterpret_cast<const T*>(xbuf + s * g.x_bytes);   // [col][64 rows]
-      // pass 1: this thread's part of the column maximum
-      double m = 0.0;
-      for (int c = st / bpad; c < kKTile / 16; c += per) {
-        const T* src = xs + j * kKTile + c * 16;
+      const uint8_t* xs = xbuf + s * g.x_bytes;
+      uint32_t w[U][NW];
+      // phase 1: load this thread's units; exponent key maxima
 #pragma unroll
-        for (int r = 0; r < 16; ++r) m = fmax(m, fabs(static_cast<double>(src[r])));
+      for (int k = 0; k < U; ++k) {
+        const int u = st + 128 * k;
+        if (u < NUNITS) {
+          load_unit<T, BPAD>(xs, j, u / BPAD, w[k]);
+          uint32_t km = 0;
+          if constexpr (kF64) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) km = max(km, Bits<double>::key(w[k][2 * e + 1]));
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) km = max(km, Bits<float>::key(w[k][e]));
+          }
+          sh.emax[u / BPAD][j] = Bits<T>::ebound(km);
+        }
       }
-      sh.colmax[st] = m;
-      named_bar(1, 64);
-      if (st < bpad) {
-        double mm = 0.0;
-        for (int k = 0; k < per; ++k) mm = fmax(mm, sh.colmax[st + k * bpad]);
-        const int eb = exp_bound(mm);
-        int raise = 0;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.x_empty[s]);     // values are in registers
+      named_bar(1, 128);
+      int raise = 0;
+      if (st < BPAD) {
+        int eb = kNone;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) eb = max(eb, sh.emax[c][st]);
         if (t == 0) {
           sh.ecur[st] = eb == kNone ? kNone : max(kEmin, eb + kHeadroom);
         } else if (eb != kNone && (sh.ecur[st] == kNone || eb > sh.ecur[st])) {
           sh.ecur[st] = max(kEmin, eb + kHeadroom);
           raise = 1;
         }
-        sh.colmax[64 + st] = raise;
       }
-      named_bar(1, 64);
-      int raise_any = 0;
-      for (int k = 0; k < bpad; ++k) raise_any |= (sh.colmax[64 + k] != 0.0);
-      const bool newacc = (t == 0) || raise_any;
-      if (newacc && t > 0) {
-        ++q;
-        if (q >= 2) mbar_wait(&sh.d_empty, (q - 2) & 1);   // flush q-2 done: ehist[q & 1] is free
+      const int raise_any = named_bar_or(1, 128, raise);
+      const bool newacc = (t == 0) || raise_any || (t - tacc >= kMaxEpochTiles);
+      const bool flush = newacc && t > 0;       // epoch q ends before tile t (epilogue below)
+      if (newacc) {
+        tacc = t;
+        if (t > 0) ++q;
+        if (st < BPAD) sh.ehist[q & 1][st] = sh.ecur[st];
       }
-      if (newacc && st < bpad) sh.ehist[q & 1][st] = sh.ecur[st];
-      if (t >= NS) mbar_wait(&sh.ab_empty[s], ((t / NS) - 1) & 1);
-      // pass 2: exact fixed-point digits of x * 2^F_j -> K-major B operand
+      if (t >= NS) mbar_wait(&sh.b_empty[s], ((t / NS) - 1) & 1);
+      // phase 2: exact fixed-point digits of x * 2^F_j -> K-major B operand
       const int e = sh.ecur[j];
-      const int F = base - e;
-      const double scl = (e == kNone) ? 0.0 : __longlong_as_double(static_cast<long long>(F + 1023) << 52);
+      const int F = kTop - e;
+      const bool zero_col = (e == kNone);
       uint8_t* bst = bbuf + s * g.b_bytes;
-      for (int c = st / bpad; c < kKTile / 16; c += per) {
-        const T* src = xs + j * kKTile + c * 16;
-        uint32_t outw[S][4];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int u = st + 128 * k;
+        if (u >= NUNITS) continue;
+        const int c16 = u / BPAD;
+        uint32_t outw[kS][4];
 #pragma unroll
         for (int w4 = 0; w4 < 4; ++w4) {
           uint32_t lo[4], hi[4];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const double x = static_cast<double>(src[4 * w4 + k]);
+          for (int r = 0; r < 4; ++r) {
+            const int e16 = 4 * w4 + r;
+            uint64_t xi;
+            double x;
+            if constexpr (kF64) {
+              const uint32_t wl = w[k][2 * e16], wh = w[k][2 * e16 + 1];
+              x = __hiloint2double(static_cast<int>(wh), static_cast<int>(wl));
+              xi = zero_col ? 0ull : fixpt64(wl, wh, F);
+            } else {
+              const uint32_t wb = w[k][e16];
+              x = static_cast<double>(__uint_as_float(wb));
+              xi = zero_col ? 0ull : fixpt32(wb, F);
+            }
             nacc = fma(x, x, nacc);
-            const long long xi = __double2ll_rn(x * scl);
-            lo[k] = static_cast<uint32_t>(xi);
-            hi[k] = static_cast<uint32_t>(static_cast<unsigned long long>(xi) >> 32);
+            lo[r] = static_cast<uint32_t>(xi);
+            hi[r] = static_cast<uint32_t>(xi >> 32);
           }
           // 4x4 byte transposes: word w4 of digit plane p = byte p of rows 4w4 .. 4w4+3
           const uint32_t x0 = prmt(lo[0], lo[1], 0x5140), x1 = prmt(lo[0], lo[1], 0x7362);
@@ -379,120 +535,82 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
           const uint32_t v0 = prmt(hi[2], hi[3], 0x5140), v1 = prmt(hi[2], hi[3], 0x7362);
           outw[4][w4] = prmt(u0, v0, 0x5410);
           outw[5][w4] = prmt(u0, v0, 0x7632);
-          if constexpr (S == 8) {
-            outw[6][w4] = prmt(u1, v1, 0x5410);
-            outw[7][w4] = prmt(u1, v1, 0x7632);
-          }
+          outw[6][w4] = prmt(u1, v1, 0x5410);
         }
 #pragma unroll
-        for (int p = 0; p < S; ++p) {
-          const int n = p * bpad + j;
-          uint4* dst = reinterpret_cast<uint4*>(bst + c * chB + (n >> 3) * 128 + (n & 7) * 16);
+        for (int p = 0; p < kS; ++p) {
+          const int n = p * BPAD + j;
+          uint4* dst = reinterpret_cast<uint4*>(bst + c16 * chB + (n >> 3) * 128 + (n & 7) * 16);
           *dst = make_uint4(outw[p][0], outw[p][1], outw[p][2], outw[p][3]);
         }
       }
       fence_proxy_async();
-      named_bar(1, 64);
+      named_bar(1, 128);
       if (st == 0) {
         sh.bflags[s] = newacc ? 1 : 0;
         mbar_arrive(&sh.b_full[s]);
       }
-      if (lane == 0) mbar_arrive(&sh.x_empty[s]);
+      if (flush) epilogue(q - 1);
     }
+    epilogue(q);
     // norms: threads sharing column j combine in fixed order (half 0 units only)
-    sh.nrm[st][0] = nacc;
-    named_bar(1, 64);
-    if (half == 0 && st < bpad && st < ncols) {
+    sh.nrm[st] = nacc;
+    named_bar(1, 128);
+    if (half == 0 && st < BPAD && st < ncols) {
       double sum = 0.0;
-      for (int k = 0; k < per; ++k) sum += sh.nrm[st + k * bpad][0];
-      npart[static_cast<int64_t>(slab) * bpad + st] = sum;
-    }
-  } else if (warp < 8) {
-    // ---------------------------------------------------------------- epilogue (4 warps)
-    const int eq = warp - 4;
-    const int base = 62;
-    int q = 0;
-    for (;;) {
-      mbar_wait(&sh.d_full, q & 1);
-      tc_fence_after();
-      const int fin = sh.flush_final[q & 1];
-      for (int tm = 0; tm < g.TM; ++tm) {
-        const int rl = tm * 128 + 32 * eq + lane;
-        const int r = half * g.rows + rl;
-        for (int jb = 0; jb < bpad; jb += 32) {
-          double acc[32];
-#pragma unroll
-          for (int k = 0; k < 32; ++k) acc[k] = 0.0;
-          for (int p = S - 1; p >= 0; --p) {
-            uint32_t v[32];
-            const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * eq) << 16) + tm * g.ntot + p * bpad + jb;
-            OID_TMEM_LD32(taddr, v);
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            const double w = __longlong_as_double(static_cast<long long>(8 * p + 1023) << 52);
-#pragma unroll
-            for (int k = 0; k < 32; ++k) acc[k] = fma(static_cast<double>(static_cast<int>(v[k])), w, acc[k]);
-          }
-          if (r < ell) {
-#pragma unroll
-            for (int k = 0; k < 32; ++k) {
-              const int jj = jb + k;
-              if (jj >= ncols) continue;
-              const int e = sh.ehist[q & 1][jj];
-              const double val = (e == kNone) ? 0.0
-                                              : acc[k] * __longlong_as_double(static_cast<long long>(e - base + 1023) << 52);
-              double* dst = part + (static_cast<int64_t>(unit) * bpad + jj) * g.rows + rl;
-              *dst = (q == 0) ? val : *dst + val;
-            }
-          }
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sh.d_empty);
-      if (fin) break;
-      ++q;
+      for (int k = 0; k < 128 / BPAD; ++k) sum += sh.nrm[st + k * BPAD];
+      npart[static_cast<int64_t>(slab) * BPAD + st] = sum;
     }
   } else {
     // ---------------------------------------------------------------- sketch generator (8 warps)
-    const int rt = threadIdx.x - 256;
-    const int parts = 256 / g.rows;
-    const int rl = rt % g.rows, pidx = rt / g.rows;
-    const int r = half * g.rows + rl;
-    const int chA = g.rows / 8 * 128;
+    // TM = 2: warp -> (M tile, lane quarter), all 4 K chunks of a tile;
+    // TM = 1: warp -> (K half, lane quarter), 2 K chunks.
+    constexpr int NK = TM == 2 ? 4 : 2;
+    const int gw = warp - kGen0;                     // 0..7
+    const int quarter = warp & 3;
+    const int tm = TM == 2 ? gw / 4 : 0;
+    const int kc0 = TM == 2 ? 0 : (gw / 4) * 2;
+    const int rl = tm * 128 + quarter * 32 + lane;
+    const int r = half * ROWS + rl;
+    const bool live = r < ell;
     const uint32_t* tl = qtab + lane;
     const uint64_t g16_0 = static_cast<uint64_t>((row_begin + r0) >> 4);
+    const uint32_t tbase = tmem + (static_cast<uint32_t>(32 * quarter) << 16) + ACOL0 + tm * 16 + kc0 * 4;
     for (int t = 0; t < ntiles; ++t) {
-      const int s = t % NS;
-      if (t >= NS) mbar_wait(&sh.ab_empty[s], ((t / NS) - 1) & 1);
-      uint8_t* ast = abuf + s * g.a_bytes;
-      for (int c = pidx; c < kKTile / 16; c += parts) {
-        uint4 o = make_uint4(0u, 0u, 0u, 0u);
-        if (r < ell) {
-          const uint32_t grp = static_cast<uint32_t>(g16_0 + static_cast<uint64_t>(t) * (kKTile / 16) + c);
-          const U4 w = philox4x32_10(grp, static_cast<uint32_t>(r), 0u, 0u, key0, key1);
-          const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-          uint32_t pk[4];
+      const int sa = t & 1;
+      if (t >= 2) mbar_wait(&sh.a_empty[sa], ((t >> 1) - 1) & 1);
+      uint32_t pk[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) pk[k] = 0u;
+      if (live) {
+#pragma unroll
+        for (int kc = 0; kc < NK; ++kc) {
+          const uint32_t grp = static_cast<uint32_t>(g16_0 + static_cast<uint64_t>(t) * (kKTile / 16) + kc0 + kc);
+          const U4 wv = philox4x32_10(grp, static_cast<uint32_t>(r), 0u, 0u, key0, key1);
+          const uint32_t ws[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const uint32_t a = ws[k];
             const uint32_t b0 = tl[(a & 0xFFu) << 5], b1 = tl[((a >> 8) & 0xFFu) << 5];
             const uint32_t b2 = tl[((a >> 16) & 0xFFu) << 5], b3 = tl[(a >> 24) << 5];
-            pk[k] = prmt(prmt(b0, b1, 0x0040), prmt(b2, b3, 0x0040), 0x5410);
+            pk[4 * kc + k] = prmt(prmt(b0, b1, 0x0040), prmt(b2, b3, 0x0040), 0x5410);
           }
-          o = make_uint4(pk[0], pk[1], pk[2], pk[3]);
         }
-        *reinterpret_cast<uint4*>(ast + c * chA + (rl >> 3) * 128 + (rl & 7) * 16) = o;
       }
-      fence_proxy_async();
+      const uint32_t ta = tbase + sa * TM * 16;
+      if constexpr (NK == 4) tmem_st16(ta, pk);
+      else tmem_st8(ta, pk);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sh.a_full[s]);
+      if (lane == 0) mbar_arrive(&sh.a_full[sa]);
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(g.tmem_cols));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
 }
 
@@ -563,37 +681,47 @@ inline bool k1tc_call_ok(const K1TcArgs& a) {
   return k1tc_encoder() != nullptr;
 }
 
+template <typename T, int BPAD, int TM>
+inline cudaError_t k1tc_launch_t(const CUtensorMap& map, const K1TcArgs& a, const k1tc::Geom& g, cudaStream_t st,
+                                 double* part, double* npart) {
+  auto fn = k1tc::k1_tc_kernel<T, BPAD, TM>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem);
+  if (e != cudaSuccess) return e;
+  fn<<<g.nslabs * g.nhalves, k1tc::kThreads, g.smem, st>>>(map, a.ncols, a.row_begin, a.row_end - a.row_begin, a.ell,
+                                                           a.key0, a.key1, g, part, npart);
+  return cudaGetLastError();
+}
+
+template <typename T>
+inline cudaError_t k1tc_dispatch(const CUtensorMap& map, const K1TcArgs& a, const k1tc::Geom& g, cudaStream_t st,
+                                 double* part, double* npart) {
+  if (g.bpad == 16) return g.TM == 2 ? k1tc_launch_t<T, 16, 2>(map, a, g, st, part, npart)
+                                     : k1tc_launch_t<T, 16, 1>(map, a, g, st, part, npart);
+  if (g.bpad == 32) return g.TM == 2 ? k1tc_launch_t<T, 32, 2>(map, a, g, st, part, npart)
+                                     : k1tc_launch_t<T, 32, 1>(map, a, g, st, part, npart);
+  return k1tc_launch_t<T, 64, 1>(map, a, g, st, part, npart);
+}
+
 inline cudaError_t k1tc_launch(const K1TcArgs& a, cudaStream_t st, int* nlaunch) {
   *nlaunch = 0;
   const int64_t m_loc = a.row_end - a.row_begin;
   const k1tc::Geom g = k1tc::make_geom(a.ell, a.ncols, m_loc, a.f64, a.num_sms);
   CUtensorMap map;
+  const int es = a.f64 ? 8 : 4;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(m_loc), static_cast<cuuint64_t>(a.ncols)};
-  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.ld) * (a.f64 ? 8 : 4)};
-  const cuuint32_t box[2] = {static_cast<cuuint32_t>(k1tc::kKTile), static_cast<cuuint32_t>(g.bpad)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.ld) * es};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / es), static_cast<cuuint32_t>(g.bpad)};
   const cuuint32_t estr[2] = {1, 1};
   CUresult cr = k1tc_encoder()(&map, a.f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                                const_cast<void*>(a.X), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
   double* part = reinterpret_cast<double*>(a.ws);
   double* npart = part + static_cast<size_t>(kTcMaxUnits) * 64 * 256;
-  const int units = g.nslabs * g.nhalves;
-  cudaError_t e;
-  if (a.f64) {
-    e = cudaFuncSetAttribute(k1tc::k1_tc_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem);
-    if (e != cudaSuccess) return e;
-    k1tc::k1_tc_kernel<double><<<units, k1tc::kThreads, g.smem, st>>>(map, a.ncols, a.row_begin, m_loc, a.ell, a.key0,
-                                                                      a.key1, g, part, npart);
-  } else {
-    e = cudaFuncSetAttribute(k1tc::k1_tc_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem);
-    if (e != cudaSuccess) return e;
-    k1tc::k1_tc_kernel<float><<<units, k1tc::kThreads, g.smem, st>>>(map, a.ncols, a.row_begin, m_loc, a.ell, a.key0,
-                                                                     a.key1, g, part, npart);
-  }
+  cudaError_t e = a.f64 ? k1tc_dispatch<double>(map, a, g, st, part, npart) : k1tc_dispatch<float>(map, a, g, st, part, npart);
   *nlaunch += 1;
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (e != cudaSuccess) return e;
   const int64_t nout = int64_t(a.ell) * a.ncols + a.ncols;
   k1tc::k1_tc_reduce_kernel<<<static_cast<unsigned>((nout + 255) / 256), 256, 0, st>>>(part, npart, g, a.ell, a.ncols,
                                                                                      a.scale, a.out, a.flags);
