@@ -52,8 +52,9 @@ typedef enum { OID_F32 = 0, OID_F64 = 1 } oid_dtype;
 typedef enum {
   OID_K1_AUTO = 0,      /* tensor-core path when available for the shape, else SIMT       */
   OID_K1_SIMT_F64 = 1,  /* CUDA-core DFMA, Omega generated in registers                    */
-  OID_K1_TC_INT8 = 2    /* tcgen05 kind::i8, Omega bytes generated into shared memory,
-                           data split into exact int8 digits (sm_100a)                     */
+  OID_K1_TC_INT8 = 2    /* tcgen05 kind::i8, Omega generated into TMEM (A operand), data
+                           split into exact int8 digit planes in shared memory (sm_100a);
+                           needs row_begin % 32 == 0, 16-byte aligned X and ld            */
 } oid_k1_mode;
 
 /* flag bits (oid_stats.flags, estimate out[6]) */
@@ -160,9 +161,10 @@ oid_status oid_get(oid_ctx ctx, int32_t field, void* host_dst, size_t bytes, voi
 oid_status oid_stats(oid_ctx ctx, oid_stats_t* out);
 oid_status oid_stats_reset(oid_ctx ctx);
 
-/* Host-only: the Gauss-256 sketch-entry table q[0..255] and scale s (reading R2,
-   Omega = s * q[u]); needs no GPU. */
-oid_status oid_sketch_table(int32_t q[256], double* scale);
+/* Host-only: the Gauss-16 sketch-entry table (reading R2): for a 4-bit Philox draw n,
+   Omega = s * (q[n] + 1/2), q[n] integer in [-111, 110]; needs no GPU.
+   Errors: OID_EINVAL on NULL pointers. */
+oid_status oid_sketch_table(int32_t q[16], double* scale);
 
 void oid_destroy(oid_ctx ctx);
 const char* oid_last_error(oid_ctx ctx);   /* ctx == NULL: last oid_init failure (this thread) */

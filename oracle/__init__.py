@@ -4,7 +4,7 @@ TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and the
 ``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import anything
 in this package.  The product path (``paper_2405_16076_b200``) never imports it
 and shares no code with it: the oracle re-implements the Philox stream, the
-Gauss-256 sketch entries, the selection draws and every arithmetic step on its
+Gauss-16 sketch entries, the selection draws and every arithmetic step on its
 own, in plain numpy fp64, following the paper step by step.
 
 Citation tags: ``P:n`` = line n of the paper's LaTeX source (PAPER.md);
@@ -12,7 +12,7 @@ readings R1..R14 are listed in DESIGN.md section 3.
 
 Parity-pin status per function:
   philox4x32_10        pinned (Random123 / cuRAND known-answer vectors)
-  gauss256_table       pinned (symmetry, independent erfc bisection, moments)
+  gauss16 levels       pinned (symmetry, independent erfc bisection, moments)
   sketch / ingest      pinned (identity sketch, slab additivity, JL statistics)
   ridge scores         pinned (exact leverage at lambda=0, closed form at lambda>0,
                        hand case A=I2, Lemma 1 direction)
@@ -24,10 +24,10 @@ Parity-pin status per function:
 """
 
 from .philox import philox4x32_10, uniform24
-from .gauss256 import gauss256_table, gauss256_scale, omega_rows
+from .gauss16 import gauss16_magnitudes, gauss16_levels, gauss16_scale, omega_rows
 from .oid import OracleParams, OracleOID, ridge_scores, hutchpp_estimate, alg4_coefficients
 
 __all__ = [
-    "philox4x32_10", "uniform24", "gauss256_table", "gauss256_scale", "omega_rows",
+    "philox4x32_10", "uniform24", "gauss16_magnitudes", "gauss16_levels", "gauss16_scale", "omega_rows",
     "OracleParams", "OracleOID", "ridge_scores", "hutchpp_estimate", "alg4_coefficients",
 ]

@@ -25,7 +25,7 @@ import math
 import numpy as np
 
 from .philox import uniform24, EVICT
-from .gauss256 import gauss256_scale, omega_rows
+from .gauss16 import gauss16_scale, omega_rows
 
 PINV_RCOND = 1e-12   # reading R9: pseudo-inverse cutoff 1e-12 * max (P:341, P:431 only write "+")
 
@@ -79,9 +79,9 @@ def sketch(params, X, Qcache=None):
         if Qcache is not None:
             Q = Qcache[:, i0:i1]
         else:
-            Q = omega_rows(params.seed, np.arange(params.ell), rb + i0, rb + i1).astype(np.float64)
+            Q = omega_rows(params.seed, np.arange(params.ell), rb + i0, rb + i1)
         acc += Q @ X[i0:i1]
-    return gauss256_scale() * acc
+    return gauss16_scale() * acc
 
 
 def column_norms2(X):
@@ -272,7 +272,7 @@ class OracleOID:
         self._Q = None
         if cache_omega and ell * params.m_loc <= 100_000_000:
             rb = params.row_begin
-            self._Q = omega_rows(params.seed, np.arange(ell), rb, rb + params.m_loc).astype(np.float64)
+            self._Q = omega_rows(params.seed, np.arange(ell), rb, rb + params.m_loc)
 
     def ingest_block(self, X, partial_sketch=None, partial_norms=None):
         """One epoch.  partial_sketch/norms: already all-reduced [Y; n] (multi-shard runs)."""

@@ -91,8 +91,8 @@ def version():
 
 
 def sketch_table():
-    """Host-only: (q[256] int32, scale) of the Gauss-256 sketch entries (reading R2)."""
-    q = (ctypes.c_int32 * 256)()
+    """Host-only: (q[16] int32, scale) of the Gauss-16 sketch entries s * (q[n] + 1/2) (reading R2)."""
+    q = (ctypes.c_int32 * 16)()
     s = ctypes.c_double()
     st = _lib.oid_sketch_table(q, ctypes.byref(s))
     if st != OID_OK:

@@ -12,8 +12,9 @@ struct U4 { uint32_t x, y, z, w; };
 
 __host__ __device__ __forceinline__ void mulhilo32(uint32_t a, uint32_t b, uint32_t& hi, uint32_t& lo) {
 #ifdef __CUDA_ARCH__
-  lo = a * b;
-  hi = __umulhi(a, b);
+  const uint64_t p = static_cast<uint64_t>(a) * b;   // one IMAD.WIDE.U32
+  lo = static_cast<uint32_t>(p);
+  hi = static_cast<uint32_t>(p >> 32);
 #else
   uint64_t p = static_cast<uint64_t>(a) * b;
   lo = static_cast<uint32_t>(p);

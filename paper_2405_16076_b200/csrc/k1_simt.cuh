@@ -1,24 +1,26 @@
 // K1, CUDA-core variant: Y_part = Z(:, slab) * X_blk and n_j = sum_i x_ij^2 in one read of X
 // (Alg 3 steps 10 and 13).  Z entries are generated in registers from Philox
-// (reading R1) through the Gauss-256 table (reading R2); products and sums in fp64 (DFMA).
+// (reading R1) through the Gauss-16 levels (reading R2); products and sums in fp64 (DFMA).
 #pragma once
 #include "common.cuh"
 
 namespace oid {
 
-__constant__ double c_qtab_f64[256];   // q(u) as exact doubles (set at init)
+__constant__ double c_qtab_f64[16];    // L(n) = q(n) + 1/2 as exact doubles (set at init)
 
-// One CTA owns a contiguous range of global 16-row groups and 256*RPT sketch rows
+constexpr int kGrp = 32;               // data rows per Philox block (8 nibbles x 4 words)
+
+// One CTA owns a contiguous range of global 32-row groups and 256*RPT sketch rows
 // (blockIdx.y selects the sketch-row slice).  Rows outside [row_begin, row_end) read as 0.
 template <typename T, int NCB, int RPT>
 __global__ void __launch_bounds__(kThreads, 1)
 k1_simt_kernel(const T* __restrict__ X, int64_t ld, int ncols, int64_t row_begin, int64_t row_end,
                int64_t grp_begin, int64_t grp_end, int64_t grp_per_cta, int ell, uint32_t key0, uint32_t key1,
                double* __restrict__ part, double* __restrict__ npart) {
-  __shared__ double xs[2][16][NCB];
-  __shared__ double qd[256];
+  __shared__ double xs[2][kGrp][NCB];
+  __shared__ double qd[16];
   const int tid = threadIdx.x;
-  for (int i = tid; i < 256; i += kThreads) qd[i] = c_qtab_f64[i];
+  if (tid < 16) qd[tid] = c_qtab_f64[tid];
 
   const int64_t g0 = grp_begin + static_cast<int64_t>(blockIdx.x) * grp_per_cta;
   const int64_t g1 = min(grp_end, g0 + grp_per_cta);
@@ -31,14 +33,14 @@ k1_simt_kernel(const T* __restrict__ X, int64_t ld, int ncols, int64_t row_begin
     for (int j = 0; j < NCB; ++j) acc[k][j] = 0.0;
   double nrm = 0.0;
 
-  constexpr int kLoads = (16 * NCB + kThreads - 1) / kThreads;
+  constexpr int kLoads = (kGrp * NCB + kThreads - 1) / kThreads;
   double pre[kLoads];
   auto fetch = [&](int64_t gq) {
 #pragma unroll
     for (int it = 0; it < kLoads; ++it) {
       const int e = tid + it * kThreads;
-      const int rr = e & 15, j = e >> 4;
-      const int64_t g = gq * 16 + rr;
+      const int rr = e & (kGrp - 1), j = e / kGrp;
+      const int64_t g = gq * kGrp + rr;
       double v = 0.0;
       if (j < ncols && g >= row_begin && g < row_end) v = static_cast<double>(X[(g - row_begin) + j * ld]);
       pre[it] = v;
@@ -48,7 +50,7 @@ k1_simt_kernel(const T* __restrict__ X, int64_t ld, int ncols, int64_t row_begin
 #pragma unroll
     for (int it = 0; it < kLoads; ++it) {
       const int e = tid + it * kThreads;
-      if (e < 16 * NCB) xs[buf][e & 15][e >> 4] = pre[it];
+      if (e < kGrp * NCB) xs[buf][e & (kGrp - 1)][e / kGrp] = pre[it];
     }
   };
 
@@ -60,7 +62,7 @@ k1_simt_kernel(const T* __restrict__ X, int64_t ld, int ncols, int64_t row_begin
     if (gq + 1 < g1) fetch(gq + 1);
     if (blockIdx.y == 0 && tid < NCB) {
 #pragma unroll
-      for (int rr = 0; rr < 16; ++rr) { const double v = xs[buf][rr][tid]; nrm = fma(v, v, nrm); }
+      for (int rr = 0; rr < kGrp; ++rr) { const double v = xs[buf][rr][tid]; nrm = fma(v, v, nrm); }
     }
 #pragma unroll
     for (int k = 0; k < RPT; ++k) {
@@ -69,8 +71,8 @@ k1_simt_kernel(const T* __restrict__ X, int64_t ld, int ncols, int64_t row_begin
         const U4 w = philox4x32_10(static_cast<uint32_t>(gq), static_cast<uint32_t>(r), 0u, 0u, key0, key1);
         const uint32_t words[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-        for (int rr = 0; rr < 16; ++rr) {
-          const double q = qd[(words[rr >> 2] >> (8 * (rr & 3))) & 255u];
+        for (int rr = 0; rr < kGrp; ++rr) {
+          const double q = qd[(words[rr >> 3] >> (4 * (rr & 7))) & 15u];
 #pragma unroll
           for (int j = 0; j < NCB; j += 2) {
             const double2 xv = *reinterpret_cast<const double2*>(&xs[buf][rr][j]);

@@ -1,12 +1,12 @@
 // K1, tensor-core variant for sm_100a: Y_part = Z(:, slab) * X_blk and n_j = ||x_j||^2 in one
 // read of X (Alg 3 steps 10 and 13), exact to fp64 rounding.
 //
-// Why exact: the sketch entries are Gauss-256 integers q in [-127, 127] (reading R2), so
-// Z = s * Q with Q int8.  Each snapshot value x is cut into S = 7 two's-complement 8-bit digit
+// Why exact: the sketch entries are Gauss-16 half-integers L = q + 1/2, q in [-111, 110]
+// (reading R2), so Z = s (Q + 1/2) with Q int8 and Z X = s (Q X + (1/2) 1 colsum(X)).  Each snapshot value x is cut into S = 7 two's-complement 8-bit digit
 // planes of a per-column fixed-point integer x_int = round(x * 2^F_j) (56-bit fixed point; the
 // column exponent F_j leaves kHeadroom bits above the first tile's maximum), and Q * X_digit
 // runs on the 5th-generation tensor cores as tcgen05.mma kind::i8 with exact int32 accumulation
-// in TMEM.  Y = s * sum_p 2^(8p - F_j) * D_p is assembled in fp64.
+// in TMEM.  Y = s * (sum_p 2^(8p - F_j) * D_p + colsum_j / 2) is assembled in fp64.
 //
 // CTA organisation (one CTA per SM, 14 warps; one work unit = row slab x 128*TM sketch rows):
 //   warp 0        TMA producer: cp.async.bulk.tensor 2D boxes (128 B x BPAD, 128B swizzle) of X
@@ -14,7 +14,9 @@
 //   warps 2-5     digit slicer: X stage -> per-column exponent check -> int8 digit planes (B op.);
 //                 also the epilogue at accumulation-epoch ends (tcgen05.ld of the int32
 //                 accumulators, fp64 assembly, partial out)
-//   warps 6-13    sketch generator: Philox4x32-10 -> Gauss-256 bytes -> tcgen05.st into TMEM (A op.)
+//   warps 6-13    sketch generator: Philox4x32-10 -> Gauss-16 nibbles -> int8 q by two PRMT
+//                 table lookups per 4 entries (levels held in 2 registers) -> tcgen05.st into
+//                 TMEM (A operand); 32 entries per Philox call
 // Per-column exponents start from the first tile of the unit plus kHeadroom bits; if a later
 // tile exceeds them, or 1024 tiles have accumulated (int32 overflow bound: 65536 rows x 255 x
 // 127 < 2^31), the accumulators are flushed to fp64 (exactly) and accumulation restarts
@@ -41,9 +43,8 @@ struct K1TcArgs {
   double* out;
   unsigned* flags;
   int num_sms;
+  uint32_t t0, t1;   // Gauss-16 magnitudes m_0..m_3, m_4..m_7 as bytes (reading R2)
 };
-
-__constant__ int8_t c_qtab_i8[256];
 
 namespace k1tc {
 
@@ -58,7 +59,6 @@ constexpr int kNone = -100000;      // "no nonzero seen yet" exponent
 constexpr int kMaxEpochTiles = 1024;
 constexpr int kMaxStages = 4;
 constexpr int kSlicer0 = 2, kGen0 = 6;   // first warp of each role
-constexpr int kQtabBytes = 256 * 32 * 4;
 
 struct Geom {
   int bpad;      // padded block width (16, 32, 64)
@@ -83,8 +83,8 @@ inline Geom make_geom(int ell, int ncols, int64_t m_loc, bool f64, int num_sms) 
   g.x_bytes = kKTile * g.bpad * (f64 ? 8 : 4);
   g.b_bytes = g.ntot * kKTile;
   g.nst = kMaxStages;
-  while (g.nst > 2 && g.nst * (g.x_bytes + g.b_bytes) + kQtabBytes + 1024 > 225 * 1024) --g.nst;
-  g.smem = g.nst * (g.x_bytes + g.b_bytes) + kQtabBytes + 1024;
+  while (g.nst > 2 && g.nst * (g.x_bytes + g.b_bytes) + 1024 + 4096 > 225 * 1024) --g.nst;
+  g.smem = g.nst * (g.x_bytes + g.b_bytes) + 1024;
   g.nhalves = (ell + g.rows - 1) / g.rows;
   g.nslabs = std::max(1, num_sms / g.nhalves);
   int64_t per = (m_loc + g.nslabs - 1) / g.nslabs;
@@ -110,7 +110,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 0x989680;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
@@ -226,26 +226,20 @@ template <> struct Bits<float> {
   }
 };
 
-// x_int = round_half_away(x * 2^F) as a 64-bit two's-complement integer, for |x| < 2^(55 - F).
-__device__ __forceinline__ uint64_t fixpt64(uint32_t lo, uint32_t hi, int F) {
-  const int E = static_cast<int>((hi >> 20) & 0x7FF);
-  const uint64_t m = (static_cast<uint64_t>((hi & 0xFFFFFu) | (E ? 0x100000u : 0u)) << 32) | lo;
-  const int sh = max(E, 1) - 1075 + F;         // x * 2^F = m * 2^sh
-  uint64_t u;
-  if (sh >= 0) u = m << min(sh, 63);
-  else if (sh > -64) u = (m + (1ull << (-sh - 1))) >> (-sh);
-  else u = 0;
-  return (hi & 0x80000000u) ? (0ull - u) : u;
-}
-__device__ __forceinline__ uint64_t fixpt32(uint32_t b, int F) {
-  const int E = static_cast<int>((b >> 23) & 0xFF);
-  const uint64_t m = static_cast<uint64_t>((b & 0x7FFFFFu) | (E ? 0x800000u : 0u));
-  const int sh = max(E, 1) - 150 + F;
-  uint64_t u;
-  if (sh >= 0) u = m << min(sh, 63);
-  else if (sh > -64) u = (m + (1ull << (-sh - 1))) >> (-sh);
-  else u = 0;
-  return (b & 0x80000000u) ? (0ull - u) : u;
+// x_int = round(x * 2^F) as a 64-bit two's-complement integer, for |x * 2^F| < 2^55, on the
+// fp64 pipe: hi = floor(x 2^(F-32)) and lo = x 2^F - hi 2^32 in [0, 2^32) are exact; lo is
+// rounded to nearest by the 2^52 magic add (a carry out of lo goes into hi).
+// p32 = 2^(F-32), p0 = 2^F, both 0 for an all-zero column.
+__device__ __forceinline__ void fixpt(double x, double p32, double p0, uint32_t& lo, uint32_t& hi) {
+  const double M = 6755399441055744.0;             // 1.5 * 2^52
+  const double t1 = __fma_rd(x, p32, M);            // M + floor(x 2^(F-32))
+  const double hd = t1 - M;                         // exact
+  const double v = x * p0;                          // exact (power-of-two scaling)
+  const double l = fma(hd, -4294967296.0, v);       // exact, in [0, 2^32)
+  const double t2 = l + 4503599627370496.0;         // 2^52 + rint(l)
+  const uint32_t t2h = static_cast<uint32_t>(__double2hiint(t2));
+  lo = static_cast<uint32_t>(__double2loint(t2));
+  hi = static_cast<uint32_t>(__double2loint(t1)) + (t2h & 1u);
 }
 
 struct Shared {
@@ -259,6 +253,7 @@ struct Shared {
   int ehist[2][64];
   int emax[4][64];
   double nrm[128];
+  double csum[128];
 };
 
 // Load the 16 values (rows 16 c16 .. +15) of column j from a 128B-swizzled X stage as raw bits.
@@ -285,7 +280,8 @@ __device__ __forceinline__ void load_unit(const uint8_t* xs, int j, int c16, uin
 template <typename T, int BPAD, int TM>
 __global__ void __launch_bounds__(kThreads, 1)
 k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_begin, int64_t m_loc, int ell,
-             uint32_t key0, uint32_t key1, Geom g, double* __restrict__ part, double* __restrict__ npart) {
+             uint32_t key0, uint32_t key1, uint32_t t0, uint32_t t1, Geom g, double* __restrict__ part,
+             double* __restrict__ npart, double* __restrict__ cpart) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ Shared sh;
   constexpr bool kF64 = sizeof(T) == 8;
@@ -305,11 +301,10 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
   const int ntiles = static_cast<int>((r1 - r0 + kKTile - 1) / kKTile);
   const int NS = g.nst;
 
-  // dynamic smem: [X stages (1024-aligned, 128B-swizzled)] [B stages] [Gauss-256 table x 32 lanes]
+  // dynamic smem: [X stages (1024-aligned, 128B-swizzled)] [B stages]
   uint8_t* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t* xbuf = base;
   uint8_t* bbuf = xbuf + NS * g.x_bytes;
-  uint32_t* qtab = reinterpret_cast<uint32_t*>(bbuf + NS * g.b_bytes);   // [256][32]
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -326,7 +321,6 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
     mbar_init(&sh.d_empty, 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int i = threadIdx.x; i < 256 * 32; i += kThreads) qtab[i] = static_cast<uint32_t>(c_qtab_i8[i >> 5]) & 0xFFu;
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sh.tmem_base)),
                  "r"(512));
@@ -443,7 +437,7 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
       __syncwarp();
       if (lane == 0) mbar_arrive(&sh.d_empty);
     };
-    double nacc = 0.0;
+    double nacc = 0.0, cacc = 0.0;
     int q = 0, tacc = 0;
     for (int t = 0; t < ntiles; ++t) {
       const int s = t % NS;
@@ -494,8 +488,10 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
       if (t >= NS) mbar_wait(&sh.b_empty[s], ((t / NS) - 1) & 1);
       // phase 2: exact fixed-point digits of x * 2^F_j -> K-major B operand
       const int e = sh.ecur[j];
-      const int F = kTop - e;
       const bool zero_col = (e == kNone);
+      const int F = zero_col ? 0 : kTop - e;
+      const double p0 = zero_col ? 0.0 : __longlong_as_double(static_cast<long long>(F + 1023) << 52);
+      const double p32 = zero_col ? 0.0 : __longlong_as_double(static_cast<long long>(F - 32 + 1023) << 52);
       uint8_t* bst = bbuf + s * g.b_bytes;
 #pragma unroll
       for (int k = 0; k < U; ++k) {
@@ -509,20 +505,12 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
             const int e16 = 4 * w4 + r;
-            uint64_t xi;
             double x;
-            if constexpr (kF64) {
-              const uint32_t wl = w[k][2 * e16], wh = w[k][2 * e16 + 1];
-              x = __hiloint2double(static_cast<int>(wh), static_cast<int>(wl));
-              xi = zero_col ? 0ull : fixpt64(wl, wh, F);
-            } else {
-              const uint32_t wb = w[k][e16];
-              x = static_cast<double>(__uint_as_float(wb));
-              xi = zero_col ? 0ull : fixpt32(wb, F);
-            }
+            if constexpr (kF64) x = __hiloint2double(static_cast<int>(w[k][2 * e16 + 1]), static_cast<int>(w[k][2 * e16]));
+            else x = static_cast<double>(__uint_as_float(w[k][e16]));
             nacc = fma(x, x, nacc);
-            lo[r] = static_cast<uint32_t>(xi);
-            hi[r] = static_cast<uint32_t>(xi >> 32);
+            cacc += x;
+            fixpt(x, p32, p0, lo[r], hi[r]);
           }
           // 4x4 byte transposes: word w4 of digit plane p = byte p of rows 4w4 .. 4w4+3
           const uint32_t x0 = prmt(lo[0], lo[1], 0x5140), x1 = prmt(lo[0], lo[1], 0x7362);
@@ -553,29 +541,30 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
       if (flush) epilogue(q - 1);
     }
     epilogue(q);
-    // norms: threads sharing column j combine in fixed order (half 0 units only)
+    // norms and column sums: threads sharing column j combine in fixed order (half 0 units only)
     sh.nrm[st] = nacc;
+    sh.csum[st] = cacc;
     named_bar(1, 128);
     if (half == 0 && st < BPAD && st < ncols) {
-      double sum = 0.0;
-      for (int k = 0; k < 128 / BPAD; ++k) sum += sh.nrm[st + k * BPAD];
+      double sum = 0.0, cs = 0.0;
+      for (int k = 0; k < 128 / BPAD; ++k) { sum += sh.nrm[st + k * BPAD]; cs += sh.csum[st + k * BPAD]; }
       npart[static_cast<int64_t>(slab) * BPAD + st] = sum;
+      cpart[static_cast<int64_t>(slab) * BPAD + st] = cs;
     }
   } else {
     // ---------------------------------------------------------------- sketch generator (8 warps)
-    // TM = 2: warp -> (M tile, lane quarter), all 4 K chunks of a tile;
-    // TM = 1: warp -> (K half, lane quarter), 2 K chunks.
-    constexpr int NK = TM == 2 ? 4 : 2;
+    // TM = 2: warp -> (M tile, lane quarter), both 32-row K chunks of a tile (2 Philox calls);
+    // TM = 1: warp -> (K chunk, lane quarter), 1 Philox call.
+    constexpr int NK = TM == 2 ? 2 : 1;
     const int gw = warp - kGen0;                     // 0..7
     const int quarter = warp & 3;
     const int tm = TM == 2 ? gw / 4 : 0;
-    const int kc0 = TM == 2 ? 0 : (gw / 4) * 2;
+    const int kc0 = TM == 2 ? 0 : gw / 4;
     const int rl = tm * 128 + quarter * 32 + lane;
     const int r = half * ROWS + rl;
     const bool live = r < ell;
-    const uint32_t* tl = qtab + lane;
-    const uint64_t g16_0 = static_cast<uint64_t>((row_begin + r0) >> 4);
-    const uint32_t tbase = tmem + (static_cast<uint32_t>(32 * quarter) << 16) + ACOL0 + tm * 16 + kc0 * 4;
+    const uint64_t g32_0 = static_cast<uint64_t>((row_begin + r0) >> 5);
+    const uint32_t tbase = tmem + (static_cast<uint32_t>(32 * quarter) << 16) + ACOL0 + tm * 16 + kc0 * 8;
     for (int t = 0; t < ntiles; ++t) {
       const int sa = t & 1;
       if (t >= 2) mbar_wait(&sh.a_empty[sa], ((t >> 1) - 1) & 1);
@@ -585,20 +574,22 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
       if (live) {
 #pragma unroll
         for (int kc = 0; kc < NK; ++kc) {
-          const uint32_t grp = static_cast<uint32_t>(g16_0 + static_cast<uint64_t>(t) * (kKTile / 16) + kc0 + kc);
+          const uint32_t grp = static_cast<uint32_t>(g32_0 + static_cast<uint64_t>(t) * (kKTile / 32) + kc0 + kc);
           const U4 wv = philox4x32_10(grp, static_cast<uint32_t>(r), 0u, 0u, key0, key1);
           const uint32_t ws[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            const uint32_t a = ws[k];
-            const uint32_t b0 = tl[(a & 0xFFu) << 5], b1 = tl[((a >> 8) & 0xFFu) << 5];
-            const uint32_t b2 = tl[((a >> 16) & 0xFFu) << 5], b3 = tl[(a >> 24) << 5];
-            pk[4 * kc + k] = prmt(prmt(b0, b1, 0x0040), prmt(b2, b3, 0x0040), 0x5410);
+            // 8 nibbles n = (sign, v): q = m_v (sign 0) or ~m_v = -m_v - 1 (sign 1), 4 per PRMT
+            const uint32_t w = ws[k], w4 = w << 4;
+            const uint32_t mlo = prmt(t0, t1, w & 0x7777u), mhi = prmt(t0, t1, (w >> 16) & 0x7777u);
+            const uint32_t slo = prmt(w, w4, 0x9D8Cu), shi = prmt(w, w4, 0xBFAEu);   // sign bytes 0x00/0xFF
+            pk[8 * kc + 2 * k] = mlo ^ slo;
+            pk[8 * kc + 2 * k + 1] = mhi ^ shi;
           }
         }
       }
       const uint32_t ta = tbase + sa * TM * 16;
-      if constexpr (NK == 4) tmem_st16(ta, pk);
+      if constexpr (NK == 2) tmem_st16(ta, pk);
       else tmem_st8(ta, pk);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
@@ -614,18 +605,21 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
   }
 }
 
-// out = [scale * sum over slabs of part (ell x ncols, col-major); sum of norm partials]
-__global__ void k1_tc_reduce_kernel(const double* __restrict__ part, const double* __restrict__ npart, Geom g, int ell,
-                                    int ncols, double scale, double* __restrict__ out, unsigned* __restrict__ flags) {
+// out = [scale * (sum over slabs of part + colsum / 2) (ell x ncols, col-major); norms]
+__global__ void k1_tc_reduce_kernel(const double* __restrict__ part, const double* __restrict__ npart,
+                                    const double* __restrict__ cpart, Geom g, int ell, int ncols, double scale,
+                                    double* __restrict__ out, unsigned* __restrict__ flags) {
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t ny = static_cast<int64_t>(ell) * ncols;
   if (idx < ny) {
     const int j = static_cast<int>(idx / ell), r = static_cast<int>(idx % ell);
     const int h = r / g.rows, rl = r % g.rows;
-    double s = 0.0;
-    for (int sl = 0; sl < g.nslabs; ++sl)
+    double s = 0.0, c = 0.0;
+    for (int sl = 0; sl < g.nslabs; ++sl) {
       s += part[(static_cast<int64_t>(sl * g.nhalves + h) * g.bpad + j) * g.rows + rl];
-    out[idx] = scale * s;
+      c += cpart[static_cast<int64_t>(sl) * g.bpad + j];
+    }
+    out[idx] = scale * fma(0.5, c, s);
   } else if (idx < ny + ncols) {
     const int j = static_cast<int>(idx - ny);
     double s = 0.0;
@@ -641,16 +635,11 @@ __global__ void k1_tc_reduce_kernel(const double* __restrict__ part, const doubl
 constexpr int kTcMaxUnits = 256;
 
 inline size_t k1tc_workspace_bytes(int /*ell*/, int /*b_max*/, int64_t /*m_loc*/, bool /*f64*/) {
-  return static_cast<size_t>(kTcMaxUnits) * 64 * 256 * sizeof(double) + static_cast<size_t>(kTcMaxUnits) * 64 * sizeof(double) + 1024;
+  return static_cast<size_t>(kTcMaxUnits) * 64 * 256 * sizeof(double) +
+         2 * static_cast<size_t>(kTcMaxUnits) * 64 * sizeof(double) + 1024;
 }
 
 inline bool k1tc_supported(int ell, int b_max, bool /*f64*/) { return ell >= 1 && ell <= 1024 && b_max <= 64; }
-
-inline cudaError_t k1tc_init_tables(const int32_t* q, cudaStream_t st) {
-  int8_t q8[256];
-  for (int i = 0; i < 256; ++i) q8[i] = static_cast<int8_t>(q[i]);
-  return cudaMemcpyToSymbolAsync(c_qtab_i8, q8, sizeof(q8), 0, cudaMemcpyHostToDevice, st);
-}
 
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -672,7 +661,7 @@ inline PFN_encodeTiled k1tc_encoder() {
 inline bool k1tc_call_ok(const K1TcArgs& a) {
   const int es = a.f64 ? 8 : 4;
   if (a.ncols < 1 || a.ncols > 64) return false;
-  if (a.row_begin % 16 != 0) return false;
+  if (a.row_begin % 32 != 0) return false;        // Philox blocks of 32 rows (reading R2)
   if ((a.ld * es) % 16 != 0) return false;
   if (reinterpret_cast<uintptr_t>(a.X) % 16 != 0) return false;
   if (a.row_end - a.row_begin >= (int64_t(1) << 31)) return false;
@@ -683,23 +672,23 @@ inline bool k1tc_call_ok(const K1TcArgs& a) {
 
 template <typename T, int BPAD, int TM>
 inline cudaError_t k1tc_launch_t(const CUtensorMap& map, const K1TcArgs& a, const k1tc::Geom& g, cudaStream_t st,
-                                 double* part, double* npart) {
+                                 double* part, double* npart, double* cpart) {
   auto fn = k1tc::k1_tc_kernel<T, BPAD, TM>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem);
   if (e != cudaSuccess) return e;
   fn<<<g.nslabs * g.nhalves, k1tc::kThreads, g.smem, st>>>(map, a.ncols, a.row_begin, a.row_end - a.row_begin, a.ell,
-                                                           a.key0, a.key1, g, part, npart);
+                                                           a.key0, a.key1, a.t0, a.t1, g, part, npart, cpart);
   return cudaGetLastError();
 }
 
 template <typename T>
 inline cudaError_t k1tc_dispatch(const CUtensorMap& map, const K1TcArgs& a, const k1tc::Geom& g, cudaStream_t st,
-                                 double* part, double* npart) {
-  if (g.bpad == 16) return g.TM == 2 ? k1tc_launch_t<T, 16, 2>(map, a, g, st, part, npart)
-                                     : k1tc_launch_t<T, 16, 1>(map, a, g, st, part, npart);
-  if (g.bpad == 32) return g.TM == 2 ? k1tc_launch_t<T, 32, 2>(map, a, g, st, part, npart)
-                                     : k1tc_launch_t<T, 32, 1>(map, a, g, st, part, npart);
-  return k1tc_launch_t<T, 64, 1>(map, a, g, st, part, npart);
+                                 double* part, double* npart, double* cpart) {
+  if (g.bpad == 16) return g.TM == 2 ? k1tc_launch_t<T, 16, 2>(map, a, g, st, part, npart, cpart)
+                                     : k1tc_launch_t<T, 16, 1>(map, a, g, st, part, npart, cpart);
+  if (g.bpad == 32) return g.TM == 2 ? k1tc_launch_t<T, 32, 2>(map, a, g, st, part, npart, cpart)
+                                     : k1tc_launch_t<T, 32, 1>(map, a, g, st, part, npart, cpart);
+  return k1tc_launch_t<T, 64, 1>(map, a, g, st, part, npart, cpart);
 }
 
 inline cudaError_t k1tc_launch(const K1TcArgs& a, cudaStream_t st, int* nlaunch) {
@@ -719,12 +708,14 @@ inline cudaError_t k1tc_launch(const K1TcArgs& a, cudaStream_t st, int* nlaunch)
   if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
   double* part = reinterpret_cast<double*>(a.ws);
   double* npart = part + static_cast<size_t>(kTcMaxUnits) * 64 * 256;
-  cudaError_t e = a.f64 ? k1tc_dispatch<double>(map, a, g, st, part, npart) : k1tc_dispatch<float>(map, a, g, st, part, npart);
+  double* cpart = npart + static_cast<size_t>(kTcMaxUnits) * 64;
+  cudaError_t e = a.f64 ? k1tc_dispatch<double>(map, a, g, st, part, npart, cpart)
+                        : k1tc_dispatch<float>(map, a, g, st, part, npart, cpart);
   *nlaunch += 1;
   if (e != cudaSuccess) return e;
   const int64_t nout = int64_t(a.ell) * a.ncols + a.ncols;
-  k1tc::k1_tc_reduce_kernel<<<static_cast<unsigned>((nout + 255) / 256), 256, 0, st>>>(part, npart, g, a.ell, a.ncols,
-                                                                                     a.scale, a.out, a.flags);
+  k1tc::k1_tc_reduce_kernel<<<static_cast<unsigned>((nout + 255) / 256), 256, 0, st>>>(part, npart, cpart, g, a.ell,
+                                                                                     a.ncols, a.scale, a.out, a.flags);
   *nlaunch += 1;
   return cudaGetLastError();
 }

@@ -64,13 +64,24 @@ double inv_norm_cdf(double p) {
   return x;
 }
 
-void gauss256(int32_t q[256], double* scale) {
-  long long sum2 = 0;
-  for (int u = 0; u < 256; ++u) {
-    q[u] = static_cast<int32_t>(std::lround(44.0 * inv_norm_cdf((u + 0.5) / 256.0)));
-    sum2 += static_cast<long long>(q[u]) * q[u];
+// Gauss-16 (reading R2): magnitudes m_k = round(56 c_k - 1/2) of the centroids c_k of the 8
+// positive equiprobable N(0,1) bins; nibble n -> L(n) = (m_{n&7} + 1/2)(1 - 2(n >> 3)),
+// q(n) = L(n) - 1/2 (int8), entry = s L(n), s = 1/sqrt(mean L^2).
+void gauss16(int32_t m[8], int32_t q[16], double* scale) {
+  const double inv_sqrt_2pi = 0.3989422804014327;
+  auto phi = [&](double x) { return std::isfinite(x) ? inv_sqrt_2pi * std::exp(-0.5 * x * x) : 0.0; };
+  for (int k = 0; k < 8; ++k) {
+    const double a = k == 0 ? 0.0 : inv_norm_cdf((k + 8) / 16.0);
+    const double b = k == 7 ? INFINITY : inv_norm_cdf((k + 9) / 16.0);
+    m[k] = static_cast<int32_t>(std::lround(56.0 * 16.0 * (phi(a) - phi(b)) - 0.5));
   }
-  *scale = 16.0 / std::sqrt(static_cast<double>(sum2));
+  double sum2 = 0.0;
+  for (int n = 0; n < 16; ++n) {
+    const double L = (m[n & 7] + 0.5) * (n >> 3 ? -1.0 : 1.0);
+    q[n] = (n >> 3) ? -m[n & 7] - 1 : m[n & 7];
+    sum2 += L * L;
+  }
+  *scale = 1.0 / std::sqrt(sum2 / 16.0);
 }
 
 // ------------------------------------------------------------------ workspace layout
@@ -170,7 +181,7 @@ const char* validate(const oid_params* p) {
   if (!(p->eps > 0.0) || !(p->delta > 0.0 && p->delta < 1.0) || !(p->c > 0.0)) return "need eps > 0, 0 < delta < 1, c > 0";
   if (p->dtype != OID_F32 && p->dtype != OID_F64) return "dtype must be OID_F32 or OID_F64";
   if (p->k1_mode < 0 || p->k1_mode > 2) return "bad k1_mode";
-  if (p->m / 16 >= (int64_t(1) << 32)) return "m too large for the 32-bit Philox row counter";
+  if (p->m / 32 >= (int64_t(1) << 32)) return "m too large for the 32-bit Philox row counter";
   return nullptr;
 }
 
@@ -187,6 +198,7 @@ struct oid_ctx_s {
   int coop_max = 0;   // max co-resident CTAs of the Jacobi kernel
   int k1_ctas_per_sm = 1;
   double qscale = 0.0;
+  int32_t qmag[8] = {0};
   double factor = 0.0;
   uint32_t key0 = 0, key1 = 0;
   int64_t n_obs = 0, epoch = 0;
@@ -312,7 +324,7 @@ oid_status launch_k1_simt(oid_ctx ctx, cudaStream_t st, const T* X, int64_t ld, 
   const int ncb = nc <= 16 ? 16 : (nc <= 32 ? 32 : 64);
   const int rpt = ncb <= 32 ? 2 : 1;
   const int ysplit = (p.ell + 256 * rpt - 1) / (256 * rpt);
-  const int64_t g_begin = p.row_begin / 16, g_end = (p.row_end + 15) / 16;
+  const int64_t g_begin = p.row_begin / kGrp, g_end = (p.row_end + kGrp - 1) / kGrp;
   const int64_t ngroups = g_end - g_begin;
   int64_t want = std::max<int64_t>(1, (int64_t(ctx->num_sms) * ctx->k1_ctas_per_sm) / ysplit);
   want = std::min<int64_t>(want, std::min<int64_t>(ngroups, kK1MaxCtas));
@@ -348,6 +360,10 @@ oid_status do_sketch(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   a.X = X; a.ld = ld; a.ncols = nc; a.row_begin = p.row_begin; a.row_end = p.row_end; a.ell = p.ell;
   a.key0 = ctx->key0; a.key1 = ctx->key1; a.scale = ctx->qscale; a.f64 = p.dtype == OID_F64;
   a.ws = ctx->ws + ctx->L.tc; a.out = ctx->d(ctx->L.Ypart); a.flags = ctx->ptr<unsigned>(ctx->L.flags);
+  a.t0 = static_cast<uint32_t>(ctx->qmag[0]) | (static_cast<uint32_t>(ctx->qmag[1]) << 8) |
+         (static_cast<uint32_t>(ctx->qmag[2]) << 16) | (static_cast<uint32_t>(ctx->qmag[3]) << 24);
+  a.t1 = static_cast<uint32_t>(ctx->qmag[4]) | (static_cast<uint32_t>(ctx->qmag[5]) << 8) |
+         (static_cast<uint32_t>(ctx->qmag[6]) << 16) | (static_cast<uint32_t>(ctx->qmag[7]) << 24);
   a.num_sms = ctx->num_sms;
   const bool tc_call = want_tc && ctx->tc_ok && k1tc_call_ok(a);
   if (p.k1_mode == OID_K1_TC_INT8 && !tc_call)
@@ -470,9 +486,10 @@ oid_status oid_workspace_query(const oid_params* p, size_t* bytes) {
   return OID_OK;
 }
 
-oid_status oid_sketch_table(int32_t q[256], double* scale) {
+oid_status oid_sketch_table(int32_t q[16], double* scale) {
   if (!q || !scale) return OID_EINVAL;
-  gauss256(q, scale);
+  int32_t m[8];
+  gauss16(m, q, scale);
   return OID_OK;
 }
 
@@ -495,8 +512,8 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
   ctx->key1 = static_cast<uint32_t>(p->seed >> 32);
   const double k = p->k;
   ctx->factor = p->c * (k * std::log(k) + k * std::log(1.0 / p->delta) / p->eps) / ctx->t;
-  int32_t q[256];
-  gauss256(q, &ctx->qscale);
+  int32_t q[16];
+  gauss16(ctx->qmag, q, &ctx->qscale);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   auto bad = [&](cudaError_t e) {
     snprintf(g_init_err, sizeof(g_init_err), "init: %s", cudaGetErrorString(e));
@@ -524,10 +541,9 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
   ctx->k1_ctas_per_sm = 1;
   ctx->cold_jacobi = getenv("OID_JACOBI_COLD") && atoi(getenv("OID_JACOBI_COLD")) != 0;
   ctx->tc_ok = (prop.major == 10 && prop.minor == 0) && k1tc_supported(p->ell, p->b_max, p->dtype == OID_F64);
-  double qd[256];
-  for (int i = 0; i < 256; ++i) qd[i] = q[i];
+  double qd[16];
+  for (int i = 0; i < 16; ++i) qd[i] = q[i] + 0.5;
   if ((e = cudaMemcpyToSymbolAsync(c_qtab_f64, qd, sizeof(qd), 0, cudaMemcpyHostToDevice, st)) != cudaSuccess) return bad(e);
-  if ((e = k1tc_init_tables(q, st)) != cudaSuccess) return bad(e);
   // state: J = -1, tau_old = 1, Gram = 0, S = 0, scalars, flags
   const Layout& L = ctx->L;
   if ((e = cudaMemsetAsync(ctx->ws + L.J, 0xff, sizeof(int64_t) * ctx->t, st)) != cudaSuccess) return bad(e);

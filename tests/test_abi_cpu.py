@@ -39,10 +39,10 @@ def test_version(oid):
 
 
 def test_sketch_table_matches_oracle(oid):
-    from oracle import gauss256_table, gauss256_scale
+    from oracle import gauss16_levels, gauss16_scale
     q, s = oid.sketch_table()
-    assert np.array_equal(q, gauss256_table())
-    assert s == gauss256_scale()
+    assert np.array_equal(q + 0.5, gauss16_levels())
+    assert abs(s - gauss16_scale()) <= 2e-16 * s
 
 
 def test_workspace_query_validates(oid):

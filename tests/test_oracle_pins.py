@@ -10,7 +10,8 @@ import os
 import numpy as np
 import pytest
 
-from oracle import philox4x32_10, uniform24, gauss256_table, gauss256_scale, omega_rows
+from oracle import philox4x32_10, uniform24, gauss16_magnitudes, gauss16_levels, gauss16_scale, omega_rows
+from oracle.gauss16 import omega_nibbles
 from oracle.oid import (OracleParams, OracleOID, ridge_scores, ridge_lambda, eig_gram, select,
                         alg4_coefficients, hutchpp_estimate, sketch)
 from synth import c1_matrix, low_rank_matrix
@@ -42,7 +43,7 @@ def test_uniform24_grid_and_range():
     assert abs(u.mean() - 0.5) < 4 * math.sqrt(1 / 12 / u.size)
 
 
-# ------------------------------------------------------------------ Gauss-256 (reading R2)
+# ------------------------------------------------------------------ Gauss-16 (reading R2)
 
 def _inv_norm_bisect(p):
     """Independent inverse normal CDF: bisection on 0.5*erfc(-x/sqrt 2) (stdlib libm)."""
@@ -56,33 +57,59 @@ def _inv_norm_bisect(p):
     return 0.5 * (lo + hi)
 
 
-def test_gauss256_table_independent_construction():
-    q = gauss256_table()
-    want = [round(44.0 * _inv_norm_bisect((u + 0.5) / 256.0)) for u in range(256)]
-    assert list(q) == want
-    assert np.all(q == -q[::-1])                  # odd about u = 127.5 -> mean exactly 0
-    assert q.min() == -127 and q.max() == 127     # fits int8
-    assert np.all(np.diff(q) >= 0)
+def _phi(x):
+    return math.exp(-0.5 * x * x) / math.sqrt(2.0 * math.pi) if math.isfinite(x) else 0.0
 
 
-def test_gauss256_unit_variance_and_shape():
-    q = gauss256_table().astype(np.float64)
-    s = gauss256_scale()
-    assert abs(s * s * np.mean(q * q) - 1.0) < 4e-16
-    z = s * q
-    # discretised N(0,1): KS distance of the equiprobable 256-point law is ~1/256
+def test_gauss16_table_independent_construction():
+    """Bin centroids of the 16 equiprobable N(0,1) bins, rebuilt with stdlib erfc/exp only."""
+    want = []
+    for k in range(8):
+        a = _inv_norm_bisect((k + 8) / 16.0) if k > 0 else 0.0
+        b = _inv_norm_bisect((k + 9) / 16.0) if k < 7 else math.inf
+        c = 16.0 * (_phi(a) - _phi(b))
+        want.append(round(56.0 * c - 0.5))
+    assert list(gauss16_magnitudes()) == want == [4, 13, 22, 32, 43, 56, 74, 110]
+    L = gauss16_levels()
+    assert np.all(L[8:] == -L[:8])                 # odd in the sign bit -> mean exactly 0
+    assert np.all(np.diff(L[:8]) > 0) and L[0] > 0
+    q = L - 0.5                                     # the integers the tensor cores see
+    assert np.all(q == np.round(q)) and q.min() >= -128 and q.max() <= 127
+
+
+def test_gauss16_unit_variance_and_shape():
+    L = gauss16_levels()
+    s = gauss16_scale()
+    assert abs(s * s * np.mean(L * L) - 1.0) < 4e-16
+    z = np.sort(s * L)
+    # equiprobable 16-point law: KS distance to N(0,1) ~ 1/32 + centroid offset
     from scipy.stats import norm
-    ks = np.max(np.abs((np.arange(1, 257) - 0.5) / 256 - norm.cdf(z)))
-    assert ks < 0.006
+    cdf = norm.cdf(z)
+    ks = max(np.max(np.abs(np.arange(1, 17) / 16 - cdf)), np.max(np.abs(np.arange(0, 16) / 16 - cdf)))
+    assert ks < 0.045
     kurt = np.mean(z ** 4)
-    assert 2.85 < kurt < 3.0
+    assert 2.5 < kurt < 2.7                          # sub-Gaussian, below the Gaussian 3
 
 
-def test_omega_bytes_uniform_and_moments():
-    Z = omega_rows(7, np.arange(64), 0, 1 << 14).astype(np.float64) * gauss256_scale()
+def test_omega_nibble_layout_from_kat():
+    """Nibble n(r, i) = nibble (i & 7) of word (i & 31) >> 3 of the Philox block (i >> 5, r, 0, 0).
+
+    Checked against the KAT row (c0=1, c1=1, key (2, 1)) of tests/golden: seed 0x100000002,
+    sketch row 1, data rows 32..63."""
+    nib = omega_nibbles(0x100000002, [1], 32, 64)[0]
+    words = [0x4f560ce1, 0xabeeceff, 0x650ea1f9, 0xc098974e]
+    want = [(words[i >> 3] >> (4 * (i & 7))) & 15 for i in range(32)]
+    assert list(nib) == want
+
+
+def test_omega_entries_uniform_and_moments():
+    Z = omega_rows(7, np.arange(64), 0, 1 << 14) * gauss16_scale()
     n = Z.size
     assert abs(Z.mean()) < 4 / math.sqrt(n)
     assert abs(Z.var() - 1.0) < 4 * math.sqrt(2.0 / n)
+    nib = omega_nibbles(7, np.arange(64), 0, 1 << 14)
+    counts = np.bincount(nib.ravel(), minlength=16)
+    assert np.all(np.abs(counts - n / 16) < 5 * math.sqrt(n / 16))
     # rows independent: empirical correlation of two sketch rows ~ 0
     c = np.corrcoef(Z[0], Z[1])[0, 1]
     assert abs(c) < 4 / math.sqrt(Z.shape[1])
@@ -112,7 +139,7 @@ def test_sketch_identity_mode():
     """Identity sketch (Omega = I, l = m) makes S = A exactly."""
     X = np.random.default_rng(1).standard_normal((40, 5))
     p = _params(40, 4, 40, 0.0)
-    Y = sketch(p, X, Qcache=np.eye(40) / gauss256_scale())
+    Y = sketch(p, X, Qcache=np.eye(40) / gauss16_scale())
     assert np.allclose(Y, X, rtol=1e-15, atol=1e-15)
 
 
