@@ -68,7 +68,7 @@ typedef struct {
   int64_t row_begin;  /* this shard's global rows [row_begin, row_end); Omega is keyed   */
   int64_t row_end;    /*   on GLOBAL rows so the sketch is independent of the sharding   */
   int64_t n_cap;      /* max columns ever ingested (sizes S: ell x n_cap, P: k x n_cap)  */
-  int32_t k;          /* target rank = basis size t (k = t)                        */
+  int32_t k;          /* target rank = basis size t (k = t); 1 <= k <= min(ell, 416) */
   int32_t ell;        /* sketch rows l = k + p; 1 <= ell <= 1024                  */
   int32_t b_max;      /* max columns per ingest call, 1..64                              */
   int32_t ell1, ell2, ell3; /* NA-Hutch++ contiguous row split, sum = ell (R11)    */

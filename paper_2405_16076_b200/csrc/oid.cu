@@ -173,6 +173,7 @@ const char* validate(const oid_params* p) {
   if (p->k < 1) return "k must be >= 1";
   if (p->ell < 1 || p->ell > 1024) return "ell must be in [1, 1024]";
   if (p->k > p->ell) return "k must be <= ell";
+  if (p->k > 416) return "k must be <= 416";
   if (p->b_max < 1 || p->b_max > 64) return "b_max must be in [1, 64]";
   if (p->n_cap < 1) return "n_cap must be >= 1";
   if (p->ell1 < 0 || p->ell2 < 0 || p->ell3 < 0 || p->ell1 + p->ell2 + p->ell3 != p->ell)
@@ -532,10 +533,10 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
     const int big = static_cast<int>(prop.sharedMemPerBlockOptin) - 2048;
     if ((e = cudaFuncSetAttribute(bjacobi_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big)) != cudaSuccess) return bad(e);
     if ((e = cudaFuncSetAttribute(bjacobi_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big)) != cudaSuccess) return bad(e);
-#define BG_ATTR(TT, JC, DQ) \
-    if ((e = cudaFuncSetAttribute(basis_gram_dirty_kernel<TT, JC, DQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, big)) != cudaSuccess) return bad(e)
-    BG_ATTR(double, 1, 32); BG_ATTR(double, 2, 32); BG_ATTR(double, 3, 16); BG_ATTR(double, 4, 16);
-    BG_ATTR(float, 1, 32); BG_ATTR(float, 2, 32); BG_ATTR(float, 3, 16); BG_ATTR(float, 4, 16);
+#define BG_ATTR(TT, JB) \
+    if ((e = cudaFuncSetAttribute(basis_gram_dirty_kernel<TT, JB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 184 * 1024)) != cudaSuccess) return bad(e)
+    BG_ATTR(double, 1); BG_ATTR(double, 2); BG_ATTR(double, 4); BG_ATTR(double, 7); BG_ATTR(double, 13);
+    BG_ATTR(float, 1); BG_ATTR(float, 2); BG_ATTR(float, 4); BG_ATTR(float, 7); BG_ATTR(float, 13);
 #undef BG_ATTR
   }
   ctx->k1_ctas_per_sm = 1;
@@ -622,20 +623,24 @@ oid_status oid_estimate_begin(oid_ctx ctx, void* stream) {
   int chunks = static_cast<int>(std::min<int64_t>(std::min(2 * ctx->num_sms, kGramChunks), (ctx->m_loc + 1023) / 1024));
   chunks = std::max(1, chunks);
   int64_t per = (ctx->m_loc + chunks - 1) / chunks;
-  per = (per + 15) / 16 * 16;
+  per = (per + kBgRows - 1) / kBgRows * kBgRows;
   chunks = static_cast<int>((ctx->m_loc + per - 1) / per);
-  const size_t smem = sizeof(double) * 16 * t;
-  const int jc = (t + 255) / 256;
-#define BG_LAUNCH(TT, JC, DQ)                                                                                   \
-  basis_gram_dirty_kernel<TT, JC, DQ><<<chunks, 256, smem, st>>>(ctx->ptr<TT>(L.C), ctx->m_loc, t, per,           \
-                                                                 ctx->ptr<int>(L.dlist), ctx->ptr<int>(L.counts), \
-                                                                 ctx->d(L.Gpart))
+  const bool f64 = ctx->p.dtype == OID_F64;
+  const size_t stage_bytes = f64 ? bg_stage_elems<double>(t) * 8 : bg_stage_elems<float>(t) * 4;
+  const int nstage = 2 * stage_bytes <= 180 * 1024 ? 2 : 1;
+  const size_t smem = nstage * stage_bytes;
+  const int jb = (t + 31) / 32;
+#define BG_LAUNCH(TT, JB)                                                                                       \
+  basis_gram_dirty_kernel<TT, JB><<<chunks, 256, smem, st>>>(ctx->ptr<TT>(L.C), ctx->m_loc, t, per, nstage,     \
+                                                             ctx->ptr<int>(L.dlist), ctx->ptr<int>(L.counts),   \
+                                                             ctx->d(L.Gpart))
 #define BG_DISPATCH(TT)                          \
-  if (jc == 1) BG_LAUNCH(TT, 1, 32);              \
-  else if (jc == 2) BG_LAUNCH(TT, 2, 32);         \
-  else if (jc == 3) BG_LAUNCH(TT, 3, 16);         \
-  else BG_LAUNCH(TT, 4, 16)
-  if (ctx->p.dtype == OID_F64) { BG_DISPATCH(double); } else { BG_DISPATCH(float); }
+  if (jb <= 1) BG_LAUNCH(TT, 1);                  \
+  else if (jb <= 2) BG_LAUNCH(TT, 2);             \
+  else if (jb <= 4) BG_LAUNCH(TT, 4);             \
+  else if (jb <= 7) BG_LAUNCH(TT, 7);             \
+  else BG_LAUNCH(TT, 13)
+  if (f64) { BG_DISPATCH(double); } else { BG_DISPATCH(float); }
 #undef BG_DISPATCH
 #undef BG_LAUNCH
   CKL();

@@ -204,57 +204,111 @@ __global__ void dirty_compact_kernel(int* __restrict__ dirty, int t, int* __rest
 
 // Incremental exact basis Gram (A9): Dpart[chunk](q, j) = sum_{rows in chunk} C(r, d_q) C(r, j)
 // for the dirty slots d_q.  Each CTA streams its row chunk of the basis once per
-// group of DQ dirty slots (one group in steady state).  Rows staged 16 at a time in smem.
-template <typename T, int JC, int DQ>
+// group of 32 dirty slots, 32 rows at a time through a 2-stage cp.async ring (column-major tile,
+// pitch BG_PITCH elements: conflict-free column-strided reads).  Thread (tq, tj) = (tid % 8,
+// tid / 8) owns the 4 x JB register tile q = tq + 8a, j = tj + 32b (fp64 FMA, fixed order).
+constexpr int kBgRows = 32;
+template <typename T> struct BgPitch { static constexpr int v = sizeof(T) == 8 ? 34 : 36; };
+
+template <typename T>
+__host__ __device__ constexpr size_t bg_stage_elems(int t) { return static_cast<size_t>(t) * BgPitch<T>::v; }
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+template <typename T, int JB>
 __global__ void __launch_bounds__(256) basis_gram_dirty_kernel(const T* __restrict__ C, int64_t m_loc, int t,
-                                                               int64_t rows_per_chunk, const int* __restrict__ list,
+                                                               int64_t rows_per_chunk, int nstage,
+                                                               const int* __restrict__ list,
                                                                const int* __restrict__ counts,
                                                                double* __restrict__ part) {
-  extern __shared__ double tile[];   // [16][t]
+  extern __shared__ __align__(16) unsigned char bg_smem[];
+  constexpr int P = BgPitch<T>::v;
+  constexpr int EPC = 16 / sizeof(T);                  // elements per 16-byte copy
+  T* tiles = reinterpret_cast<T*>(bg_smem);            // [nstage][t][P]
+  __shared__ double dt[kBgRows][33];                   // dirty columns of the current tile
+  __shared__ int dl[32];
   const int nd = counts[2];
   if (nd == 0) return;
+  const int tid = threadIdx.x, tq = tid & 7, tj = tid >> 3;
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * rows_per_chunk;
   const int64_t r1 = min(m_loc, r0 + rows_per_chunk);
+  const int ntile = static_cast<int>((r1 - r0 + kBgRows - 1) / kBgRows);
+  const size_t stage = bg_stage_elems<T>(t);
+  const bool vec = ((m_loc * sizeof(T)) % 16 == 0) && (r0 % EPC == 0);
   double* out = part + static_cast<int64_t>(blockIdx.x) * t * t;
-  for (int q0 = 0; q0 < nd; q0 += DQ) {
-    int dq[DQ];
+
+  auto load = [&](int it, int buf) {
+    T* dst = tiles + buf * stage;
+    const int64_t rb = r0 + static_cast<int64_t>(it) * kBgRows;
+    constexpr int CH = kBgRows / EPC;                  // 16-byte chunks per column
+    for (int e = tid; e < t * CH; e += 256) {
+      const int col = e / CH, c = e - col * CH;
+      const int64_t r = rb + c * EPC;
+      T* d = dst + col * P + c * EPC;
+      const T* src = C + static_cast<int64_t>(col) * m_loc + r;
+      if (vec && r + EPC <= r1) {
+        cp_async16(d, src);
+      } else {
 #pragma unroll
-    for (int q = 0; q < DQ; ++q) dq[q] = (q0 + q < nd) ? list[q0 + q] : 0;
-    double acc[JC][DQ];
+        for (int k = 0; k < EPC; ++k) d[k] = (r + k < r1) ? src[k] : T(0);
+      }
+    }
+  };
+
+  for (int q0 = 0; q0 < nd; q0 += 32) {
+    if (tid < 32) dl[tid] = (q0 + tid < nd) ? list[q0 + tid] : -1;
+    double acc[4][JB];
 #pragma unroll
-    for (int c = 0; c < JC; ++c)
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int q = 0; q < DQ; ++q) acc[c][q] = 0.0;
-    for (int64_t rb = r0; rb < r1; rb += 16) {
+      for (int b = 0; b < JB; ++b) acc[a][b] = 0.0;
+    __syncthreads();
+    load(0, 0);
+    cp_async_commit();
+    for (int it = 0; it < ntile; ++it) {
+      const int buf = nstage == 2 ? (it & 1) : 0;
+      if (nstage == 2 && it + 1 < ntile) load(it + 1, buf ^ 1);
+      cp_async_commit();
+      if (nstage == 2) cp_async_wait<1>(); else cp_async_wait<0>();
       __syncthreads();
-      for (int e = threadIdx.x; e < 16 * t; e += 256) {
-        const int rr = e & 15, col = e >> 4;
-        const int64_t r = rb + rr;
-        tile[rr * t + col] = r < r1 ? static_cast<double>(C[static_cast<int64_t>(col) * m_loc + r]) : 0.0;
+      const T* tile = tiles + buf * stage;
+      for (int e = tid; e < 32 * kBgRows; e += 256) {        // gather the dirty columns
+        const int q = e >> 5, rr = e & 31;
+        const int d = dl[q];
+        dt[rr][q] = d >= 0 ? static_cast<double>(tile[d * P + rr]) : 0.0;
       }
       __syncthreads();
 #pragma unroll 4
-      for (int rr = 0; rr < 16; ++rr) {
-        const double* row = tile + rr * t;
-        double dv[DQ];
+      for (int rr = 0; rr < kBgRows; ++rr) {
+        double dv[4], xv[JB];
 #pragma unroll
-        for (int q = 0; q < DQ; ++q) dv[q] = row[dq[q]];
+        for (int a = 0; a < 4; ++a) dv[a] = dt[rr][tq + 8 * a];
 #pragma unroll
-        for (int c = 0; c < JC; ++c) {
-          const int j = threadIdx.x + 256 * c;
-          const double xj = j < t ? row[j] : 0.0;
-#pragma unroll
-          for (int q = 0; q < DQ; ++q) acc[c][q] = fma(dv[q], xj, acc[c][q]);
+        for (int b = 0; b < JB; ++b) {
+          const int j = tj + 32 * b;
+          xv[b] = j < t ? static_cast<double>(tile[j * P + rr]) : 0.0;
         }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < JB; ++b) acc[a][b] = fma(dv[a], xv[b], acc[a][b]);
       }
+      __syncthreads();
+      if (nstage == 1 && it + 1 < ntile) load(it + 1, 0);
     }
 #pragma unroll
-    for (int c = 0; c < JC; ++c) {
-      const int j = threadIdx.x + 256 * c;
-      if (j < t) {
+    for (int a = 0; a < 4; ++a) {
+      const int q = tq + 8 * a;
+      if (q0 + q >= nd) continue;
 #pragma unroll
-        for (int q = 0; q < DQ; ++q)
-          if (q0 + q < nd) out[(q0 + q) + static_cast<int64_t>(j) * t] = acc[c][q];
+      for (int b = 0; b < JB; ++b) {
+        const int j = tj + 32 * b;
+        if (j < t) out[(q0 + q) + static_cast<int64_t>(j) * t] = acc[a][b];
       }
     }
   }
