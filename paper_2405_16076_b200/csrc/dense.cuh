@@ -268,6 +268,216 @@ __global__ void __launch_bounds__(32 * W) bjacobi_kernel(double* __restrict__ B,
   }
 }
 
+// Two-sided block Jacobi eigen-solver for a symmetric n x n matrix H (col-major, ld n):
+// on exit H is (numerically) diagonal and V <- V U holds the accumulated rotations, so with
+// H = V0^T A V0 on entry (warm start: V0 = previous eigenvectors), A = V diag(H) V^T.
+// Indices are cut into blocks of W; each outer round pairs blocks round-robin.  Phase A: one
+// CTA per block pair runs one cyclic sweep of scalar rotations on the 2W x 2W diagonal
+// block in shared memory (parallel ordering, W rotations per step) and publishes its
+// accumulated 2W x 2W rotation U_p.  Phase B: every CTA applies H[I,K] <- U_I^T H[I,K] U_K
+// to 2W x 2W tiles (pairs I <= K, mirrored) and V[:, I] <- V[:, I] U_I.  Two grid barriers
+// per round; sweeps stop when a sweep applies no rotation.  A rotation of (p, q) is applied
+// when |h_pq| > max(tol sqrt(|h_pp h_qq|), abs_tol).  Cooperative launch.
+constexpr int kSymW = 16;
+constexpr int kSymB = 2 * kSymW;     // 32
+constexpr int kSymP = kSymB + 1;     // smem pitch
+
+__device__ __forceinline__ void sym_pair(int k, int pi, int m1, int& P, int& Q) {
+  int a, b;
+  if (pi == 0) { a = m1; b = k; } else { a = (k + pi) % m1; b = (k - pi + m1) % m1; }
+  if (m1 == 0) { a = 0; b = 1; }
+  P = min(a, b); Q = max(a, b);
+}
+__device__ __forceinline__ int sym_idx(int P, int Q, int i) { return i < kSymW ? P * kSymW + i : Q * kSymW + (i - kSymW); }
+
+__global__ void __launch_bounds__(256) sym_bjacobi_kernel(double* __restrict__ H, double* __restrict__ V, int n,
+                                                          double* __restrict__ Ubuf, int* __restrict__ flags,
+                                                          int* __restrict__ counters, int max_sweeps, double tol,
+                                                          const double* __restrict__ abs_tol_p) {
+  cg::grid_group grid = cg::this_grid();
+  const double abs_tol = *abs_tol_p;
+  __shared__ double S[kSymB][kSymP];
+  __shared__ double U[kSymB][kSymP];
+  __shared__ double T[kSymB][kSymP];
+  __shared__ double rot[kSymW][2];
+  __shared__ int rp[kSymW][2];
+  __shared__ int nrot;
+  const int tid = threadIdx.x;
+  const int nb = (n + kSymW - 1) / kSymW;
+  const int nbb = nb + (nb & 1);
+  const int npairs = nbb / 2;
+  const int m1 = nbb - 1;
+  const int rounds = max(m1, 1);
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    for (int k = 0; k < rounds; ++k) {
+      // ---------------- phase A: one inner cyclic sweep per block pair
+      for (int pi = blockIdx.x; pi < npairs; pi += gridDim.x) {
+        int P, Q;
+        sym_pair(k, pi, m1, P, Q);
+        for (int e = tid; e < kSymB * kSymB; e += 256) {
+          const int i = e % kSymB, j = e / kSymB;
+          const int gi = sym_idx(P, Q, i), gj = sym_idx(P, Q, j);
+          S[i][j] = (gi < n && gj < n) ? H[gi + static_cast<int64_t>(gj) * n] : 0.0;
+          U[i][j] = (i == j) ? 1.0 : 0.0;
+        }
+        if (tid == 0) nrot = 0;
+        __syncthreads();
+        for (int step = 0; step < kSymB - 1; ++step) {
+          if (tid < kSymW) {
+            int p, q;
+            if (tid == 0) { p = kSymB - 1; q = step; }
+            else { p = (step + tid) % (kSymB - 1); q = (step - tid + kSymB - 1) % (kSymB - 1); }
+            if (p > q) { const int x = p; p = q; q = x; }
+            const double app = S[p][p], aqq = S[q][q], apq = S[p][q];
+            double cs = 1.0, sn = 0.0;
+            if (apq != 0.0 && fabs(apq) > fmax(tol * sqrt(fabs(app * aqq)), abs_tol)) {
+              const double zeta = (aqq - app) / (2.0 * apq);
+              double t;
+              if (fabs(zeta) > 1e150) t = 0.5 / zeta;
+              else t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+              cs = 1.0 / sqrt(fma(t, t, 1.0));
+              sn = cs * t;
+              atomicAdd(&nrot, 1);
+            }
+            rot[tid][0] = cs; rot[tid][1] = sn; rp[tid][0] = p; rp[tid][1] = q;
+          }
+          __syncthreads();
+          for (int e = tid; e < kSymW * kSymB; e += 256) {      // rows: S <- J^T S
+            const int r = e / kSymB, j = e % kSymB;
+            const double cs = rot[r][0], sn = rot[r][1];
+            if (sn == 0.0) continue;
+            const int p = rp[r][0], q = rp[r][1];
+            const double x = S[p][j], y = S[q][j];
+            S[p][j] = cs * x - sn * y;
+            S[q][j] = sn * x + cs * y;
+          }
+          __syncthreads();
+          for (int e = tid; e < kSymW * kSymB; e += 256) {      // columns: S <- S J, U <- U J
+            const int r = e / kSymB, i = e % kSymB;
+            const double cs = rot[r][0], sn = rot[r][1];
+            if (sn == 0.0) continue;
+            const int p = rp[r][0], q = rp[r][1];
+            const double x = S[i][p], y = S[i][q];
+            S[i][p] = cs * x - sn * y;
+            S[i][q] = sn * x + cs * y;
+            const double u = U[i][p], v = U[i][q];
+            U[i][p] = cs * u - sn * v;
+            U[i][q] = sn * u + cs * v;
+          }
+          __syncthreads();
+        }
+        double* Ug = Ubuf + static_cast<int64_t>(pi) * kSymB * kSymB;
+        for (int e = tid; e < kSymB * kSymB; e += 256) Ug[e] = U[e % kSymB][e / kSymB];
+        if (tid == 0) {
+          flags[pi] = nrot > 0;
+          if (nrot) atomicAdd(&counters[sweep], nrot);
+        }
+        __syncthreads();
+      }
+      grid.sync();
+      // ---------------- phase B: apply the rotations to H tiles and V column blocks
+      const int ntri = npairs * (npairs + 1) / 2;
+      const int nvt = npairs * ((n + kSymB - 1) / kSymB);
+      for (int w = blockIdx.x; w < ntri + nvt; w += gridDim.x) {
+        if (w < ntri) {
+          int I = 0, rem = w;
+          while (rem >= npairs - I) { rem -= npairs - I; ++I; }
+          const int K = I + rem;
+          const bool fi = flags[I] != 0, fk = flags[K] != 0;
+          if (!fi && !fk) continue;
+          int PI, QI, PK, QK;
+          sym_pair(k, I, m1, PI, QI);
+          sym_pair(k, K, m1, PK, QK);
+          const double* UI = Ubuf + static_cast<int64_t>(I) * kSymB * kSymB;
+          const double* UK = Ubuf + static_cast<int64_t>(K) * kSymB * kSymB;
+          for (int e = tid; e < kSymB * kSymB; e += 256) {
+            const int i = e % kSymB, j = e / kSymB;
+            const int gi = sym_idx(PI, QI, i), gj = sym_idx(PK, QK, j);
+            T[i][j] = (gi < n && gj < n) ? H[gi + static_cast<int64_t>(gj) * n] : 0.0;
+            S[i][j] = UI[e];           // S = U_I (i, j) col-major source
+            U[i][j] = UK[e];
+          }
+          __syncthreads();
+          // R = T U_K  (kept in registers: each thread 4 entries)
+          double r4[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int e = tid + 256 * c;
+            const int i = e % kSymB, j = e / kSymB;
+            double acc = 0.0;
+#pragma unroll 8
+            for (int l = 0; l < kSymB; ++l) acc = fma(T[i][l], U[l][j], acc);
+            r4[c] = acc;
+          }
+          __syncthreads();
+#pragma unroll
+          for (int c = 0; c < 4; ++c) { const int e = tid + 256 * c; T[e % kSymB][e / kSymB] = r4[c]; }
+          __syncthreads();
+          // out = U_I^T R
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int e = tid + 256 * c;
+            const int i = e % kSymB, j = e / kSymB;
+            double acc = 0.0;
+#pragma unroll 8
+            for (int l = 0; l < kSymB; ++l) acc = fma(S[l][i], T[l][j], acc);
+            const int gi = sym_idx(PI, QI, i), gj = sym_idx(PK, QK, j);
+            if (gi < n && gj < n) {
+              H[gi + static_cast<int64_t>(gj) * n] = acc;
+              if (I != K) H[gj + static_cast<int64_t>(gi) * n] = acc;
+            }
+          }
+          __syncthreads();
+        } else {
+          const int v = w - ntri;
+          const int I = v % npairs, rc = v / npairs;
+          if (!flags[I]) continue;
+          int PI, QI;
+          sym_pair(k, I, m1, PI, QI);
+          const double* UI = Ubuf + static_cast<int64_t>(I) * kSymB * kSymB;
+          const int r0 = rc * kSymB;
+          for (int e = tid; e < kSymB * kSymB; e += 256) {
+            const int i = e % kSymB, j = e / kSymB;
+            const int gj = sym_idx(PI, QI, j);
+            T[i][j] = (r0 + i < n && gj < n) ? V[(r0 + i) + static_cast<int64_t>(gj) * n] : 0.0;
+            U[i][j] = UI[e];
+          }
+          __syncthreads();
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int e = tid + 256 * c;
+            const int i = e % kSymB, j = e / kSymB;
+            double acc = 0.0;
+#pragma unroll 8
+            for (int l = 0; l < kSymB; ++l) acc = fma(T[i][l], U[l][j], acc);
+            const int gj = sym_idx(PI, QI, j);
+            if (r0 + i < n && gj < n) V[(r0 + i) + static_cast<int64_t>(gj) * n] = acc;
+          }
+          __syncthreads();
+        }
+      }
+      grid.sync();
+    }
+    const int rotated = atomicAdd(&counters[sweep], 0);
+    if (rotated == 0) break;
+  }
+}
+
+// d[i] = H(i, i)
+__global__ void diag_kernel(const double* __restrict__ H, int n, double* __restrict__ d) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) d[i] = H[i + static_cast<int64_t>(i) * n];
+}
+
+// abs_tol = c * ||A||_F (fixed order, one CTA)
+__global__ void frob_scale_kernel(const double* __restrict__ A, int64_t len, double c, double* __restrict__ out) {
+  __shared__ double red[8];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < len; i += blockDim.x) s = fma(A[i], A[i], s);
+  s = block_sum<256>(s, red);
+  if (threadIdx.x == 0) *out = c * sqrt(s);
+}
+
 // col_norm[i] = ||B(:, i)||_2 (fixed order), one CTA per column.
 __global__ void col_norms_kernel(const double* __restrict__ B, int L, int n, double* __restrict__ out) {
   __shared__ double red[8];

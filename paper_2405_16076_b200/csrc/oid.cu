@@ -30,6 +30,7 @@ thread_local char g_init_err[512] = "no error";
 constexpr int kGramChunks = 296;
 constexpr int kMaxSweeps = 48;
 constexpr int kNumJacobiUses = 3;
+constexpr int kSymMaxPairs = 33;   // ceil(1024 / 16) / 2 + 1
 
 // ------------------------------------------------------------------ Gauss-256 (reading R2)
 // Inverse normal CDF: Acklam's rational approximation refined by one Halley step on erfc.
@@ -97,7 +98,7 @@ struct Bump {
 struct Layout {
   size_t S, gram, Ypart, k1part, k1npart, gB, gV, mu, mu_sorted, Yc, Tsc, tau, scal, J, tau_old, admit, counts,
       flags, counters, C, SJ, sjB, sjV, sjsig, sjw, sjZ, Sjpinv, Pexp, AJP, G, Gsum, Gpart, cB, cV, csig, cw, cZ, M,
-      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, total;
+      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, total;
 };
 
 int64_t m_local(const oid_params& p) { return p.row_end - p.row_begin; }
@@ -161,6 +162,10 @@ Layout make_layout(const oid_params& p) {
   L.dirty = b.take(t * sizeof(int));
   L.dlist = b.take(t * sizeof(int));
   L.jfro2 = b.take(kNumJacobiUses * d);
+  L.symU = b.take(static_cast<size_t>(kSymMaxPairs) * kSymB * kSymB * d);
+  L.symF = b.take(kSymMaxPairs * sizeof(int));
+  L.symTol = b.take(kNumJacobiUses * d);
+  L.gT = b.take(ell * ell * d);
   L.tc = b.take(k1tc_workspace_bytes(p.ell, p.b_max, m_local(p), p.dtype == OID_F64));
   L.total = b.off;
   return L;
@@ -197,6 +202,7 @@ struct oid_ctx_s {
   int t = 0;
   int num_sms = 0;
   int coop_max = 0;   // max co-resident CTAs of the Jacobi kernel
+  int sym_coop_max = 0;
   int k1_ctas_per_sm = 1;
   double qscale = 0.0;
   int32_t qmag[8] = {0};
@@ -285,6 +291,37 @@ oid_status jacobi(oid_ctx ctx, cudaStream_t st, double* B, int L, int n, double*
     CKL();
   }
   col_norms_kernel<<<n, 256, 0, st>>>(B, L, n, sig);
+  CKL();
+  return OID_OK;
+}
+
+// Symmetric eigen-decomposition by two-sided block Jacobi (sym_bjacobi_kernel): H (n x n) is
+// overwritten by (numerically) diag(mu); V holds the eigenvectors.  warm = true: the caller set
+// H = V0^T A V0 and V = V0.  mu receives diag(H).
+oid_status sym_eig(oid_ctx ctx, cudaStream_t st, double* H, int n, double* V, double* mu, int use, bool warm) {
+  if (n <= 0) return OID_OK;
+  if (!warm) {
+    set_identity_kernel<<<blocks_for(int64_t(n) * n), 256, 0, st>>>(V, n);
+    CKL();
+  }
+  int* counters = ctx->ptr<int>(ctx->L.counters) + use * kMaxSweeps;
+  CK(cudaMemsetAsync(counters, 0, kMaxSweeps * sizeof(int), st));
+  double* tolp = ctx->d(ctx->L.symTol) + use;
+  frob_scale_kernel<<<1, 256, 0, st>>>(H, int64_t(n) * n, 1e-15, tolp);
+  CKL();
+  if (n > 1) {
+    const int nb = (n + kSymW - 1) / kSymW, nbb = nb + (nb & 1), npairs = nbb / 2;
+    const int work = npairs * (npairs + 1) / 2 + npairs * ((n + kSymB - 1) / kSymB);
+    const int grid = std::max(1, std::min(work, ctx->sym_coop_max));
+    double* Ub = ctx->d(ctx->L.symU);
+    int* fl = ctx->ptr<int>(ctx->L.symF);
+    int ni = n, ms = kMaxSweeps;
+    double tol = 1e-14;
+    void* args[] = {&H, &V, &ni, &Ub, &fl, &counters, &ms, &tol, &tolp};
+    CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(sym_bjacobi_kernel), dim3(grid), dim3(256), args, 0, st));
+    CKL();
+  }
+  diag_kernel<<<blocks_for(n), 256, 0, st>>>(H, n, mu);
   CKL();
   return OID_OK;
 }
@@ -401,11 +438,13 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   oid_status s;
   if (ctx->epoch == 0 || ctx->cold_jacobi) {
     CK(cudaMemcpyAsync(ctx->d(L.gB), ctx->d(L.gram), sizeof(double) * ell * ell, cudaMemcpyDeviceToDevice, st));
-    s = jacobi(ctx, st, ctx->d(L.gB), ell, ell, ctx->d(L.gV), ctx->d(L.mu), 0);
-  } else {   // warm start from the previous eigenvectors: B = Gram V_prev
-    s = gemm(ctx, st, false, false, ell, ell, ell, 1.0, ctx->d(L.gram), ell, ctx->d(L.gV), ell, 0.0, ctx->d(L.gB), ell);
+    s = sym_eig(ctx, st, ctx->d(L.gB), ell, ctx->d(L.gV), ctx->d(L.mu), 0, false);
+  } else {   // warm start from the previous eigenvectors: H = V^T Gram V
+    s = gemm(ctx, st, false, false, ell, ell, ell, 1.0, ctx->d(L.gram), ell, ctx->d(L.gV), ell, 0.0, ctx->d(L.gT), ell);
     if (s != OID_OK) return s;
-    s = jacobi(ctx, st, ctx->d(L.gB), ell, ell, ctx->d(L.gV), ctx->d(L.mu), 0, true);
+    s = gemm(ctx, st, true, false, ell, ell, ell, 1.0, ctx->d(L.gV), ell, ctx->d(L.gT), ell, 0.0, ctx->d(L.gB), ell);
+    if (s != OID_OK) return s;
+    s = sym_eig(ctx, st, ctx->d(L.gB), ell, ctx->d(L.gV), ctx->d(L.mu), 0, true);
   }
   if (s != OID_OK) return s;
   lambda_kernel<<<1, 256, 0, st>>>(ctx->d(L.mu), ell, p.k, ctx->d(L.gram), p.lambda, ell, scal, ctx->d(L.mu_sorted));
@@ -529,6 +568,8 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
   int per_sm = 0;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_svd_kernel, 256, 0)) != cudaSuccess) return bad(e);
   ctx->coop_max = std::max(1, per_sm * ctx->num_sms);
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sym_bjacobi_kernel, 256, 0)) != cudaSuccess) return bad(e);
+  ctx->sym_coop_max = std::max(1, std::min(per_sm, 2) * ctx->num_sms);
   {
     const int big = static_cast<int>(prop.sharedMemPerBlockOptin) - 2048;
     if ((e = cudaFuncSetAttribute(bjacobi_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big)) != cudaSuccess) return bad(e);
