@@ -27,7 +27,8 @@ __global__ void fro2_kernel(const double* __restrict__ A, int64_t len, double* _
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(256) dgemm_kernel(int M, int N, int K, double alpha, const double* __restrict__ A,
                                                     int64_t lda, const double* __restrict__ B, int64_t ldb, double beta,
-                                                    double* __restrict__ C, int64_t ldc) {
+                                                    double* __restrict__ C, int64_t ldc, const int* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   __shared__ double As[16][33];
   __shared__ double Bs[16][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // ty: 0..7
@@ -293,7 +294,9 @@ __device__ __forceinline__ int sym_idx(int P, int Q, int i) { return i < kSymW ?
 __global__ void __launch_bounds__(256) sym_bjacobi_kernel(double* __restrict__ H, double* __restrict__ V, int n,
                                                           double* __restrict__ Ubuf, int* __restrict__ flags,
                                                           int* __restrict__ counters, int max_sweeps, double tol,
-                                                          const double* __restrict__ abs_tol_p) {
+                                                          const double* __restrict__ abs_tol_p,
+                                                          const int* __restrict__ gate) {
+  if (gate && *gate == 0) return;   // uniform over the grid: no grid.sync reached
   cg::grid_group grid = cg::this_grid();
   const double abs_tol = *abs_tol_p;
   __shared__ double S[kSymB][kSymP];
@@ -464,13 +467,16 @@ __global__ void __launch_bounds__(256) sym_bjacobi_kernel(double* __restrict__ H
 }
 
 // d[i] = H(i, i)
-__global__ void diag_kernel(const double* __restrict__ H, int n, double* __restrict__ d) {
+__global__ void diag_kernel(const double* __restrict__ H, int n, double* __restrict__ d, const int* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) d[i] = H[i + static_cast<int64_t>(i) * n];
 }
 
 // abs_tol = c * ||A||_F (fixed order, one CTA)
-__global__ void frob_scale_kernel(const double* __restrict__ A, int64_t len, double c, double* __restrict__ out) {
+__global__ void frob_scale_kernel(const double* __restrict__ A, int64_t len, double c, double* __restrict__ out,
+                                  const int* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   __shared__ double red[8];
   double s = 0.0;
   for (int64_t i = threadIdx.x; i < len; i += blockDim.x) s = fma(A[i], A[i], s);

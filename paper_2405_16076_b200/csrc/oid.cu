@@ -20,6 +20,7 @@
 #include "k1_simt.cuh"
 #include "k1_tc.cuh"
 #include "path.cuh"
+#include "tri.cuh"
 
 using namespace oid;
 
@@ -98,7 +99,7 @@ struct Bump {
 struct Layout {
   size_t S, gram, Ypart, k1part, k1npart, gB, gV, mu, mu_sorted, Yc, Tsc, tau, scal, J, tau_old, admit, counts,
       flags, counters, C, SJ, sjB, sjV, sjsig, sjw, sjZ, Sjpinv, Pexp, AJP, G, Gsum, Gpart, cB, cV, csig, cw, cZ, M,
-      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, total;
+      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, total;
 };
 
 int64_t m_local(const oid_params& p) { return p.row_end - p.row_begin; }
@@ -166,6 +167,14 @@ Layout make_layout(const oid_params& p) {
   L.symF = b.take(kSymMaxPairs * sizeof(int));
   L.symTol = b.take(kNumJacobiUses * d);
   L.gT = b.take(ell * ell * d);
+  L.td = b.take(ell * d);
+  L.te = b.take(ell * d);
+  L.Vh = b.take(ell * ell * d);
+  L.tauv = b.take(ell * d);
+  L.gv = b.take((ell + 1) * d);
+  L.gp = b.take((ell + 16) * d);
+  L.gate = b.take(4 * sizeof(int));
+  L.ldl = b.take(2 * ell * d);
   L.tc = b.take(k1tc_workspace_bytes(p.ell, p.b_max, m_local(p), p.dtype == OID_F64));
   L.total = b.off;
   return L;
@@ -246,15 +255,16 @@ namespace {
 
 unsigned blocks_for(int64_t n, int threads = 256) { return static_cast<unsigned>((n + threads - 1) / threads); }
 
-// C = alpha op(A) op(B) + beta C (column-major)
+// C = alpha op(A) op(B) + beta C (column-major); skipped on the device when *gate == 0
 oid_status gemm(oid_ctx ctx, cudaStream_t st, bool ta, bool tb, int M, int N, int K, double alpha, const double* A,
-                int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
+                int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+                const int* gate = nullptr) {
   if (M <= 0 || N <= 0) return OID_OK;
   dim3 grid((M + 31) / 32, (N + 31) / 32);
-  if (!ta && !tb) dgemm_kernel<false, false><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-  else if (!ta && tb) dgemm_kernel<false, true><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-  else if (ta && !tb) dgemm_kernel<true, false><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-  else dgemm_kernel<true, true><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  if (!ta && !tb) dgemm_kernel<false, false><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, gate);
+  else if (!ta && tb) dgemm_kernel<false, true><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, gate);
+  else if (ta && !tb) dgemm_kernel<true, false><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, gate);
+  else dgemm_kernel<true, true><<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, gate);
   CKL();
   return OID_OK;
 }
@@ -298,7 +308,8 @@ oid_status jacobi(oid_ctx ctx, cudaStream_t st, double* B, int L, int n, double*
 // Symmetric eigen-decomposition by two-sided block Jacobi (sym_bjacobi_kernel): H (n x n) is
 // overwritten by (numerically) diag(mu); V holds the eigenvectors.  warm = true: the caller set
 // H = V0^T A V0 and V = V0.  mu receives diag(H).
-oid_status sym_eig(oid_ctx ctx, cudaStream_t st, double* H, int n, double* V, double* mu, int use, bool warm) {
+oid_status sym_eig(oid_ctx ctx, cudaStream_t st, double* H, int n, double* V, double* mu, int use, bool warm,
+                   const int* gate = nullptr) {
   if (n <= 0) return OID_OK;
   if (!warm) {
     set_identity_kernel<<<blocks_for(int64_t(n) * n), 256, 0, st>>>(V, n);
@@ -307,7 +318,7 @@ oid_status sym_eig(oid_ctx ctx, cudaStream_t st, double* H, int n, double* V, do
   int* counters = ctx->ptr<int>(ctx->L.counters) + use * kMaxSweeps;
   CK(cudaMemsetAsync(counters, 0, kMaxSweeps * sizeof(int), st));
   double* tolp = ctx->d(ctx->L.symTol) + use;
-  frob_scale_kernel<<<1, 256, 0, st>>>(H, int64_t(n) * n, 1e-15, tolp);
+  frob_scale_kernel<<<1, 256, 0, st>>>(H, int64_t(n) * n, 1e-15, tolp, gate);
   CKL();
   if (n > 1) {
     const int nb = (n + kSymW - 1) / kSymW, nbb = nb + (nb & 1), npairs = nbb / 2;
@@ -317,11 +328,11 @@ oid_status sym_eig(oid_ctx ctx, cudaStream_t st, double* H, int n, double* V, do
     int* fl = ctx->ptr<int>(ctx->L.symF);
     int ni = n, ms = kMaxSweeps;
     double tol = 1e-14;
-    void* args[] = {&H, &V, &ni, &Ub, &fl, &counters, &ms, &tol, &tolp};
+    void* args[] = {&H, &V, &ni, &Ub, &fl, &counters, &ms, &tol, &tolp, &gate};
     CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(sym_bjacobi_kernel), dim3(grid), dim3(256), args, 0, st));
     CKL();
   }
-  diag_kernel<<<blocks_for(n), 256, 0, st>>>(H, n, mu);
+  diag_kernel<<<blocks_for(n), 256, 0, st>>>(H, n, mu, gate);
   CKL();
   return OID_OK;
 }
@@ -434,29 +445,54 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   gram_update_kernel<<<blocks_for(int64_t(ell) * ell), 256, 0, st>>>(Yp, ell, nc, ctx->d(L.gram), ctx->d(L.S), ctx->n_obs,
                                                                     scal);
   CKL();
-  // A4: eigen-decomposition of the Gram (one-sided Jacobi on a copy), lambda
+  // A4: spectrum of the Gram and lambda; A5: ridge scores
   oid_status s;
-  if (ctx->epoch == 0 || ctx->cold_jacobi) {
-    CK(cudaMemcpyAsync(ctx->d(L.gB), ctx->d(L.gram), sizeof(double) * ell * ell, cudaMemcpyDeviceToDevice, st));
-    s = sym_eig(ctx, st, ctx->d(L.gB), ell, ctx->d(L.gV), ctx->d(L.mu), 0, false);
-  } else {   // warm start from the previous eigenvectors: H = V^T Gram V
+  const int ns = t + nc;
+  gather_scored_kernel<<<blocks_for(int64_t(ell) * ns), 256, 0, st>>>(ctx->d(L.S), ctx->ptr<int64_t>(L.J), t, Yp, nc, ell,
+                                                                      ctx->d(L.Yc));
+  CKL();
+  int* gate = ctx->ptr<int>(L.gate);
+  if (ell <= kTriMaxN && !ctx->cold_jacobi) {
+    // tridiagonal fast path (tri.cuh); the eigenvector path below runs only when gate[1] is set
+    const size_t smem = sizeof(double) * (static_cast<size_t>((ell + kTriCtas - 1) / kTriCtas) * ell + 2 * ell);
+    tridiag_cluster_kernel<<<kTriCtas, 256, smem, st>>>(ctx->d(L.gram), ell, ctx->d(L.td), ctx->d(L.te), ctx->d(L.Vh),
+                                                        ctx->d(L.tauv), ctx->d(L.gv), ctx->d(L.gp));
+    CKL();
+    multisect_kernel<<<(ell * 32 + 255) / 256, 256, sizeof(double) * 2 * ell, st>>>(ctx->d(L.td), ctx->d(L.te), ell,
+                                                                                  ctx->d(L.mu));
+    CKL();
+    lambda_sorted_kernel<<<1, 256, 0, st>>>(ctx->d(L.mu), ell, p.k, ctx->d(L.gram), p.lambda, ell, scal, gate,
+                                            ctx->d(L.td), ctx->d(L.te), ctx->d(L.ldl), 1);
+    CKL();
+    tri_scores_kernel<<<ns, 256, 0, st>>>(ctx->d(L.Yc), ell, ns, ctx->d(L.Vh), ctx->d(L.tauv), ctx->d(L.ldl), gate,
+                                          ctx->d(L.tau));
+    CKL();
+    const int* g1 = gate + 1;
+    s = gemm(ctx, st, false, false, ell, ell, ell, 1.0, ctx->d(L.gram), ell, ctx->d(L.gV), ell, 0.0, ctx->d(L.gT), ell, g1);
+    if (s != OID_OK) return s;
+    s = gemm(ctx, st, true, false, ell, ell, ell, 1.0, ctx->d(L.gV), ell, ctx->d(L.gT), ell, 0.0, ctx->d(L.gB), ell, g1);
+    if (s != OID_OK) return s;
+    s = sym_eig(ctx, st, ctx->d(L.gB), ell, ctx->d(L.gV), ctx->d(L.mu), 0, true, g1);
+    if (s != OID_OK) return s;
+    s = gemm(ctx, st, true, false, ell, ns, ell, 1.0, ctx->d(L.gV), ell, ctx->d(L.Yc), ell, 0.0, ctx->d(L.Tsc), ell, g1);
+    if (s != OID_OK) return s;
+    scores_kernel<<<ns, 256, 0, st>>>(ctx->d(L.Tsc), ctx->d(L.mu), ell, ns, scal, ctx->d(L.tau), g1);
+    CKL();
+  } else {
+    // eigenvector path only: warm-started two-sided block Jacobi (gV starts as the identity)
     s = gemm(ctx, st, false, false, ell, ell, ell, 1.0, ctx->d(L.gram), ell, ctx->d(L.gV), ell, 0.0, ctx->d(L.gT), ell);
     if (s != OID_OK) return s;
     s = gemm(ctx, st, true, false, ell, ell, ell, 1.0, ctx->d(L.gV), ell, ctx->d(L.gT), ell, 0.0, ctx->d(L.gB), ell);
     if (s != OID_OK) return s;
     s = sym_eig(ctx, st, ctx->d(L.gB), ell, ctx->d(L.gV), ctx->d(L.mu), 0, true);
+    if (s != OID_OK) return s;
+    lambda_kernel<<<1, 256, 0, st>>>(ctx->d(L.mu), ell, p.k, ctx->d(L.gram), p.lambda, ell, scal, ctx->d(L.mu_sorted));
+    CKL();
+    s = gemm(ctx, st, true, false, ell, ns, ell, 1.0, ctx->d(L.gV), ell, ctx->d(L.Yc), ell, 0.0, ctx->d(L.Tsc), ell);
+    if (s != OID_OK) return s;
+    scores_kernel<<<ns, 256, 0, st>>>(ctx->d(L.Tsc), ctx->d(L.mu), ell, ns, scal, ctx->d(L.tau), nullptr);
+    CKL();
   }
-  if (s != OID_OK) return s;
-  lambda_kernel<<<1, 256, 0, st>>>(ctx->d(L.mu), ell, p.k, ctx->d(L.gram), p.lambda, ell, scal, ctx->d(L.mu_sorted));
-  CKL();
-  // A5: ridge scores of the basis slots and the candidates
-  gather_scored_kernel<<<blocks_for(int64_t(ell) * (t + nc)), 256, 0, st>>>(ctx->d(L.S), ctx->ptr<int64_t>(L.J), t, Yp, nc,
-                                                                           ell, ctx->d(L.Yc));
-  CKL();
-  s = gemm(ctx, st, true, false, ell, t + nc, ell, 1.0, ctx->d(L.gV), ell, ctx->d(L.Yc), ell, 0.0, ctx->d(L.Tsc), ell);
-  if (s != OID_OK) return s;
-  scores_kernel<<<t + nc, 256, 0, st>>>(ctx->d(L.Tsc), ctx->d(L.mu), ell, t + nc, scal, ctx->d(L.tau));
-  CKL();
   // A6: selection / replacement
   select_kernel<<<1, 32, 0, st>>>(ctx->ptr<int64_t>(L.J), ctx->d(L.tau_old), ctx->d(L.tau), Yp + int64_t(ell) * nc, t, nc,
                                   ctx->factor, static_cast<uint32_t>(ctx->epoch), ctx->n_obs, ctx->key0, ctx->key1,
@@ -580,6 +616,13 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
     BG_ATTR(float, 1); BG_ATTR(float, 2); BG_ATTR(float, 4); BG_ATTR(float, 7); BG_ATTR(float, 13);
 #undef BG_ATTR
   }
+  if (p->ell <= kTriMaxN) {
+    const int tri_smem = static_cast<int>(sizeof(double) * (((p->ell + kTriCtas - 1) / kTriCtas) * p->ell + 2 * p->ell));
+    if ((e = cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
+      return bad(e);
+    if ((e = cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tri_smem)) != cudaSuccess)
+      return bad(e);
+  }
   ctx->k1_ctas_per_sm = 1;
   ctx->cold_jacobi = getenv("OID_JACOBI_COLD") && atoi(getenv("OID_JACOBI_COLD")) != 0;
   ctx->tc_ok = (prop.major == 10 && prop.minor == 0) && k1tc_supported(p->ell, p->b_max, p->dtype == OID_F64);
@@ -593,6 +636,10 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
   if ((e = cudaMemcpyAsync(ctx->ws + L.tau_old, ones.data(), sizeof(double) * ctx->t, cudaMemcpyHostToDevice, st)) != cudaSuccess)
     return bad(e);
   if ((e = cudaMemsetAsync(ctx->ws + L.gram, 0, sizeof(double) * p->ell * p->ell, st)) != cudaSuccess) return bad(e);
+  if ((e = cudaMemsetAsync(ctx->ws + L.Vh, 0, sizeof(double) * p->ell * p->ell, st)) != cudaSuccess) return bad(e);
+  set_identity_kernel<<<static_cast<unsigned>((int64_t(p->ell) * p->ell + 255) / 256), 256, 0, st>>>(
+      reinterpret_cast<double*>(ctx->ws + L.gV), p->ell);
+  if ((e = cudaGetLastError()) != cudaSuccess) return bad(e);
   double sc[SC_COUNT] = {0};
   sc[SC_MINMARGIN] = INFINITY;
   sc[SC_KAPPA] = 1.0;

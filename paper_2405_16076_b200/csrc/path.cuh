@@ -65,7 +65,8 @@ __global__ void gather_scored_kernel(const double* __restrict__ S, const int64_t
 // tau_j = sum_{i: mu_i + shift > 1e-12 dmax} T(i, j)^2 / (mu_i + shift), T = W^T Yc
 // (eq:sketch_ridge_leverage_score; readings R3, R9).  One CTA per column.
 __global__ void scores_kernel(const double* __restrict__ T, const double* __restrict__ mu, int ell, int ncol,
-                              const double* __restrict__ scal, double* __restrict__ tau) {
+                              const double* __restrict__ scal, double* __restrict__ tau, const int* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   __shared__ double red[8];
   const int j = blockIdx.x;
   if (j >= ncol) return;
