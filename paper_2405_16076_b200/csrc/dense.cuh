@@ -14,7 +14,9 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // out = ||A||_F^2 over len doubles (one CTA, fixed order)
-__global__ void fro2_kernel(const double* __restrict__ A, int64_t len, double* __restrict__ out) {
+__global__ void fro2_kernel(const double* __restrict__ A, int64_t len, double* __restrict__ out,
+                            const int* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   __shared__ double red[8];
   double s = 0.0;
   for (int64_t i = threadIdx.x; i < len; i += blockDim.x) s = fma(A[i], A[i], s);
@@ -164,7 +166,8 @@ __global__ void __launch_bounds__(256) jacobi_svd_kernel(double* __restrict__ B,
 template <int W>
 __global__ void __launch_bounds__(32 * W) bjacobi_kernel(double* __restrict__ B, int L, int n, double* __restrict__ V,
                                                          int* __restrict__ counters, int max_sweeps, double tol,
-                                                         const double* __restrict__ fro2) {
+                                                         const double* __restrict__ fro2, const int* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double sm[];
   double* Bs = sm;                       // [2W][L]
@@ -485,7 +488,9 @@ __global__ void frob_scale_kernel(const double* __restrict__ A, int64_t len, dou
 }
 
 // col_norm[i] = ||B(:, i)||_2 (fixed order), one CTA per column.
-__global__ void col_norms_kernel(const double* __restrict__ B, int L, int n, double* __restrict__ out) {
+__global__ void col_norms_kernel(const double* __restrict__ B, int L, int n, double* __restrict__ out,
+                                 const int* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   __shared__ double red[8];
   const int i = blockIdx.x;
   if (i >= n) return;
@@ -495,7 +500,8 @@ __global__ void col_norms_kernel(const double* __restrict__ B, int L, int n, dou
   if (threadIdx.x == 0) out[i] = sqrt(s);
 }
 
-__global__ void set_identity_kernel(double* __restrict__ V, int n) {
+__global__ void set_identity_kernel(double* __restrict__ V, int n, const int* __restrict__ gate = nullptr) {
+  if (gate && *gate == 0) return;
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx < static_cast<int64_t>(n) * n) V[idx] = (idx % n == idx / n) ? 1.0 : 0.0;
 }
@@ -503,7 +509,9 @@ __global__ void set_identity_kernel(double* __restrict__ V, int n) {
 // Z(i, r) = w_i * B(r, i) with w_i = 1/sigma_i^2 if sigma_i > rcond * max sigma else 0
 // (pseudo-inverse assembly pinv = V Z, reading R9).  Z is n x L.  One CTA.
 __global__ void pinv_weights_kernel(const double* __restrict__ sig, int n, double rcond, double* __restrict__ w,
-                                    double* __restrict__ kappa_out, unsigned* __restrict__ flags, unsigned flagbit) {
+                                    double* __restrict__ kappa_out, unsigned* __restrict__ flags, unsigned flagbit,
+                                    const int* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   __shared__ double red[8];
   double mx = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) mx = fmax(mx, sig[i]);
@@ -525,7 +533,8 @@ __global__ void pinv_weights_kernel(const double* __restrict__ sig, int n, doubl
 }
 
 __global__ void scale_transpose_kernel(const double* __restrict__ B, int L, int n, const double* __restrict__ w,
-                                       double* __restrict__ Z) {
+                                       double* __restrict__ Z, const int* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= static_cast<int64_t>(L) * n) return;
   const int i = static_cast<int>(idx % n), r = static_cast<int>(idx / n);   // Z(i, r), ld = n

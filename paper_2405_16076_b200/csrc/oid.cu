@@ -99,7 +99,7 @@ struct Bump {
 struct Layout {
   size_t S, gram, Ypart, k1part, k1npart, gB, gV, mu, mu_sorted, Yc, Tsc, tau, scal, J, tau_old, admit, counts,
       flags, counters, C, SJ, sjB, sjV, sjsig, sjw, sjZ, Sjpinv, Pexp, AJP, G, Gsum, Gpart, cB, cV, csig, cw, cZ, M,
-      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, total;
+      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, sjG, cG, total;
 };
 
 int64_t m_local(const oid_params& p) { return p.row_end - p.row_begin; }
@@ -173,7 +173,9 @@ Layout make_layout(const oid_params& p) {
   L.tauv = b.take(ell * d);
   L.gv = b.take((ell + 1) * d);
   L.gp = b.take((ell + 16) * d);
-  L.gate = b.take(4 * sizeof(int));
+  L.gate = b.take(8 * sizeof(int));
+  L.sjG = b.take(t * t * d);
+  L.cG = b.take(std::max<size_t>(1, std::min(l1, l2) * std::min(l1, l2)) * d);
   L.ldl = b.take(2 * ell * d);
   L.tc = b.take(k1tc_workspace_bytes(p.ell, p.b_max, m_local(p), p.dtype == OID_F64));
   L.total = b.off;
@@ -272,10 +274,10 @@ oid_status gemm(oid_ctx ctx, cudaStream_t st, bool ta, bool tb, int M, int N, in
 // Block one-sided Jacobi SVD of B (L x n) in place.  warm = false: V <- I first (B = A);
 // warm = true: V holds an orthogonal start and the caller has set B = A V.  sig = column norms.
 oid_status jacobi(oid_ctx ctx, cudaStream_t st, double* B, int L, int n, double* V, double* sig, int use,
-                  bool warm = false) {
+                  bool warm = false, const int* gate = nullptr) {
   if (n <= 0) return OID_OK;
   if (!warm) {
-    set_identity_kernel<<<blocks_for(int64_t(n) * n), 256, 0, st>>>(V, n);
+    set_identity_kernel<<<blocks_for(int64_t(n) * n), 256, 0, st>>>(V, n, gate);
     CKL();
   }
   int* counters = ctx->ptr<int>(ctx->L.counters) + use * kMaxSweeps;
@@ -291,16 +293,51 @@ oid_status jacobi(oid_ctx ctx, cudaStream_t st, double* B, int L, int n, double*
     const int npairs = (nb + (nb & 1)) / 2;
     const int grid = std::max(1, std::min(npairs, std::max(1, per_sm) * ctx->num_sms));
     double* fro2 = ctx->d(ctx->L.jfro2) + use;
-    fro2_kernel<<<1, 256, 0, st>>>(B, int64_t(L) * n, fro2);
+    fro2_kernel<<<1, 256, 0, st>>>(B, int64_t(L) * n, fro2, gate);
     CKL();
     int Li = L, ni = n, ms = kMaxSweeps;
     // relative orthogonality target: well above the dot-product rounding level (~L eps)
     double tol = 4e-14 * std::max(1.0, std::sqrt(static_cast<double>(L) / 16.0));
-    void* args[] = {&B, &Li, &ni, &V, &counters, &ms, &tol, &fro2};
+    void* args[] = {&B, &Li, &ni, &V, &counters, &ms, &tol, &fro2, &gate};
     CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(32 * Wd), args, smem, st));
     CKL();
   }
-  col_norms_kernel<<<n, 256, 0, st>>>(B, L, n, sig);
+  col_norms_kernel<<<n, 256, 0, st>>>(B, L, n, sig, gate);
+  CKL();
+  return OID_OK;
+}
+
+// pinv(A) for A = B_orig (L x n) given the Jacobi result (B, V, sig): out (n x L) = V diag(w) B^T
+oid_status pinv_assemble(oid_ctx ctx, cudaStream_t st, const double* B, int L, int n, const double* V,
+                         const double* sig, double* w, double* Z, double* out, double* kappa, unsigned flagbit,
+                         const int* gate = nullptr) {
+  if (n <= 0 || L <= 0) return OID_OK;
+  pinv_weights_kernel<<<1, 256, 0, st>>>(sig, n, 1e-12, w, kappa, flagbit ? ctx->ptr<unsigned>(ctx->L.flags) : nullptr,
+                                         flagbit, gate);
+  CKL();
+  scale_transpose_kernel<<<blocks_for(int64_t(L) * n), 256, 0, st>>>(B, L, n, w, Z, gate);
+  CKL();
+  return gemm(ctx, st, false, false, n, L, n, 1.0, V, n, Z, n, 0.0, out, n, gate);
+}
+
+// X = A^-1 R for a symmetric positive definite n x n A (overwritten) by the cluster
+// tridiagonalisation when kappa(A) <= kmax2 (gate[0] set on the device); otherwise gate[1] is set
+// and nothing is written (the caller's pseudo-inverse fallback runs).  n <= kTriMaxN.
+oid_status spd_solve(oid_ctx ctx, cudaStream_t st, const double* A, int n, const double* R, int64_t ldr, bool in_t,
+                     int nrhs, double* X, int64_t ldx, bool out_t, double kmax2, int* gate, double* kappa_out) {
+  const Layout& L = ctx->L;
+  const size_t smem = sizeof(double) * (static_cast<size_t>((n + kTriCtas - 1) / kTriCtas) * n + 2 * n);
+  tridiag_cluster_kernel<<<kTriCtas, 256, smem, st>>>(A, n, ctx->d(L.td), ctx->d(L.te), ctx->d(L.Vh), ctx->d(L.tauv),
+                                                      ctx->d(L.gv), ctx->d(L.gp));
+  CKL();
+  multisect_kernel<<<(n * 32 + 255) / 256, 256, sizeof(double) * 2 * n, st>>>(ctx->d(L.td), ctx->d(L.te), n,
+                                                                            ctx->d(L.mu_sorted));
+  CKL();
+  spd_gate_kernel<<<1, 32, 0, st>>>(ctx->d(L.mu_sorted), n, kmax2, ctx->d(L.td), ctx->d(L.te), ctx->d(L.ldl), gate,
+                                    kappa_out);
+  CKL();
+  tri_solve_kernel<<<nrhs, 256, 0, st>>>(R, ldr, in_t ? 1 : 0, n, nrhs, ctx->d(L.Vh), ctx->d(L.tauv), ctx->d(L.ldl), gate, X, ldx,
+                                         out_t ? 1 : 0);
   CKL();
   return OID_OK;
 }
@@ -337,17 +374,6 @@ oid_status sym_eig(oid_ctx ctx, cudaStream_t st, double* H, int n, double* V, do
   return OID_OK;
 }
 
-// pinv(A) for A = B_orig (L x n) given the Jacobi result (B, V, sig): out (n x L) = V diag(w) B^T
-oid_status pinv_assemble(oid_ctx ctx, cudaStream_t st, const double* B, int L, int n, const double* V,
-                         const double* sig, double* w, double* Z, double* out, double* kappa, unsigned flagbit) {
-  if (n <= 0 || L <= 0) return OID_OK;
-  pinv_weights_kernel<<<1, 256, 0, st>>>(sig, n, 1e-12, w, kappa, flagbit ? ctx->ptr<unsigned>(ctx->L.flags) : nullptr,
-                                         flagbit);
-  CKL();
-  scale_transpose_kernel<<<blocks_for(int64_t(L) * n), 256, 0, st>>>(B, L, n, w, Z);
-  CKL();
-  return gemm(ctx, st, false, false, n, L, n, 1.0, V, n, Z, n, 0.0, out, n);
-}
 
 struct EvScope {
   oid_ctx ctx;
@@ -510,20 +536,31 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
     CKL();
   }
   ctx->n_obs += nc;
-  // A8: Alg 4 kept implicit: S_J^+ = V diag(1/sigma^2) B^T from the SVD of S_J
+  // A8: Alg 4 kept implicit: S_J^+ per epoch.  Fast path: S_J^+ = (S_J^T S_J)^-1 S_J^T
+  // by the cluster tridiagonalisation when kappa(S_J) <= 1e5 (no R9 cutoff can act); else the
+  // one-sided Jacobi SVD pseudo-inverse (gated on the device).
   gather_sj_kernel<<<blocks_for(int64_t(ell) * t), 256, 0, st>>>(ctx->d(L.S), ctx->ptr<int64_t>(L.J), t, ell, ctx->d(L.SJ));
   CKL();
-  if (ctx->epoch == 0 || ctx->cold_jacobi) {
-    CK(cudaMemcpyAsync(ctx->d(L.sjB), ctx->d(L.SJ), sizeof(double) * ell * t, cudaMemcpyDeviceToDevice, st));
-    s = jacobi(ctx, st, ctx->d(L.sjB), ell, t, ctx->d(L.sjV), ctx->d(L.sjsig), 1);
-  } else {   // warm start: B = S_J V_prev
-    s = gemm(ctx, st, false, false, ell, t, t, 1.0, ctx->d(L.SJ), ell, ctx->d(L.sjV), t, 0.0, ctx->d(L.sjB), ell);
+  int* sjgate = ctx->ptr<int>(L.gate) + 2;
+  if (t <= kTriMaxN) {
+    s = gemm(ctx, st, true, false, t, t, ell, 1.0, ctx->d(L.SJ), ell, ctx->d(L.SJ), ell, 0.0, ctx->d(L.sjG), t);
     if (s != OID_OK) return s;
-    s = jacobi(ctx, st, ctx->d(L.sjB), ell, t, ctx->d(L.sjV), ctx->d(L.sjsig), 1, true);
+    fill_vacant_diag_kernel<<<1, 256, 0, st>>>(ctx->d(L.sjG), t, ctx->ptr<int64_t>(L.J));
+    CKL();
+    s = spd_solve(ctx, st, ctx->d(L.sjG), t, ctx->d(L.SJ), ell, true, ell, ctx->d(L.Sjpinv), t, false, 1e10, sjgate,
+                  scal + SC_KAPPA);
+    if (s != OID_OK) return s;
+  } else {
+    set_flag_kernel<<<1, 1, 0, st>>>(sjgate, 0, 1);
+    CKL();
   }
+  const int* fb = sjgate + 1;
+  s = gemm(ctx, st, false, false, ell, t, t, 1.0, ctx->d(L.SJ), ell, ctx->d(L.sjV), t, 0.0, ctx->d(L.sjB), ell, fb);
+  if (s != OID_OK) return s;
+  s = jacobi(ctx, st, ctx->d(L.sjB), ell, t, ctx->d(L.sjV), ctx->d(L.sjsig), 1, true, fb);
   if (s != OID_OK) return s;
   s = pinv_assemble(ctx, st, ctx->d(L.sjB), ell, t, ctx->d(L.sjV), ctx->d(L.sjsig), ctx->d(L.sjw), ctx->d(L.sjZ),
-                    ctx->d(L.Sjpinv), scal + SC_KAPPA, OID_FLAG_SJ_RANK_DEFICIENT);
+                    ctx->d(L.Sjpinv), scal + SC_KAPPA, OID_FLAG_SJ_RANK_DEFICIENT, fb);
   if (s != OID_OK) return s;
   ctx->epoch += 1;
   ctx->estimate_ready = true;
@@ -639,6 +676,8 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
   if ((e = cudaMemsetAsync(ctx->ws + L.Vh, 0, sizeof(double) * p->ell * p->ell, st)) != cudaSuccess) return bad(e);
   set_identity_kernel<<<static_cast<unsigned>((int64_t(p->ell) * p->ell + 255) / 256), 256, 0, st>>>(
       reinterpret_cast<double*>(ctx->ws + L.gV), p->ell);
+  set_identity_kernel<<<static_cast<unsigned>((int64_t(p->k) * p->k + 255) / 256), 256, 0, st>>>(
+      reinterpret_cast<double*>(ctx->ws + L.sjV), p->k);
   if ((e = cudaGetLastError()) != cudaSuccess) return bad(e);
   double sc[SC_COUNT] = {0};
   sc[SC_MINMARGIN] = INFINITY;
@@ -765,10 +804,22 @@ oid_status oid_estimate_end(oid_ctx ctx, double* out_dev, void* stream) {
     // M = (Omega1 A (Omega2 A_J P)^T)^+   
     s = gemm(ctx, st, false, true, l1, l2, n, 1.0, S, ell, AJP + l1, ell, 0.0, ctx->d(L.cB), l1);
     if (s != OID_OK) return s;
-    s = jacobi(ctx, st, ctx->d(L.cB), l1, l2, ctx->d(L.cV), ctx->d(L.csig), 2);
+    // M = B^+ (l2 x l1).  Fast path (l1 <= l2, kappa(B) <= 1e5): M = ((B B^T)^-1 B)^T by the cluster
+    // tridiagonalisation; else the one-sided Jacobi SVD pseudo-inverse (R9), gated on the device.
+    int* cgate = ctx->ptr<int>(L.gate) + 4;
+    if (l1 <= l2 && l1 <= kTriMaxN) {
+      s = gemm(ctx, st, false, true, l1, l1, l2, 1.0, ctx->d(L.cB), l1, ctx->d(L.cB), l1, 0.0, ctx->d(L.cG), l1);
+      if (s != OID_OK) return s;
+      s = spd_solve(ctx, st, ctx->d(L.cG), l1, ctx->d(L.cB), l1, false, l2, ctx->d(L.M), l2, true, 1e10, cgate, nullptr);
+      if (s != OID_OK) return s;
+    } else {
+      set_flag_kernel<<<1, 1, 0, st>>>(cgate, 0, 1);
+      CKL();
+    }
+    s = jacobi(ctx, st, ctx->d(L.cB), l1, l2, ctx->d(L.cV), ctx->d(L.csig), 2, false, cgate + 1);
     if (s != OID_OK) return s;
     s = pinv_assemble(ctx, st, ctx->d(L.cB), l1, l2, ctx->d(L.cV), ctx->d(L.csig), ctx->d(L.cw), ctx->d(L.cZ), ctx->d(L.M),
-                      nullptr, 0);
+                      nullptr, 0, cgate + 1);
     if (s != OID_OK) return s;
     // term1 = tr(M (Omega1 A P^T) G (Omega2 A P^T)^T)
     s = gemm(ctx, st, false, true, l1, t, n, 1.0, S, ell, P, t, 0.0, ctx->d(L.X1), l1);

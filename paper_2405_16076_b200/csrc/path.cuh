@@ -336,4 +336,10 @@ __global__ void sum_chunks_kernel(const double* __restrict__ part, int nchunks, 
   out[idx] = s;
 }
 
+// gate[0] = a, gate[1] = b
+__global__ void set_flag_kernel(int* __restrict__ gate, int a, int b) {
+  gate[0] = a;
+  gate[1] = b;
+}
+
 }  // namespace oid

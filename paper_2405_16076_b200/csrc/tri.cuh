@@ -276,4 +276,91 @@ __global__ void __launch_bounds__(256) tri_scores_kernel(const double* __restric
   }
 }
 
+// SPD solve gate for A = Q T Q^T (tridiagonalised): mu = eigenvalues (descending).  gate[0] = 1
+// when mu_min > 0 and mu_max <= kmax2 mu_min (no pseudo-inverse cutoff can act, reading R9, and
+// the normal-equation error kmax2 eps stays far below the 1e-5 parity bar); then ldl holds the
+// LDL^T of T (1/D_j, L_j) and *kappa_out = sqrt(mu_max / mu_min).  gate[1] = !gate[0].
+__global__ void spd_gate_kernel(const double* __restrict__ mu, int n, double kmax2, const double* __restrict__ d,
+                                const double* __restrict__ e, double* __restrict__ ldl, int* __restrict__ gate,
+                                double* __restrict__ kappa_out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double mx = n > 0 ? mu[0] : 0.0, mn = n > 0 ? mu[n - 1] : 0.0;
+  const int ok = n > 0 && mn > 0.0 && mx <= kmax2 * mn;
+  gate[0] = ok;
+  gate[1] = !ok;
+  if (!ok) return;
+  if (kappa_out) *kappa_out = sqrt(mx / mn);
+  double Dj = d[0];
+  ldl[0] = 1.0 / Dj;
+  for (int j = 1; j < n; ++j) {
+    const double Lj = e[j - 1] / Dj;
+    ldl[n + j - 1] = Lj;
+    Dj = d[j] - Lj * e[j - 1];
+    ldl[j] = 1.0 / Dj;
+  }
+}
+
+// X(:, c) = A^-1 R(:, c) with A = Q T Q^T: z = Q^T r, solve T u = z (LDL^T), x = Q u.
+// One CTA per right-hand side; runs when gate[0] != 0.  in_transposed: R(i, c) = R[c + i ldr];
+// out_transposed: write X^T (nrhs x n).
+__global__ void __launch_bounds__(256) tri_solve_kernel(const double* __restrict__ R, int64_t ldr, int in_transposed,
+                                                        int n, int nrhs,
+                                                        const double* __restrict__ Vh, const double* __restrict__ tauv,
+                                                        const double* __restrict__ ldl, const int* __restrict__ gate,
+                                                        double* __restrict__ X, int64_t ldx, int out_transposed) {
+  if (gate[0] == 0) return;
+  __shared__ double z[kTriMaxN];
+  __shared__ double red[8];
+  const int c = blockIdx.x, tid = threadIdx.x;
+  if (c >= nrhs) return;
+  for (int i = tid; i < n; i += 256)
+    z[i] = in_transposed ? R[c + static_cast<int64_t>(i) * ldr] : R[static_cast<int64_t>(c) * ldr + i];
+  __syncthreads();
+  for (int k = 0; k < n - 2; ++k) {                 // z = H_{n-3} ... H_0 r
+    const double tk = tauv[k];
+    if (tk == 0.0) continue;
+    const double* v = Vh + static_cast<int64_t>(k) * n;
+    double s = 0.0;
+    for (int i = k + 1 + tid; i < n; i += 256) s = fma(v[i], z[i], s);
+    s = block_sum<256>(s, red);
+    for (int i = k + 1 + tid; i < n; i += 256) z[i] = fma(-tk * s, v[i], z[i]);
+    __syncthreads();
+  }
+  if (tid == 0) {                                   // T u = z by LDL^T
+    for (int i = 1; i < n; ++i) z[i] -= ldl[n + i - 1] * z[i - 1];
+    for (int i = 0; i < n; ++i) z[i] *= ldl[i];
+    for (int i = n - 2; i >= 0; --i) z[i] -= ldl[n + i] * z[i + 1];
+  }
+  __syncthreads();
+  for (int k = n - 3; k >= 0; --k) {               // x = H_0 ... H_{n-3} u
+    const double tk = tauv[k];
+    if (tk == 0.0) continue;
+    const double* v = Vh + static_cast<int64_t>(k) * n;
+    double s = 0.0;
+    for (int i = k + 1 + tid; i < n; i += 256) s = fma(v[i], z[i], s);
+    s = block_sum<256>(s, red);
+    for (int i = k + 1 + tid; i < n; i += 256) z[i] = fma(-tk * s, v[i], z[i]);
+    __syncthreads();
+  }
+  for (int i = tid; i < n; i += 256) {
+    if (out_transposed) X[static_cast<int64_t>(i) * ldx + c] = z[i];
+    else X[static_cast<int64_t>(c) * ldx + i] = z[i];
+  }
+}
+
+// A(i, i) = cval for zero rows/columns of a Gram (vacant basis slots, reading R10) where cval =
+// max diagonal, so the inverse leaves their coefficient rows zero and the spectrum bounds of the
+// occupied block are unchanged.
+__global__ void fill_vacant_diag_kernel(double* __restrict__ A, int n, const int64_t* __restrict__ J) {
+  __shared__ double mx;
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int i = 0; i < n; ++i) m = fmax(m, A[i + static_cast<int64_t>(i) * n]);
+    mx = m > 0.0 ? m : 1.0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    if (J[i] < 0) A[i + static_cast<int64_t>(i) * n] = mx;
+}
+
 }  // namespace oid
