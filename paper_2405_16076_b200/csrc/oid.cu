@@ -32,6 +32,7 @@ constexpr int kGramChunks = 296;
 constexpr int kMaxSweeps = 48;
 constexpr int kNumJacobiUses = 3;
 constexpr int kSymMaxPairs = 33;   // ceil(1024 / 16) / 2 + 1
+constexpr size_t kSmallSvdSmem = 200 * 1024;
 
 // ------------------------------------------------------------------ Gauss-256 (reading R2)
 // Inverse normal CDF: Acklam's rational approximation refined by one Halley step on erfc.
@@ -99,7 +100,7 @@ struct Bump {
 struct Layout {
   size_t S, gram, Ypart, k1part, k1npart, gB, gV, mu, mu_sorted, Yc, Tsc, tau, scal, J, tau_old, admit, counts,
       flags, counters, C, SJ, sjB, sjV, sjsig, sjw, sjZ, Sjpinv, Pexp, AJP, G, Gsum, Gpart, cB, cV, csig, cw, cZ, M,
-      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, sjG, cG, total;
+      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, sjG, cG, cBt, cZ2, total;
 };
 
 int64_t m_local(const oid_params& p) { return p.row_end - p.row_begin; }
@@ -175,6 +176,8 @@ Layout make_layout(const oid_params& p) {
   L.gp = b.take((ell + 16) * d);
   L.gate = b.take(8 * sizeof(int));
   L.sjG = b.take(t * t * d);
+  L.cBt = b.take(std::max<size_t>(1, l1 * l2) * d);
+  L.cZ2 = b.take(std::max<size_t>(1, l1 * l2) * d);
   L.cG = b.take(std::max<size_t>(1, std::min(l1, l2) * std::min(l1, l2)) * d);
   L.ldl = b.take(2 * ell * d);
   L.tc = b.take(k1tc_workspace_bytes(p.ell, p.b_max, m_local(p), p.dtype == OID_F64));
@@ -326,7 +329,7 @@ oid_status pinv_assemble(oid_ctx ctx, cudaStream_t st, const double* B, int L, i
 oid_status spd_solve(oid_ctx ctx, cudaStream_t st, const double* A, int n, const double* R, int64_t ldr, bool in_t,
                      int nrhs, double* X, int64_t ldx, bool out_t, double kmax2, int* gate, double* kappa_out) {
   const Layout& L = ctx->L;
-  const size_t smem = sizeof(double) * (static_cast<size_t>((n + kTriCtas - 1) / kTriCtas) * n + 2 * n);
+  const size_t smem = sizeof(double) * (0);
   tridiag_cluster_kernel<<<kTriCtas, 256, smem, st>>>(A, n, ctx->d(L.td), ctx->d(L.te), ctx->d(L.Vh), ctx->d(L.tauv),
                                                       ctx->d(L.gv), ctx->d(L.gp));
   CKL();
@@ -336,7 +339,7 @@ oid_status spd_solve(oid_ctx ctx, cudaStream_t st, const double* A, int n, const
   spd_gate_kernel<<<1, 32, 0, st>>>(ctx->d(L.mu_sorted), n, kmax2, ctx->d(L.td), ctx->d(L.te), ctx->d(L.ldl), gate,
                                     kappa_out);
   CKL();
-  tri_solve_kernel<<<nrhs, 256, 0, st>>>(R, ldr, in_t ? 1 : 0, n, nrhs, ctx->d(L.Vh), ctx->d(L.tauv), ctx->d(L.ldl), gate, X, ldx,
+  tri_solve_kernel<<<(nrhs + 7) / 8, 256, sizeof(double) * 2 * kRefChunk * n, st>>>(R, ldr, in_t ? 1 : 0, n, nrhs, ctx->d(L.Vh), ctx->d(L.tauv), ctx->d(L.ldl), gate, X, ldx,
                                          out_t ? 1 : 0);
   CKL();
   return OID_OK;
@@ -480,7 +483,7 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   int* gate = ctx->ptr<int>(L.gate);
   if (ell <= kTriMaxN && !ctx->cold_jacobi) {
     // tridiagonal fast path (tri.cuh); the eigenvector path below runs only when gate[1] is set
-    const size_t smem = sizeof(double) * (static_cast<size_t>((ell + kTriCtas - 1) / kTriCtas) * ell + 2 * ell);
+    const size_t smem = sizeof(double) * (0);
     tridiag_cluster_kernel<<<kTriCtas, 256, smem, st>>>(ctx->d(L.gram), ell, ctx->d(L.td), ctx->d(L.te), ctx->d(L.Vh),
                                                         ctx->d(L.tauv), ctx->d(L.gv), ctx->d(L.gp));
     CKL();
@@ -490,7 +493,7 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
     lambda_sorted_kernel<<<1, 256, 0, st>>>(ctx->d(L.mu), ell, p.k, ctx->d(L.gram), p.lambda, ell, scal, gate,
                                             ctx->d(L.td), ctx->d(L.te), ctx->d(L.ldl), 1);
     CKL();
-    tri_scores_kernel<<<ns, 256, 0, st>>>(ctx->d(L.Yc), ell, ns, ctx->d(L.Vh), ctx->d(L.tauv), ctx->d(L.ldl), gate,
+    tri_scores_kernel<<<(ns + 7) / 8, 256, sizeof(double) * 2 * kRefChunk * ell, st>>>(ctx->d(L.Yc), ell, ns, ctx->d(L.Vh), ctx->d(L.tauv), ctx->d(L.ldl), gate,
                                           ctx->d(L.tau));
     CKL();
     const int* g1 = gate + 1;
@@ -654,12 +657,17 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
 #undef BG_ATTR
   }
   if (p->ell <= kTriMaxN) {
-    const int tri_smem = static_cast<int>(sizeof(double) * (((p->ell + kTriCtas - 1) / kTriCtas) * p->ell + 2 * p->ell));
     if ((e = cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
       return bad(e);
-    if ((e = cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tri_smem)) != cudaSuccess)
+    const int ref_smem = static_cast<int>(sizeof(double) * 2 * kRefChunk * kTriMaxN);
+    if ((e = cudaFuncSetAttribute(tri_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ref_smem)) != cudaSuccess)
+      return bad(e);
+    if ((e = cudaFuncSetAttribute(tri_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ref_smem)) != cudaSuccess)
       return bad(e);
   }
+  if ((e = cudaFuncSetAttribute(small_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(kSmallSvdSmem))) != cudaSuccess)
+    return bad(e);
   ctx->k1_ctas_per_sm = 1;
   ctx->cold_jacobi = getenv("OID_JACOBI_COLD") && atoi(getenv("OID_JACOBI_COLD")) != 0;
   ctx->tc_ok = (prop.major == 10 && prop.minor == 0) && k1tc_supported(p->ell, p->b_max, p->dtype == OID_F64);
@@ -816,11 +824,40 @@ oid_status oid_estimate_end(oid_ctx ctx, double* out_dev, void* stream) {
       set_flag_kernel<<<1, 1, 0, st>>>(cgate, 0, 1);
       CKL();
     }
-    s = jacobi(ctx, st, ctx->d(L.cB), l1, l2, ctx->d(L.cV), ctx->d(L.csig), 2, false, cgate + 1);
-    if (s != OID_OK) return s;
-    s = pinv_assemble(ctx, st, ctx->d(L.cB), l1, l2, ctx->d(L.cV), ctx->d(L.csig), ctx->d(L.cw), ctx->d(L.cZ), ctx->d(L.M),
-                      nullptr, 0, cgate + 1);
-    if (s != OID_OK) return s;
+    const int lo = std::min(l1, l2), hi = std::max(l1, l2);
+    if (static_cast<size_t>(hi + lo) * lo * sizeof(double) <= kSmallSvdSmem) {
+      // small pseudo-inverse in one CTA: SVD of the tall orientation (hi x lo)
+      double* Bt = ctx->d(L.cBt);
+      if (l1 < l2) {
+        transpose_kernel<<<blocks_for(int64_t(l1) * l2), 256, 0, st>>>(ctx->d(L.cB), l1, l2, Bt, cgate + 1);
+        CKL();
+      } else {
+        CK(cudaMemcpyAsync(Bt, ctx->d(L.cB), sizeof(double) * l1 * l2, cudaMemcpyDeviceToDevice, st));
+      }
+      int* counters = ctx->ptr<int>(L.counters) + 2 * kMaxSweeps;
+      small_svd_kernel<<<1, 1024, static_cast<size_t>(hi + lo) * lo * sizeof(double), st>>>(
+          Bt, hi, lo, ctx->d(L.cV), ctx->d(L.csig), counters, kMaxSweeps, 4e-14 * std::max(1.0, std::sqrt(hi / 16.0)),
+          cgate + 1);
+      CKL();
+      if (l1 < l2) {
+        // pinv(B^T) (l1 x l2) = V diag(w) Bt^T; M = pinv(B) = pinv(B^T)^T (l2 x l1)
+        s = pinv_assemble(ctx, st, Bt, hi, lo, ctx->d(L.cV), ctx->d(L.csig), ctx->d(L.cw), ctx->d(L.cZ), ctx->d(L.cZ2),
+                          nullptr, 0, cgate + 1);
+        if (s != OID_OK) return s;
+        transpose_kernel<<<blocks_for(int64_t(l1) * l2), 256, 0, st>>>(ctx->d(L.cZ2), l1, l2, ctx->d(L.M), cgate + 1);
+        CKL();
+      } else {
+        s = pinv_assemble(ctx, st, Bt, hi, lo, ctx->d(L.cV), ctx->d(L.csig), ctx->d(L.cw), ctx->d(L.cZ), ctx->d(L.M),
+                          nullptr, 0, cgate + 1);
+        if (s != OID_OK) return s;
+      }
+    } else {
+      s = jacobi(ctx, st, ctx->d(L.cB), l1, l2, ctx->d(L.cV), ctx->d(L.csig), 2, false, cgate + 1);
+      if (s != OID_OK) return s;
+      s = pinv_assemble(ctx, st, ctx->d(L.cB), l1, l2, ctx->d(L.cV), ctx->d(L.csig), ctx->d(L.cw), ctx->d(L.cZ), ctx->d(L.M),
+                        nullptr, 0, cgate + 1);
+      if (s != OID_OK) return s;
+    }
     // term1 = tr(M (Omega1 A P^T) G (Omega2 A P^T)^T)
     s = gemm(ctx, st, false, true, l1, t, n, 1.0, S, ell, P, t, 0.0, ctx->d(L.X1), l1);
     if (s != OID_OK) return s;

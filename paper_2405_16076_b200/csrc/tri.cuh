@@ -21,133 +21,192 @@ constexpr int kTriRows = kTriMaxN / kTriCtas;   // 32 rows per CTA at the maximu
 // Householder tridiagonalisation of the symmetric n x n matrix A (col-major), n <= 512.
 // Outputs: d (n), e (n-1) of T; reflectors H_k = I - tau_k v_k v_k^T, k = 0..n-3, with v_k
 // stored in Vh(:, k) (rows k+1..n-1; zero elsewhere) and tau_k in tauv[k].
-// gv (n + 1), gp (n + kTriCtas): global broadcast buffers.  Launch: 16 CTAs in one cluster.
-__global__ void __cluster_dims__(kTriCtas, 1, 1) __launch_bounds__(256)
+// Launch: 16 CTAs in one cluster.  CTA c owns rows [c R, c R + R) (R <= 32); warp w of the CTA
+// owns 4 of them and lane l the columns l + 32 q (q < 16), held in REGISTERS (64 doubles per
+// thread), so the matrix-vector product and the rank-2 update never touch shared memory.
+// Step k: every CTA sends its slice of column k (= row k by symmetry) and its partial ||x||^2
+// to all CTAs through distributed shared memory; after a cluster barrier each CTA forms the
+// reflector redundantly, computes p = tau A v on its rows and sends its p slice and partial
+// v^T p; after a second barrier it applies A <- A - v w^T - w v^T, w = p - (tau v^T p / 2) v.
+constexpr int kTriRW = 4;     // rows per warp
+constexpr int kTriCL = 16;    // column registers per lane
+
+__device__ __forceinline__ double tri_pick(const double (&a)[kTriCL], int q) {
+  double x = 0.0;
+#pragma unroll
+  for (int c = 0; c < kTriCL; ++c) x = (c == q) ? a[c] : x;
+  return x;
+}
+
+__global__ void __cluster_dims__(kTriCtas, 1, 1) __launch_bounds__(256, 1)
 tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__ d, double* __restrict__ e,
-                       double* __restrict__ Vh, double* __restrict__ tauv, double* __restrict__ gv,
-                       double* __restrict__ gp) {
+                       double* __restrict__ Vh, double* __restrict__ tauv, double* __restrict__ /*gv*/,
+                       double* __restrict__ /*gp*/) {
   cg2::cluster_group cluster = cg2::this_cluster();
-  extern __shared__ double tri_smem[];
   const int c = static_cast<int>(cluster.block_rank());
   const int R = (n + kTriCtas - 1) / kTriCtas;
   const int r0 = c * R, r1 = min(n, r0 + R);
-  double* Al = tri_smem;                 // [R][n] rows r0..r1-1 (row-major)
-  double* vv = Al + R * n;               // [n]
-  double* pw = vv + n;                   // [n]  p, then w
-  __shared__ double red[8];
-  __shared__ double sc[4];
+  __shared__ double xb[2][kTriMaxN];     // column k, all CTAs' slices (double-buffered)
+  __shared__ double pb[kTriMaxN];        // p, all CTAs' slices
+  __shared__ double loc[kTriRows];       // this CTA's slice (x, then p)
+  __shared__ double ssb[2][kTriCtas];
+  __shared__ double kb[kTriCtas];
+  __shared__ double wred[8];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int idx = tid; idx < (r1 - r0) * n; idx += 256) {
-    const int i = idx / n, j = idx - i * n;
-    Al[i * n + j] = A[j + static_cast<int64_t>(r0 + i) * n];     // row r0+i = column r0+i (symmetric)
+  double a[kTriRW][kTriCL];
+  int gi[kTriRW];
+#pragma unroll
+  for (int r = 0; r < kTriRW; ++r) {
+    const int i = r0 + warp * kTriRW + r;
+    gi[r] = (warp * kTriRW + r < R && i < r1) ? i : -1;
+#pragma unroll
+    for (int q = 0; q < kTriCL; ++q) {
+      const int j = lane + 32 * q;
+      a[r][q] = (gi[r] >= 0 && j < n) ? A[j + static_cast<int64_t>(gi[r]) * n] : 0.0;   // row i = column i
+    }
   }
-  __syncthreads();
   cluster.sync();
   for (int k = 0; k < n - 2; ++k) {
-    const int owner = k / R;
-    const int len = n - k - 1;
-    if (c == owner) {
-      // Householder vector of row k (columns k+1..n-1): v = x - alpha e1, tau = 2 / v^T v
-      const double* x = Al + (k - r0) * n + (k + 1);
-      double ss = 0.0;
-      for (int j = tid; j < len; j += 256) ss = fma(x[j], x[j], ss);
-      ss = block_sum<256>(ss, red);
-      const double x0 = x[0];
-      double alpha = 0.0, tau = 0.0, v0 = 0.0;
-      const double tail = ss - x0 * x0;
-      if (tail > 0.0) {
-        alpha = -copysign(sqrt(ss), x0);
-        v0 = x0 - alpha;
-        tau = 2.0 / (tail + v0 * v0);
-      } else {
-        alpha = x0;    // already tridiagonal in this column: H_k = I
-      }
-      for (int j = tid; j < len; j += 256) {
-        const double vj = (j == 0) ? v0 : x[j];
-        const double out = tau != 0.0 ? vj : 0.0;
-        gv[k + 1 + j] = out;
-        Vh[(k + 1 + j) + static_cast<int64_t>(k) * n] = out;
-      }
-      if (tid == 0) {
-        gv[0] = tau;
-        tauv[k] = tau;
-        d[k] = Al[(k - r0) * n + k];
-        e[k] = alpha;
-      }
-    }
-    cluster.sync();
-    const double tau = __ldcg(gv);
-    for (int j = k + 1 + tid; j < n; j += 256) vv[j] = __ldcg(gv + j);
-    __syncthreads();
-    // p = tau A v on my rows i > k; K partial = v^T p
-    const int i0 = max(r0, k + 1);
-    double kp = 0.0;
-    if (tau != 0.0) {
-      for (int i = i0 + warp; i < r1; i += 8) {
-        const double* row = Al + (i - r0) * n;
-        double s = 0.0;
-        for (int j = k + 1 + lane; j < n; j += 32) s = fma(row[j], vv[j], s);
+    const int buf = k & 1;
+    double* xk = xb[buf];
+    const int qk = k >> 5, lk = k & 31;
+    // phase 1: x_i = A(i, k) for my rows i > k -> every CTA, with the partial sum of squares
+    double ssw = 0.0;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) {
-          const double pi = tau * s;
-          gp[i] = pi;
-          pw[i] = pi;
-        }
-      }
+    for (int r = 0; r < kTriRW; ++r) {
+      const double xi = __shfl_sync(0xffffffffu, tri_pick(a[r], qk), lk);
+      if (gi[r] > k) { ssw = fma(xi, xi, ssw); if (lane == 0) loc[gi[r] - r0] = xi; }
+      else if (gi[r] >= 0 && lane == 0) loc[gi[r] - r0] = 0.0;
     }
+    if (lane == 0) wred[warp] = ssw;
     __syncthreads();
-    if (tau != 0.0 && tid == 0) {
-      for (int i = i0; i < r1; ++i) kp = fma(vv[i], pw[i], kp);   // fixed order
-      gp[n + c] = kp;
+    for (int t = tid; t < R * kTriCtas; t += 256) {
+      const int q = t / R, il = t - q * R;
+      if (r0 + il < n) cluster.map_shared_rank(xk, q)[r0 + il] = loc[il];
+    }
+    if (tid < kTriCtas) {
+      double ss = 0.0;
+      for (int w = 0; w < 8; ++w) ss += wred[w];
+      cluster.map_shared_rank(&ssb[buf][0], tid)[c] = ss;
     }
     cluster.sync();
+    // phase 2: reflector (redundant in every CTA)
+    double ss = 0.0;
+    for (int q = 0; q < kTriCtas; ++q) ss += ssb[buf][q];
+    const double x0 = xk[k + 1];
+    const double tail = ss - x0 * x0;
+    double alpha, tau = 0.0, v0 = 0.0;
+    if (tail > 0.0) {
+      alpha = -copysign(sqrt(ss), x0);
+      v0 = x0 - alpha;
+      tau = 2.0 / (tail + v0 * v0);
+    } else {
+      alpha = x0;
+    }
+    if (tid == 0 && c == 0) tauv[k] = tau;
+#pragma unroll
+    for (int r = 0; r < kTriRW; ++r)
+      if (gi[r] == k && lane == lk) { d[k] = tri_pick(a[r], qk); e[k] = alpha; }
+    // v_i for my rows; p_i = tau sum_j A_ij v_j
+    double vi[kTriRW], pi[kTriRW];
+#pragma unroll
+    for (int r = 0; r < kTriRW; ++r) {
+      vi[r] = (gi[r] > k) ? (gi[r] == k + 1 ? v0 : xk[gi[r]]) : 0.0;
+      pi[r] = 0.0;
+    }
     if (tau != 0.0) {
-      if (tid == 0) {
-        double K = 0.0;
-        for (int q = 0; q < kTriCtas; ++q) K += __ldcg(gp + n + q);
-        sc[0] = 0.5 * tau * K;
-      }
-      for (int j = k + 1 + tid; j < n; j += 256) pw[j] = __ldcg(gp + j);
-      __syncthreads();
-      const double h = sc[0];
-      for (int j = k + 1 + tid; j < n; j += 256) pw[j] = pw[j] - h * vv[j];   // w = p - (tau K / 2) v
-      __syncthreads();
-      // A <- A - v w^T - w v^T on my rows i > k, columns j > k
-      for (int i = i0; i < r1; ++i) {
-        double* row = Al + (i - r0) * n;
-        const double vi = vv[i], wi = pw[i];
-        for (int j = k + 1 + tid; j < n; j += 256) row[j] = row[j] - vi * pw[j] - wi * vv[j];
+#pragma unroll
+      for (int q = 0; q < kTriCL; ++q) {
+        const int j = lane + 32 * q;
+        const double vj = (j > k && j < n) ? (j == k + 1 ? v0 : xk[j]) : 0.0;
+#pragma unroll
+        for (int r = 0; r < kTriRW; ++r) pi[r] = fma(a[r][q], vj, pi[r]);
       }
     }
+    double kw = 0.0;
+#pragma unroll
+    for (int r = 0; r < kTriRW; ++r) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) pi[r] += __shfl_xor_sync(0xffffffffu, pi[r], o);
+      pi[r] *= tau;
+      if (gi[r] > k) kw = fma(vi[r], pi[r], kw);
+      if (gi[r] >= 0 && lane == 0) {
+        loc[gi[r] - r0] = gi[r] > k ? pi[r] : 0.0;
+        if (gi[r] > k) Vh[gi[r] + static_cast<int64_t>(k) * n] = tau != 0.0 ? vi[r] : 0.0;
+      }
+    }
+    if (lane == 0) wred[warp] = kw;
     __syncthreads();
+    for (int t = tid; t < R * kTriCtas; t += 256) {
+      const int q = t / R, il = t - q * R;
+      if (r0 + il < n) cluster.map_shared_rank(pb, q)[r0 + il] = loc[il];
+    }
+    if (tid < kTriCtas) {
+      double kp = 0.0;
+      for (int w = 0; w < 8; ++w) kp += wred[w];
+      cluster.map_shared_rank(kb, tid)[c] = kp;
+    }
+    cluster.sync();
+    // phase 3: w = p - (tau K / 2) v; A <- A - v w^T - w v^T (zeros outside i, j > k)
+    if (tau != 0.0) {
+      double K = 0.0;
+      for (int q = 0; q < kTriCtas; ++q) K += kb[q];
+      const double h = 0.5 * tau * K;
+      double wi[kTriRW];
+#pragma unroll
+      for (int r = 0; r < kTriRW; ++r) wi[r] = (gi[r] > k) ? pi[r] - h * vi[r] : 0.0;
+#pragma unroll
+      for (int q = 0; q < kTriCL; ++q) {
+        const int j = lane + 32 * q;
+        const bool act = j > k && j < n;
+        const double vj = act ? (j == k + 1 ? v0 : xk[j]) : 0.0;
+        const double wj = act ? pb[j] - h * vj : 0.0;
+#pragma unroll
+        for (int r = 0; r < kTriRW; ++r) a[r][q] = a[r][q] - vi[r] * wj - wi[r] * vj;
+      }
+    }
   }
   // trailing 2 x 2 block
-  if (n >= 2) {
-    const int a = n - 2, b = n - 1;
-    if (tid == 0 && a >= r0 && a < r1) { d[a] = Al[(a - r0) * n + a]; e[a] = Al[(a - r0) * n + b]; }
-    if (tid == 0 && b >= r0 && b < r1) d[b] = Al[(b - r0) * n + b];
-  } else if (n == 1 && c == 0 && tid == 0) {
-    d[0] = Al[0];
+#pragma unroll
+  for (int r = 0; r < kTriRW; ++r) {
+    if (n >= 2 && gi[r] == n - 2) {
+      const double dd = __shfl_sync(0xffffffffu, tri_pick(a[r], (n - 2) >> 5), (n - 2) & 31);
+      const double ee = __shfl_sync(0xffffffffu, tri_pick(a[r], (n - 1) >> 5), (n - 1) & 31);
+      if (lane == 0) { d[n - 2] = dd; e[n - 2] = ee; }
+    }
+    if (gi[r] == n - 1) {
+      const double dd = __shfl_sync(0xffffffffu, tri_pick(a[r], (n - 1) >> 5), (n - 1) & 31);
+      if (lane == 0) d[n - 1] = dd;
+    }
   }
   cluster.sync();
 }
 
-// Eigenvalues of the symmetric tridiagonal (d, e) in descending order, mu[i] = (i+1)-th
-// largest, by Sturm-count multisection: one warp per eigenvalue, 32 shifts per iteration.
+// Number of eigenvalues >= x of the symmetric tridiagonal (d, e2 = e^2): n minus the number of
+// sign changes of the Sturm sequence p_0 = 1, p_j = (d_j - x) p_{j-1} - e_{j-1}^2 p_{j-2} (no
+// divisions; both terms rescaled by exact powers of two when large or small; a zero p_j takes
+// the sign opposite to p_{j-1}).
 __device__ __forceinline__ int sturm_count_gt(const double* __restrict__ d, const double* __restrict__ e2, int n,
-                                              double x, double pivmin) {
-  // number of eigenvalues < x (negative pivots of LDL^T of T - x I)
+                                              double x, double /*pivmin*/) {
   int neg = 0;
-  double q = d[0] - x;
-  if (fabs(q) < pivmin) q = -pivmin;
-  neg += q < 0.0;
+  double pm = 1.0, pc = d[0] - x;
+  if (pc == 0.0) pc = -0x1p-1000;
+  neg += pc < 0.0;
   for (int j = 1; j < n; ++j) {
-    q = d[j] - x - e2[j - 1] / q;
-    if (fabs(q) < pivmin) q = -pivmin;
-    neg += q < 0.0;
+    double pn = (d[j] - x) * pc - e2[j - 1] * pm;
+    if (pn == 0.0) pn = (pc < 0.0) ? 0x1p-1000 : -0x1p-1000;
+    neg += (pn < 0.0) != (pc < 0.0);
+    pm = pc;
+    pc = pn;
+    const double a = fabs(pc);
+    if (a > 0x1p+400 || a < 0x1p-400) {
+      const int ex = ilogb(pc);
+      const double sc = ldexp(1.0, -ex);
+      pc *= sc;
+      pm *= sc;
+    }
   }
-  return n - neg;   // eigenvalues >= x
+  return n - neg;
 }
 
 __global__ void __launch_bounds__(256) multisect_kernel(const double* __restrict__ d, const double* __restrict__ e, int n,
@@ -155,7 +214,7 @@ __global__ void __launch_bounds__(256) multisect_kernel(const double* __restrict
   extern __shared__ double ms_smem[];
   double* ds = ms_smem;
   double* e2 = ms_smem + n;
-  __shared__ double bnd[3];
+  __shared__ double bnd[4];
   const int tid = threadIdx.x;
   for (int j = tid; j < n; j += blockDim.x) {
     ds[j] = d[j];
@@ -176,6 +235,7 @@ __global__ void __launch_bounds__(256) multisect_kernel(const double* __restrict
     bnd[0] = lo - pad;
     bnd[1] = hi + pad;
     bnd[2] = 2.2250738585072014e-308 * fmax(1.0, emax2);   // LAPACK pivmin
+    bnd[3] = 4.0 * eps * tmax;                                 // absolute accuracy of a Sturm count
   }
   __syncthreads();
   const double pivmin = bnd[2];
@@ -185,7 +245,7 @@ __global__ void __launch_bounds__(256) multisect_kernel(const double* __restrict
   double lo = bnd[0], hi = bnd[1];
   const double eps = 2.220446049250313e-16;
   for (int it = 0; it < 40; ++it) {
-    if (hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi)) + pivmin) break;
+    if (hi - lo <= fmax(2.0 * eps * fmax(fabs(lo), fabs(hi)), bnd[3]) + pivmin) break;
     const double x = lo + (hi - lo) * static_cast<double>(lane + 1) / 33.0;
     const int gt = sturm_count_gt(ds, e2, n, x, pivmin);   // #eigenvalues >= x
     // new lo: largest x with gt >= i+1; new hi: smallest x with gt <= i
@@ -241,38 +301,89 @@ __global__ void lambda_sorted_kernel(const double* __restrict__ mu, int n, int k
   }
 }
 
+// z_w <- H_k z_w for k = k_first .. k_last (step +-1), for the 8 vectors z_w (one per warp) of a
+// CTA: the reflectors are streamed through shared memory in chunks of kRefChunk (cp.async, double
+// buffer); each warp applies them to its vector with shuffle dot products (fixed order).
+constexpr int kRefChunk = 8;
+__device__ __forceinline__ void cta_apply_reflectors(double (*z)[kTriMaxN], int nvec, int n,
+                                                     const double* __restrict__ Vh, const double* __restrict__ tauv,
+                                                     int k_first, int k_last, int step, double* __restrict__ vbuf) {
+  // vbuf: [2][kRefChunk][n]
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int nk = (step > 0 ? k_last - k_first : k_first - k_last) + 1;
+  if (nk <= 0) return;
+  const int nchunks = (nk + kRefChunk - 1) / kRefChunk;
+  __shared__ double tb[2][kRefChunk];
+  auto stage = [&](int ch, int b) {
+    double* dst = vbuf + static_cast<int64_t>(b) * kRefChunk * n;
+    if (tid < kRefChunk) {
+      const int q = ch * kRefChunk + tid;
+      tb[b][tid] = q < nk ? tauv[k_first + step * q] : 0.0;
+    }
+    for (int e = tid; e < kRefChunk * n; e += blockDim.x) {
+      const int r = e / n, i = e - r * n;
+      const int q = ch * kRefChunk + r;
+      if (q < nk) {
+        const int k = k_first + step * q;
+        const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst + e));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(Vh + static_cast<int64_t>(k) * n + i));
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  stage(0, 0);
+  for (int ch = 0; ch < nchunks; ++ch) {
+    if (ch + 1 < nchunks) { stage(ch + 1, (ch + 1) & 1); asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+    else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    const double* vb = vbuf + static_cast<int64_t>(ch & 1) * kRefChunk * n;
+    if (w < nvec) {
+      double* zw = z[w];
+      for (int r = 0; r < kRefChunk; ++r) {
+        const int q = ch * kRefChunk + r;
+        if (q >= nk) break;
+        const int k = k_first + step * q;
+        const double tk = tb[ch & 1][r];
+        if (tk == 0.0) continue;
+        const double* v = vb + r * n;
+        double sacc = 0.0;
+        for (int i = k + 1 + lane; i < n; i += 32) sacc = fma(v[i], zw[i], sacc);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+        const double f = tk * sacc;
+        for (int i = k + 1 + lane; i < n; i += 32) zw[i] = fma(-f, v[i], zw[i]);
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // tau(y) = z^T (T + sI)^-1 z, z = Q^T y = H_{n-3} ... H_0 y; y = column j of Yc (ell x ncol).
-// One CTA per column.  Runs when gate[0] != 0.
+// 8 columns per CTA (one per warp); runs when gate[0] != 0.  Dynamic smem: 2 kRefChunk n doubles.
 __global__ void __launch_bounds__(256) tri_scores_kernel(const double* __restrict__ Yc, int n, int ncol,
                                                          const double* __restrict__ Vh, const double* __restrict__ tauv,
                                                          const double* __restrict__ ldl, const int* __restrict__ gate,
                                                          double* __restrict__ tau_out) {
   if (gate[0] == 0) return;
-  __shared__ double z[kTriMaxN];
-  __shared__ double red[8];
-  const int j = blockIdx.x, tid = threadIdx.x;
-  if (j >= ncol) return;
-  for (int i = tid; i < n; i += 256) z[i] = Yc[static_cast<int64_t>(j) * n + i];
+  extern __shared__ double ref_smem[];
+  __shared__ double zs[8][kTriMaxN];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j0 = blockIdx.x * 8;
+  const int nvec = min(8, ncol - j0);
+  if (w < nvec)
+    for (int i = lane; i < n; i += 32) zs[w][i] = Yc[static_cast<int64_t>(j0 + w) * n + i];
   __syncthreads();
-  for (int k = 0; k < n - 2; ++k) {
-    const double tk = tauv[k];
-    if (tk == 0.0) continue;                      // uniform across the CTA
-    const double* v = Vh + static_cast<int64_t>(k) * n;
-    double s = 0.0;
-    for (int i = k + 1 + tid; i < n; i += 256) s = fma(v[i], z[i], s);
-    s = block_sum<256>(s, red);
-    const double f = tk * s;
-    for (int i = k + 1 + tid; i < n; i += 256) z[i] = fma(-f, v[i], z[i]);
-    __syncthreads();
-  }
-  if (tid == 0) {
+  cta_apply_reflectors(zs, nvec, n, Vh, tauv, 0, n - 3, 1, ref_smem);
+  if (w < nvec && lane == 0) {
+    const double* z = zs[w];
     double y = z[0];
     double acc = y * y * ldl[0];
     for (int i = 1; i < n; ++i) {
       y = z[i] - ldl[n + i - 1] * y;
       acc = fma(y * y, ldl[i], acc);
     }
-    tau_out[j] = acc;
+    tau_out[j0 + w] = acc;
   }
 }
 
@@ -301,51 +412,40 @@ __global__ void spd_gate_kernel(const double* __restrict__ mu, int n, double kma
 }
 
 // X(:, c) = A^-1 R(:, c) with A = Q T Q^T: z = Q^T r, solve T u = z (LDL^T), x = Q u.
-// One CTA per right-hand side; runs when gate[0] != 0.  in_transposed: R(i, c) = R[c + i ldr];
-// out_transposed: write X^T (nrhs x n).
+// 8 right-hand sides per CTA (one per warp); runs when gate[0] != 0.  in_transposed:
+// R(i, c) = R[c + i ldr]; out_transposed: write X^T (nrhs x n).  Dynamic smem: 2 kRefChunk n.
 __global__ void __launch_bounds__(256) tri_solve_kernel(const double* __restrict__ R, int64_t ldr, int in_transposed,
-                                                        int n, int nrhs,
-                                                        const double* __restrict__ Vh, const double* __restrict__ tauv,
-                                                        const double* __restrict__ ldl, const int* __restrict__ gate,
-                                                        double* __restrict__ X, int64_t ldx, int out_transposed) {
+                                                        int n, int nrhs, const double* __restrict__ Vh,
+                                                        const double* __restrict__ tauv, const double* __restrict__ ldl,
+                                                        const int* __restrict__ gate, double* __restrict__ X,
+                                                        int64_t ldx, int out_transposed) {
   if (gate[0] == 0) return;
-  __shared__ double z[kTriMaxN];
-  __shared__ double red[8];
-  const int c = blockIdx.x, tid = threadIdx.x;
-  if (c >= nrhs) return;
-  for (int i = tid; i < n; i += 256)
-    z[i] = in_transposed ? R[c + static_cast<int64_t>(i) * ldr] : R[static_cast<int64_t>(c) * ldr + i];
+  extern __shared__ double ref_smem[];
+  __shared__ double zs[8][kTriMaxN];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c0 = blockIdx.x * 8;
+  const int nvec = min(8, nrhs - c0);
+  if (w < nvec)
+    for (int i = lane; i < n; i += 32) {
+      const int c = c0 + w;
+      zs[w][i] = in_transposed ? R[c + static_cast<int64_t>(i) * ldr] : R[static_cast<int64_t>(c) * ldr + i];
+    }
   __syncthreads();
-  for (int k = 0; k < n - 2; ++k) {                 // z = H_{n-3} ... H_0 r
-    const double tk = tauv[k];
-    if (tk == 0.0) continue;
-    const double* v = Vh + static_cast<int64_t>(k) * n;
-    double s = 0.0;
-    for (int i = k + 1 + tid; i < n; i += 256) s = fma(v[i], z[i], s);
-    s = block_sum<256>(s, red);
-    for (int i = k + 1 + tid; i < n; i += 256) z[i] = fma(-tk * s, v[i], z[i]);
-    __syncthreads();
-  }
-  if (tid == 0) {                                   // T u = z by LDL^T
+  cta_apply_reflectors(zs, nvec, n, Vh, tauv, 0, n - 3, 1, ref_smem);      // z = Q^T r
+  if (w < nvec && lane == 0) {                                              // T u = z by LDL^T
+    double* z = zs[w];
     for (int i = 1; i < n; ++i) z[i] -= ldl[n + i - 1] * z[i - 1];
     for (int i = 0; i < n; ++i) z[i] *= ldl[i];
     for (int i = n - 2; i >= 0; --i) z[i] -= ldl[n + i] * z[i + 1];
   }
   __syncthreads();
-  for (int k = n - 3; k >= 0; --k) {               // x = H_0 ... H_{n-3} u
-    const double tk = tauv[k];
-    if (tk == 0.0) continue;
-    const double* v = Vh + static_cast<int64_t>(k) * n;
-    double s = 0.0;
-    for (int i = k + 1 + tid; i < n; i += 256) s = fma(v[i], z[i], s);
-    s = block_sum<256>(s, red);
-    for (int i = k + 1 + tid; i < n; i += 256) z[i] = fma(-tk * s, v[i], z[i]);
-    __syncthreads();
-  }
-  for (int i = tid; i < n; i += 256) {
-    if (out_transposed) X[static_cast<int64_t>(i) * ldx + c] = z[i];
-    else X[static_cast<int64_t>(c) * ldx + i] = z[i];
-  }
+  cta_apply_reflectors(zs, nvec, n, Vh, tauv, n - 3, 0, -1, ref_smem);     // x = Q u
+  if (w < nvec)
+    for (int i = lane; i < n; i += 32) {
+      const int c = c0 + w;
+      if (out_transposed) X[static_cast<int64_t>(i) * ldx + c] = zs[w][i];
+      else X[static_cast<int64_t>(c) * ldx + i] = zs[w][i];
+    }
 }
 
 // A(i, i) = cval for zero rows/columns of a Gram (vacant basis slots, reading R10) where cval =
