@@ -11,10 +11,11 @@
 // CTA organisation (one CTA per SM, 14 warps; one work unit = row slab x 128*TM sketch rows):
 //   warp 0        TMA producer: cp.async.bulk.tensor 2D boxes (128 B x BPAD, 128B swizzle) of X
 //   warp 1        TMEM allocator + single-thread tcgen05.mma issuer (A from TMEM, B from smem)
-//   warps 2-5     digit slicer: X stage -> per-column exponent check -> int8 digit planes (B op.);
-//                 also the epilogue at accumulation-epoch ends (tcgen05.ld of the int32
-//                 accumulators, fp64 assembly, partial out)
-//   warps 6-13    sketch generator: Philox4x32-10 -> Gauss-16 nibbles -> int8 q by two PRMT
+//   warps 6-13    digit slicer: X stage -> per-column exponent check -> int8 digit planes (B op.),
+//                 8 rows per thread, software-pipelined one tile ahead (the exponent decision
+//                 for tile t+1 is made while tile t is converted); also the epilogue at
+//                 accumulation-epoch ends (tcgen05.ld of the int32 accumulators, fp64 partials)
+//   warps 2-5     sketch generator: Philox4x32-10 -> Gauss-16 nibbles -> int8 q by two PRMT
 //                 table lookups per 4 entries (levels held in 2 registers) -> tcgen05.st into
 //                 TMEM (A operand); 32 entries per Philox call
 // Per-column exponents start from the first tile of the unit plus kHeadroom bits; if a later
@@ -44,6 +45,7 @@ struct K1TcArgs {
   unsigned* flags;
   int num_sms;
   uint32_t t0, t1;   // Gauss-16 magnitudes m_0..m_3, m_4..m_7 as bytes (reading R2)
+  long long* dbg;     // diagnostics (may be null): per-tile role timestamps of CTA 0
 };
 
 namespace k1tc {
@@ -58,7 +60,11 @@ constexpr int kEmin = -900;         // exponents are clamped here (data below 2^
 constexpr int kNone = -100000;      // "no nonzero seen yet" exponent
 constexpr int kMaxEpochTiles = 1024;
 constexpr int kMaxStages = 4;
-constexpr int kSlicer0 = 2, kGen0 = 6;   // first warp of each role
+// Roles by warp id.  The slicer is the critical path and the warp arbiter favours higher warp
+// ids, so the slicer gets the top warps and the (run-ahead) generator the ones below.
+constexpr int kGen0 = 2, kSlicer0 = 6;    // first warp of each role
+constexpr int kSlW = 8;                   // slicer warps (6..13)
+constexpr int kSlT = 32 * kSlW;           // slicer threads
 
 struct Geom {
   int bpad;      // padded block width (16, 32, 64)
@@ -71,7 +77,10 @@ struct Geom {
   int nhalves;   // sketch-row slices
   int nslabs;
   int64_t rows_per_slab;
+  long long* dbg;  // [5][kDbgTiles] clock64 of CTA 0: A ready, B ready, MMA start, MMA issued, TMA issue
 };
+constexpr int kDbgTiles = 4096;
+constexpr int kDbgRows = 10;
 
 inline Geom make_geom(int ell, int ncols, int64_t m_loc, bool f64, int num_sms) {
   Geom g{};
@@ -177,6 +186,45 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
+// Warp-uniform variants: all 32 lanes execute the asm with warp-uniform operands (so the
+// compiler keeps them in uniform registers, no per-lane waterfall loop); elect.sync picks the
+// single lane that issues.
+__device__ __forceinline__ void mma_i8_ta_e(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_e(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_e(uint64_t* bar) {
+  asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t@e mbarrier.arrive.shared::cta.b64 _, [%0];\n\t}" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx_e(uint64_t* bar, uint32_t bytes) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_e(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n\t}" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
 #define OID_TMEM_LD16(taddr, r)                                                                                   \
   asm volatile(                                                                                                   \
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, " \
@@ -249,28 +297,31 @@ struct Shared {
   uint64_t d_full, d_empty;
   uint32_t tmem_base;
   int bflags[kMaxStages];
-  int ecur[64];
-  int ehist[2][64];
-  int emax[4][64];
-  double nrm[128];
-  double csum[128];
+  int ecur[2][64];
+  int ehist[4][64];
+  uint64_t tok[2];
+  int egen, qsh;
+  int emax[2][4][2][64];
+  double nrm[kSlT];
+  double csum[kSlT];
 };
 
-// Load the 16 values (rows 16 c16 .. +15) of column j from a 128B-swizzled X stage as raw bits.
+// Load the 8 values (rows 16 c16 + 8 h .. +7) of column j from a 128B-swizzled X stage as raw
+// bits (fp64: 16 words, fp32: 8 words).
 template <typename T, int BPAD>
-__device__ __forceinline__ void load_unit(const uint8_t* xs, int j, int c16, uint32_t (&w)[2 * Bits<T>::kPer16 * 2]) {
+__device__ __forceinline__ void load_half(const uint8_t* xs, int j, int c16, int h, uint32_t (&w)[sizeof(T) == 8 ? 16 : 8]) {
   if constexpr (sizeof(T) == 8) {
     const uint8_t* base = xs + (c16 * BPAD + j) * 128;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const uint4 v = *reinterpret_cast<const uint4*>(base + ((q ^ (j & 7)) << 4));
+    for (int q = 0; q < 4; ++q) {
+      const uint4 v = *reinterpret_cast<const uint4*>(base + (((4 * h + q) ^ (j & 7)) << 4));
       w[4 * q + 0] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
     }
   } else {
     const uint8_t* base = xs + ((c16 >> 1) * BPAD + j) * 128;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int qq = (c16 & 1) * 4 + q;
+    for (int q = 0; q < 2; ++q) {
+      const int qq = (c16 & 1) * 4 + 2 * h + q;
       const uint4 v = *reinterpret_cast<const uint4*>(base + ((qq ^ (j & 7)) << 4));
       w[4 * q + 0] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
     }
@@ -290,9 +341,9 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
   constexpr int ACOL0 = TM * NTOT;                 // first TMEM column of the A stages
   constexpr int BOX_ROWS = 128 / sizeof(T);
   constexpr int NBOX = kKTile / BOX_ROWS;
-  constexpr int NUNITS = 4 * BPAD;                 // (column, 16-row chunk) units per tile
-  constexpr int U = (NUNITS + 127) / 128;          // units per slicer thread
-  constexpr int NW = kF64 ? 32 : 16;               // 32-bit words per unit
+  constexpr int NHU = 8 * BPAD;                    // (column, 8-row half chunk) units per tile
+  constexpr int HU = (NHU + kSlT - 1) / kSlT;      // half units per slicer thread
+  constexpr int NWH = kF64 ? 16 : 8;               // 32-bit words per half unit
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int unit = blockIdx.x;
   const int slab = unit / g.nhalves, half = unit % g.nhalves;
@@ -309,16 +360,20 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&sh.x_full[s], 1);
-      mbar_init(&sh.x_empty[s], 4);
+      mbar_init(&sh.x_empty[s], kSlW / 2);
       mbar_init(&sh.b_full[s], 1);
       mbar_init(&sh.b_empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&sh.a_full[s], 8);
+      mbar_init(&sh.a_full[s], 4);
       mbar_init(&sh.a_empty[s], 1);
     }
     mbar_init(&sh.d_full, 2);
-    mbar_init(&sh.d_empty, 4);
+    mbar_init(&sh.d_empty, kSlW / 2);
+    mbar_init(&sh.tok[0], 1);
+    mbar_init(&sh.tok[1], 1);
+    sh.egen = 0;
+    sh.qsh = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -332,71 +387,85 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
   const uint32_t tmem = sh.tmem_base;
 
   if (warp == 0) {
-    // ---------------------------------------------------------------- TMA producer
-    if (lane == 0) {
-      for (int t = 0; t < ntiles; ++t) {
-        const int s = t % NS;
-        if (t >= NS) mbar_wait(&sh.x_empty[s], ((t / NS) - 1) & 1);
-        mbar_arrive_expect_tx(&sh.x_full[s], g.x_bytes);
-        uint8_t* dst = xbuf + s * g.x_bytes;
+    // ---------------------------------------------------------------- TMA producer (warp-uniform)
+    int s = 0;
+    uint32_t ph = 0;
+    for (int t = 0; t < ntiles; ++t) {
+      if (t >= NS) mbar_wait(&sh.x_empty[s], ph ^ 1);
+      if (g.dbg && blockIdx.x == 0 && t < kDbgTiles && lane == 0) g.dbg[4 * kDbgTiles + t] = clock64();
+      mbar_arrive_expect_tx_e(&sh.x_full[s], g.x_bytes);
+      uint8_t* dst = xbuf + s * g.x_bytes;
 #pragma unroll
-        for (int bx = 0; bx < NBOX; ++bx)
-          tma_load_2d(dst + bx * BPAD * 128, &tmap, &sh.x_full[s], static_cast<int>(r0 + int64_t(t) * kKTile + bx * BOX_ROWS),
-                      0);
-      }
+      for (int bx = 0; bx < NBOX; ++bx)
+        tma_load_2d_e(dst + bx * BPAD * 128, &tmap, &sh.x_full[s], static_cast<int>(r0 + int64_t(t) * kKTile + bx * BOX_ROWS), 0);
+      if (++s == NS) { s = 0; ph ^= 1; }
     }
   } else if (warp == 1) {
-    // ---------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      constexpr int chB = NTOT / 8 * 128;      // bytes per 16-byte K chunk of the B stage
-      constexpr int NU = (kS - 1) * BPAD;      // unsigned digit planes 0 .. S-2
-      constexpr int NUC = NU > 256 ? NU / 2 : NU;
-      int q = 0;
-      bool first = true;
-      for (int t = 0; t < ntiles; ++t) {
-        const int s = t % NS, sa = t & 1;
-        mbar_wait(&sh.a_full[sa], (t >> 1) & 1);
-        mbar_wait(&sh.b_full[s], (t / NS) & 1);
+    // ---------------------------------------------------------------- MMA issuer (warp-uniform, elected lane)
+    constexpr int chB = NTOT / 8 * 128;      // bytes per 16-byte K chunk of the B stage
+    constexpr int NU = (kS - 1) * BPAD;      // unsigned digit planes 0 .. S-2
+    constexpr int NUC = NU > 256 ? NU / 2 : NU;
+    int q = 0;
+    bool first = true;
+    int s = 0;
+    uint32_t ph = 0;
+    const uint32_t bbase0 = smem_u32(bbuf);
+    for (int t = 0; t < ntiles; ++t) {
+      const int sa = t & 1;
+      mbar_wait(&sh.a_full[sa], (t >> 1) & 1);
+      mbar_wait(&sh.b_full[s], ph);
+      tc_fence_after();
+      if (g.dbg && blockIdx.x == 0 && t < kDbgTiles && lane == 0) g.dbg[2 * kDbgTiles + t] = clock64();
+      if (sh.bflags[s] && t > 0) {           // close accumulation epoch q: flush D to fp64
+        mma_commit_e(&sh.d_full);
+        mbar_arrive_e(&sh.d_full);
+        mbar_wait(&sh.d_empty, q & 1);
         tc_fence_after();
-        if (sh.bflags[s] && t > 0) {           // close accumulation epoch q: flush D to fp64
-          mma_commit(&sh.d_full);
-          mbar_arrive(&sh.d_full);
-          mbar_wait(&sh.d_empty, q & 1);
-          tc_fence_after();
-          ++q;
-          first = true;
-        }
-        const uint32_t bbase = smem_u32(bbuf + s * g.b_bytes);
-#pragma unroll
-        for (int ks = 0; ks < kKTile / 32; ++ks) {
-#pragma unroll
-          for (int tm = 0; tm < TM; ++tm) {
-            const uint32_t at = tmem + ACOL0 + (sa * TM + tm) * 16 + ks * 8;
-            const uint32_t acc = (first && ks == 0) ? 0u : 1u;
-            const uint32_t dcol = tmem + tm * NTOT;
-#pragma unroll
-            for (int n0 = 0; n0 < NU; n0 += NUC) {
-              const uint64_t bd = umma_desc(bbase + 2 * ks * chB + (n0 / 8) * 128, chB, 128);
-              mma_i8_ta(dcol + n0, at, bd, idesc_i8(NUC, false), acc);
-            }
-            const uint64_t bd = umma_desc(bbase + 2 * ks * chB + (NU / 8) * 128, chB, 128);
-            mma_i8_ta(dcol + NU, at, bd, idesc_i8(BPAD, true), acc);
-          }
-        }
-        first = false;
-        mma_commit(&sh.a_empty[sa]);
-        mma_commit(&sh.b_empty[s]);
+        ++q;
+        first = true;
       }
-      mma_commit(&sh.d_full);
-      mbar_arrive(&sh.d_full);
+      const uint32_t bbase = bbase0 + s * g.b_bytes;
+#pragma unroll
+      for (int ks = 0; ks < kKTile / 32; ++ks) {
+#pragma unroll
+        for (int tm = 0; tm < TM; ++tm) {
+          const uint32_t at = tmem + ACOL0 + (sa * TM + tm) * 16 + ks * 8;
+          const uint32_t acc = (first && ks == 0) ? 0u : 1u;
+          const uint32_t dcol = tmem + tm * NTOT;
+#pragma unroll
+          for (int n0 = 0; n0 < NU; n0 += NUC) {
+            const uint64_t bd = umma_desc(bbase + 2 * ks * chB + (n0 / 8) * 128, chB, 128);
+            mma_i8_ta_e(dcol + n0, at, bd, idesc_i8(NUC, false), acc);
+          }
+          const uint64_t bd = umma_desc(bbase + 2 * ks * chB + (NU / 8) * 128, chB, 128);
+          mma_i8_ta_e(dcol + NU, at, bd, idesc_i8(BPAD, true), acc);
+        }
+      }
+      first = false;
+      mma_commit_e(&sh.a_empty[sa]);
+      mma_commit_e(&sh.b_empty[s]);
+      if (g.dbg && blockIdx.x == 0 && t < kDbgTiles && lane == 0) g.dbg[3 * kDbgTiles + t] = clock64();
+      if (++s == NS) { s = 0; ph ^= 1; }
     }
-  } else if (warp < kGen0) {
-    // ---------------------------------------------------------------- digit slicer (128 threads)
-    const int st = threadIdx.x - 32 * kSlicer0;     // 0..127
-    const int j = st % BPAD;                         // this thread's column (all its units)
+    mma_commit_e(&sh.d_full);
+    mbar_arrive_e(&sh.d_full);
+  } else if (warp >= kSlicer0) {
+    // ---------------------------------------------------------------- digit slicer (2 x 128 threads)
+    // Two groups of 4 warps convert alternate tiles concurrently (group g: tiles t = g mod 2).
+    // Shared per-tile bookkeeping (epoch index, exponent raises, b_full) is serialised in tile
+    // order by a token passed between the groups (mbarriers tok[0..1]).
+    constexpr int GT = 128;
+    constexpr int GHU = (NHU + GT - 1) / GT;         // half units per thread per tile
+    const int sw = warp - kSlicer0;                  // 0..7
+    const int grp = sw >> 2;
+    const int gt = threadIdx.x - 32 * (kSlicer0 + 4 * grp);   // 0..127
+    const int st = threadIdx.x - 32 * kSlicer0;      // 0..255
+    const int j = (gt >> 1) % BPAD;                  // this thread's column (all its half units)
+    const int barg = 1 + grp;                        // group barrier
+    constexpr int kBarAll = 3;
     constexpr int chB = NTOT / 8 * 128;
-    // epilogue of accumulation epoch qe: D (int32, TMEM) -> fp64 partial sums
     const int quarter = warp & 3;                    // TMEM lane quarter this warp may access
+    // epilogue of accumulation epoch qe: D (int32, TMEM) -> fp64 partial sums, one group
     auto epilogue = [&](int qe) {
       mbar_wait(&sh.d_full, qe & 1);
       tc_fence_after();
@@ -424,7 +493,7 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
             for (int k = 0; k < 16; ++k) {
               const int jj = jb + k;
               if (jj >= ncols) continue;
-              const int e = sh.ehist[qe & 1][jj];
+              const int e = sh.ehist[qe & 3][jj];
               const double val =
                   (e == kNone) ? 0.0 : acc[k] * __longlong_as_double(static_cast<long long>(e - kTop + 1023) << 52);
               double* dst = part + (static_cast<int64_t>(unit) * BPAD + jj) * ROWS + rl;
@@ -437,79 +506,74 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
       __syncwarp();
       if (lane == 0) mbar_arrive(&sh.d_empty);
     };
-    double nacc = 0.0, cacc = 0.0;
-    int q = 0, tacc = 0;
-    for (int t = 0; t < ntiles; ++t) {
-      const int s = t % NS;
-      const uint32_t ph = (t / NS) & 1;
-      mbar_wait(&sh.x_full[s], ph);
+    auto keymax = [&](const uint32_t (&w)[NWH]) -> uint32_t {
+      uint32_t km = 0;
+      if constexpr (kF64) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) km = max(km, Bits<double>::key(w[2 * e + 1]));
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) km = max(km, Bits<float>::key(w[e]));
+      }
+      return km;
+    };
+    auto load_tile = [&](int s, uint32_t (&w)[GHU][NWH]) {
       const uint8_t* xs = xbuf + s * g.x_bytes;
-      uint32_t w[U][NW];
-      // phase 1: load this thread's units; exponent key maxima
 #pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const int u = st + 128 * k;
-        if (u < NUNITS) {
-          load_unit<T, BPAD>(xs, j, u / BPAD, w[k]);
-          uint32_t km = 0;
-          if constexpr (kF64) {
-#pragma unroll
-            for (int e = 0; e < 16; ++e) km = max(km, Bits<double>::key(w[k][2 * e + 1]));
-          } else {
-#pragma unroll
-            for (int e = 0; e < 16; ++e) km = max(km, Bits<float>::key(w[k][e]));
-          }
-          sh.emax[u / BPAD][j] = Bits<T>::ebound(km);
-        }
+      for (int k = 0; k < GHU; ++k) {
+        const int hu = gt + GT * k;
+        if (hu < NHU) load_half<T, BPAD>(xs, j, (hu >> 1) / BPAD, hu & 1, w[k]);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sh.x_empty[s]);     // values are in registers
-      named_bar(1, 128);
-      int raise = 0;
-      if (st < BPAD) {
-        int eb = kNone;
+    };
+    auto publish = [&](const uint32_t (&w)[GHU][NWH]) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) eb = max(eb, sh.emax[c][st]);
-        if (t == 0) {
-          sh.ecur[st] = eb == kNone ? kNone : max(kEmin, eb + kHeadroom);
-        } else if (eb != kNone && (sh.ecur[st] == kNone || eb > sh.ecur[st])) {
-          sh.ecur[st] = max(kEmin, eb + kHeadroom);
-          raise = 1;
-        }
+      for (int k = 0; k < GHU; ++k) {
+        const int hu = gt + GT * k;
+        if (hu < NHU) sh.emax[0][(hu >> 1) / BPAD][hu & 1][j] = Bits<T>::ebound(keymax(w[k]));
       }
-      const int raise_any = named_bar_or(1, 128, raise);
-      const bool newacc = (t == 0) || raise_any || (t - tacc >= kMaxEpochTiles);
-      const bool flush = newacc && t > 0;       // epoch q ends before tile t (epilogue below)
-      if (newacc) {
-        tacc = t;
-        if (t > 0) ++q;
-        if (st < BPAD) sh.ehist[q & 1][st] = sh.ecur[st];
-      }
-      if (t >= NS) mbar_wait(&sh.b_empty[s], ((t / NS) - 1) & 1);
-      // phase 2: exact fixed-point digits of x * 2^F_j -> K-major B operand
-      const int e = sh.ecur[j];
+    };
+    // columns (threads gt < BPAD): first tile sets the exponents, later tiles only raise them
+    auto set_ecur = [&](bool first) {
+      if (gt >= BPAD) return;
+      int eb = kNone;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) eb = max(eb, max(sh.emax[0][c][0][gt], sh.emax[0][c][1][gt]));
+      const int ep = sh.ecur[0][gt];
+      if (first) sh.ecur[0][gt] = eb == kNone ? kNone : max(kEmin, eb + kHeadroom);
+      else if (eb != kNone && (ep == kNone || eb > ep)) sh.ecur[0][gt] = max(kEmin, eb + kHeadroom);
+    };
+    double nacc = 0.0, cacc = 0.0;
+    // exact fixed-point digits of x * 2^F_j -> K-major B operand of stage s; returns 1 when an
+    // element of this thread exceeds its column's current exponent bound (needs a raise)
+    auto convert = [&](const uint32_t (&wc)[GHU][NWH], int s, bool norms) -> int {
+      const int e = sh.ecur[0][j];
       const bool zero_col = (e == kNone);
       const int F = zero_col ? 0 : kTop - e;
       const double p0 = zero_col ? 0.0 : __longlong_as_double(static_cast<long long>(F + 1023) << 52);
       const double p32 = zero_col ? 0.0 : __longlong_as_double(static_cast<long long>(F - 32 + 1023) << 52);
       uint8_t* bst = bbuf + s * g.b_bytes;
+      int viol = 0;
 #pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const int u = st + 128 * k;
-        if (u >= NUNITS) continue;
-        const int c16 = u / BPAD;
-        uint32_t outw[kS][4];
+      for (int k = 0; k < GHU; ++k) {
+        const int hu = gt + GT * k;
+        if (hu >= NHU) continue;
+        const int u = hu >> 1, h = hu & 1, c16 = u / BPAD;
+        const int eb = Bits<T>::ebound(keymax(wc[k]));
+        viol |= (eb != kNone) && (zero_col || eb > e);
+        uint32_t outw[kS][2];
 #pragma unroll
-        for (int w4 = 0; w4 < 4; ++w4) {
+        for (int w4 = 0; w4 < 2; ++w4) {
           uint32_t lo[4], hi[4];
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
-            const int e16 = 4 * w4 + r;
+            const int e8 = 4 * w4 + r;
             double x;
-            if constexpr (kF64) x = __hiloint2double(static_cast<int>(w[k][2 * e16 + 1]), static_cast<int>(w[k][2 * e16]));
-            else x = static_cast<double>(__uint_as_float(w[k][e16]));
-            nacc = fma(x, x, nacc);
-            cacc += x;
+            if constexpr (kF64) x = __hiloint2double(static_cast<int>(wc[k][2 * e8 + 1]), static_cast<int>(wc[k][2 * e8]));
+            else x = static_cast<double>(__uint_as_float(wc[k][e8]));
+            if (norms) {
+              nacc = fma(x, x, nacc);
+              cacc += x;
+            }
             fixpt(x, p32, p0, lo[r], hi[r]);
           }
           // 4x4 byte transposes: word w4 of digit plane p = byte p of rows 4w4 .. 4w4+3
@@ -528,73 +592,141 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
 #pragma unroll
         for (int p = 0; p < kS; ++p) {
           const int n = p * BPAD + j;
-          uint4* dst = reinterpret_cast<uint4*>(bst + c16 * chB + (n >> 3) * 128 + (n & 7) * 16);
-          *dst = make_uint4(outw[p][0], outw[p][1], outw[p][2], outw[p][3]);
+          uint2* dst = reinterpret_cast<uint2*>(bst + c16 * chB + (n >> 3) * 128 + (n & 7) * 16 + h * 8);
+          *dst = make_uint2(outw[p][0], outw[p][1]);
         }
       }
-      fence_proxy_async();
-      named_bar(1, 128);
-      if (st == 0) {
-        sh.bflags[s] = newacc ? 1 : 0;
-        mbar_arrive(&sh.b_full[s]);
-      }
-      if (flush) epilogue(q - 1);
+      return viol;
+    };
+    // tile 0 sets the exponents (group 0 reads it, both groups synchronise)
+    if (grp == 0 && ntiles > 0) {
+      mbar_wait(&sh.x_full[0], 0);
+      uint32_t w0[GHU][NWH];
+      load_tile(0, w0);
+      publish(w0);
     }
-    epilogue(q);
+    named_bar(kBarAll, 2 * GT);
+    if (grp == 0) set_ecur(true);
+    named_bar(kBarAll, 2 * GT);
+    int s = grp % NS;
+    uint32_t ph = (grp / NS) & 1;
+    int k = 0;
+    int qlast = -1;
+#pragma unroll 1
+    for (int t = grp; t < ntiles; t += 2, ++k) {
+      const bool dbgt = g.dbg && blockIdx.x == 0 && gt == 0 && t < kDbgTiles;
+      if (dbgt) g.dbg[5 * kDbgTiles + t] = clock64();
+      mbar_wait(&sh.x_full[s], ph);
+      uint32_t wc[GHU][NWH];
+      load_tile(s, wc);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.x_empty[s]);     // values are in registers
+      if (t >= NS) mbar_wait(&sh.b_empty[s], ph ^ 1u);
+      if (dbgt) g.dbg[6 * kDbgTiles + t] = clock64();
+      int egen = *reinterpret_cast<volatile int*>(&sh.egen);
+      int viol = convert(wc, s, true);
+      fence_proxy_async();
+      int viol_any = named_bar_or(barg, GT, viol);
+      if (dbgt) g.dbg[7 * kDbgTiles + t] = clock64();
+      // ---- token: bookkeeping in tile order
+      if (t > 0) mbar_wait(&sh.tok[grp], grp == 1 ? (k & 1) : ((k - 1) & 1));
+      if (dbgt) g.dbg[8 * kDbgTiles + t] = clock64();
+      int newacc = (t % kMaxEpochTiles) == 0;
+      for (;;) {
+        // (the token holder alone writes egen, so eg is uniform here; the snapshots egen taken
+        // before the conversion may differ between threads, hence the reduction)
+        const int eg = *reinterpret_cast<volatile int*>(&sh.egen);
+        if (named_bar_or(barg, GT, eg != egen)) {  // exponents raised by the other group: redo
+          egen = eg;
+          viol = convert(wc, s, false);
+          fence_proxy_async();
+          viol_any = named_bar_or(barg, GT, viol);
+        }
+        if (!viol_any) break;
+        publish(wc);                             // raise the exponents of the offending columns
+        named_bar(barg, GT);
+        set_ecur(false);
+        named_bar(barg, GT);
+        if (gt == 0) sh.egen = egen + 1;
+        named_bar(barg, GT);
+        newacc = 1;
+      }
+      const int q0 = *reinterpret_cast<volatile int*>(&sh.qsh);
+      const int q = (newacc && t > 0) ? q0 + 1 : q0;
+      if (newacc && gt < BPAD) sh.ehist[q & 3][gt] = sh.ecur[0][gt];
+      named_bar(barg, GT);
+      if (gt == 0) {
+        sh.qsh = q;
+        sh.bflags[s] = newacc;
+        mbar_arrive(&sh.b_full[s]);
+        if (g.dbg && blockIdx.x == 0 && t < kDbgTiles) g.dbg[1 * kDbgTiles + t] = clock64();
+        mbar_arrive(&sh.tok[grp ^ 1]);           // hand the token to tile t + 1
+      }
+      if (dbgt) g.dbg[9 * kDbgTiles + t] = clock64();
+      if (newacc && t > 0) epilogue(q - 1);
+      qlast = q;
+      s += 2;
+      if (s >= NS) { s -= NS; ph ^= 1u; }
+    }
+    if (ntiles > 0 && ((ntiles - 1) & 1) == grp) epilogue(qlast);   // the last tile's group
     // norms and column sums: threads sharing column j combine in fixed order (half 0 units only)
     sh.nrm[st] = nacc;
     sh.csum[st] = cacc;
-    named_bar(1, 128);
+    named_bar(kBarAll, 2 * GT);
     if (half == 0 && st < BPAD && st < ncols) {
       double sum = 0.0, cs = 0.0;
-      for (int k = 0; k < 128 / BPAD; ++k) { sum += sh.nrm[st + k * BPAD]; cs += sh.csum[st + k * BPAD]; }
+      for (int kk = 0; kk < 2 * GT; ++kk) {
+        const int gtk = kk % GT;
+        if (((gtk >> 1) % BPAD) != st || gtk >= NHU) continue;
+        sum += sh.nrm[kk];
+        cs += sh.csum[kk];
+      }
       npart[static_cast<int64_t>(slab) * BPAD + st] = sum;
       cpart[static_cast<int64_t>(slab) * BPAD + st] = cs;
     }
   } else {
-    // ---------------------------------------------------------------- sketch generator (8 warps)
-    // TM = 2: warp -> (M tile, lane quarter), both 32-row K chunks of a tile (2 Philox calls);
-    // TM = 1: warp -> (K chunk, lane quarter), 1 Philox call.
-    constexpr int NK = TM == 2 ? 2 : 1;
-    const int gw = warp - kGen0;                     // 0..7
+    // ---------------------------------------------------------------- sketch generator (4 warps)
+    // warp -> TMEM lane quarter; each thread owns sketch row rl (and rl + 128 when TM = 2) and
+    // writes both 32-row K chunks of a tile (2 Philox calls per row) with one tcgen05.st each.
+    const int gw = warp - kGen0;                     // 0..3
     const int quarter = warp & 3;
-    const int tm = TM == 2 ? gw / 4 : 0;
-    const int kc0 = TM == 2 ? 0 : gw / 4;
-    const int rl = tm * 128 + quarter * 32 + lane;
-    const int r = half * ROWS + rl;
-    const bool live = r < ell;
     const uint64_t g32_0 = static_cast<uint64_t>((row_begin + r0) >> 5);
-    const uint32_t tbase = tmem + (static_cast<uint32_t>(32 * quarter) << 16) + ACOL0 + tm * 16 + kc0 * 8;
     for (int t = 0; t < ntiles; ++t) {
       const int sa = t & 1;
       if (t >= 2) mbar_wait(&sh.a_empty[sa], ((t >> 1) - 1) & 1);
-      uint32_t pk[16];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) pk[k] = 0u;
-      if (live) {
+      for (int tm = 0; tm < TM; ++tm) {
+        const int rl = tm * 128 + quarter * 32 + lane;
+        const int r = half * ROWS + rl;
+        uint32_t pk[16];
 #pragma unroll
-        for (int kc = 0; kc < NK; ++kc) {
-          const uint32_t grp = static_cast<uint32_t>(g32_0 + static_cast<uint64_t>(t) * (kKTile / 32) + kc0 + kc);
-          const U4 wv = philox4x32_10(grp, static_cast<uint32_t>(r), 0u, 0u, key0, key1);
-          const uint32_t ws[4] = {wv.x, wv.y, wv.z, wv.w};
+        for (int k = 0; k < 16; ++k) pk[k] = 0u;
+        if (r < ell) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            // 8 nibbles n = (sign, v): q = m_v (sign 0) or ~m_v = -m_v - 1 (sign 1), 4 per PRMT
-            const uint32_t w = ws[k], w4 = w << 4;
-            const uint32_t mlo = prmt(t0, t1, w & 0x7777u), mhi = prmt(t0, t1, (w >> 16) & 0x7777u);
-            const uint32_t slo = prmt(w, w4, 0x9D8Cu), shi = prmt(w, w4, 0xBFAEu);   // sign bytes 0x00/0xFF
-            pk[8 * kc + 2 * k] = mlo ^ slo;
-            pk[8 * kc + 2 * k + 1] = mhi ^ shi;
+          for (int kc = 0; kc < 2; ++kc) {
+            const uint32_t grp = static_cast<uint32_t>(g32_0 + static_cast<uint64_t>(t) * (kKTile / 32) + kc);
+            uint32_t kk0 = key0, kk1 = key1;
+            asm volatile("" : "+r"(kk0), "+r"(kk1));   // keep the key schedule in-loop (register budget)
+            const U4 wv = philox4x32_10(grp, static_cast<uint32_t>(r), 0u, 0u, kk0, kk1);
+            const uint32_t ws[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              // 8 nibbles n = (sign, v): q = m_v (sign 0) or ~m_v = -m_v - 1 (sign 1), 4 per PRMT
+              const uint32_t w = ws[k], w4 = w << 4;
+              const uint32_t mlo = prmt(t0, t1, w & 0x7777u), mhi = prmt(t0, t1, (w >> 16) & 0x7777u);
+              const uint32_t slo = prmt(w, w4, 0x9D8Cu), shi = prmt(w, w4, 0xBFAEu);   // sign bytes 0x00/0xFF
+              pk[8 * kc + 2 * k] = mlo ^ slo;
+              pk[8 * kc + 2 * k + 1] = mhi ^ shi;
+            }
           }
         }
+        tmem_st16(tmem + (static_cast<uint32_t>(32 * quarter) << 16) + ACOL0 + (sa * TM + tm) * 16, pk);
       }
-      const uint32_t ta = tbase + sa * TM * 16;
-      if constexpr (NK == 2) tmem_st16(ta, pk);
-      else tmem_st8(ta, pk);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sh.a_full[sa]);
+      if (g.dbg && blockIdx.x == 0 && gw == 0 && lane == 0 && t < kDbgTiles) g.dbg[t] = clock64();
     }
   }
   tc_fence_before();
@@ -694,7 +826,8 @@ inline cudaError_t k1tc_dispatch(const CUtensorMap& map, const K1TcArgs& a, cons
 inline cudaError_t k1tc_launch(const K1TcArgs& a, cudaStream_t st, int* nlaunch) {
   *nlaunch = 0;
   const int64_t m_loc = a.row_end - a.row_begin;
-  const k1tc::Geom g = k1tc::make_geom(a.ell, a.ncols, m_loc, a.f64, a.num_sms);
+  k1tc::Geom g = k1tc::make_geom(a.ell, a.ncols, m_loc, a.f64, a.num_sms);
+  g.dbg = a.dbg;
   CUtensorMap map;
   const int es = a.f64 ? 8 : 4;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(m_loc), static_cast<cuuint64_t>(a.ncols)};

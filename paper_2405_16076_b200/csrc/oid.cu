@@ -100,7 +100,7 @@ struct Bump {
 struct Layout {
   size_t S, gram, Ypart, k1part, k1npart, gB, gV, mu, mu_sorted, Yc, Tsc, tau, scal, J, tau_old, admit, counts,
       flags, counters, C, SJ, sjB, sjV, sjsig, sjw, sjZ, Sjpinv, Pexp, AJP, G, Gsum, Gpart, cB, cV, csig, cw, cZ, M,
-      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, sjG, cG, cBt, cZ2, total;
+      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, sjG, cG, cBt, cZ2, dbg, total;
 };
 
 int64_t m_local(const oid_params& p) { return p.row_end - p.row_begin; }
@@ -176,6 +176,7 @@ Layout make_layout(const oid_params& p) {
   L.gp = b.take((ell + 16) * d);
   L.gate = b.take(8 * sizeof(int));
   L.sjG = b.take(t * t * d);
+  L.dbg = b.take(k1tc::kDbgRows * k1tc::kDbgTiles * sizeof(long long));
   L.cBt = b.take(std::max<size_t>(1, l1 * l2) * d);
   L.cZ2 = b.take(std::max<size_t>(1, l1 * l2) * d);
   L.cG = b.take(std::max<size_t>(1, std::min(l1, l2) * std::min(l1, l2)) * d);
@@ -229,6 +230,7 @@ struct oid_ctx_s {
   int k1_mode_used = 0;
   bool tc_ok = false;
   bool cold_jacobi = false;   // diagnostics: OID_JACOBI_COLD=1 disables the warm starts
+  bool k1_debug = false;      // diagnostics: OID_K1_DEBUG=1 records K1 role timestamps (oid_get 10)
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_k1, ev_post, ev_est;
   char err[512] = {0};
 
@@ -443,6 +445,7 @@ oid_status do_sketch(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   a.t1 = static_cast<uint32_t>(ctx->qmag[4]) | (static_cast<uint32_t>(ctx->qmag[5]) << 8) |
          (static_cast<uint32_t>(ctx->qmag[6]) << 16) | (static_cast<uint32_t>(ctx->qmag[7]) << 24);
   a.num_sms = ctx->num_sms;
+  a.dbg = ctx->k1_debug ? ctx->ptr<long long>(ctx->L.dbg) : nullptr;
   const bool tc_call = want_tc && ctx->tc_ok && k1tc_call_ok(a);
   if (p.k1_mode == OID_K1_TC_INT8 && !tc_call)
     return ctx->fail(OID_EINVAL, "tensor-core K1 unavailable for this device/shape/alignment");
@@ -670,6 +673,7 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
     return bad(e);
   ctx->k1_ctas_per_sm = 1;
   ctx->cold_jacobi = getenv("OID_JACOBI_COLD") && atoi(getenv("OID_JACOBI_COLD")) != 0;
+  ctx->k1_debug = getenv("OID_K1_DEBUG") && atoi(getenv("OID_K1_DEBUG")) != 0;
   ctx->tc_ok = (prop.major == 10 && prop.minor == 0) && k1tc_supported(p->ell, p->b_max, p->dtype == OID_F64);
   double qd[16];
   for (int i = 0; i < 16; ++i) qd[i] = q[i] + 0.5;
@@ -944,6 +948,7 @@ oid_status oid_get(oid_ctx ctx, int32_t field, void* host_dst, size_t bytes, voi
     case 7: off = L.Ypart; need = sizeof(double) * (p.ell + 1) * p.b_max; break;
     case 8: off = L.Sjpinv; need = sizeof(double) * ctx->t * p.ell; break;
     case 9: off = L.counters; need = sizeof(int) * kNumJacobiUses * kMaxSweeps; break;
+    case 10: off = L.dbg; need = k1tc::kDbgRows * k1tc::kDbgTiles * sizeof(long long); break;
     default: return ctx->fail(OID_EINVAL, "unknown field %d", field);
   }
   if (bytes < need) return ctx->fail(OID_ESHAPE, "field %d needs %zu bytes", field, need);
