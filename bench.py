@@ -200,7 +200,8 @@ def main():
     grid, b, k, ell, dt, desc = WORKLOADS[args.workload]
     gen = ChannelFlow(*grid, seed=1003)
     m = gen.m
-    rb, re = (m * rank) // world, (m * (rank + 1)) // world
+    from paper_2405_16076_b200.sharded import ShardedIngest, row_slab
+    rb, re = row_slab(m, rank, world)
     m_loc = re - rb
     W, K, E = args.warmup, args.steps, args.e2e_steps
     nblk = W + K + E
@@ -219,18 +220,15 @@ def main():
     est_out = torch.empty(8, dtype=torch.float64, device=dev)
     sharded = world > 1
 
+    drv = ShardedIngest(eng)
+
     def step(X):
         if sharded:
-            eng.ingest_sketch(X)
-            dist.all_reduce(eng.partials(0))
-            eng.ingest_commit(X)
+            drv.ingest(X)                 # sketch -> all-reduce of the (l+1) x b partials -> commit
         else:
             eng.ingest_block(X)
         if not args.no_estimate:
-            eng.estimate_begin()
-            if sharded:
-                dist.all_reduce(eng.partials(1))
-            eng.estimate_end(est_out)
+            drv.estimate(est_out)         # basis-Gram partials all-reduced when sharded
 
     for s in range(W):
         step(blocks[s])

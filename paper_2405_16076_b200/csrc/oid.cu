@@ -331,7 +331,7 @@ oid_status pinv_assemble(oid_ctx ctx, cudaStream_t st, const double* B, int L, i
 oid_status spd_solve(oid_ctx ctx, cudaStream_t st, const double* A, int n, const double* R, int64_t ldr, bool in_t,
                      int nrhs, double* X, int64_t ldx, bool out_t, double kmax2, int* gate, double* kappa_out) {
   const Layout& L = ctx->L;
-  const size_t smem = sizeof(double) * (0);
+  const size_t smem = sizeof(double) * static_cast<size_t>(n) * ((n + kTriCtas - 1) / kTriCtas);
   tridiag_cluster_kernel<<<kTriCtas, 256, smem, st>>>(A, n, ctx->d(L.td), ctx->d(L.te), ctx->d(L.Vh), ctx->d(L.tauv),
                                                       ctx->d(L.gv), ctx->d(L.gp));
   CKL();
@@ -486,7 +486,7 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   int* gate = ctx->ptr<int>(L.gate);
   if (ell <= kTriMaxN && !ctx->cold_jacobi) {
     // tridiagonal fast path (tri.cuh); the eigenvector path below runs only when gate[1] is set
-    const size_t smem = sizeof(double) * (0);
+    const size_t smem = sizeof(double) * static_cast<size_t>(ell) * ((ell + kTriCtas - 1) / kTriCtas);
     tridiag_cluster_kernel<<<kTriCtas, 256, smem, st>>>(ctx->d(L.gram), ell, ctx->d(L.td), ctx->d(L.te), ctx->d(L.Vh),
                                                         ctx->d(L.tauv), ctx->d(L.gv), ctx->d(L.gp));
     CKL();
@@ -661,6 +661,10 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
   }
   if (p->ell <= kTriMaxN) {
     if ((e = cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
+      return bad(e);
+    if ((e = cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sizeof(double) * p->ell * ((p->ell + kTriCtas - 1) / kTriCtas)))) !=
+        cudaSuccess)
       return bad(e);
     const int ref_smem = static_cast<int>(sizeof(double) * 2 * kRefChunk * kTriMaxN);
     if ((e = cudaFuncSetAttribute(tri_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ref_smem)) != cudaSuccess)

@@ -52,6 +52,8 @@ tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__
   __shared__ double ssb[2][kTriCtas];
   __shared__ double kb[kTriCtas];
   __shared__ double wred[8];
+  __shared__ double tau_s[kTriMaxN], d_s[kTriMaxN], e_s[kTriMaxN];
+  extern __shared__ double vh_s[];       // [n][R]: this CTA's rows of every reflector (dynamic)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double a[kTriRW][kTriCL];
   int gi[kTriRW];
@@ -103,10 +105,10 @@ tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__
     } else {
       alpha = x0;
     }
-    if (tid == 0 && c == 0) tauv[k] = tau;
+    if (tid == 0) tau_s[k] = tau;
 #pragma unroll
     for (int r = 0; r < kTriRW; ++r)
-      if (gi[r] == k && lane == lk) { d[k] = tri_pick(a[r], qk); e[k] = alpha; }
+      if (gi[r] == k && lane == lk) { d_s[k] = tri_pick(a[r], qk); e_s[k] = alpha; }
     // v_i for my rows; p_i = tau sum_j A_ij v_j
     double vi[kTriRW], pi[kTriRW];
 #pragma unroll
@@ -132,7 +134,7 @@ tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__
       if (gi[r] > k) kw = fma(vi[r], pi[r], kw);
       if (gi[r] >= 0 && lane == 0) {
         loc[gi[r] - r0] = gi[r] > k ? pi[r] : 0.0;
-        if (gi[r] > k) Vh[gi[r] + static_cast<int64_t>(k) * n] = tau != 0.0 ? vi[r] : 0.0;
+        vh_s[k * R + (gi[r] - r0)] = (gi[r] > k && tau != 0.0) ? vi[r] : 0.0;
       }
     }
     if (lane == 0) wred[warp] = kw;
@@ -172,12 +174,22 @@ tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__
     if (n >= 2 && gi[r] == n - 2) {
       const double dd = __shfl_sync(0xffffffffu, tri_pick(a[r], (n - 2) >> 5), (n - 2) & 31);
       const double ee = __shfl_sync(0xffffffffu, tri_pick(a[r], (n - 1) >> 5), (n - 1) & 31);
-      if (lane == 0) { d[n - 2] = dd; e[n - 2] = ee; }
+      if (lane == 0) { d_s[n - 2] = dd; e_s[n - 2] = ee; }
     }
     if (gi[r] == n - 1) {
       const double dd = __shfl_sync(0xffffffffu, tri_pick(a[r], (n - 1) >> 5), (n - 1) & 31);
-      if (lane == 0) d[n - 1] = dd;
+      if (lane == 0) d_s[n - 1] = dd;
     }
+  }
+  __syncthreads();
+  // bulk writes: reflector rows of this CTA (Vh(i, k) for i in [r0, r1), k < n - 2), tau/d/e
+  for (int idx = tid; idx < (r1 - r0) * (n - 2); idx += 256) {
+    const int k = idx / (r1 - r0), il = idx - k * (r1 - r0);
+    Vh[(r0 + il) + static_cast<int64_t>(k) * n] = vh_s[k * R + il];
+  }
+  for (int k = tid; k < n; k += 256) {
+    if (c == 0 && k < n - 2) tauv[k] = tau_s[k];
+    if (k >= r0 && k < r1) { d[k] = d_s[k]; if (k < n - 1) e[k] = e_s[k]; }
   }
   cluster.sync();
 }
