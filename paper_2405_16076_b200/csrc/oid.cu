@@ -655,8 +655,8 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
     if ((e = cudaFuncSetAttribute(bjacobi_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big)) != cudaSuccess) return bad(e);
 #define BG_ATTR(TT, JB) \
     if ((e = cudaFuncSetAttribute(basis_gram_dirty_kernel<TT, JB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 184 * 1024)) != cudaSuccess) return bad(e)
-    BG_ATTR(double, 1); BG_ATTR(double, 2); BG_ATTR(double, 4); BG_ATTR(double, 7); BG_ATTR(double, 13);
-    BG_ATTR(float, 1); BG_ATTR(float, 2); BG_ATTR(float, 4); BG_ATTR(float, 7); BG_ATTR(float, 13);
+    BG_ATTR(double, 1); BG_ATTR(double, 2);
+    BG_ATTR(float, 1); BG_ATTR(float, 2);
 #undef BG_ATTR
   }
   if (p->ell <= kTriMaxN) {
@@ -772,17 +772,14 @@ oid_status oid_estimate_begin(oid_ctx ctx, void* stream) {
   const size_t stage_bytes = f64 ? bg_stage_elems<double>(t) * 8 : bg_stage_elems<float>(t) * 4;
   const int nstage = 2 * stage_bytes <= 180 * 1024 ? 2 : 1;
   const size_t smem = nstage * stage_bytes;
-  const int jb = (t + 31) / 32;
+  const int jbw = (t + 255) / 256;   // j blocks of 32 per warp (8 warps)
 #define BG_LAUNCH(TT, JB)                                                                                       \
   basis_gram_dirty_kernel<TT, JB><<<chunks, 256, smem, st>>>(ctx->ptr<TT>(L.C), ctx->m_loc, t, per, nstage,     \
                                                              ctx->ptr<int>(L.dlist), ctx->ptr<int>(L.counts),   \
                                                              ctx->d(L.Gpart))
 #define BG_DISPATCH(TT)                          \
-  if (jb <= 1) BG_LAUNCH(TT, 1);                  \
-  else if (jb <= 2) BG_LAUNCH(TT, 2);             \
-  else if (jb <= 4) BG_LAUNCH(TT, 4);             \
-  else if (jb <= 7) BG_LAUNCH(TT, 7);             \
-  else BG_LAUNCH(TT, 13)
+  if (jbw <= 1) BG_LAUNCH(TT, 1);                 \
+  else BG_LAUNCH(TT, 2)
   if (f64) { BG_DISPATCH(double); } else { BG_DISPATCH(float); }
 #undef BG_DISPATCH
 #undef BG_LAUNCH

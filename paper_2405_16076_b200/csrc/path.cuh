@@ -221,7 +221,17 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N> __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-template <typename T, int JB>
+// fp64 tensor-core MMA (DMMA): D (8x8) += A (8x4, row) * B (4x8, col).  Fragments: a = A[lane/4][lane%4],
+// b = B[lane%4][lane/4], c = C[lane/4][2 (lane%4) + {0, 1}].
+__device__ __forceinline__ void dmma_m8n8k4(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// Warp w owns the output columns j in [32 (w + 8 i), +32) for i < JBW (t <= 256 JBW); the 32 dirty
+// slots q of the group are the M dimension (4 m8 blocks), the basis rows the K dimension.
+template <typename T, int JBW>
 __global__ void __launch_bounds__(256) basis_gram_dirty_kernel(const T* __restrict__ C, int64_t m_loc, int t,
                                                                int64_t rows_per_chunk, int nstage,
                                                                const int* __restrict__ list,
@@ -235,7 +245,8 @@ __global__ void __launch_bounds__(256) basis_gram_dirty_kernel(const T* __restri
   __shared__ int dl[32];
   const int nd = counts[2];
   if (nd == 0) return;
-  const int tid = threadIdx.x, tq = tid & 7, tj = tid >> 3;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g4 = lane >> 2, i4 = lane & 3;
   const int64_t r0 = static_cast<int64_t>(blockIdx.x) * rows_per_chunk;
   const int64_t r1 = min(m_loc, r0 + rows_per_chunk);
   const int ntile = static_cast<int>((r1 - r0 + kBgRows - 1) / kBgRows);
@@ -263,11 +274,13 @@ __global__ void __launch_bounds__(256) basis_gram_dirty_kernel(const T* __restri
 
   for (int q0 = 0; q0 < nd; q0 += 32) {
     if (tid < 32) dl[tid] = (q0 + tid < nd) ? list[q0 + tid] : -1;
-    double acc[4][JB];
+    double acc[JBW][4][4][2];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int b = 0; b < JBW; ++b)
 #pragma unroll
-      for (int b = 0; b < JB; ++b) acc[a][b] = 0.0;
+      for (int mm = 0; mm < 4; ++mm)
+#pragma unroll
+        for (int n = 0; n < 4; ++n) { acc[b][mm][n][0] = 0.0; acc[b][mm][n][1] = 0.0; }
     __syncthreads();
     load(0, 0);
     cp_async_commit();
@@ -284,32 +297,41 @@ __global__ void __launch_bounds__(256) basis_gram_dirty_kernel(const T* __restri
         dt[rr][q] = d >= 0 ? static_cast<double>(tile[d * P + rr]) : 0.0;
       }
       __syncthreads();
-#pragma unroll 4
-      for (int rr = 0; rr < kBgRows; ++rr) {
-        double dv[4], xv[JB];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) dv[a] = dt[rr][tq + 8 * a];
+      for (int ks = 0; ks < kBgRows; ks += 4) {
+        double a[4];
 #pragma unroll
-        for (int b = 0; b < JB; ++b) {
-          const int j = tj + 32 * b;
-          xv[b] = j < t ? static_cast<double>(tile[j * P + rr]) : 0.0;
+        for (int mm = 0; mm < 4; ++mm) a[mm] = dt[ks + i4][8 * mm + g4];
+#pragma unroll
+        for (int b = 0; b < JBW; ++b) {
+          const int jb = 32 * (warp + 8 * b);
+          if (jb >= t) continue;                             // warp-uniform
+#pragma unroll
+          for (int n = 0; n < 4; ++n) {
+            const int j = jb + 8 * n + g4;
+            const double bv = j < t ? static_cast<double>(tile[j * P + ks + i4]) : 0.0;
+#pragma unroll
+            for (int mm = 0; mm < 4; ++mm) dmma_m8n8k4(acc[b][mm][n], a[mm], bv);
+          }
         }
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < JB; ++b) acc[a][b] = fma(dv[a], xv[b], acc[a][b]);
       }
       __syncthreads();
       if (nstage == 1 && it + 1 < ntile) load(it + 1, 0);
     }
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int q = tq + 8 * a;
-      if (q0 + q >= nd) continue;
+    for (int b = 0; b < JBW; ++b) {
+      const int jb = 32 * (warp + 8 * b);
 #pragma unroll
-      for (int b = 0; b < JB; ++b) {
-        const int j = tj + 32 * b;
-        if (j < t) out[(q0 + q) + static_cast<int64_t>(j) * t] = acc[a][b];
+      for (int mm = 0; mm < 4; ++mm) {
+        const int q = 8 * mm + g4;
+        if (q0 + q >= nd) continue;
+#pragma unroll
+        for (int n = 0; n < 4; ++n)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int j = jb + 8 * n + 2 * i4 + h;
+            if (j < t) out[(q0 + q) + static_cast<int64_t>(j) * t] = acc[b][mm][n][h];
+          }
       }
     }
   }
