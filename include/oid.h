@@ -155,7 +155,11 @@ oid_status oid_finalize(oid_ctx ctx, int64_t* J_host, double* P, int32_t P_on_de
           7 last ingest partials ((ell+1) * ncols), 8 S_J^+ (k x ell),
           9 Jacobi rotation counts per sweep (3 x 48 int32: Gram, S_J, NA-Hutch++ core),
           10 K1 role timestamps of CTA 0 (10 x 4096 int64 clock64; recorded when the environment
-             variable OID_K1_DEBUG=1 was set at oid_init). */
+             variable OID_K1_DEBUG=1 was set at oid_init),
+          11 basis Gram G = A_J^T A_J of the last estimate (k x k; rows/columns of vacant
+             slots zero),
+          12 tridiagonalisation phase timestamps of the last ingest (4 x 1024 int64 clock64 of
+             cluster CTA 0; recorded with OID_K1_DEBUG=1). */
 oid_status oid_get(oid_ctx ctx, int32_t field, void* host_dst, size_t bytes, void* stream);
 
 /* Counters and CUDA-event timings (synchronizes the context's recorded events).

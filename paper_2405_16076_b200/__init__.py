@@ -215,7 +215,7 @@ class Engine:
         shapes = {0: ((t,), np.int64), 1: ((t,), np.float64), 2: ((n_obs, ell), np.float64),
                   3: ((ell, ell), np.float64), 4: ((8,), np.float64), 5: ((t + bm,), np.float64),
                   6: ((ell,), np.float64), 7: (((ell + 1) * bm,), np.float64), 8: ((ell, t), np.float64),
-                  9: ((3, 48), np.int32), 10: ((10, 4096), np.int64)}
+                  9: ((3, 48), np.int32), 10: ((10, 4096), np.int64), 11: ((t, t), np.float64), 12: ((1024, 4), np.int64)}
         shape, dt = shapes[field]
         a = np.empty(shape, dtype=dt)
         self._check(_lib.oid_get(self.h, field, ctypes.c_void_p(a.ctypes.data), a.nbytes, self._st()), "oid_get")

@@ -488,9 +488,11 @@ __global__ void frob_scale_kernel(const double* __restrict__ A, int64_t len, dou
 }
 
 // One-sided (Hestenes) Jacobi SVD of a small L x n matrix B (col-major) in ONE CTA with B and V
-// resident in shared memory (no grid barriers): round-robin parallel ordering, one warp per
-// column pair, shuffle dot products, the same rotation rule and stopping test as bjacobi_kernel.
+// resident in shared memory (no grid barriers): round-robin parallel ordering, kSvdG lanes per
+// column pair (two pairs per warp, so every pair of a round runs at once), shuffle dot
+// products, the same rotation rule and stopping test as bjacobi_kernel.
 // On exit B <- B V (orthogonal columns), V (n x n), sig = column norms.  Dynamic smem: (L + n) n.
+constexpr int kSvdG = 16;
 __global__ void __launch_bounds__(1024) small_svd_kernel(double* __restrict__ Bg, int L, int n, double* __restrict__ Vg,
                                                         double* __restrict__ sig, int* __restrict__ counters,
                                                         int max_sweeps, double tol, const int* __restrict__ gate) {
@@ -499,8 +501,9 @@ __global__ void __launch_bounds__(1024) small_svd_kernel(double* __restrict__ Bg
   double* B = ss_smem;            // [n][L]
   double* V = ss_smem + static_cast<int64_t>(L) * n;   // [n][n]
   __shared__ double red[32];
-  __shared__ int nrot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+  const int sub = lane / kSvdG, gl = lane % kSvdG;
+  constexpr int ppw = 32 / kSvdG;
   double f2 = 0.0;
   for (int e = tid; e < L * n; e += blockDim.x) { const double x = Bg[e]; B[e] = x; f2 = fma(x, x, f2); }
   for (int e = tid; e < n * n; e += blockDim.x) V[e] = (e % n == e / n) ? 1.0 : 0.0;
@@ -511,31 +514,38 @@ __global__ void __launch_bounds__(1024) small_svd_kernel(double* __restrict__ Bg
   double fro2 = 0.0;
   for (int w = 0; w < nw; ++w) fro2 += red[w];
   const double floor2 = 1e-28 * fro2;
+  const double tol2 = tol * tol;
   const int nn = n + (n & 1), np = nn / 2, m1 = nn - 1;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
-    if (tid == 0) nrot = 0;
-    __syncthreads();
+    int rotated = 0;
     for (int k = 0; k < max(m1, 1); ++k) {
-      for (int pi = warp; pi < np; pi += nw) {
+      for (int base = warp * ppw; base < np; base += nw * ppw) {    // warp-uniform
+        const int pi = base + sub;
         int a, b;
-        if (pi == 0) { a = m1; b = k; } else { a = (k + pi) % m1; b = (k - pi + m1) % m1; }
         if (m1 == 0) { a = 0; b = 1; }
+        else if (pi == 0) { a = m1; b = k; }
+        else {
+          a = k + pi; if (a >= m1) a -= m1;
+          b = k - pi; if (b < 0) b += m1;
+        }
         const int p = min(a, b), q = max(a, b);
-        if (q >= n) continue;
+        const bool act = pi < np && q < n;
         double* bp = B + static_cast<int64_t>(p) * L;
         double* bq = B + static_cast<int64_t>(q) * L;
         double al = 0.0, be = 0.0, ga = 0.0;
-        for (int i = lane; i < L; i += 32) {
-          const double x = bp[i], y = bq[i];
-          al = fma(x, x, al); be = fma(y, y, be); ga = fma(x, y, ga);
+        if (act) {
+          for (int i = gl; i < L; i += kSvdG) {
+            const double x = bp[i], y = bq[i];
+            al = fma(x, x, al); be = fma(y, y, be); ga = fma(x, y, ga);
+          }
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
+        for (int o = kSvdG / 2; o > 0; o >>= 1) {
           al += __shfl_xor_sync(0xffffffffu, al, o);
           be += __shfl_xor_sync(0xffffffffu, be, o);
           ga += __shfl_xor_sync(0xffffffffu, ga, o);
         }
-        if (ga != 0.0 && ga * ga > tol * tol * (al * be) && fmin(al, be) > floor2) {
+        if (act && ga != 0.0 && ga * ga > tol2 * (al * be) && fmin(al, be) > floor2) {
           // rotation parameters from the reciprocal square root (rsqrt + Newton), one division
           const double zeta = (be - al) / (2.0 * ga);
           double t;
@@ -550,27 +560,26 @@ __global__ void __launch_bounds__(1024) small_svd_kernel(double* __restrict__ Bg
           double cs = rsqrt(u);
           cs = cs * fma(-0.5 * u, cs * cs, 1.5);
           const double sn = cs * t;
-          for (int i = lane; i < L; i += 32) {
+          for (int i = gl; i < L; i += kSvdG) {
             const double x = bp[i], y = bq[i];
             bp[i] = cs * x - sn * y;
             bq[i] = sn * x + cs * y;
           }
           double* vp = V + static_cast<int64_t>(p) * n;
           double* vq = V + static_cast<int64_t>(q) * n;
-          for (int i = lane; i < n; i += 32) {
+          for (int i = gl; i < n; i += kSvdG) {
             const double x = vp[i], y = vq[i];
             vp[i] = cs * x - sn * y;
             vq[i] = sn * x + cs * y;
           }
-          if (lane == 0) atomicAdd(&nrot, 1);
+          rotated = 1;
         }
       }
       __syncthreads();
     }
-    if (tid == 0) counters[sweep] = nrot;
-    const int r = nrot;
-    __syncthreads();
-    if (r == 0) break;
+    const int any = __syncthreads_or(rotated);
+    if (tid == 0) counters[sweep] = any;
+    if (!any) break;
   }
   for (int e = tid; e < L * n; e += blockDim.x) Bg[e] = B[e];
   for (int e = tid; e < n * n; e += blockDim.x) Vg[e] = V[e];

@@ -19,6 +19,7 @@
 #include "dense.cuh"
 #include "k1_simt.cuh"
 #include "k1_tc.cuh"
+#include "gram_tc.cuh"
 #include "path.cuh"
 #include "tri.cuh"
 
@@ -176,7 +177,7 @@ Layout make_layout(const oid_params& p) {
   L.gp = b.take((ell + 16) * d);
   L.gate = b.take(8 * sizeof(int));
   L.sjG = b.take(t * t * d);
-  L.dbg = b.take(k1tc::kDbgRows * k1tc::kDbgTiles * sizeof(long long));
+  L.dbg = b.take((k1tc::kDbgRows + 1) * k1tc::kDbgTiles * sizeof(long long));
   L.cBt = b.take(std::max<size_t>(1, l1 * l2) * d);
   L.cZ2 = b.take(std::max<size_t>(1, l1 * l2) * d);
   L.cG = b.take(std::max<size_t>(1, std::min(l1, l2) * std::min(l1, l2)) * d);
@@ -229,9 +230,18 @@ struct oid_ctx_s {
   int64_t launches = 0, k1_launches = 0;
   int k1_mode_used = 0;
   bool tc_ok = false;
+  bool bg_tc = false;         // A9 on the TMA + DMMA kernel (gram_tc.cuh); else the cp.async kernel
+  CUtensorMap bg_map{};       // basis slab C as a 2-D tensor {m_loc rows, t columns}
   bool cold_jacobi = false;   // diagnostics: OID_JACOBI_COLD=1 disables the warm starts
   bool k1_debug = false;      // diagnostics: OID_K1_DEBUG=1 records K1 role timestamps (oid_get 10)
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_k1, ev_post, ev_est;
+  // Side stream (highest priority) for the latency-bound chains that do not depend on the
+  // HBM-bound kernels of the caller's stream: the Alg 4 factorisation (A8) runs beside the basis
+  // copy (A7) and the basis-Gram-independent part of Alg 8 (A10) beside the basis Gram (A9).
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int bg_free_sms = 12;       // SMs the A9 kernel leaves to the side stream (measured best of 0/4/12/20)
+  bool use_side = true;       // diagnostics: OID_NO_SIDE=1 runs everything on the caller's stream
   char err[512] = {0};
 
   template <typename T> T* ptr(size_t off) const { return reinterpret_cast<T*>(ws + off); }
@@ -333,7 +343,7 @@ oid_status spd_solve(oid_ctx ctx, cudaStream_t st, const double* A, int n, const
   const Layout& L = ctx->L;
   const size_t smem = sizeof(double) * static_cast<size_t>(n) * ((n + kTriCtas - 1) / kTriCtas);
   tridiag_cluster_kernel<<<kTriCtas, 256, smem, st>>>(A, n, ctx->d(L.td), ctx->d(L.te), ctx->d(L.Vh), ctx->d(L.tauv),
-                                                      ctx->d(L.gv), ctx->d(L.gp));
+                                                      nullptr);
   CKL();
   multisect_kernel<<<(n * 32 + 255) / 256, 256, sizeof(double) * 2 * n, st>>>(ctx->d(L.td), ctx->d(L.te), n,
                                                                             ctx->d(L.mu_sorted));
@@ -397,6 +407,21 @@ struct EvScope {
     v->emplace_back(b, e);
   }
 };
+
+// side stream waits for all work enqueued on st so far
+oid_status fork_side(oid_ctx ctx, cudaStream_t st) {
+  if (!ctx->use_side) return OID_OK;
+  CK(cudaEventRecord(ctx->ev_fork, st));
+  CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+  return OID_OK;
+}
+// st waits for all work enqueued on the side stream so far
+oid_status join_side(oid_ctx ctx, cudaStream_t st) {
+  if (!ctx->use_side) return OID_OK;
+  CK(cudaEventRecord(ctx->ev_join, ctx->side));
+  CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
+  return OID_OK;
+}
 
 template <typename T>
 oid_status launch_k1_simt(oid_ctx ctx, cudaStream_t st, const T* X, int64_t ld, int nc) {
@@ -473,12 +498,14 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   double* Yp = ctx->d(L.Ypart);
   double* scal = ctx->d(L.scal);
   EvScope ev(ctx, st, &ctx->ev_post);
+  // the side stream's previous work shares the tridiagonal workspace with A4 below
+  oid_status s = join_side(ctx, st);
+  if (s != OID_OK) return s;
   // A3: S <- [S, Y], SS^T += YY^T, ||A_obs||^2 += sum n_j
   gram_update_kernel<<<blocks_for(int64_t(ell) * ell), 256, 0, st>>>(Yp, ell, nc, ctx->d(L.gram), ctx->d(L.S), ctx->n_obs,
                                                                     scal);
   CKL();
   // A4: spectrum of the Gram and lambda; A5: ridge scores
-  oid_status s;
   const int ns = t + nc;
   gather_scored_kernel<<<blocks_for(int64_t(ell) * ns), 256, 0, st>>>(ctx->d(L.S), ctx->ptr<int64_t>(L.J), t, Yp, nc, ell,
                                                                       ctx->d(L.Yc));
@@ -488,7 +515,7 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
     // tridiagonal fast path (tri.cuh); the eigenvector path below runs only when gate[1] is set
     const size_t smem = sizeof(double) * static_cast<size_t>(ell) * ((ell + kTriCtas - 1) / kTriCtas);
     tridiag_cluster_kernel<<<kTriCtas, 256, smem, st>>>(ctx->d(L.gram), ell, ctx->d(L.td), ctx->d(L.te), ctx->d(L.Vh),
-                                                        ctx->d(L.tauv), ctx->d(L.gv), ctx->d(L.gp));
+                                                        ctx->d(L.tauv), ctx->k1_debug ? ctx->ptr<long long>(L.dbg) + k1tc::kDbgRows * k1tc::kDbgTiles : nullptr);
     CKL();
     multisect_kernel<<<(ell * 32 + 255) / 256, 256, sizeof(double) * 2 * ell, st>>>(ctx->d(L.td), ctx->d(L.te), ell,
                                                                                   ctx->d(L.mu));
@@ -530,6 +557,9 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
                                   ctx->factor, static_cast<uint32_t>(ctx->epoch), ctx->n_obs, ctx->key0, ctx->key1,
                                   ctx->ptr<int>(L.admit), ctx->ptr<int>(L.counts), scal, ctx->ptr<int>(L.dirty));
   CKL();
+  // A8 runs on the side stream, beside the basis copy
+  s = fork_side(ctx, st);
+  if (s != OID_OK) return s;
   // A7: basis copy of this shard's rows
   {
     dim3 grid(std::max(1u, std::min(blocks_for(ctx->m_loc), 2048u)), nc + t);
@@ -542,30 +572,31 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
     CKL();
   }
   ctx->n_obs += nc;
+  cudaStream_t cs = ctx->use_side ? ctx->side : st;
   // A8: Alg 4 kept implicit: S_J^+ per epoch.  Fast path: S_J^+ = (S_J^T S_J)^-1 S_J^T
   // by the cluster tridiagonalisation when kappa(S_J) <= 1e5 (no R9 cutoff can act); else the
   // one-sided Jacobi SVD pseudo-inverse (gated on the device).
-  gather_sj_kernel<<<blocks_for(int64_t(ell) * t), 256, 0, st>>>(ctx->d(L.S), ctx->ptr<int64_t>(L.J), t, ell, ctx->d(L.SJ));
+  gather_sj_kernel<<<blocks_for(int64_t(ell) * t), 256, 0, cs>>>(ctx->d(L.S), ctx->ptr<int64_t>(L.J), t, ell, ctx->d(L.SJ));
   CKL();
   int* sjgate = ctx->ptr<int>(L.gate) + 2;
   if (t <= kTriMaxN) {
-    s = gemm(ctx, st, true, false, t, t, ell, 1.0, ctx->d(L.SJ), ell, ctx->d(L.SJ), ell, 0.0, ctx->d(L.sjG), t);
+    s = gemm(ctx, cs, true, false, t, t, ell, 1.0, ctx->d(L.SJ), ell, ctx->d(L.SJ), ell, 0.0, ctx->d(L.sjG), t);
     if (s != OID_OK) return s;
-    fill_vacant_diag_kernel<<<1, 256, 0, st>>>(ctx->d(L.sjG), t, ctx->ptr<int64_t>(L.J));
+    fill_vacant_diag_kernel<<<1, 256, 0, cs>>>(ctx->d(L.sjG), t, ctx->ptr<int64_t>(L.J));
     CKL();
-    s = spd_solve(ctx, st, ctx->d(L.sjG), t, ctx->d(L.SJ), ell, true, ell, ctx->d(L.Sjpinv), t, false, 1e10, sjgate,
+    s = spd_solve(ctx, cs, ctx->d(L.sjG), t, ctx->d(L.SJ), ell, true, ell, ctx->d(L.Sjpinv), t, false, 1e10, sjgate,
                   scal + SC_KAPPA);
     if (s != OID_OK) return s;
   } else {
-    set_flag_kernel<<<1, 1, 0, st>>>(sjgate, 0, 1);
+    set_flag_kernel<<<1, 1, 0, cs>>>(sjgate, 0, 1);
     CKL();
   }
   const int* fb = sjgate + 1;
-  s = gemm(ctx, st, false, false, ell, t, t, 1.0, ctx->d(L.SJ), ell, ctx->d(L.sjV), t, 0.0, ctx->d(L.sjB), ell, fb);
+  s = gemm(ctx, cs, false, false, ell, t, t, 1.0, ctx->d(L.SJ), ell, ctx->d(L.sjV), t, 0.0, ctx->d(L.sjB), ell, fb);
   if (s != OID_OK) return s;
-  s = jacobi(ctx, st, ctx->d(L.sjB), ell, t, ctx->d(L.sjV), ctx->d(L.sjsig), 1, true, fb);
+  s = jacobi(ctx, cs, ctx->d(L.sjB), ell, t, ctx->d(L.sjV), ctx->d(L.sjsig), 1, true, fb);
   if (s != OID_OK) return s;
-  s = pinv_assemble(ctx, st, ctx->d(L.sjB), ell, t, ctx->d(L.sjV), ctx->d(L.sjsig), ctx->d(L.sjw), ctx->d(L.sjZ),
+  s = pinv_assemble(ctx, cs, ctx->d(L.sjB), ell, t, ctx->d(L.sjV), ctx->d(L.sjsig), ctx->d(L.sjw), ctx->d(L.sjZ),
                     ctx->d(L.Sjpinv), scal + SC_KAPPA, OID_FLAG_SJ_RANK_DEFICIENT, fb);
   if (s != OID_OK) return s;
   ctx->epoch += 1;
@@ -588,6 +619,93 @@ oid_status explicit_P(oid_ctx ctx, cudaStream_t st) {
   const Layout& L = ctx->L;
   return gemm(ctx, st, false, false, ctx->t, static_cast<int>(ctx->n_obs), ctx->p.ell, 1.0, ctx->d(L.Sjpinv), ctx->t,
               ctx->d(L.S), ctx->p.ell, 0.0, ctx->d(L.Pexp), ctx->t);
+}
+
+// Alg 8 factors that do not involve the basis Gram G (A10): P = S_J^+ S, Omega A_J P, the core
+// pseudo-inverse M, Omega_k A P^T, the third-block trace terms and P P^T; enqueued on stream cs.
+oid_status estimate_pre(oid_ctx ctx, cudaStream_t st) {
+  const Layout& L = ctx->L;
+  const oid_params& p = ctx->p;
+  const int t = ctx->t, ell = p.ell, l1 = p.ell1, l2 = p.ell2, l3 = p.ell3;
+  const int n = static_cast<int>(ctx->n_obs);
+  double* S = ctx->d(L.S);
+  double* scal = ctx->d(L.scal);
+  oid_status s = explicit_P(ctx, st);                                                 // P = S_J^+ S
+  if (s != OID_OK) return s;
+  double* P = ctx->d(L.Pexp);
+  double* AJP = ctx->d(L.AJP);
+  s = gemm(ctx, st, false, false, ell, n, t, 1.0, ctx->d(L.SJ), ell, P, t, 0.0, AJP, ell);   // Omega A_J P
+  if (s != OID_OK) return s;
+  CK(cudaMemsetAsync(scal + SC_T1, 0, 4 * sizeof(double), st));
+  if (l1 > 0 && l2 > 0) {
+    // M = (Omega1 A (Omega2 A_J P)^T)^+   (P:595)
+    s = gemm(ctx, st, false, true, l1, l2, n, 1.0, S, ell, AJP + l1, ell, 0.0, ctx->d(L.cB), l1);
+    if (s != OID_OK) return s;
+    // M = B^+ (l2 x l1) by the one-sided Jacobi SVD pseudo-inverse with the R9 cutoff: the core
+    // is routinely ill-conditioned (kappa 1e5-1e17 on C3), so no normal-equation fast path
+    const int* cgate = nullptr;
+    const int lo = std::min(l1, l2), hi = std::max(l1, l2);
+    if (static_cast<size_t>(hi + lo) * lo * sizeof(double) <= kSmallSvdSmem) {
+      // small pseudo-inverse in one CTA: SVD of the tall orientation (hi x lo)
+      double* Bt = ctx->d(L.cBt);
+      if (l1 < l2) {
+        transpose_kernel<<<blocks_for(int64_t(l1) * l2), 256, 0, st>>>(ctx->d(L.cB), l1, l2, Bt, cgate);
+        CKL();
+      } else {
+        CK(cudaMemcpyAsync(Bt, ctx->d(L.cB), sizeof(double) * l1 * l2, cudaMemcpyDeviceToDevice, st));
+      }
+      int* counters = ctx->ptr<int>(L.counters) + 2 * kMaxSweeps;
+      small_svd_kernel<<<1, 1024, static_cast<size_t>(hi + lo) * lo * sizeof(double), st>>>(
+          Bt, hi, lo, ctx->d(L.cV), ctx->d(L.csig), counters, kMaxSweeps, 4e-14 * std::max(1.0, std::sqrt(hi / 16.0)),
+          cgate);
+      CKL();
+      if (l1 < l2) {
+        // pinv(B^T) (l1 x l2) = V diag(w) Bt^T; M = pinv(B) = pinv(B^T)^T (l2 x l1)
+        s = pinv_assemble(ctx, st, Bt, hi, lo, ctx->d(L.cV), ctx->d(L.csig), ctx->d(L.cw), ctx->d(L.cZ), ctx->d(L.cZ2),
+                          nullptr, 0, cgate);
+        if (s != OID_OK) return s;
+        transpose_kernel<<<blocks_for(int64_t(l1) * l2), 256, 0, st>>>(ctx->d(L.cZ2), l1, l2, ctx->d(L.M), cgate);
+        CKL();
+      } else {
+        s = pinv_assemble(ctx, st, Bt, hi, lo, ctx->d(L.cV), ctx->d(L.csig), ctx->d(L.cw), ctx->d(L.cZ), ctx->d(L.M),
+                          nullptr, 0, cgate);
+        if (s != OID_OK) return s;
+      }
+    } else {
+      s = jacobi(ctx, st, ctx->d(L.cB), l1, l2, ctx->d(L.cV), ctx->d(L.csig), 2, false, cgate);
+      if (s != OID_OK) return s;
+      s = pinv_assemble(ctx, st, ctx->d(L.cB), l1, l2, ctx->d(L.cV), ctx->d(L.csig), ctx->d(L.cw), ctx->d(L.cZ), ctx->d(L.M),
+                        nullptr, 0, cgate);
+      if (s != OID_OK) return s;
+    }
+    // term1 = tr(M (Omega1 A P^T) G (Omega2 A P^T)^T)
+    s = gemm(ctx, st, false, true, l1, t, n, 1.0, S, ell, P, t, 0.0, ctx->d(L.X1), l1);
+    if (s != OID_OK) return s;
+    s = gemm(ctx, st, false, true, l2, t, n, 1.0, S + l1, ell, P, t, 0.0, ctx->d(L.X2), l2);
+    if (s != OID_OK) return s;
+    s = gemm(ctx, st, false, false, l2, t, l1, 1.0, ctx->d(L.M), l2, ctx->d(L.X1), l1, 0.0, ctx->d(L.Q1), l2);
+    if (s != OID_OK) return s;
+  }
+  if (l3 > 0) {
+    // t3a = tr((Omega3 A)(Omega3 A_J P)^T)
+    frob_dot_kernel<<<1, 256, 0, st>>>(S + l1 + l2, ell, AJP + l1 + l2, ell, l3, n, scal + SC_T3A);
+    CKL();
+    if (l1 > 0 && l2 > 0) {
+      // t3b = tr((Omega3 A_J P)(Omega2 A)^T M (Omega1 A)(Omega3 A_J P)^T)
+      s = gemm(ctx, st, false, true, l3, l2, n, 1.0, AJP + l1 + l2, ell, S + l1, ell, 0.0, ctx->d(L.R1), l3);
+      if (s != OID_OK) return s;
+      s = gemm(ctx, st, false, true, l3, l1, n, 1.0, AJP + l1 + l2, ell, S, ell, 0.0, ctx->d(L.R2t), l3);
+      if (s != OID_OK) return s;
+      s = gemm(ctx, st, false, false, l3, l1, l2, 1.0, ctx->d(L.R1), l3, ctx->d(L.M), l2, 0.0, ctx->d(L.R3), l3);
+      if (s != OID_OK) return s;
+      frob_dot_kernel<<<1, 256, 0, st>>>(ctx->d(L.R3), l3, ctx->d(L.R2t), l3, l3, l1, scal + SC_T3B);
+      CKL();
+    }
+  }
+  // tr(G P P^T) = ||A_J P||_F^2
+  s = gemm(ctx, st, false, true, t, t, n, 1.0, P, t, P, t, 0.0, ctx->d(L.PPt), t);
+  if (s != OID_OK) return s;
+  return OID_OK;
 }
 
 }  // namespace
@@ -675,10 +793,42 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
   if ((e = cudaFuncSetAttribute(small_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(kSmallSvdSmem))) != cudaSuccess)
     return bad(e);
+  {
+    int lo = 0, hi = 0;
+    if ((e = cudaDeviceGetStreamPriorityRange(&lo, &hi)) != cudaSuccess) return bad(e);
+    if ((e = cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, hi)) != cudaSuccess) return bad(e);
+    if ((e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming)) != cudaSuccess) return bad(e);
+    if ((e = cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming)) != cudaSuccess) return bad(e);
+    if (getenv("OID_BG_FREE")) ctx->bg_free_sms = std::max(0, atoi(getenv("OID_BG_FREE")));
+    ctx->use_side = !(getenv("OID_NO_SIDE") && atoi(getenv("OID_NO_SIDE")) != 0);
+  }
   ctx->k1_ctas_per_sm = 1;
   ctx->cold_jacobi = getenv("OID_JACOBI_COLD") && atoi(getenv("OID_JACOBI_COLD")) != 0;
   ctx->k1_debug = getenv("OID_K1_DEBUG") && atoi(getenv("OID_K1_DEBUG")) != 0;
   ctx->tc_ok = (prop.major == 10 && prop.minor == 0) && k1tc_supported(p->ell, p->b_max, p->dtype == OID_F64);
+  {
+    // A9 tensor-map of the basis slab (fixed for the life of the context)
+    const bool f64 = p->dtype == OID_F64;
+    const int es = f64 ? 8 : 4;
+    const Layout& Lb = ctx->L;
+    if (prop.major == 10 && ctx->t <= 512 && (ctx->m_loc * es) % 16 == 0 && k1tc_encoder() != nullptr &&
+        !(getenv("OID_BG_SIMT") && atoi(getenv("OID_BG_SIMT")) != 0)) {
+      const cuuint64_t dims[2] = {static_cast<cuuint64_t>(ctx->m_loc), static_cast<cuuint64_t>(ctx->t)};
+      const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ctx->m_loc) * es};
+      const cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / es), static_cast<cuuint32_t>(std::min(ctx->t, 256))};
+      const cuuint32_t estr[2] = {1, 1};
+      CUresult cr = k1tc_encoder()(&ctx->bg_map, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                                   ctx->ws + Lb.C, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      ctx->bg_tc = cr == CUDA_SUCCESS;
+    }
+    const int bgmax = 200 * 1024 + 1024;
+#define BGT_ATTR(TT, CW) \
+    if ((e = cudaFuncSetAttribute(bgtc::basis_gram_tc_kernel<TT, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, bgmax)) != cudaSuccess) return bad(e)
+    BGT_ATTR(double, 8); BGT_ATTR(double, 16); BGT_ATTR(float, 8); BGT_ATTR(float, 16);
+#undef BGT_ATTR
+  }
   double qd[16];
   for (int i = 0; i < 16; ++i) qd[i] = q[i] + 0.5;
   if ((e = cudaMemcpyToSymbolAsync(c_qtab_f64, qd, sizeof(qd), 0, cudaMemcpyHostToDevice, st)) != cudaSuccess) return bad(e);
@@ -759,10 +909,39 @@ oid_status oid_estimate_begin(oid_ctx ctx, void* stream) {
   const Layout& L = ctx->L;
   const int t = ctx->t;
   EvScope ev(ctx, st, &ctx->ev_est);
+  // A10 factors that do not need G: on the side stream, concurrently with A9 below
+  oid_status s0 = fork_side(ctx, st);
+  if (s0 != OID_OK) return s0;
+  s0 = estimate_pre(ctx, ctx->use_side ? ctx->side : st);
+  if (s0 != OID_OK) return s0;
   // A9: exact basis Gram G = A_J^T A_J, incremental: only the rows/columns of
   // slots admitted since the last estimate are recomputed, over this shard's rows.
   dirty_compact_kernel<<<1, 32, 0, st>>>(ctx->ptr<int>(L.dirty), t, ctx->ptr<int>(L.dlist), ctx->ptr<int>(L.counts));
   CKL();
+  if (ctx->bg_tc) {
+    const bool f64 = ctx->p.dtype == OID_F64;
+    const int RL = f64 ? 16 : 32;
+    const int sms = std::max(1, ctx->num_sms - ctx->bg_free_sms);   // leave SMs to the side stream
+    int grid = static_cast<int>(std::min<int64_t>(std::min(sms, kGramChunks), (ctx->m_loc + RL - 1) / RL));
+    int64_t per = (ctx->m_loc + grid - 1) / grid;
+    per = (per + RL - 1) / RL * RL;
+    grid = static_cast<int>((ctx->m_loc + per - 1) / per);
+    const int nbox = (t + 255) / 256;
+    const int stage_bytes = (nbox * std::min(t, 256) * 128 + 1023) / 1024 * 1024;
+    const int nstage = std::max(2, std::min(bgtc::kMaxStages, (200 * 1024) / stage_bytes));
+    const size_t smem = static_cast<size_t>(nstage) * stage_bytes + 1024;
+#define BGT_LAUNCH(TT, CW)                                                                                         \
+  bgtc::basis_gram_tc_kernel<TT, CW><<<grid, 32 * (CW + 1), smem, st>>>(ctx->bg_map, ctx->m_loc, t, per, nstage,     \
+                                                                      stage_bytes, nbox, ctx->ptr<int>(L.dlist),   \
+                                                                      ctx->ptr<int>(L.counts), ctx->d(L.Gpart))
+    if (f64) { if (t <= 256) BGT_LAUNCH(double, 8); else BGT_LAUNCH(double, 16); }
+    else { if (t <= 256) BGT_LAUNCH(float, 8); else BGT_LAUNCH(float, 16); }
+#undef BGT_LAUNCH
+    CKL();
+    sum_chunks_kernel<<<blocks_for(int64_t(t) * t), 256, 0, st>>>(ctx->d(L.Gpart), grid, int64_t(t) * t, ctx->d(L.Gsum));
+    CKL();
+    return OID_OK;
+  }
   int chunks = static_cast<int>(std::min<int64_t>(std::min(2 * ctx->num_sms, kGramChunks), (ctx->m_loc + 1023) / 1024));
   chunks = std::max(1, chunks);
   int64_t per = (ctx->m_loc + chunks - 1) / chunks;
@@ -795,9 +974,7 @@ oid_status oid_estimate_end(oid_ctx ctx, double* out_dev, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const Layout& L = ctx->L;
   const oid_params& p = ctx->p;
-  const int t = ctx->t, ell = p.ell, l1 = p.ell1, l2 = p.ell2, l3 = p.ell3;
-  const int n = static_cast<int>(ctx->n_obs);
-  double* S = ctx->d(L.S);
+  const int t = ctx->t, l1 = p.ell1, l2 = p.ell2;
   double* scal = ctx->d(L.scal);
   EvScope ev(ctx, st, &ctx->ev_est);
   gram_scatter_kernel<<<blocks_for(int64_t(t) * t), 256, 0, st>>>(ctx->d(L.Gsum), ctx->ptr<int>(L.dlist),
@@ -806,97 +983,20 @@ oid_status oid_estimate_end(oid_ctx ctx, double* out_dev, void* stream) {
   CK(cudaMemcpyAsync(ctx->d(L.G), ctx->d(L.Gfull), sizeof(double) * t * t, cudaMemcpyDeviceToDevice, st));
   mask_gram_kernel<<<blocks_for(int64_t(t) * t), 256, 0, st>>>(ctx->d(L.G), ctx->ptr<int64_t>(L.J), t);
   CKL();
-  oid_status s = explicit_P(ctx, st);                                                 // P = S_J^+ S
+  // the G-independent factors were formed on the side stream (estimate_pre)
+  oid_status s = join_side(ctx, st);
   if (s != OID_OK) return s;
-  double* P = ctx->d(L.Pexp);
-  double* AJP = ctx->d(L.AJP);
-  s = gemm(ctx, st, false, false, ell, n, t, 1.0, ctx->d(L.SJ), ell, P, t, 0.0, AJP, ell);   // Omega A_J P
-  if (s != OID_OK) return s;
-  CK(cudaMemsetAsync(scal + SC_T1, 0, 4 * sizeof(double), st));
   if (l1 > 0 && l2 > 0) {
-    // M = (Omega1 A (Omega2 A_J P)^T)^+   (P:595)
-    s = gemm(ctx, st, false, true, l1, l2, n, 1.0, S, ell, AJP + l1, ell, 0.0, ctx->d(L.cB), l1);
-    if (s != OID_OK) return s;
-    // M = B^+ (l2 x l1).  Fast path (l1 <= l2, kappa(B) <= 1e5): M = ((B B^T)^-1 B)^T by the cluster
-    // tridiagonalisation; else the one-sided Jacobi SVD pseudo-inverse (R9), gated on the device.
-    int* cgate = ctx->ptr<int>(L.gate) + 4;
-    if (l1 <= l2 && l1 <= kTriMaxN) {
-      s = gemm(ctx, st, false, true, l1, l1, l2, 1.0, ctx->d(L.cB), l1, ctx->d(L.cB), l1, 0.0, ctx->d(L.cG), l1);
-      if (s != OID_OK) return s;
-      s = spd_solve(ctx, st, ctx->d(L.cG), l1, ctx->d(L.cB), l1, false, l2, ctx->d(L.M), l2, true, 1e10, cgate, nullptr);
-      if (s != OID_OK) return s;
-    } else {
-      set_flag_kernel<<<1, 1, 0, st>>>(cgate, 0, 1);
-      CKL();
-    }
-    const int lo = std::min(l1, l2), hi = std::max(l1, l2);
-    if (static_cast<size_t>(hi + lo) * lo * sizeof(double) <= kSmallSvdSmem) {
-      // small pseudo-inverse in one CTA: SVD of the tall orientation (hi x lo)
-      double* Bt = ctx->d(L.cBt);
-      if (l1 < l2) {
-        transpose_kernel<<<blocks_for(int64_t(l1) * l2), 256, 0, st>>>(ctx->d(L.cB), l1, l2, Bt, cgate + 1);
-        CKL();
-      } else {
-        CK(cudaMemcpyAsync(Bt, ctx->d(L.cB), sizeof(double) * l1 * l2, cudaMemcpyDeviceToDevice, st));
-      }
-      int* counters = ctx->ptr<int>(L.counters) + 2 * kMaxSweeps;
-      small_svd_kernel<<<1, 1024, static_cast<size_t>(hi + lo) * lo * sizeof(double), st>>>(
-          Bt, hi, lo, ctx->d(L.cV), ctx->d(L.csig), counters, kMaxSweeps, 4e-14 * std::max(1.0, std::sqrt(hi / 16.0)),
-          cgate + 1);
-      CKL();
-      if (l1 < l2) {
-        // pinv(B^T) (l1 x l2) = V diag(w) Bt^T; M = pinv(B) = pinv(B^T)^T (l2 x l1)
-        s = pinv_assemble(ctx, st, Bt, hi, lo, ctx->d(L.cV), ctx->d(L.csig), ctx->d(L.cw), ctx->d(L.cZ), ctx->d(L.cZ2),
-                          nullptr, 0, cgate + 1);
-        if (s != OID_OK) return s;
-        transpose_kernel<<<blocks_for(int64_t(l1) * l2), 256, 0, st>>>(ctx->d(L.cZ2), l1, l2, ctx->d(L.M), cgate + 1);
-        CKL();
-      } else {
-        s = pinv_assemble(ctx, st, Bt, hi, lo, ctx->d(L.cV), ctx->d(L.csig), ctx->d(L.cw), ctx->d(L.cZ), ctx->d(L.M),
-                          nullptr, 0, cgate + 1);
-        if (s != OID_OK) return s;
-      }
-    } else {
-      s = jacobi(ctx, st, ctx->d(L.cB), l1, l2, ctx->d(L.cV), ctx->d(L.csig), 2, false, cgate + 1);
-      if (s != OID_OK) return s;
-      s = pinv_assemble(ctx, st, ctx->d(L.cB), l1, l2, ctx->d(L.cV), ctx->d(L.csig), ctx->d(L.cw), ctx->d(L.cZ), ctx->d(L.M),
-                        nullptr, 0, cgate + 1);
-      if (s != OID_OK) return s;
-    }
-    // term1 = tr(M (Omega1 A P^T) G (Omega2 A P^T)^T)
-    s = gemm(ctx, st, false, true, l1, t, n, 1.0, S, ell, P, t, 0.0, ctx->d(L.X1), l1);
-    if (s != OID_OK) return s;
-    s = gemm(ctx, st, false, true, l2, t, n, 1.0, S + l1, ell, P, t, 0.0, ctx->d(L.X2), l2);
-    if (s != OID_OK) return s;
-    s = gemm(ctx, st, false, false, l2, t, l1, 1.0, ctx->d(L.M), l2, ctx->d(L.X1), l1, 0.0, ctx->d(L.Q1), l2);
-    if (s != OID_OK) return s;
+    // term1 = tr(M (Omega1 A P^T) G (Omega2 A P^T)^T) = <Q1 G, X2>
     s = gemm(ctx, st, false, false, l2, t, t, 1.0, ctx->d(L.Q1), l2, ctx->d(L.G), t, 0.0, ctx->d(L.Q2), l2);
     if (s != OID_OK) return s;
     frob_dot_kernel<<<1, 256, 0, st>>>(ctx->d(L.Q2), l2, ctx->d(L.X2), l2, l2, t, scal + SC_T1);
     CKL();
   }
-  if (l3 > 0) {
-    // t3a = tr((Omega3 A)(Omega3 A_J P)^T)
-    frob_dot_kernel<<<1, 256, 0, st>>>(S + l1 + l2, ell, AJP + l1 + l2, ell, l3, n, scal + SC_T3A);
-    CKL();
-    if (l1 > 0 && l2 > 0) {
-      // t3b = tr((Omega3 A_J P)(Omega2 A)^T M (Omega1 A)(Omega3 A_J P)^T)
-      s = gemm(ctx, st, false, true, l3, l2, n, 1.0, AJP + l1 + l2, ell, S + l1, ell, 0.0, ctx->d(L.R1), l3);
-      if (s != OID_OK) return s;
-      s = gemm(ctx, st, false, true, l3, l1, n, 1.0, AJP + l1 + l2, ell, S, ell, 0.0, ctx->d(L.R2t), l3);
-      if (s != OID_OK) return s;
-      s = gemm(ctx, st, false, false, l3, l1, l2, 1.0, ctx->d(L.R1), l3, ctx->d(L.M), l2, 0.0, ctx->d(L.R3), l3);
-      if (s != OID_OK) return s;
-      frob_dot_kernel<<<1, 256, 0, st>>>(ctx->d(L.R3), l3, ctx->d(L.R2t), l3, l3, l1, scal + SC_T3B);
-      CKL();
-    }
-  }
   // tr(G P P^T) = ||A_J P||_F^2
-  s = gemm(ctx, st, false, true, t, t, n, 1.0, P, t, P, t, 0.0, ctx->d(L.PPt), t);
-  if (s != OID_OK) return s;
   frob_dot_kernel<<<1, 256, 0, st>>>(ctx->d(L.G), t, ctx->d(L.PPt), t, t, t, scal + SC_GPP);
   CKL();
-  hutch_final_kernel<<<1, 32, 0, st>>>(scal, l3, ctx->ptr<unsigned>(L.flags), ctx->d(L.est));
+  hutch_final_kernel<<<1, 32, 0, st>>>(scal, p.ell3, ctx->ptr<unsigned>(L.flags), ctx->d(L.est));
   CKL();
   if (out_dev) CK(cudaMemcpyAsync(out_dev, ctx->d(L.est), 8 * sizeof(double), cudaMemcpyDeviceToDevice, st));
   return OID_OK;
@@ -920,6 +1020,8 @@ oid_status oid_finalize(oid_ctx ctx, int64_t* J_host, double* P, int32_t P_on_de
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const Layout& L = ctx->L;
   const int t = ctx->t;
+  oid_status sj = join_side(ctx, st);
+  if (sj != OID_OK) return sj;
   if (ctx->n_obs > 0 && P) {
     oid_status s = explicit_P(ctx, st);
     if (s != OID_OK) return s;
@@ -950,10 +1052,14 @@ oid_status oid_get(oid_ctx ctx, int32_t field, void* host_dst, size_t bytes, voi
     case 8: off = L.Sjpinv; need = sizeof(double) * ctx->t * p.ell; break;
     case 9: off = L.counters; need = sizeof(int) * kNumJacobiUses * kMaxSweeps; break;
     case 10: off = L.dbg; need = k1tc::kDbgRows * k1tc::kDbgTiles * sizeof(long long); break;
+    case 11: off = L.G; need = sizeof(double) * ctx->t * ctx->t; break;
+    case 12: off = L.dbg + k1tc::kDbgRows * k1tc::kDbgTiles * sizeof(long long); need = k1tc::kDbgTiles * sizeof(long long); break;
     default: return ctx->fail(OID_EINVAL, "unknown field %d", field);
   }
   if (bytes < need) return ctx->fail(OID_ESHAPE, "field %d needs %zu bytes", field, need);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  oid_status sj = join_side(ctx, st);
+  if (sj != OID_OK) return sj;
   if (need) CK(cudaMemcpyAsync(host_dst, ctx->ws + off, need, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   return OID_OK;
@@ -984,6 +1090,7 @@ oid_status oid_stats(oid_ctx ctx, oid_stats_t* out) {
   CK(sum(ctx->ev_post, &out->post_ms));
   CK(sum(ctx->ev_est, &out->est_ms));
   unsigned f = 0;
+  CK(cudaStreamSynchronize(ctx->side));
   CK(cudaMemcpy(&f, ctx->ws + ctx->L.flags, sizeof(unsigned), cudaMemcpyDeviceToHost));
   out->flags = f;
   return OID_OK;
@@ -1002,6 +1109,12 @@ oid_status oid_stats_reset(oid_ctx ctx) {
 
 void oid_destroy(oid_ctx ctx) {
   if (!ctx) return;
+  if (ctx->side) {
+    cudaStreamSynchronize(ctx->side);
+    cudaStreamDestroy(ctx->side);
+  }
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   oid_stats_reset(ctx);
   delete ctx;
 }

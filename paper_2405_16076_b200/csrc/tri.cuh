@@ -40,8 +40,7 @@ __device__ __forceinline__ double tri_pick(const double (&a)[kTriCL], int q) {
 
 __global__ void __cluster_dims__(kTriCtas, 1, 1) __launch_bounds__(256, 1)
 tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__ d, double* __restrict__ e,
-                       double* __restrict__ Vh, double* __restrict__ tauv, double* __restrict__ /*gv*/,
-                       double* __restrict__ /*gp*/) {
+                       double* __restrict__ Vh, double* __restrict__ tauv, long long* __restrict__ dbg) {
   cg2::cluster_group cluster = cg2::this_cluster();
   const int c = static_cast<int>(cluster.block_rank());
   const int R = (n + kTriCtas - 1) / kTriCtas;
@@ -68,9 +67,11 @@ tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__
     }
   }
   cluster.sync();
+  const bool rec = dbg != nullptr && c == 0 && tid == 0;   // diagnostics: phase timestamps of CTA 0
   for (int k = 0; k < n - 2; ++k) {
     const int buf = k & 1;
     double* xk = xb[buf];
+    if (rec && k < 1024) dbg[4 * k] = clock64();
     const int qk = k >> 5, lk = k & 31;
     // phase 1: x_i = A(i, k) for my rows i > k -> every CTA, with the partial sum of squares
     double ssw = 0.0;
@@ -91,7 +92,9 @@ tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__
       for (int w = 0; w < 8; ++w) ss += wred[w];
       cluster.map_shared_rank(&ssb[buf][0], tid)[c] = ss;
     }
+    if (rec && k < 1024) dbg[4 * k + 1] = clock64();
     cluster.sync();
+    if (rec && k < 1024) dbg[4 * k + 2] = clock64();
     // phase 2: reflector (redundant in every CTA)
     double ss = 0.0;
     for (int q = 0; q < kTriCtas; ++q) ss += ssb[buf][q];
@@ -149,6 +152,7 @@ tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__
       cluster.map_shared_rank(kb, tid)[c] = kp;
     }
     cluster.sync();
+    if (rec && k < 1024) dbg[4 * k + 3] = clock64();
     // phase 3: w = p - (tau K / 2) v; A <- A - v w^T - w v^T (zeros outside i, j > k)
     if (tau != 0.0) {
       double K = 0.0;

@@ -72,3 +72,36 @@ def test_c3_fullsize_sampled_parity(oid):
         if col >= 0:
             assert torch.equal(basis[rows, slot], X[rows, col]), slot
     eng.close()
+
+
+def test_c3_fullsize_basis_gram(oid):
+    """A9 at full size in the bench launch configuration: after each estimate, sampled entries
+    of G = A_J^T A_J equal fp64 dot products of the basis columns (computed on the host from the
+    finalized basis), across several blocks so the incremental (dirty-slot) update is covered."""
+    gen = ChannelFlow(192, 129, 192, seed=C3.data_seed)
+    m, b = gen.m, C3.b
+    dev = torch.device("cuda", 0)
+    p = oid.make_params(m=m, k=C3.k, ell=C3.ell, b_max=b, n_cap=128, lam=-1.0, seed=0)
+    eng = oid.Engine(p)
+    rng = np.random.default_rng(3)
+    for blk in range(3):
+        X = gen.block_torch(blk * b, (blk + 1) * b, dev).T
+        eng.ingest_block(X)
+        est = eng.error_estimate()
+        assert np.isfinite(est["est_rel"])
+        del X
+        G = eng.get(11)
+        J = eng.J()
+        occ = np.flatnonzero(J >= 0)
+        basis = eng.finalize(basis=True)["basis"]
+        pick = rng.choice(occ, size=min(6, len(occ)), replace=False)
+        cols = {int(i): basis[:, int(i)].cpu().numpy() for i in pick}
+        for i in pick:
+            for j in pick:
+                ref = float(np.dot(cols[int(i)], cols[int(j)]))
+                scale = np.sqrt(np.dot(cols[int(i)], cols[int(i)]) * np.dot(cols[int(j)], cols[int(j)]))
+                assert abs(G[i, j] - ref) <= 1e-13 * scale, (blk, i, j, G[i, j], ref)
+        vac = np.flatnonzero(J < 0)
+        assert np.all(G[vac, :] == 0) and np.all(G[:, vac] == 0)
+        del basis
+    eng.close()
