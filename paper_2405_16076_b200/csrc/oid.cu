@@ -101,7 +101,7 @@ struct Bump {
 struct Layout {
   size_t S, gram, Ypart, k1part, k1npart, gB, gV, mu, mu_sorted, Yc, Tsc, tau, scal, J, tau_old, admit, counts,
       flags, counters, C, SJ, sjB, sjV, sjsig, sjw, sjZ, Sjpinv, Pexp, AJP, G, Gsum, Gpart, cB, cV, csig, cw, cZ, M,
-      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, sjG, cG, cBt, cZ2, dbg, total;
+      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, wyT, sjG, cG, cBt, cZ2, dbg, total;
 };
 
 int64_t m_local(const oid_params& p) { return p.row_end - p.row_begin; }
@@ -171,7 +171,7 @@ Layout make_layout(const oid_params& p) {
   L.gT = b.take(ell * ell * d);
   L.td = b.take(ell * d);
   L.te = b.take(ell * d);
-  L.Vh = b.take(ell * ell * d);
+  L.Vh = b.take(ell * (ell + 1) * d);   // leading dimension tri_ldv(n) <= ell + 1
   L.tauv = b.take(ell * d);
   L.gv = b.take((ell + 1) * d);
   L.gp = b.take((ell + 16) * d);
@@ -182,6 +182,7 @@ Layout make_layout(const oid_params& p) {
   L.cZ2 = b.take(std::max<size_t>(1, l1 * l2) * d);
   L.cG = b.take(std::max<size_t>(1, std::min(l1, l2) * std::min(l1, l2)) * d);
   L.ldl = b.take(2 * ell * d);
+  L.wyT = b.take(static_cast<size_t>(kMaxRefChunks) * kRefChunk * kRefChunk * d);
   L.tc = b.take(k1tc_workspace_bytes(p.ell, p.b_max, m_local(p), p.dtype == OID_F64));
   L.total = b.off;
   return L;
@@ -341,17 +342,21 @@ oid_status pinv_assemble(oid_ctx ctx, cudaStream_t st, const double* B, int L, i
 oid_status spd_solve(oid_ctx ctx, cudaStream_t st, const double* A, int n, const double* R, int64_t ldr, bool in_t,
                      int nrhs, double* X, int64_t ldx, bool out_t, double kmax2, int* gate, double* kappa_out) {
   const Layout& L = ctx->L;
-  const size_t smem = sizeof(double) * static_cast<size_t>(n) * ((n + kTriCtas - 1) / kTriCtas);
+  const size_t smem = sizeof(double) * static_cast<size_t>(n) * tri_rows(n);
   tridiag_cluster_kernel<<<kTriCtas, 256, smem, st>>>(A, n, ctx->d(L.td), ctx->d(L.te), ctx->d(L.Vh), ctx->d(L.tauv),
                                                       nullptr);
   CKL();
+  if (n > 2) {
+    wy_t_kernel<<<(n - 2 + kRefChunk - 1) / kRefChunk, 256, 0, st>>>(ctx->d(L.Vh), ctx->d(L.tauv), n, ctx->d(L.wyT));
+    CKL();
+  }
   multisect_kernel<<<(n * 32 + 255) / 256, 256, sizeof(double) * 2 * n, st>>>(ctx->d(L.td), ctx->d(L.te), n,
                                                                             ctx->d(L.mu_sorted));
   CKL();
   spd_gate_kernel<<<1, 32, 0, st>>>(ctx->d(L.mu_sorted), n, kmax2, ctx->d(L.td), ctx->d(L.te), ctx->d(L.ldl), gate,
                                     kappa_out);
   CKL();
-  tri_solve_kernel<<<(nrhs + 7) / 8, 256, sizeof(double) * 2 * kRefChunk * n, st>>>(R, ldr, in_t ? 1 : 0, n, nrhs, ctx->d(L.Vh), ctx->d(L.tauv), ctx->d(L.ldl), gate, X, ldx,
+  tri_solve_kernel<<<nrhs, 256, sizeof(double) * kQStages * kRefChunk * tri_ldv(n), st>>>(R, ldr, in_t ? 1 : 0, n, nrhs, ctx->d(L.Vh), ctx->d(L.wyT), ctx->d(L.ldl), gate, X, ldx,
                                          out_t ? 1 : 0);
   CKL();
   return OID_OK;
@@ -513,17 +518,21 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   int* gate = ctx->ptr<int>(L.gate);
   if (ell <= kTriMaxN && !ctx->cold_jacobi) {
     // tridiagonal fast path (tri.cuh); the eigenvector path below runs only when gate[1] is set
-    const size_t smem = sizeof(double) * static_cast<size_t>(ell) * ((ell + kTriCtas - 1) / kTriCtas);
+    const size_t smem = sizeof(double) * static_cast<size_t>(ell) * tri_rows(ell);
     tridiag_cluster_kernel<<<kTriCtas, 256, smem, st>>>(ctx->d(L.gram), ell, ctx->d(L.td), ctx->d(L.te), ctx->d(L.Vh),
                                                         ctx->d(L.tauv), ctx->k1_debug ? ctx->ptr<long long>(L.dbg) + k1tc::kDbgRows * k1tc::kDbgTiles : nullptr);
     CKL();
+    if (ell > 2) {
+      wy_t_kernel<<<(ell - 2 + kRefChunk - 1) / kRefChunk, 256, 0, st>>>(ctx->d(L.Vh), ctx->d(L.tauv), ell, ctx->d(L.wyT));
+      CKL();
+    }
     multisect_kernel<<<(ell * 32 + 255) / 256, 256, sizeof(double) * 2 * ell, st>>>(ctx->d(L.td), ctx->d(L.te), ell,
                                                                                   ctx->d(L.mu));
     CKL();
     lambda_sorted_kernel<<<1, 256, 0, st>>>(ctx->d(L.mu), ell, p.k, ctx->d(L.gram), p.lambda, ell, scal, gate,
                                             ctx->d(L.td), ctx->d(L.te), ctx->d(L.ldl), 1);
     CKL();
-    tri_scores_kernel<<<(ns + 7) / 8, 256, sizeof(double) * 2 * kRefChunk * ell, st>>>(ctx->d(L.Yc), ell, ns, ctx->d(L.Vh), ctx->d(L.tauv), ctx->d(L.ldl), gate,
+    tri_scores_kernel<<<ns, 256, sizeof(double) * kQStages * kRefChunk * tri_ldv(ell), st>>>(ctx->d(L.Yc), ell, ns, ctx->d(L.Vh), ctx->d(L.wyT), ctx->d(L.ldl), gate,
                                           ctx->d(L.tau));
     CKL();
     const int* g1 = gate + 1;
@@ -781,10 +790,10 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
     if ((e = cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
       return bad(e);
     if ((e = cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(sizeof(double) * p->ell * ((p->ell + kTriCtas - 1) / kTriCtas)))) !=
+                                  static_cast<int>(sizeof(double) * p->ell * tri_rows(p->ell)))) !=
         cudaSuccess)
       return bad(e);
-    const int ref_smem = static_cast<int>(sizeof(double) * 2 * kRefChunk * kTriMaxN);
+    const int ref_smem = static_cast<int>(sizeof(double) * kQStages * kRefChunk * tri_ldv(kTriMaxN));
     if ((e = cudaFuncSetAttribute(tri_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ref_smem)) != cudaSuccess)
       return bad(e);
     if ((e = cudaFuncSetAttribute(tri_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ref_smem)) != cudaSuccess)

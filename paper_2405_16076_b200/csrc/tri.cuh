@@ -21,15 +21,24 @@ constexpr int kTriRows = kTriMaxN / kTriCtas;   // 32 rows per CTA at the maximu
 // Householder tridiagonalisation of the symmetric n x n matrix A (col-major), n <= 512.
 // Outputs: d (n), e (n-1) of T; reflectors H_k = I - tau_k v_k v_k^T, k = 0..n-3, with v_k
 // stored in Vh(:, k) (rows k+1..n-1; zero elsewhere) and tau_k in tauv[k].
-// Launch: 16 CTAs in one cluster.  CTA c owns rows [c R, c R + R) (R <= 32); warp w of the CTA
-// owns 4 of them and lane l the columns l + 32 q (q < 16), held in REGISTERS (64 doubles per
-// thread), so the matrix-vector product and the rank-2 update never touch shared memory.
-// Step k: every CTA sends its slice of column k (= row k by symmetry) and its partial ||x||^2
-// to all CTAs through distributed shared memory; after a cluster barrier each CTA forms the
-// reflector redundantly, computes p = tau A v on its rows and sends its p slice and partial
-// v^T p; after a second barrier it applies A <- A - v w^T - w v^T, w = p - (tau v^T p / 2) v.
+// Launch: 16 CTAs in one cluster.  CTA c owns rows [c R, c R + R) (R = tri_rows(n) <= 32, even);
+// warp w of the CTA owns 4 of them and lane l the columns l + 32 q (q < 16), held in REGISTERS
+// (64 doubles per thread), so the matrix-vector product and the rank-2 update never touch
+// shared memory.
+// Step k: every CTA pushes its slice of column k (= row k by symmetry) and its partial ||x||^2
+// into every CTA's shared memory with st.async (distributed shared memory), which completes
+// bytes on the receiver's mbarrier; each CTA waits on its own mbarrier only (no cluster-wide
+// barrier), forms the reflector redundantly, computes p = tau A v on its rows and pushes its p
+// slice and partial v^T p the same way; then it applies A <- A - v w^T - w v^T,
+// w = p - (tau v^T p / 2) v.  Buffers and mbarriers alternate between even and odd steps: a
+// CTA can only send step k+2's data after every CTA has sent its step-k+1 p, i.e. after every
+// receiver has finished step k, so a buffer is never overwritten while it is read.
 constexpr int kTriRW = 4;     // rows per warp
 constexpr int kTriCL = 16;    // column registers per lane
+
+__host__ __device__ constexpr int tri_rows(int n) { return 2 * ((n + 2 * kTriCtas - 1) / (2 * kTriCtas)); }
+// leading dimension of the reflector matrix Vh (even, so every column start is 16-byte aligned)
+__host__ __device__ constexpr int tri_ldv(int n) { return (n + 1) & ~1; }
 
 __device__ __forceinline__ double tri_pick(const double (&a)[kTriCL], int q) {
   double x = 0.0;
@@ -38,22 +47,60 @@ __device__ __forceinline__ double tri_pick(const double (&a)[kTriCL], int q) {
   return x;
 }
 
+__device__ __forceinline__ uint32_t tri_saddr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ uint32_t tri_mapa(uint32_t a, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void tri_st_async2(uint32_t raddr, double x, double y, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(raddr), "d"(x),
+               "d"(y), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void tri_st_async1(uint32_t raddr, double x, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(raddr), "d"(x), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void tri_mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tri_saddr(bar)), "r"(count));
+}
+__device__ __forceinline__ void tri_mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tri_saddr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tri_mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "TRI_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra TRI_WAIT_%=;\n\t}" ::"r"(tri_saddr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 __global__ void __cluster_dims__(kTriCtas, 1, 1) __launch_bounds__(256, 1)
 tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__ d, double* __restrict__ e,
                        double* __restrict__ Vh, double* __restrict__ tauv, long long* __restrict__ dbg) {
   cg2::cluster_group cluster = cg2::this_cluster();
   const int c = static_cast<int>(cluster.block_rank());
-  const int R = (n + kTriCtas - 1) / kTriCtas;
+  const int R = tri_rows(n);
   const int r0 = c * R, r1 = min(n, r0 + R);
-  __shared__ double xb[2][kTriMaxN];     // column k, all CTAs' slices (double-buffered)
-  __shared__ double pb[kTriMaxN];        // p, all CTAs' slices
-  __shared__ double loc[kTriRows];       // this CTA's slice (x, then p)
+  __shared__ __align__(16) double xb[2][kTriCtas * kTriRows];   // column k, all CTAs' slices
+  __shared__ __align__(16) double pb[2][kTriCtas * kTriRows];   // p, all CTAs' slices
+  __shared__ __align__(16) double locx[kTriRows], locp[kTriRows];
   __shared__ double ssb[2][kTriCtas];
-  __shared__ double kb[kTriCtas];
+  __shared__ double kb[2][kTriCtas];
   __shared__ double wred[8];
+  __shared__ __align__(8) uint64_t barx[2], barp[2];
   __shared__ double tau_s[kTriMaxN], d_s[kTriMaxN], e_s[kTriMaxN];
   extern __shared__ double vh_s[];       // [n][R]: this CTA's rows of every reflector (dynamic)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t phase_bytes = static_cast<uint32_t>(kTriCtas) * (R + 1) * 8u;
+  if (tid == 0) {
+    tri_mbar_init(&barx[0], 1); tri_mbar_init(&barx[1], 1);
+    tri_mbar_init(&barp[0], 1); tri_mbar_init(&barp[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   double a[kTriRW][kTriCL];
   int gi[kTriRW];
 #pragma unroll
@@ -66,34 +113,40 @@ tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__
       a[r][q] = (gi[r] >= 0 && j < n) ? A[j + static_cast<int64_t>(gi[r]) * n] : 0.0;   // row i = column i
     }
   }
-  cluster.sync();
+  // sender roles: thread -> (target CTA, pair of rows)
+  const int hp = R >> 1;                          // v2 stores per slice
+  const int tq = hp > 0 ? tid / hp : 0, tu = hp > 0 ? tid - tq * hp : 0;
+  const bool sender = hp > 0 && tq < kTriCtas;
+  cluster.sync();                                 // mbarrier inits visible cluster-wide
   const bool rec = dbg != nullptr && c == 0 && tid == 0;   // diagnostics: phase timestamps of CTA 0
   for (int k = 0; k < n - 2; ++k) {
     const int buf = k & 1;
+    const uint32_t par = (k >> 1) & 1;
     double* xk = xb[buf];
-    if (rec && k < 1024) dbg[4 * k] = clock64();
     const int qk = k >> 5, lk = k & 31;
+    if (rec && k < 1024) dbg[4 * k] = clock64();
+    if (tid == 0) { tri_mbar_expect(&barx[buf], phase_bytes); tri_mbar_expect(&barp[buf], phase_bytes); }
     // phase 1: x_i = A(i, k) for my rows i > k -> every CTA, with the partial sum of squares
     double ssw = 0.0;
 #pragma unroll
     for (int r = 0; r < kTriRW; ++r) {
       const double xi = __shfl_sync(0xffffffffu, tri_pick(a[r], qk), lk);
-      if (gi[r] > k) { ssw = fma(xi, xi, ssw); if (lane == 0) loc[gi[r] - r0] = xi; }
-      else if (gi[r] >= 0 && lane == 0) loc[gi[r] - r0] = 0.0;
+      if (gi[r] > k) { ssw = fma(xi, xi, ssw); if (lane == 0) locx[gi[r] - r0] = xi; }
+      else if (lane == 0 && warp * kTriRW + r < R) locx[warp * kTriRW + r] = 0.0;
     }
     if (lane == 0) wred[warp] = ssw;
     __syncthreads();
-    for (int t = tid; t < R * kTriCtas; t += 256) {
-      const int q = t / R, il = t - q * R;
-      if (r0 + il < n) cluster.map_shared_rank(xk, q)[r0 + il] = loc[il];
+    if (sender) {
+      const uint32_t la = tri_saddr(&xk[r0 + 2 * tu]);
+      tri_st_async2(tri_mapa(la, tq), locx[2 * tu], locx[2 * tu + 1], tri_mapa(tri_saddr(&barx[buf]), tq));
     }
     if (tid < kTriCtas) {
       double ss = 0.0;
       for (int w = 0; w < 8; ++w) ss += wred[w];
-      cluster.map_shared_rank(&ssb[buf][0], tid)[c] = ss;
+      tri_st_async1(tri_mapa(tri_saddr(&ssb[buf][c]), tid), ss, tri_mapa(tri_saddr(&barx[buf]), tid));
     }
     if (rec && k < 1024) dbg[4 * k + 1] = clock64();
-    cluster.sync();
+    tri_mbar_wait(&barx[buf], par);
     if (rec && k < 1024) dbg[4 * k + 2] = clock64();
     // phase 2: reflector (redundant in every CTA)
     double ss = 0.0;
@@ -135,29 +188,30 @@ tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__
       for (int o = 16; o > 0; o >>= 1) pi[r] += __shfl_xor_sync(0xffffffffu, pi[r], o);
       pi[r] *= tau;
       if (gi[r] > k) kw = fma(vi[r], pi[r], kw);
-      if (gi[r] >= 0 && lane == 0) {
-        loc[gi[r] - r0] = gi[r] > k ? pi[r] : 0.0;
-        vh_s[k * R + (gi[r] - r0)] = (gi[r] > k && tau != 0.0) ? vi[r] : 0.0;
+      if (lane == 0 && warp * kTriRW + r < R) {
+        locp[warp * kTriRW + r] = gi[r] > k ? pi[r] : 0.0;
+        if (gi[r] >= 0) vh_s[k * R + (gi[r] - r0)] = (gi[r] > k && tau != 0.0) ? vi[r] : 0.0;
       }
     }
     if (lane == 0) wred[warp] = kw;
     __syncthreads();
-    for (int t = tid; t < R * kTriCtas; t += 256) {
-      const int q = t / R, il = t - q * R;
-      if (r0 + il < n) cluster.map_shared_rank(pb, q)[r0 + il] = loc[il];
+    if (sender) {
+      const uint32_t la = tri_saddr(&pb[buf][r0 + 2 * tu]);
+      tri_st_async2(tri_mapa(la, tq), locp[2 * tu], locp[2 * tu + 1], tri_mapa(tri_saddr(&barp[buf]), tq));
     }
     if (tid < kTriCtas) {
       double kp = 0.0;
       for (int w = 0; w < 8; ++w) kp += wred[w];
-      cluster.map_shared_rank(kb, tid)[c] = kp;
+      tri_st_async1(tri_mapa(tri_saddr(&kb[buf][c]), tid), kp, tri_mapa(tri_saddr(&barp[buf]), tid));
     }
-    cluster.sync();
+    tri_mbar_wait(&barp[buf], par);
     if (rec && k < 1024) dbg[4 * k + 3] = clock64();
     // phase 3: w = p - (tau K / 2) v; A <- A - v w^T - w v^T (zeros outside i, j > k)
     if (tau != 0.0) {
       double K = 0.0;
-      for (int q = 0; q < kTriCtas; ++q) K += kb[q];
+      for (int q = 0; q < kTriCtas; ++q) K += kb[buf][q];
       const double h = 0.5 * tau * K;
+      const double* pk = pb[buf];
       double wi[kTriRW];
 #pragma unroll
       for (int r = 0; r < kTriRW; ++r) wi[r] = (gi[r] > k) ? pi[r] - h * vi[r] : 0.0;
@@ -166,7 +220,7 @@ tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__
         const int j = lane + 32 * q;
         const bool act = j > k && j < n;
         const double vj = act ? (j == k + 1 ? v0 : xk[j]) : 0.0;
-        const double wj = act ? pb[j] - h * vj : 0.0;
+        const double wj = act ? pk[j] - h * vj : 0.0;
 #pragma unroll
         for (int r = 0; r < kTriRW; ++r) a[r][q] = a[r][q] - vi[r] * wj - wi[r] * vj;
       }
@@ -186,11 +240,15 @@ tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__
     }
   }
   __syncthreads();
-  // bulk writes: reflector rows of this CTA (Vh(i, k) for i in [r0, r1), k < n - 2), tau/d/e
+  // bulk writes: reflector rows of this CTA (Vh(i, k) for i in [r0, r1), k < n - 2; leading
+  // dimension tri_ldv(n), the pad row of odd n written as zero by the last CTA), tau/d/e
+  const int ldv = tri_ldv(n);
   for (int idx = tid; idx < (r1 - r0) * (n - 2); idx += 256) {
     const int k = idx / (r1 - r0), il = idx - k * (r1 - r0);
-    Vh[(r0 + il) + static_cast<int64_t>(k) * n] = vh_s[k * R + il];
+    Vh[(r0 + il) + static_cast<int64_t>(k) * ldv] = vh_s[k * R + il];
   }
+  if (ldv > n && r0 <= n - 1 && n - 1 < r0 + R)
+    for (int k = tid; k < n - 2; k += 256) Vh[n + static_cast<int64_t>(k) * ldv] = 0.0;
   for (int k = tid; k < n; k += 256) {
     if (c == 0 && k < n - 2) tauv[k] = tau_s[k];
     if (k >= r0 && k < r1) { d[k] = d_s[k]; if (k < n - 1) e[k] = e_s[k]; }
@@ -317,89 +375,205 @@ __global__ void lambda_sorted_kernel(const double* __restrict__ mu, int n, int k
   }
 }
 
-// z_w <- H_k z_w for k = k_first .. k_last (step +-1), for the 8 vectors z_w (one per warp) of a
-// CTA: the reflectors are streamed through shared memory in chunks of kRefChunk (cp.async, double
-// buffer); each warp applies them to its vector with shuffle dot products (fixed order).
+// Compact-WY form of the reflectors in chunks of kRefChunk: for chunk b (k = 8b .. 8b+7, k < n-2)
+// H_{8b} H_{8b+1} ... H_{8b+7} = I - V_b T_b V_b^T with T_b upper triangular (LAPACK larft,
+// forward columnwise: T(i,i) = tau_i, T(0:i, i) = -tau_i T(0:i, 0:i) V(:, 0:i)^T v_i).  One CTA per
+// chunk; T_b row-major in wyT[64 b ..].  Reflectors with tau = 0 give zero rows/columns.
 constexpr int kRefChunk = 8;
-__device__ __forceinline__ void cta_apply_reflectors(double (*z)[kTriMaxN], int nvec, int n,
-                                                     const double* __restrict__ Vh, const double* __restrict__ tauv,
-                                                     int k_first, int k_last, int step, double* __restrict__ vbuf) {
-  // vbuf: [2][kRefChunk][n]
-  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  const int nk = (step > 0 ? k_last - k_first : k_first - k_last) + 1;
-  if (nk <= 0) return;
-  const int nchunks = (nk + kRefChunk - 1) / kRefChunk;
-  __shared__ double tb[2][kRefChunk];
-  auto stage = [&](int ch, int b) {
-    double* dst = vbuf + static_cast<int64_t>(b) * kRefChunk * n;
-    if (tid < kRefChunk) {
-      const int q = ch * kRefChunk + tid;
-      tb[b][tid] = q < nk ? tauv[k_first + step * q] : 0.0;
+constexpr int kMaxRefChunks = (kTriMaxN + kRefChunk - 1) / kRefChunk;
+constexpr int kQStages = 3;
+__global__ void __launch_bounds__(256) wy_t_kernel(const double* __restrict__ Vh, const double* __restrict__ tauv, int n,
+                                                   double* __restrict__ wyT) {
+  __shared__ double G[kRefChunk][kRefChunk];
+  const int b = blockIdx.x, k0 = b * kRefChunk, nk = n - 2, ldv = tri_ldv(n);
+  const int nr = min(kRefChunk, nk - k0);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // V^T V, pairs r < c (28), one warp per pair, fixed-order shuffle reduction
+  for (int pr = w; pr < kRefChunk * (kRefChunk - 1) / 2; pr += 8) {
+    int r = 0, rem = pr;
+    while (rem >= kRefChunk - 1 - r) { rem -= kRefChunk - 1 - r; ++r; }
+    const int c = r + 1 + rem;
+    double acc = 0.0;
+    if (c < nr) {
+      const double* vr = Vh + static_cast<int64_t>(k0 + r) * ldv;
+      const double* vc = Vh + static_cast<int64_t>(k0 + c) * ldv;
+      for (int i = k0 + 1 + lane; i < n; i += 32) acc = fma(vr[i], vc[i], acc);
     }
-    for (int e = tid; e < kRefChunk * n; e += blockDim.x) {
-      const int r = e / n, i = e - r * n;
-      const int q = ch * kRefChunk + r;
-      if (q < nk) {
-        const int k = k_first + step * q;
-        const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst + e));
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(Vh + static_cast<int64_t>(k) * n + i));
-      }
-    }
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-  };
-  stage(0, 0);
-  for (int ch = 0; ch < nchunks; ++ch) {
-    if (ch + 1 < nchunks) { stage(ch + 1, (ch + 1) & 1); asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
-    else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    __syncthreads();
-    const double* vb = vbuf + static_cast<int64_t>(ch & 1) * kRefChunk * n;
-    if (w < nvec) {
-      double* zw = z[w];
-      for (int r = 0; r < kRefChunk; ++r) {
-        const int q = ch * kRefChunk + r;
-        if (q >= nk) break;
-        const int k = k_first + step * q;
-        const double tk = tb[ch & 1][r];
-        if (tk == 0.0) continue;
-        const double* v = vb + r * n;
-        double sacc = 0.0;
-        for (int i = k + 1 + lane; i < n; i += 32) sacc = fma(v[i], zw[i], sacc);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
-        const double f = tk * sacc;
-        for (int i = k + 1 + lane; i < n; i += 32) zw[i] = fma(-f, v[i], zw[i]);
-        __syncwarp();
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) G[r][c] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double T[kRefChunk][kRefChunk];
+#pragma unroll
+    for (int r = 0; r < kRefChunk; ++r)
+#pragma unroll
+      for (int c = 0; c < kRefChunk; ++c) T[r][c] = 0.0;
+#pragma unroll
+    for (int c = 0; c < kRefChunk; ++c) {
+      if (c < nr) {
+        const double tc = tauv[k0 + c];
+        T[c][c] = tc;
+#pragma unroll
+        for (int r = 0; r < c; ++r) {
+          double acc = 0.0;
+#pragma unroll
+          for (int q = r; q < c; ++q) acc = fma(T[r][q], G[q][c], acc);
+          T[r][c] = -tc * acc;
+        }
       }
     }
-    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kRefChunk; ++r)
+#pragma unroll
+      for (int c = 0; c < kRefChunk; ++c) wyT[b * kRefChunk * kRefChunk + r * kRefChunk + c] = T[r][c];
   }
 }
 
+// Shared-memory state of cta_apply_q (one vector per CTA): kQStages ring of reflector chunks
+// (V rows [k0_even, ldv) of 8 reflectors + their T) filled by cp.async.bulk on mbarriers.
+struct QSmem {
+  double* v;          // [kQStages][kRefChunk][ldv] (dynamic)
+  double* t;          // [kQStages][64]
+  uint64_t* full;     // [kQStages]
+  double (*red)[8][kRefChunk];   // [2][warps][8]
+};
+
+__device__ __forceinline__ void q_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   tri_saddr(dst)),
+               "l"(src), "r"(bytes), "r"(tri_saddr(bar))
+               : "memory");
+}
+
+// z <- Q^T z (forward: H_{n-3} ... H_0 z) or Q z (backward: H_0 ... H_{n-3} z) for ONE vector held in
+// registers (thread tid owns rows tid and tid + 256), one compact-WY chunk at a time:
+// w = V^T z (per-thread partial products, fixed-order warp and cross-warp sums), u = T^T w
+// (forward) or T w (backward), z -= V u.  `uses` counts the ring's fills across calls (parity).
+__device__ __forceinline__ void cta_apply_q(double (&z)[2], int n, const double* __restrict__ Vh,
+                                            const double* __restrict__ wyT, bool forward, QSmem& sm, int& uses) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nk = n - 2, ldv = tri_ldv(n);
+  if (nk <= 0) return;
+  const int nch = (nk + kRefChunk - 1) / kRefChunk;
+  auto chunk_of = [&](int it) { return forward ? it : nch - 1 - it; };
+  auto issue = [&](int it) {        // thread 0 only
+    const int b = chunk_of(it), k0 = b * kRefChunk, k0e = k0 & ~1;
+    const int nr = min(kRefChunk, nk - k0);
+    const int st = (uses + it) % kQStages;
+    const uint32_t row_bytes = static_cast<uint32_t>(ldv - k0e) * 8u;
+    tri_mbar_expect(&sm.full[st], static_cast<uint32_t>(nr) * row_bytes + 64u * 8u);
+    q_bulk(sm.t + st * 64, wyT + b * 64, 64u * 8u, &sm.full[st]);
+    for (int r = 0; r < nr; ++r)
+      q_bulk(sm.v + (static_cast<size_t>(st) * kRefChunk + r) * ldv + k0e, Vh + static_cast<int64_t>(k0 + r) * ldv + k0e,
+             row_bytes, &sm.full[st]);
+  };
+  if (tid == 0) {
+    issue(0);
+    if (nch > 1) issue(1);
+  }
+  for (int it = 0; it < nch; ++it) {
+    const int b = chunk_of(it), k0 = b * kRefChunk;
+    const int nr = min(kRefChunk, nk - k0);
+    const int g = uses + it, st = g % kQStages;
+    tri_mbar_wait(&sm.full[st], (g / kQStages) & 1);
+    const double* vb = sm.v + static_cast<size_t>(st) * kRefChunk * ldv;
+    double v[kRefChunk][2], pr[kRefChunk];
+#pragma unroll
+    for (int r = 0; r < kRefChunk; ++r) {
+      pr[r] = 0.0;
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int i = tid + 256 * s;
+        v[r][s] = (r < nr && i > k0 && i < n) ? vb[r * ldv + i] : 0.0;   // rows <= k0 are zero in V
+        pr[r] = fma(v[r][s], z[s], pr[r]);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int r = 0; r < kRefChunk; ++r) pr[r] += __shfl_xor_sync(0xffffffffu, pr[r], o);
+    double (*red)[kRefChunk] = sm.red[it & 1];
+#pragma unroll
+    for (int r = 0; r < kRefChunk; ++r)   // every lane holds the warp sums after the xor tree
+      if (lane == r) red[warp][r] = pr[r];
+    double T[kRefChunk * kRefChunk];
+#pragma unroll
+    for (int q = 0; q < kRefChunk * kRefChunk; ++q) T[q] = sm.t[st * 64 + q];
+    __syncthreads();                      // V_it in registers, red complete; stage (it-1) % 3 free
+    if (tid == 0 && it + 2 < nch) issue(it + 2);
+    double w[kRefChunk];
+#pragma unroll
+    for (int r = 0; r < kRefChunk; ++r) {
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc += red[q][r];
+      w[r] = acc;
+    }
+    double u[kRefChunk];
+#pragma unroll
+    for (int c = 0; c < kRefChunk; ++c) {
+      double acc = 0.0;
+      if (forward) {
+#pragma unroll
+        for (int r = 0; r <= c; ++r) acc = fma(T[r * kRefChunk + c], w[r], acc);    // (T^T w)_c
+      } else {
+#pragma unroll
+        for (int q = c; q < kRefChunk; ++q) acc = fma(T[c * kRefChunk + q], w[q], acc);   // (T w)_c
+      }
+      u[c] = acc;
+    }
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      double zi = z[s];
+#pragma unroll
+      for (int r = 0; r < kRefChunk; ++r) zi = fma(-v[r][s], u[r], zi);
+      z[s] = zi;
+    }
+  }
+  uses += nch;
+  __syncthreads();                        // red / ring reuse by a following call
+}
+
 // tau(y) = z^T (T + sI)^-1 z, z = Q^T y = H_{n-3} ... H_0 y; y = column j of Yc (ell x ncol).
-// 8 columns per CTA (one per warp); runs when gate[0] != 0.  Dynamic smem: 2 kRefChunk n doubles.
+// One column per CTA; runs when gate[0] != 0.  Dynamic smem: kQStages kRefChunk tri_ldv(n) doubles.
 __global__ void __launch_bounds__(256) tri_scores_kernel(const double* __restrict__ Yc, int n, int ncol,
-                                                         const double* __restrict__ Vh, const double* __restrict__ tauv,
+                                                         const double* __restrict__ Vh, const double* __restrict__ wyT,
                                                          const double* __restrict__ ldl, const int* __restrict__ gate,
                                                          double* __restrict__ tau_out) {
   if (gate[0] == 0) return;
-  extern __shared__ double ref_smem[];
-  __shared__ double zs[8][kTriMaxN];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int j0 = blockIdx.x * 8;
-  const int nvec = min(8, ncol - j0);
-  if (w < nvec)
-    for (int i = lane; i < n; i += 32) zs[w][i] = Yc[static_cast<int64_t>(j0 + w) * n + i];
+  extern __shared__ __align__(16) double ref_smem[];
+  __shared__ __align__(16) double tsm[kQStages * 64];
+  __shared__ __align__(8) uint64_t full[kQStages];
+  __shared__ double red[2][8][kRefChunk];
+  __shared__ double zs[kTriMaxN];
+  const int tid = threadIdx.x, j = blockIdx.x;
+  if (tid == 0) {
+    for (int q = 0; q < kQStages; ++q) tri_mbar_init(&full[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  double z[2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const int i = tid + 256 * s;
+    z[s] = i < n ? Yc[static_cast<int64_t>(j) * n + i] : 0.0;
+  }
   __syncthreads();
-  cta_apply_reflectors(zs, nvec, n, Vh, tauv, 0, n - 3, 1, ref_smem);
-  if (w < nvec && lane == 0) {
-    const double* z = zs[w];
-    double y = z[0];
+  QSmem sm{ref_smem, tsm, full, red};
+  int uses = 0;
+  cta_apply_q(z, n, Vh, wyT, true, sm, uses);
+#pragma unroll
+  for (int s = 0; s < 2; ++s) if (tid + 256 * s < n) zs[tid + 256 * s] = z[s];
+  __syncthreads();
+  if (tid == 0) {
+    double y = zs[0];
     double acc = y * y * ldl[0];
     for (int i = 1; i < n; ++i) {
-      y = z[i] - ldl[n + i - 1] * y;
+      y = zs[i] - ldl[n + i - 1] * y;
       acc = fma(y * y, ldl[i], acc);
     }
-    tau_out[j0 + w] = acc;
+    tau_out[j] = acc;
   }
 }
 
@@ -428,40 +602,54 @@ __global__ void spd_gate_kernel(const double* __restrict__ mu, int n, double kma
 }
 
 // X(:, c) = A^-1 R(:, c) with A = Q T Q^T: z = Q^T r, solve T u = z (LDL^T), x = Q u.
-// 8 right-hand sides per CTA (one per warp); runs when gate[0] != 0.  in_transposed:
-// R(i, c) = R[c + i ldr]; out_transposed: write X^T (nrhs x n).  Dynamic smem: 2 kRefChunk n.
+// One right-hand side per CTA; runs when gate[0] != 0.  in_transposed: R(i, c) = R[c + i ldr];
+// out_transposed: write X^T (nrhs x n).  Dynamic smem: kQStages kRefChunk tri_ldv(n) doubles.
 __global__ void __launch_bounds__(256) tri_solve_kernel(const double* __restrict__ R, int64_t ldr, int in_transposed,
                                                         int n, int nrhs, const double* __restrict__ Vh,
-                                                        const double* __restrict__ tauv, const double* __restrict__ ldl,
+                                                        const double* __restrict__ wyT, const double* __restrict__ ldl,
                                                         const int* __restrict__ gate, double* __restrict__ X,
                                                         int64_t ldx, int out_transposed) {
   if (gate[0] == 0) return;
-  extern __shared__ double ref_smem[];
-  __shared__ double zs[8][kTriMaxN];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c0 = blockIdx.x * 8;
-  const int nvec = min(8, nrhs - c0);
-  if (w < nvec)
-    for (int i = lane; i < n; i += 32) {
-      const int c = c0 + w;
-      zs[w][i] = in_transposed ? R[c + static_cast<int64_t>(i) * ldr] : R[static_cast<int64_t>(c) * ldr + i];
-    }
-  __syncthreads();
-  cta_apply_reflectors(zs, nvec, n, Vh, tauv, 0, n - 3, 1, ref_smem);      // z = Q^T r
-  if (w < nvec && lane == 0) {                                              // T u = z by LDL^T
-    double* z = zs[w];
-    for (int i = 1; i < n; ++i) z[i] -= ldl[n + i - 1] * z[i - 1];
-    for (int i = 0; i < n; ++i) z[i] *= ldl[i];
-    for (int i = n - 2; i >= 0; --i) z[i] -= ldl[n + i] * z[i + 1];
+  extern __shared__ __align__(16) double ref_smem[];
+  __shared__ __align__(16) double tsm[kQStages * 64];
+  __shared__ __align__(8) uint64_t full[kQStages];
+  __shared__ double red[2][8][kRefChunk];
+  __shared__ double zs[kTriMaxN];
+  const int tid = threadIdx.x, c = blockIdx.x;
+  if (tid == 0) {
+    for (int q = 0; q < kQStages; ++q) tri_mbar_init(&full[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  double z[2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const int i = tid + 256 * s;
+    z[s] = i < n ? (in_transposed ? R[c + static_cast<int64_t>(i) * ldr] : R[static_cast<int64_t>(c) * ldr + i]) : 0.0;
   }
   __syncthreads();
-  cta_apply_reflectors(zs, nvec, n, Vh, tauv, n - 3, 0, -1, ref_smem);     // x = Q u
-  if (w < nvec)
-    for (int i = lane; i < n; i += 32) {
-      const int c = c0 + w;
-      if (out_transposed) X[static_cast<int64_t>(i) * ldx + c] = zs[w][i];
-      else X[static_cast<int64_t>(c) * ldx + i] = zs[w][i];
+  QSmem sm{ref_smem, tsm, full, red};
+  int uses = 0;
+  cta_apply_q(z, n, Vh, wyT, true, sm, uses);                                // z = Q^T r
+#pragma unroll
+  for (int s = 0; s < 2; ++s) if (tid + 256 * s < n) zs[tid + 256 * s] = z[s];
+  __syncthreads();
+  if (tid == 0) {                                                            // T u = z by LDL^T
+    for (int i = 1; i < n; ++i) zs[i] -= ldl[n + i - 1] * zs[i - 1];
+    for (int i = 0; i < n; ++i) zs[i] *= ldl[i];
+    for (int i = n - 2; i >= 0; --i) zs[i] -= ldl[n + i] * zs[i + 1];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < 2; ++s) z[s] = tid + 256 * s < n ? zs[tid + 256 * s] : 0.0;
+  cta_apply_q(z, n, Vh, wyT, false, sm, uses);                               // x = Q u
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const int i = tid + 256 * s;
+    if (i < n) {
+      if (out_transposed) X[static_cast<int64_t>(i) * ldx + c] = z[s];
+      else X[static_cast<int64_t>(c) * ldx + i] = z[s];
     }
+  }
 }
 
 // A(i, i) = cval for zero rows/columns of a Gram (vacant basis slots, reading R10) where cval =

@@ -213,6 +213,18 @@ def test_zero_columns_never_admitted_and_empty_block(oid):
     assert not set(J.tolist()) & {0, 5, 6}
 
 
+@pytest.mark.parametrize("ell,k", [(25, 7), (31, 9), (48, 20)])
+def test_odd_sizes_tridiagonal_paths(oid, ell, k):
+    """Odd Gram / S_J orders through the tridiagonal score and solve paths (fixed lambda > 0, so
+    the shifted fast path is taken), against the oracle: J per epoch, P."""
+    A = c1_matrix(seed=11, m=900, n=48, rank=12, noise=1e-3)
+    eng, o = _pair(oid, 900, k, ell, 8, 48, 0.05, seed=2)
+    low = _stream_compare(oid, eng, o, A, 8)
+    if low is None:
+        P = eng.finalize()["P"].cpu().numpy()
+        assert np.linalg.norm(P - o.P) / np.linalg.norm(o.P) < 1e-5
+
+
 def test_nonfinite_input_flagged(oid):
     A = np.random.default_rng(5).standard_normal((320, 8))
     A[7, 3] = np.nan
