@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--k1-mode", type=int, default=0)
     ap.add_argument("--no-estimate", action="store_true", help="ingest only (estimate not in the step)")
+    ap.add_argument("--one-stream", action="store_true", help="estimates on the ingest stream (no overlap)")
     ap.add_argument("--cpu-sample-rows", type=int, default=1 << 18)
     ap.add_argument("--skip-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -216,8 +217,11 @@ def main():
     split = (ell // 6, ell // 3, ell - ell // 6 - ell // 3)
     p = oid.make_params(m=m, k=k, ell=ell, b_max=b, n_cap=n_cap, lam=-1.0, split=split, seed=0, dtype=dt,
                         row_begin=rb, row_end=re, k1_mode=args.k1_mode, profile=True, device=local)
-    eng = oid.Engine(p)
-    stream = eng.stream
+    # ingest on a high-priority stream, estimates on a second stream: the basis Gram of block k
+    # (HBM/DMMA-bound) overlaps the latency-bound post-pass of block k+1
+    stream = torch.cuda.Stream(dev, priority=-1)
+    est_stream = torch.cuda.Stream(dev, priority=0) if not args.one_stream else stream
+    eng = oid.Engine(p, stream=stream, estimate_stream=est_stream)
 
     # synthetic blocks, generated on the device outside any timed region (inputs >> L2)
     blocks = []
@@ -238,7 +242,8 @@ def main():
             drv.estimate(est_out)         # basis-Gram partials all-reduced when sharded
 
     for s in range(W):
-        step(blocks[s % ring])
+        with torch.cuda.stream(stream):
+            step(blocks[s % ring])
     torch.cuda.synchronize()
     eng.stats_reset()
     if sharded:
@@ -249,8 +254,10 @@ def main():
     time.sleep(0.3)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    for s in range(W, W + K):
-        step(blocks[s % ring])
+    with torch.cuda.stream(stream):
+        for s in range(W, W + K):
+            step(blocks[s % ring])
+    stream.wait_stream(est_stream)
     ev1.record(stream)
     torch.cuda.synchronize()
     if sharded:
@@ -314,9 +321,12 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for hb in host:
-            dbuf.copy_(hb, non_blocking=True)
-            step(dbuf.T)
-            est_host.copy_(est_out, non_blocking=True)
+            with torch.cuda.stream(stream):
+                dbuf.copy_(hb, non_blocking=True)
+                step(dbuf.T)
+            with torch.cuda.stream(est_stream):
+                est_host.copy_(est_out, non_blocking=True)
+        stream.wait_stream(est_stream)
         e1.record(stream)
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1)

@@ -123,9 +123,14 @@ def workspace_bytes(params):
 
 
 class Engine:
-    """One oid context on one CUDA device (C ABI calls with torch-owned memory)."""
+    """One oid context on one CUDA device (C ABI calls with torch-owned memory).
 
-    def __init__(self, params, stream=None):
+    stream: CUDA stream of the ingest calls (default: the current stream).  estimate_stream
+    (optional): a second stream for the error-estimate calls, so that an estimate (basis Gram,
+    Alg 8) overlaps the next block's ingest; the library orders the two internally.
+    """
+
+    def __init__(self, params, stream=None, estimate_stream=None):
         import torch
         self._torch = torch
         self.p = params
@@ -134,6 +139,7 @@ class Engine:
         self.ws_bytes = workspace_bytes(params)
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self.estimate_stream = estimate_stream if estimate_stream is not None else self.stream
         h = ctypes.c_void_p()
         st = _lib.oid_init(ctypes.byref(params), ctypes.c_void_p(self.ws.data_ptr()), self.ws_bytes,
                            self._st(), ctypes.byref(h))
@@ -144,6 +150,9 @@ class Engine:
 
     def _st(self):
         return ctypes.c_void_p(self.stream.cuda_stream)
+
+    def _est(self):
+        return ctypes.c_void_p(self.estimate_stream.cuda_stream)
 
     def _check(self, st, what):
         if st != OID_OK:
@@ -182,15 +191,15 @@ class Engine:
         return self.ws[off:off + 8 * n.value].view(self._torch.float64)
 
     def estimate_begin(self):
-        self._check(_lib.oid_estimate_begin(self.h, self._st()), "oid_estimate_begin")
+        self._check(_lib.oid_estimate_begin(self.h, self._est()), "oid_estimate_begin")
 
     def estimate_end(self, out=None):
         ptr = ctypes.c_void_p(out.data_ptr()) if out is not None else ctypes.c_void_p()
-        self._check(_lib.oid_estimate_end(self.h, ptr, self._st()), "oid_estimate_end")
+        self._check(_lib.oid_estimate_end(self.h, ptr, self._est()), "oid_estimate_end")
 
     def error_estimate(self):
         out = (ctypes.c_double * 8)()
-        self._check(_lib.oid_error_estimate(self.h, out, self._st()), "oid_error_estimate")
+        self._check(_lib.oid_error_estimate(self.h, out, self._est()), "oid_error_estimate")
         v = list(out)
         return dict(e2=v[0], T=v[1], gpp=v[2], frob2=v[3], est_abs=v[4], est_rel=v[5], flags=int(v[6]), kappa=v[7])
 
@@ -215,7 +224,7 @@ class Engine:
         shapes = {0: ((t,), np.int64), 1: ((t,), np.float64), 2: ((n_obs, ell), np.float64),
                   3: ((ell, ell), np.float64), 4: ((8,), np.float64), 5: ((t + bm,), np.float64),
                   6: ((ell,), np.float64), 7: (((ell + 1) * bm,), np.float64), 8: ((ell, t), np.float64),
-                  9: ((3, 48), np.int32), 10: ((10, 4096), np.int64), 11: ((t, t), np.float64), 12: ((1024, 4), np.int64)}
+                  9: ((3, 48), np.int32), 10: ((10, 4096), np.int64), 11: ((t, t), np.float64), 12: ((1024, 4), np.int64), 13: ((4096, 2), np.float64)}
         shape, dt = shapes[field]
         a = np.empty(shape, dtype=dt)
         self._check(_lib.oid_get(self.h, field, ctypes.c_void_p(a.ctypes.data), a.nbytes, self._st()), "oid_get")

@@ -29,7 +29,12 @@ namespace {
 
 constexpr int kK1MaxCtas = 1024;
 thread_local char g_init_err[512] = "no error";
-constexpr int kGramChunks = 296;
+constexpr int kGramChunks = 296;            // cp.async fallback kernel
+constexpr size_t kGramPartBudget = size_t(1536) << 20;  // per-chunk A9 partials (TMA kernel)
+inline int gram_tc_chunks(int t) {           // short CTAs (several waves) so higher-priority work interleaves
+  const size_t per = static_cast<size_t>(t) * t * sizeof(double);
+  return static_cast<int>(std::max<size_t>(kGramChunks, std::min<size_t>(148 * 32, kGramPartBudget / per)));
+}
 constexpr int kMaxSweeps = 48;
 constexpr int kNumJacobiUses = 3;
 constexpr int kSymMaxPairs = 33;   // ceil(1024 / 16) / 2 + 1
@@ -101,7 +106,7 @@ struct Bump {
 struct Layout {
   size_t S, gram, Ypart, k1part, k1npart, gB, gV, mu, mu_sorted, Yc, Tsc, tau, scal, J, tau_old, admit, counts,
       flags, counters, C, SJ, sjB, sjV, sjsig, sjw, sjZ, Sjpinv, Pexp, AJP, G, Gsum, Gpart, cB, cV, csig, cw, cZ, M,
-      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, wyT, sjG, cG, cBt, cZ2, dbg, total;
+      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, wyT, sjG, cG, cBt, cZ2, dbg, Jsnap, td2, te2, Vh2, tauv2, wyT2, ldl2, mu2, total;
 };
 
 int64_t m_local(const oid_params& p) { return p.row_end - p.row_begin; }
@@ -132,7 +137,11 @@ Layout make_layout(const oid_params& p) {
   L.counts = b.take(4 * sizeof(int));
   L.flags = b.take(4 * sizeof(unsigned));
   L.counters = b.take(kNumJacobiUses * kMaxSweeps * sizeof(int));
-  L.C = b.take(static_cast<size_t>(m_local(p)) * t * dsize(p));
+  {
+    // row-tiled basis C_blk[tile][slot][RL] (RL = 128 bytes of rows), padded to whole tiles
+    const int64_t RL = 128 / static_cast<int64_t>(dsize(p));
+    L.C = b.take(static_cast<size_t>((m_local(p) + RL - 1) / RL * RL) * t * dsize(p));
+  }
   L.SJ = b.take(ell * t * d);
   L.sjB = b.take(ell * t * d);
   L.sjV = b.take(t * t * d);
@@ -144,7 +153,7 @@ Layout make_layout(const oid_params& p) {
   L.AJP = b.take(ell * n * d);
   L.G = b.take(t * t * d);
   L.Gsum = b.take(t * t * d);
-  L.Gpart = b.take(static_cast<size_t>(kGramChunks) * t * t * d);
+  L.Gpart = b.take(static_cast<size_t>(gram_tc_chunks(static_cast<int>(t)) + 64) * t * t * d);   // + 64 segment sums
   const size_t l1 = p.ell1, l2 = p.ell2, l3 = p.ell3;
   L.cB = b.take(std::max<size_t>(1, l1 * l2) * d);
   L.cV = b.take(std::max<size_t>(1, l2 * l2) * d);
@@ -183,6 +192,15 @@ Layout make_layout(const oid_params& p) {
   L.cG = b.take(std::max<size_t>(1, std::min(l1, l2) * std::min(l1, l2)) * d);
   L.ldl = b.take(2 * ell * d);
   L.wyT = b.take(static_cast<size_t>(kMaxRefChunks) * kRefChunk * kRefChunk * d);
+  // second tridiagonal workspace: the Alg 4 SPD solve (side stream) runs beside A4 of the next block
+  L.td2 = b.take(ell * d);
+  L.te2 = b.take(ell * d);
+  L.Vh2 = b.take(ell * (ell + 1) * d);
+  L.tauv2 = b.take(ell * d);
+  L.wyT2 = b.take(static_cast<size_t>(kMaxRefChunks) * kRefChunk * kRefChunk * d);
+  L.ldl2 = b.take(2 * ell * d);
+  L.mu2 = b.take(ell * d);
+  L.Jsnap = b.take(t * sizeof(int64_t));
   L.tc = b.take(k1tc_workspace_bytes(p.ell, p.b_max, m_local(p), p.dtype == OID_F64));
   L.total = b.off;
   return L;
@@ -231,7 +249,6 @@ struct oid_ctx_s {
   int64_t launches = 0, k1_launches = 0;
   int k1_mode_used = 0;
   bool tc_ok = false;
-  bool bg_tc = false;         // A9 on the TMA + DMMA kernel (gram_tc.cuh); else the cp.async kernel
   CUtensorMap bg_map{};       // basis slab C as a 2-D tensor {m_loc rows, t columns}
   bool cold_jacobi = false;   // diagnostics: OID_JACOBI_COLD=1 disables the warm starts
   bool k1_debug = false;      // diagnostics: OID_K1_DEBUG=1 records K1 role timestamps (oid_get 10)
@@ -241,8 +258,16 @@ struct oid_ctx_s {
   // copy (A7) and the basis-Gram-independent part of Alg 8 (A10) beside the basis Gram (A9).
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  int bg_free_sms = 12;       // SMs the A9 kernel leaves to the side stream (measured best of 0/4/12/20)
+  // cross-stream hazards when estimates run on another stream than the ingests:
+  // committed = end of a commit; snap = estimate's snapshot of J / frob2 / dirty list taken;
+  // gram_done = estimate's basis reads finished; sj_j = Alg 4 chain finished reading J;
+  // est_done = end of an estimate.
+  cudaEvent_t ev_committed = nullptr, ev_snap = nullptr, ev_gram_done = nullptr, ev_sj_j = nullptr, ev_est_done = nullptr;
+  int bg_free_sms = 0;        // SMs the A9 kernel leaves free (diagnostics: OID_BG_FREE)
+  int bg_waves = 32;          // A9 CTAs per SM (short CTAs; diagnostics: OID_BG_WAVES)
   bool use_side = true;       // diagnostics: OID_NO_SIDE=1 runs everything on the caller's stream
+  bool timeline = false;      // diagnostics: OID_TIMELINE=1 records tagged events (oid_get 13)
+  std::vector<std::pair<int, cudaEvent_t>> tl;
   char err[512] = {0};
 
   template <typename T> T* ptr(size_t off) const { return reinterpret_cast<T*>(ws + off); }
@@ -341,22 +366,22 @@ oid_status pinv_assemble(oid_ctx ctx, cudaStream_t st, const double* B, int L, i
 // and nothing is written (the caller's pseudo-inverse fallback runs).  n <= kTriMaxN.
 oid_status spd_solve(oid_ctx ctx, cudaStream_t st, const double* A, int n, const double* R, int64_t ldr, bool in_t,
                      int nrhs, double* X, int64_t ldx, bool out_t, double kmax2, int* gate, double* kappa_out) {
-  const Layout& L = ctx->L;
+  const Layout& L = ctx->L;   // second tridiagonal workspace (td2 ...)
   const size_t smem = sizeof(double) * static_cast<size_t>(n) * tri_rows(n);
-  tridiag_cluster_kernel<<<kTriCtas, 256, smem, st>>>(A, n, ctx->d(L.td), ctx->d(L.te), ctx->d(L.Vh), ctx->d(L.tauv),
+  tridiag_cluster_kernel<<<kTriCtas, 256, smem, st>>>(A, n, ctx->d(L.td2), ctx->d(L.te2), ctx->d(L.Vh2), ctx->d(L.tauv2),
                                                       nullptr);
   CKL();
   if (n > 2) {
-    wy_t_kernel<<<(n - 2 + kRefChunk - 1) / kRefChunk, 256, 0, st>>>(ctx->d(L.Vh), ctx->d(L.tauv), n, ctx->d(L.wyT));
+    wy_t_kernel<<<(n - 2 + kRefChunk - 1) / kRefChunk, 256, 0, st>>>(ctx->d(L.Vh2), ctx->d(L.tauv2), n, ctx->d(L.wyT2));
     CKL();
   }
-  multisect_kernel<<<(n * 32 + 255) / 256, 256, sizeof(double) * 2 * n, st>>>(ctx->d(L.td), ctx->d(L.te), n,
-                                                                            ctx->d(L.mu_sorted));
+  multisect_kernel<<<(n * 32 + 255) / 256, 256, sizeof(double) * 2 * n, st>>>(ctx->d(L.td2), ctx->d(L.te2), n,
+                                                                            ctx->d(L.mu2));
   CKL();
-  spd_gate_kernel<<<1, 32, 0, st>>>(ctx->d(L.mu_sorted), n, kmax2, ctx->d(L.td), ctx->d(L.te), ctx->d(L.ldl), gate,
+  spd_gate_kernel<<<1, 32, 0, st>>>(ctx->d(L.mu2), n, kmax2, ctx->d(L.td2), ctx->d(L.te2), ctx->d(L.ldl2), gate,
                                     kappa_out);
   CKL();
-  tri_solve_kernel<<<nrhs, 256, sizeof(double) * kQStages * kRefChunk * tri_ldv(n), st>>>(R, ldr, in_t ? 1 : 0, n, nrhs, ctx->d(L.Vh), ctx->d(L.wyT), ctx->d(L.ldl), gate, X, ldx,
+  tri_solve_kernel<<<nrhs, 256, sizeof(double) * kQStages * kRefChunk * tri_ldv(n), st>>>(R, ldr, in_t ? 1 : 0, n, nrhs, ctx->d(L.Vh2), ctx->d(L.wyT2), ctx->d(L.ldl2), gate, X, ldx,
                                          out_t ? 1 : 0);
   CKL();
   return OID_OK;
@@ -412,6 +437,15 @@ struct EvScope {
     v->emplace_back(b, e);
   }
 };
+
+// diagnostics timeline: tagged event on st (OID_TIMELINE=1)
+void tl_mark(oid_ctx ctx, cudaStream_t st, int tag) {
+  if (!ctx->timeline || ctx->tl.size() >= 4096) return;
+  cudaEvent_t ev;
+  if (cudaEventCreate(&ev) != cudaSuccess) return;
+  cudaEventRecord(ev, st);
+  ctx->tl.emplace_back(tag, ev);
+}
 
 // side stream waits for all work enqueued on st so far
 oid_status fork_side(oid_ctx ctx, cudaStream_t st) {
@@ -484,7 +518,9 @@ oid_status do_sketch(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
     cudaError_t e;
     {
       EvScope ev(ctx, st, &ctx->ev_k1);
+      tl_mark(ctx, st, 1);
       e = k1tc_launch(a, st, &nl);
+      tl_mark(ctx, st, 2);
     }
     ctx->launches += nl;
     ctx->k1_launches += 1;
@@ -503,9 +539,10 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   double* Yp = ctx->d(L.Ypart);
   double* scal = ctx->d(L.scal);
   EvScope ev(ctx, st, &ctx->ev_post);
-  // the side stream's previous work shares the tridiagonal workspace with A4 below
-  oid_status s = join_side(ctx, st);
-  if (s != OID_OK) return s;
+  // an estimate on another stream must have snapshotted J / frob2 / the dirty list first
+  CK(cudaStreamWaitEvent(st, ctx->ev_snap, 0));
+  tl_mark(ctx, st, 3);
+  oid_status s = OID_OK;
   // A3: S <- [S, Y], SS^T += YY^T, ||A_obs||^2 += sum n_j
   gram_update_kernel<<<blocks_for(int64_t(ell) * ell), 256, 0, st>>>(Yp, ell, nc, ctx->d(L.gram), ctx->d(L.S), ctx->n_obs,
                                                                     scal);
@@ -561,7 +598,9 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
     scores_kernel<<<ns, 256, 0, st>>>(ctx->d(L.Tsc), ctx->d(L.mu), ell, ns, scal, ctx->d(L.tau), nullptr);
     CKL();
   }
-  // A6: selection / replacement
+  // A6: selection / replacement; the previous block's Alg 4 chain reads J first
+  tl_mark(ctx, st, 4);
+  CK(cudaStreamWaitEvent(st, ctx->ev_sj_j, 0));
   select_kernel<<<1, 32, 0, st>>>(ctx->ptr<int64_t>(L.J), ctx->d(L.tau_old), ctx->d(L.tau), Yp + int64_t(ell) * nc, t, nc,
                                   ctx->factor, static_cast<uint32_t>(ctx->epoch), ctx->n_obs, ctx->key0, ctx->key1,
                                   ctx->ptr<int>(L.admit), ctx->ptr<int>(L.counts), scal, ctx->ptr<int>(L.dirty));
@@ -569,9 +608,11 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   // A8 runs on the side stream, beside the basis copy
   s = fork_side(ctx, st);
   if (s != OID_OK) return s;
-  // A7: basis copy of this shard's rows
+  // A7: basis copy of this shard's rows, after the last estimate's basis reads
+  CK(cudaStreamWaitEvent(st, ctx->ev_gram_done, 0));
+  tl_mark(ctx, st, 5);
   {
-    dim3 grid(std::max(1u, std::min(blocks_for(ctx->m_loc), 2048u)), nc + t);
+    dim3 grid(std::max(1u, std::min(blocks_for(ctx->m_loc), static_cast<unsigned>(8 * ctx->num_sms))));
     if (p.dtype == OID_F64)
       basis_copy_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(X), ld, ctx->ptr<double>(L.C), ctx->m_loc,
                                                       ctx->ptr<int>(L.admit), ctx->ptr<int>(L.counts), nc, t);
@@ -580,8 +621,10 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
                                                      ctx->ptr<int>(L.admit), ctx->ptr<int>(L.counts), nc, t);
     CKL();
   }
+  tl_mark(ctx, st, 6);
   ctx->n_obs += nc;
   cudaStream_t cs = ctx->use_side ? ctx->side : st;
+  tl_mark(ctx, cs, 11);
   // A8: Alg 4 kept implicit: S_J^+ per epoch.  Fast path: S_J^+ = (S_J^T S_J)^-1 S_J^T
   // by the cluster tridiagonalisation when kappa(S_J) <= 1e5 (no R9 cutoff can act); else the
   // one-sided Jacobi SVD pseudo-inverse (gated on the device).
@@ -593,10 +636,12 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
     if (s != OID_OK) return s;
     fill_vacant_diag_kernel<<<1, 256, 0, cs>>>(ctx->d(L.sjG), t, ctx->ptr<int64_t>(L.J));
     CKL();
+    CK(cudaEventRecord(ctx->ev_sj_j, cs));   // last read of J in this chain
     s = spd_solve(ctx, cs, ctx->d(L.sjG), t, ctx->d(L.SJ), ell, true, ell, ctx->d(L.Sjpinv), t, false, 1e10, sjgate,
                   scal + SC_KAPPA);
     if (s != OID_OK) return s;
   } else {
+    CK(cudaEventRecord(ctx->ev_sj_j, cs));
     set_flag_kernel<<<1, 1, 0, cs>>>(sjgate, 0, 1);
     CKL();
   }
@@ -608,6 +653,8 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   s = pinv_assemble(ctx, cs, ctx->d(L.sjB), ell, t, ctx->d(L.sjV), ctx->d(L.sjsig), ctx->d(L.sjw), ctx->d(L.sjZ),
                     ctx->d(L.Sjpinv), scal + SC_KAPPA, OID_FLAG_SJ_RANK_DEFICIENT, fb);
   if (s != OID_OK) return s;
+  tl_mark(ctx, cs, 12);
+  CK(cudaEventRecord(ctx->ev_committed, st));
   ctx->epoch += 1;
   ctx->estimate_ready = true;
   return OID_OK;
@@ -639,6 +686,8 @@ oid_status estimate_pre(oid_ctx ctx, cudaStream_t st) {
   const int n = static_cast<int>(ctx->n_obs);
   double* S = ctx->d(L.S);
   double* scal = ctx->d(L.scal);
+  // kappa(S_J) of this epoch (the next Alg 4 chain on this stream overwrites it)
+  CK(cudaMemcpyAsync(scal + SC_KAPPA_EST, scal + SC_KAPPA, sizeof(double), cudaMemcpyDeviceToDevice, st));
   oid_status s = explicit_P(ctx, st);                                                 // P = S_J^+ S
   if (s != OID_OK) return s;
   double* P = ctx->d(L.Pexp);
@@ -780,11 +829,6 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
     const int big = static_cast<int>(prop.sharedMemPerBlockOptin) - 2048;
     if ((e = cudaFuncSetAttribute(bjacobi_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big)) != cudaSuccess) return bad(e);
     if ((e = cudaFuncSetAttribute(bjacobi_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big)) != cudaSuccess) return bad(e);
-#define BG_ATTR(TT, JB) \
-    if ((e = cudaFuncSetAttribute(basis_gram_dirty_kernel<TT, JB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 184 * 1024)) != cudaSuccess) return bad(e)
-    BG_ATTR(double, 1); BG_ATTR(double, 2);
-    BG_ATTR(float, 1); BG_ATTR(float, 2);
-#undef BG_ATTR
   }
   if (p->ell <= kTriMaxN) {
     if ((e = cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
@@ -808,8 +852,12 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
     if ((e = cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, hi)) != cudaSuccess) return bad(e);
     if ((e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming)) != cudaSuccess) return bad(e);
     if ((e = cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming)) != cudaSuccess) return bad(e);
+    for (cudaEvent_t* ev : {&ctx->ev_committed, &ctx->ev_snap, &ctx->ev_gram_done, &ctx->ev_sj_j, &ctx->ev_est_done})
+      if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess) return bad(e);
     if (getenv("OID_BG_FREE")) ctx->bg_free_sms = std::max(0, atoi(getenv("OID_BG_FREE")));
+    if (getenv("OID_BG_WAVES")) ctx->bg_waves = std::max(1, atoi(getenv("OID_BG_WAVES")));
     ctx->use_side = !(getenv("OID_NO_SIDE") && atoi(getenv("OID_NO_SIDE")) != 0);
+    ctx->timeline = getenv("OID_TIMELINE") && atoi(getenv("OID_TIMELINE")) != 0;
   }
   ctx->k1_ctas_per_sm = 1;
   ctx->cold_jacobi = getenv("OID_JACOBI_COLD") && atoi(getenv("OID_JACOBI_COLD")) != 0;
@@ -820,23 +868,31 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
     const bool f64 = p->dtype == OID_F64;
     const int es = f64 ? 8 : 4;
     const Layout& Lb = ctx->L;
-    if (prop.major == 10 && ctx->t <= 512 && (ctx->m_loc * es) % 16 == 0 && k1tc_encoder() != nullptr &&
-        !(getenv("OID_BG_SIMT") && atoi(getenv("OID_BG_SIMT")) != 0)) {
-      const cuuint64_t dims[2] = {static_cast<cuuint64_t>(ctx->m_loc), static_cast<cuuint64_t>(ctx->t)};
-      const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ctx->m_loc) * es};
-      const cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / es), static_cast<cuuint32_t>(std::min(ctx->t, 256))};
-      const cuuint32_t estr[2] = {1, 1};
-      CUresult cr = k1tc_encoder()(&ctx->bg_map, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
-                                   ctx->ws + Lb.C, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      ctx->bg_tc = cr == CUDA_SUCCESS;
+    // {RL rows, t slots, tiles} over the row-tiled basis: one box = one tile of all slots,
+    // t x 128 contiguous bytes (two boxes of <= 256 slots when t > 256)
+    const int64_t RL = 128 / es;
+    const int64_t ntiles = (ctx->m_loc + RL - 1) / RL;
+    if (k1tc_encoder() == nullptr) {
+      snprintf(g_init_err, sizeof(g_init_err), "init: cuTensorMapEncodeTiled unavailable");
+      delete ctx;
+      return OID_ECUDA;
+    }
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(RL), static_cast<cuuint64_t>(ctx->t), static_cast<cuuint64_t>(ntiles)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(RL * es), static_cast<cuuint64_t>(RL * es * ctx->t)};
+    const cuuint32_t box[3] = {static_cast<cuuint32_t>(RL), static_cast<cuuint32_t>(std::min(ctx->t, 256)), 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult cr = k1tc_encoder()(&ctx->bg_map, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                                 ctx->ws + Lb.C, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) {
+      snprintf(g_init_err, sizeof(g_init_err), "init: basis tensor map encoding failed (%d)", static_cast<int>(cr));
+      delete ctx;
+      return OID_ECUDA;
     }
     const int bgmax = 200 * 1024 + 1024;
-#define BGT_ATTR(TT, CW) \
-    if ((e = cudaFuncSetAttribute(bgtc::basis_gram_tc_kernel<TT, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, bgmax)) != cudaSuccess) return bad(e)
-    BGT_ATTR(double, 8); BGT_ATTR(double, 16); BGT_ATTR(float, 8); BGT_ATTR(float, 16);
-#undef BGT_ATTR
+    if ((e = cudaFuncSetAttribute(bgtc::basis_gram_tc_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, bgmax)) != cudaSuccess) return bad(e);
+    if ((e = cudaFuncSetAttribute(bgtc::basis_gram_tc_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, bgmax)) != cudaSuccess) return bad(e);
   }
   double qd[16];
   for (int i = 0; i < 16; ++i) qd[i] = q[i] + 0.5;
@@ -862,7 +918,11 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
   if ((e = cudaMemsetAsync(ctx->ws + L.Gfull, 0, sizeof(double) * ctx->t * ctx->t, st)) != cudaSuccess) return bad(e);
   if ((e = cudaMemsetAsync(ctx->ws + L.dirty, 0, sizeof(int) * ctx->t, st)) != cudaSuccess) return bad(e);
   if ((e = cudaMemsetAsync(ctx->ws + L.counts, 0, 4 * sizeof(int), st)) != cudaSuccess) return bad(e);
-  if ((e = cudaMemsetAsync(ctx->ws + L.C, 0, static_cast<size_t>(ctx->m_loc) * ctx->t * dsize(*p), st)) != cudaSuccess) return bad(e);
+  {
+    const int64_t RL = 128 / static_cast<int64_t>(dsize(*p));
+    const size_t cb = static_cast<size_t>((ctx->m_loc + RL - 1) / RL * RL) * ctx->t * dsize(*p);
+    if ((e = cudaMemsetAsync(ctx->ws + L.C, 0, cb, st)) != cudaSuccess) return bad(e);
+  }
   if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return bad(e);   // host arrays above go out of scope
   *out = ctx;
   return OID_OK;
@@ -918,62 +978,61 @@ oid_status oid_estimate_begin(oid_ctx ctx, void* stream) {
   const Layout& L = ctx->L;
   const int t = ctx->t;
   EvScope ev(ctx, st, &ctx->ev_est);
+  // this estimate may run on another stream than the ingests: order it after the last commit and
+  // snapshot what the next commit will change (J, frob2, the dirty-slot list)
+  CK(cudaStreamWaitEvent(st, ctx->ev_committed, 0));
+  tl_mark(ctx, st, 7);
+  dirty_compact_kernel<<<1, 32, 0, st>>>(ctx->ptr<int>(L.dirty), t, ctx->ptr<int>(L.dlist), ctx->ptr<int>(L.counts));
+  CKL();
+  est_snapshot_kernel<<<1, 256, 0, st>>>(ctx->ptr<int64_t>(L.J), t, ctx->ptr<int64_t>(L.Jsnap), ctx->d(L.scal));
+  CKL();
+  CK(cudaEventRecord(ctx->ev_snap, st));
   // A10 factors that do not need G: on the side stream, concurrently with A9 below
   oid_status s0 = fork_side(ctx, st);
   if (s0 != OID_OK) return s0;
+  tl_mark(ctx, ctx->use_side ? ctx->side : st, 13);
   s0 = estimate_pre(ctx, ctx->use_side ? ctx->side : st);
   if (s0 != OID_OK) return s0;
+  tl_mark(ctx, ctx->use_side ? ctx->side : st, 14);
+  tl_mark(ctx, st, 8);
   // A9: exact basis Gram G = A_J^T A_J, incremental: only the rows/columns of
   // slots admitted since the last estimate are recomputed, over this shard's rows.
-  dirty_compact_kernel<<<1, 32, 0, st>>>(ctx->ptr<int>(L.dirty), t, ctx->ptr<int>(L.dlist), ctx->ptr<int>(L.counts));
-  CKL();
-  if (ctx->bg_tc) {
+  {
     const bool f64 = ctx->p.dtype == OID_F64;
-    const int RL = f64 ? 16 : 32;
-    const int sms = std::max(1, ctx->num_sms - ctx->bg_free_sms);   // leave SMs to the side stream
-    int grid = static_cast<int>(std::min<int64_t>(std::min(sms, kGramChunks), (ctx->m_loc + RL - 1) / RL));
-    int64_t per = (ctx->m_loc + grid - 1) / grid;
-    per = (per + RL - 1) / RL * RL;
-    grid = static_cast<int>((ctx->m_loc + per - 1) / per);
+    const int64_t RL = f64 ? 16 : 32;
+    const int64_t ntiles = (ctx->m_loc + RL - 1) / RL;
+    // many short CTAs (waves of num_sms - bg_free_sms): kernels of higher-priority streams (the next
+    // block's K1 and post-pass, the side stream) are scheduled as they retire
+    const int sms = std::max(1, ctx->num_sms - ctx->bg_free_sms);
+    const int want = std::min(gram_tc_chunks(t), sms * ctx->bg_waves);
+    int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, (ntiles + 7) / 8)));
+    const int64_t per = (ntiles + grid - 1) / grid;
+    grid = static_cast<int>((ntiles + per - 1) / per);
     const int nbox = (t + 255) / 256;
     const int stage_bytes = (nbox * std::min(t, 256) * 128 + 1023) / 1024 * 1024;
     const int nstage = std::max(2, std::min(bgtc::kMaxStages, (200 * 1024) / stage_bytes));
     const size_t smem = static_cast<size_t>(nstage) * stage_bytes + 1024;
-#define BGT_LAUNCH(TT, CW)                                                                                         \
-  bgtc::basis_gram_tc_kernel<TT, CW><<<grid, 32 * (CW + 1), smem, st>>>(ctx->bg_map, ctx->m_loc, t, per, nstage,     \
-                                                                      stage_bytes, nbox, ctx->ptr<int>(L.dlist),   \
-                                                                      ctx->ptr<int>(L.counts), ctx->d(L.Gpart))
-    if (f64) { if (t <= 256) BGT_LAUNCH(double, 8); else BGT_LAUNCH(double, 16); }
-    else { if (t <= 256) BGT_LAUNCH(float, 8); else BGT_LAUNCH(float, 16); }
-#undef BGT_LAUNCH
+    if (f64)
+      bgtc::basis_gram_tc_kernel<double><<<grid, 32 * (bgtc::kCW + 1), smem, st>>>(
+          ctx->bg_map, ntiles, t, per, nstage, stage_bytes, nbox, ctx->ptr<int>(L.dlist), ctx->ptr<int>(L.counts),
+          ctx->d(L.Gpart));
+    else
+      bgtc::basis_gram_tc_kernel<float><<<grid, 32 * (bgtc::kCW + 1), smem, st>>>(
+          ctx->bg_map, ntiles, t, per, nstage, stage_bytes, nbox, ctx->ptr<int>(L.dlist), ctx->ptr<int>(L.counts),
+          ctx->d(L.Gpart));
     CKL();
-    sum_chunks_kernel<<<blocks_for(int64_t(t) * t), 256, 0, st>>>(ctx->d(L.Gpart), grid, int64_t(t) * t, ctx->d(L.Gsum));
+    CK(cudaEventRecord(ctx->ev_gram_done, st));
+    tl_mark(ctx, st, 9);
+    // two-level fixed-order sum: up to 64 segment sums into the tail of Gpart, then one
+    const int nseg = std::min(64, std::max(1, grid / 16));
+    double* seg = ctx->d(L.Gpart) + static_cast<size_t>(grid) * t * t;
+    sum_dirty_chunks_kernel<<<dim3(blocks_for(int64_t(t) * t), nseg), 256, 0, st>>>(ctx->d(L.Gpart), grid, t,
+                                                                                   ctx->ptr<int>(L.counts), seg);
     CKL();
-    return OID_OK;
+    sum_dirty_chunks_kernel<<<dim3(blocks_for(int64_t(t) * t), 1), 256, 0, st>>>(seg, nseg, t, ctx->ptr<int>(L.counts),
+                                                                                ctx->d(L.Gsum));
+    CKL();
   }
-  int chunks = static_cast<int>(std::min<int64_t>(std::min(2 * ctx->num_sms, kGramChunks), (ctx->m_loc + 1023) / 1024));
-  chunks = std::max(1, chunks);
-  int64_t per = (ctx->m_loc + chunks - 1) / chunks;
-  per = (per + kBgRows - 1) / kBgRows * kBgRows;
-  chunks = static_cast<int>((ctx->m_loc + per - 1) / per);
-  const bool f64 = ctx->p.dtype == OID_F64;
-  const size_t stage_bytes = f64 ? bg_stage_elems<double>(t) * 8 : bg_stage_elems<float>(t) * 4;
-  const int nstage = 2 * stage_bytes <= 180 * 1024 ? 2 : 1;
-  const size_t smem = nstage * stage_bytes;
-  const int jbw = (t + 255) / 256;   // j blocks of 32 per warp (8 warps)
-#define BG_LAUNCH(TT, JB)                                                                                       \
-  basis_gram_dirty_kernel<TT, JB><<<chunks, 256, smem, st>>>(ctx->ptr<TT>(L.C), ctx->m_loc, t, per, nstage,     \
-                                                             ctx->ptr<int>(L.dlist), ctx->ptr<int>(L.counts),   \
-                                                             ctx->d(L.Gpart))
-#define BG_DISPATCH(TT)                          \
-  if (jbw <= 1) BG_LAUNCH(TT, 1);                 \
-  else BG_LAUNCH(TT, 2)
-  if (f64) { BG_DISPATCH(double); } else { BG_DISPATCH(float); }
-#undef BG_DISPATCH
-#undef BG_LAUNCH
-  CKL();
-  sum_chunks_kernel<<<blocks_for(int64_t(t) * t), 256, 0, st>>>(ctx->d(L.Gpart), chunks, int64_t(t) * t, ctx->d(L.Gsum));
-  CKL();
   return OID_OK;
 }
 
@@ -986,28 +1045,35 @@ oid_status oid_estimate_end(oid_ctx ctx, double* out_dev, void* stream) {
   const int t = ctx->t, l1 = p.ell1, l2 = p.ell2;
   double* scal = ctx->d(L.scal);
   EvScope ev(ctx, st, &ctx->ev_est);
-  gram_scatter_kernel<<<blocks_for(int64_t(t) * t), 256, 0, st>>>(ctx->d(L.Gsum), ctx->ptr<int>(L.dlist),
+  // The G-dependent tail runs on the (highest-priority) side stream, after the G-independent
+  // factors already queued there (estimate_pre): it is short and must not wait behind the next
+  // block's K1 on a lower-priority estimate stream.  `st` joins it at the end.
+  oid_status s = fork_side(ctx, st);
+  if (s != OID_OK) return s;
+  cudaStream_t cs = ctx->use_side ? ctx->side : st;
+  gram_scatter_kernel<<<blocks_for(int64_t(t) * t), 256, 0, cs>>>(ctx->d(L.Gsum), ctx->ptr<int>(L.dlist),
                                                                   ctx->ptr<int>(L.counts), t, ctx->d(L.Gfull));
   CKL();
-  CK(cudaMemcpyAsync(ctx->d(L.G), ctx->d(L.Gfull), sizeof(double) * t * t, cudaMemcpyDeviceToDevice, st));
-  mask_gram_kernel<<<blocks_for(int64_t(t) * t), 256, 0, st>>>(ctx->d(L.G), ctx->ptr<int64_t>(L.J), t);
+  CK(cudaMemcpyAsync(ctx->d(L.G), ctx->d(L.Gfull), sizeof(double) * t * t, cudaMemcpyDeviceToDevice, cs));
+  mask_gram_kernel<<<blocks_for(int64_t(t) * t), 256, 0, cs>>>(ctx->d(L.G), ctx->ptr<int64_t>(L.Jsnap), t);
   CKL();
-  // the G-independent factors were formed on the side stream (estimate_pre)
-  oid_status s = join_side(ctx, st);
-  if (s != OID_OK) return s;
   if (l1 > 0 && l2 > 0) {
     // term1 = tr(M (Omega1 A P^T) G (Omega2 A P^T)^T) = <Q1 G, X2>
-    s = gemm(ctx, st, false, false, l2, t, t, 1.0, ctx->d(L.Q1), l2, ctx->d(L.G), t, 0.0, ctx->d(L.Q2), l2);
+    s = gemm(ctx, cs, false, false, l2, t, t, 1.0, ctx->d(L.Q1), l2, ctx->d(L.G), t, 0.0, ctx->d(L.Q2), l2);
     if (s != OID_OK) return s;
-    frob_dot_kernel<<<1, 256, 0, st>>>(ctx->d(L.Q2), l2, ctx->d(L.X2), l2, l2, t, scal + SC_T1);
+    frob_dot_kernel<<<1, 256, 0, cs>>>(ctx->d(L.Q2), l2, ctx->d(L.X2), l2, l2, t, scal + SC_T1);
     CKL();
   }
   // tr(G P P^T) = ||A_J P||_F^2
-  frob_dot_kernel<<<1, 256, 0, st>>>(ctx->d(L.G), t, ctx->d(L.PPt), t, t, t, scal + SC_GPP);
+  frob_dot_kernel<<<1, 256, 0, cs>>>(ctx->d(L.G), t, ctx->d(L.PPt), t, t, t, scal + SC_GPP);
   CKL();
-  hutch_final_kernel<<<1, 32, 0, st>>>(scal, p.ell3, ctx->ptr<unsigned>(L.flags), ctx->d(L.est));
+  hutch_final_kernel<<<1, 32, 0, cs>>>(scal, p.ell3, ctx->ptr<unsigned>(L.flags), ctx->d(L.est));
   CKL();
-  if (out_dev) CK(cudaMemcpyAsync(out_dev, ctx->d(L.est), 8 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  if (out_dev) CK(cudaMemcpyAsync(out_dev, ctx->d(L.est), 8 * sizeof(double), cudaMemcpyDeviceToDevice, cs));
+  s = join_side(ctx, st);
+  if (s != OID_OK) return s;
+  CK(cudaEventRecord(ctx->ev_est_done, st));
+  tl_mark(ctx, st, 10);
   return OID_OK;
 }
 
@@ -1031,6 +1097,7 @@ oid_status oid_finalize(oid_ctx ctx, int64_t* J_host, double* P, int32_t P_on_de
   const int t = ctx->t;
   oid_status sj = join_side(ctx, st);
   if (sj != OID_OK) return sj;
+  CK(cudaStreamWaitEvent(st, ctx->ev_est_done, 0));
   if (ctx->n_obs > 0 && P) {
     oid_status s = explicit_P(ctx, st);
     if (s != OID_OK) return s;
@@ -1039,7 +1106,14 @@ oid_status oid_finalize(oid_ctx ctx, int64_t* J_host, double* P, int32_t P_on_de
   }
   if (J_host) CK(cudaMemcpyAsync(J_host, ctx->ws + L.J, sizeof(int64_t) * t, cudaMemcpyDeviceToHost, st));
   if (basis_dev)
-    CK(cudaMemcpyAsync(basis_dev, ctx->ws + L.C, static_cast<size_t>(ctx->m_loc) * t * dsize(ctx->p), cudaMemcpyDeviceToDevice, st));
+  {
+    const unsigned g = static_cast<unsigned>(std::min<int64_t>(blocks_for(ctx->m_loc * t), 8 * ctx->num_sms));
+    if (ctx->p.dtype == OID_F64)
+      basis_untile_kernel<double><<<g, 256, 0, st>>>(ctx->ptr<double>(L.C), ctx->m_loc, t, static_cast<double*>(basis_dev));
+    else
+      basis_untile_kernel<float><<<g, 256, 0, st>>>(ctx->ptr<float>(L.C), ctx->m_loc, t, static_cast<float*>(basis_dev));
+    CKL();
+  }
   CK(cudaStreamSynchronize(st));
   return OID_OK;
 }
@@ -1063,12 +1137,28 @@ oid_status oid_get(oid_ctx ctx, int32_t field, void* host_dst, size_t bytes, voi
     case 10: off = L.dbg; need = k1tc::kDbgRows * k1tc::kDbgTiles * sizeof(long long); break;
     case 11: off = L.G; need = sizeof(double) * ctx->t * ctx->t; break;
     case 12: off = L.dbg + k1tc::kDbgRows * k1tc::kDbgTiles * sizeof(long long); need = k1tc::kDbgTiles * sizeof(long long); break;
+    case 13: {   // timeline: up to 4096 (tag, ms since the first mark) pairs, then cleared
+      if (bytes < 2 * 4096 * sizeof(double)) return ctx->fail(OID_ESHAPE, "field 13 needs %zu bytes", 2 * 4096 * sizeof(double));
+      CK(cudaDeviceSynchronize());
+      double* o = static_cast<double*>(host_dst);
+      for (size_t i = 0; i < 4096; ++i) { o[2 * i] = -1.0; o[2 * i + 1] = 0.0; }
+      for (size_t i = 0; i < ctx->tl.size(); ++i) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->tl[0].second, ctx->tl[i].second);
+        o[2 * i] = ctx->tl[i].first;
+        o[2 * i + 1] = ms;
+      }
+      for (auto& pr : ctx->tl) cudaEventDestroy(pr.second);
+      ctx->tl.clear();
+      return OID_OK;
+    }
     default: return ctx->fail(OID_EINVAL, "unknown field %d", field);
   }
   if (bytes < need) return ctx->fail(OID_ESHAPE, "field %d needs %zu bytes", field, need);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   oid_status sj = join_side(ctx, st);
   if (sj != OID_OK) return sj;
+  CK(cudaStreamWaitEvent(st, ctx->ev_est_done, 0));
   if (need) CK(cudaMemcpyAsync(host_dst, ctx->ws + off, need, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   return OID_OK;
@@ -1100,6 +1190,7 @@ oid_status oid_stats(oid_ctx ctx, oid_stats_t* out) {
   CK(sum(ctx->ev_est, &out->est_ms));
   unsigned f = 0;
   CK(cudaStreamSynchronize(ctx->side));
+  CK(cudaEventSynchronize(ctx->ev_est_done));
   CK(cudaMemcpy(&f, ctx->ws + ctx->L.flags, sizeof(unsigned), cudaMemcpyDeviceToHost));
   out->flags = f;
   return OID_OK;
@@ -1124,6 +1215,8 @@ void oid_destroy(oid_ctx ctx) {
   }
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  for (cudaEvent_t ev : {ctx->ev_committed, ctx->ev_snap, ctx->ev_gram_done, ctx->ev_sj_j, ctx->ev_est_done})
+    if (ev) cudaEventDestroy(ev);
   oid_stats_reset(ctx);
   delete ctx;
 }

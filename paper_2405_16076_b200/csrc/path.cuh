@@ -8,7 +8,7 @@ namespace oid {
 // scalars layout (device double array)
 enum Scal : int {
   SC_FROB2 = 0, SC_LAM = 1, SC_EK = 2, SC_SHIFT = 3, SC_TRACE = 4, SC_DMAX = 5, SC_MINMARGIN = 6, SC_KAPPA = 7,
-  SC_T1 = 8, SC_T3A = 9, SC_T3B = 10, SC_GPP = 11, SC_COUNT = 16
+  SC_T1 = 8, SC_T3A = 9, SC_T3B = 10, SC_GPP = 11, SC_FROB2_EST = 12, SC_KAPPA_EST = 13, SC_COUNT = 16
 };
 
 // Ridge regulariser (reading R8): eigenvalues mu of the unscaled Gram, E_k = sum of the k
@@ -137,22 +137,46 @@ __global__ void select_kernel(int64_t* __restrict__ J, double* __restrict__ tau_
 }
 
 // C(:, slot) <- X(:, r) for admissions, C(:, slot) <- 0 for vacated slots.
+// A7: basis slab C(:, slot) <- X(:, r) bit-exactly for every admission and C(:, slot) <- 0
+// for vacated slots, in the row-tiled layout C_blk[tile][slot][RL] (RL = 128 bytes of rows;
+// DESIGN.md section 6) that A9 streams with one TMA box per tile.  Each column is spread over
+// the whole (small, persistent) grid, so the kernel never floods the block scheduler.
 template <typename T>
-__global__ void basis_copy_kernel(const T* __restrict__ X, int64_t ld, T* __restrict__ C, int64_t m_loc,
+__global__ void basis_copy_kernel(const T* __restrict__ X, int64_t ld, T* __restrict__ Cb, int64_t m_loc,
                                   const int* __restrict__ admit, const int* __restrict__ counts, int nc, int t) {
-  const int a = blockIdx.y;
+  constexpr int RL = 128 / sizeof(T);
+  constexpr int V = 16 / sizeof(T);
   const int na = counts[0], nz = counts[1];
-  int slot, r = -1;
-  if (a < na) { slot = admit[2 * a]; r = admit[2 * a + 1]; }
-  else if (a - na < nz) { slot = admit[2 * (nc + t) - 2 - 2 * (a - na)]; }
-  else return;
-  T* dst = C + static_cast<int64_t>(slot) * m_loc;
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  if (r >= 0) {
-    const T* src = X + static_cast<int64_t>(r) * ld;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < m_loc; i += stride) dst[i] = src[i];
-  } else {
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < m_loc; i += stride) dst[i] = T(0);
+  const bool vec = (m_loc % V == 0) && (ld % V == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0);
+  for (int a = 0; a < na + nz; ++a) {
+    int slot, r = -1;
+    if (a < na) { slot = admit[2 * a]; r = admit[2 * a + 1]; }
+    else slot = admit[2 * (nc + t) - 2 - 2 * (a - na)];
+    const T* src = r >= 0 ? X + static_cast<int64_t>(r) * ld : nullptr;
+    if (vec) {
+      for (int64_t v = tid; v < m_loc / V; v += stride) {
+        const int64_t i = v * V;
+        const uint4 x = src ? __ldcs(reinterpret_cast<const uint4*>(src + i)) : make_uint4(0u, 0u, 0u, 0u);
+        __stcs(reinterpret_cast<uint4*>(Cb + ((i / RL) * t + slot) * RL + (i % RL)), x);
+      }
+    } else {
+      for (int64_t i = tid; i < m_loc; i += stride) Cb[((i / RL) * t + slot) * RL + (i % RL)] = src ? src[i] : T(0);
+    }
+  }
+}
+
+// out (m_loc x t, column-major) <- the row-tiled basis C_blk (oid_finalize)
+template <typename T>
+__global__ void basis_untile_kernel(const T* __restrict__ Cb, int64_t m_loc, int t, T* __restrict__ out) {
+  constexpr int RL = 128 / sizeof(T);
+  const int64_t n = m_loc * t;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int slot = static_cast<int>(e / m_loc);
+    const int64_t i = e - static_cast<int64_t>(slot) * m_loc;
+    out[e] = Cb[((i / RL) * t + slot) * RL + (i % RL)];
   }
 }
 
@@ -182,7 +206,7 @@ __global__ void hutch_final_kernel(const double* __restrict__ scal, int ell3, co
   const double term1 = scal[SC_T1];
   const double T = ell3 > 0 ? term1 + (scal[SC_T3A] - scal[SC_T3B]) / ell3 : term1;
   const double gpp = scal[SC_GPP];
-  const double frob2 = scal[SC_FROB2];
+  const double frob2 = scal[SC_FROB2_EST];    // ||A_obs||^2 of the estimated state (snapshot)
   const double e2 = frob2 - 2.0 * T + gpp;
   unsigned f = *flags;
   if (e2 < 0.0) f |= 4u;
@@ -190,7 +214,14 @@ __global__ void hutch_final_kernel(const double* __restrict__ scal, int ell3, co
   out[0] = e2; out[1] = T; out[2] = gpp; out[3] = frob2; out[4] = est;
   out[5] = frob2 > 0.0 ? est / sqrt(frob2) : 0.0;
   out[6] = static_cast<double>(f);
-  out[7] = scal[SC_KAPPA];
+  out[7] = scal[SC_KAPPA_EST];
+}
+
+// Snapshot for an estimate that may overlap the next commit: J and ||A_obs||^2.
+__global__ void est_snapshot_kernel(const int64_t* __restrict__ J, int t, int64_t* __restrict__ Jsnap,
+                                    double* __restrict__ scal) {
+  for (int i = threadIdx.x; i < t; i += blockDim.x) Jsnap[i] = J[i];
+  if (threadIdx.x == 0) scal[SC_FROB2_EST] = scal[SC_FROB2];
 }
 
 // Slots admitted since the last estimate (dirty flags set by select_kernel), compacted in
@@ -201,140 +232,6 @@ __global__ void dirty_compact_kernel(int* __restrict__ dirty, int t, int* __rest
   for (int i = 0; i < t; ++i)
     if (dirty[i]) { list[c++] = i; dirty[i] = 0; }
   counts[2] = c;
-}
-
-// Incremental exact basis Gram (A9): Dpart[chunk](q, j) = sum_{rows in chunk} C(r, d_q) C(r, j)
-// for the dirty slots d_q.  Each CTA streams its row chunk of the basis once per
-// group of 32 dirty slots, 32 rows at a time through a 2-stage cp.async ring (column-major tile,
-// pitch BG_PITCH elements: conflict-free column-strided reads).  Thread (tq, tj) = (tid % 8,
-// tid / 8) owns the 4 x JB register tile q = tq + 8a, j = tj + 32b (fp64 FMA, fixed order).
-constexpr int kBgRows = 32;
-template <typename T> struct BgPitch { static constexpr int v = sizeof(T) == 8 ? 34 : 36; };
-
-template <typename T>
-__host__ __device__ constexpr size_t bg_stage_elems(int t) { return static_cast<size_t>(t) * BgPitch<T>::v; }
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N> __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
-
-// fp64 tensor-core MMA (DMMA): D (8x8) += A (8x4, row) * B (4x8, col).  Fragments: a = A[lane/4][lane%4],
-// b = B[lane%4][lane/4], c = C[lane/4][2 (lane%4) + {0, 1}].
-__device__ __forceinline__ void dmma_m8n8k4(double (&c)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-               : "+d"(c[0]), "+d"(c[1])
-               : "d"(a), "d"(b));
-}
-
-// Warp w owns the output columns j in [32 (w + 8 i), +32) for i < JBW (t <= 256 JBW); the 32 dirty
-// slots q of the group are the M dimension (4 m8 blocks), the basis rows the K dimension.
-template <typename T, int JBW>
-__global__ void __launch_bounds__(256) basis_gram_dirty_kernel(const T* __restrict__ C, int64_t m_loc, int t,
-                                                               int64_t rows_per_chunk, int nstage,
-                                                               const int* __restrict__ list,
-                                                               const int* __restrict__ counts,
-                                                               double* __restrict__ part) {
-  extern __shared__ __align__(16) unsigned char bg_smem[];
-  constexpr int P = BgPitch<T>::v;
-  constexpr int EPC = 16 / sizeof(T);                  // elements per 16-byte copy
-  T* tiles = reinterpret_cast<T*>(bg_smem);            // [nstage][t][P]
-  __shared__ double dt[kBgRows][33];                   // dirty columns of the current tile
-  __shared__ int dl[32];
-  const int nd = counts[2];
-  if (nd == 0) return;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g4 = lane >> 2, i4 = lane & 3;
-  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * rows_per_chunk;
-  const int64_t r1 = min(m_loc, r0 + rows_per_chunk);
-  const int ntile = static_cast<int>((r1 - r0 + kBgRows - 1) / kBgRows);
-  const size_t stage = bg_stage_elems<T>(t);
-  const bool vec = ((m_loc * sizeof(T)) % 16 == 0) && (r0 % EPC == 0);
-  double* out = part + static_cast<int64_t>(blockIdx.x) * t * t;
-
-  auto load = [&](int it, int buf) {
-    T* dst = tiles + buf * stage;
-    const int64_t rb = r0 + static_cast<int64_t>(it) * kBgRows;
-    constexpr int CH = kBgRows / EPC;                  // 16-byte chunks per column
-    for (int e = tid; e < t * CH; e += 256) {
-      const int col = e / CH, c = e - col * CH;
-      const int64_t r = rb + c * EPC;
-      T* d = dst + col * P + c * EPC;
-      const T* src = C + static_cast<int64_t>(col) * m_loc + r;
-      if (vec && r + EPC <= r1) {
-        cp_async16(d, src);
-      } else {
-#pragma unroll
-        for (int k = 0; k < EPC; ++k) d[k] = (r + k < r1) ? src[k] : T(0);
-      }
-    }
-  };
-
-  for (int q0 = 0; q0 < nd; q0 += 32) {
-    if (tid < 32) dl[tid] = (q0 + tid < nd) ? list[q0 + tid] : -1;
-    double acc[JBW][4][4][2];
-#pragma unroll
-    for (int b = 0; b < JBW; ++b)
-#pragma unroll
-      for (int mm = 0; mm < 4; ++mm)
-#pragma unroll
-        for (int n = 0; n < 4; ++n) { acc[b][mm][n][0] = 0.0; acc[b][mm][n][1] = 0.0; }
-    __syncthreads();
-    load(0, 0);
-    cp_async_commit();
-    for (int it = 0; it < ntile; ++it) {
-      const int buf = nstage == 2 ? (it & 1) : 0;
-      if (nstage == 2 && it + 1 < ntile) load(it + 1, buf ^ 1);
-      cp_async_commit();
-      if (nstage == 2) cp_async_wait<1>(); else cp_async_wait<0>();
-      __syncthreads();
-      const T* tile = tiles + buf * stage;
-      for (int e = tid; e < 32 * kBgRows; e += 256) {        // gather the dirty columns
-        const int q = e >> 5, rr = e & 31;
-        const int d = dl[q];
-        dt[rr][q] = d >= 0 ? static_cast<double>(tile[d * P + rr]) : 0.0;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int ks = 0; ks < kBgRows; ks += 4) {
-        double a[4];
-#pragma unroll
-        for (int mm = 0; mm < 4; ++mm) a[mm] = dt[ks + i4][8 * mm + g4];
-#pragma unroll
-        for (int b = 0; b < JBW; ++b) {
-          const int jb = 32 * (warp + 8 * b);
-          if (jb >= t) continue;                             // warp-uniform
-#pragma unroll
-          for (int n = 0; n < 4; ++n) {
-            const int j = jb + 8 * n + g4;
-            const double bv = j < t ? static_cast<double>(tile[j * P + ks + i4]) : 0.0;
-#pragma unroll
-            for (int mm = 0; mm < 4; ++mm) dmma_m8n8k4(acc[b][mm][n], a[mm], bv);
-          }
-        }
-      }
-      __syncthreads();
-      if (nstage == 1 && it + 1 < ntile) load(it + 1, 0);
-    }
-#pragma unroll
-    for (int b = 0; b < JBW; ++b) {
-      const int jb = 32 * (warp + 8 * b);
-#pragma unroll
-      for (int mm = 0; mm < 4; ++mm) {
-        const int q = 8 * mm + g4;
-        if (q0 + q >= nd) continue;
-#pragma unroll
-        for (int n = 0; n < 4; ++n)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int j = jb + 8 * n + 2 * i4 + h;
-            if (j < t) out[(q0 + q) + static_cast<int64_t>(j) * t] = acc[b][mm][n][h];
-          }
-      }
-    }
-  }
 }
 
 // G(d_q, j) = G(j, d_q) = D(q, j) for the dirty slots (after the cross-shard reduction).
@@ -356,6 +253,24 @@ __global__ void sum_chunks_kernel(const double* __restrict__ part, int nchunks, 
   double s = 0.0;
   for (int c = 0; c < nchunks; ++c) s += part[static_cast<int64_t>(c) * n + idx];
   out[idx] = s;
+}
+
+// Two-level fixed-order sum of the per-chunk A9 partials over the dirty rows q < counts[2]:
+// pass 1 (grid.y = nseg segments of the chunk range) writes seg[y](q, j); pass 2 (nseg = 1 view)
+// sums the segments into out(q, j).  Layout of every partial: t x t column-major.
+__global__ void sum_dirty_chunks_kernel(const double* __restrict__ part, int nchunks, int t, const int* __restrict__ counts,
+                                        double* __restrict__ out) {
+  const int nd = counts[2];
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<int64_t>(nd) * t) return;
+  const int q = static_cast<int>(idx % nd), j = static_cast<int>(idx / nd);
+  const int64_t e = q + static_cast<int64_t>(j) * t;
+  const int64_t n = static_cast<int64_t>(t) * t;
+  const int per = (nchunks + gridDim.y - 1) / gridDim.y;
+  const int c0 = blockIdx.y * per, c1 = min(nchunks, c0 + per);
+  double s = 0.0;
+  for (int c = c0; c < c1; ++c) s += part[static_cast<int64_t>(c) * n + e];
+  out[static_cast<int64_t>(blockIdx.y) * n + e] = s;
 }
 
 // gate[0] = a, gate[1] = b

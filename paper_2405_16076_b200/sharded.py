@@ -14,8 +14,14 @@ This module is host-side plumbing only: it calls the engine's C-ABI entry points
 of the method.
 """
 
+import contextlib
+
 import torch
 import torch.distributed as dist
+
+
+def _null():
+    return contextlib.nullcontext()
 
 ROW_ALIGN = 32   # Philox row-group size of the sketch entries (reading R2): slab starts stay aligned
 
@@ -58,7 +64,11 @@ class ShardedIngest:
         self.engine.ingest_commit(X)
 
     def estimate(self, out=None):
-        """NA-Hutch++ estimate (Alg 8); out: 8 fp64 values (see include/oid.h)."""
-        self.engine.estimate_begin()
-        self._reduce(self.engine.partials(1))
-        return self.engine.estimate_end(out)
+        """NA-Hutch++ estimate (Alg 8); out: 8 fp64 values (see include/oid.h).  The reduction runs
+        on the engine's estimate stream when it has one (torch.distributed uses the current stream)."""
+        est = getattr(self.engine, "estimate_stream", None)
+        ctx = torch.cuda.stream(est) if est is not None and self.world > 1 else _null()
+        with ctx:
+            self.engine.estimate_begin()
+            self._reduce(self.engine.partials(1))
+            return self.engine.estimate_end(out)

@@ -1,0 +1,38 @@
+"""Diagnostics: per-step stream timeline of the C3 bench loop (OID_TIMELINE=1), two streams
+(ingest high priority, estimate low) unless --one-stream.  Prints each tagged mark in ms."""
+import os
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ["OID_TIMELINE"] = "1"
+import __graft_entry__ as ge
+ge.build()
+import paper_2405_16076_b200 as oid
+from synth import ChannelFlow, C3
+
+one = "--one-stream" in sys.argv
+steps = 6
+gen = ChannelFlow(192, 129, 192, seed=1003)
+dev = torch.device("cuda", 0)
+p = oid.make_params(m=gen.m, k=C3.k, ell=C3.ell, b_max=C3.b, n_cap=1000, lam=-1.0, seed=0)
+I = torch.cuda.Stream(dev, priority=-1)
+E = I if one else torch.cuda.Stream(dev, priority=0)
+eng = oid.Engine(p, stream=I, estimate_stream=E)
+blocks = [gen.block_torch(s * C3.b, (s + 1) * C3.b, dev).T for s in range(steps)]
+torch.cuda.synchronize()
+out = torch.empty(8, dtype=torch.float64, device=dev)
+for s in range(steps):
+    eng.ingest_block(blocks[s])
+    eng.estimate_begin()
+    eng.estimate_end(out)
+torch.cuda.synchronize()
+tl = eng.get(13)
+names = {1: "K1 start", 2: "K1 end", 3: "commit start", 4: "post chain end", 5: "copy start", 6: "copy end",
+         11: "S_J chain start (side)", 12: "S_J chain end (side)", 7: "est begin (E)", 13: "est_pre start (side)",
+         14: "est_pre end (side)", 8: "Gram start (E)", 9: "Gram end (E)", 10: "est end (E)"}
+rows = [(int(t), ms) for t, ms in tl if t >= 0]
+for t, ms in rows:
+    print(f"{ms:9.3f}  {names.get(t, t)}")
+k1s = [ms for t, ms in rows if t == 1]
+print("K1 start deltas:", np.round(np.diff(k1s), 3))

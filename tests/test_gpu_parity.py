@@ -282,3 +282,36 @@ def test_virtual_shards_match_single(oid):
     s1.estimate_end(out)
     ref = single.error_estimate()
     assert abs(out[5].item() - ref["est_rel"]) < 1e-8
+
+
+def test_two_stream_estimates_match_one_stream(oid):
+    """Estimates on a second stream (overlapping the next block's ingest)
+    give bitwise the same J, estimates and P as the single-stream engine."""
+    cfg = C3R
+    gen = ChannelFlow(48, 33, 48, seed=cfg.data_seed)
+    A = gen.block(0, 8 * cfg.b)
+    split = _split(cfg.ell)
+    p = oid.make_params(m=cfg.m, k=cfg.k, ell=cfg.ell, b_max=cfg.b, n_cap=8 * cfg.b, lam=-1.0, split=split, seed=0)
+    one = oid.Engine(p)
+    hi = torch.cuda.Stream(priority=-1)
+    lo = torch.cuda.Stream(priority=0)
+    two = oid.Engine(p, stream=hi, estimate_stream=lo)
+    Ad = _dev(A, np.float64)
+    torch.cuda.synchronize()
+    out1 = torch.empty((8, 8), dtype=torch.float64, device="cuda:0")
+    out2 = torch.empty((8, 8), dtype=torch.float64, device="cuda:0")
+    for e, j in enumerate(range(0, 8 * cfg.b, cfg.b)):
+        one.ingest_block(Ad[:, j:j + cfg.b])
+        one.estimate_begin()
+        one.estimate_end(out1[e])
+        with torch.cuda.stream(hi):
+            two.ingest_block(Ad[:, j:j + cfg.b])
+        two.estimate_begin()
+        two.estimate_end(out2[e])
+    torch.cuda.synchronize()
+    assert torch.equal(out1, out2)
+    assert np.array_equal(one.J(), two.J())
+    P1 = one.finalize()["P"]
+    P2 = two.finalize()["P"]
+    torch.cuda.synchronize()
+    assert torch.equal(P1, P2)
