@@ -31,3 +31,7 @@ print("slicer (median cycles): prefetch load %.0f | wait b_empty + convert %.0f 
       (np.median(S1 - S0), np.median(S2 - S1), np.median(S3 - S2), np.median(S4 - S3), np.median(S0[1:] - S4[:-1])))
 for t in [0, 1, 2, 3, 10, 100, 1000, n - 1]:
     print(t, "A %.0f B %.0f M0 %.0f M1 %.0f T %.0f" % (A[t] - base, B[t] - base, M0[t] - base, M1[t] - base, T[t] - base))
+# slicer rows (group of tile t): 5 before x_full wait, 6 after load + b_empty wait, 7 after convert +
+# bar_or, 8 after the token wait, 9 after the bookkeeping
+print("slicer phases (median cycles): x wait+load+b_empty %.0f | convert+bar_or %.0f | token wait %.0f | bookkeeping %.0f | to next own tile %.0f" %
+      (np.median(S1 - S0), np.median(S2 - S1), np.median(S3 - S2), np.median(S4 - S3), np.median(S0[2:] - S4[:-2])))
