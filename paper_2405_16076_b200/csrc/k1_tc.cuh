@@ -125,6 +125,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// polling wait (mbarrier.test_wait): no suspend/wake-up latency, for the single MMA-issuer warp
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "SPIN_%=:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra SPIN_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -279,11 +289,12 @@ template <> struct Bits<float> {
 // fp64 pipe: hi = floor(x 2^(F-32)) and lo = x 2^F - hi 2^32 in [0, 2^32) are exact; lo is
 // rounded to nearest by the 2^52 magic add (a carry out of lo goes into hi).
 // p32 = 2^(F-32), p0 = 2^F, both 0 for an all-zero column.
-__device__ __forceinline__ void fixpt(double x, double p32, double p0, uint32_t& lo, uint32_t& hi) {
+__device__ __forceinline__ void fixpt(double x, double p32, double p0, uint32_t& lo, uint32_t& hi, double& vout) {
   const double M = 6755399441055744.0;             // 1.5 * 2^52
   const double t1 = __fma_rd(x, p32, M);            // M + floor(x 2^(F-32))
   const double hd = t1 - M;                         // exact
   const double v = x * p0;                          // exact (power-of-two scaling)
+  vout = v;
   const double l = fma(hd, -4294967296.0, v);       // exact, in [0, 2^32)
   const double t2 = l + 4503599627370496.0;         // 2^52 + rint(l)
   const uint32_t t2h = static_cast<uint32_t>(__double2hiint(t2));
@@ -575,7 +586,8 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
               nacc = fma(x, x, nacc);
               cacc += x;
             }
-            fixpt(x, p32, p0, lo[r], hi[r]);
+            double v;
+            fixpt(x, p32, p0, lo[r], hi[r], v);
           }
           // 4x4 byte transposes: word w4 of digit plane p = byte p of rows 4w4 .. 4w4+3
           const uint32_t x0 = prmt(lo[0], lo[1], 0x5140), x1 = prmt(lo[0], lo[1], 0x7362);
@@ -694,7 +706,11 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
     const uint64_t g32_0 = static_cast<uint64_t>((row_begin + r0) >> 5);
     for (int t = 0; t < ntiles; ++t) {
       const int sa = t & 1;
-      if (t >= 2) mbar_wait(&sh.a_empty[sa], ((t >> 1) - 1) & 1);
+      if (t >= 2) {
+        if (lane == 0) mbar_wait(&sh.a_empty[sa], ((t >> 1) - 1) & 1);
+        __syncwarp();
+        tc_fence_after();
+      }
       // all 2 TM Philox calls of this thread's rows run interleaved (independent streams, shared
       // key schedule): instruction-level parallelism instead of 2 TM dependent 10-round chains
       constexpr int NC = 2 * TM;
@@ -742,9 +758,13 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
             const uint32_t w = ws[k], w4 = w << 4;
             const uint32_t mlo = prmt(t0, t1, w & 0x7777u), mhi = prmt(t0, t1, (w >> 16) & 0x7777u);
             const uint32_t slo = prmt(w, w4, 0x9D8Cu), shi = prmt(w, w4, 0xBFAEu);   // sign bytes 0x00/0xFF
-            pk[8 * kc + 2 * k] = r < ell ? (mlo ^ slo) : 0u;
-            pk[8 * kc + 2 * k + 1] = r < ell ? (mhi ^ shi) : 0u;
+            pk[8 * kc + 2 * k] = mlo ^ slo;
+            pk[8 * kc + 2 * k + 1] = mhi ^ shi;
           }
+        }
+        if (half * ROWS + tm * 128 + quarter * 32 + 31 >= ell && r >= ell) {   // warp-uniform test first
+#pragma unroll
+          for (int k = 0; k < 16; ++k) pk[k] = 0u;
         }
         tmem_st16(tmem + (static_cast<uint32_t>(32 * quarter) << 16) + ACOL0 + (sa * TM + tm) * 16, pk);
       }
