@@ -106,7 +106,7 @@ struct Bump {
 struct Layout {
   size_t S, gram, Ypart, k1part, k1npart, gB, gV, mu, mu_sorted, Yc, Tsc, tau, scal, J, tau_old, admit, counts,
       flags, counters, C, SJ, sjB, sjV, sjsig, sjw, sjZ, Sjpinv, Pexp, AJP, G, Gsum, Gpart, cB, cV, csig, cw, cZ, M,
-      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, wyT, sjG, cG, cBt, cZ2, dbg, Jsnap, td2, te2, Vh2, tauv2, wyT2, ldl2, mu2, total;
+      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, wyT, sjG, cG, cBt, cZ2, dbg, Jsnap, Dsnap, td2, te2, Vh2, tauv2, wyT2, ldl2, mu2, total;
 };
 
 int64_t m_local(const oid_params& p) { return p.row_end - p.row_begin; }
@@ -142,13 +142,13 @@ Layout make_layout(const oid_params& p) {
     const int64_t RL = 128 / static_cast<int64_t>(dsize(p));
     L.C = b.take(static_cast<size_t>((m_local(p) + RL - 1) / RL * RL) * t * dsize(p));
   }
-  L.SJ = b.take(ell * t * d);
+  L.SJ = b.take(2 * ell * t * d);          // per epoch parity (the next A8 overlaps this estimate)
   L.sjB = b.take(ell * t * d);
   L.sjV = b.take(t * t * d);
   L.sjsig = b.take(t * d);
   L.sjw = b.take(t * d);
   L.sjZ = b.take(t * ell * d);
-  L.Sjpinv = b.take(t * ell * d);
+  L.Sjpinv = b.take(2 * t * ell * d);
   L.Pexp = b.take(t * n * d);
   L.AJP = b.take(ell * n * d);
   L.G = b.take(t * t * d);
@@ -200,7 +200,8 @@ Layout make_layout(const oid_params& p) {
   L.wyT2 = b.take(static_cast<size_t>(kMaxRefChunks) * kRefChunk * kRefChunk * d);
   L.ldl2 = b.take(2 * ell * d);
   L.mu2 = b.take(ell * d);
-  L.Jsnap = b.take(t * sizeof(int64_t));
+  L.Jsnap = b.take(2 * t * sizeof(int64_t));
+  L.Dsnap = b.take(2 * t * sizeof(int));
   L.tc = b.take(k1tc_workspace_bytes(p.ell, p.b_max, m_local(p), p.dtype == OID_F64));
   L.total = b.off;
   return L;
@@ -256,13 +257,17 @@ struct oid_ctx_s {
   // Side stream (highest priority) for the latency-bound chains that do not depend on the
   // HBM-bound kernels of the caller's stream: the Alg 4 factorisation (A8) runs beside the basis
   // copy (A7) and the basis-Gram-independent part of Alg 8 (A10) beside the basis Gram (A9).
-  cudaStream_t side = nullptr;
+  cudaStream_t side = nullptr;    // Alg 4 chains (A8)
+  cudaStream_t side2 = nullptr;   // estimate factors and tail (A10)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_sj_done[2] = {nullptr, nullptr};   // A8 of an epoch parity finished (S_J, S_J^+ ready)
+  cudaEvent_t ev_sj_free[2] = {nullptr, nullptr};   // the estimate finished reading that parity's S_J, S_J^+
+  cudaEvent_t ev_snap_free[2] = {nullptr, nullptr}; // the estimate finished reading that parity's snapshot
+  int last_est_tag = 0;       // admission tag of the last estimated epoch (dirty = newer tags)
   // cross-stream hazards when estimates run on another stream than the ingests:
-  // committed = end of a commit; snap = estimate's snapshot of J / frob2 / dirty list taken;
-  // gram_done = estimate's basis reads finished; sj_j = Alg 4 chain finished reading J;
-  // est_done = end of an estimate.
-  cudaEvent_t ev_committed = nullptr, ev_snap = nullptr, ev_gram_done = nullptr, ev_sj_j = nullptr, ev_est_done = nullptr;
+  // committed = end of a commit (its snapshot taken); gram_done = estimate's basis reads
+  // finished; sj_j = Alg 4 chain finished reading J; est_done = end of an estimate.
+  cudaEvent_t ev_committed = nullptr, ev_gram_done = nullptr, ev_sj_j = nullptr, ev_est_done = nullptr;
   int bg_free_sms = 0;        // SMs the A9 kernel leaves free (diagnostics: OID_BG_FREE)
   int bg_waves = 32;          // A9 CTAs per SM (short CTAs; diagnostics: OID_BG_WAVES)
   bool use_side = true;       // diagnostics: OID_NO_SIDE=1 runs everything on the caller's stream
@@ -448,18 +453,24 @@ void tl_mark(oid_ctx ctx, cudaStream_t st, int tag) {
 }
 
 // side stream waits for all work enqueued on st so far
-oid_status fork_side(oid_ctx ctx, cudaStream_t st) {
+oid_status fork_to(oid_ctx ctx, cudaStream_t st, cudaStream_t to) {
   if (!ctx->use_side) return OID_OK;
   CK(cudaEventRecord(ctx->ev_fork, st));
-  CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+  CK(cudaStreamWaitEvent(to, ctx->ev_fork, 0));
   return OID_OK;
 }
+oid_status fork_side(oid_ctx ctx, cudaStream_t st) { return fork_to(ctx, st, ctx->side); }
 // st waits for all work enqueued on the side stream so far
-oid_status join_side(oid_ctx ctx, cudaStream_t st) {
+oid_status join_from(oid_ctx ctx, cudaStream_t st, cudaStream_t from) {
   if (!ctx->use_side) return OID_OK;
-  CK(cudaEventRecord(ctx->ev_join, ctx->side));
+  CK(cudaEventRecord(ctx->ev_join, from));
   CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
   return OID_OK;
+}
+// st waits for all work enqueued on both side streams so far
+oid_status join_side(oid_ctx ctx, cudaStream_t st) {
+  oid_status s = join_from(ctx, st, ctx->side);
+  return s != OID_OK ? s : join_from(ctx, st, ctx->side2);
 }
 
 template <typename T>
@@ -539,8 +550,6 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   double* Yp = ctx->d(L.Ypart);
   double* scal = ctx->d(L.scal);
   EvScope ev(ctx, st, &ctx->ev_post);
-  // an estimate on another stream must have snapshotted J / frob2 / the dirty list first
-  CK(cudaStreamWaitEvent(st, ctx->ev_snap, 0));
   tl_mark(ctx, st, 3);
   oid_status s = OID_OK;
   // A3: S <- [S, Y], SS^T += YY^T, ||A_obs||^2 += sum n_j
@@ -603,7 +612,8 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   CK(cudaStreamWaitEvent(st, ctx->ev_sj_j, 0));
   select_kernel<<<1, 32, 0, st>>>(ctx->ptr<int64_t>(L.J), ctx->d(L.tau_old), ctx->d(L.tau), Yp + int64_t(ell) * nc, t, nc,
                                   ctx->factor, static_cast<uint32_t>(ctx->epoch), ctx->n_obs, ctx->key0, ctx->key1,
-                                  ctx->ptr<int>(L.admit), ctx->ptr<int>(L.counts), scal, ctx->ptr<int>(L.dirty));
+                                  ctx->ptr<int>(L.admit), ctx->ptr<int>(L.counts), scal, ctx->ptr<int>(L.dirty),
+                                  static_cast<int>(ctx->epoch + 1));
   CKL();
   // A8 runs on the side stream, beside the basis copy
   s = fork_side(ctx, st);
@@ -624,21 +634,26 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   tl_mark(ctx, st, 6);
   ctx->n_obs += nc;
   cudaStream_t cs = ctx->use_side ? ctx->side : st;
+  const int par = static_cast<int>(ctx->epoch & 1);
+  double* SJp = ctx->d(L.SJ) + static_cast<size_t>(par) * ell * t;
+  double* Sjpinvp = ctx->d(L.Sjpinv) + static_cast<size_t>(par) * ell * t;
+  // the estimate of epoch - 2 (same parity) must have finished reading S_J, S_J^+
+  CK(cudaStreamWaitEvent(cs, ctx->ev_sj_free[par], 0));
   tl_mark(ctx, cs, 11);
   // A8: Alg 4 kept implicit: S_J^+ per epoch.  Fast path: S_J^+ = (S_J^T S_J)^-1 S_J^T
   // by the cluster tridiagonalisation when kappa(S_J) <= 1e5 (no R9 cutoff can act); else the
   // one-sided Jacobi SVD pseudo-inverse (gated on the device).
-  gather_sj_kernel<<<blocks_for(int64_t(ell) * t), 256, 0, cs>>>(ctx->d(L.S), ctx->ptr<int64_t>(L.J), t, ell, ctx->d(L.SJ));
+  gather_sj_kernel<<<blocks_for(int64_t(ell) * t), 256, 0, cs>>>(ctx->d(L.S), ctx->ptr<int64_t>(L.J), t, ell, SJp);
   CKL();
   int* sjgate = ctx->ptr<int>(L.gate) + 2;
   if (t <= kTriMaxN) {
-    s = gemm(ctx, cs, true, false, t, t, ell, 1.0, ctx->d(L.SJ), ell, ctx->d(L.SJ), ell, 0.0, ctx->d(L.sjG), t);
+    s = gemm(ctx, cs, true, false, t, t, ell, 1.0, SJp, ell, SJp, ell, 0.0, ctx->d(L.sjG), t);
     if (s != OID_OK) return s;
     fill_vacant_diag_kernel<<<1, 256, 0, cs>>>(ctx->d(L.sjG), t, ctx->ptr<int64_t>(L.J));
     CKL();
     CK(cudaEventRecord(ctx->ev_sj_j, cs));   // last read of J in this chain
-    s = spd_solve(ctx, cs, ctx->d(L.sjG), t, ctx->d(L.SJ), ell, true, ell, ctx->d(L.Sjpinv), t, false, 1e10, sjgate,
-                  scal + SC_KAPPA);
+    s = spd_solve(ctx, cs, ctx->d(L.sjG), t, SJp, ell, true, ell, Sjpinvp, t, false, 1e10, sjgate,
+                  scal + SC_KAPPA_SNAP + par);
     if (s != OID_OK) return s;
   } else {
     CK(cudaEventRecord(ctx->ev_sj_j, cs));
@@ -646,14 +661,23 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
     CKL();
   }
   const int* fb = sjgate + 1;
-  s = gemm(ctx, cs, false, false, ell, t, t, 1.0, ctx->d(L.SJ), ell, ctx->d(L.sjV), t, 0.0, ctx->d(L.sjB), ell, fb);
+  s = gemm(ctx, cs, false, false, ell, t, t, 1.0, SJp, ell, ctx->d(L.sjV), t, 0.0, ctx->d(L.sjB), ell, fb);
   if (s != OID_OK) return s;
   s = jacobi(ctx, cs, ctx->d(L.sjB), ell, t, ctx->d(L.sjV), ctx->d(L.sjsig), 1, true, fb);
   if (s != OID_OK) return s;
   s = pinv_assemble(ctx, cs, ctx->d(L.sjB), ell, t, ctx->d(L.sjV), ctx->d(L.sjsig), ctx->d(L.sjw), ctx->d(L.sjZ),
-                    ctx->d(L.Sjpinv), scal + SC_KAPPA, OID_FLAG_SJ_RANK_DEFICIENT, fb);
+                    Sjpinvp, scal + SC_KAPPA_SNAP + par, OID_FLAG_SJ_RANK_DEFICIENT, fb);
   if (s != OID_OK) return s;
+  CK(cudaMemcpyAsync(scal + SC_KAPPA, scal + SC_KAPPA_SNAP + par, sizeof(double), cudaMemcpyDeviceToDevice, cs));
+  CK(cudaEventRecord(ctx->ev_sj_done[par], cs));
   tl_mark(ctx, cs, 12);
+  // snapshot of this epoch for an estimate that may overlap the next commit (after the
+  // estimate of epoch - 2 has released this parity's snapshot)
+  CK(cudaStreamWaitEvent(st, ctx->ev_snap_free[par], 0));
+  commit_snapshot_kernel<<<1, 256, 0, st>>>(ctx->ptr<int64_t>(L.J), ctx->ptr<int>(L.dirty), t,
+                                            ctx->ptr<int64_t>(L.Jsnap) + static_cast<size_t>(par) * t,
+                                            ctx->ptr<int>(L.Dsnap) + static_cast<size_t>(par) * t, scal, par);
+  CKL();
   CK(cudaEventRecord(ctx->ev_committed, st));
   ctx->epoch += 1;
   ctx->estimate_ready = true;
@@ -673,26 +697,27 @@ oid_status check_block(oid_ctx ctx, const void* X, int64_t ld, int32_t nc) {
 
 oid_status explicit_P(oid_ctx ctx, cudaStream_t st) {
   const Layout& L = ctx->L;
-  return gemm(ctx, st, false, false, ctx->t, static_cast<int>(ctx->n_obs), ctx->p.ell, 1.0, ctx->d(L.Sjpinv), ctx->t,
+  const int par = static_cast<int>((ctx->epoch + 1) & 1);   // parity of the last committed epoch (epoch - 1)
+  return gemm(ctx, st, false, false, ctx->t, static_cast<int>(ctx->n_obs), ctx->p.ell, 1.0,
+              ctx->d(L.Sjpinv) + static_cast<size_t>(par) * ctx->t * ctx->p.ell, ctx->t,
               ctx->d(L.S), ctx->p.ell, 0.0, ctx->d(L.Pexp), ctx->t);
 }
 
 // Alg 8 factors that do not involve the basis Gram G (A10): P = S_J^+ S, Omega A_J P, the core
 // pseudo-inverse M, Omega_k A P^T, the third-block trace terms and P P^T; enqueued on stream cs.
-oid_status estimate_pre(oid_ctx ctx, cudaStream_t st) {
+oid_status estimate_pre(oid_ctx ctx, cudaStream_t st, int par) {
   const Layout& L = ctx->L;
   const oid_params& p = ctx->p;
   const int t = ctx->t, ell = p.ell, l1 = p.ell1, l2 = p.ell2, l3 = p.ell3;
   const int n = static_cast<int>(ctx->n_obs);
   double* S = ctx->d(L.S);
   double* scal = ctx->d(L.scal);
-  // kappa(S_J) of this epoch (the next Alg 4 chain on this stream overwrites it)
-  CK(cudaMemcpyAsync(scal + SC_KAPPA_EST, scal + SC_KAPPA, sizeof(double), cudaMemcpyDeviceToDevice, st));
   oid_status s = explicit_P(ctx, st);                                                 // P = S_J^+ S
   if (s != OID_OK) return s;
   double* P = ctx->d(L.Pexp);
   double* AJP = ctx->d(L.AJP);
-  s = gemm(ctx, st, false, false, ell, n, t, 1.0, ctx->d(L.SJ), ell, P, t, 0.0, AJP, ell);   // Omega A_J P
+  s = gemm(ctx, st, false, false, ell, n, t, 1.0, ctx->d(L.SJ) + static_cast<size_t>(par) * ell * t, ell, P, t, 0.0, AJP,
+           ell);   // Omega A_J P
   if (s != OID_OK) return s;
   CK(cudaMemsetAsync(scal + SC_T1, 0, 4 * sizeof(double), st));
   if (l1 > 0 && l2 > 0) {
@@ -850,9 +875,12 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
     int lo = 0, hi = 0;
     if ((e = cudaDeviceGetStreamPriorityRange(&lo, &hi)) != cudaSuccess) return bad(e);
     if ((e = cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, hi)) != cudaSuccess) return bad(e);
+    if ((e = cudaStreamCreateWithPriority(&ctx->side2, cudaStreamNonBlocking, hi)) != cudaSuccess) return bad(e);
     if ((e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming)) != cudaSuccess) return bad(e);
     if ((e = cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming)) != cudaSuccess) return bad(e);
-    for (cudaEvent_t* ev : {&ctx->ev_committed, &ctx->ev_snap, &ctx->ev_gram_done, &ctx->ev_sj_j, &ctx->ev_est_done})
+    for (cudaEvent_t* ev : {&ctx->ev_committed, &ctx->ev_gram_done, &ctx->ev_sj_j, &ctx->ev_est_done, &ctx->ev_sj_done[0],
+                            &ctx->ev_sj_done[1], &ctx->ev_sj_free[0], &ctx->ev_sj_free[1], &ctx->ev_snap_free[0],
+                            &ctx->ev_snap_free[1]})
       if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess) return bad(e);
     if (getenv("OID_BG_FREE")) ctx->bg_free_sms = std::max(0, atoi(getenv("OID_BG_FREE")));
     if (getenv("OID_BG_WAVES")) ctx->bg_waves = std::max(1, atoi(getenv("OID_BG_WAVES")));
@@ -978,22 +1006,25 @@ oid_status oid_estimate_begin(oid_ctx ctx, void* stream) {
   const Layout& L = ctx->L;
   const int t = ctx->t;
   EvScope ev(ctx, st, &ctx->ev_est);
-  // this estimate may run on another stream than the ingests: order it after the last commit and
-  // snapshot what the next commit will change (J, frob2, the dirty-slot list)
+  // this estimate may run on another stream than the ingests: it reads the snapshot (J,
+  // admission tags, ||A_obs||^2) and the S_J, S_J^+ buffers of the last committed epoch's parity
+  const int par = static_cast<int>((ctx->epoch + 1) & 1);
   CK(cudaStreamWaitEvent(st, ctx->ev_committed, 0));
   tl_mark(ctx, st, 7);
-  dirty_compact_kernel<<<1, 32, 0, st>>>(ctx->ptr<int>(L.dirty), t, ctx->ptr<int>(L.dlist), ctx->ptr<int>(L.counts));
+  dirty_compact_kernel<<<1, 32, 0, st>>>(ctx->ptr<int>(L.Dsnap) + static_cast<size_t>(par) * t, t, ctx->last_est_tag,
+                                         ctx->ptr<int>(L.dlist), ctx->ptr<int>(L.counts));
   CKL();
-  est_snapshot_kernel<<<1, 256, 0, st>>>(ctx->ptr<int64_t>(L.J), t, ctx->ptr<int64_t>(L.Jsnap), ctx->d(L.scal));
-  CKL();
-  CK(cudaEventRecord(ctx->ev_snap, st));
-  // A10 factors that do not need G: on the side stream, concurrently with A9 below
-  oid_status s0 = fork_side(ctx, st);
+  ctx->last_est_tag = static_cast<int>(ctx->epoch);   // newest admission tag of this state
+  // A10 factors that do not need G: on the second side stream, concurrently with A9 below
+  cudaStream_t cs2 = ctx->use_side ? ctx->side2 : st;
+  oid_status s0 = fork_to(ctx, st, cs2);
   if (s0 != OID_OK) return s0;
-  tl_mark(ctx, ctx->use_side ? ctx->side : st, 13);
-  s0 = estimate_pre(ctx, ctx->use_side ? ctx->side : st);
+  CK(cudaStreamWaitEvent(cs2, ctx->ev_sj_done[par], 0));
+  tl_mark(ctx, cs2, 13);
+  s0 = estimate_pre(ctx, cs2, par);
   if (s0 != OID_OK) return s0;
-  tl_mark(ctx, ctx->use_side ? ctx->side : st, 14);
+  CK(cudaEventRecord(ctx->ev_sj_free[par], cs2));   // S_J, S_J^+ of this parity are free again
+  tl_mark(ctx, cs2, 14);
   tl_mark(ctx, st, 8);
   // A9: exact basis Gram G = A_J^T A_J, incremental: only the rows/columns of
   // slots admitted since the last estimate are recomputed, over this shard's rows.
@@ -1045,17 +1076,20 @@ oid_status oid_estimate_end(oid_ctx ctx, double* out_dev, void* stream) {
   const int t = ctx->t, l1 = p.ell1, l2 = p.ell2;
   double* scal = ctx->d(L.scal);
   EvScope ev(ctx, st, &ctx->ev_est);
-  // The G-dependent tail runs on the (highest-priority) side stream, after the G-independent
-  // factors already queued there (estimate_pre): it is short and must not wait behind the next
-  // block's K1 on a lower-priority estimate stream.  `st` joins it at the end.
-  oid_status s = fork_side(ctx, st);
+  // The G-dependent tail runs on the (highest-priority) second side stream, after the
+  // G-independent factors already queued there (estimate_pre): it is short and must not wait
+  // behind the next block's K1 on a lower-priority estimate stream.  `st` joins it at the end.
+  const int par = static_cast<int>((ctx->epoch + 1) & 1);
+  cudaStream_t cs = ctx->use_side ? ctx->side2 : st;
+  oid_status s = fork_to(ctx, st, cs);
   if (s != OID_OK) return s;
-  cudaStream_t cs = ctx->use_side ? ctx->side : st;
+  est_scalars_kernel<<<1, 1, 0, cs>>>(scal, par);
+  CKL();
   gram_scatter_kernel<<<blocks_for(int64_t(t) * t), 256, 0, cs>>>(ctx->d(L.Gsum), ctx->ptr<int>(L.dlist),
                                                                   ctx->ptr<int>(L.counts), t, ctx->d(L.Gfull));
   CKL();
   CK(cudaMemcpyAsync(ctx->d(L.G), ctx->d(L.Gfull), sizeof(double) * t * t, cudaMemcpyDeviceToDevice, cs));
-  mask_gram_kernel<<<blocks_for(int64_t(t) * t), 256, 0, cs>>>(ctx->d(L.G), ctx->ptr<int64_t>(L.Jsnap), t);
+  mask_gram_kernel<<<blocks_for(int64_t(t) * t), 256, 0, cs>>>(ctx->d(L.G), ctx->ptr<int64_t>(L.Jsnap) + static_cast<size_t>(par) * t, t);
   CKL();
   if (l1 > 0 && l2 > 0) {
     // term1 = tr(M (Omega1 A P^T) G (Omega2 A P^T)^T) = <Q1 G, X2>
@@ -1070,7 +1104,8 @@ oid_status oid_estimate_end(oid_ctx ctx, double* out_dev, void* stream) {
   hutch_final_kernel<<<1, 32, 0, cs>>>(scal, p.ell3, ctx->ptr<unsigned>(L.flags), ctx->d(L.est));
   CKL();
   if (out_dev) CK(cudaMemcpyAsync(out_dev, ctx->d(L.est), 8 * sizeof(double), cudaMemcpyDeviceToDevice, cs));
-  s = join_side(ctx, st);
+  CK(cudaEventRecord(ctx->ev_snap_free[par], cs));   // this parity's snapshot may be rewritten
+  s = join_from(ctx, st, cs);
   if (s != OID_OK) return s;
   CK(cudaEventRecord(ctx->ev_est_done, st));
   tl_mark(ctx, st, 10);
@@ -1132,7 +1167,8 @@ oid_status oid_get(oid_ctx ctx, int32_t field, void* host_dst, size_t bytes, voi
     case 5: off = L.tau; need = sizeof(double) * (ctx->t + p.b_max); break;
     case 6: off = L.mu; need = sizeof(double) * p.ell; break;
     case 7: off = L.Ypart; need = sizeof(double) * (p.ell + 1) * p.b_max; break;
-    case 8: off = L.Sjpinv; need = sizeof(double) * ctx->t * p.ell; break;
+    case 8: off = L.Sjpinv + static_cast<size_t>((ctx->epoch + 1) & 1) * ctx->t * p.ell * sizeof(double);
+            need = sizeof(double) * ctx->t * p.ell; break;
     case 9: off = L.counters; need = sizeof(int) * kNumJacobiUses * kMaxSweeps; break;
     case 10: off = L.dbg; need = k1tc::kDbgRows * k1tc::kDbgTiles * sizeof(long long); break;
     case 11: off = L.G; need = sizeof(double) * ctx->t * ctx->t; break;
@@ -1190,6 +1226,7 @@ oid_status oid_stats(oid_ctx ctx, oid_stats_t* out) {
   CK(sum(ctx->ev_est, &out->est_ms));
   unsigned f = 0;
   CK(cudaStreamSynchronize(ctx->side));
+  CK(cudaStreamSynchronize(ctx->side2));
   CK(cudaEventSynchronize(ctx->ev_est_done));
   CK(cudaMemcpy(&f, ctx->ws + ctx->L.flags, sizeof(unsigned), cudaMemcpyDeviceToHost));
   out->flags = f;
@@ -1209,13 +1246,15 @@ oid_status oid_stats_reset(oid_ctx ctx) {
 
 void oid_destroy(oid_ctx ctx) {
   if (!ctx) return;
-  if (ctx->side) {
-    cudaStreamSynchronize(ctx->side);
-    cudaStreamDestroy(ctx->side);
-  }
+  for (cudaStream_t* sp : {&ctx->side, &ctx->side2})
+    if (*sp) {
+      cudaStreamSynchronize(*sp);
+      cudaStreamDestroy(*sp);
+    }
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
-  for (cudaEvent_t ev : {ctx->ev_committed, ctx->ev_snap, ctx->ev_gram_done, ctx->ev_sj_j, ctx->ev_est_done})
+  for (cudaEvent_t ev : {ctx->ev_committed, ctx->ev_gram_done, ctx->ev_sj_j, ctx->ev_est_done, ctx->ev_sj_done[0],
+                         ctx->ev_sj_done[1], ctx->ev_sj_free[0], ctx->ev_sj_free[1], ctx->ev_snap_free[0], ctx->ev_snap_free[1]})
     if (ev) cudaEventDestroy(ev);
   oid_stats_reset(ctx);
   delete ctx;

@@ -8,7 +8,10 @@ namespace oid {
 // scalars layout (device double array)
 enum Scal : int {
   SC_FROB2 = 0, SC_LAM = 1, SC_EK = 2, SC_SHIFT = 3, SC_TRACE = 4, SC_DMAX = 5, SC_MINMARGIN = 6, SC_KAPPA = 7,
-  SC_T1 = 8, SC_T3A = 9, SC_T3B = 10, SC_GPP = 11, SC_FROB2_EST = 12, SC_KAPPA_EST = 13, SC_COUNT = 16
+  SC_T1 = 8, SC_T3A = 9, SC_T3B = 10, SC_GPP = 11, SC_FROB2_EST = 12, SC_KAPPA_EST = 13,
+  SC_FROB2_SNAP = 16,   // + epoch parity: ||A_obs||^2 snapshot taken at the end of a commit
+  SC_KAPPA_SNAP = 18,   // + epoch parity: kappa(S_J) of that epoch's Alg 4 chain
+  SC_COUNT = 24
 };
 
 // Ridge regulariser (reading R8): eigenvalues mu of the unscaled Gram, E_k = sum of the k
@@ -89,7 +92,7 @@ __global__ void scores_kernel(const double* __restrict__ T, const double* __rest
 __global__ void select_kernel(int64_t* __restrict__ J, double* __restrict__ tau_old, const double* __restrict__ tau,
                               const double* __restrict__ nrm, int t, int nc, double factor, uint32_t epoch,
                               int64_t base, uint32_t key0, uint32_t key1, int* __restrict__ admit,
-                              int* __restrict__ counts, double* __restrict__ scal, int* __restrict__ dirty) {
+                              int* __restrict__ counts, double* __restrict__ scal, int* __restrict__ dirty, int dtag) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   unsigned consumed[2] = {0u, 0u};   // nc <= 64
   int na = 0, nz = 0;
@@ -122,7 +125,7 @@ __global__ void select_kernel(int64_t* __restrict__ J, double* __restrict__ tau_
           consumed[r >> 5] |= 1u << (r & 31);
           admit[2 * na] = i;
           admit[2 * na + 1] = r;
-          dirty[i] = 1;
+          dirty[i] = dtag;   // epoch tag of the admission (estimates pick tags newer than theirs)
           ++na;
           filled = true;
           break;
@@ -217,20 +220,29 @@ __global__ void hutch_final_kernel(const double* __restrict__ scal, int ell3, co
   out[7] = scal[SC_KAPPA_EST];
 }
 
-// Snapshot for an estimate that may overlap the next commit: J and ||A_obs||^2.
-__global__ void est_snapshot_kernel(const int64_t* __restrict__ J, int t, int64_t* __restrict__ Jsnap,
-                                    double* __restrict__ scal) {
-  for (int i = threadIdx.x; i < t; i += blockDim.x) Jsnap[i] = J[i];
-  if (threadIdx.x == 0) scal[SC_FROB2_EST] = scal[SC_FROB2];
+// End-of-commit snapshot (epoch parity par) for an estimate that may overlap the next commit:
+// J, the admission tags, ||A_obs||^2.
+__global__ void commit_snapshot_kernel(const int64_t* __restrict__ J, const int* __restrict__ dirty, int t,
+                                       int64_t* __restrict__ Jsnap, int* __restrict__ Dsnap, double* __restrict__ scal,
+                                       int par) {
+  for (int i = threadIdx.x; i < t; i += blockDim.x) { Jsnap[i] = J[i]; Dsnap[i] = dirty[i]; }
+  if (threadIdx.x == 0) scal[SC_FROB2_SNAP + par] = scal[SC_FROB2];
 }
 
-// Slots admitted since the last estimate (dirty flags set by select_kernel), compacted in
-// slot order; flags cleared.  counts[2] = number of dirty slots.
-__global__ void dirty_compact_kernel(int* __restrict__ dirty, int t, int* __restrict__ list, int* __restrict__ counts) {
+// Scalars of the estimated epoch (parity par) for hutch_final_kernel.
+__global__ void est_scalars_kernel(double* __restrict__ scal, int par) {
+  scal[SC_FROB2_EST] = scal[SC_FROB2_SNAP + par];
+  scal[SC_KAPPA_EST] = scal[SC_KAPPA_SNAP + par];
+}
+
+// Slots admitted after the last estimate (admission tags > last_tag), compacted in slot order;
+// counts[2] = number of such (dirty) slots.  Tags are never cleared (no race with the next commit).
+__global__ void dirty_compact_kernel(const int* __restrict__ dtag, int t, int last_tag, int* __restrict__ list,
+                                     int* __restrict__ counts) {
   if (threadIdx.x != 0) return;
   int c = 0;
   for (int i = 0; i < t; ++i)
-    if (dirty[i]) { list[c++] = i; dirty[i] = 0; }
+    if (dtag[i] > last_tag) list[c++] = i;
   counts[2] = c;
 }
 

@@ -13,15 +13,23 @@ from synth import ChannelFlow, C3
 
 one = "--one-stream" in sys.argv
 steps = 6
+start = int(sys.argv[sys.argv.index("--start") + 1]) if "--start" in sys.argv else 0
 gen = ChannelFlow(192, 129, 192, seed=1003)
 dev = torch.device("cuda", 0)
 p = oid.make_params(m=gen.m, k=C3.k, ell=C3.ell, b_max=C3.b, n_cap=1000, lam=-1.0, seed=0)
 I = torch.cuda.Stream(dev, priority=-1)
 E = I if one else torch.cuda.Stream(dev, priority=0)
 eng = oid.Engine(p, stream=I, estimate_stream=E)
-blocks = [gen.block_torch(s * C3.b, (s + 1) * C3.b, dev).T for s in range(steps)]
+blocks = [gen.block_torch(s * C3.b, (s + 1) * C3.b, dev).T for s in range(start + steps)]
 torch.cuda.synchronize()
 out = torch.empty(8, dtype=torch.float64, device=dev)
+for s in range(start):
+    eng.ingest_block(blocks[s])
+    eng.estimate_begin()
+    eng.estimate_end(out)
+torch.cuda.synchronize()
+eng.get(13)   # drop the warm-up marks
+blocks = blocks[start:]
 for s in range(steps):
     eng.ingest_block(blocks[s])
     eng.estimate_begin()
