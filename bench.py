@@ -165,7 +165,7 @@ def run_reference(args, rank, world):
         return
     steps = max(1, args.steps)
     rows = min(args.cpu_sample_rows, 1 << 16)
-    gbs, secs, thr, sample = oracle_sample(args.workload, rows, steps=steps, warmup=min(args.warmup, 1))
+    gbs, secs, thr, sample = oracle_sample(args.workload, rows, steps=steps, warmup=args.warmup)
     line = {
         "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus, "steps": steps,
         "warmup": args.warmup, "ms_per_step": secs * 1e3, "higher_is_better": True, "scaling": "strong",
