@@ -855,11 +855,14 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
     if ((e = cudaFuncSetAttribute(bjacobi_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big)) != cudaSuccess) return bad(e);
     if ((e = cudaFuncSetAttribute(bjacobi_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big)) != cudaSuccess) return bad(e);
   }
-  if (p->ell <= kTriMaxN) {
+  if (std::min(p->ell, p->k) <= kTriMaxN) {
+    // the cluster tridiagonalisation serves A4 (order ell, when ell <= 512) and the A8 SPD solve
+    // (order k, when k <= 512)
+    const int ntri = std::min(p->ell, kTriMaxN);
     if ((e = cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
       return bad(e);
     if ((e = cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(sizeof(double) * p->ell * tri_rows(p->ell)))) !=
+                                  static_cast<int>(sizeof(double) * ntri * tri_rows(ntri)))) !=
         cudaSuccess)
       return bad(e);
     const int ref_smem = static_cast<int>(sizeof(double) * kQStages * kRefChunk * tri_ldv(kTriMaxN));

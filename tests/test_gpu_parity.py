@@ -225,6 +225,21 @@ def test_odd_sizes_tridiagonal_paths(oid, ell, k):
         assert np.linalg.norm(P - o.P) / np.linalg.norm(o.P) < 1e-5
 
 
+def test_large_basis_and_sketch_paths(oid):
+    """k > 256 (two TMA boxes per basis tile, dirty groups of 16 in A9) and ell > 512 (eigenvector
+    path for A4/A5, multi-CTA Jacobi for the NA-Hutch++ core): J, P and the estimate vs the oracle."""
+    A = c1_matrix(seed=12, m=2600, n=192, rank=60, noise=1e-3)
+    eng, o = _pair(oid, 2600, 300, 640, 64, 192, 0.05, seed=5)
+    low = _stream_compare(oid, eng, o, A, 64)
+    if low is None:
+        P = eng.finalize()["P"].cpu().numpy()
+        assert np.linalg.norm(P - o.P) / np.linalg.norm(o.P) < 1e-5
+        est, ref = eng.error_estimate(), o.error_estimate()
+        assert abs(est["est_rel"] - ref["est_rel"]) < 1e-5
+    else:
+        pytest.skip(f"decision margin < 1e-6 at epoch {low}")
+
+
 def test_nonfinite_input_flagged(oid):
     A = np.random.default_rng(5).standard_normal((320, 8))
     A[7, 3] = np.nan
