@@ -240,6 +240,22 @@ def test_large_basis_and_sketch_paths(oid):
         pytest.skip(f"decision margin < 1e-6 at epoch {low}")
 
 
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_maximum_sizes(oid, dtype):
+    """ell = 1024 and k = 416 (the validated maxima), b = 64, fp64 and fp32 data (row-tiled basis
+    with 16 / 32 rows per 128-byte line): J, P and the estimate vs the oracle."""
+    A = c1_matrix(seed=13, m=2048, n=192, rank=80, noise=1e-3).astype(dtype)
+    eng, o = _pair(oid, 2048, 416, 1024, 64, 192, 0.05, seed=6, dtype="f64" if dtype == np.float64 else "f32")
+    low = _stream_compare(oid, eng, o, A, 64, dtype=dtype)
+    if low is None:
+        P = eng.finalize()["P"].cpu().numpy()
+        assert np.linalg.norm(P - o.P) / np.linalg.norm(o.P) < 1e-5
+        est, ref = eng.error_estimate(), o.error_estimate()
+        assert abs(est["est_rel"] - ref["est_rel"]) < 1e-5
+    else:
+        pytest.skip(f"decision margin < 1e-6 at epoch {low}")
+
+
 def test_nonfinite_input_flagged(oid):
     A = np.random.default_rng(5).standard_normal((320, 8))
     A[7, 3] = np.nan
