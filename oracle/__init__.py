@@ -19,6 +19,10 @@ Parity-pin status per function:
   selection            pinned (C1 block 1 forced admissions, MC frequencies)
   Alg 4 coefficients   pinned (exact recovery, self-representation, identity sketch)
   NA-Hutch++ estimate  pinned (P=0 case, exactness, unbiasedness over seeds)
+  gradient variant     (oracle/gradient.py) pinned: exact simplex gradients of
+                       linear fields, central / one-sided stencils, P(0) = Alg 4 and the
+                       stacked normal equations, GCV(0) closed form, golden section on
+                       known functions, constant fields = plain selection
   ridge scores at lambda>0 with Gaussian sketch / Bernoulli trajectories on
   C2-C5 are "parity unpinned" beyond the above.
 """
