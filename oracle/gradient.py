@@ -26,8 +26,8 @@ import math
 import numpy as np
 import scipy.sparse as sp
 
-from .oid import (OracleOID, OracleParams, PINV_RCOND, column_norms2, eig_gram, ridge_lambda, ridge_scores,
-                  select, sketch, EpochLog)
+from .oid import (OracleOID, OracleParams, PINV_RCOND, alg4_coefficients, column_norms2, eig_gram, ridge_lambda,
+                  ridge_scores, select, sketch, EpochLog)
 from .gauss16 import gauss16_scale, omega_rows
 
 
@@ -127,6 +127,7 @@ class OracleGradOID(OracleOID):
         d = len(Gops)
         self.Sg = [np.zeros((params.ell, 0)) for _ in range(d)]
         self.gram = np.zeros(((d + 1) * params.ell, (d + 1) * params.ell))
+        self.frob2_aug = 0.0       # ||A_obs||^2 + sum_p ||G^p A_obs||^2 (augmented energy, A11(2))
 
     def ingest_block(self, X, partial_sketch=None, partial_norms=None):
         p = self.p
@@ -136,15 +137,17 @@ class OracleGradOID(OracleOID):
         Y = sketch(p, X, self._Q)
         Yg = [sketch(p, g, self._Q) for g in GX]
         Yaug = np.vstack([Y] + Yg)                                      # [Omega a; Omega G^p a]
-        nrm = column_norms2(X) + sum(column_norms2(g) for g in GX)      # augmented energy
+        nrm = column_norms2(X)
+        nrm_aug = nrm + sum(column_norms2(g) for g in GX)               # augmented energy
         base = self.n_obs
         self.S = np.concatenate([self.S, Y], axis=1)
         self.Sg = [np.concatenate([Sp, Yp], axis=1) for Sp, Yp in zip(self.Sg, Yg)]
         self.gram = self.gram + Yaug @ Yaug.T
-        self.frob2 += float(np.sum(nrm))
+        self.frob2 += float(np.sum(nrm))                                 # plain energy (estimates)
+        self.frob2_aug += float(np.sum(nrm_aug))
         self.n_obs += ncols
         mu, W = eig_gram(self.gram)
-        lam_eff, Ek = ridge_lambda(p, mu, self.frob2, float(np.trace(self.gram)))
+        lam_eff, Ek = ridge_lambda(p, mu, self.frob2_aug, float(np.trace(self.gram)))
         shift = p.ell * lam_eff
         Saug = np.vstack([self.S] + self.Sg)
         occ = self.J >= 0
@@ -152,7 +155,7 @@ class OracleGradOID(OracleOID):
         if occ.any():
             tau_slot[occ] = ridge_scores(mu, W, shift, Saug[:, self.J[occ]])
         tau_cand = ridge_scores(mu, W, shift, Yaug)
-        cand_zero = column_norms2(X) == 0.0
+        cand_zero = nrm == 0.0
         J, tau_old, admits, decisions = select(p.seed, self.epoch, self.J, self.tau_old, tau_slot,
                                                tau_cand, cand_zero, p.admission_factor(), base)
         for (i, r) in admits:
@@ -161,8 +164,9 @@ class OracleGradOID(OracleOID):
             if J[i] < 0:
                 self.C[:, i] = 0.0
         self.J, self.tau_old = J, tau_old
+        self.P, self.kappa = alg4_coefficients(self.S, self.J)        # plain Alg 4 (estimates)
         self.log.append(EpochLog(self.epoch, lam_eff, Ek, tau_slot, tau_cand, J.copy(), tau_old.copy(),
-                                 admits, decisions, 1.0))
+                                 admits, decisions, self.kappa))
         self.epoch += 1
         return self.log[-1]
 
