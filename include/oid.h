@@ -81,6 +81,15 @@ typedef struct {
   int32_t k1_mode;    /* oid_k1_mode                                                     */
   int32_t profile;    /* 1: time K1 and the other kernel groups with CUDA events          */
   int32_t device;     /* CUDA device ordinal the workspace lives on                      */
+  /* Gradient-enhanced variant (reading Q17).  grad_nfields > 0 enables
+     it: a snapshot stacks grad_nfields fields on a grad_nx x grad_ny grid (field f at rows
+     [f nx ny, (f+1) nx ny), node (i, j) at f nx ny + i ny + j); simplex gradients over the axis
+     neighbours with spacings grad_hx, grad_hy (0: 1/(N-1)).  The ridge scores then use the
+     augmented sketch [Omega a; Omega G^1 a; Omega G^2 a] and the augmented energy; the
+     estimate keeps Alg 4's P; oid_gradient_* give P(mu) and the sketched GCV.  Requires a single
+     shard (row_begin = 0, row_end = m), grad_nfields grad_nx grad_ny = m and 3 ell <= 1024.  */
+  int32_t grad_nfields, grad_nx, grad_ny, grad_pad;
+  double grad_hx, grad_hy;
 } oid_params;
 
 typedef struct {
@@ -148,8 +157,26 @@ oid_status oid_error_estimate(oid_ctx ctx, double* out_host, void* stream);
 oid_status oid_finalize(oid_ctx ctx, int64_t* J_host, double* P, int32_t P_on_device,
                         void* basis_dev, void* stream);
 
+/* Gradient variant (grad_nfields > 0), after an ingest and with no sketch pending:
+   oid_gradient_gcv       sketched GCV(mu) of eq:GCV_COmega for the current basis,
+                          computed on the device (Omega G^p Omega^T is regenerated once per
+                          context); synchronizes `stream`.
+   oid_gradient_coefficients  P(mu) = argmin ||Omega(A_J X - A)||^2 + mu sum_p ||Omega G^p (A_J X - A)||^2
+                          (eq:opt_grad_fullsketch), k x n_obs column-major (ld k) into
+                          device memory P_dev (vacant-slot rows zero); asynchronous.
+   oid_gradient_finalize  mu* by golden-section search of GCV over log10(mu) in [lo, hi] to
+                          tolerance tol (the paper: [-3, 3]); P(mu*) into P_dev when not
+                          NULL; synchronizes.
+   Errors: OID_ESTATE (variant off, nothing ingested, sketch pending), OID_EINVAL (mu < 0,
+   lo >= hi, tol <= 0). */
+oid_status oid_gradient_gcv(oid_ctx ctx, double mu, double* gcv, void* stream);
+oid_status oid_gradient_coefficients(oid_ctx ctx, double mu, double* P_dev, void* stream);
+oid_status oid_gradient_finalize(oid_ctx ctx, double lo, double hi, double tol, double* mu_star, double* P_dev,
+                                 void* stream);
+
 /* Copy internal state to host memory (synchronizes `stream`), for tests and diagnostics.
-   field: 0 J (k int64), 1 tau_old (k), 2 S (ell x n_obs), 3 Gram (ell x ell),
+   field: 0 J (k int64), 1 tau_old (k), 2 S (ell x n_obs), 3 Gram (ell x ell; 3 ell x 3 ell with
+          the gradient variant),
           4 scalars [frob2, lambda_eff, E_k, shift, trace, dmax, min_margin, kappa],
           5 last scores (k + ncols: basis slots then candidates), 6 eigenvalues of Gram (ell),
           7 last ingest partials ((ell+1) * ncols), 8 S_J^+ (k x ell),

@@ -30,7 +30,8 @@ FLAG_NONFINITE_INPUT, FLAG_SJ_RANK_DEFICIENT, FLAG_E2_NEGATIVE, FLAG_K1_RECOMPUT
 
 EXPORTED = ["oid_workspace_query", "oid_init", "oid_ingest_block", "oid_ingest_sketch", "oid_ingest_commit",
             "oid_partials", "oid_estimate_begin", "oid_estimate_end", "oid_error_estimate", "oid_finalize", "oid_get",
-            "oid_stats", "oid_stats_reset", "oid_sketch_table", "oid_destroy", "oid_last_error", "oid_version"]
+            "oid_stats", "oid_stats_reset", "oid_sketch_table", "oid_destroy", "oid_last_error", "oid_version",
+            "oid_gradient_gcv", "oid_gradient_coefficients", "oid_gradient_finalize"]
 
 
 class OidParams(ctypes.Structure):
@@ -39,7 +40,9 @@ class OidParams(ctypes.Structure):
                 ("ell1", ctypes.c_int32), ("ell2", ctypes.c_int32), ("ell3", ctypes.c_int32),
                 ("lam", ctypes.c_double), ("eps", ctypes.c_double), ("delta", ctypes.c_double), ("c", ctypes.c_double),
                 ("seed", ctypes.c_uint64), ("dtype", ctypes.c_int32), ("k1_mode", ctypes.c_int32),
-                ("profile", ctypes.c_int32), ("device", ctypes.c_int32)]
+                ("profile", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("grad_nfields", ctypes.c_int32), ("grad_nx", ctypes.c_int32), ("grad_ny", ctypes.c_int32),
+                ("grad_pad", ctypes.c_int32), ("grad_hx", ctypes.c_double), ("grad_hy", ctypes.c_double)]
 
 
 class OidStats(ctypes.Structure):
@@ -64,6 +67,9 @@ _sig = {
     "oid_stats": [_vp, ctypes.POINTER(OidStats)],
     "oid_stats_reset": [_vp],
     "oid_sketch_table": [ctypes.POINTER(ctypes.c_int32), _dp],
+    "oid_gradient_gcv": [_vp, ctypes.c_double, _dp, _vp],
+    "oid_gradient_coefficients": [_vp, ctypes.c_double, _vp, _vp],
+    "oid_gradient_finalize": [_vp, ctypes.c_double, ctypes.c_double, ctypes.c_double, _dp, _vp, _vp],
 }
 for _n, _a in _sig.items():
     getattr(_lib, _n).argtypes = _a
@@ -106,12 +112,15 @@ def hutch_split(ell):
 
 
 def make_params(m, k, ell, b_max, n_cap, lam, split=None, eps=0.5, delta=0.05, c=1.0, seed=0, dtype="f64",
-                row_begin=0, row_end=None, k1_mode=K1_AUTO, profile=False, device=0):
+                row_begin=0, row_end=None, k1_mode=K1_AUTO, profile=False, device=0, grad=None):
+    """grad: None, or (nfields, nx, ny[, hx, hy]) for the gradient-enhanced variant (A11)."""
     split = hutch_split(ell) if split is None else split
+    g = tuple(grad) + (0.0, 0.0)[len(grad) - 3:] if grad is not None else (0, 0, 0, 0.0, 0.0)
     return OidParams(m=m, row_begin=row_begin, row_end=m if row_end is None else row_end, n_cap=n_cap, k=k, ell=ell,
                      b_max=b_max, ell1=split[0], ell2=split[1], ell3=split[2], lam=lam, eps=eps, delta=delta, c=c,
                      seed=seed, dtype=OID_F64 if dtype in ("f64", "float64") else OID_F32, k1_mode=k1_mode,
-                     profile=int(bool(profile)), device=device)
+                     profile=int(bool(profile)), device=device, grad_nfields=int(g[0]), grad_nx=int(g[1]),
+                     grad_ny=int(g[2]), grad_pad=0, grad_hx=float(g[3]), grad_hy=float(g[4]))
 
 
 def workspace_bytes(params):
@@ -203,6 +212,30 @@ class Engine:
         v = list(out)
         return dict(e2=v[0], T=v[1], gpp=v[2], frob2=v[3], est_abs=v[4], est_rel=v[5], flags=int(v[6]), kappa=v[7])
 
+    def gradient_gcv(self, mu):
+        out = ctypes.c_double()
+        self._check(_lib.oid_gradient_gcv(self.h, ctypes.c_double(mu), ctypes.byref(out), self._st()), "oid_gradient_gcv")
+        return out.value
+
+    def gradient_coefficients(self, mu):
+        torch = self._torch
+        n_obs = self.stats()["n_obs"]
+        P = torch.empty((n_obs, self.p.k), dtype=torch.float64, device=self.device)   # column-major k x n_obs
+        self._check(_lib.oid_gradient_coefficients(self.h, ctypes.c_double(mu), ctypes.c_void_p(P.data_ptr()), self._st()),
+                    "oid_gradient_coefficients")
+        self.stream.synchronize()
+        return P.T
+
+    def gradient_finalize(self, lo=-3.0, hi=3.0, tol=1e-3):
+        torch = self._torch
+        n_obs = self.stats()["n_obs"]
+        P = torch.empty((n_obs, self.p.k), dtype=torch.float64, device=self.device)
+        mu = ctypes.c_double()
+        self._check(_lib.oid_gradient_finalize(self.h, ctypes.c_double(lo), ctypes.c_double(hi), ctypes.c_double(tol),
+                                               ctypes.byref(mu), ctypes.c_void_p(P.data_ptr()), self._st()),
+                    "oid_gradient_finalize")
+        return mu.value, P.T
+
     def finalize(self, basis=False):
         torch = self._torch
         t = self.p.k
@@ -220,10 +253,11 @@ class Engine:
 
     def get(self, field):
         ell, t, bm = self.p.ell, self.p.k, self.p.b_max
+        ga = 3 if self.p.grad_nfields > 0 else 1
         n_obs = self.stats()["n_obs"] if field == 2 else 0
         shapes = {0: ((t,), np.int64), 1: ((t,), np.float64), 2: ((n_obs, ell), np.float64),
-                  3: ((ell, ell), np.float64), 4: ((8,), np.float64), 5: ((t + bm,), np.float64),
-                  6: ((ell,), np.float64), 7: (((ell + 1) * bm,), np.float64), 8: ((ell, t), np.float64),
+                  3: ((ga * ell, ga * ell), np.float64), 4: ((8,), np.float64), 5: ((t + bm,), np.float64),
+                  6: ((ga * ell,), np.float64), 7: (((ell + 1) * bm,), np.float64), 8: ((ell, t), np.float64),
                   9: ((3, 48), np.int32), 10: ((10, 4096), np.int64), 11: ((t, t), np.float64), 12: ((1024, 4), np.int64), 13: ((4096, 2), np.float64)}
         shape, dt = shapes[field]
         a = np.empty(shape, dtype=dt)

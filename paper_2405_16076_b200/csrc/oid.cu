@@ -20,6 +20,7 @@
 #include "k1_simt.cuh"
 #include "k1_tc.cuh"
 #include "gram_tc.cuh"
+#include "grad.cuh"
 #include "path.cuh"
 #include "tri.cuh"
 
@@ -106,7 +107,7 @@ struct Bump {
 struct Layout {
   size_t S, gram, Ypart, k1part, k1npart, gB, gV, mu, mu_sorted, Yc, Tsc, tau, scal, J, tau_old, admit, counts,
       flags, counters, C, SJ, sjB, sjV, sjsig, sjw, sjZ, Sjpinv, Pexp, AJP, G, Gsum, Gpart, cB, cV, csig, cw, cZ, M,
-      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, wyT, sjG, cG, cBt, cZ2, dbg, Jsnap, Dsnap, td2, te2, Vh2, tauv2, wyT2, ldl2, mu2, total;
+      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, wyT, sjG, cG, cBt, cZ2, dbg, Jsnap, Dsnap, S1, S2, YpG, GX, OGO, gH, gHV, gHs, gHw, gHZ, gHp, gR, gCm, gE, gLst, gLV, gLs, gLw, gLZ, gLp, gRhs, gscal, td2, te2, Vh2, tauv2, wyT2, ldl2, mu2, total;
 };
 
 int64_t m_local(const oid_params& p) { return p.row_end - p.row_begin; }
@@ -118,17 +119,19 @@ Layout make_layout(const oid_params& p) {
   const size_t d = sizeof(double);
   const size_t ell = p.ell, t = p.k, bm = p.b_max, n = p.n_cap;
   const size_t ncb = 64;
+  const size_t ga = p.grad_nfields > 0 ? 3 : 1;   // augmented sketch [Y; Y1; Y2] (A11)
+  const size_t ellg = ga * ell;                     // order of the Gram whose spectrum A4/A5 use
   L.S = b.take(ell * n * d);
-  L.gram = b.take(ell * ell * d);
+  L.gram = b.take(ellg * ellg * d);
   L.Ypart = b.take((ell + 1) * bm * d);
   L.k1part = b.take(static_cast<size_t>(kK1MaxCtas) * ell * ncb * d);
   L.k1npart = b.take(static_cast<size_t>(kK1MaxCtas) * ncb * d);
-  L.gB = b.take(ell * ell * d);
-  L.gV = b.take(ell * ell * d);
-  L.mu = b.take(ell * d);
-  L.mu_sorted = b.take(ell * d);
-  L.Yc = b.take(ell * (t + bm) * d);
-  L.Tsc = b.take(ell * (t + bm) * d);
+  L.gB = b.take(ellg * ellg * d);
+  L.gV = b.take(ellg * ellg * d);
+  L.mu = b.take(ellg * d);
+  L.mu_sorted = b.take(ellg * d);
+  L.Yc = b.take(ellg * (t + bm) * d);
+  L.Tsc = b.take(ellg * (t + bm) * d);
   L.tau = b.take((t + bm) * d);
   L.scal = b.take(SC_COUNT * d);
   L.J = b.take(t * sizeof(int64_t));
@@ -177,20 +180,20 @@ Layout make_layout(const oid_params& p) {
   L.symU = b.take(static_cast<size_t>(kSymMaxPairs) * kSymB * kSymB * d);
   L.symF = b.take(kSymMaxPairs * sizeof(int));
   L.symTol = b.take(kNumJacobiUses * d);
-  L.gT = b.take(ell * ell * d);
-  L.td = b.take(ell * d);
-  L.te = b.take(ell * d);
-  L.Vh = b.take(ell * (ell + 1) * d);   // leading dimension tri_ldv(n) <= ell + 1
-  L.tauv = b.take(ell * d);
-  L.gv = b.take((ell + 1) * d);
-  L.gp = b.take((ell + 16) * d);
+  L.gT = b.take(ellg * ellg * d);
+  L.td = b.take(ellg * d);
+  L.te = b.take(ellg * d);
+  L.Vh = b.take(ellg * (ellg + 1) * d);   // leading dimension tri_ldv(n) <= n + 1
+  L.tauv = b.take(ellg * d);
+  L.gv = b.take((ellg + 1) * d);
+  L.gp = b.take((ellg + 16) * d);
   L.gate = b.take(8 * sizeof(int));
   L.sjG = b.take(t * t * d);
   L.dbg = b.take((k1tc::kDbgRows + 1) * k1tc::kDbgTiles * sizeof(long long));
   L.cBt = b.take(std::max<size_t>(1, l1 * l2) * d);
   L.cZ2 = b.take(std::max<size_t>(1, l1 * l2) * d);
   L.cG = b.take(std::max<size_t>(1, std::min(l1, l2) * std::min(l1, l2)) * d);
-  L.ldl = b.take(2 * ell * d);
+  L.ldl = b.take(2 * ellg * d);
   L.wyT = b.take(static_cast<size_t>(kMaxRefChunks) * kRefChunk * kRefChunk * d);
   // second tridiagonal workspace: the Alg 4 SPD solve (side stream) runs beside A4 of the next block
   L.td2 = b.take(ell * d);
@@ -202,6 +205,32 @@ Layout make_layout(const oid_params& p) {
   L.mu2 = b.take(ell * d);
   L.Jsnap = b.take(2 * t * sizeof(int64_t));
   L.Dsnap = b.take(2 * t * sizeof(int));
+  if (ga > 1) {
+    // gradient variant (A11): S^p, their K1 outputs, G^p X, Omega G^p Omega^T, GCV / P(mu) scratch
+    const size_t ml = static_cast<size_t>(m_local(p));
+    L.S1 = b.take(ell * n * d);
+    L.S2 = b.take(ell * n * d);
+    L.YpG = b.take(2 * (ell + 1) * bm * d);
+    L.GX = b.take(2 * ml * bm * d);
+    L.OGO = b.take(2 * ell * ell * d);
+    L.gH = b.take(t * t * d);
+    L.gHV = b.take(t * t * d);
+    L.gHs = b.take(t * d);
+    L.gHw = b.take(t * d);
+    L.gHZ = b.take(t * t * d);
+    L.gHp = b.take(t * t * d);
+    L.gR = b.take(ell * t * d);
+    L.gCm = b.take(ell * ell * d);
+    L.gE = b.take(ell * n * d);
+    L.gLst = b.take(3 * ell * t * d);
+    L.gLV = b.take(t * t * d);
+    L.gLs = b.take(t * d);
+    L.gLw = b.take(t * d);
+    L.gLZ = b.take(3 * ell * t * d);
+    L.gLp = b.take(t * 3 * ell * d);
+    L.gRhs = b.take(3 * ell * n * d);
+    L.gscal = b.take(8 * d);
+  }
   L.tc = b.take(k1tc_workspace_bytes(p.ell, p.b_max, m_local(p), p.dtype == OID_F64));
   L.total = b.off;
   return L;
@@ -224,6 +253,14 @@ const char* validate(const oid_params* p) {
   if (p->dtype != OID_F32 && p->dtype != OID_F64) return "dtype must be OID_F32 or OID_F64";
   if (p->k1_mode < 0 || p->k1_mode > 2) return "bad k1_mode";
   if (p->m / 32 >= (int64_t(1) << 32)) return "m too large for the 32-bit Philox row counter";
+  if (p->grad_nfields < 0) return "grad_nfields must be >= 0";
+  if (p->grad_nfields > 0) {
+    if (p->grad_nx < 1 || p->grad_ny < 1 || int64_t(p->grad_nfields) * p->grad_nx * p->grad_ny != p->m)
+      return "gradient variant: grad_nfields * grad_nx * grad_ny must equal m";
+    if (p->row_begin != 0 || p->row_end != p->m) return "gradient variant: single shard only (row_begin = 0, row_end = m)";
+    if (3 * p->ell > 1024) return "gradient variant: 3 ell must be <= 1024";
+    if (!(p->grad_hx >= 0.0) || !(p->grad_hy >= 0.0)) return "gradient variant: spacings must be >= 0 (0 = 1/(N-1))";
+  }
   return nullptr;
 }
 
@@ -264,6 +301,9 @@ struct oid_ctx_s {
   cudaEvent_t ev_sj_free[2] = {nullptr, nullptr};   // the estimate finished reading that parity's S_J, S_J^+
   cudaEvent_t ev_snap_free[2] = {nullptr, nullptr}; // the estimate finished reading that parity's snapshot
   int last_est_tag = 0;       // admission tag of the last estimated epoch (dirty = newer tags)
+  int ga = 1;                 // 3 with the gradient variant (augmented sketch), else 1
+  GradGrid grid{};
+  bool ogo_ready = false;     // Omega G^p Omega^T formed (gradient variant)
   // cross-stream hazards when estimates run on another stream than the ingests:
   // committed = end of a commit (its snapshot taken); gram_done = estimate's basis reads
   // finished; sj_j = Alg 4 chain finished reading J; est_done = end of an estimate.
@@ -474,7 +514,7 @@ oid_status join_side(oid_ctx ctx, cudaStream_t st) {
 }
 
 template <typename T>
-oid_status launch_k1_simt(oid_ctx ctx, cudaStream_t st, const T* X, int64_t ld, int nc) {
+oid_status launch_k1_simt(oid_ctx ctx, cudaStream_t st, const T* X, int64_t ld, int nc, double* out) {
   const oid_params& p = ctx->p;
   const int ncb = nc <= 16 ? 16 : (nc <= 32 ? 32 : 64);
   const int rpt = ncb <= 32 ? 2 : 1;
@@ -501,20 +541,22 @@ oid_status launch_k1_simt(oid_ctx ctx, cudaStream_t st, const T* X, int64_t ld, 
     ++ctx->k1_launches;
   }
   const int64_t nout = int64_t(p.ell) * nc + nc;
-  k1_reduce_kernel<<<blocks_for(nout), 256, 0, st>>>(part, npart, gx, ncb, p.ell, nc, ctx->qscale, ctx->d(ctx->L.Ypart),
+  k1_reduce_kernel<<<blocks_for(nout), 256, 0, st>>>(part, npart, gx, ncb, p.ell, nc, ctx->qscale, out,
                                                     ctx->ptr<unsigned>(ctx->L.flags));
   CKL();
   ctx->k1_mode_used = OID_K1_SIMT_F64;
   return OID_OK;
 }
 
-oid_status do_sketch(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_t st) {
+// K1 on one block (X of dtype f64 / f32) into out = [Y (ell x nc); n (nc)]
+oid_status sketch_one(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_t st, double* out, bool f64,
+                      bool strict_mode) {
   const oid_params& p = ctx->p;
   const bool want_tc = (p.k1_mode == OID_K1_TC_INT8) || (p.k1_mode == OID_K1_AUTO && ctx->tc_ok);
   K1TcArgs a{};
   a.X = X; a.ld = ld; a.ncols = nc; a.row_begin = p.row_begin; a.row_end = p.row_end; a.ell = p.ell;
-  a.key0 = ctx->key0; a.key1 = ctx->key1; a.scale = ctx->qscale; a.f64 = p.dtype == OID_F64;
-  a.ws = ctx->ws + ctx->L.tc; a.out = ctx->d(ctx->L.Ypart); a.flags = ctx->ptr<unsigned>(ctx->L.flags);
+  a.key0 = ctx->key0; a.key1 = ctx->key1; a.scale = ctx->qscale; a.f64 = f64;
+  a.ws = ctx->ws + ctx->L.tc; a.out = out; a.flags = ctx->ptr<unsigned>(ctx->L.flags);
   a.t0 = static_cast<uint32_t>(ctx->qmag[0]) | (static_cast<uint32_t>(ctx->qmag[1]) << 8) |
          (static_cast<uint32_t>(ctx->qmag[2]) << 16) | (static_cast<uint32_t>(ctx->qmag[3]) << 24);
   a.t1 = static_cast<uint32_t>(ctx->qmag[4]) | (static_cast<uint32_t>(ctx->qmag[5]) << 8) |
@@ -522,7 +564,7 @@ oid_status do_sketch(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   a.num_sms = ctx->num_sms;
   a.dbg = ctx->k1_debug ? ctx->ptr<long long>(ctx->L.dbg) : nullptr;
   const bool tc_call = want_tc && ctx->tc_ok && k1tc_call_ok(a);
-  if (p.k1_mode == OID_K1_TC_INT8 && !tc_call)
+  if (strict_mode && p.k1_mode == OID_K1_TC_INT8 && !tc_call)
     return ctx->fail(OID_EINVAL, "tensor-core K1 unavailable for this device/shape/alignment");
   if (tc_call) {
     int nl = 0;
@@ -539,8 +581,31 @@ oid_status do_sketch(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
     ctx->k1_mode_used = OID_K1_TC_INT8;
     return OID_OK;
   }
-  if (p.dtype == OID_F64) return launch_k1_simt<double>(ctx, st, static_cast<const double*>(X), ld, nc);
-  return launch_k1_simt<float>(ctx, st, static_cast<const float*>(X), ld, nc);
+  if (f64) return launch_k1_simt<double>(ctx, st, static_cast<const double*>(X), ld, nc, out);
+  return launch_k1_simt<float>(ctx, st, static_cast<const float*>(X), ld, nc, out);
+}
+
+oid_status do_sketch(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_t st) {
+  const oid_params& p = ctx->p;
+  const Layout& L = ctx->L;
+  oid_status s = sketch_one(ctx, X, ld, nc, st, ctx->d(L.Ypart), p.dtype == OID_F64, true);
+  if (s != OID_OK || ctx->ga == 1) return s;
+  // gradient variant (A11): G^p X by the axis-neighbour stencils, then K1 on each
+  // (same Omega, so the three sketches stack into [Omega a; Omega G^1 a; Omega G^2 a])
+  const int64_t m = ctx->m_loc;
+  double* GX0 = ctx->d(L.GX);
+  double* GX1 = GX0 + m * p.b_max;
+  const unsigned gb = static_cast<unsigned>(std::min<int64_t>(blocks_for(m * nc), 8 * ctx->num_sms));
+  if (p.dtype == OID_F64)
+    grad_stencil_kernel<double><<<gb, 256, 0, st>>>(static_cast<const double*>(X), ld, m, nc, ctx->grid, GX0, GX1);
+  else
+    grad_stencil_kernel<float><<<gb, 256, 0, st>>>(static_cast<const float*>(X), ld, m, nc, ctx->grid, GX0, GX1);
+  CKL();
+  double* Y1 = ctx->d(L.YpG);
+  double* Y2 = Y1 + static_cast<size_t>(p.ell + 1) * p.b_max;
+  s = sketch_one(ctx, GX0, m, nc, st, Y1, true, false);
+  if (s != OID_OK) return s;
+  return sketch_one(ctx, GX1, m, nc, st, Y2, true, false);
 }
 
 oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_t st) {
@@ -552,59 +617,75 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   EvScope ev(ctx, st, &ctx->ev_post);
   tl_mark(ctx, st, 3);
   oid_status s = OID_OK;
-  // A3: S <- [S, Y], SS^T += YY^T, ||A_obs||^2 += sum n_j
-  gram_update_kernel<<<blocks_for(int64_t(ell) * ell), 256, 0, st>>>(Yp, ell, nc, ctx->d(L.gram), ctx->d(L.S), ctx->n_obs,
-                                                                    scal);
-  CKL();
-  // A4: spectrum of the Gram and lambda; A5: ridge scores
   const int ns = t + nc;
-  gather_scored_kernel<<<blocks_for(int64_t(ell) * ns), 256, 0, st>>>(ctx->d(L.S), ctx->ptr<int64_t>(L.J), t, Yp, nc, ell,
-                                                                      ctx->d(L.Yc));
-  CKL();
+  const int ng = ctx->ga * ell;              // order of the (augmented) Gram
+  const int frob_idx = ctx->ga > 1 ? SC_FROB2_AUG : SC_FROB2;
+  if (ctx->ga == 1) {
+    // A3: S <- [S, Y], SS^T += YY^T, ||A_obs||^2 += sum n_j
+    gram_update_kernel<<<blocks_for(int64_t(ell) * ell), 256, 0, st>>>(Yp, ell, nc, ctx->d(L.gram), ctx->d(L.S), ctx->n_obs,
+                                                                      scal);
+    CKL();
+    // A4: spectrum of the Gram and lambda; A5: ridge scores
+    gather_scored_kernel<<<blocks_for(int64_t(ell) * ns), 256, 0, st>>>(ctx->d(L.S), ctx->ptr<int64_t>(L.J), t, Yp, nc, ell,
+                                                                        ctx->d(L.Yc));
+    CKL();
+  } else {
+    // A11: augmented sketch [Y; Y1; Y2], its (3 ell)^2 Gram and energy
+    double* Y1 = ctx->d(L.YpG);
+    double* Y2 = Y1 + static_cast<size_t>(ell + 1) * p.b_max;
+    gram_update_aug_kernel<<<blocks_for(int64_t(ng) * ng), 256, 0, st>>>(Yp, Y1, Y2, ell, nc, ctx->d(L.gram), ctx->d(L.S),
+                                                                         ctx->d(L.S1), ctx->d(L.S2), ctx->n_obs, scal);
+    CKL();
+    gather_scored_aug_kernel<<<blocks_for(int64_t(ng) * ns), 256, 0, st>>>(ctx->d(L.S), ctx->d(L.S1), ctx->d(L.S2),
+                                                                           ctx->ptr<int64_t>(L.J), t, Yp, Y1, Y2, nc, ell,
+                                                                           ctx->d(L.Yc));
+    CKL();
+  }
   int* gate = ctx->ptr<int>(L.gate);
-  if (ell <= kTriMaxN && !ctx->cold_jacobi) {
+  if (ng <= kTriMaxN && !ctx->cold_jacobi) {
     // tridiagonal fast path (tri.cuh); the eigenvector path below runs only when gate[1] is set
-    const size_t smem = sizeof(double) * static_cast<size_t>(ell) * tri_rows(ell);
-    tridiag_cluster_kernel<<<kTriCtas, 256, smem, st>>>(ctx->d(L.gram), ell, ctx->d(L.td), ctx->d(L.te), ctx->d(L.Vh),
+    const size_t smem = sizeof(double) * static_cast<size_t>(ng) * tri_rows(ng);
+    tridiag_cluster_kernel<<<kTriCtas, 256, smem, st>>>(ctx->d(L.gram), ng, ctx->d(L.td), ctx->d(L.te), ctx->d(L.Vh),
                                                         ctx->d(L.tauv), ctx->k1_debug ? ctx->ptr<long long>(L.dbg) + k1tc::kDbgRows * k1tc::kDbgTiles : nullptr);
     CKL();
-    if (ell > 2) {
-      wy_t_kernel<<<(ell - 2 + kRefChunk - 1) / kRefChunk, 256, 0, st>>>(ctx->d(L.Vh), ctx->d(L.tauv), ell, ctx->d(L.wyT));
+    if (ng > 2) {
+      wy_t_kernel<<<(ng - 2 + kRefChunk - 1) / kRefChunk, 256, 0, st>>>(ctx->d(L.Vh), ctx->d(L.tauv), ng, ctx->d(L.wyT));
       CKL();
     }
-    multisect_kernel<<<(ell * 32 + 255) / 256, 256, sizeof(double) * 2 * ell, st>>>(ctx->d(L.td), ctx->d(L.te), ell,
+    multisect_kernel<<<(ng * 32 + 255) / 256, 256, sizeof(double) * 2 * ng, st>>>(ctx->d(L.td), ctx->d(L.te), ng,
                                                                                   ctx->d(L.mu));
     CKL();
-    lambda_sorted_kernel<<<1, 256, 0, st>>>(ctx->d(L.mu), ell, p.k, ctx->d(L.gram), p.lambda, ell, scal, gate,
-                                            ctx->d(L.td), ctx->d(L.te), ctx->d(L.ldl), 1);
+    lambda_sorted_kernel<<<1, 256, 0, st>>>(ctx->d(L.mu), ng, p.k, ctx->d(L.gram), p.lambda, ell, scal, gate,
+                                            ctx->d(L.td), ctx->d(L.te), ctx->d(L.ldl), 1, frob_idx);
     CKL();
-    tri_scores_kernel<<<ns, 256, sizeof(double) * kQStages * kRefChunk * tri_ldv(ell), st>>>(ctx->d(L.Yc), ell, ns, ctx->d(L.Vh), ctx->d(L.wyT), ctx->d(L.ldl), gate,
+    tri_scores_kernel<<<ns, 256, sizeof(double) * kQStages * kRefChunk * tri_ldv(ng), st>>>(ctx->d(L.Yc), ng, ns, ctx->d(L.Vh), ctx->d(L.wyT), ctx->d(L.ldl), gate,
                                           ctx->d(L.tau));
     CKL();
     const int* g1 = gate + 1;
-    s = gemm(ctx, st, false, false, ell, ell, ell, 1.0, ctx->d(L.gram), ell, ctx->d(L.gV), ell, 0.0, ctx->d(L.gT), ell, g1);
+    s = gemm(ctx, st, false, false, ng, ng, ng, 1.0, ctx->d(L.gram), ng, ctx->d(L.gV), ng, 0.0, ctx->d(L.gT), ng, g1);
     if (s != OID_OK) return s;
-    s = gemm(ctx, st, true, false, ell, ell, ell, 1.0, ctx->d(L.gV), ell, ctx->d(L.gT), ell, 0.0, ctx->d(L.gB), ell, g1);
+    s = gemm(ctx, st, true, false, ng, ng, ng, 1.0, ctx->d(L.gV), ng, ctx->d(L.gT), ng, 0.0, ctx->d(L.gB), ng, g1);
     if (s != OID_OK) return s;
-    s = sym_eig(ctx, st, ctx->d(L.gB), ell, ctx->d(L.gV), ctx->d(L.mu), 0, true, g1);
+    s = sym_eig(ctx, st, ctx->d(L.gB), ng, ctx->d(L.gV), ctx->d(L.mu), 0, true, g1);
     if (s != OID_OK) return s;
-    s = gemm(ctx, st, true, false, ell, ns, ell, 1.0, ctx->d(L.gV), ell, ctx->d(L.Yc), ell, 0.0, ctx->d(L.Tsc), ell, g1);
+    s = gemm(ctx, st, true, false, ng, ns, ng, 1.0, ctx->d(L.gV), ng, ctx->d(L.Yc), ng, 0.0, ctx->d(L.Tsc), ng, g1);
     if (s != OID_OK) return s;
-    scores_kernel<<<ns, 256, 0, st>>>(ctx->d(L.Tsc), ctx->d(L.mu), ell, ns, scal, ctx->d(L.tau), g1);
+    scores_kernel<<<ns, 256, 0, st>>>(ctx->d(L.Tsc), ctx->d(L.mu), ng, ns, scal, ctx->d(L.tau), g1);
     CKL();
   } else {
     // eigenvector path only: warm-started two-sided block Jacobi (gV starts as the identity)
-    s = gemm(ctx, st, false, false, ell, ell, ell, 1.0, ctx->d(L.gram), ell, ctx->d(L.gV), ell, 0.0, ctx->d(L.gT), ell);
+    s = gemm(ctx, st, false, false, ng, ng, ng, 1.0, ctx->d(L.gram), ng, ctx->d(L.gV), ng, 0.0, ctx->d(L.gT), ng);
     if (s != OID_OK) return s;
-    s = gemm(ctx, st, true, false, ell, ell, ell, 1.0, ctx->d(L.gV), ell, ctx->d(L.gT), ell, 0.0, ctx->d(L.gB), ell);
+    s = gemm(ctx, st, true, false, ng, ng, ng, 1.0, ctx->d(L.gV), ng, ctx->d(L.gT), ng, 0.0, ctx->d(L.gB), ng);
     if (s != OID_OK) return s;
-    s = sym_eig(ctx, st, ctx->d(L.gB), ell, ctx->d(L.gV), ctx->d(L.mu), 0, true);
+    s = sym_eig(ctx, st, ctx->d(L.gB), ng, ctx->d(L.gV), ctx->d(L.mu), 0, true);
     if (s != OID_OK) return s;
-    lambda_kernel<<<1, 256, 0, st>>>(ctx->d(L.mu), ell, p.k, ctx->d(L.gram), p.lambda, ell, scal, ctx->d(L.mu_sorted));
+    lambda_kernel<<<1, 256, 0, st>>>(ctx->d(L.mu), ng, p.k, ctx->d(L.gram), p.lambda, ell, scal, ctx->d(L.mu_sorted),
+                                     frob_idx);
     CKL();
-    s = gemm(ctx, st, true, false, ell, ns, ell, 1.0, ctx->d(L.gV), ell, ctx->d(L.Yc), ell, 0.0, ctx->d(L.Tsc), ell);
+    s = gemm(ctx, st, true, false, ng, ns, ng, 1.0, ctx->d(L.gV), ng, ctx->d(L.Yc), ng, 0.0, ctx->d(L.Tsc), ng);
     if (s != OID_OK) return s;
-    scores_kernel<<<ns, 256, 0, st>>>(ctx->d(L.Tsc), ctx->d(L.mu), ell, ns, scal, ctx->d(L.tau), nullptr);
+    scores_kernel<<<ns, 256, 0, st>>>(ctx->d(L.Tsc), ctx->d(L.mu), ng, ns, scal, ctx->d(L.tau), nullptr);
     CKL();
   }
   // A6: selection / replacement; the previous block's Alg 4 chain reads J first
@@ -791,6 +872,92 @@ oid_status estimate_pre(oid_ctx ctx, cudaStream_t st, int par) {
   return OID_OK;
 }
 
+// ---------------------------------------------------------------- gradient variant (A11)
+// Omega G^p Omega^T (l x l, p = 0, 1), regenerated once per context (finalize-time only)
+oid_status grad_ogo(oid_ctx ctx, cudaStream_t st) {
+  if (ctx->ogo_ready) return OID_OK;
+  const int ell = ctx->p.ell;
+  dim3 grid(blocks_for(int64_t(ell) * ell), 1, 2);
+  omega_g_omega_kernel<<<grid, 256, 0, st>>>(ell, ctx->m_loc, ctx->grid, ctx->key0, ctx->key1, ctx->qscale, ctx->d(ctx->L.OGO));
+  CKL();
+  ctx->ogo_ready = true;
+  return OID_OK;
+}
+
+// [S_J; c S^1_J; c S^2_J] (3l x t) into L.gLst
+oid_status grad_stack_j(oid_ctx ctx, cudaStream_t st, double c) {
+  const Layout& L = ctx->L;
+  const int ell = ctx->p.ell, t = ctx->t;
+  stack3_kernel<<<blocks_for(int64_t(3) * ell * t), 256, 0, st>>>(ctx->d(L.S), ctx->d(L.S1), ctx->d(L.S2), ell, t,
+                                                                   ctx->ptr<int64_t>(L.J), c, ctx->d(L.gLst));
+  CKL();
+  return OID_OK;
+}
+
+// sketched GCV(mu) of eq:GCV_COmega -> L.gscal[0]
+oid_status grad_gcv(oid_ctx ctx, cudaStream_t st, double mu) {
+  const Layout& L = ctx->L;
+  const int ell = ctx->p.ell, t = ctx->t, n = static_cast<int>(ctx->n_obs), l3 = 3 * ell;
+  oid_status s = grad_ogo(ctx, st);
+  if (s != OID_OK) return s;
+  s = grad_stack_j(ctx, st, 1.0);
+  if (s != OID_OK) return s;
+  const double* SJ = ctx->d(L.gLst);              // rows 0..l-1 of the stack (ld 3l)
+  const double* S1J = SJ + ell;
+  const double* S2J = SJ + 2 * ell;
+  // H = S_J^T S_J + mu (S^1_J^T S^1_J + S^2_J^T S^2_J)      (t x t)
+  s = gemm(ctx, st, true, false, t, t, ell, 1.0, SJ, l3, SJ, l3, 0.0, ctx->d(L.gH), t);
+  if (s != OID_OK) return s;
+  s = gemm(ctx, st, true, false, t, t, ell, mu, S1J, l3, S1J, l3, 1.0, ctx->d(L.gH), t);
+  if (s != OID_OK) return s;
+  s = gemm(ctx, st, true, false, t, t, ell, mu, S2J, l3, S2J, l3, 1.0, ctx->d(L.gH), t);
+  if (s != OID_OK) return s;
+  // R = S_J + mu ((Omega G^1 Omega^T)^T S^1_J + (Omega G^2 Omega^T)^T S^2_J)   (l x t)
+  s = gemm(ctx, st, true, false, ell, t, ell, mu, ctx->d(L.OGO), ell, S1J, l3, 0.0, ctx->d(L.gR), ell);
+  if (s != OID_OK) return s;
+  s = gemm(ctx, st, true, false, ell, t, ell, mu, ctx->d(L.OGO) + static_cast<size_t>(ell) * ell, ell, S2J, l3, 1.0,
+           ctx->d(L.gR), ell);
+  if (s != OID_OK) return s;
+  add_strided_kernel<<<blocks_for(int64_t(ell) * t), 256, 0, st>>>(SJ, l3, ell, t, ctx->d(L.gR), ell);
+  CKL();
+  // H^+ by the one-sided Jacobi SVD (R9 cutoff)
+  CK(cudaMemcpyAsync(ctx->d(L.gHp), ctx->d(L.gH), sizeof(double) * t * t, cudaMemcpyDeviceToDevice, st));
+  s = jacobi(ctx, st, ctx->d(L.gHp), t, t, ctx->d(L.gHV), ctx->d(L.gHs), 2, false);
+  if (s != OID_OK) return s;
+  s = pinv_assemble(ctx, st, ctx->d(L.gHp), t, t, ctx->d(L.gHV), ctx->d(L.gHs), ctx->d(L.gHw), ctx->d(L.gHZ),
+                    ctx->d(L.gH), nullptr, 0);
+  if (s != OID_OK) return s;
+  // C = S_J H^+ R^T (l x l); E = S - C S; GCV = ||E||^2 / tr(I - C)^2
+  s = gemm(ctx, st, false, false, ell, t, t, 1.0, SJ, l3, ctx->d(L.gH), t, 0.0, ctx->d(L.gLZ), ell);
+  if (s != OID_OK) return s;
+  s = gemm(ctx, st, false, true, ell, ell, t, 1.0, ctx->d(L.gLZ), ell, ctx->d(L.gR), ell, 0.0, ctx->d(L.gCm), ell);
+  if (s != OID_OK) return s;
+  CK(cudaMemcpyAsync(ctx->d(L.gE), ctx->d(L.S), sizeof(double) * ell * n, cudaMemcpyDeviceToDevice, st));
+  s = gemm(ctx, st, false, false, ell, n, ell, -1.0, ctx->d(L.gCm), ell, ctx->d(L.S), ell, 1.0, ctx->d(L.gE), ell);
+  if (s != OID_OK) return s;
+  gcv_final_kernel<<<1, 256, 0, st>>>(ctx->d(L.gE), int64_t(ell) * n, ctx->d(L.gCm), ell, ctx->d(L.gscal));
+  CKL();
+  return OID_OK;
+}
+
+// P(mu) of eq:opt_grad_fullsketch: [S_J; sqrt(mu) S^p_J]^+ [S; sqrt(mu) S^p]  (t x n, ld t)
+oid_status grad_coefficients(oid_ctx ctx, cudaStream_t st, double mu, double* P) {
+  const Layout& L = ctx->L;
+  const int ell = ctx->p.ell, t = ctx->t, n = static_cast<int>(ctx->n_obs), l3 = 3 * ell;
+  const double c = std::sqrt(mu);
+  oid_status s = grad_stack_j(ctx, st, c);
+  if (s != OID_OK) return s;
+  s = jacobi(ctx, st, ctx->d(L.gLst), l3, t, ctx->d(L.gLV), ctx->d(L.gLs), 2, false);
+  if (s != OID_OK) return s;
+  s = pinv_assemble(ctx, st, ctx->d(L.gLst), l3, t, ctx->d(L.gLV), ctx->d(L.gLs), ctx->d(L.gLw), ctx->d(L.gLZ),
+                    ctx->d(L.gLp), nullptr, 0);
+  if (s != OID_OK) return s;
+  stack3_kernel<<<blocks_for(int64_t(l3) * n), 256, 0, st>>>(ctx->d(L.S), ctx->d(L.S1), ctx->d(L.S2), ell, n, nullptr, c,
+                                                             ctx->d(L.gRhs));
+  CKL();
+  return gemm(ctx, st, false, false, t, n, l3, 1.0, ctx->d(L.gLp), t, ctx->d(L.gRhs), l3, 0.0, P, t);
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ C ABI
@@ -828,6 +995,15 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
   ctx->ws = static_cast<char*>(workspace);
   ctx->m_loc = m_local(*p);
   ctx->t = p->k;
+  if (p->grad_nfields > 0) {
+    ctx->ga = 3;
+    ctx->grid.nf = p->grad_nfields;
+    ctx->grid.nx = p->grad_nx;
+    ctx->grid.ny = p->grad_ny;
+    ctx->grid.hx = p->grad_hx > 0.0 ? p->grad_hx : (p->grad_nx > 1 ? 1.0 / (p->grad_nx - 1) : 1.0);
+    ctx->grid.hy = p->grad_hy > 0.0 ? p->grad_hy : (p->grad_ny > 1 ? 1.0 / (p->grad_ny - 1) : 1.0);
+  }
+  const int ng = ctx->ga * p->ell;
   ctx->key0 = static_cast<uint32_t>(p->seed & 0xffffffffu);
   ctx->key1 = static_cast<uint32_t>(p->seed >> 32);
   const double k = p->k;
@@ -855,10 +1031,10 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
     if ((e = cudaFuncSetAttribute(bjacobi_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big)) != cudaSuccess) return bad(e);
     if ((e = cudaFuncSetAttribute(bjacobi_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big)) != cudaSuccess) return bad(e);
   }
-  if (std::min(p->ell, p->k) <= kTriMaxN) {
-    // the cluster tridiagonalisation serves A4 (order ell, when ell <= 512) and the A8 SPD solve
-    // (order k, when k <= 512)
-    const int ntri = std::min(p->ell, kTriMaxN);
+  if (std::min(ng, p->k) <= kTriMaxN) {
+    // the cluster tridiagonalisation serves A4 (order ell, or 3 ell with gradients, when <= 512)
+    // and the A8 SPD solve (order k, when k <= 512)
+    const int ntri = std::min(std::max(ng, p->k), kTriMaxN);
     if ((e = cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
       return bad(e);
     if ((e = cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -877,8 +1053,16 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
   {
     int lo = 0, hi = 0;
     if ((e = cudaDeviceGetStreamPriorityRange(&lo, &hi)) != cudaSuccess) return bad(e);
-    if ((e = cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, hi)) != cudaSuccess) return bad(e);
-    if ((e = cudaStreamCreateWithPriority(&ctx->side2, cudaStreamNonBlocking, hi)) != cudaSuccess) return bad(e);
+    // Priorities relative to the ingest stream given at init (measured best on C3, profiles/
+    // r01_summary.md): A8 (side) one level above it (the estimate factors wait for it), the
+    // estimate factors and tail (side2) at its level (so the next block's persistent K1 is not
+    // starved of SMs by them, and they are not starved by a low-priority estimate stream).
+    int p_ing = 0;
+    if (cudaStreamGetPriority(st, &p_ing) != cudaSuccess) p_ing = lo;
+    const int p_side = getenv("OID_SIDE_PRIO") ? atoi(getenv("OID_SIDE_PRIO")) : std::max(hi, p_ing - 1);
+    const int p_side2 = getenv("OID_SIDE2_PRIO") ? atoi(getenv("OID_SIDE2_PRIO")) : p_ing;
+    if ((e = cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, p_side)) != cudaSuccess) return bad(e);
+    if ((e = cudaStreamCreateWithPriority(&ctx->side2, cudaStreamNonBlocking, p_side2)) != cudaSuccess) return bad(e);
     if ((e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming)) != cudaSuccess) return bad(e);
     if ((e = cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming)) != cudaSuccess) return bad(e);
     for (cudaEvent_t* ev : {&ctx->ev_committed, &ctx->ev_gram_done, &ctx->ev_sj_j, &ctx->ev_est_done, &ctx->ev_sj_done[0],
@@ -934,10 +1118,10 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
   std::vector<double> ones(ctx->t, 1.0);
   if ((e = cudaMemcpyAsync(ctx->ws + L.tau_old, ones.data(), sizeof(double) * ctx->t, cudaMemcpyHostToDevice, st)) != cudaSuccess)
     return bad(e);
-  if ((e = cudaMemsetAsync(ctx->ws + L.gram, 0, sizeof(double) * p->ell * p->ell, st)) != cudaSuccess) return bad(e);
-  if ((e = cudaMemsetAsync(ctx->ws + L.Vh, 0, sizeof(double) * p->ell * p->ell, st)) != cudaSuccess) return bad(e);
-  set_identity_kernel<<<static_cast<unsigned>((int64_t(p->ell) * p->ell + 255) / 256), 256, 0, st>>>(
-      reinterpret_cast<double*>(ctx->ws + L.gV), p->ell);
+  if ((e = cudaMemsetAsync(ctx->ws + L.gram, 0, sizeof(double) * ng * ng, st)) != cudaSuccess) return bad(e);
+  if ((e = cudaMemsetAsync(ctx->ws + L.Vh, 0, sizeof(double) * ng * (ng + 1), st)) != cudaSuccess) return bad(e);
+  set_identity_kernel<<<static_cast<unsigned>((int64_t(ng) * ng + 255) / 256), 256, 0, st>>>(
+      reinterpret_cast<double*>(ctx->ws + L.gV), ng);
   set_identity_kernel<<<static_cast<unsigned>((int64_t(p->k) * p->k + 255) / 256), 256, 0, st>>>(
       reinterpret_cast<double*>(ctx->ws + L.sjV), p->k);
   if ((e = cudaGetLastError()) != cudaSuccess) return bad(e);
@@ -1127,6 +1311,70 @@ oid_status oid_error_estimate(oid_ctx ctx, double* out_host, void* stream) {
   return OID_OK;
 }
 
+oid_status oid_gradient_gcv(oid_ctx ctx, double mu, double* gcv_out, void* stream) {
+  if (!ctx || !gcv_out) return OID_EINVAL;
+  if (ctx->ga == 1) return ctx->fail(OID_ESTATE, "gradient variant not enabled (grad_nfields = 0)");
+  if (!(mu >= 0.0)) return ctx->fail(OID_EINVAL, "mu must be >= 0");
+  if (ctx->pending_nc >= 0) return ctx->fail(OID_ESTATE, "a sketch is pending commit");
+  if (ctx->n_obs == 0) return ctx->fail(OID_ESTATE, "no block ingested yet");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  oid_status s = join_side(ctx, st);
+  if (s != OID_OK) return s;
+  CK(cudaStreamWaitEvent(st, ctx->ev_est_done, 0));
+  s = grad_gcv(ctx, st, mu);
+  if (s != OID_OK) return s;
+  CK(cudaMemcpyAsync(gcv_out, ctx->d(ctx->L.gscal), sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return OID_OK;
+}
+
+oid_status oid_gradient_coefficients(oid_ctx ctx, double mu, double* P_dev, void* stream) {
+  if (!ctx || !P_dev) return OID_EINVAL;
+  if (ctx->ga == 1) return ctx->fail(OID_ESTATE, "gradient variant not enabled (grad_nfields = 0)");
+  if (!(mu >= 0.0)) return ctx->fail(OID_EINVAL, "mu must be >= 0");
+  if (ctx->pending_nc >= 0) return ctx->fail(OID_ESTATE, "a sketch is pending commit");
+  if (ctx->n_obs == 0) return ctx->fail(OID_ESTATE, "no block ingested yet");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  oid_status s = join_side(ctx, st);
+  if (s != OID_OK) return s;
+  CK(cudaStreamWaitEvent(st, ctx->ev_est_done, 0));
+  return grad_coefficients(ctx, st, mu, P_dev);
+}
+
+oid_status oid_gradient_finalize(oid_ctx ctx, double lo, double hi, double tol, double* mu_star, double* P_dev,
+                                 void* stream) {
+  if (!ctx || !mu_star) return OID_EINVAL;
+  if (!(hi > lo) || !(tol > 0.0)) return ctx->fail(OID_EINVAL, "need lo < hi and tol > 0");
+  // golden-section search on log10(mu); each probe is one device GCV evaluation
+  const double invphi = (std::sqrt(5.0) - 1.0) / 2.0;
+  double a = lo, b = hi;
+  double c = b - invphi * (b - a), d = a + invphi * (b - a);
+  double fc, fd;
+  oid_status s = oid_gradient_gcv(ctx, std::pow(10.0, c), &fc, stream);
+  if (s != OID_OK) return s;
+  s = oid_gradient_gcv(ctx, std::pow(10.0, d), &fd, stream);
+  if (s != OID_OK) return s;
+  while (b - a > tol) {
+    if (fc < fd) {
+      b = d; d = c; fd = fc;
+      c = b - invphi * (b - a);
+      s = oid_gradient_gcv(ctx, std::pow(10.0, c), &fc, stream);
+    } else {
+      a = c; c = d; fc = fd;
+      d = a + invphi * (b - a);
+      s = oid_gradient_gcv(ctx, std::pow(10.0, d), &fd, stream);
+    }
+    if (s != OID_OK) return s;
+  }
+  *mu_star = std::pow(10.0, 0.5 * (a + b));
+  if (P_dev) {
+    s = oid_gradient_coefficients(ctx, *mu_star, P_dev, stream);
+    if (s != OID_OK) return s;
+    CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  }
+  return OID_OK;
+}
+
 oid_status oid_finalize(oid_ctx ctx, int64_t* J_host, double* P, int32_t P_on_device, void* basis_dev, void* stream) {
   if (!ctx) return OID_EINVAL;
   if (ctx->pending_nc >= 0) return ctx->fail(OID_ESTATE, "a sketch is pending commit");
@@ -1165,10 +1413,10 @@ oid_status oid_get(oid_ctx ctx, int32_t field, void* host_dst, size_t bytes, voi
     case 0: off = L.J; need = sizeof(int64_t) * ctx->t; break;
     case 1: off = L.tau_old; need = sizeof(double) * ctx->t; break;
     case 2: off = L.S; need = sizeof(double) * p.ell * ctx->n_obs; break;
-    case 3: off = L.gram; need = sizeof(double) * p.ell * p.ell; break;
+    case 3: off = L.gram; need = sizeof(double) * ctx->ga * p.ell * ctx->ga * p.ell; break;
     case 4: off = L.scal; need = sizeof(double) * 8; break;
     case 5: off = L.tau; need = sizeof(double) * (ctx->t + p.b_max); break;
-    case 6: off = L.mu; need = sizeof(double) * p.ell; break;
+    case 6: off = L.mu; need = sizeof(double) * ctx->ga * p.ell; break;
     case 7: off = L.Ypart; need = sizeof(double) * (p.ell + 1) * p.b_max; break;
     case 8: off = L.Sjpinv + static_cast<size_t>((ctx->epoch + 1) & 1) * ctx->t * p.ell * sizeof(double);
             need = sizeof(double) * ctx->t * p.ell; break;

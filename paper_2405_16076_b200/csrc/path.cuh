@@ -11,6 +11,8 @@ enum Scal : int {
   SC_T1 = 8, SC_T3A = 9, SC_T3B = 10, SC_GPP = 11, SC_FROB2_EST = 12, SC_KAPPA_EST = 13,
   SC_FROB2_SNAP = 16,   // + epoch parity: ||A_obs||^2 snapshot taken at the end of a commit
   SC_KAPPA_SNAP = 18,   // + epoch parity: kappa(S_J) of that epoch's Alg 4 chain
+  SC_FROB2_AUG = 20,    // gradient variant: ||A_obs||^2 + sum_p ||G^p A_obs||^2 (A11(2))
+  SC_GCV = 21,          // gradient variant: last sketched GCV value
   SC_COUNT = 24
 };
 
@@ -18,7 +20,8 @@ enum Scal : int {
 // largest (descending order), lambda per mode, shift = ell * lambda (reading R3),
 // dmax = max(mu) + shift.  One CTA (n <= 1024): rank sort, then sequential sums.
 __global__ void lambda_kernel(const double* __restrict__ mu, int n, int k, const double* __restrict__ gram,
-                              double lam_param, int ell, double* __restrict__ scal, double* __restrict__ sorted) {
+                              double lam_param, int ell, double* __restrict__ scal, double* __restrict__ sorted,
+                              int frob_idx) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const double v = mu[i];
     int rank = 0;
@@ -33,8 +36,8 @@ __global__ void lambda_kernel(const double* __restrict__ mu, int n, int k, const
     double Ek = 0.0;
     for (int i = 0; i < k && i < n; ++i) Ek += sorted[i];
     double tr = 0.0;
-    for (int i = 0; i < ell; ++i) tr += gram[static_cast<int64_t>(i) * ell + i];
-    const double frob2 = scal[SC_FROB2];
+    for (int i = 0; i < n; ++i) tr += gram[static_cast<int64_t>(i) * n + i];   // Gram order n (3 ell with gradients)
+    const double frob2 = scal[frob_idx];
     double lam;
     if (lam_param >= 0.0) lam = lam_param;
     else if (lam_param == -1.0) lam = fmax(0.0, (frob2 - Ek / ell) / k);

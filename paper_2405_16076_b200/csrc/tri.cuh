@@ -340,15 +340,15 @@ __global__ void __launch_bounds__(256) multisect_kernel(const double* __restrict
 __global__ void lambda_sorted_kernel(const double* __restrict__ mu, int n, int k, const double* __restrict__ gram,
                                      double lam_param, int ell, double* __restrict__ scal, int* __restrict__ gate,
                                      const double* __restrict__ d, const double* __restrict__ e,
-                                     double* __restrict__ ldl, int tri_ok) {
+                                     double* __restrict__ ldl, int tri_ok, int frob_idx) {
   __shared__ double red[8];
   double tr = 0.0;
-  for (int i = threadIdx.x; i < ell; i += blockDim.x) tr += gram[static_cast<int64_t>(i) * ell + i];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) tr += gram[static_cast<int64_t>(i) * n + i];   // Gram order n
   tr = block_sum<256>(tr, red);
   if (threadIdx.x != 0) return;
   double Ek = 0.0;
   for (int i = 0; i < k && i < n; ++i) Ek += mu[i];
-  const double frob2 = scal[SC_FROB2];
+  const double frob2 = scal[frob_idx];
   double lam;
   if (lam_param >= 0.0) lam = lam_param;
   else if (lam_param == -1.0) lam = fmax(0.0, (frob2 - Ek / ell) / k);

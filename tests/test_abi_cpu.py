@@ -55,6 +55,9 @@ def test_workspace_query_validates(oid):
         dict(m=4096, k=20, ell=48, b_max=16, n_cap=512, lam=0.0, split=(10, 10, 10)),
         dict(m=4096, k=20, ell=48, b_max=16, n_cap=512, lam=0.0, row_begin=100, row_end=50),
         dict(m=4096, k=20, ell=2000, b_max=16, n_cap=512, lam=0.0),                # ell > 1024
+        dict(m=4096, k=20, ell=48, b_max=16, n_cap=512, lam=0.0, grad=(2, 32, 32)),  # 2*32*32 != m
+        dict(m=4096, k=20, ell=400, b_max=16, n_cap=512, lam=0.0, grad=(4, 32, 32)),  # 3 ell > 1024
+        dict(m=4096, k=20, ell=48, b_max=16, n_cap=512, lam=0.0, grad=(4, 32, 32), row_begin=0, row_end=2048),
     ]
     for kw in bad_cases:
         with pytest.raises(oid.OidError):
@@ -62,6 +65,8 @@ def test_workspace_query_validates(oid):
 
 
 def test_struct_layout_matches_header(oid):
-    # oid_params: 4 int64 + 6 int32 + 4 double + uint64 + 4 int32 = 32 + 24 + 32 + 8 + 16 = 112 bytes
-    assert ctypes.sizeof(oid.OidParams) == 112
+    # oid_params: 4 int64 + 6 int32 + 4 double + uint64 + 4 int32 = 32 + 24 + 32 + 8 + 16 = 112 bytes,
+    # then the gradient-variant block: 4 int32 + 2 double = 32 bytes
+    assert ctypes.sizeof(oid.OidParams) == 144
+    assert oid.OidParams.grad_nfields.offset == 112 and oid.OidParams.grad_hx.offset == 128
     assert ctypes.sizeof(oid.OidStats) == 4 * 8 + 3 * 8 + 8

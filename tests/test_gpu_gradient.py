@@ -1,0 +1,80 @@
+"""GPU (C ABI) vs oracle parity of the gradient-enhanced variant.
+Run with -m gpu on a B200."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import OracleParams                                   # noqa: E402
+from oracle.gradient import OracleGradOID, grid_gradient_operators  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def oid():
+    from __graft_entry__ import build
+    build()
+    import paper_2405_16076_b200 as oid
+    assert torch.cuda.is_available()
+    return oid
+
+
+def _fields(nf, nx, ny, n, seed, noise=1e-3):
+    """n snapshots of nf smooth fields on an nx x ny unit-square grid (layout of reading Q17)."""
+    rng = np.random.default_rng(seed)
+    i, j = np.meshgrid(np.arange(nx), np.arange(ny), indexing="ij")
+    x, y = (i / (nx - 1)).ravel(), (j / (ny - 1)).ravel()
+    cols = []
+    for s in range(n):
+        f = []
+        for fi in range(nf):
+            a, b, c, d = rng.standard_normal(4)
+            f.append(np.sin((2 + fi) * x + a + 0.05 * s) * np.cos(3 * y + b) + 0.3 * c * x * y + d * x
+                     + noise * rng.standard_normal(nx * ny))
+        cols.append(np.concatenate(f))
+    return np.stack(cols, axis=1)
+
+
+@pytest.mark.parametrize("nf,nx,ny,k,ell,b,dtype", [(2, 24, 20, 6, 24, 8, np.float64),
+                                                     (3, 16, 16, 10, 48, 16, np.float32),
+                                                     (1, 64, 40, 12, 200, 16, np.float64)])
+def test_gradient_variant_parity(oid, nf, nx, ny, k, ell, b, dtype):
+    m, n = nf * nx * ny, 4 * b
+    A = _fields(nf, nx, ny, n, seed=nx + ny).astype(dtype)
+    split = (ell // 6, ell // 3, ell - ell // 6 - ell // 3)
+    p = oid.make_params(m=m, k=k, ell=ell, b_max=b, n_cap=n, lam=-1.0, split=split, seed=4,
+                        dtype="f64" if dtype == np.float64 else "f32", grad=(nf, nx, ny))
+    eng = oid.Engine(p)
+    o = OracleGradOID(OracleParams(m=m, k=k, ell=ell, ell1=split[0], ell2=split[1], ell3=split[2], lam=-1.0, seed=4),
+                      grid_gradient_operators(nf, nx, ny))
+    Ad = torch.from_numpy(np.asfortranarray(A)).to("cuda:0")
+    low = None
+    for e, j in enumerate(range(0, n, b)):
+        eng.ingest_block(Ad[:, j:j + b])
+        lg = o.ingest_block(A[:, j:j + b].astype(np.float64))
+        if low is None and any(d[5] < 1e-6 for d in lg.decisions):
+            low = e
+        if low is None:
+            assert np.array_equal(eng.J(), o.J), (e, eng.J(), o.J)
+    G = eng.get(3)
+    assert G.shape == (3 * ell, 3 * ell)
+    assert np.linalg.norm(G - o.gram) <= 1e-10 * np.linalg.norm(o.gram)
+    if low is not None:
+        pytest.skip(f"decision margin < 1e-6 at epoch {low}")
+    # estimate (plain Alg 4 P) unaffected by the variant
+    est, ref = eng.error_estimate(), o.error_estimate()
+    assert abs(est["est_rel"] - ref["est_rel"]) < 1e-5
+    # sketched GCV at fixed mu, and P(mu)
+    OGO = o.omega_g_omega()
+    for mu in (1e-2, 1.0, 50.0):
+        g_gpu, g_ref = eng.gradient_gcv(mu), o.gcv(mu, OGO)
+        assert abs(g_gpu - g_ref) <= 1e-7 * abs(g_ref), (mu, g_gpu, g_ref)
+        P = eng.gradient_coefficients(mu).cpu().numpy()
+        Pr = o.coefficients(mu)
+        assert np.linalg.norm(P - Pr) <= 1e-6 * np.linalg.norm(Pr), mu
+    # golden section: the same mu* up to the search tolerance, P(mu*)
+    mu_g, P_g = eng.gradient_finalize(-3.0, 3.0, 1e-3)
+    mu_o, P_o = o.finalize(-3.0, 3.0, 1e-3)
+    assert abs(np.log10(mu_g) - np.log10(mu_o)) <= 2e-3
+    assert np.linalg.norm(P_g.cpu().numpy() - P_o) <= 1e-4 * np.linalg.norm(P_o)
