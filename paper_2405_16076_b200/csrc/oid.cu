@@ -311,6 +311,7 @@ struct oid_ctx_s {
   int bg_free_sms = 0;        // SMs the A9 kernel leaves free (diagnostics: OID_BG_FREE)
   int bg_waves = 32;          // A9 CTAs per SM (short CTAs; diagnostics: OID_BG_WAVES)
   bool use_side = true;       // diagnostics: OID_NO_SIDE=1 runs everything on the caller's stream
+  int k1_free_sms = 0;        // SMs the persistent K1 grid leaves to concurrent streams (OID_K1_FREE)
   bool timeline = false;      // diagnostics: OID_TIMELINE=1 records tagged events (oid_get 13)
   std::vector<std::pair<int, cudaEvent_t>> tl;
   char err[512] = {0};
@@ -561,7 +562,7 @@ oid_status sketch_one(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream
          (static_cast<uint32_t>(ctx->qmag[2]) << 16) | (static_cast<uint32_t>(ctx->qmag[3]) << 24);
   a.t1 = static_cast<uint32_t>(ctx->qmag[4]) | (static_cast<uint32_t>(ctx->qmag[5]) << 8) |
          (static_cast<uint32_t>(ctx->qmag[6]) << 16) | (static_cast<uint32_t>(ctx->qmag[7]) << 24);
-  a.num_sms = ctx->num_sms;
+  a.num_sms = std::max(2, ctx->num_sms - ctx->k1_free_sms);
   a.dbg = ctx->k1_debug ? ctx->ptr<long long>(ctx->L.dbg) : nullptr;
   const bool tc_call = want_tc && ctx->tc_ok && k1tc_call_ok(a);
   if (strict_mode && p.k1_mode == OID_K1_TC_INT8 && !tc_call)
@@ -1053,13 +1054,13 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
   {
     int lo = 0, hi = 0;
     if ((e = cudaDeviceGetStreamPriorityRange(&lo, &hi)) != cudaSuccess) return bad(e);
-    // Priorities relative to the ingest stream given at init (measured best on C3, profiles/
-    // r01_summary.md): A8 (side) one level above it (the estimate factors wait for it), the
-    // estimate factors and tail (side2) at its level (so the next block's persistent K1 is not
-    // starved of SMs by them, and they are not starved by a low-priority estimate stream).
+    // Both side streams at the priority of the ingest stream given at init (measured best on C3
+    // among above / equal / below, profiles/r01_summary.md): above it they starve the next block's
+    // persistent K1 of SMs, below it (with a low-priority estimate stream) the estimate chain lags.
     int p_ing = 0;
     if (cudaStreamGetPriority(st, &p_ing) != cudaSuccess) p_ing = lo;
-    const int p_side = getenv("OID_SIDE_PRIO") ? atoi(getenv("OID_SIDE_PRIO")) : std::max(hi, p_ing - 1);
+    (void)hi;
+    const int p_side = getenv("OID_SIDE_PRIO") ? atoi(getenv("OID_SIDE_PRIO")) : p_ing;
     const int p_side2 = getenv("OID_SIDE2_PRIO") ? atoi(getenv("OID_SIDE2_PRIO")) : p_ing;
     if ((e = cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, p_side)) != cudaSuccess) return bad(e);
     if ((e = cudaStreamCreateWithPriority(&ctx->side2, cudaStreamNonBlocking, p_side2)) != cudaSuccess) return bad(e);
@@ -1072,6 +1073,7 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
     if (getenv("OID_BG_FREE")) ctx->bg_free_sms = std::max(0, atoi(getenv("OID_BG_FREE")));
     if (getenv("OID_BG_WAVES")) ctx->bg_waves = std::max(1, atoi(getenv("OID_BG_WAVES")));
     ctx->use_side = !(getenv("OID_NO_SIDE") && atoi(getenv("OID_NO_SIDE")) != 0);
+    if (getenv("OID_K1_FREE")) ctx->k1_free_sms = std::max(0, atoi(getenv("OID_K1_FREE")));
     ctx->timeline = getenv("OID_TIMELINE") && atoi(getenv("OID_TIMELINE")) != 0;
   }
   ctx->k1_ctas_per_sm = 1;
