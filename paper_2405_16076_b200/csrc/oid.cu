@@ -692,7 +692,7 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   // A6: selection / replacement; the previous block's Alg 4 chain reads J first
   tl_mark(ctx, st, 4);
   CK(cudaStreamWaitEvent(st, ctx->ev_sj_j, 0));
-  select_kernel<<<1, 32, 0, st>>>(ctx->ptr<int64_t>(L.J), ctx->d(L.tau_old), ctx->d(L.tau), Yp + int64_t(ell) * nc, t, nc,
+  select_kernel<<<1, 256, 0, st>>>(ctx->ptr<int64_t>(L.J), ctx->d(L.tau_old), ctx->d(L.tau), Yp + int64_t(ell) * nc, t, nc,
                                   ctx->factor, static_cast<uint32_t>(ctx->epoch), ctx->n_obs, ctx->key0, ctx->key1,
                                   ctx->ptr<int>(L.admit), ctx->ptr<int>(L.counts), scal, ctx->ptr<int>(L.dirty),
                                   static_cast<int>(ctx->epoch + 1));

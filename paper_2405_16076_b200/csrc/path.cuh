@@ -88,58 +88,103 @@ __global__ void scores_kernel(const double* __restrict__ T, const double* __rest
   if (threadIdx.x == 0) tau[j] = s;
 }
 
+constexpr int kSelMaxT = 416;   // validated maximum of k
+
 // Alg 3 steps 15-27, readings R4-R7, R14.  Single thread (sequential by nature:
 // slot i+1 sees the candidates consumed by slot i).
 // tau: [t slot scores | nc candidate scores]; nrm: candidate norms (zero columns skipped).
 // Outputs: admit list (slot, r) pairs, count; zero list (slots vacated, not refilled).
-__global__ void select_kernel(int64_t* __restrict__ J, double* __restrict__ tau_old, const double* __restrict__ tau,
-                              const double* __restrict__ nrm, int t, int nc, double factor, uint32_t epoch,
-                              int64_t base, uint32_t key0, uint32_t key1, int* __restrict__ admit,
-                              int* __restrict__ counts, double* __restrict__ scal, int* __restrict__ dirty, int dtag) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  unsigned consumed[2] = {0u, 0u};   // nc <= 64
-  int na = 0, nz = 0;
-  double minm = scal[SC_MINMARGIN];
-  for (int i = 0; i < t; ++i) {
-    bool occupied = J[i] >= 0;
-    bool evicted = false;
-    if (occupied) {
+__global__ void __launch_bounds__(256) select_kernel(int64_t* __restrict__ J, double* __restrict__ tau_old,
+                                                      const double* __restrict__ tau, const double* __restrict__ nrm, int t,
+                                                      int nc, double factor, uint32_t epoch, int64_t base, uint32_t key0,
+                                                      uint32_t key1, int* __restrict__ admit, int* __restrict__ counts,
+                                                      double* __restrict__ scal, int* __restrict__ dirty, int dtag) {
+  // The decisions are sequential only through the candidates consumed by earlier slots: the
+  // eviction of slot i depends on slot i alone (steps 16-19), so
+  //   (1) the evictions are decided in parallel, one thread per slot;
+  //   (2) one warp walks the vacant slots in order; for each, the lanes draw and test the
+  //       candidates r = lane, lane + 32 at once and the first success in index order is the
+  //       admission (the same as the sequential scan: candidates before it fail, later draws
+  //       are never looked at).
+  // The R14 margin is the min over exactly the draws the sequential scan evaluates.  Small
+  // footprint (256 threads, no dynamic shared memory) so the kernel fits beside the Gram CTAs.
+  __shared__ unsigned char s_vac[kSelMaxT], s_ev[kSelMaxT];
+  __shared__ double s_red[32];
+  double mm = INFINITY;
+  for (int i = threadIdx.x; i < t; i += blockDim.x) {
+    bool vac = J[i] < 0, ev = false;
+    if (!vac) {
       const double told = tau_old[i];
       const double ti = fmin(told, tau[i]);
       const double rho = told > 0.0 ? ti / told : 1.0;
       const double pev = 1.0 - rho;
       const double u = select_uniform(epoch, static_cast<uint32_t>(i), 0xFFFFFFFFu, key0, key1);
-      minm = fmin(minm, fabs(u - pev) / fmax(rho, 0x1p-24));
-      if (u < pev) { J[i] = -1; tau_old[i] = 1.0; occupied = false; evicted = true; }
+      mm = fmin(mm, fabs(u - pev) / fmax(rho, 0x1p-24));
+      if (u < pev) { J[i] = -1; tau_old[i] = 1.0; vac = ev = true; }
       else tau_old[i] = ti;
     }
-    if (!occupied) {
-      bool filled = false;
-      for (int r = 0; r < nc; ++r) {
-        if ((consumed[r >> 5] >> (r & 31)) & 1u) continue;
-        if (nrm[r] == 0.0) continue;
-        const double praw = tau[t + r] * factor;
-        const double p = fmin(1.0, praw);
-        const double u = select_uniform(epoch, static_cast<uint32_t>(i), static_cast<uint32_t>(r), key0, key1);
-        minm = fmin(minm, fabs(u - praw) / fmax(praw, 0x1p-24));
-        if (u < p) {
-          J[i] = base + r;
-          tau_old[i] = tau[t + r];
-          consumed[r >> 5] |= 1u << (r & 31);
-          admit[2 * na] = i;
-          admit[2 * na + 1] = r;
-          dirty[i] = dtag;   // epoch tag of the admission (estimates pick tags newer than theirs)
+    s_vac[i] = vac;
+    s_ev[i] = ev;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    // candidate r's probability (float copies only index the smem; the tests use fp64)
+    double praw[2], pr[2];
+    bool ok[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = lane + 32 * h;
+      ok[h] = r < nc && nrm[r] != 0.0;
+      praw[h] = r < nc ? tau[t + r] * factor : 0.0;
+      pr[h] = fmin(1.0, praw[h]);
+    }
+    int na = 0, nz = 0;
+    for (int i0 = 0; i0 < t; i0 += 32) {
+      uint32_t vm = __ballot_sync(0xffffffffu, i0 + lane < t && s_vac[i0 + lane]);
+      while (vm) {
+        const int i = i0 + __ffs(vm) - 1;
+        vm &= vm - 1;
+        bool hit[2];
+        double u[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          u[h] = ok[h] ? select_uniform(epoch, static_cast<uint32_t>(i), static_cast<uint32_t>(lane + 32 * h), key0, key1)
+                       : 1.0;
+          hit[h] = ok[h] && u[h] < pr[h];
+        }
+        const uint32_t b0 = __ballot_sync(0xffffffffu, hit[0]), b1 = __ballot_sync(0xffffffffu, hit[1]);
+        const int rs = b0 ? __ffs(b0) - 1 : (b1 ? 32 + __ffs(b1) - 1 : 64);   // 64: no admission
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (ok[h] && lane + 32 * h <= rs) mm = fmin(mm, fabs(u[h] - praw[h]) / fmax(praw[h], 0x1p-24));
+        if (rs < 64) {
+          if (lane == 0) {
+            J[i] = base + rs;
+            tau_old[i] = tau[t + rs];
+            admit[2 * na] = i;
+            admit[2 * na + 1] = rs;
+            dirty[i] = dtag;   // epoch tag of the admission (estimates pick tags newer than theirs)
+          }
+          if (lane == (rs & 31)) ok[rs >> 5] = false;   // consumed
           ++na;
-          filled = true;
-          break;
+        } else if (s_ev[i]) {
+          if (lane == 0) admit[2 * (nc + t) - 2 - 2 * nz] = i;
+          ++nz;
         }
       }
-      if (evicted && !filled) { admit[2 * (nc + t) - 2 - 2 * nz] = i; ++nz; }
     }
+    if (lane == 0) { counts[0] = na; counts[1] = nz; }
   }
-  counts[0] = na;
-  counts[1] = nz;
-  scal[SC_MINMARGIN] = minm;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mm = fmin(mm, __shfl_xor_sync(0xffffffffu, mm, o));
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = mm;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = scal[SC_MINMARGIN];
+    for (int q = 0; q < static_cast<int>(blockDim.x >> 5); ++q) m = fmin(m, s_red[q]);
+    scal[SC_MINMARGIN] = m;
+  }
 }
 
 // C(:, slot) <- X(:, r) for admissions, C(:, slot) <- 0 for vacated slots.

@@ -1,5 +1,6 @@
 python -c "import __graft_entry__ as g; g.build()" || exit 1
-for cfg in "OID_SIDE_PRIO=0" "OID_SIDE_PRIO=-1" "OID_SIDE_PRIO=0 OID_SIDE2_PRIO=-2"; do
-  env $cfg timeout 900 python bench.py --skip-cpu-baseline --e2e-steps 0 > gpurun_out/bench.log 2>&1
-  echo "$cfg: $(tail -1 gpurun_out/bench.log | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(round(d["ms_per_step"],3), round(d["value"],1), round(d["roofline"]["frac"],3), d["breakdown_ms_per_step"]["k1"])')"
-done
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_gpu.log
+timeout 900 python bench.py --skip-cpu-baseline --e2e-steps 0 > gpurun_out/bench.log 2>&1
+echo "$(tail -1 gpurun_out/bench.log | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(round(d["ms_per_step"],3), round(d["value"],1), round(d["roofline"]["frac"],3), d["breakdown_ms_per_step"])')"
+timeout 600 python bench.py --steps 4 --warmup 3 --skip-cpu-baseline --e2e-steps 0 > gpurun_out/plain_b.log 2>&1 && \
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_iter.csv python bench.py --steps 4 --warmup 3 --skip-cpu-baseline --e2e-steps 0 > gpurun_out/ncu_b.log 2>&1; echo "ncu rc=$?"
