@@ -421,7 +421,7 @@ oid_status spd_solve(oid_ctx ctx, cudaStream_t st, const double* A, int n, const
     wy_t_kernel<<<(n - 2 + kRefChunk - 1) / kRefChunk, 256, 0, st>>>(ctx->d(L.Vh2), ctx->d(L.tauv2), n, ctx->d(L.wyT2));
     CKL();
   }
-  multisect_kernel<<<(n * 32 + 255) / 256, 256, sizeof(double) * 2 * n, st>>>(ctx->d(L.td2), ctx->d(L.te2), n,
+  multisect_kernel<<<(n * 32 + 255) / 256, 256, sizeof(double) * multisect_smem_doubles(n), st>>>(ctx->d(L.td2), ctx->d(L.te2), n,
                                                                             ctx->d(L.mu2));
   CKL();
   spd_gate_kernel<<<1, 32, 0, st>>>(ctx->d(L.mu2), n, kmax2, ctx->d(L.td2), ctx->d(L.te2), ctx->d(L.ldl2), gate,
@@ -653,7 +653,7 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
       wy_t_kernel<<<(ng - 2 + kRefChunk - 1) / kRefChunk, 256, 0, st>>>(ctx->d(L.Vh), ctx->d(L.tauv), ng, ctx->d(L.wyT));
       CKL();
     }
-    multisect_kernel<<<(ng * 32 + 255) / 256, 256, sizeof(double) * 2 * ng, st>>>(ctx->d(L.td), ctx->d(L.te), ng,
+    multisect_kernel<<<(ng * 32 + 255) / 256, 256, sizeof(double) * multisect_smem_doubles(ng), st>>>(ctx->d(L.td), ctx->d(L.te), ng,
                                                                                   ctx->d(L.mu));
     CKL();
     lambda_sorted_kernel<<<1, 256, 0, st>>>(ctx->d(L.mu), ng, p.k, ctx->d(L.gram), p.lambda, ell, scal, gate,

@@ -257,25 +257,37 @@ tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__
 }
 
 // Number of eigenvalues >= x of the symmetric tridiagonal (d, e2 = e^2): n minus the number of
-// sign changes of the Sturm sequence p_0 = 1, p_j = (d_j - x) p_{j-1} - e_{j-1}^2 p_{j-2} (no
-// divisions; both terms rescaled by exact powers of two when large or small; a zero p_j takes
-// the sign opposite to p_{j-1}).
+// sign changes of the Sturm sequence p_{-1} = 1, p_j = (d_j - x) p_{j-1} - e_{j-1}^2 p_{j-2}
+// (e2[0] = 0; no divisions; a zero p_j takes the sign opposite to p_{j-1}).  The caller scales
+// (d, e2, x) by (s, s^2, s) with s an exact power of two so that |d|, |x| <= 2 and e2 <= 1:
+// every p_j scales by s^(j+1) exactly, so the count is unchanged, and |p_j| grows by at most 2^3
+// per step, which lets the power-of-two renormalisation run once per 8 steps.  d and e2 are
+// padded to a multiple of 8 with (d = 4, e2 = 0): d - x > 0 there, no sign change.
+constexpr int kSturmUnroll = 8;
 __device__ __forceinline__ int sturm_count_gt(const double* __restrict__ d, const double* __restrict__ e2, int n,
-                                              double x, double /*pivmin*/) {
+                                              double x) {
   int neg = 0;
-  double pm = 1.0, pc = d[0] - x;
-  if (pc == 0.0) pc = -0x1p-1000;
-  neg += pc < 0.0;
-  for (int j = 1; j < n; ++j) {
-    double pn = (d[j] - x) * pc - e2[j - 1] * pm;
-    if (pn == 0.0) pn = (pc < 0.0) ? 0x1p-1000 : -0x1p-1000;
-    neg += (pn < 0.0) != (pc < 0.0);
-    pm = pc;
-    pc = pn;
+  double pm = 0.0, pc = 1.0;
+  const int npad = (n + kSturmUnroll - 1) & ~(kSturmUnroll - 1);
+  for (int j0 = 0; j0 < npad; j0 += kSturmUnroll) {
+    double dv[kSturmUnroll], ev[kSturmUnroll];
+#pragma unroll
+    for (int u = 0; u < kSturmUnroll; u += 2) {
+      const double2 a = *reinterpret_cast<const double2*>(d + j0 + u);
+      const double2 b = *reinterpret_cast<const double2*>(e2 + j0 + u);
+      dv[u] = a.x; dv[u + 1] = a.y; ev[u] = b.x; ev[u + 1] = b.y;
+    }
+#pragma unroll
+    for (int u = 0; u < kSturmUnroll; ++u) {
+      double pn = fma(dv[u] - x, pc, -ev[u] * pm);
+      if (pn == 0.0) pn = (pc < 0.0) ? 0x1p-1000 : -0x1p-1000;
+      neg += (pn < 0.0) != (pc < 0.0);
+      pm = pc;
+      pc = pn;
+    }
     const double a = fabs(pc);
     if (a > 0x1p+400 || a < 0x1p-400) {
-      const int ex = ilogb(pc);
-      const double sc = ldexp(1.0, -ex);
+      const double sc = ldexp(1.0, -ilogb(pc));
       pc *= sc;
       pm *= sc;
     }
@@ -283,45 +295,50 @@ __device__ __forceinline__ int sturm_count_gt(const double* __restrict__ d, cons
   return n - neg;
 }
 
+// smem doubles multisect_kernel needs for order n
+__host__ __device__ constexpr int multisect_smem_doubles(int n) { return 2 * ((n + kSturmUnroll - 1) & ~(kSturmUnroll - 1)); }
+
 __global__ void __launch_bounds__(256) multisect_kernel(const double* __restrict__ d, const double* __restrict__ e, int n,
                                                         double* __restrict__ mu) {
   extern __shared__ double ms_smem[];
+  const int npad = (n + kSturmUnroll - 1) & ~(kSturmUnroll - 1);
   double* ds = ms_smem;
-  double* e2 = ms_smem + n;
+  double* e2 = ms_smem + npad;
   __shared__ double bnd[4];
   const int tid = threadIdx.x;
-  for (int j = tid; j < n; j += blockDim.x) {
-    ds[j] = d[j];
-    if (j < n - 1) e2[j] = e[j] * e[j];
-  }
-  __syncthreads();
   if (tid == 0) {
-    double lo = INFINITY, hi = -INFINITY, tmax = 0.0, emax2 = 0.0;
+    double lo = INFINITY, hi = -INFINITY, tmax = 0.0;
     for (int j = 0; j < n; ++j) {
       const double r = (j > 0 ? fabs(e[j - 1]) : 0.0) + (j < n - 1 ? fabs(e[j]) : 0.0);
       lo = fmin(lo, d[j] - r);
       hi = fmax(hi, d[j] + r);
       tmax = fmax(tmax, fabs(d[j]) + r);
-      if (j < n - 1) emax2 = fmax(emax2, e[j] * e[j]);
     }
     const double eps = 2.220446049250313e-16;
     const double pad = 2.0 * eps * tmax + 1e-300;
     bnd[0] = lo - pad;
     bnd[1] = hi + pad;
-    bnd[2] = 2.2250738585072014e-308 * fmax(1.0, emax2);   // LAPACK pivmin
-    bnd[3] = 4.0 * eps * tmax;                                 // absolute accuracy of a Sturm count
+    bnd[2] = tmax > 0.0 ? ldexp(1.0, -ilogb(tmax) - 1) : 1.0;   // s: s tmax in [0.5, 1)
+    bnd[3] = 4.0 * eps * tmax;                                    // absolute accuracy of a Sturm count
   }
   __syncthreads();
-  const double pivmin = bnd[2];
+  const double sc = bnd[2];
+  for (int j = tid; j < npad; j += blockDim.x) {
+    // |d_j| + |e_j| <= tmax, so s |d_j| < 1, s^2 e_j^2 < 1; |s x| < 2 for x in [lo, hi]
+    ds[j] = j < n ? sc * d[j] : 4.0;
+    const double ev = (j > 0 && j < n) ? sc * e[j - 1] : 0.0;
+    e2[j] = ev * ev;
+  }
+  __syncthreads();
   const int warp = (blockIdx.x * blockDim.x + tid) >> 5, lane = tid & 31;
   if (warp >= n) return;
   const int i = warp;                     // target: (i+1)-th largest
   double lo = bnd[0], hi = bnd[1];
   const double eps = 2.220446049250313e-16;
   for (int it = 0; it < 40; ++it) {
-    if (hi - lo <= fmax(2.0 * eps * fmax(fabs(lo), fabs(hi)), bnd[3]) + pivmin) break;
+    if (hi - lo <= fmax(2.0 * eps * fmax(fabs(lo), fabs(hi)), bnd[3]) + 1e-300) break;
     const double x = lo + (hi - lo) * static_cast<double>(lane + 1) / 33.0;
-    const int gt = sturm_count_gt(ds, e2, n, x, pivmin);   // #eigenvalues >= x
+    const int gt = sturm_count_gt(ds, e2, n, sc * x);   // #eigenvalues >= x
     // new lo: largest x with gt >= i+1; new hi: smallest x with gt <= i
     const unsigned okm = __ballot_sync(0xffffffffu, gt >= i + 1);
     const int last_ok = okm ? 31 - __clz(okm) : -1;          // lanes with larger x have smaller counts
