@@ -107,7 +107,7 @@ struct Bump {
 struct Layout {
   size_t S, gram, Ypart, k1part, k1npart, gB, gV, mu, mu_sorted, Yc, Tsc, tau, scal, J, tau_old, admit, counts,
       flags, counters, C, SJ, sjB, sjV, sjsig, sjw, sjZ, Sjpinv, Pexp, AJP, G, Gsum, Gpart, cB, cV, csig, cw, cZ, M,
-      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, wyT, sjG, cG, cBt, cZ2, dbg, Jsnap, Dsnap, S1, S2, YpG, GX, OGO, gH, gHV, gHs, gHw, gHZ, gHp, gR, gCm, gE, gLst, gLV, gLs, gLw, gLZ, gLp, gRhs, gscal, td2, te2, Vh2, tauv2, wyT2, ldl2, mu2, total;
+      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, wyT, sjG, cG, cBt, cZ2, dbg, Jsnap, Dsnap, gcnt, S1, S2, YpG, GX, OGO, gH, gHV, gHs, gHw, gHZ, gHp, gR, gCm, gE, gLst, gLV, gLs, gLw, gLZ, gLp, gRhs, gscal, td2, te2, Vh2, tauv2, wyT2, ldl2, mu2, total;
 };
 
 int64_t m_local(const oid_params& p) { return p.row_end - p.row_begin; }
@@ -155,7 +155,7 @@ Layout make_layout(const oid_params& p) {
   L.Pexp = b.take(t * n * d);
   L.AJP = b.take(ell * n * d);
   L.G = b.take(t * t * d);
-  L.Gsum = b.take(t * t * d);
+  L.Gsum = b.take(2 * t * t * d);           // by estimate parity (A9 stream vs estimate tail)
   L.Gpart = b.take(static_cast<size_t>(gram_tc_chunks(static_cast<int>(t)) + 64) * t * t * d);   // + 64 segment sums
   const size_t l1 = p.ell1, l2 = p.ell2, l3 = p.ell3;
   L.cB = b.take(std::max<size_t>(1, l1 * l2) * d);
@@ -175,7 +175,8 @@ Layout make_layout(const oid_params& p) {
   L.est = b.take(8 * d);
   L.Gfull = b.take(t * t * d);
   L.dirty = b.take(t * sizeof(int));
-  L.dlist = b.take(t * sizeof(int));
+  L.dlist = b.take(2 * t * sizeof(int));
+  L.gcnt = b.take(8 * sizeof(int));          // [4 par + 2] = dirty count of estimate parity par
   L.jfro2 = b.take(kNumJacobiUses * d);
   L.symU = b.take(static_cast<size_t>(kSymMaxPairs) * kSymB * kSymB * d);
   L.symF = b.take(kSymMaxPairs * sizeof(int));
@@ -296,6 +297,10 @@ struct oid_ctx_s {
   // copy (A7) and the basis-Gram-independent part of Alg 8 (A10) beside the basis Gram (A9).
   cudaStream_t side = nullptr;    // Alg 4 chains (A8)
   cudaStream_t side2 = nullptr;   // estimate factors and tail (A10)
+  cudaStream_t gs = nullptr;      // A9 basis Gram (and its dirty list / sums), lowest priority
+  cudaEvent_t ev_gs_done = nullptr;                  // the last estimate's A9 partial sums are ready
+  cudaEvent_t ev_gsum_free[2] = {nullptr, nullptr};  // the estimate tail scattered that parity's sums
+  int n_est = 0, est_par = 0;  // estimates begun; parity of the current one
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_sj_done[2] = {nullptr, nullptr};   // A8 of an epoch parity finished (S_J, S_J^+ ready)
   cudaEvent_t ev_sj_free[2] = {nullptr, nullptr};   // the estimate finished reading that parity's S_J, S_J^+
@@ -310,6 +315,7 @@ struct oid_ctx_s {
   cudaEvent_t ev_committed = nullptr, ev_gram_done = nullptr, ev_sj_j = nullptr, ev_est_done = nullptr;
   int bg_free_sms = 0;        // SMs the A9 kernel leaves free (diagnostics: OID_BG_FREE)
   int bg_waves = 32;          // A9 CTAs per SM (short CTAs; diagnostics: OID_BG_WAVES)
+  int bg_smem_kb = 200;       // A9 ring budget (diagnostics: OID_BG_SMEM)
   bool use_side = true;       // diagnostics: OID_NO_SIDE=1 runs everything on the caller's stream
   int k1_free_sms = 0;        // SMs the persistent K1 grid leaves to concurrent streams (OID_K1_FREE)
   bool timeline = false;      // diagnostics: OID_TIMELINE=1 records tagged events (oid_get 13)
@@ -649,6 +655,7 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
     tridiag_cluster_kernel<<<kTriCtas, 256, smem, st>>>(ctx->d(L.gram), ng, ctx->d(L.td), ctx->d(L.te), ctx->d(L.Vh),
                                                         ctx->d(L.tauv), ctx->k1_debug ? ctx->ptr<long long>(L.dbg) + k1tc::kDbgRows * k1tc::kDbgTiles : nullptr);
     CKL();
+    tl_mark(ctx, st, 15);
     if (ng > 2) {
       wy_t_kernel<<<(ng - 2 + kRefChunk - 1) / kRefChunk, 256, 0, st>>>(ctx->d(L.Vh), ctx->d(L.tauv), ng, ctx->d(L.wyT));
       CKL();
@@ -662,6 +669,7 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
     tri_scores_kernel<<<ns, 256, sizeof(double) * kQStages * kRefChunk * tri_ldv(ng), st>>>(ctx->d(L.Yc), ng, ns, ctx->d(L.Vh), ctx->d(L.wyT), ctx->d(L.ldl), gate,
                                           ctx->d(L.tau));
     CKL();
+    tl_mark(ctx, st, 16);
     const int* g1 = gate + 1;
     s = gemm(ctx, st, false, false, ng, ng, ng, 1.0, ctx->d(L.gram), ng, ctx->d(L.gV), ng, 0.0, ctx->d(L.gT), ng, g1);
     if (s != OID_OK) return s;
@@ -1064,14 +1072,18 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
     const int p_side2 = getenv("OID_SIDE2_PRIO") ? atoi(getenv("OID_SIDE2_PRIO")) : p_ing;
     if ((e = cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, p_side)) != cudaSuccess) return bad(e);
     if ((e = cudaStreamCreateWithPriority(&ctx->side2, cudaStreamNonBlocking, p_side2)) != cudaSuccess) return bad(e);
+    // A9 at the lowest priority: throughput work that fills whatever the latency-bound chains leave
+    const int p_gs = getenv("OID_GS_PRIO") ? atoi(getenv("OID_GS_PRIO")) : lo;
+    if ((e = cudaStreamCreateWithPriority(&ctx->gs, cudaStreamNonBlocking, p_gs)) != cudaSuccess) return bad(e);
     if ((e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming)) != cudaSuccess) return bad(e);
     if ((e = cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming)) != cudaSuccess) return bad(e);
     for (cudaEvent_t* ev : {&ctx->ev_committed, &ctx->ev_gram_done, &ctx->ev_sj_j, &ctx->ev_est_done, &ctx->ev_sj_done[0],
                             &ctx->ev_sj_done[1], &ctx->ev_sj_free[0], &ctx->ev_sj_free[1], &ctx->ev_snap_free[0],
-                            &ctx->ev_snap_free[1]})
+                            &ctx->ev_snap_free[1], &ctx->ev_gs_done, &ctx->ev_gsum_free[0], &ctx->ev_gsum_free[1]})
       if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess) return bad(e);
     if (getenv("OID_BG_FREE")) ctx->bg_free_sms = std::max(0, atoi(getenv("OID_BG_FREE")));
     if (getenv("OID_BG_WAVES")) ctx->bg_waves = std::max(1, atoi(getenv("OID_BG_WAVES")));
+    if (getenv("OID_BG_SMEM")) ctx->bg_smem_kb = std::min(200, std::max(8, atoi(getenv("OID_BG_SMEM"))));
     ctx->use_side = !(getenv("OID_NO_SIDE") && atoi(getenv("OID_NO_SIDE")) != 0);
     if (getenv("OID_K1_FREE")) ctx->k1_free_sms = std::max(0, atoi(getenv("OID_K1_FREE")));
     ctx->timeline = getenv("OID_TIMELINE") && atoi(getenv("OID_TIMELINE")) != 0;
@@ -1135,6 +1147,7 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
   if ((e = cudaMemsetAsync(ctx->ws + L.Gfull, 0, sizeof(double) * ctx->t * ctx->t, st)) != cudaSuccess) return bad(e);
   if ((e = cudaMemsetAsync(ctx->ws + L.dirty, 0, sizeof(int) * ctx->t, st)) != cudaSuccess) return bad(e);
   if ((e = cudaMemsetAsync(ctx->ws + L.counts, 0, 4 * sizeof(int), st)) != cudaSuccess) return bad(e);
+  if ((e = cudaMemsetAsync(ctx->ws + L.gcnt, 0, 8 * sizeof(int), st)) != cudaSuccess) return bad(e);
   {
     const int64_t RL = 128 / static_cast<int64_t>(dsize(*p));
     const size_t cb = static_cast<size_t>((ctx->m_loc + RL - 1) / RL * RL) * ctx->t * dsize(*p);
@@ -1180,7 +1193,7 @@ oid_status oid_partials(oid_ctx ctx, int32_t which, double** dev_ptr, int64_t* c
     *dev_ptr = ctx->d(ctx->L.Ypart);
     *count = int64_t(ctx->p.ell + 1) * std::max(0, ctx->pending_nc);
   } else if (which == 1) {
-    *dev_ptr = ctx->d(ctx->L.Gsum);
+    *dev_ptr = ctx->d(ctx->L.Gsum) + static_cast<size_t>(ctx->est_par) * ctx->t * ctx->t;
     *count = int64_t(ctx->t) * ctx->t;
   } else {
     return OID_EINVAL;
@@ -1200,8 +1213,21 @@ oid_status oid_estimate_begin(oid_ctx ctx, void* stream) {
   const int par = static_cast<int>((ctx->epoch + 1) & 1);
   CK(cudaStreamWaitEvent(st, ctx->ev_committed, 0));
   tl_mark(ctx, st, 7);
-  dirty_compact_kernel<<<1, 32, 0, st>>>(ctx->ptr<int>(L.Dsnap) + static_cast<size_t>(par) * t, t, ctx->last_est_tag,
-                                         ctx->ptr<int>(L.dlist), ctx->ptr<int>(L.counts));
+  // A9 on its own stream, ordered after the commit it reads (and after the tail of the estimate
+  // two back, which read this parity's sums) but not behind the previous estimate's tail on `st`:
+  // the Gram of estimate e+1 must not wait for the A10 factors of estimate e.
+  const int gp = ctx->n_est & 1;
+  ctx->est_par = gp;
+  ctx->n_est += 1;
+  cudaStream_t gs = ctx->use_side ? ctx->gs : st;
+  if (ctx->use_side) {
+    CK(cudaStreamWaitEvent(gs, ctx->ev_committed, 0));
+    CK(cudaStreamWaitEvent(gs, ctx->ev_gsum_free[gp], 0));
+  }
+  int* dl = ctx->ptr<int>(L.dlist) + static_cast<size_t>(gp) * t;
+  int* gc = ctx->ptr<int>(L.gcnt) + 4 * gp;
+  double* Gs = ctx->d(L.Gsum) + static_cast<size_t>(gp) * t * t;
+  dirty_compact_kernel<<<1, 32, 0, gs>>>(ctx->ptr<int>(L.Dsnap) + static_cast<size_t>(par) * t, t, ctx->last_est_tag, dl, gc);
   CKL();
   ctx->last_est_tag = static_cast<int>(ctx->epoch);   // newest admission tag of this state
   // A10 factors that do not need G: on the second side stream, concurrently with A9 below
@@ -1214,7 +1240,7 @@ oid_status oid_estimate_begin(oid_ctx ctx, void* stream) {
   if (s0 != OID_OK) return s0;
   CK(cudaEventRecord(ctx->ev_sj_free[par], cs2));   // S_J, S_J^+ of this parity are free again
   tl_mark(ctx, cs2, 14);
-  tl_mark(ctx, st, 8);
+  tl_mark(ctx, gs, 8);
   // A9: exact basis Gram G = A_J^T A_J, incremental: only the rows/columns of
   // slots admitted since the last estimate are recomputed, over this shard's rows.
   {
@@ -1230,28 +1256,29 @@ oid_status oid_estimate_begin(oid_ctx ctx, void* stream) {
     grid = static_cast<int>((ntiles + per - 1) / per);
     const int nbox = (t + 255) / 256;
     const int stage_bytes = (nbox * std::min(t, 256) * 128 + 1023) / 1024 * 1024;
-    const int nstage = std::max(2, std::min(bgtc::kMaxStages, (200 * 1024) / stage_bytes));
+    const int nstage = std::max(2, std::min(bgtc::kMaxStages, (ctx->bg_smem_kb * 1024) / stage_bytes));
     const size_t smem = static_cast<size_t>(nstage) * stage_bytes + 1024;
     if (f64)
-      bgtc::basis_gram_tc_kernel<double><<<grid, 32 * (bgtc::kCW + 1), smem, st>>>(
-          ctx->bg_map, ntiles, t, per, nstage, stage_bytes, nbox, ctx->ptr<int>(L.dlist), ctx->ptr<int>(L.counts),
-          ctx->d(L.Gpart));
+      bgtc::basis_gram_tc_kernel<double><<<grid, 32 * (bgtc::kCW + 1), smem, gs>>>(
+          ctx->bg_map, ntiles, t, per, nstage, stage_bytes, nbox, dl, gc, ctx->d(L.Gpart));
     else
-      bgtc::basis_gram_tc_kernel<float><<<grid, 32 * (bgtc::kCW + 1), smem, st>>>(
-          ctx->bg_map, ntiles, t, per, nstage, stage_bytes, nbox, ctx->ptr<int>(L.dlist), ctx->ptr<int>(L.counts),
-          ctx->d(L.Gpart));
+      bgtc::basis_gram_tc_kernel<float><<<grid, 32 * (bgtc::kCW + 1), smem, gs>>>(
+          ctx->bg_map, ntiles, t, per, nstage, stage_bytes, nbox, dl, gc, ctx->d(L.Gpart));
     CKL();
-    CK(cudaEventRecord(ctx->ev_gram_done, st));
-    tl_mark(ctx, st, 9);
+    CK(cudaEventRecord(ctx->ev_gram_done, gs));
+    tl_mark(ctx, gs, 9);
     // two-level fixed-order sum: up to 64 segment sums into the tail of Gpart, then one
     const int nseg = std::min(64, std::max(1, grid / 16));
     double* seg = ctx->d(L.Gpart) + static_cast<size_t>(grid) * t * t;
-    sum_dirty_chunks_kernel<<<dim3(blocks_for(int64_t(t) * t), nseg), 256, 0, st>>>(ctx->d(L.Gpart), grid, t,
-                                                                                   ctx->ptr<int>(L.counts), seg);
+    sum_dirty_chunks_kernel<<<dim3(blocks_for(int64_t(t) * t), nseg), 256, 0, gs>>>(ctx->d(L.Gpart), grid, t, gc, seg);
     CKL();
-    sum_dirty_chunks_kernel<<<dim3(blocks_for(int64_t(t) * t), 1), 256, 0, st>>>(seg, nseg, t, ctx->ptr<int>(L.counts),
-                                                                                ctx->d(L.Gsum));
+    sum_dirty_chunks_kernel<<<dim3(blocks_for(int64_t(t) * t), 1), 256, 0, gs>>>(seg, nseg, t, gc, Gs);
     CKL();
+  }
+  // the caller's stream sees the partial sums (the sharded path reduces them on it)
+  if (ctx->use_side) {
+    CK(cudaEventRecord(ctx->ev_gs_done, gs));
+    CK(cudaStreamWaitEvent(st, ctx->ev_gs_done, 0));
   }
   return OID_OK;
 }
@@ -1274,9 +1301,12 @@ oid_status oid_estimate_end(oid_ctx ctx, double* out_dev, void* stream) {
   if (s != OID_OK) return s;
   est_scalars_kernel<<<1, 1, 0, cs>>>(scal, par);
   CKL();
-  gram_scatter_kernel<<<blocks_for(int64_t(t) * t), 256, 0, cs>>>(ctx->d(L.Gsum), ctx->ptr<int>(L.dlist),
-                                                                  ctx->ptr<int>(L.counts), t, ctx->d(L.Gfull));
+  const int gp = ctx->est_par;
+  gram_scatter_kernel<<<blocks_for(int64_t(t) * t), 256, 0, cs>>>(ctx->d(L.Gsum) + static_cast<size_t>(gp) * t * t,
+                                                                  ctx->ptr<int>(L.dlist) + static_cast<size_t>(gp) * t,
+                                                                  ctx->ptr<int>(L.gcnt) + 4 * gp, t, ctx->d(L.Gfull));
   CKL();
+  CK(cudaEventRecord(ctx->ev_gsum_free[gp], cs));   // the A9 stream may reuse this parity
   CK(cudaMemcpyAsync(ctx->d(L.G), ctx->d(L.Gfull), sizeof(double) * t * t, cudaMemcpyDeviceToDevice, cs));
   mask_gram_kernel<<<blocks_for(int64_t(t) * t), 256, 0, cs>>>(ctx->d(L.G), ctx->ptr<int64_t>(L.Jsnap) + static_cast<size_t>(par) * t, t);
   CKL();
@@ -1499,7 +1529,7 @@ oid_status oid_stats_reset(oid_ctx ctx) {
 
 void oid_destroy(oid_ctx ctx) {
   if (!ctx) return;
-  for (cudaStream_t* sp : {&ctx->side, &ctx->side2})
+  for (cudaStream_t* sp : {&ctx->side, &ctx->side2, &ctx->gs})
     if (*sp) {
       cudaStreamSynchronize(*sp);
       cudaStreamDestroy(*sp);
@@ -1507,7 +1537,8 @@ void oid_destroy(oid_ctx ctx) {
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   for (cudaEvent_t ev : {ctx->ev_committed, ctx->ev_gram_done, ctx->ev_sj_j, ctx->ev_est_done, ctx->ev_sj_done[0],
-                         ctx->ev_sj_done[1], ctx->ev_sj_free[0], ctx->ev_sj_free[1], ctx->ev_snap_free[0], ctx->ev_snap_free[1]})
+                         ctx->ev_sj_done[1], ctx->ev_sj_free[0], ctx->ev_sj_free[1], ctx->ev_snap_free[0], ctx->ev_snap_free[1],
+                         ctx->ev_gs_done, ctx->ev_gsum_free[0], ctx->ev_gsum_free[1]})
     if (ev) cudaEventDestroy(ev);
   oid_stats_reset(ctx);
   delete ctx;

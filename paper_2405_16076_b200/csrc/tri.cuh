@@ -256,6 +256,17 @@ tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__
   cluster.sync();
 }
 
+// 1/x for normal x: hardware approximation refined by two Newton steps (about 1 ulp); keeps the
+// divide off the sequential LDL^T pivot chains
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double q = fma(-x, r, 1.0);
+  r = fma(r, q, r);
+  q = fma(-x, r, 1.0);
+  return fma(r, q, r);
+}
+
 // Number of eigenvalues >= x of the symmetric tridiagonal (d, e2 = e^2): n minus the number of
 // sign changes of the Sturm sequence p_{-1} = 1, p_j = (d_j - x) p_{j-1} - e_{j-1}^2 p_{j-2}
 // (e2[0] = 0; no divisions; a zero p_j takes the sign opposite to p_{j-1}).  The caller scales
@@ -359,12 +370,20 @@ __global__ void lambda_sorted_kernel(const double* __restrict__ mu, int n, int k
                                      const double* __restrict__ d, const double* __restrict__ e,
                                      double* __restrict__ ldl, int tri_ok, int frob_idx) {
   __shared__ double red[8];
+  __shared__ double mus[kTriMaxN], ds[kTriMaxN], es[kTriMaxN];   // the serial loops read shared memory
   double tr = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) tr += gram[static_cast<int64_t>(i) * n + i];   // Gram order n
-  tr = block_sum<256>(tr, red);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    tr += gram[static_cast<int64_t>(i) * n + i];   // Gram order n
+    mus[i] = mu[i];
+    ds[i] = d[i];
+    if (i < n - 1) es[i] = e[i];
+  }
+  tr = block_sum<256>(tr, red);   // (synchronises the block)
   if (threadIdx.x != 0) return;
+  d = ds;
+  e = es;
   double Ek = 0.0;
-  for (int i = 0; i < k && i < n; ++i) Ek += mu[i];
+  for (int i = 0; i < k && i < n; ++i) Ek += mus[i];
   const double frob2 = scal[frob_idx];
   double lam;
   if (lam_param >= 0.0) lam = lam_param;
@@ -381,13 +400,19 @@ __global__ void lambda_sorted_kernel(const double* __restrict__ mu, int n, int k
   gate[0] = fast;
   gate[1] = !fast;
   if (fast) {
+    // D_j >= shift > 0 (T + sI is positive definite); one reciprocal per pivot on the sequential
+    // chain, from the hardware approximation refined by two Newton steps (about 1 ulp)
+    const auto rcp = rcp_nr;
     double Dj = d[0] + shift;
-    ldl[0] = 1.0 / Dj;
+    double rj = rcp(Dj);
+    ldl[0] = rj;
     for (int j = 1; j < n; ++j) {
-      const double Lj = e[j - 1] / Dj;
+      const double ej = e[j - 1];
+      const double Lj = ej * rj;
       ldl[n + j - 1] = Lj;
-      Dj = d[j] + shift - Lj * e[j - 1];
-      ldl[j] = 1.0 / Dj;
+      Dj = fma(-Lj, ej, d[j] + shift);
+      rj = rcp(Dj);
+      ldl[j] = rj;
     }
   }
 }
@@ -565,6 +590,7 @@ __global__ void __launch_bounds__(256) tri_scores_kernel(const double* __restric
   __shared__ __align__(8) uint64_t full[kQStages];
   __shared__ double red[2][8][kRefChunk];
   __shared__ double zs[kTriMaxN];
+  __shared__ double ls[2 * kTriMaxN];   // LDL^T factors (1/D, L)
   const int tid = threadIdx.x, j = blockIdx.x;
   if (tid == 0) {
     for (int q = 0; q < kQStages; ++q) tri_mbar_init(&full[q], 1);
@@ -583,12 +609,14 @@ __global__ void __launch_bounds__(256) tri_scores_kernel(const double* __restric
 #pragma unroll
   for (int s = 0; s < 2; ++s) if (tid + 256 * s < n) zs[tid + 256 * s] = z[s];
   __syncthreads();
+  for (int i = tid; i < 2 * n - 1; i += blockDim.x) ls[i] = ldl[i];   // the chain below reads shared memory
+  __syncthreads();
   if (tid == 0) {
     double y = zs[0];
-    double acc = y * y * ldl[0];
+    double acc = y * y * ls[0];
     for (int i = 1; i < n; ++i) {
-      y = zs[i] - ldl[n + i - 1] * y;
-      acc = fma(y * y, ldl[i], acc);
+      y = zs[i] - ls[n + i - 1] * y;
+      acc = fma(y * y, ls[i], acc);
     }
     tau_out[j] = acc;
   }
@@ -609,12 +637,15 @@ __global__ void spd_gate_kernel(const double* __restrict__ mu, int n, double kma
   if (!ok) return;
   if (kappa_out) *kappa_out = sqrt(mx / mn);
   double Dj = d[0];
-  ldl[0] = 1.0 / Dj;
+  double rj = rcp_nr(Dj);   // D_j > 0: A is positive definite here
+  ldl[0] = rj;
   for (int j = 1; j < n; ++j) {
-    const double Lj = e[j - 1] / Dj;
+    const double ej = e[j - 1];
+    const double Lj = ej * rj;
     ldl[n + j - 1] = Lj;
-    Dj = d[j] - Lj * e[j - 1];
-    ldl[j] = 1.0 / Dj;
+    Dj = fma(-Lj, ej, d[j]);
+    rj = rcp_nr(Dj);
+    ldl[j] = rj;
   }
 }
 
@@ -632,6 +663,7 @@ __global__ void __launch_bounds__(256) tri_solve_kernel(const double* __restrict
   __shared__ __align__(8) uint64_t full[kQStages];
   __shared__ double red[2][8][kRefChunk];
   __shared__ double zs[kTriMaxN];
+  __shared__ double ls[2 * kTriMaxN];   // LDL^T factors (1/D, L)
   const int tid = threadIdx.x, c = blockIdx.x;
   if (tid == 0) {
     for (int q = 0; q < kQStages; ++q) tri_mbar_init(&full[q], 1);
@@ -650,10 +682,14 @@ __global__ void __launch_bounds__(256) tri_solve_kernel(const double* __restrict
 #pragma unroll
   for (int s = 0; s < 2; ++s) if (tid + 256 * s < n) zs[tid + 256 * s] = z[s];
   __syncthreads();
+  for (int i = tid; i < 2 * n - 1; i += blockDim.x) ls[i] = ldl[i];   // the chains below read shared memory
+  __syncthreads();
   if (tid == 0) {                                                            // T u = z by LDL^T
-    for (int i = 1; i < n; ++i) zs[i] -= ldl[n + i - 1] * zs[i - 1];
-    for (int i = 0; i < n; ++i) zs[i] *= ldl[i];
-    for (int i = n - 2; i >= 0; --i) zs[i] -= ldl[n + i] * zs[i + 1];
+    double y = zs[0];
+    for (int i = 1; i < n; ++i) { y = zs[i] - ls[n + i - 1] * y; zs[i] = y; }
+    for (int i = 0; i < n; ++i) zs[i] *= ls[i];
+    y = zs[n - 1];
+    for (int i = n - 2; i >= 0; --i) { y = zs[i] - ls[n + i] * y; zs[i] = y; }
   }
   __syncthreads();
 #pragma unroll

@@ -38,7 +38,7 @@ torch.cuda.synchronize()
 tl = eng.get(13)
 names = {1: "K1 start", 2: "K1 end", 3: "commit start", 4: "post chain end", 5: "copy start", 6: "copy end",
          11: "S_J chain start (side)", 12: "S_J chain end (side)", 7: "est begin (E)", 13: "est_pre start (side)",
-         14: "est_pre end (side)", 8: "Gram start (E)", 9: "Gram end (E)", 10: "est end (E)"}
+         14: "est_pre end (side)", 15: "  tridiag end", 16: "  tri_scores end", 8: "Gram start (E)", 9: "Gram end (E)", 10: "est end (E)"}
 rows = [(int(t), ms) for t, ms in tl if t >= 0]
 for t, ms in rows:
     print(f"{ms:9.3f}  {names.get(t, t)}")
