@@ -316,6 +316,7 @@ struct oid_ctx_s {
   int bg_free_sms = 0;        // SMs the A9 kernel leaves free (diagnostics: OID_BG_FREE)
   int bg_waves = 32;          // A9 CTAs per SM (short CTAs; diagnostics: OID_BG_WAVES)
   int bg_smem_kb = 200;       // A9 ring budget (diagnostics: OID_BG_SMEM)
+  int gs_gate = 0;            // A9 also waits for the epoch's A8 chain (diagnostics: OID_GS_GATE)
   bool use_side = true;       // diagnostics: OID_NO_SIDE=1 runs everything on the caller's stream
   int k1_free_sms = 0;        // SMs the persistent K1 grid leaves to concurrent streams (OID_K1_FREE)
   bool timeline = false;      // diagnostics: OID_TIMELINE=1 records tagged events (oid_get 13)
@@ -1083,6 +1084,7 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
       if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess) return bad(e);
     if (getenv("OID_BG_FREE")) ctx->bg_free_sms = std::max(0, atoi(getenv("OID_BG_FREE")));
     if (getenv("OID_BG_WAVES")) ctx->bg_waves = std::max(1, atoi(getenv("OID_BG_WAVES")));
+    if (getenv("OID_GS_GATE")) ctx->gs_gate = atoi(getenv("OID_GS_GATE"));
     if (getenv("OID_BG_SMEM")) ctx->bg_smem_kb = std::min(200, std::max(8, atoi(getenv("OID_BG_SMEM"))));
     ctx->use_side = !(getenv("OID_NO_SIDE") && atoi(getenv("OID_NO_SIDE")) != 0);
     if (getenv("OID_K1_FREE")) ctx->k1_free_sms = std::max(0, atoi(getenv("OID_K1_FREE")));
@@ -1223,6 +1225,7 @@ oid_status oid_estimate_begin(oid_ctx ctx, void* stream) {
   if (ctx->use_side) {
     CK(cudaStreamWaitEvent(gs, ctx->ev_committed, 0));
     CK(cudaStreamWaitEvent(gs, ctx->ev_gsum_free[gp], 0));
+    if (ctx->gs_gate) CK(cudaStreamWaitEvent(gs, ctx->ev_sj_done[par], 0));
   }
   int* dl = ctx->ptr<int>(L.dlist) + static_cast<size_t>(gp) * t;
   int* gc = ctx->ptr<int>(L.gcnt) + 4 * gp;

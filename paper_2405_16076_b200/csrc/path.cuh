@@ -207,7 +207,22 @@ __global__ void basis_copy_kernel(const T* __restrict__ X, int64_t ld, T* __rest
     else slot = admit[2 * (nc + t) - 2 - 2 * (a - na)];
     const T* src = r >= 0 ? X + static_cast<int64_t>(r) * ld : nullptr;
     if (vec) {
-      for (int64_t v = tid; v < m_loc / V; v += stride) {
+      // four independent 16-byte loads in flight per thread before their stores
+      constexpr int U = 4;
+      const int64_t nv = m_loc / V;
+      int64_t v = tid;
+      for (; v + (U - 1) * stride < nv; v += U * stride) {
+        uint4 x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          x[u] = src ? __ldcs(reinterpret_cast<const uint4*>(src + (v + u * stride) * V)) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t i = (v + u * stride) * V;
+          __stcs(reinterpret_cast<uint4*>(Cb + ((i / RL) * t + slot) * RL + (i % RL)), x[u]);
+        }
+      }
+      for (; v < nv; v += stride) {
         const int64_t i = v * V;
         const uint4 x = src ? __ldcs(reinterpret_cast<const uint4*>(src + i)) : make_uint4(0u, 0u, 0u, 0u);
         __stcs(reinterpret_cast<uint4*>(Cb + ((i / RL) * t + slot) * RL + (i % RL)), x);
