@@ -316,6 +316,7 @@ struct oid_ctx_s {
   int bg_free_sms = 0;        // SMs the A9 kernel leaves free (diagnostics: OID_BG_FREE)
   int bg_waves = 32;          // A9 CTAs per SM (short CTAs; diagnostics: OID_BG_WAVES)
   int bg_smem_kb = 200;       // A9 ring budget (diagnostics: OID_BG_SMEM)
+  int bg_cluster = 1;         // A9 CTAs per cluster: whole groups of SMs retire together (OID_BG_CLUSTER)
   int gs_gate = 0;            // A9 also waits for the epoch's A8 chain (diagnostics: OID_GS_GATE)
   bool use_side = true;       // diagnostics: OID_NO_SIDE=1 runs everything on the caller's stream
   int k1_free_sms = 0;        // SMs the persistent K1 grid leaves to concurrent streams (OID_K1_FREE)
@@ -1085,6 +1086,10 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
     if (getenv("OID_BG_FREE")) ctx->bg_free_sms = std::max(0, atoi(getenv("OID_BG_FREE")));
     if (getenv("OID_BG_WAVES")) ctx->bg_waves = std::max(1, atoi(getenv("OID_BG_WAVES")));
     if (getenv("OID_GS_GATE")) ctx->gs_gate = atoi(getenv("OID_GS_GATE"));
+    if (getenv("OID_BG_CLUSTER")) {
+      const int v = atoi(getenv("OID_BG_CLUSTER"));
+      ctx->bg_cluster = (v == 2 || v == 4 || v == 8 || v == 16) ? v : 1;
+    }
     if (getenv("OID_BG_SMEM")) ctx->bg_smem_kb = std::min(200, std::max(8, atoi(getenv("OID_BG_SMEM"))));
     ctx->use_side = !(getenv("OID_NO_SIDE") && atoi(getenv("OID_NO_SIDE")) != 0);
     if (getenv("OID_K1_FREE")) ctx->k1_free_sms = std::max(0, atoi(getenv("OID_K1_FREE")));
@@ -1124,6 +1129,8 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
     const int bgmax = 200 * 1024 + 1024;
     if ((e = cudaFuncSetAttribute(bgtc::basis_gram_tc_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, bgmax)) != cudaSuccess) return bad(e);
     if ((e = cudaFuncSetAttribute(bgtc::basis_gram_tc_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, bgmax)) != cudaSuccess) return bad(e);
+    if ((e = cudaFuncSetAttribute(bgtc::basis_gram_tc_kernel<double>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess) return bad(e);
+    if ((e = cudaFuncSetAttribute(bgtc::basis_gram_tc_kernel<float>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess) return bad(e);
   }
   double qd[16];
   for (int i = 0; i < 16; ++i) qd[i] = q[i] + 0.5;
@@ -1253,20 +1260,37 @@ oid_status oid_estimate_begin(oid_ctx ctx, void* stream) {
     // many short CTAs (waves of num_sms - bg_free_sms): kernels of higher-priority streams (the next
     // block's K1 and post-pass, the side stream) are scheduled as they retire
     const int sms = std::max(1, ctx->num_sms - ctx->bg_free_sms);
-    const int want = std::min(gram_tc_chunks(t), sms * ctx->bg_waves);
+    const int cl = ctx->bg_cluster;   // CTAs per cluster (1: plain launch)
+    int want = std::min(gram_tc_chunks(t), sms * ctx->bg_waves);
+    want = std::max(cl, want / cl * cl);
     int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, (ntiles + 7) / 8)));
     const int64_t per = (ntiles + grid - 1) / grid;
     grid = static_cast<int>((ntiles + per - 1) / per);
+    grid = (grid + cl - 1) / cl * cl;   // CTAs past the last tile contribute zero partials
     const int nbox = (t + 255) / 256;
     const int stage_bytes = (nbox * std::min(t, 256) * 128 + 1023) / 1024 * 1024;
     const int nstage = std::max(2, std::min(bgtc::kMaxStages, (ctx->bg_smem_kb * 1024) / stage_bytes));
     const size_t smem = static_cast<size_t>(nstage) * stage_bytes + 1024;
+    cudaLaunchConfig_t lc = {};
+    cudaLaunchAttribute la[1];
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(32 * (bgtc::kCW + 1));
+    lc.dynamicSmemBytes = smem;
+    lc.stream = gs;
+    if (cl > 1) {
+      la[0].id = cudaLaunchAttributeClusterDimension;
+      la[0].val.clusterDim.x = cl;
+      la[0].val.clusterDim.y = 1;
+      la[0].val.clusterDim.z = 1;
+      lc.attrs = la;
+      lc.numAttrs = 1;
+    }
     if (f64)
-      bgtc::basis_gram_tc_kernel<double><<<grid, 32 * (bgtc::kCW + 1), smem, gs>>>(
-          ctx->bg_map, ntiles, t, per, nstage, stage_bytes, nbox, dl, gc, ctx->d(L.Gpart));
+      CK(cudaLaunchKernelEx(&lc, bgtc::basis_gram_tc_kernel<double>, ctx->bg_map, ntiles, t, per, nstage, stage_bytes,
+                            nbox, static_cast<const int*>(dl), static_cast<const int*>(gc), ctx->d(L.Gpart)));
     else
-      bgtc::basis_gram_tc_kernel<float><<<grid, 32 * (bgtc::kCW + 1), smem, gs>>>(
-          ctx->bg_map, ntiles, t, per, nstage, stage_bytes, nbox, dl, gc, ctx->d(L.Gpart));
+      CK(cudaLaunchKernelEx(&lc, bgtc::basis_gram_tc_kernel<float>, ctx->bg_map, ntiles, t, per, nstage, stage_bytes,
+                            nbox, static_cast<const int*>(dl), static_cast<const int*>(gc), ctx->d(L.Gpart)));
     CKL();
     CK(cudaEventRecord(ctx->ev_gram_done, gs));
     tl_mark(ctx, gs, 9);
