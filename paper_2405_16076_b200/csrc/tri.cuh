@@ -40,6 +40,28 @@ __host__ __device__ constexpr int tri_rows(int n) { return 2 * ((n + 2 * kTriCta
 // leading dimension of the reflector matrix Vh (even, so every column start is 16-byte aligned)
 __host__ __device__ constexpr int tri_ldv(int n) { return (n + 1) & ~1; }
 
+// 1/x for normal x: hardware approximation refined by two Newton steps (about 1 ulp); keeps the
+// divide off the sequential LDL^T pivot chains
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double q = fma(-x, r, 1.0);
+  r = fma(r, q, r);
+  q = fma(-x, r, 1.0);
+  return fma(r, q, r);
+}
+
+// column block q of all kTriRW rows, q warp-uniform: one indexed branch instead of a select chain
+__device__ __forceinline__ void tri_pick_rows(const double (&a)[kTriRW][kTriCL], int q, double (&x)[kTriRW]) {
+  switch (q) {
+#define TRI_CASE(Q) \
+  case Q: { _Pragma("unroll") for (int r = 0; r < kTriRW; ++r) x[r] = a[r][Q]; } break;
+    TRI_CASE(0) TRI_CASE(1) TRI_CASE(2) TRI_CASE(3) TRI_CASE(4) TRI_CASE(5) TRI_CASE(6) TRI_CASE(7)
+    TRI_CASE(8) TRI_CASE(9) TRI_CASE(10) TRI_CASE(11) TRI_CASE(12) TRI_CASE(13) TRI_CASE(14)
+    default: { _Pragma("unroll") for (int r = 0; r < kTriRW; ++r) x[r] = a[r][15]; } break;
+#undef TRI_CASE
+  }
+}
 __device__ __forceinline__ double tri_pick(const double (&a)[kTriCL], int q) {
   double x = 0.0;
 #pragma unroll
@@ -117,6 +139,11 @@ tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__
   const int hp = R >> 1;                          // v2 stores per slice
   const int tq = hp > 0 ? tid / hp : 0, tu = hp > 0 ? tid - tq * hp : 0;
   const bool sender = hp > 0 && tq < kTriCtas;
+  // entries past the senders' slices (rows >= kTriCtas R) are never pushed: keep them zero, so the
+  // unmasked products below see v_j = p_j = 0 there
+  for (int i = kTriCtas * R + tid; i < kTriCtas * kTriRows; i += blockDim.x) {
+    xb[0][i] = 0.0; xb[1][i] = 0.0; pb[0][i] = 0.0; pb[1][i] = 0.0;
+  }
   cluster.sync();                                 // mbarrier inits visible cluster-wide
   const bool rec = dbg != nullptr && c == 0 && tid == 0;   // diagnostics: phase timestamps of CTA 0
   for (int k = 0; k < n - 2; ++k) {
@@ -128,9 +155,11 @@ tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__
     if (tid == 0) { tri_mbar_expect(&barx[buf], phase_bytes); tri_mbar_expect(&barp[buf], phase_bytes); }
     // phase 1: x_i = A(i, k) for my rows i > k -> every CTA, with the partial sum of squares
     double ssw = 0.0;
+    double colk[kTriRW];
+    tri_pick_rows(a, qk, colk);
 #pragma unroll
     for (int r = 0; r < kTriRW; ++r) {
-      const double xi = __shfl_sync(0xffffffffu, tri_pick(a[r], qk), lk);
+      const double xi = __shfl_sync(0xffffffffu, colk[r], lk);
       if (gi[r] > k) { ssw = fma(xi, xi, ssw); if (lane == 0) locx[gi[r] - r0] = xi; }
       else if (lane == 0 && warp * kTriRW + r < R) locx[warp * kTriRW + r] = 0.0;
     }
@@ -157,7 +186,7 @@ tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__
     if (tail > 0.0) {
       alpha = -copysign(sqrt(ss), x0);
       v0 = x0 - alpha;
-      tau = 2.0 / (tail + v0 * v0);
+      tau = 2.0 * rcp_nr(tail + v0 * v0);
     } else {
       alpha = x0;
     }
@@ -172,11 +201,14 @@ tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__
       vi[r] = (gi[r] > k) ? (gi[r] == k + 1 ? v0 : xk[gi[r]]) : 0.0;
       pi[r] = 0.0;
     }
+    // The received slices are zero at rows <= k and past n (the senders zero them), so
+    // v_j = x_j except v_{k+1} = v0, and w_j = p_j - h v_j needs no masks either: the stale
+    // entries of A in finished rows / columns only ever meet zeros.
     if (tau != 0.0) {
 #pragma unroll
       for (int q = 0; q < kTriCL; ++q) {
         const int j = lane + 32 * q;
-        const double vj = (j > k && j < n) ? (j == k + 1 ? v0 : xk[j]) : 0.0;
+        const double vj = j == k + 1 ? v0 : xk[j];
 #pragma unroll
         for (int r = 0; r < kTriRW; ++r) pi[r] = fma(a[r][q], vj, pi[r]);
       }
@@ -218,9 +250,8 @@ tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__
 #pragma unroll
       for (int q = 0; q < kTriCL; ++q) {
         const int j = lane + 32 * q;
-        const bool act = j > k && j < n;
-        const double vj = act ? (j == k + 1 ? v0 : xk[j]) : 0.0;
-        const double wj = act ? pk[j] - h * vj : 0.0;
+        const double vj = j == k + 1 ? v0 : xk[j];
+        const double wj = pk[j] - h * vj;
 #pragma unroll
         for (int r = 0; r < kTriRW; ++r) a[r][q] = a[r][q] - vi[r] * wj - wi[r] * vj;
       }
@@ -256,16 +287,6 @@ tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__
   cluster.sync();
 }
 
-// 1/x for normal x: hardware approximation refined by two Newton steps (about 1 ulp); keeps the
-// divide off the sequential LDL^T pivot chains
-__device__ __forceinline__ double rcp_nr(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double q = fma(-x, r, 1.0);
-  r = fma(r, q, r);
-  q = fma(-x, r, 1.0);
-  return fma(r, q, r);
-}
 
 // Number of eigenvalues >= x of the symmetric tridiagonal (d, e2 = e^2): n minus the number of
 // sign changes of the Sturm sequence p_{-1} = 1, p_j = (d_j - x) p_{j-1} - e_{j-1}^2 p_{j-2}
