@@ -162,6 +162,7 @@ tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__
       const double xi = __shfl_sync(0xffffffffu, colk[r], lk);
       if (gi[r] > k) { ssw = fma(xi, xi, ssw); if (lane == 0) locx[gi[r] - r0] = xi; }
       else if (lane == 0 && warp * kTriRW + r < R) locx[warp * kTriRW + r] = 0.0;
+      if (gi[r] == k && lane == 0) d_s[k] = xi;   // the diagonal entry A(k, k)
     }
     if (lane == 0) wred[warp] = ssw;
     __syncthreads();
@@ -190,10 +191,7 @@ tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__
     } else {
       alpha = x0;
     }
-    if (tid == 0) tau_s[k] = tau;
-#pragma unroll
-    for (int r = 0; r < kTriRW; ++r)
-      if (gi[r] == k && lane == lk) { d_s[k] = tri_pick(a[r], qk); e_s[k] = alpha; }
+    if (tid == 0) { tau_s[k] = tau; e_s[k] = alpha; }
     // v_i for my rows; p_i = tau sum_j A_ij v_j
     double vi[kTriRW], pi[kTriRW];
 #pragma unroll
@@ -205,13 +203,21 @@ tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__
     // v_j = x_j except v_{k+1} = v0, and w_j = p_j - h v_j needs no masks either: the stale
     // entries of A in finished rows / columns only ever meet zeros.
     if (tau != 0.0) {
+      double p2[kTriRW];   // second accumulator per row (odd column blocks): half the FMA chain
+#pragma unroll
+      for (int r = 0; r < kTriRW; ++r) p2[r] = 0.0;
 #pragma unroll
       for (int q = 0; q < kTriCL; ++q) {
         const int j = lane + 32 * q;
         const double vj = j == k + 1 ? v0 : xk[j];
 #pragma unroll
-        for (int r = 0; r < kTriRW; ++r) pi[r] = fma(a[r][q], vj, pi[r]);
+        for (int r = 0; r < kTriRW; ++r) {
+          if (q & 1) p2[r] = fma(a[r][q], vj, p2[r]);
+          else pi[r] = fma(a[r][q], vj, pi[r]);
+        }
       }
+#pragma unroll
+      for (int r = 0; r < kTriRW; ++r) pi[r] += p2[r];
     }
     double kw = 0.0;
 #pragma unroll
