@@ -668,8 +668,8 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
     lambda_sorted_kernel<<<1, 256, 0, st>>>(ctx->d(L.mu), ng, p.k, ctx->d(L.gram), p.lambda, ell, scal, gate,
                                             ctx->d(L.td), ctx->d(L.te), ctx->d(L.ldl), 1, frob_idx);
     CKL();
-    tri_scores_kernel<<<ns, 256, sizeof(double) * kQStages * kRefChunk * tri_ldv(ng), st>>>(ctx->d(L.Yc), ng, ns, ctx->d(L.Vh), ctx->d(L.wyT), ctx->d(L.ldl), gate,
-                                          ctx->d(L.tau));
+    tri_scores_multi_kernel<<<(ns + kQV - 1) / kQV, 256, sizeof(double) * kQStages * kRefChunk * tri_ldv(ng), st>>>(
+        ctx->d(L.Yc), ng, ns, ctx->d(L.Vh), ctx->d(L.wyT), ctx->d(L.ldl), gate, ctx->d(L.tau));
     CKL();
     tl_mark(ctx, st, 16);
     const int* g1 = gate + 1;
@@ -1054,6 +1054,8 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
       return bad(e);
     const int ref_smem = static_cast<int>(sizeof(double) * kQStages * kRefChunk * tri_ldv(kTriMaxN));
     if ((e = cudaFuncSetAttribute(tri_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ref_smem)) != cudaSuccess)
+      return bad(e);
+    if ((e = cudaFuncSetAttribute(tri_scores_multi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ref_smem)) != cudaSuccess)
       return bad(e);
     if ((e = cudaFuncSetAttribute(tri_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ref_smem)) != cudaSuccess)
       return bad(e);

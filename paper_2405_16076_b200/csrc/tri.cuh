@@ -605,6 +605,141 @@ __device__ __forceinline__ void cta_apply_q(double (&z)[2], int n, const double*
   __syncthreads();                        // red / ring reuse by a following call
 }
 
+// z_v <- Q^T z_v for kQV vectors at once (the reflector chunks are read once per CTA for all of
+// them).  Per chunk: the 8 kQV partial dot products of each thread are reduced over the warp by a
+// butterfly reduce-scatter (lane l ends with value l: 31 shuffles instead of 5 per value), over
+// the warps through shared memory; warp 0 forms u = T^T w (one (vector, column) per lane) and
+// every thread applies z -= V u.
+constexpr int kQV = 4;   // vectors per CTA (kQV * kRefChunk == 32: one reduced value per lane)
+static_assert(kQV * kRefChunk == 32, "one reduced value per lane");
+__device__ __forceinline__ void cta_apply_qt_multi(double (&z)[kQV][2], int n, const double* __restrict__ Vh,
+                                                   const double* __restrict__ wyT, double* vring, double* tring,
+                                                   uint64_t* full, double (*redm)[8][32], double* us) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nk = n - 2, ldv = tri_ldv(n);
+  if (nk <= 0) return;
+  const int nch = (nk + kRefChunk - 1) / kRefChunk;
+  auto issue = [&](int b) {        // thread 0 only
+    const int k0 = b * kRefChunk, k0e = k0 & ~1;
+    const int nr = min(kRefChunk, nk - k0);
+    const int st = b % kQStages;
+    const uint32_t row_bytes = static_cast<uint32_t>(ldv - k0e) * 8u;
+    tri_mbar_expect(&full[st], static_cast<uint32_t>(nr) * row_bytes + 64u * 8u);
+    q_bulk(tring + st * 64, wyT + b * 64, 64u * 8u, &full[st]);
+    for (int r = 0; r < nr; ++r)
+      q_bulk(vring + (static_cast<size_t>(st) * kRefChunk + r) * ldv + k0e, Vh + static_cast<int64_t>(k0 + r) * ldv + k0e,
+             row_bytes, &full[st]);
+  };
+  if (tid == 0) {
+    issue(0);
+    if (nch > 1) issue(1);
+  }
+  for (int it = 0; it < nch; ++it) {
+    const int k0 = it * kRefChunk;
+    const int nr = min(kRefChunk, nk - k0);
+    const int st = it % kQStages;
+    tri_mbar_wait(&full[st], (it / kQStages) & 1);
+    const double* vb = vring + static_cast<size_t>(st) * kRefChunk * ldv;
+    double v[kRefChunk][2];
+#pragma unroll
+    for (int r = 0; r < kRefChunk; ++r)
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int i = tid + 256 * s;
+        v[r][s] = (r < nr && i > k0 && i < n) ? vb[r * ldv + i] : 0.0;   // rows <= k0 are zero in V
+      }
+    double val[32];
+#pragma unroll
+    for (int q = 0; q < kQV; ++q)
+#pragma unroll
+      for (int r = 0; r < kRefChunk; ++r) val[q * kRefChunk + r] = fma(v[r][1], z[q][1], v[r][0] * z[q][0]);
+#pragma unroll
+    for (int half = 16; half > 0; half >>= 1) {
+      const bool hi = (lane & half) != 0;
+#pragma unroll
+      for (int i = 0; i < half; ++i) {
+        const double send = hi ? val[i] : val[i + half];
+        const double keep = hi ? val[i + half] : val[i];
+        val[i] = keep + __shfl_xor_sync(0xffffffffu, send, half);
+      }
+    }
+    redm[it & 1][warp][lane] = val[0];   // warp sum of value `lane` = (vector lane / 8, row lane % 8)
+    __syncthreads();                     // V_it in registers, redm complete; stage (it - 1) % 3 free
+    if (tid == 0 && it + 2 < nch) issue(it + 2);
+    if (warp == 0) {
+      double w = 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) w += redm[it & 1][q][lane];
+      const int c = lane & (kRefChunk - 1), base = lane & ~(kRefChunk - 1);
+      const double* T = tring + st * 64;
+      double u = 0.0;
+#pragma unroll
+      for (int r = 0; r < kRefChunk; ++r) {
+        const double wr = __shfl_sync(0xffffffffu, w, base + r);
+        if (r <= c) u = fma(T[r * kRefChunk + c], wr, u);   // (T^T w)_c
+      }
+      us[(it & 1) * 32 + lane] = u;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kQV; ++q)
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        double zi = z[q][s];
+#pragma unroll
+        for (int r = 0; r < kRefChunk; ++r) zi = fma(-v[r][s], us[(it & 1) * 32 + q * kRefChunk + r], zi);
+        z[q][s] = zi;
+      }
+  }
+  __syncthreads();
+}
+
+// tau for kQV columns of Yc per CTA (see tri_scores_kernel); the LDL^T chains run on kQV threads.
+__global__ void __launch_bounds__(256) tri_scores_multi_kernel(const double* __restrict__ Yc, int n, int ncol,
+                                                               const double* __restrict__ Vh, const double* __restrict__ wyT,
+                                                               const double* __restrict__ ldl, const int* __restrict__ gate,
+                                                               double* __restrict__ tau_out) {
+  if (gate[0] == 0) return;
+  extern __shared__ __align__(16) double ref_smem[];
+  __shared__ __align__(16) double tsm[kQStages * 64];
+  __shared__ __align__(8) uint64_t full[kQStages];
+  __shared__ double redm[2][8][32];
+  __shared__ double us[64];
+  __shared__ double zs[kQV][kTriMaxN];
+  __shared__ double ls[2 * kTriMaxN];
+  const int tid = threadIdx.x, j0 = blockIdx.x * kQV;
+  if (tid == 0) {
+    for (int q = 0; q < kQStages; ++q) tri_mbar_init(&full[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  double z[kQV][2];
+#pragma unroll
+  for (int q = 0; q < kQV; ++q)
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int i = tid + 256 * s;
+      z[q][s] = (i < n && j0 + q < ncol) ? Yc[static_cast<int64_t>(j0 + q) * n + i] : 0.0;
+    }
+  __syncthreads();
+  cta_apply_qt_multi(z, n, Vh, wyT, ref_smem, tsm, full, redm, us);
+#pragma unroll
+  for (int q = 0; q < kQV; ++q)
+#pragma unroll
+    for (int s = 0; s < 2; ++s) if (tid + 256 * s < n) zs[q][tid + 256 * s] = z[q][s];
+  for (int i = tid; i < 2 * n - 1; i += blockDim.x) ls[i] = ldl[i];
+  __syncthreads();
+  if (tid < kQV && j0 + tid < ncol) {
+    const double* zq = zs[tid];
+    double y = zq[0];
+    double acc = y * y * ls[0];
+    for (int i = 1; i < n; ++i) {
+      y = zq[i] - ls[n + i - 1] * y;
+      acc = fma(y * y, ls[i], acc);
+    }
+    tau_out[j0 + tid] = acc;
+  }
+}
+
 // tau(y) = z^T (T + sI)^-1 z, z = Q^T y = H_{n-3} ... H_0 y; y = column j of Yc (ell x ncol).
 // One column per CTA; runs when gate[0] != 0.  Dynamic smem: kQStages kRefChunk tri_ldv(n) doubles.
 __global__ void __launch_bounds__(256) tri_scores_kernel(const double* __restrict__ Yc, int n, int ncol,
