@@ -423,14 +423,11 @@ oid_status spd_solve(oid_ctx ctx, cudaStream_t st, const double* A, int n, const
   const Layout& L = ctx->L;   // second tridiagonal workspace (td2 ...)
   const size_t smem = sizeof(double) * static_cast<size_t>(n) * tri_rows(n);
   tridiag_cluster_kernel<<<kTriCtas, 256, smem, st>>>(A, n, ctx->d(L.td2), ctx->d(L.te2), ctx->d(L.Vh2), ctx->d(L.tauv2),
-                                                      nullptr);
+                                                      nullptr, ctx->d(L.wyT2));
   CKL();
-  if (n > 2) {
-    wy_t_kernel<<<(n - 2 + kRefChunk - 1) / kRefChunk, 256, 0, st>>>(ctx->d(L.Vh2), ctx->d(L.tauv2), n, ctx->d(L.wyT2));
-    CKL();
-  }
-  multisect_kernel<<<(n * 32 + 255) / 256, 256, sizeof(double) * multisect_smem_doubles(n), st>>>(ctx->d(L.td2), ctx->d(L.te2), n,
-                                                                            ctx->d(L.mu2));
+  // the SPD gate needs only the extreme eigenvalues
+  multisect_kernel<<<1, 64, sizeof(double) * multisect_smem_doubles(n), st>>>(ctx->d(L.td2), ctx->d(L.te2), n,
+                                                                            ctx->d(L.mu2), 1, 1);
   CKL();
   spd_gate_kernel<<<1, 32, 0, st>>>(ctx->d(L.mu2), n, kmax2, ctx->d(L.td2), ctx->d(L.te2), ctx->d(L.ldl2), gate,
                                     kappa_out);
@@ -655,15 +652,14 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
     // tridiagonal fast path (tri.cuh); the eigenvector path below runs only when gate[1] is set
     const size_t smem = sizeof(double) * static_cast<size_t>(ng) * tri_rows(ng);
     tridiag_cluster_kernel<<<kTriCtas, 256, smem, st>>>(ctx->d(L.gram), ng, ctx->d(L.td), ctx->d(L.te), ctx->d(L.Vh),
-                                                        ctx->d(L.tauv), ctx->k1_debug ? ctx->ptr<long long>(L.dbg) + k1tc::kDbgRows * k1tc::kDbgTiles : nullptr);
+                                                        ctx->d(L.tauv), ctx->k1_debug ? ctx->ptr<long long>(L.dbg) + k1tc::kDbgRows * k1tc::kDbgTiles : nullptr,
+                                                        ctx->d(L.wyT));   // the compact-WY T factors too
     CKL();
     tl_mark(ctx, st, 15);
-    if (ng > 2) {
-      wy_t_kernel<<<(ng - 2 + kRefChunk - 1) / kRefChunk, 256, 0, st>>>(ctx->d(L.Vh), ctx->d(L.tauv), ng, ctx->d(L.wyT));
-      CKL();
-    }
-    multisect_kernel<<<(ng * 32 + 255) / 256, 256, sizeof(double) * multisect_smem_doubles(ng), st>>>(ctx->d(L.td), ctx->d(L.te), ng,
-                                                                                  ctx->d(L.mu));
+    // lambda needs E_k (the k largest) and mu_0 only
+    const int nev = std::min(p.k, ng);
+    multisect_kernel<<<(nev * 32 + 255) / 256, 256, sizeof(double) * multisect_smem_doubles(ng), st>>>(
+        ctx->d(L.td), ctx->d(L.te), ng, ctx->d(L.mu), nev, 0);
     CKL();
     lambda_sorted_kernel<<<1, 256, 0, st>>>(ctx->d(L.mu), ng, p.k, ctx->d(L.gram), p.lambda, ell, scal, gate,
                                             ctx->d(L.td), ctx->d(L.te), ctx->d(L.ldl), 1, frob_idx);

@@ -100,9 +100,67 @@ __device__ __forceinline__ void tri_mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Compact-WY form of the reflectors in chunks of kRefChunk: for chunk b (k = 8b .. 8b+7, k < n-2)
+// H_{8b} H_{8b+1} ... H_{8b+7} = I - V_b T_b V_b^T with T_b upper triangular (LAPACK larft,
+// forward columnwise: T(i,i) = tau_i, T(0:i, i) = -tau_i T(0:i, 0:i) V(:, 0:i)^T v_i).  One CTA per
+// chunk; T_b row-major in wyT[64 b ..].  Reflectors with tau = 0 give zero rows/columns.
+constexpr int kRefChunk = 8;
+constexpr int kMaxRefChunks = (kTriMaxN + kRefChunk - 1) / kRefChunk;
+constexpr int kQStages = 3;
+// T factor of reflector chunk b (256 threads; G: 8 x 8 shared scratch); tau from tau_src.
+__device__ __forceinline__ void wy_t_chunk(int b, const double* __restrict__ Vh, const double* tau_src, int n,
+                                           double* __restrict__ wyT, double (*G)[kRefChunk]) {
+  const int k0 = b * kRefChunk, nk = n - 2, ldv = tri_ldv(n);
+  const int nr = min(kRefChunk, nk - k0);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // V^T V, pairs r < c (28), one warp per pair, fixed-order shuffle reduction
+  for (int pr = w; pr < kRefChunk * (kRefChunk - 1) / 2; pr += 8) {
+    int r = 0, rem = pr;
+    while (rem >= kRefChunk - 1 - r) { rem -= kRefChunk - 1 - r; ++r; }
+    const int c = r + 1 + rem;
+    double acc = 0.0;
+    if (c < nr) {
+      const double* vr = Vh + static_cast<int64_t>(k0 + r) * ldv;
+      const double* vc = Vh + static_cast<int64_t>(k0 + c) * ldv;
+      for (int i = k0 + 1 + lane; i < n; i += 32) acc = fma(__ldcg(vr + i), __ldcg(vc + i), acc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) G[r][c] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double T[kRefChunk][kRefChunk];
+#pragma unroll
+    for (int r = 0; r < kRefChunk; ++r)
+#pragma unroll
+      for (int c = 0; c < kRefChunk; ++c) T[r][c] = 0.0;
+#pragma unroll
+    for (int c = 0; c < kRefChunk; ++c) {
+      if (c < nr) {
+        const double tc = tau_src[k0 + c];
+        T[c][c] = tc;
+#pragma unroll
+        for (int r = 0; r < c; ++r) {
+          double acc = 0.0;
+#pragma unroll
+          for (int q = r; q < c; ++q) acc = fma(T[r][q], G[q][c], acc);
+          T[r][c] = -tc * acc;
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kRefChunk; ++r)
+#pragma unroll
+      for (int c = 0; c < kRefChunk; ++c) wyT[b * kRefChunk * kRefChunk + r * kRefChunk + c] = T[r][c];
+  }
+  __syncthreads();   // G reused by the next chunk
+}
+
 __global__ void __cluster_dims__(kTriCtas, 1, 1) __launch_bounds__(256, 1)
 tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__ d, double* __restrict__ e,
-                       double* __restrict__ Vh, double* __restrict__ tauv, long long* __restrict__ dbg) {
+                       double* __restrict__ Vh, double* __restrict__ tauv, long long* __restrict__ dbg,
+                       double* __restrict__ wyT) {
   cg2::cluster_group cluster = cg2::this_cluster();
   const int c = static_cast<int>(cluster.block_rank());
   const int R = tri_rows(n);
@@ -290,7 +348,13 @@ tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__
     if (c == 0 && k < n - 2) tauv[k] = tau_s[k];
     if (k >= r0 && k < r1) { d[k] = d_s[k]; if (k < n - 1) e[k] = e_s[k]; }
   }
-  cluster.sync();
+  cluster.sync();   // also: every CTA's Vh rows are visible to the whole cluster (global memory)
+  // compact-WY T factors of the reflector chunks, chunk b on CTA b mod 16 (wy_t_kernel fused)
+  if (wyT != nullptr && n > 2) {
+    __shared__ double G[kRefChunk][kRefChunk];
+    const int nch = (n - 2 + kRefChunk - 1) / kRefChunk;
+    for (int b = c; b < nch; b += kTriCtas) wy_t_chunk(b, Vh, tau_s, n, wyT, G);
+  }
 }
 
 
@@ -336,8 +400,9 @@ __device__ __forceinline__ int sturm_count_gt(const double* __restrict__ d, cons
 // smem doubles multisect_kernel needs for order n
 __host__ __device__ constexpr int multisect_smem_doubles(int n) { return 2 * ((n + kSturmUnroll - 1) & ~(kSturmUnroll - 1)); }
 
+// Eigenvalues mu[i] (descending) for i < nev, plus mu[n-1] when `smallest` (one warp each).
 __global__ void __launch_bounds__(256) multisect_kernel(const double* __restrict__ d, const double* __restrict__ e, int n,
-                                                        double* __restrict__ mu) {
+                                                        double* __restrict__ mu, int nev, int smallest) {
   extern __shared__ double ms_smem[];
   const int npad = (n + kSturmUnroll - 1) & ~(kSturmUnroll - 1);
   double* ds = ms_smem;
@@ -369,8 +434,8 @@ __global__ void __launch_bounds__(256) multisect_kernel(const double* __restrict
   }
   __syncthreads();
   const int warp = (blockIdx.x * blockDim.x + tid) >> 5, lane = tid & 31;
-  if (warp >= n) return;
-  const int i = warp;                     // target: (i+1)-th largest
+  if (warp >= nev + smallest) return;
+  const int i = warp < nev ? warp : n - 1;   // target: (i+1)-th largest
   double lo = bnd[0], hi = bnd[1];
   const double eps = 2.220446049250313e-16;
   for (int it = 0; it < 40; ++it) {
@@ -444,60 +509,10 @@ __global__ void lambda_sorted_kernel(const double* __restrict__ mu, int n, int k
   }
 }
 
-// Compact-WY form of the reflectors in chunks of kRefChunk: for chunk b (k = 8b .. 8b+7, k < n-2)
-// H_{8b} H_{8b+1} ... H_{8b+7} = I - V_b T_b V_b^T with T_b upper triangular (LAPACK larft,
-// forward columnwise: T(i,i) = tau_i, T(0:i, i) = -tau_i T(0:i, 0:i) V(:, 0:i)^T v_i).  One CTA per
-// chunk; T_b row-major in wyT[64 b ..].  Reflectors with tau = 0 give zero rows/columns.
-constexpr int kRefChunk = 8;
-constexpr int kMaxRefChunks = (kTriMaxN + kRefChunk - 1) / kRefChunk;
-constexpr int kQStages = 3;
 __global__ void __launch_bounds__(256) wy_t_kernel(const double* __restrict__ Vh, const double* __restrict__ tauv, int n,
                                                    double* __restrict__ wyT) {
   __shared__ double G[kRefChunk][kRefChunk];
-  const int b = blockIdx.x, k0 = b * kRefChunk, nk = n - 2, ldv = tri_ldv(n);
-  const int nr = min(kRefChunk, nk - k0);
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // V^T V, pairs r < c (28), one warp per pair, fixed-order shuffle reduction
-  for (int pr = w; pr < kRefChunk * (kRefChunk - 1) / 2; pr += 8) {
-    int r = 0, rem = pr;
-    while (rem >= kRefChunk - 1 - r) { rem -= kRefChunk - 1 - r; ++r; }
-    const int c = r + 1 + rem;
-    double acc = 0.0;
-    if (c < nr) {
-      const double* vr = Vh + static_cast<int64_t>(k0 + r) * ldv;
-      const double* vc = Vh + static_cast<int64_t>(k0 + c) * ldv;
-      for (int i = k0 + 1 + lane; i < n; i += 32) acc = fma(vr[i], vc[i], acc);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) G[r][c] = acc;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double T[kRefChunk][kRefChunk];
-#pragma unroll
-    for (int r = 0; r < kRefChunk; ++r)
-#pragma unroll
-      for (int c = 0; c < kRefChunk; ++c) T[r][c] = 0.0;
-#pragma unroll
-    for (int c = 0; c < kRefChunk; ++c) {
-      if (c < nr) {
-        const double tc = tauv[k0 + c];
-        T[c][c] = tc;
-#pragma unroll
-        for (int r = 0; r < c; ++r) {
-          double acc = 0.0;
-#pragma unroll
-          for (int q = r; q < c; ++q) acc = fma(T[r][q], G[q][c], acc);
-          T[r][c] = -tc * acc;
-        }
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < kRefChunk; ++r)
-#pragma unroll
-      for (int c = 0; c < kRefChunk; ++c) wyT[b * kRefChunk * kRefChunk + r * kRefChunk + c] = T[r][c];
-  }
+  wy_t_chunk(blockIdx.x, Vh, tauv, n, wyT, G);
 }
 
 // Shared-memory state of cta_apply_q (one vector per CTA): kQStages ring of reflector chunks
