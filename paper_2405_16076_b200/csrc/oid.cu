@@ -297,6 +297,7 @@ struct oid_ctx_s {
   // copy (A7) and the basis-Gram-independent part of Alg 8 (A10) beside the basis Gram (A9).
   cudaStream_t side = nullptr;    // Alg 4 chains (A8)
   cudaStream_t side2 = nullptr;   // estimate factors and tail (A10)
+  cudaStream_t side3 = nullptr;   // A4 spectrum -> lambda chain beside the Q^T application of A5
   cudaStream_t gs = nullptr;      // A9 basis Gram (and its dirty list / sums), lowest priority
   cudaEvent_t ev_gs_done = nullptr;                  // the last estimate's A9 partial sums are ready
   cudaEvent_t ev_gsum_free[2] = {nullptr, nullptr};  // the estimate tail scattered that parity's sums
@@ -656,16 +657,25 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
                                                         ctx->d(L.wyT));   // the compact-WY T factors too
     CKL();
     tl_mark(ctx, st, 15);
+    // the spectrum -> lambda -> LDL^T chain on side stream 3, beside z = Q^T y for all scored columns
+    cudaStream_t s3 = ctx->use_side ? ctx->side3 : st;
+    s = fork_to(ctx, st, s3);
+    if (s != OID_OK) return s;
     // lambda needs E_k (the k largest) and mu_0 only
     const int nev = std::min(p.k, ng);
-    multisect_kernel<<<(nev * 32 + 255) / 256, 256, sizeof(double) * multisect_smem_doubles(ng), st>>>(
+    multisect_kernel<<<(nev * 32 + 255) / 256, 256, sizeof(double) * multisect_smem_doubles(ng), s3>>>(
         ctx->d(L.td), ctx->d(L.te), ng, ctx->d(L.mu), nev, 0);
     CKL();
-    lambda_sorted_kernel<<<1, 256, 0, st>>>(ctx->d(L.mu), ng, p.k, ctx->d(L.gram), p.lambda, ell, scal, gate,
+    lambda_sorted_kernel<<<1, 256, 0, s3>>>(ctx->d(L.mu), ng, p.k, ctx->d(L.gram), p.lambda, ell, scal, gate,
                                             ctx->d(L.td), ctx->d(L.te), ctx->d(L.ldl), 1, frob_idx);
     CKL();
     tri_scores_multi_kernel<<<(ns + kQV - 1) / kQV, 256, sizeof(double) * kQStages * kRefChunk * tri_ldv(ng), st>>>(
-        ctx->d(L.Yc), ng, ns, ctx->d(L.Vh), ctx->d(L.wyT), ctx->d(L.ldl), gate, ctx->d(L.tau));
+        ctx->d(L.Yc), ng, ns, ctx->d(L.Vh), ctx->d(L.wyT), ctx->d(L.ldl), gate, ctx->d(L.tau), ctx->d(L.Tsc));
+    CKL();
+    s = join_from(ctx, st, s3);
+    if (s != OID_OK) return s;
+    tri_scores_chain_kernel<<<(ns + kQV - 1) / kQV, 128, 0, st>>>(ctx->d(L.Tsc), ng, ns, ctx->d(L.ldl), gate,
+                                                                  ctx->d(L.tau));
     CKL();
     tl_mark(ctx, st, 16);
     const int* g1 = gate + 1;
@@ -1049,8 +1059,6 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
         cudaSuccess)
       return bad(e);
     const int ref_smem = static_cast<int>(sizeof(double) * kQStages * kRefChunk * tri_ldv(kTriMaxN));
-    if ((e = cudaFuncSetAttribute(tri_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ref_smem)) != cudaSuccess)
-      return bad(e);
     if ((e = cudaFuncSetAttribute(tri_scores_multi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ref_smem)) != cudaSuccess)
       return bad(e);
     if ((e = cudaFuncSetAttribute(tri_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ref_smem)) != cudaSuccess)
@@ -1072,6 +1080,7 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
     const int p_side2 = getenv("OID_SIDE2_PRIO") ? atoi(getenv("OID_SIDE2_PRIO")) : p_ing;
     if ((e = cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, p_side)) != cudaSuccess) return bad(e);
     if ((e = cudaStreamCreateWithPriority(&ctx->side2, cudaStreamNonBlocking, p_side2)) != cudaSuccess) return bad(e);
+    if ((e = cudaStreamCreateWithPriority(&ctx->side3, cudaStreamNonBlocking, p_ing)) != cudaSuccess) return bad(e);
     // A9 at the lowest priority: throughput work that fills whatever the latency-bound chains leave
     const int p_gs = getenv("OID_GS_PRIO") ? atoi(getenv("OID_GS_PRIO")) : lo;
     if ((e = cudaStreamCreateWithPriority(&ctx->gs, cudaStreamNonBlocking, p_gs)) != cudaSuccess) return bad(e);
@@ -1554,7 +1563,7 @@ oid_status oid_stats_reset(oid_ctx ctx) {
 
 void oid_destroy(oid_ctx ctx) {
   if (!ctx) return;
-  for (cudaStream_t* sp : {&ctx->side, &ctx->side2, &ctx->gs})
+  for (cudaStream_t* sp : {&ctx->side, &ctx->side2, &ctx->side3, &ctx->gs})
     if (*sp) {
       cudaStreamSynchronize(*sp);
       cudaStreamDestroy(*sp);

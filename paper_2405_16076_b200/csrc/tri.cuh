@@ -709,12 +709,15 @@ __device__ __forceinline__ void cta_apply_qt_multi(double (&z)[kQV][2], int n, c
   __syncthreads();
 }
 
-// tau for kQV columns of Yc per CTA (see tri_scores_kernel); the LDL^T chains run on kQV threads.
+// A5 fast path: tau(y) = z^T (T + sI)^-1 z with z = Q^T y = H_{n-3} ... H_0 y, y = column j of Yc
+// (ell x ncol), for kQV columns per CTA; the LDL^T chains run on kQV threads.  Runs when gate[0] != 0.
 __global__ void __launch_bounds__(256) tri_scores_multi_kernel(const double* __restrict__ Yc, int n, int ncol,
                                                                const double* __restrict__ Vh, const double* __restrict__ wyT,
                                                                const double* __restrict__ ldl, const int* __restrict__ gate,
-                                                               double* __restrict__ tau_out) {
-  if (gate[0] == 0) return;
+                                                               double* __restrict__ tau_out, double* __restrict__ zout) {
+  // zout != nullptr: only z = Q^T y (n x ncol into zout), before the gate and the LDL^T factors
+  // exist (tri_scores_chain_kernel finishes); otherwise the whole score
+  if (zout == nullptr && gate[0] == 0) return;
   extern __shared__ __align__(16) double ref_smem[];
   __shared__ __align__(16) double tsm[kQStages * 64];
   __shared__ __align__(8) uint64_t full[kQStages];
@@ -737,6 +740,16 @@ __global__ void __launch_bounds__(256) tri_scores_multi_kernel(const double* __r
     }
   __syncthreads();
   cta_apply_qt_multi(z, n, Vh, wyT, ref_smem, tsm, full, redm, us);
+  if (zout != nullptr) {
+#pragma unroll
+    for (int q = 0; q < kQV; ++q)
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int i = tid + 256 * s;
+        if (i < n && j0 + q < ncol) zout[static_cast<int64_t>(j0 + q) * n + i] = z[q][s];
+      }
+    return;
+  }
 #pragma unroll
   for (int q = 0; q < kQV; ++q)
 #pragma unroll
@@ -755,47 +768,30 @@ __global__ void __launch_bounds__(256) tri_scores_multi_kernel(const double* __r
   }
 }
 
-// tau(y) = z^T (T + sI)^-1 z, z = Q^T y = H_{n-3} ... H_0 y; y = column j of Yc (ell x ncol).
-// One column per CTA; runs when gate[0] != 0.  Dynamic smem: kQStages kRefChunk tri_ldv(n) doubles.
-__global__ void __launch_bounds__(256) tri_scores_kernel(const double* __restrict__ Yc, int n, int ncol,
-                                                         const double* __restrict__ Vh, const double* __restrict__ wyT,
-                                                         const double* __restrict__ ldl, const int* __restrict__ gate,
-                                                         double* __restrict__ tau_out) {
+// tau_j = z_j^T (T + sI)^-1 z_j from z = Q^T y (tri_scores_multi_kernel with zout): kQV columns
+// per CTA, the serial LDL^T chains on kQV threads; runs when gate[0] != 0.
+__global__ void __launch_bounds__(128) tri_scores_chain_kernel(const double* __restrict__ Z, int n, int ncol,
+                                                               const double* __restrict__ ldl, const int* __restrict__ gate,
+                                                               double* __restrict__ tau_out) {
   if (gate[0] == 0) return;
-  extern __shared__ __align__(16) double ref_smem[];
-  __shared__ __align__(16) double tsm[kQStages * 64];
-  __shared__ __align__(8) uint64_t full[kQStages];
-  __shared__ double red[2][8][kRefChunk];
-  __shared__ double zs[kTriMaxN];
-  __shared__ double ls[2 * kTriMaxN];   // LDL^T factors (1/D, L)
-  const int tid = threadIdx.x, j = blockIdx.x;
-  if (tid == 0) {
-    for (int q = 0; q < kQStages; ++q) tri_mbar_init(&full[q], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __shared__ double zs[kQV][kTriMaxN];
+  __shared__ double ls[2 * kTriMaxN];
+  const int tid = threadIdx.x, j0 = blockIdx.x * kQV;
+  for (int e = tid; e < kQV * n; e += blockDim.x) {
+    const int q = e / n, i = e - q * n;
+    zs[q][i] = j0 + q < ncol ? Z[static_cast<int64_t>(j0 + q) * n + i] : 0.0;
   }
-  double z[2];
-#pragma unroll
-  for (int s = 0; s < 2; ++s) {
-    const int i = tid + 256 * s;
-    z[s] = i < n ? Yc[static_cast<int64_t>(j) * n + i] : 0.0;
-  }
+  for (int i = tid; i < 2 * n - 1; i += blockDim.x) ls[i] = ldl[i];
   __syncthreads();
-  QSmem sm{ref_smem, tsm, full, red};
-  int uses = 0;
-  cta_apply_q(z, n, Vh, wyT, true, sm, uses);
-#pragma unroll
-  for (int s = 0; s < 2; ++s) if (tid + 256 * s < n) zs[tid + 256 * s] = z[s];
-  __syncthreads();
-  for (int i = tid; i < 2 * n - 1; i += blockDim.x) ls[i] = ldl[i];   // the chain below reads shared memory
-  __syncthreads();
-  if (tid == 0) {
-    double y = zs[0];
+  if (tid < kQV && j0 + tid < ncol) {
+    const double* zq = zs[tid];
+    double y = zq[0];
     double acc = y * y * ls[0];
     for (int i = 1; i < n; ++i) {
-      y = zs[i] - ls[n + i - 1] * y;
+      y = zq[i] - ls[n + i - 1] * y;
       acc = fma(y * y, ls[i], acc);
     }
-    tau_out[j] = acc;
+    tau_out[j0 + tid] = acc;
   }
 }
 
