@@ -347,3 +347,43 @@ def test_two_stream_estimates_match_one_stream(oid):
     P2 = two.finalize()["P"]
     torch.cuda.synchronize()
     assert torch.equal(P1, P2)
+
+
+@pytest.mark.gpu
+def test_internal_side_streams_match_serial(oid, monkeypatch):
+    """The internal side streams (A8 chain, A10 factors and tail, A4 spectrum chain, A9 stream)
+    are ordered by events only; with every kernel on the caller's stream (OID_NO_SIDE=1, read at
+    oid_init) the results are bitwise the same.  A missing or misplaced event shows up here as a
+    race (the two-stream bench configuration, estimates overlapping the next block's ingest)."""
+    cfg = C3R
+    gen = ChannelFlow(48, 33, 48, seed=cfg.data_seed + 1)
+    nblk = 10
+    A = gen.block(0, nblk * cfg.b)
+    split = _split(cfg.ell)
+    p = oid.make_params(m=cfg.m, k=cfg.k, ell=cfg.ell, b_max=cfg.b, n_cap=nblk * cfg.b, lam=-1.0, split=split, seed=5)
+    monkeypatch.setenv("OID_NO_SIDE", "1")
+    serial = oid.Engine(p)
+    monkeypatch.delenv("OID_NO_SIDE")
+    hi = torch.cuda.Stream(priority=-1)
+    lo = torch.cuda.Stream(priority=0)
+    par = oid.Engine(p, stream=hi, estimate_stream=lo)
+    Ad = _dev(A, np.float64)
+    torch.cuda.synchronize()
+    out1 = torch.empty((nblk, 8), dtype=torch.float64, device="cuda:0")
+    out2 = torch.empty((nblk, 8), dtype=torch.float64, device="cuda:0")
+    for e, j in enumerate(range(0, nblk * cfg.b, cfg.b)):
+        serial.ingest_block(Ad[:, j:j + cfg.b])
+        serial.estimate_begin()
+        serial.estimate_end(out1[e])
+        with torch.cuda.stream(hi):
+            par.ingest_block(Ad[:, j:j + cfg.b])
+        par.estimate_begin()
+        par.estimate_end(out2[e])
+    torch.cuda.synchronize()
+    diff = (out1 != out2).any(dim=1).cpu().numpy()
+    assert not diff.any(), (np.flatnonzero(diff), out1[diff].cpu().numpy(), out2[diff].cpu().numpy())
+    assert np.array_equal(serial.J(), par.J())
+    r1, r2 = serial.finalize(basis=True), par.finalize(basis=True)
+    torch.cuda.synchronize()
+    assert torch.equal(r1["P"], r2["P"])
+    assert torch.equal(r1["basis"], r2["basis"])
