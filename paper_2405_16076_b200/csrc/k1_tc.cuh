@@ -793,6 +793,7 @@ __global__ void k1_tc_reduce_kernel(const double* __restrict__ part, const doubl
     const int j = static_cast<int>(idx / ell), r = static_cast<int>(idx % ell);
     const int h = r / g.rows, rl = r % g.rows;
     double s = 0.0, c = 0.0;
+#pragma unroll 8   // the loads of several slabs in flight; the sums keep their fixed order
     for (int sl = 0; sl < g.nslabs; ++sl) {
       s += part[(static_cast<int64_t>(sl * g.nhalves + h) * g.bpad + j) * g.rows + rl];
       c += cpart[static_cast<int64_t>(sl) * g.bpad + j];
@@ -801,6 +802,7 @@ __global__ void k1_tc_reduce_kernel(const double* __restrict__ part, const doubl
   } else if (idx < ny + ncols) {
     const int j = static_cast<int>(idx - ny);
     double s = 0.0;
+#pragma unroll 8
     for (int sl = 0; sl < g.nslabs; ++sl) s += npart[static_cast<int64_t>(sl) * g.bpad + j];
     out[idx] = s;
     if (!isfinite(s)) atomicOr(flags, 1u);
