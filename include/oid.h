@@ -142,7 +142,13 @@ oid_status oid_partials(oid_ctx ctx, int32_t which, double** dev_ptr, int64_t* c
    out_dev: device array of 8 doubles receiving
      [0] ||E||^2 estimate (unclamped), [1] T = estimate of tr(A (A_J P)^T), [2] tr(G P P^T),
      [3] ||A_obs||_F^2, [4] ||E||_F estimate (clamped at 0), [5] relative estimate,
-     [6] flags (as double), [7] kappa(S_J).  Errors: OID_ESTATE before the first block. */
+     [6] flags (as double), [7] kappa(S_J).  Errors: OID_ESTATE before the first block.
+   Ordering: the estimate reads the state of the last committed ingest (whatever stream it ran
+   on); its internal work runs on library streams ordered by events after that commit, and
+   `stream` (which may differ from the ingest stream and overlap the next ingest) waits for the
+   partials at the end of _begin and for the whole estimate at the end of _end, so out_dev is
+   written in `stream` order.  The partials (oid_partials 1) alternate between two buffers by
+   estimate parity: reduce them between _begin and _end of the same estimate. */
 oid_status oid_estimate_begin(oid_ctx ctx, void* stream);
 oid_status oid_estimate_end(oid_ctx ctx, double* out_dev, void* stream);
 
