@@ -277,11 +277,24 @@ tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__
 #pragma unroll
       for (int r = 0; r < kTriRW; ++r) pi[r] += p2[r];
     }
+    // warp sums of the 4 rows by a butterfly reduce-scatter (row 2 b4 + b3 ends in the lanes with
+    // lane bits b4, b3), then broadcast: 10 shuffles instead of 20
+    static_assert(kTriRW == 4, "butterfly below is written for 4 rows per warp");
+    {
+      const bool h16 = (lane & 16) != 0, h8 = (lane & 8) != 0;
+      const double s0 = h16 ? pi[0] : pi[2], s1 = h16 ? pi[1] : pi[3];
+      const double k0 = h16 ? pi[2] : pi[0], k1 = h16 ? pi[3] : pi[1];
+      const double q0 = k0 + __shfl_xor_sync(0xffffffffu, s0, 16);
+      const double q1 = k1 + __shfl_xor_sync(0xffffffffu, s1, 16);
+      double t = (h8 ? q1 : q0) + __shfl_xor_sync(0xffffffffu, h8 ? q0 : q1, 8);
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+#pragma unroll
+      for (int r = 0; r < kTriRW; ++r) pi[r] = __shfl_sync(0xffffffffu, t, (r >> 1) * 16 + (r & 1) * 8);
+    }
     double kw = 0.0;
 #pragma unroll
     for (int r = 0; r < kTriRW; ++r) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) pi[r] += __shfl_xor_sync(0xffffffffu, pi[r], o);
       pi[r] *= tau;
       if (gi[r] > k) kw = fma(vi[r], pi[r], kw);
       if (lane == 0 && warp * kTriRW + r < R) {
