@@ -587,14 +587,23 @@ __device__ __forceinline__ void cta_apply_q(double (&z)[2], int n, const double*
         pr[r] = fma(v[r][s], z[s], pr[r]);
       }
     }
+    // warp sums by a butterfly reduce-scatter: value r ends in lanes 4 r .. 4 r + 3 (9 shuffles
+    // instead of 40)
+    static_assert(kRefChunk == 8, "butterfly below is written for 8 values");
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
+    for (int half = 4; half > 0; half >>= 1) {
+      const bool hi = (lane & (4 * half)) != 0;
 #pragma unroll
-      for (int r = 0; r < kRefChunk; ++r) pr[r] += __shfl_xor_sync(0xffffffffu, pr[r], o);
+      for (int i = 0; i < half; ++i) {
+        const double send = hi ? pr[i] : pr[i + half];
+        const double keep = hi ? pr[i + half] : pr[i];
+        pr[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4 * half);
+      }
+    }
+#pragma unroll
+    for (int o = 2; o > 0; o >>= 1) pr[0] += __shfl_xor_sync(0xffffffffu, pr[0], o);
     double (*red)[kRefChunk] = sm.red[it & 1];
-#pragma unroll
-    for (int r = 0; r < kRefChunk; ++r)   // every lane holds the warp sums after the xor tree
-      if (lane == r) red[warp][r] = pr[r];
+    if ((lane & 3) == 0) red[warp][lane >> 2] = pr[0];
     double T[kRefChunk * kRefChunk];
 #pragma unroll
     for (int q = 0; q < kRefChunk * kRefChunk; ++q) T[q] = sm.t[st * 64 + q];
