@@ -52,9 +52,11 @@ typedef enum { OID_F32 = 0, OID_F64 = 1 } oid_dtype;
 typedef enum {
   OID_K1_AUTO = 0,      /* tensor-core path when available for the shape, else SIMT       */
   OID_K1_SIMT_F64 = 1,  /* CUDA-core DFMA, Omega generated in registers                    */
-  OID_K1_TC_INT8 = 2    /* tcgen05 kind::i8, Omega generated into TMEM (A operand), data
+  OID_K1_TC_INT8 = 2,   /* tcgen05 kind::i8, Omega generated into TMEM (A operand), data
                            split into exact int8 digit planes in shared memory (sm_100a);
                            needs row_begin % 32 == 0, 16-byte aligned X and ld            */
+  OID_K1_TC_PAIR = 3    /* experimental: 2-CTA (cta_group::2) variant of OID_K1_TC_INT8 with
+                           48-bit digit planes converted by integer arithmetic            */
 } oid_k1_mode;
 
 /* flag bits (oid_stats.flags, estimate out[6]) */

@@ -25,7 +25,7 @@ OID_OK, OID_EINVAL, OID_ESHAPE, OID_ENOMEM, OID_ECUDA, OID_ENCCL, OID_ENUMERIC, 
 _STATUS = {0: "OID_OK", -1: "OID_EINVAL", -2: "OID_ESHAPE", -3: "OID_ENOMEM", -4: "OID_ECUDA", -5: "OID_ENCCL",
            -6: "OID_ENUMERIC", -7: "OID_ESTATE"}
 OID_F32, OID_F64 = 0, 1
-K1_AUTO, K1_SIMT_F64, K1_TC_INT8 = 0, 1, 2
+K1_AUTO, K1_SIMT_F64, K1_TC_INT8, K1_TC_PAIR = 0, 1, 2, 3
 FLAG_NONFINITE_INPUT, FLAG_SJ_RANK_DEFICIENT, FLAG_E2_NEGATIVE, FLAG_K1_RECOMPUTED = 1, 2, 4, 8
 
 EXPORTED = ["oid_workspace_query", "oid_init", "oid_ingest_block", "oid_ingest_sketch", "oid_ingest_commit",
@@ -258,7 +258,7 @@ class Engine:
         shapes = {0: ((t,), np.int64), 1: ((t,), np.float64), 2: ((n_obs, ell), np.float64),
                   3: ((ga * ell, ga * ell), np.float64), 4: ((8,), np.float64), 5: ((t + bm,), np.float64),
                   6: ((ga * ell,), np.float64), 7: (((ell + 1) * bm,), np.float64), 8: ((ell, t), np.float64),
-                  9: ((3, 48), np.int32), 10: ((10, 4096), np.int64), 11: ((t, t), np.float64), 12: ((1024, 4), np.int64), 13: ((4096, 2), np.float64)}
+                  9: ((3, 48), np.int32), 10: ((12, 4096), np.int64), 11: ((t, t), np.float64), 12: ((1024, 4), np.int64), 13: ((4096, 2), np.float64)}
         shape, dt = shapes[field]
         a = np.empty(shape, dtype=dt)
         self._check(_lib.oid_get(self.h, field, ctypes.c_void_p(a.ctypes.data), a.nbytes, self._st()), "oid_get")

@@ -23,7 +23,7 @@
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_runtime.h>
-#include "k1_tc.cuh"
+#include "sm100.cuh"
 
 namespace oid {
 namespace bgtc {

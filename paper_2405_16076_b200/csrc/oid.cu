@@ -19,6 +19,7 @@
 #include "dense.cuh"
 #include "k1_simt.cuh"
 #include "k1_tc.cuh"
+#include "k1_pair.cuh"
 #include "gram_tc.cuh"
 #include "grad.cuh"
 #include "path.cuh"
@@ -190,7 +191,7 @@ Layout make_layout(const oid_params& p) {
   L.gp = b.take((ellg + 16) * d);
   L.gate = b.take(8 * sizeof(int));
   L.sjG = b.take(t * t * d);
-  L.dbg = b.take((k1tc::kDbgRows + 1) * k1tc::kDbgTiles * sizeof(long long));
+  L.dbg = b.take((k1p::kDbgRows + 1) * k1tc::kDbgTiles * sizeof(long long));
   L.cBt = b.take(std::max<size_t>(1, l1 * l2) * d);
   L.cZ2 = b.take(std::max<size_t>(1, l1 * l2) * d);
   L.cG = b.take(std::max<size_t>(1, std::min(l1, l2) * std::min(l1, l2)) * d);
@@ -232,7 +233,8 @@ Layout make_layout(const oid_params& p) {
     L.gRhs = b.take(3 * ell * n * d);
     L.gscal = b.take(8 * d);
   }
-  L.tc = b.take(k1tc_workspace_bytes(p.ell, p.b_max, m_local(p), p.dtype == OID_F64));
+  L.tc = b.take(std::max(k1tc_workspace_bytes(p.ell, p.b_max, m_local(p), p.dtype == OID_F64),
+                         k1p_workspace_bytes(p.ell, p.b_max, m_local(p), p.dtype == OID_F64)));
   L.total = b.off;
   return L;
 }
@@ -252,7 +254,7 @@ const char* validate(const oid_params* p) {
   if (!(p->lambda >= 0.0 || p->lambda == -1.0 || p->lambda == -2.0)) return "lambda must be >= 0, -1 or -2";
   if (!(p->eps > 0.0) || !(p->delta > 0.0 && p->delta < 1.0) || !(p->c > 0.0)) return "need eps > 0, 0 < delta < 1, c > 0";
   if (p->dtype != OID_F32 && p->dtype != OID_F64) return "dtype must be OID_F32 or OID_F64";
-  if (p->k1_mode < 0 || p->k1_mode > 2) return "bad k1_mode";
+  if (p->k1_mode < 0 || p->k1_mode > 3) return "bad k1_mode";
   if (p->m / 32 >= (int64_t(1) << 32)) return "m too large for the 32-bit Philox row counter";
   if (p->grad_nfields < 0) return "grad_nfields must be >= 0";
   if (p->grad_nfields > 0) {
@@ -559,7 +561,8 @@ oid_status launch_k1_simt(oid_ctx ctx, cudaStream_t st, const T* X, int64_t ld, 
 oid_status sketch_one(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_t st, double* out, bool f64,
                       bool strict_mode) {
   const oid_params& p = ctx->p;
-  const bool want_tc = (p.k1_mode == OID_K1_TC_INT8) || (p.k1_mode == OID_K1_AUTO && ctx->tc_ok);
+  const bool want_pair = p.k1_mode == OID_K1_TC_PAIR;
+  const bool want_tc = (p.k1_mode == OID_K1_TC_INT8) || want_pair || (p.k1_mode == OID_K1_AUTO && ctx->tc_ok);
   K1TcArgs a{};
   a.X = X; a.ld = ld; a.ncols = nc; a.row_begin = p.row_begin; a.row_end = p.row_end; a.ell = p.ell;
   a.key0 = ctx->key0; a.key1 = ctx->key1; a.scale = ctx->qscale; a.f64 = f64;
@@ -570,8 +573,8 @@ oid_status sketch_one(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream
          (static_cast<uint32_t>(ctx->qmag[6]) << 16) | (static_cast<uint32_t>(ctx->qmag[7]) << 24);
   a.num_sms = std::max(2, ctx->num_sms - ctx->k1_free_sms);
   a.dbg = ctx->k1_debug ? ctx->ptr<long long>(ctx->L.dbg) : nullptr;
-  const bool tc_call = want_tc && ctx->tc_ok && k1tc_call_ok(a);
-  if (strict_mode && p.k1_mode == OID_K1_TC_INT8 && !tc_call)
+  const bool tc_call = want_tc && ctx->tc_ok && (want_pair ? k1p_call_ok(a) : k1tc_call_ok(a));
+  if (strict_mode && (p.k1_mode == OID_K1_TC_INT8 || want_pair) && !tc_call)
     return ctx->fail(OID_EINVAL, "tensor-core K1 unavailable for this device/shape/alignment");
   if (tc_call) {
     int nl = 0;
@@ -579,13 +582,13 @@ oid_status sketch_one(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream
     {
       EvScope ev(ctx, st, &ctx->ev_k1);
       tl_mark(ctx, st, 1);
-      e = k1tc_launch(a, st, &nl);
+      e = want_pair ? k1p_launch(a, st, &nl) : k1tc_launch(a, st, &nl);
       tl_mark(ctx, st, 2);
     }
     ctx->launches += nl;
     ctx->k1_launches += 1;
     if (e != cudaSuccess) return ctx->fail(OID_ECUDA, "k1 tc: %s", cudaGetErrorString(e));
-    ctx->k1_mode_used = OID_K1_TC_INT8;
+    ctx->k1_mode_used = want_pair ? OID_K1_TC_PAIR : OID_K1_TC_INT8;
     return OID_OK;
   }
   if (f64) return launch_k1_simt<double>(ctx, st, static_cast<const double*>(X), ld, nc, out);
@@ -653,7 +656,7 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
     // tridiagonal fast path (tri.cuh); the eigenvector path below runs only when gate[1] is set
     const size_t smem = sizeof(double) * static_cast<size_t>(ng) * tri_rows(ng);
     tridiag_cluster_kernel<<<kTriCtas, 256, smem, st>>>(ctx->d(L.gram), ng, ctx->d(L.td), ctx->d(L.te), ctx->d(L.Vh),
-                                                        ctx->d(L.tauv), ctx->k1_debug ? ctx->ptr<long long>(L.dbg) + k1tc::kDbgRows * k1tc::kDbgTiles : nullptr,
+                                                        ctx->d(L.tauv), ctx->k1_debug ? ctx->ptr<long long>(L.dbg) + k1p::kDbgRows * k1tc::kDbgTiles : nullptr,
                                                         ctx->d(L.wyT));   // the compact-WY T factors too
     CKL();
     tl_mark(ctx, st, 15);
@@ -1487,9 +1490,9 @@ oid_status oid_get(oid_ctx ctx, int32_t field, void* host_dst, size_t bytes, voi
     case 8: off = L.Sjpinv + static_cast<size_t>((ctx->epoch + 1) & 1) * ctx->t * p.ell * sizeof(double);
             need = sizeof(double) * ctx->t * p.ell; break;
     case 9: off = L.counters; need = sizeof(int) * kNumJacobiUses * kMaxSweeps; break;
-    case 10: off = L.dbg; need = k1tc::kDbgRows * k1tc::kDbgTiles * sizeof(long long); break;
+    case 10: off = L.dbg; need = k1p::kDbgRows * k1tc::kDbgTiles * sizeof(long long); break;
     case 11: off = L.G; need = sizeof(double) * ctx->t * ctx->t; break;
-    case 12: off = L.dbg + k1tc::kDbgRows * k1tc::kDbgTiles * sizeof(long long); need = k1tc::kDbgTiles * sizeof(long long); break;
+    case 12: off = L.dbg + k1p::kDbgRows * k1tc::kDbgTiles * sizeof(long long); need = k1tc::kDbgTiles * sizeof(long long); break;
     case 13: {   // timeline: up to 4096 (tag, ms since the first mark) pairs, then cleared
       if (bytes < 2 * 4096 * sizeof(double)) return ctx->fail(OID_ESHAPE, "field 13 needs %zu bytes", 2 * 4096 * sizeof(double));
       CK(cudaDeviceSynchronize());
