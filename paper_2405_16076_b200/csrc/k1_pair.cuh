@@ -51,12 +51,16 @@ namespace oid {
 
 namespace k1p {
 using namespace k1tc;  // PTX helpers (sm100.cuh)
+#ifndef K1P_WAIT
+#define K1P_WAIT mbar_wait_nh
+#endif
 
-constexpr int kKTile = 64;          // data rows per pipeline stage (two 32-row Philox groups)
+constexpr int kKTile = 128;         // data rows per pipeline stage (four 32-row Philox groups)
+constexpr int kACols = kKTile / 4;  // TMEM columns of one M tile's sketch entries per stage
 constexpr int kH = 6;               // exponent headroom bits over the first tile
 constexpr int kEmin = -900;         // exponents are clamped here (data below 2^-900 lose bits)
 constexpr int kNone = -100000;      // "no nonzero seen yet" exponent
-constexpr int kMaxEpochTiles = 1024;
+constexpr int kMaxEpochTiles = 65536 / kKTile;   // int32 bound: 65536 rows x 255 x 127 < 2^31
 constexpr int kMaxStages = 8;
 constexpr int kMaxA = 4;
 // Roles by warp id (24 warps; SMSP = id % 4, slot = id / 4): slot 0 epilogue, slots 1-2 generator
@@ -133,7 +137,7 @@ inline Geom make_geom(int ell, int ncols, int64_t m_loc, bool f64, int num_sms) 
   g.R = 128 * g.TM * g.nc;
   g.nh = (ell + g.R - 1) / g.R;
   g.ellp = g.nh * g.R;
-  g.na = std::min(kMaxA, (512 - g.TM * ntot) / (16 * g.TM));
+  g.na = std::min(kMaxA, (512 - g.TM * ntot) / (kACols * g.TM));
   const int bh = g.bpad / g.nc;
   g.x_bytes = kKTile * bh * (f64 ? 8 : 4);
   g.b_bytes = kKTile * g.ks * bh;
@@ -268,7 +272,7 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
   constexpr int NBOX = kKTile / BOXR;
   constexpr int RPT = kKTile * BH / (32 * kSlW);    // rows per slicer thread (4, 8, 16)
   constexpr int chB = NB * 16;                      // bytes per 16-byte K chunk of a B stage
-  static_assert(RPT % 4 == 0 && RPT <= 16, "slicer rows per thread");
+  static_assert(RPT % 4 == 0 && (RPT <= 16 || RPT % 16 == 0), "slicer rows per thread");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int ridx = 0;
@@ -315,8 +319,9 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
     int s = 0;
     uint32_t ph = 0;
     for (int t = 0; t < ntiles; ++t) {
-      if (t >= NS) mbar_wait(&sh.x_empty[s], ph ^ 1u);
+      if (t >= NS) K1P_WAIT(&sh.x_empty[s], ph ^ 1u);
       if (g.dbg && blockIdx.x == 0 && t < kDbgTiles && lane == 0) g.dbg[4 * kDbgTiles + t] = clock64();
+      if (g.exp & 512) { mbar_arrive_e(&sh.x_full[s]); if (++s == NS) { s = 0; ph ^= 1u; } continue; }
       mbar_arrive_expect_tx_e(&sh.x_full[s], g.x_bytes);
       uint8_t* dst = xbuf + s * g.x_bytes;
 #pragma unroll
@@ -352,7 +357,7 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
           }
         }
         mbar_arrive(&sh.d_full);
-        mbar_wait(&sh.d_empty, par);                     // both epilogues have read D
+        K1P_WAIT(&sh.d_empty, par);                     // both epilogues have read D
         tc_fence_after();
         ++q;
       };
@@ -360,9 +365,9 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
       uint32_t ph = 0, pha = 0;
       for (int t = 0; t < ntiles; ++t) {
         if (g.dbg && blockIdx.x == 0 && t < kDbgTiles && lane == 0) g.dbg[9 * kDbgTiles + t] = clock64();
-        mbar_wait(&sh.a_full[sa], pha);
+        K1P_WAIT(&sh.a_full[sa], pha);
         if (g.dbg && blockIdx.x == 0 && t < 2048 && lane == 0) g.dbg[9 * kDbgTiles + 2048 + t] = clock64();
-        mbar_wait(&sh.b_full[s], ph);
+        K1P_WAIT(&sh.b_full[s], ph);
         tc_fence_after();
         if (g.dbg && blockIdx.x == 0 && t < kDbgTiles && lane == 0) g.dbg[2 * kDbgTiles + t] = clock64();
         // exponents of the stage (only ever raised): a change closes the accumulation epoch
@@ -374,23 +379,28 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
         if (newacc && t > 0) close_epoch(0);
         if (lane < BPAD) cur0 = e0;
         if (BPAD > 32) cur1 = e1;
-        const uint32_t bbase = bbase0 + s * g.b_bytes;
+        // one elected thread issues the tile's MMAs: descriptors are the stage's base descriptor
+        // plus compile-time offsets (address field = byte address >> 4)
+        if (!(g.exp & 256) && elect_one()) {
+          const uint64_t bd0 = umma_desc(bbase0 + s * g.b_bytes, chB, 128);
+          const uint32_t a0 = tmem + ACOL0 + sa * TM * kACols;
 #pragma unroll
-        for (int ks = 0; ks < kKTile / 32; ++ks) {
+          for (int ks = 0; ks < kKTile / 32; ++ks) {
 #pragma unroll
-          for (int tm = 0; tm < TM; ++tm) {
-            const uint32_t at = tmem + ACOL0 + (sa * TM + tm) * 16 + ks * 8;
-            const uint32_t acc = (newacc && ks == 0) ? 0u : 1u;
-            const uint32_t dcol = tmem + tm * NTOT;
+            for (int tm = 0; tm < TM; ++tm) {
+              const uint32_t at = a0 + tm * kACols + ks * 8;
+              const uint32_t acc = (newacc && ks == 0) ? 0u : 1u;
+              const uint32_t dcol = tmem + tm * NTOT;
 #pragma unroll
-            for (int c = 0; c < NCH; ++c) {
-              const uint64_t bd = umma_desc(bbase + 2 * ks * chB + (c * NUC / 8) * 128, chB, 128);
-              mma_i8_ts<NC>(dcol + c * NC * NUC, at, bd, idesc_i8m(MM, NC * NUC, false), acc);
+              for (int c = 0; c < NCH; ++c)
+                mma_i8_ts_1<NC>(dcol + c * NC * NUC, at, bd0 + ((2 * ks * chB + (c * NUC / 8) * 128) >> 4),
+                                idesc_i8m(MM, NC * NUC, false), acc);
+              mma_i8_ts_1<NC>(dcol + NC * NU, at, bd0 + ((2 * ks * chB + (NU / 8) * 128) >> 4),
+                              idesc_i8m(MM, NC * BH, true), acc);
             }
-            const uint64_t bd = umma_desc(bbase + 2 * ks * chB + (NU / 8) * 128, chB, 128);
-            mma_i8_ts<NC>(dcol + NC * NU, at, bd, idesc_i8m(MM, NC * BH, true), acc);
           }
         }
+        __syncwarp();
         mma_commit_mc<NC>(&sh.a_empty[sa], mask);
         mma_commit_mc<NC>(&sh.b_empty[s], mask);
         if (g.dbg && blockIdx.x == 0 && t < kDbgTiles && lane == 0) g.dbg[3 * kDbgTiles + t] = clock64();
@@ -406,9 +416,9 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
     const int gw = ridx;
     const int quarter = warp & 3;
     const int sl = gw >> 2;
+    constexpr int NCALL = (kKTile / 32) * TM / 2;   // Philox calls (32 entries each) per thread per tile
     const int tm = TM == 2 ? sl : 0;
-    const int kc0 = TM == 2 ? 0 : sl;
-    constexpr int NCALL = TM == 2 ? 2 : 1;
+    const int kc0 = TM == 2 ? 0 : sl * NCALL;
     const int rl = tm * MM + h * 128 + quarter * 32 + lane;   // row within the unit
     const int r = u * R + rl;
     const bool warp_live = (u * R + tm * MM + h * 128 + quarter * 32) < ell;
@@ -418,11 +428,11 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
     uint32_t pha = 0;
     for (int t = 0; t < ntiles; ++t) {
       if (t >= NA) {
-        mbar_wait(&sh.a_empty[sa], pha ^ 1u);
+        K1P_WAIT(&sh.a_empty[sa], pha ^ 1u);
         tc_fence_after();
       }
 
-      uint32_t pk[16];
+      uint32_t pk[8 * NCALL];
       if (warp_live && !(g.exp & 1)) {
         uint32_t c0[NCALL], c1[NCALL], c2[NCALL], c3[NCALL];
 #pragma unroll
@@ -470,10 +480,9 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
 #pragma unroll
         for (int k = 0; k < 8 * NCALL; ++k) pk[k] = 0u;
       }
-      const uint32_t ta = tmem + (static_cast<uint32_t>(32 * quarter) << 16) + ACOL0 + (sa * TM + tm) * 16 + kc0 * 8;
+      const uint32_t ta = tmem + (static_cast<uint32_t>(32 * quarter) << 16) + ACOL0 + (sa * TM + tm) * kACols + kc0 * 8;
       if (!(g.exp & 4)) {
-        if constexpr (NCALL == 2) tmem_st16(ta, pk);
-        else tmem_st8(ta, pk);
+        tmem_store<8 * NCALL>(ta, pk);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       }
       tc_fence_before();
@@ -582,6 +591,7 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
         if constexpr (KS == 7) tr4_lo3(qh[0], qh[1], qh[2], qh[3], P[q4][4], P[q4][5], P[q4][6]);
         else tr4_lo2(qh[0], qh[1], qh[2], qh[3], P[q4][4], P[q4][5]);
         // norms: sum over the 4 rows of d_p d_q by IDP4A (planes 0..KS-2 unsigned, KS-1 signed)
+        if (!(g.exp & 64))
 #pragma unroll
         for (int p = 0; p < KS; ++p) {
 #pragma unroll
@@ -605,27 +615,30 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
     int since_flush = 0;
     // two tiles per iteration: the barrier waits, shared-memory loads and the proxy fence of the
     // pair overlap (a warp's work per tile is short; its latencies are not)
-    constexpr int G = 2;
+    constexpr int G = 1;
     for (int t = 0; t < ntiles; t += G) {
       const int cnt = min(G, ntiles - t);
-      const bool dbgt = g.dbg && blockIdx.x == 0 && sw == (g.exp >> 4) && lane == 0 && t < kDbgTiles;
+      const bool dbgt = g.dbg && blockIdx.x == 0 && sw == (g.exp >> 12) && lane == 0 && t < kDbgTiles;
       if (dbgt) g.dbg[5 * kDbgTiles + t] = clock64();
       int sg_[G];
       uint32_t pg_[G];
       sg_[0] = s; pg_[0] = ph;
-      sg_[1] = s + 1 == NS ? 0 : s + 1;
-      pg_[1] = s + 1 == NS ? ph ^ 1u : ph;
+      if constexpr (G > 1) {
+        sg_[1] = s + 1 == NS ? 0 : s + 1;
+        pg_[1] = s + 1 == NS ? ph ^ 1u : ph;
+      }
       uint32_t w[G][RPT * NW];
 #pragma unroll
       for (int gi = 0; gi < G; ++gi) {
         if (gi < cnt) {
-          mbar_wait(&sh.x_full[sg_[gi]], pg_[gi]);
-          // RPT rows of column jc from the 128B-swizzled boxes
-          const uint8_t* bx = xbuf + sg_[gi] * g.x_bytes + (row0 / BOXR) * BH * 128 + jc * 128;
-          const int c0 = (row0 % BOXR) * static_cast<int>(sizeof(T)) / 16;
+          K1P_WAIT(&sh.x_full[sg_[gi]], pg_[gi]);
+          // RPT rows of column jc from the 128B-swizzled boxes (16-byte chunks of 16 / sizeof(T) rows)
+          const uint8_t* xs = xbuf + sg_[gi] * g.x_bytes + jc * 128;
 #pragma unroll
           for (int c = 0; c < RPT * NW / 4; ++c) {
-            const uint4 v = *reinterpret_cast<const uint4*>(bx + (((c0 + c) ^ (jc & 7)) << 4));
+            const int rc = row0 + c * (16 / static_cast<int>(sizeof(T)));
+            const int cl = (rc % BOXR) * static_cast<int>(sizeof(T)) / 16;
+            const uint4 v = *reinterpret_cast<const uint4*>(xs + (rc / BOXR) * BH * 128 + ((cl ^ (jc & 7)) << 4));
             w[gi][4 * c + 0] = v.x; w[gi][4 * c + 1] = v.y; w[gi][4 * c + 2] = v.z; w[gi][4 * c + 3] = v.w;
           }
         } else {
@@ -636,8 +649,9 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
       if (dbgt) g.dbg[6 * kDbgTiles + t] = clock64();
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(&sh.x_empty[sg_[0]]);
-        if (cnt > 1) mbar_arrive(&sh.x_empty[sg_[1]]);
+#pragma unroll
+        for (int gi = 0; gi < G; ++gi)
+          if (gi < cnt) mbar_arrive(&sh.x_empty[sg_[gi]]);
       }
       // fp64-layout words (hi, lo), biased exponents, and the exponent check of each tile in order;
       // a raise at the pair's second tile flushes the accumulators only after the first tile
@@ -687,7 +701,7 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
       if (dbgt) g.dbg[10 * kDbgTiles + t] = clock64();
 #pragma unroll
       for (int gi = 0; gi < G; ++gi)
-        if (gi < cnt && t + gi >= NS) mbar_wait(&sh.b_empty[sg_[gi]], pg_[gi] ^ 1u);
+        if (gi < cnt && t + gi >= NS) K1P_WAIT(&sh.b_empty[sg_[gi]], pg_[gi] ^ 1u);
       if (dbgt) g.dbg[7 * kDbgTiles + t] = clock64();
 #pragma unroll
       for (int gi = 0; gi < G; ++gi) {
@@ -697,14 +711,26 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
             since_flush = 0;
           }
           uint32_t P[RPT / 4][KS];
-          convert_acc(vh[gi], vl[gi], ex[gi], ecg[gi], P);
+          if (g.exp & 128) {
+#pragma unroll
+            for (int q4 = 0; q4 < RPT / 4; ++q4)
+#pragma unroll
+              for (int p = 0; p < KS; ++p) P[q4][p] = vl[gi][q4] ^ vh[gi][p % RPT];
+          } else {
+            convert_acc(vh[gi], vl[gi], ex[gi], ecg[gi], P);
+          }
 #pragma unroll
           for (int p = 0; p < KS; ++p) {
             const int n = p * BH + jc;
             uint8_t* dst = bbuf + sg_[gi] * g.b_bytes + (row0 / 16) * chB + (n >> 3) * 128 + (n & 7) * 16 + (row0 % 16);
             if constexpr (RPT == 4) *reinterpret_cast<uint32_t*>(dst) = P[0][p];
             else if constexpr (RPT == 8) *reinterpret_cast<uint2*>(dst) = make_uint2(P[0][p], P[1][p]);
-            else *reinterpret_cast<uint4*>(dst) = make_uint4(P[0][p], P[1][p], P[2][p], P[3][p]);
+            else {
+#pragma unroll
+              for (int c16 = 0; c16 < RPT / 16; ++c16)
+                *reinterpret_cast<uint4*>(dst + c16 * chB) =
+                    make_uint4(P[4 * c16][p], P[4 * c16 + 1][p], P[4 * c16 + 2][p], P[4 * c16 + 3][p]);
+            }
           }
           // this column's exponent for the stage (CTA 1: st.async completing 4 transaction bytes on
           // the leader's b_full, whose expected bytes the leader's first slicer warp posts)
@@ -717,7 +743,7 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
       since_flush += cnt;
       if (since_flush >= kFlushTiles) { flush(ecur); since_flush = 0; }
       if (dbgt) g.dbg[8 * kDbgTiles + t] = clock64();
-      fence_proxy_async();
+      if (!(g.exp & 32)) fence_proxy_async();
       __syncwarp();
       if (lane == 0) {
 #pragma unroll
@@ -753,7 +779,7 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
     for (int qe = 0;; ++qe) {
       const int par = qe & 1;
       // one warp polls the barrier, the others sleep on a named barrier (no mbarrier polling)
-      if (ridx == 0) mbar_wait(&sh.d_full, par);
+      if (ridx == 0) K1P_WAIT(&sh.d_full, par);
       named_bar(2, 32 * kEpiW);
       tc_fence_after();
       const int last = *reinterpret_cast<volatile int*>(&sh.elast[par]);
