@@ -254,7 +254,7 @@ class EpochLog:
 class OracleOID:
     """Step-by-step oracle of Algorithm 3's hot path; one ingest block = one epoch (R4)."""
 
-    def __init__(self, params, cache_omega=True):
+    def __init__(self, params, cache_omega=True, cache_limit=100_000_000):
         self.p = params
         t, ell = params.t, params.ell
         assert params.ell1 + params.ell2 + params.ell3 == ell
@@ -270,7 +270,7 @@ class OracleOID:
         self.kappa = 1.0
         self.log = []
         self._Q = None
-        if cache_omega and ell * params.m_loc <= 100_000_000:
+        if cache_omega and ell * params.m_loc <= cache_limit:
             rb = params.row_begin
             self._Q = omega_rows(params.seed, np.arange(ell), rb, rb + params.m_loc)
 

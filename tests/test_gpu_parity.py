@@ -162,9 +162,10 @@ def test_c1_other_sketch_seeds(oid, seed):
     lam = _lam_exact(A, 20)
     eng, o = _pair(oid, 4096, 20, 48, 16, 512, lam, split=(16, 16, 16), seed=seed)
     low = _stream_compare(oid, eng, o, A, 16)
-    if low is None:
-        P = eng.finalize()["P"].cpu().numpy()
-        assert np.linalg.norm(P - o.P) / np.linalg.norm(o.P) < 1e-5
+    if low is not None:
+        pytest.skip(f"C1 sketch seed {seed}: oracle decision margin < 1e-6 at epoch {low} (J compared up to it)")
+    P = eng.finalize()["P"].cpu().numpy()
+    assert np.linalg.norm(P - o.P) / np.linalg.norm(o.P) < 1e-5
 
 
 # ----------------------------------------------------------------------------- C2 / C3r prefixes
@@ -176,11 +177,12 @@ def test_c2_prefix_parity(oid):
     A = gen.block(0, 12 * cfg.b)
     eng, o = _pair(oid, cfg.m, cfg.k, cfg.ell, cfg.b, 12 * cfg.b, -1.0, seed=0, dtype="f32")
     low = _stream_compare(oid, eng, o, A, cfg.b, dtype=np.float32)
-    if low is None:
-        P = eng.finalize()["P"].cpu().numpy()
-        assert np.linalg.norm(P - o.P) / np.linalg.norm(o.P) < 1e-5
-        est, ref = eng.error_estimate(), o.error_estimate()
-        assert abs(est["est_rel"] - ref["est_rel"]) < 1e-5
+    if low is not None:
+        pytest.skip(f"C2 prefix: oracle decision margin < 1e-6 at epoch {low} (J compared up to it)")
+    P = eng.finalize()["P"].cpu().numpy()
+    assert np.linalg.norm(P - o.P) / np.linalg.norm(o.P) < 1e-5
+    est, ref = eng.error_estimate(), o.error_estimate()
+    assert abs(est["est_rel"] - ref["est_rel"]) < 1e-5
 
 
 def test_c3r_prefix_parity(oid):
@@ -190,9 +192,54 @@ def test_c3r_prefix_parity(oid):
     A = gen.block(0, 8 * cfg.b)
     eng, o = _pair(oid, cfg.m, cfg.k, cfg.ell, cfg.b, 8 * cfg.b, -1.0, seed=0)
     low = _stream_compare(oid, eng, o, A, cfg.b)
-    if low is None:
-        P = eng.finalize()["P"].cpu().numpy()
-        assert np.linalg.norm(P - o.P) / np.linalg.norm(o.P) < 1e-5
+    if low is not None:
+        pytest.skip(f"C3r prefix: oracle decision margin < 1e-6 at epoch {low} (J compared up to it)")
+    P = eng.finalize()["P"].cpu().numpy()
+    assert np.linalg.norm(P - o.P) / np.linalg.norm(o.P) < 1e-5
+
+
+def test_c3r_whole_stream(oid):
+    """BASELINE config 2 on the 48x33x48 grid (C3r), the WHOLE 1000-snapshot stream (31 blocks of 32
+    + one of 8), lambda = paper surrogate, seed 0, against the oracle (Alg 3, Alg 4 P:431,
+    Alg 8): J bit-exact after every epoch (the oracle's minimum decision margin on this
+    stream is ~1e-5 >= 1e-6), lambda_eff and E_k to 1e-10, tau_old to 1e-8; after blocks 8, 16, 25
+    and 32: P to 1e-5 (relative Frobenius), NA-Hutch++ |dT|/||A||^2 and |d tr(GPP^T)|/||A||^2 to
+    1e-5 and |d r_hat| to 1e-5 (unclamped components)."""
+    cfg = C3R
+    gen = ChannelFlow(48, 33, 48, seed=cfg.data_seed)
+    n = cfg.n
+    A = gen.block(0, n)
+    split = _split(cfg.ell)
+    p = oid.make_params(m=cfg.m, k=cfg.k, ell=cfg.ell, b_max=cfg.b, n_cap=n, lam=-1.0, split=split, seed=0)
+    eng = oid.Engine(p)
+    o = OracleOID(OracleParams(m=cfg.m, k=cfg.k, ell=cfg.ell, ell1=split[0], ell2=split[1], ell3=split[2], lam=-1.0,
+                               seed=0), cache_limit=200_000_000)
+    Ad = _dev(A, np.float64)
+    checks = {8, 16, 25, 32}
+    for e, j in enumerate(range(0, n, cfg.b)):
+        X = A[:, j:j + cfg.b]
+        eng.ingest_block(Ad[:, j:j + cfg.b])
+        lg = o.ingest_block(X)
+        low = [d for d in lg.decisions if d[5] < 1e-6]
+        if low:
+            pytest.skip(f"oracle decision margin {min(d[5] for d in low):.2e} < 1e-6 at epoch {e}: J compared up to it")
+        Jg = eng.J()
+        assert np.array_equal(Jg, o.J), f"epoch {e}: GPU J {Jg} != oracle J {o.J}"
+        sc = eng.scalars()
+        assert abs(sc["lam"] - lg.lam_eff) <= 1e-10 * max(abs(lg.lam_eff), 1e-300), (e, sc["lam"], lg.lam_eff)
+        assert abs(sc["Ek"] - lg.Ek) <= 1e-10 * abs(lg.Ek), (e, sc["Ek"], lg.Ek)
+        assert np.allclose(eng.get(1), o.tau_old, rtol=1e-8, atol=0), e
+        if e + 1 in checks:
+            est, ref = eng.error_estimate(), o.error_estimate()
+            fro = o.frob2
+            assert abs(est["frob2"] - fro) <= 1e-12 * fro
+            assert abs(est["T"] - ref["T"]) / fro < 1e-5, (e, est["T"], ref["T"])
+            assert abs(est["gpp"] - ref["gpp"]) / fro < 1e-5, (e, est["gpp"], ref["gpp"])
+            assert abs(est["e2"] - ref["e2"]) / fro < 1e-5, (e, est["e2"], ref["e2"])
+            assert abs(est["est_rel"] - ref["est_rel"]) < 1e-5, (e, est["est_rel"], ref["est_rel"])
+            P = eng.finalize()["P"].cpu().numpy()
+            assert np.linalg.norm(P - o.P) / np.linalg.norm(o.P) < 1e-5, e
+    assert o.min_margin() >= 1e-6
 
 
 # ----------------------------------------------------------------------------- ragged / edge cases
@@ -207,8 +254,9 @@ def test_ragged_tail_and_exact_recovery(oid):
     B = fin["basis"].cpu().numpy()
     err = np.linalg.norm(A - B @ P) / np.linalg.norm(A)
     assert err < 1e-10
-    if low is None:
-        assert np.array_equal(fin["J"], o.J)
+    if low is not None:
+        pytest.skip(f"exact recovery checked; oracle decision margin < 1e-6 at epoch {low}, final J not compared")
+    assert np.array_equal(fin["J"], o.J)
 
 
 def test_zero_columns_never_admitted_and_empty_block(oid):
@@ -230,9 +278,10 @@ def test_odd_sizes_tridiagonal_paths(oid, ell, k):
     A = c1_matrix(seed=11, m=900, n=48, rank=12, noise=1e-3)
     eng, o = _pair(oid, 900, k, ell, 8, 48, 0.05, seed=2)
     low = _stream_compare(oid, eng, o, A, 8)
-    if low is None:
-        P = eng.finalize()["P"].cpu().numpy()
-        assert np.linalg.norm(P - o.P) / np.linalg.norm(o.P) < 1e-5
+    if low is not None:
+        pytest.skip(f"oracle decision margin < 1e-6 at epoch {low} (J compared up to it)")
+    P = eng.finalize()["P"].cpu().numpy()
+    assert np.linalg.norm(P - o.P) / np.linalg.norm(o.P) < 1e-5
 
 
 def test_large_basis_and_sketch_paths(oid):

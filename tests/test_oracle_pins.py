@@ -43,6 +43,20 @@ def test_uniform24_grid_and_range():
     assert abs(u.mean() - 0.5) < 4 * math.sqrt(1 / 12 / u.size)
 
 
+def test_uniform24_known_answers_from_curand(golden_dir):
+    """Selection draws u(e, i, x) (reading R6: Philox counter (e, i, x, 1), first output word, top 24
+    bits) against cuRAND's Philox4x32-10 (tests/golden/uniform24_kat.txt, scripts/golden/uniform24_kat.cu):
+    pins the counter layout, the tag and the choice of output word."""
+    rows = [l.split() for l in open(os.path.join(golden_dir, "uniform24_kat.txt")) if l.strip() and not l.startswith("#")]
+    assert len(rows) >= 8
+    for r in rows:
+        seed, e, i, x = int(r[0], 16), int(r[1]), int(r[2]), int(r[3], 16)
+        w0 = int(r[4], 16)
+        u = float(r[8])
+        assert u == (w0 >> 8) * 2.0 ** -24
+        assert float(uniform24(seed, e, i, x)) == u, (r, float(uniform24(seed, e, i, x)))
+
+
 # ------------------------------------------------------------------ Gauss-16 (reading R2)
 
 def _inv_norm_bisect(p):
@@ -176,6 +190,27 @@ def test_topk_energy_worked_example():
     assert lam == pytest.approx((5.0 - 4.0) / (2 * 1))
 
 
+def test_ridge_surrogate_worked_example():
+    """Streaming ridge surrogate lambda_s = (||A_obs||^2 - ||S_k||^2)/k (eq:sketch_ridge_leverage_score,
+    P:341) with S = Y/sqrt(l) (reading R3: ||S_k||^2 = E_k/l, E_k the sum of the k largest
+    eigenvalues of YY^T), clamped at 0 (R8), and the sketch-tail variant (tr - E_k)/(l k).
+    Hand-computed: l = 4, k = 2, eigenvalues (8, 4, 2, 1) -> E_k = 12, E_k/l = 3."""
+    mu = np.array([8.0, 4.0, 2.0, 1.0])
+    p = _params(100, 2, 4, -1.0, split=(1, 1, 2))
+    lam, Ek = ridge_lambda(p, mu, 5.0, 15.0)
+    assert Ek == 12.0 and lam == 1.0                     # (5 - 3) / 2
+    lam, _ = ridge_lambda(p, mu, 2.0, 15.0)
+    assert lam == 0.0                                    # (2 - 3) / 2 < 0, clamped
+    p2 = _params(100, 2, 4, -2.0, split=(1, 1, 2))
+    lam, _ = ridge_lambda(p2, mu, 5.0, 15.0)
+    assert lam == 0.375                                  # (15 - 12) / (4 * 2)
+    p0 = _params(100, 2, 4, 0.25, split=(1, 1, 2))
+    assert ridge_lambda(p0, mu, 5.0, 15.0)[0] == 0.25    # fixed lambda (P:203)
+    # k >= rank: E_k = trace, so lambda_s = (||A||^2 - tr/l)/k
+    p3 = _params(100, 4, 4, -1.0, split=(1, 1, 2))
+    assert ridge_lambda(p3, mu, 5.0, 15.0)[0] == (5.0 - 15.0 / 4.0) / 4.0
+
+
 def test_scores_lambda0_equal_exact_leverage():
     """At lam = 0 and l >= rank(A): sketched scores equal exact leverage ||V(j,:)||^2 and sum to rank."""
     A = low_rank_matrix(11, 300, 80, 7)
@@ -260,6 +295,21 @@ def test_no_eviction_when_scores_unchanged():
     for e in range(200):
         J2, t2, adm, _ = select(1, e, J, tau_old, tau_old.copy(), np.array([0.9]), np.array([False]), 2.0, 100)
         assert np.array_equal(J2, J) and not adm
+
+
+def test_eviction_frequency_matches_probability():
+    """Alg 3 step 20: an occupied slot whose score drops from tau_old to tau is evicted with
+    probability 1 - tau/tau_old.  Monte Carlo over 4000 epochs (independent draws u(e, i, EVICT)),
+    for two score ratios: frequencies within 4 binomial standard errors."""
+    for tau_old, tau_new in ((0.8, 0.2), (0.5, 0.45)):
+        ev = 0
+        trials = 4000
+        for e in range(trials):
+            J, _, _, _ = select(7, e, np.array([5]), np.array([tau_old]), np.array([tau_new]), np.zeros(0),
+                                np.zeros(0, dtype=bool), 1.0, 100)
+            ev += J[0] < 0
+        p = 1.0 - tau_new / tau_old
+        assert abs(ev / trials - p) <= 4 * math.sqrt(p * (1 - p) / trials), (tau_old, tau_new, ev / trials, p)
 
 
 def test_admission_frequency_matches_probability():
@@ -356,6 +406,30 @@ def test_hutchpp_unbiased_over_sketch_seeds():
         S = sketch(p, A)
         out = hutchpp_estimate(S, S[:, J], P, G, float(np.sum(A * A)), 5, 10, 15)
         diffs.append((out["T"] - T_true) / np.sum(A * A))
+    d = np.array(diffs)
+    assert abs(d.mean()) < 3 * d.std(ddof=1) / math.sqrt(d.size)
+
+
+def test_hutchpp_unbiased_with_deflation_rank_below_t():
+    """NA-Hutch++ with l1 = 2 < t = 16 (split (2, 4, 24)): B = A (A_J P)^T has rank 16 > l1, so the
+    low-rank part B~ captures little and the Omega_3 correction (1/l3)[tr(O3 A (O3 A_J P)^T)
+    - tr(...)] carries most of tr(B); with P = A_J^+ A (flat spectrum, A_J P the
+    projection of A) tr(B) = ||A_J P||_F^2 > 0.  The estimate is unbiased: mean over 400
+    sketch seeds within 3 standard errors of the exact trace."""
+    rng = np.random.default_rng(23)
+    m, n, t, ell = 200, 48, 16, 30
+    A = rng.standard_normal((m, n))
+    J = np.arange(t)
+    P = np.linalg.pinv(A[:, J]) @ A
+    G = A[:, J].T @ A[:, J]
+    fro = float(np.sum(A * A))
+    T_true = float(np.trace(A @ (A[:, J] @ P).T))
+    diffs = []
+    for seed in range(400):
+        p = _params(m, t, ell, 0.0, seed=1000 + seed, split=(2, 4, 24))
+        S = sketch(p, A)
+        out = hutchpp_estimate(S, S[:, J], P, G, fro, 2, 4, 24)
+        diffs.append((out["T"] - T_true) / fro)
     d = np.array(diffs)
     assert abs(d.mean()) < 3 * d.std(ddof=1) / math.sqrt(d.size)
 
