@@ -246,6 +246,7 @@ def main():
             step(blocks[s % ring])
     torch.cuda.synchronize()
     eng.stats_reset()
+    st0 = eng.stats()                    # device counters (admissions, dirty slots) before the timed region
     if sharded:
         dist.barrier()
     torch.cuda.synchronize()
@@ -274,34 +275,65 @@ def main():
     value = K * block_bytes / (ms * 1e-3) / 1e9
     est_val = est_out.cpu().tolist()
 
-    # roofline of the dominant kernel (K1, fused ingest) on this rank
+    # roofline of the dominant kernel (K1, fused ingest) on this rank, as SURVEY.md section 8(d)
+    # defines it: t_roof = max(HBM read of the block, 2 l m b sketch flops at the chosen pipe's peak),
+    # frac = t_roof / t_K1 (DESIGN.md section 7 lists the per-unit figures)
     hbm, bf16, bf16_sus, src = peaks()
+    int8_tops = 2.0 * bf16_sus                      # B200 dense int8 = 2 x bf16 (nominal 4.5 / 2.25 PFLOP/s);
+                                                    # sustained: K1 is timed inside the long step
     k1_avg_ms = st["k1_ms"] / max(1, st["k1_launches"])
     k1_bytes = m_loc * b * dsz
     k1_flops = 2.0 * ell * m_loc * b
     mode = st["k1_mode_used"]
-    achieved_gbs = k1_bytes / (k1_avg_ms * 1e-3) / 1e9
-    if mode == oid.K1_TC_INT8:
-        # int8 dense = 2x the measured bf16 (B200 nominal ratio 4.5 / 2.25 PFLOP/s); sustained figure
-        # since K1 is timed inside the long step.  An fp64-exact sketch costs 7 int8 digit-plane MACs
-        # per multiply-add, so the pipe's effective fp64 peak is int8 / 7.
-        pipe_peak = 2 * bf16_sus * 1e12
-        slices = 7
-        pipe_time = slices * k1_flops / pipe_peak
-    else:
-        pipe_peak = bf16_sus * FP64_NOMINAL_TF / BF16_NOMINAL_TF * 1e12
-        pipe_time = k1_flops / pipe_peak
-    hbm_time = k1_bytes / (hbm * 1e9)
-    if hbm_time >= pipe_time:
-        roof = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s", "frac": achieved_gbs / hbm}
-    else:
-        ach = (k1_flops if mode != oid.K1_TC_INT8 else slices * k1_flops) / (k1_avg_ms * 1e-3) / 1e12
-        roof = {"bound": "tensor" if mode == oid.K1_TC_INT8 else "fp64",
-                "achieved": ach, "peak": pipe_peak / 1e12, "unit": "TFLOP/s", "frac": ach * 1e12 / pipe_peak}
-    roof["peak_source"] = src
-    roof["kernel"] = "k1_tc_int8" if mode == oid.K1_TC_INT8 else "k1_simt_kernel"
-    roof["traffic"] = _traffic_from_profiles(args.workload, mode)
-    roof["k1_ms"] = k1_avg_ms
+    t_hbm = k1_bytes / (hbm * 1e9) * 1e3
+    t_flop = k1_flops / (int8_tops * 1e12) * 1e3 if mode in (oid.K1_TC_INT8, oid.K1_TC_PAIR) else \
+        k1_flops / (bf16_sus * FP64_NOMINAL_TF / BF16_NOMINAL_TF * 1e12) * 1e3
+    t_roof = max(t_hbm, t_flop)
+    traffic, traffic_src = _traffic_from_profiles(args.workload, mode)
+    roof = {"bound": "hbm" if t_hbm >= t_flop else "tensor",
+            "achieved": k1_bytes / (k1_avg_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+            "frac": t_roof / k1_avg_ms, "traffic": traffic, "traffic_source": traffic_src,
+            "kernel": {oid.K1_TC_INT8: "k1_tc_kernel", oid.K1_TC_PAIR: "k1p::k1_tc_kernel"}.get(mode, "k1_simt_kernel"),
+            "k1_ms": k1_avg_ms, "hbm_roof_ms": t_hbm, "flop_roof_ms": t_flop, "peak_source": src,
+            "definition": "frac = max(block bytes / HBM peak, 2 l m b / int8 peak) / t_K1 (SURVEY 8(d)); "
+                          "t_K1 = CUDA events on the ingest stream inside the timed region"}
+    planes = (7 if dt == "f64" else 6) if mode == oid.K1_TC_INT8 else 6
+    emul = None
+    if mode in (oid.K1_TC_INT8, oid.K1_TC_PAIR):
+        ops = planes * k1_flops
+        emul = {"planes": planes, "int8_ops_per_launch": ops, "achieved_tops": ops / (k1_avg_ms * 1e-3) / 1e12,
+                "peak_tops": int8_tops, "frac": ops / (k1_avg_ms * 1e-3) / 1e12 / int8_tops,
+                "note": "exact fixed-point emulation: one int8 MAC per digit plane per sketch multiply-add"}
+    # sketch-entry (RNG) roof: l m_loc Gauss-16 entries per launch; ALU-pipe bound at 1.5 ALU ops per
+    # entry (Philox4x32-10: 20 LOP3 per 32 entries; Gauss-16 decode: 7 ALU ops per 8 entries, sm_100a
+    # SASS) on 148 SMs x 64 ALU lanes per clock
+    clk = clocks.get("sm_mhz") or 1965.0
+    entries = float(ell) * m_loc
+    rng_peak = 148 * 64 * clk * 1e6 / 1.5
+    rng = {"entries_per_launch": entries, "entries_per_s": entries / (k1_avg_ms * 1e-3),
+           "alu_ops_per_entry": 1.5, "peak_entries_per_s": rng_peak, "rng_roof_ms": entries / rng_peak * 1e3,
+           "frac": entries / rng_peak * 1e3 / k1_avg_ms, "sm_mhz": clk}
+    # A9 (exact basis Gram, one read of the basis slab per estimate) and the whole step
+    a9 = None
+    if st.get("a9_launches", 0):
+        a9_ms = st["a9_ms"] / st["a9_launches"]
+        basis_bytes = m_loc * k * dsz
+        nd = (st["dirty_slots"] - st0["dirty_slots"]) / max(1, st["estimates"] - st0["estimates"])
+        fp64_tf = bf16_sus * FP64_NOMINAL_TF / BF16_NOMINAL_TF
+        t_a9_hbm = basis_bytes / (hbm * 1e9) * 1e3
+        t_a9_flop = 2.0 * nd * k * m_loc / (fp64_tf * 1e12) * 1e3
+        a9 = {"kernel": "basis_gram_tc_kernel", "ms_per_launch": a9_ms, "bytes_per_launch": basis_bytes,
+              "achieved_gbs": basis_bytes / (a9_ms * 1e-3) / 1e9, "dirty_slots_per_estimate": nd,
+              "hbm_roof_ms": t_a9_hbm, "dmma_roof_ms": t_a9_flop, "fp64_tensor_peak_tflops": fp64_tf,
+              "frac": max(t_a9_hbm, t_a9_flop) / a9_ms}
+    adm = (st["admissions"] - st0["admissions"]) / K
+    step_bytes = block_bytes + (0 if args.no_estimate else m * k * dsz) + 2.0 * m * dsz * adm
+    step_roof = {"algorithmic_bytes_per_step": step_bytes, "admissions_per_step": adm,
+                 "hbm_floor_ms": step_bytes / (hbm * 1e9) * 1e3, "ms_per_step": ms / K,
+                 "frac": step_bytes / (hbm * 1e9) * 1e3 / (ms / K),
+                 "terms": "block read + basis read by the estimate (A9) + 2 column bytes per admission (A7)"}
+    latency = {"min_ms": st["lat_min_ms"], "median_ms": st["lat_med_ms"], "max_ms": st["lat_max_ms"],
+               "span": "start of the block's K1 to the end of its commit (ingest stream)"}
 
     # e2e through the public API with HOST buffers (pinned), H2D + D2H inside the timed region
     e2e = None
@@ -369,6 +401,11 @@ def main():
                                  + ("" if ring >= W + K else " (cycled)"),
                        "parallelism": f"rows sharded over {world} GPU(s)"},
             "roofline": roof,
+            "emulation_pipe": emul,
+            "rng": rng,
+            "a9": a9,
+            "step_roofline": step_roof,
+            "block_latency": latency,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clocks,
@@ -384,15 +421,19 @@ def main():
 
 
 def _traffic_from_profiles(workload, mode):
-    """dram bytes per K1 launch from the committed ncu capture, when it matches this workload/kernel."""
+    """dram bytes per K1 launch (read + write) copied from a committed ncu --set full capture of the
+    same kernel on the same workload (profiles/k1_traffic.json names the capture), or None."""
     path = os.path.join(ROOT, "profiles", "k1_traffic.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        key = f"{workload}:{'tc' if mode == 2 else 'simt'}"
-        return d.get(key)
+        key = f"{workload}:{ {2: 'tc', 3: 'pair'}.get(mode, 'simt') }"
+        ent = d.get(key)
+        if isinstance(ent, dict):
+            return ent.get("bytes"), "copied from " + ent.get("capture", "profiles/k1_traffic.json")
+        return ent, "copied from profiles/k1_traffic.json"
     except Exception:
-        return None
+        return None, None
 
 
 if __name__ == "__main__":

@@ -104,6 +104,13 @@ typedef struct {
   double est_ms;          /* summed CUDA-event time of error estimates                  */
   uint32_t flags;         /* OR of OID_FLAG_* seen so far (read at this call; syncs)     */
   int32_t k1_mode_used;   /* oid_k1_mode actually used by the last ingest               */
+  double a9_ms;           /* summed CUDA-event time of the basis-Gram kernel (A9, profile) */
+  int64_t a9_launches;    /* timed basis-Gram launches                                   */
+  int64_t admissions;     /* basis admissions so far (A6; each costs one A7 column copy)  */
+  int64_t dirty_slots;    /* slots whose Gram rows estimates recomputed (A9), summed      */
+  int64_t estimates;      /* estimates begun                                             */
+  double lat_min_ms, lat_med_ms, lat_max_ms;  /* per-block ingest latency, K1 start to the
+                             end of the commit (profile = 1; 0 when not measured)        */
 } oid_stats_t;
 
 /* Size in bytes of the device workspace oid_init needs for these parameters.
@@ -186,7 +193,9 @@ oid_status oid_gradient_finalize(oid_ctx ctx, double lo, double hi, double tol, 
    field: 0 J (k int64), 1 tau_old (k), 2 S (ell x n_obs), 3 Gram (ell x ell; 3 ell x 3 ell with
           the gradient variant),
           4 scalars [frob2, lambda_eff, E_k, shift, trace, dmax, min_margin, kappa],
-          5 last scores (k + ncols: basis slots then candidates), 6 eigenvalues of Gram (ell),
+          5 last scores (k + ncols: basis slots then candidates), 6 eigenvalues of Gram (ell; on the
+          tridiagonal fast path only the k largest, entries 0..k-1, are computed - the rest are
+          stale),
           7 last ingest partials ((ell+1) * ncols), 8 S_J^+ (k x ell),
           9 Jacobi rotation counts per sweep (3 x 48 int32: Gram, S_J, NA-Hutch++ core),
           10 K1 role timestamps of CTA 0 (10 x 4096 int64 clock64; recorded when the environment
@@ -200,6 +209,16 @@ oid_status oid_get(oid_ctx ctx, int32_t field, void* host_dst, size_t bytes, voi
 /* Counters and CUDA-event timings (synchronizes the context's recorded events).
    oid_stats_reset clears the launch counters and the recorded timings. */
 oid_status oid_stats(oid_ctx ctx, oid_stats_t* out);
+
+/* Run report (A12; the outputs of P:357 and the error metrics of P:729) as one JSON
+   object written to host memory buf (cap bytes, NUL-terminated): totals (n_obs, epochs,
+   estimates, OR of the OID_FLAG_* bits, admissions, dirty slots), "epoch_log" (per epoch: epoch,
+   n_obs, admissions, evictions, lambda_eff, E_k, the minimum decision margin of reading R14,
+   kappa(S_J) of Alg 4) and "estimate_log" (per estimate: the epoch it follows, the unclamped
+   ||E||^2 estimate e2, T, tr(G P P^T), ||A_obs||^2, the relative estimate, flags, kappa(S_J)).
+   At most n_cap rows each.  *needed (may be NULL) receives the size including the NUL.
+   Synchronizes `stream` and the library's streams.  Errors: OID_ESHAPE if cap is too small. */
+oid_status oid_report(oid_ctx ctx, char* buf, size_t cap, size_t* needed, void* stream);
 oid_status oid_stats_reset(oid_ctx ctx);
 
 /* Host-only: the Gauss-16 sketch-entry table (reading R2): for a 4-bit Philox draw n,

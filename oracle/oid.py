@@ -45,6 +45,8 @@ class OracleParams:
     seed: int = 0
     row_begin: int = 0     # this shard's global row range
     row_end: int = -1
+    omega_law: str = "gauss16"   # "gauss16" (reading R2, the build's law) or "gaussian" (the paper's
+                                 # randn; numpy draws, for the R2 ablation only - not the GPU's)
 
     @property
     def t(self):
@@ -72,6 +74,8 @@ def sketch(params, X, Qcache=None):
     X = np.asarray(X, dtype=np.float64)
     rb = params.row_begin
     m_loc = X.shape[0]
+    if params.omega_law == "gaussian":
+        return gaussian_omega(params)[:, rb:rb + m_loc] @ X
     acc = np.zeros((params.ell, X.shape[1]))
     chunk = 1 << 16
     for i0 in range(0, m_loc, chunk):
@@ -82,6 +86,19 @@ def sketch(params, X, Qcache=None):
             Q = omega_rows(params.seed, np.arange(params.ell), rb + i0, rb + i1)
         acc += Q @ X[i0:i1]
     return gauss16_scale() * acc
+
+
+def gaussian_omega(params):
+    """Omega = randn(l, m) with unit variance (reading R3), from numpy's PCG64 keyed on the
+    seed: the paper's Gaussian sketch for the R2 ablation."""
+    key = (params.seed, params.ell, params.m)
+    if _GAUSS_CACHE.get("key") != key:
+        _GAUSS_CACHE["key"] = key
+        _GAUSS_CACHE["Z"] = np.random.default_rng([params.seed, 0x5EED]).standard_normal((params.ell, params.m))
+    return _GAUSS_CACHE["Z"]
+
+
+_GAUSS_CACHE = {}
 
 
 def column_norms2(X):
@@ -270,7 +287,7 @@ class OracleOID:
         self.kappa = 1.0
         self.log = []
         self._Q = None
-        if cache_omega and ell * params.m_loc <= cache_limit:
+        if cache_omega and params.omega_law == "gauss16" and ell * params.m_loc <= cache_limit:
             rb = params.row_begin
             self._Q = omega_rows(params.seed, np.arange(ell), rb, rb + params.m_loc)
 

@@ -31,7 +31,7 @@ FLAG_NONFINITE_INPUT, FLAG_SJ_RANK_DEFICIENT, FLAG_E2_NEGATIVE, FLAG_K1_RECOMPUT
 EXPORTED = ["oid_workspace_query", "oid_init", "oid_ingest_block", "oid_ingest_sketch", "oid_ingest_commit",
             "oid_partials", "oid_estimate_begin", "oid_estimate_end", "oid_error_estimate", "oid_finalize", "oid_get",
             "oid_stats", "oid_stats_reset", "oid_sketch_table", "oid_destroy", "oid_last_error", "oid_version",
-            "oid_gradient_gcv", "oid_gradient_coefficients", "oid_gradient_finalize"]
+            "oid_gradient_gcv", "oid_gradient_coefficients", "oid_gradient_finalize", "oid_report"]
 
 
 class OidParams(ctypes.Structure):
@@ -48,7 +48,10 @@ class OidParams(ctypes.Structure):
 class OidStats(ctypes.Structure):
     _fields_ = [("n_obs", ctypes.c_int64), ("epochs", ctypes.c_int64), ("launches", ctypes.c_int64),
                 ("k1_launches", ctypes.c_int64), ("k1_ms", ctypes.c_double), ("post_ms", ctypes.c_double),
-                ("est_ms", ctypes.c_double), ("flags", ctypes.c_uint32), ("k1_mode_used", ctypes.c_int32)]
+                ("est_ms", ctypes.c_double), ("flags", ctypes.c_uint32), ("k1_mode_used", ctypes.c_int32),
+                ("a9_ms", ctypes.c_double), ("a9_launches", ctypes.c_int64), ("admissions", ctypes.c_int64),
+                ("dirty_slots", ctypes.c_int64), ("estimates", ctypes.c_int64), ("lat_min_ms", ctypes.c_double),
+                ("lat_med_ms", ctypes.c_double), ("lat_max_ms", ctypes.c_double)]
 
 
 _vp, _i64, _i32, _dp = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_double)
@@ -70,6 +73,7 @@ _sig = {
     "oid_gradient_gcv": [_vp, ctypes.c_double, _dp, _vp],
     "oid_gradient_coefficients": [_vp, ctypes.c_double, _vp, _vp],
     "oid_gradient_finalize": [_vp, ctypes.c_double, ctypes.c_double, ctypes.c_double, _dp, _vp, _vp],
+    "oid_report": [_vp, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t), _vp],
 }
 for _n, _a in _sig.items():
     getattr(_lib, _n).argtypes = _a
@@ -174,7 +178,7 @@ class Engine:
         if X.dim() != 2 or X.shape[0] != self.m_loc:
             raise ValueError(f"block must have shape (m_loc={self.m_loc}, ncols)")
         ncols = X.shape[1]
-        if ncols > 1 and X.stride(0) != 1:
+        if self.m_loc > 1 and X.stride(0) != 1:
             raise ValueError("block must be column-major (X.stride(0) == 1); pass Xt.T for a (ncols, m) tensor")
         ld = X.stride(1) if ncols > 1 else self.m_loc
         return ctypes.c_void_p(X.data_ptr()), ld, ncols
@@ -277,6 +281,15 @@ class Engine:
         s = OidStats()
         self._check(_lib.oid_stats(self.h, ctypes.byref(s)), "oid_stats")
         return {f: getattr(s, f) for f, _ in OidStats._fields_}
+
+    def report(self):
+        """Run report (include/oid.h oid_report): totals, per-epoch and per-estimate logs, as a dict."""
+        import json
+        need = ctypes.c_size_t()
+        _lib.oid_report(self.h, None, 0, ctypes.byref(need), self._st())
+        buf = ctypes.create_string_buffer(need.value)
+        self._check(_lib.oid_report(self.h, buf, need.value, ctypes.byref(need), self._st()), "oid_report")
+        return json.loads(buf.value.decode())
 
     def stats_reset(self):
         self._check(_lib.oid_stats_reset(self.h), "oid_stats_reset")

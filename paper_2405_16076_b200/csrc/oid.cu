@@ -4,12 +4,14 @@
 // The caller owns all device memory (one workspace buffer, sized by oid_workspace_query);
 // every step runs in the kernels below on the caller's stream; the host never waits during
 // ingest.  See DESIGN.md sections 1 and 6 for the kernel list and the data layout.
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <string>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -108,10 +110,13 @@ struct Bump {
 struct Layout {
   size_t S, gram, Ypart, k1part, k1npart, gB, gV, mu, mu_sorted, Yc, Tsc, tau, scal, J, tau_old, admit, counts,
       flags, counters, C, SJ, sjB, sjV, sjsig, sjw, sjZ, Sjpinv, Pexp, AJP, G, Gsum, Gpart, cB, cV, csig, cw, cZ, M,
-      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, wyT, sjG, cG, cBt, cZ2, dbg, Jsnap, Dsnap, gcnt, S1, S2, YpG, GX, OGO, gH, gHV, gHs, gHw, gHZ, gHp, gR, gCm, gE, gLst, gLV, gLs, gLw, gLZ, gLp, gRhs, gscal, td2, te2, Vh2, tauv2, wyT2, ldl2, mu2, total;
+      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, wyT, sjG, cG, cBt, cZ2, dbg, Jsnap, Dsnap, gcnt, S1, S2, YpG, GX, OGO, gH, gHV, gHs, gHw, gHZ, gHp, gR, gCm, gE, gLst, gLV, gLs, gLw, gLZ, gLp, gRhs, gscal, td2, te2, Vh2, tauv2, wyT2, ldl2, mu2, cum, elog, eslog, total;
 };
 
 int64_t m_local(const oid_params& p) { return p.row_end - p.row_begin; }
+constexpr int kElogCols = 8;   // report row: epoch log [epoch, n_obs, admissions, evictions, lambda, E_k,
+                               // min margin, kappa(S_J)]; estimate log [epoch, e2, T, gpp, frob2, est_rel,
+                               // flags, kappa]
 size_t dsize(const oid_params& p) { return p.dtype == OID_F64 ? 8 : 4; }
 
 Layout make_layout(const oid_params& p) {
@@ -139,6 +144,9 @@ Layout make_layout(const oid_params& p) {
   L.tau_old = b.take(t * d);
   L.admit = b.take(2 * (t + bm) * sizeof(int));
   L.counts = b.take(4 * sizeof(int));
+  L.cum = b.take(4 * sizeof(unsigned long long));   // [admissions, dirty slots at estimates, estimates]
+  L.elog = b.take(n * kElogCols * d);                 // per-epoch report rows (A12)
+  L.eslog = b.take(n * kElogCols * d);                // per-estimate report rows (A12)
   L.flags = b.take(4 * sizeof(unsigned));
   L.counters = b.take(kNumJacobiUses * kMaxSweeps * sizeof(int));
   {
@@ -293,7 +301,7 @@ struct oid_ctx_s {
   CUtensorMap bg_map{};       // basis slab C as a 2-D tensor {m_loc rows, t columns}
   bool cold_jacobi = false;   // diagnostics: OID_JACOBI_COLD=1 disables the warm starts
   bool k1_debug = false;      // diagnostics: OID_K1_DEBUG=1 records K1 role timestamps (oid_get 10)
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_k1, ev_post, ev_est;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_k1, ev_post, ev_est, ev_a9;
   // Side stream (highest priority) for the latency-bound chains that do not depend on the
   // HBM-bound kernels of the caller's stream: the Alg 4 factorisation (A8) runs beside the basis
   // copy (A7) and the basis-Gram-independent part of Alg 8 (A10) beside the basis Gram (A9).
@@ -714,7 +722,8 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   select_kernel<<<1, 256, 0, st>>>(ctx->ptr<int64_t>(L.J), ctx->d(L.tau_old), ctx->d(L.tau), Yp + int64_t(ell) * nc, t, nc,
                                   ctx->factor, static_cast<uint32_t>(ctx->epoch), ctx->n_obs, ctx->key0, ctx->key1,
                                   ctx->ptr<int>(L.admit), ctx->ptr<int>(L.counts), scal, ctx->ptr<int>(L.dirty),
-                                  static_cast<int>(ctx->epoch + 1));
+                                  static_cast<int>(ctx->epoch + 1), ctx->ptr<unsigned long long>(L.cum),
+                                  ctx->d(L.elog) + static_cast<size_t>(ctx->epoch) * kElogCols);
   CKL();
   // A8 runs on the side stream, beside the basis copy
   s = fork_side(ctx, st);
@@ -770,6 +779,8 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
                     Sjpinvp, scal + SC_KAPPA_SNAP + par, OID_FLAG_SJ_RANK_DEFICIENT, fb);
   if (s != OID_OK) return s;
   CK(cudaMemcpyAsync(scal + SC_KAPPA, scal + SC_KAPPA_SNAP + par, sizeof(double), cudaMemcpyDeviceToDevice, cs));
+  log_scalar_kernel<<<1, 32, 0, cs>>>(scal + SC_KAPPA_SNAP + par, ctx->d(L.elog) + static_cast<size_t>(ctx->epoch) * kElogCols + 7);
+  CKL();
   CK(cudaEventRecord(ctx->ev_sj_done[par], cs));
   tl_mark(ctx, cs, 12);
   // snapshot of this epoch for an estimate that may overlap the next commit (after the
@@ -1009,7 +1020,7 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
   ctx->p = *p;
   ctx->L = make_layout(*p);
   if (!workspace || bytes < ctx->L.total || (reinterpret_cast<uintptr_t>(workspace) & 255)) {
-    delete ctx;
+    oid_destroy(ctx);   // releases the streams / events created so far
     return OID_ESHAPE;
   }
   ctx->ws = static_cast<char*>(workspace);
@@ -1033,7 +1044,7 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   auto bad = [&](cudaError_t e) {
     snprintf(g_init_err, sizeof(g_init_err), "init: %s", cudaGetErrorString(e));
-    delete ctx;
+    oid_destroy(ctx);   // releases the streams / events created so far
     return OID_ECUDA;
   };
   cudaError_t e = cudaSetDevice(p->device);
@@ -1120,7 +1131,7 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
     const int64_t ntiles = (ctx->m_loc + RL - 1) / RL;
     if (k1tc_encoder() == nullptr) {
       snprintf(g_init_err, sizeof(g_init_err), "init: cuTensorMapEncodeTiled unavailable");
-      delete ctx;
+      oid_destroy(ctx);   // releases the streams / events created so far
       return OID_ECUDA;
     }
     const cuuint64_t dims[3] = {static_cast<cuuint64_t>(RL), static_cast<cuuint64_t>(ctx->t), static_cast<cuuint64_t>(ntiles)};
@@ -1133,7 +1144,7 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) {
       snprintf(g_init_err, sizeof(g_init_err), "init: basis tensor map encoding failed (%d)", static_cast<int>(cr));
-      delete ctx;
+      oid_destroy(ctx);   // releases the streams / events created so far
       return OID_ECUDA;
     }
     const int bgmax = 200 * 1024 + 1024;
@@ -1166,6 +1177,9 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
   if ((e = cudaMemsetAsync(ctx->ws + L.Gfull, 0, sizeof(double) * ctx->t * ctx->t, st)) != cudaSuccess) return bad(e);
   if ((e = cudaMemsetAsync(ctx->ws + L.dirty, 0, sizeof(int) * ctx->t, st)) != cudaSuccess) return bad(e);
   if ((e = cudaMemsetAsync(ctx->ws + L.counts, 0, 4 * sizeof(int), st)) != cudaSuccess) return bad(e);
+  if ((e = cudaMemsetAsync(ctx->ws + L.cum, 0, 4 * sizeof(unsigned long long), st)) != cudaSuccess) return bad(e);
+  if ((e = cudaMemsetAsync(ctx->ws + L.elog, 0, sizeof(double) * kElogCols * p->n_cap, st)) != cudaSuccess) return bad(e);
+  if ((e = cudaMemsetAsync(ctx->ws + L.eslog, 0, sizeof(double) * kElogCols * p->n_cap, st)) != cudaSuccess) return bad(e);
   if ((e = cudaMemsetAsync(ctx->ws + L.gcnt, 0, 8 * sizeof(int), st)) != cudaSuccess) return bad(e);
   {
     const int64_t RL = 128 / static_cast<int64_t>(dsize(*p));
@@ -1247,7 +1261,8 @@ oid_status oid_estimate_begin(oid_ctx ctx, void* stream) {
   int* dl = ctx->ptr<int>(L.dlist) + static_cast<size_t>(gp) * t;
   int* gc = ctx->ptr<int>(L.gcnt) + 4 * gp;
   double* Gs = ctx->d(L.Gsum) + static_cast<size_t>(gp) * t * t;
-  dirty_compact_kernel<<<1, 32, 0, gs>>>(ctx->ptr<int>(L.Dsnap) + static_cast<size_t>(par) * t, t, ctx->last_est_tag, dl, gc);
+  dirty_compact_kernel<<<1, 32, 0, gs>>>(ctx->ptr<int>(L.Dsnap) + static_cast<size_t>(par) * t, t, ctx->last_est_tag, dl, gc,
+                                         ctx->ptr<unsigned long long>(L.cum));
   CKL();
   ctx->last_est_tag = static_cast<int>(ctx->epoch);   // newest admission tag of this state
   // A10 factors that do not need G: on the second side stream, concurrently with A9 below
@@ -1295,13 +1310,16 @@ oid_status oid_estimate_begin(oid_ctx ctx, void* stream) {
       lc.attrs = la;
       lc.numAttrs = 1;
     }
-    if (f64)
-      CK(cudaLaunchKernelEx(&lc, bgtc::basis_gram_tc_kernel<double>, ctx->bg_map, ntiles, t, per, nstage, stage_bytes,
-                            nbox, static_cast<const int*>(dl), static_cast<const int*>(gc), ctx->d(L.Gpart)));
-    else
-      CK(cudaLaunchKernelEx(&lc, bgtc::basis_gram_tc_kernel<float>, ctx->bg_map, ntiles, t, per, nstage, stage_bytes,
-                            nbox, static_cast<const int*>(dl), static_cast<const int*>(gc), ctx->d(L.Gpart)));
-    CKL();
+    {
+      EvScope eva9(ctx, gs, &ctx->ev_a9);
+      if (f64)
+        CK(cudaLaunchKernelEx(&lc, bgtc::basis_gram_tc_kernel<double>, ctx->bg_map, ntiles, t, per, nstage, stage_bytes,
+                              nbox, static_cast<const int*>(dl), static_cast<const int*>(gc), ctx->d(L.Gpart)));
+      else
+        CK(cudaLaunchKernelEx(&lc, bgtc::basis_gram_tc_kernel<float>, ctx->bg_map, ntiles, t, per, nstage, stage_bytes,
+                              nbox, static_cast<const int*>(dl), static_cast<const int*>(gc), ctx->d(L.Gpart)));
+      CKL();
+    }
     CK(cudaEventRecord(ctx->ev_gram_done, gs));
     tl_mark(ctx, gs, 9);
     // two-level fixed-order sum: up to 64 segment sums into the tail of Gpart, then one
@@ -1360,6 +1378,11 @@ oid_status oid_estimate_end(oid_ctx ctx, double* out_dev, void* stream) {
   hutch_final_kernel<<<1, 32, 0, cs>>>(scal, p.ell3, ctx->ptr<unsigned>(L.flags), ctx->d(L.est));
   CKL();
   if (out_dev) CK(cudaMemcpyAsync(out_dev, ctx->d(L.est), 8 * sizeof(double), cudaMemcpyDeviceToDevice, cs));
+  if (ctx->n_est <= p.n_cap) {
+    est_log_kernel<<<1, 32, 0, cs>>>(ctx->d(L.est), static_cast<double>(ctx->epoch - 1),
+                                     ctx->d(L.eslog) + static_cast<size_t>(ctx->n_est - 1) * kElogCols);
+    CKL();
+  }
   CK(cudaEventRecord(ctx->ev_snap_free[par], cs));   // this parity's snapshot may be rewritten
   s = join_from(ctx, st, cs);
   if (s != OID_OK) return s;
@@ -1544,18 +1567,102 @@ oid_status oid_stats(oid_ctx ctx, oid_stats_t* out) {
   CK(sum(ctx->ev_k1, &out->k1_ms));
   CK(sum(ctx->ev_post, &out->post_ms));
   CK(sum(ctx->ev_est, &out->est_ms));
+  CK(sum(ctx->ev_a9, &out->a9_ms));
+  out->a9_launches = static_cast<int64_t>(ctx->ev_a9.size());
+  // per-block ingest latency: start of the block's K1 to the end of its commit (one K1 per block
+  // on the plain path; the gradient variant runs three)
+  {
+    const size_t nb = ctx->ev_post.size();
+    const size_t per = nb ? ctx->ev_k1.size() / nb : 0;
+    std::vector<double> lat;
+    if (per >= 1 && ctx->ev_k1.size() == per * nb) {
+      for (size_t i = 0; i < nb; ++i) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ctx->ev_k1[i * per].first, ctx->ev_post[i].second));
+        lat.push_back(ms);
+      }
+    }
+    if (!lat.empty()) {
+      std::sort(lat.begin(), lat.end());
+      out->lat_min_ms = lat.front();
+      out->lat_med_ms = lat[lat.size() / 2];
+      out->lat_max_ms = lat.back();
+    }
+  }
   unsigned f = 0;
   CK(cudaStreamSynchronize(ctx->side));
   CK(cudaStreamSynchronize(ctx->side2));
   CK(cudaEventSynchronize(ctx->ev_est_done));
+  CK(cudaStreamSynchronize(ctx->side3));
+  CK(cudaStreamSynchronize(ctx->gs));
+  CK(cudaEventSynchronize(ctx->ev_committed));
   CK(cudaMemcpy(&f, ctx->ws + ctx->L.flags, sizeof(unsigned), cudaMemcpyDeviceToHost));
   out->flags = f;
+  unsigned long long cum[4] = {0, 0, 0, 0};
+  CK(cudaMemcpy(cum, ctx->ws + ctx->L.cum, sizeof(cum), cudaMemcpyDeviceToHost));
+  out->admissions = static_cast<int64_t>(cum[0]);
+  out->dirty_slots = static_cast<int64_t>(cum[1]);
+  out->estimates = static_cast<int64_t>(cum[2]);
+  return OID_OK;
+}
+
+oid_status oid_report(oid_ctx ctx, char* buf, size_t cap, size_t* needed, void* stream) {
+  if (!ctx) return OID_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CK(cudaStreamSynchronize(st));
+  for (cudaStream_t sp : {ctx->side, ctx->side2, ctx->side3, ctx->gs})
+    if (sp) CK(cudaStreamSynchronize(sp));
+  CK(cudaEventSynchronize(ctx->ev_est_done));
+  const int64_t ne = std::min<int64_t>(ctx->epoch, ctx->p.n_cap);
+  const int64_t nest = std::min<int64_t>(ctx->n_est, ctx->p.n_cap);
+  std::vector<double> el(static_cast<size_t>(std::max<int64_t>(1, ne)) * kElogCols),
+      es(static_cast<size_t>(std::max<int64_t>(1, nest)) * kElogCols);
+  if (ne) CK(cudaMemcpy(el.data(), ctx->ws + ctx->L.elog, sizeof(double) * kElogCols * ne, cudaMemcpyDeviceToHost));
+  if (nest) CK(cudaMemcpy(es.data(), ctx->ws + ctx->L.eslog, sizeof(double) * kElogCols * nest, cudaMemcpyDeviceToHost));
+  unsigned f = 0;
+  CK(cudaMemcpy(&f, ctx->ws + ctx->L.flags, sizeof(unsigned), cudaMemcpyDeviceToHost));
+  unsigned long long cum[4] = {0, 0, 0, 0};
+  CK(cudaMemcpy(cum, ctx->ws + ctx->L.cum, sizeof(cum), cudaMemcpyDeviceToHost));
+  std::string j;
+  char tmp[512];
+  auto num = [&](double v) {
+    if (std::isfinite(v)) snprintf(tmp, sizeof(tmp), "%.17g", v);
+    else snprintf(tmp, sizeof(tmp), "%s", std::isnan(v) ? "\"nan\"" : (v > 0 ? "\"inf\"" : "\"-inf\""));
+    return std::string(tmp);
+  };
+  snprintf(tmp, sizeof(tmp),
+           "{\"n_obs\": %lld, \"epochs\": %lld, \"estimates\": %lld, \"flags\": %u, \"admissions\": %llu, "
+           "\"dirty_slots_at_estimates\": %llu, \"k\": %d, \"ell\": %d, \"lambda_mode\": ",
+           static_cast<long long>(ctx->n_obs), static_cast<long long>(ctx->epoch), static_cast<long long>(ctx->n_est), f,
+           cum[0], cum[1], ctx->p.k, ctx->p.ell);
+  j += tmp;
+  j += num(ctx->p.lambda);
+  j += ", \"epoch_log\": [";
+  for (int64_t e = 0; e < ne; ++e) {
+    const double* r = el.data() + e * kElogCols;
+    j += e ? ", " : "";
+    j += "{\"epoch\": " + num(r[0]) + ", \"n_obs\": " + num(r[1]) + ", \"admissions\": " + num(r[2]) +
+         ", \"evictions\": " + num(r[3]) + ", \"lambda_eff\": " + num(r[4]) + ", \"E_k\": " + num(r[5]) +
+         ", \"min_margin\": " + num(r[6]) + ", \"kappa_SJ\": " + num(r[7]) + "}";
+  }
+  j += "], \"estimate_log\": [";
+  for (int64_t q = 0; q < nest; ++q) {
+    const double* r = es.data() + q * kElogCols;
+    j += q ? ", " : "";
+    j += "{\"after_epoch\": " + num(r[0]) + ", \"e2\": " + num(r[1]) + ", \"T\": " + num(r[2]) +
+         ", \"gpp\": " + num(r[3]) + ", \"frob2\": " + num(r[4]) + ", \"est_rel\": " + num(r[5]) +
+         ", \"flags\": " + num(r[6]) + ", \"kappa_SJ\": " + num(r[7]) + "}";
+  }
+  j += "]}";
+  if (needed) *needed = j.size() + 1;
+  if (!buf || cap < j.size() + 1) return ctx->fail(OID_ESHAPE, "report needs %zu bytes (cap %zu)", j.size() + 1, cap);
+  std::memcpy(buf, j.c_str(), j.size() + 1);
   return OID_OK;
 }
 
 oid_status oid_stats_reset(oid_ctx ctx) {
   if (!ctx) return OID_EINVAL;
-  for (auto* v : {&ctx->ev_k1, &ctx->ev_post, &ctx->ev_est}) {
+  for (auto* v : {&ctx->ev_k1, &ctx->ev_post, &ctx->ev_est, &ctx->ev_a9}) {
     for (auto& pr : *v) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
     v->clear();
   }

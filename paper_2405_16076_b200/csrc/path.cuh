@@ -98,7 +98,8 @@ __global__ void __launch_bounds__(256) select_kernel(int64_t* __restrict__ J, do
                                                       const double* __restrict__ tau, const double* __restrict__ nrm, int t,
                                                       int nc, double factor, uint32_t epoch, int64_t base, uint32_t key0,
                                                       uint32_t key1, int* __restrict__ admit, int* __restrict__ counts,
-                                                      double* __restrict__ scal, int* __restrict__ dirty, int dtag) {
+                                                      double* __restrict__ scal, int* __restrict__ dirty, int dtag,
+                                                      unsigned long long* __restrict__ cum, double* __restrict__ elog) {
   // The decisions are sequential only through the candidates consumed by earlier slots: the
   // eviction of slot i depends on slot i alone (steps 16-19), so
   //   (1) the evictions are decided in parallel, one thread per slot;
@@ -175,15 +176,37 @@ __global__ void __launch_bounds__(256) select_kernel(int64_t* __restrict__ J, do
       }
     }
     if (lane == 0) { counts[0] = na; counts[1] = nz; }
+    if (lane == 0 && cum) cum[0] += static_cast<unsigned long long>(na);
+  }
+  // per-epoch report row (A12): evictions (slots vacated this epoch, refilled or not)
+  {
+    int ne = 0;
+    for (int i = threadIdx.x; i < t; i += blockDim.x) ne += s_ev[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ne += __shfl_xor_sync(0xffffffffu, ne, o);
+    __shared__ int s_ne[8];
+    if ((threadIdx.x & 31) == 0) s_ne[threadIdx.x >> 5] = ne;
+    __syncthreads();
+    if (threadIdx.x == 0 && elog) {
+      int tot = 0;
+      for (int q = 0; q < static_cast<int>(blockDim.x >> 5); ++q) tot += s_ne[q];
+      elog[0] = static_cast<double>(epoch);
+      elog[1] = static_cast<double>(base + nc);
+      elog[2] = static_cast<double>(counts[0]);
+      elog[3] = static_cast<double>(tot);
+      elog[4] = scal[SC_LAM];
+      elog[5] = scal[SC_EK];
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mm = fmin(mm, __shfl_xor_sync(0xffffffffu, mm, o));
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = mm;
   __syncthreads();
   if (threadIdx.x == 0) {
-    double m = scal[SC_MINMARGIN];
-    for (int q = 0; q < static_cast<int>(blockDim.x >> 5); ++q) m = fmin(m, s_red[q]);
-    scal[SC_MINMARGIN] = m;
+    double me = INFINITY;
+    for (int q = 0; q < static_cast<int>(blockDim.x >> 5); ++q) me = fmin(me, s_red[q]);
+    scal[SC_MINMARGIN] = fmin(scal[SC_MINMARGIN], me);
+    if (elog) elog[6] = me;
   }
 }
 
@@ -301,12 +324,28 @@ __global__ void est_scalars_kernel(double* __restrict__ scal, int par) {
 // Slots admitted after the last estimate (admission tags > last_tag), compacted in slot order;
 // counts[2] = number of such (dirty) slots.  Tags are never cleared (no race with the next commit).
 __global__ void dirty_compact_kernel(const int* __restrict__ dtag, int t, int last_tag, int* __restrict__ list,
-                                     int* __restrict__ counts) {
+                                     int* __restrict__ counts, unsigned long long* __restrict__ cum) {
   if (threadIdx.x != 0) return;
   int c = 0;
   for (int i = 0; i < t; ++i)
     if (dtag[i] > last_tag) list[c++] = i;
   counts[2] = c;
+  if (cum) { cum[1] += static_cast<unsigned long long>(c); cum[2] += 1ull; }
+}
+
+// per-estimate report row (A12): [epoch, e2, T, gpp, frob2, est_rel, flags, kappa] from est[8] =
+// [e2, T, gpp, frob2, est_abs, est_rel, flags, kappa]
+__global__ void est_log_kernel(const double* __restrict__ est, double epoch, double* __restrict__ dst) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    dst[0] = epoch;
+    dst[1] = est[0]; dst[2] = est[1]; dst[3] = est[2]; dst[4] = est[3];
+    dst[5] = est[5]; dst[6] = est[6]; dst[7] = est[7];
+  }
+}
+
+// copies a scalar of the state into a report row (the kappa of an epoch's S_J, once A8 has run)
+__global__ void log_scalar_kernel(const double* __restrict__ src, double* __restrict__ dst) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *dst = *src;
 }
 
 // G(d_q, j) = G(j, d_q) = D(q, j) for the dirty slots (after the cross-shard reduction).

@@ -58,10 +58,15 @@ class ShardedIngest:
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
 
     def ingest(self, X):
-        """One block (this rank's rows, column-major m_loc x ncols)."""
-        self.engine.ingest_sketch(X)
-        self._reduce(self.engine.partials(0))
-        self.engine.ingest_commit(X)
+        """One block (this rank's rows, column-major m_loc x ncols).  The all-reduce runs on the
+        engine's ingest stream (torch.distributed enqueues on the current stream), between the
+        sketch that writes the partials and the commit that reads them."""
+        st = getattr(self.engine, "stream", None)
+        ctx = torch.cuda.stream(st) if st is not None and self.world > 1 else _null()
+        with ctx:
+            self.engine.ingest_sketch(X)
+            self._reduce(self.engine.partials(0))
+            self.engine.ingest_commit(X)
 
     def estimate(self, out=None):
         """NA-Hutch++ estimate (Alg 8); out: 8 fp64 values (see include/oid.h).  The reduction runs

@@ -1,5 +1,5 @@
 """CPU-side checks of the C ABI: the library loads, exports every symbol include/oid.h declares,
-validates parameters, and its Gauss-256 table equals the oracle's (built independently)."""
+validates parameters, and its Gauss-16 table equals the oracle's (built independently)."""
 
 import ctypes
 import os
@@ -69,4 +69,6 @@ def test_struct_layout_matches_header(oid):
     # then the gradient-variant block: 4 int32 + 2 double = 32 bytes
     assert ctypes.sizeof(oid.OidParams) == 144
     assert oid.OidParams.grad_nfields.offset == 112 and oid.OidParams.grad_hx.offset == 128
-    assert ctypes.sizeof(oid.OidStats) == 4 * 8 + 3 * 8 + 8
+    # oid_stats_t: 4 int64 + 3 double + uint32 + int32, then a9_ms, 4 int64, 3 double
+    assert ctypes.sizeof(oid.OidStats) == 4 * 8 + 3 * 8 + 8 + 8 + 4 * 8 + 3 * 8
+    assert oid.OidStats.a9_ms.offset == 64 and oid.OidStats.lat_max_ms.offset == 120
