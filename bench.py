@@ -26,11 +26,30 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
-    # name: (grid, b, k, ell, dtype, description)
-    "C3": ((192, 129, 192), 32, 200, 512, "f64",
+    # name: (generator spec, b, k, ell, dtype, description)
+    "C3": (("channel", (192, 129, 192)), 32, 200, 512, "f64",
            "C3 channel-flow stand-in: 3 components on 192x129x192 (m=14,266,368) fp64, b=32, k=200, l=512"),
-    "C3r": ((48, 33, 48), 32, 200, 512, "f64", "C3r: C3 on a 48x33x48 grid (m=228,096)"),
+    "C3r": (("channel", (48, 33, 48)), 32, 200, 512, "f64", "C3r: C3 on a 48x33x48 grid (m=228,096)"),
+    "C5": (("lowrank", 1 << 27), 64, 400, 1024, "f32",
+           "C5 scaling sweep: m=2^27 fp32 rows split over the GPUs, rank-500 (sigma_i=i^-1.5) + 1e-5 noise, "
+           "n=4096, b=64, k=400, l=1024"),
+    "C5r": (("lowrank", 1 << 18), 64, 400, 1024, "f32", "C5r: C5 with m=2^18 rows"),
 }
+
+
+def make_gen(workload):
+    from synth import ChannelFlow, LowRankStream
+    (kind, arg) = WORKLOADS[workload][0]
+    return ChannelFlow(*arg, seed=1003) if kind == "channel" else LowRankStream(m=arg, seed=1005)
+
+
+def host_rows(workload, gen, t0, t1, rows):
+    """Rows [0, rows) of a block on the host (numpy, the generator's host formula)."""
+    if WORKLOADS[workload][0][0] == "channel":
+        return _host_rows(gen, t0, t1, rows)
+    return gen.block(t0, t1, 0, rows).astype("float64")
+
+
 METRIC = "snapshot ingest GB/s (sketch+CSS+Hutch++) at 1/2/4/8 B200; % of roofline"
 FP64_NOMINAL_TF, BF16_NOMINAL_TF = 40.0, 2250.0    # B200 datasheet ratio used to derive the fp64 peak
 
@@ -113,15 +132,14 @@ def oracle_sample(workload, rows, steps=1, warmup=0):
     Returns (GB/s over the timed steps, seconds per step, BLAS threads, sample description).
     """
     from oracle import OracleParams, OracleOID
-    from synth import ChannelFlow
-    grid, b, k, ell, dt, _ = WORKLOADS[workload]
-    gen = ChannelFlow(*grid, seed=1003)
+    _, b, k, ell, dt, _ = WORKLOADS[workload]
+    gen = make_gen(workload)
     m = gen.m
     rows = min(rows, m)
     sp = (ell // 6, ell // 3, ell - ell // 6 - ell // 3)
     o = OracleOID(OracleParams(m=m, k=k, ell=ell, ell1=sp[0], ell2=sp[1], ell3=sp[2], lam=-1.0, seed=0,
                                row_begin=0, row_end=rows), cache_omega=False)
-    blocks = [_host_rows(gen, s * b, (s + 1) * b, rows) for s in range(warmup + steps)]
+    blocks = [host_rows(workload, gen, s * b, (s + 1) * b, rows) for s in range(warmup + steps)]
     for X in blocks[:warmup]:
         o.ingest_block(X)
         o.error_estimate()
@@ -192,14 +210,13 @@ def main():
     from __graft_entry__ import build
     build()
     import paper_2405_16076_b200 as oid
-    from synth import ChannelFlow
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    grid, b, k, ell, dt, desc = WORKLOADS[args.workload]
-    gen = ChannelFlow(*grid, seed=1003)
+    _, b, k, ell, dt, desc = WORKLOADS[args.workload]
+    gen = make_gen(args.workload)
     m = gen.m
     from paper_2405_16076_b200.sharded import ShardedIngest, row_slab
     rb, re = row_slab(m, rank, world)
@@ -213,6 +230,16 @@ def main():
     free = torch.cuda.mem_get_info(dev)[0]
     blk_bytes_loc = (re - rb) * b * dsz
     ws_bytes = oid.workspace_bytes(oid.make_params(m=m, k=k, ell=ell, b_max=b, n_cap=n_cap, lam=-1.0, split=(ell // 6, ell // 3, ell - ell // 6 - ell // 3), seed=0, dtype=dt, row_begin=rb, row_end=re))
+    if ws_bytes + 2 * blk_bytes_loc + (4 << 30) > free:
+        # e.g. C5 at N = 1: the 400-column basis alone is 215 GB; E(P) is taken from P = 2
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "n_gpus": world, "config": {"workload": desc},
+                              "unavailable": f"workspace {ws_bytes / 1e9:.1f} GB + two blocks of "
+                                             f"{blk_bytes_loc / 1e9:.1f} GB exceed the {free / 1e9:.0f} GB free "
+                                             f"on this GPU at {world} GPU(s)"}), flush=True)
+        if world > 1:
+            dist.destroy_process_group()
+        return
     ring = max(2, min(W + K, int((free - ws_bytes - (8 << 30)) // blk_bytes_loc)))
     split = (ell // 6, ell // 3, ell - ell // 6 - ell // 3)
     p = oid.make_params(m=m, k=k, ell=ell, b_max=b, n_cap=n_cap, lam=-1.0, split=split, seed=0, dtype=dt,

@@ -90,7 +90,11 @@ typedef struct {
      augmented sketch [Omega a; Omega G^1 a; Omega G^2 a] and the augmented energy; the
      estimate keeps Alg 4's P; oid_gradient_* give P(mu) and the sketched GCV.  Requires a single
      shard (row_begin = 0, row_end = m), grad_nfields grad_nx grad_ny = m and 3 ell <= 1024.  */
-  int32_t grad_nfields, grad_nx, grad_ny, grad_pad;
+  int32_t grad_nfields, grad_nx, grad_ny;
+  int32_t omega_cache; /* NEXT-3 ablation: 1 = store the sketch entries (their Philox words,
+                          ell * m_loc / 2 bytes of workspace, filled at oid_init) and stream them
+                          into the tensor-core K1 instead of generating them; 0 = generate in
+                          registers (the default).  Same entries, bitwise-identical results.   */
   double grad_hx, grad_hy;
 } oid_params;
 

@@ -42,7 +42,7 @@ class OidParams(ctypes.Structure):
                 ("seed", ctypes.c_uint64), ("dtype", ctypes.c_int32), ("k1_mode", ctypes.c_int32),
                 ("profile", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("grad_nfields", ctypes.c_int32), ("grad_nx", ctypes.c_int32), ("grad_ny", ctypes.c_int32),
-                ("grad_pad", ctypes.c_int32), ("grad_hx", ctypes.c_double), ("grad_hy", ctypes.c_double)]
+                ("omega_cache", ctypes.c_int32), ("grad_hx", ctypes.c_double), ("grad_hy", ctypes.c_double)]
 
 
 class OidStats(ctypes.Structure):
@@ -116,7 +116,8 @@ def hutch_split(ell):
 
 
 def make_params(m, k, ell, b_max, n_cap, lam, split=None, eps=0.5, delta=0.05, c=1.0, seed=0, dtype="f64",
-                row_begin=0, row_end=None, k1_mode=K1_AUTO, profile=False, device=0, grad=None):
+                row_begin=0, row_end=None, k1_mode=K1_AUTO, profile=False, device=0, grad=None,
+                omega_cache=False):
     """grad: None, or (nfields, nx, ny[, hx, hy]) for the gradient-enhanced variant (A11)."""
     split = hutch_split(ell) if split is None else split
     g = tuple(grad) + (0.0, 0.0)[len(grad) - 3:] if grad is not None else (0, 0, 0, 0.0, 0.0)
@@ -124,7 +125,7 @@ def make_params(m, k, ell, b_max, n_cap, lam, split=None, eps=0.5, delta=0.05, c
                      b_max=b_max, ell1=split[0], ell2=split[1], ell3=split[2], lam=lam, eps=eps, delta=delta, c=c,
                      seed=seed, dtype=OID_F64 if dtype in ("f64", "float64") else OID_F32, k1_mode=k1_mode,
                      profile=int(bool(profile)), device=device, grad_nfields=int(g[0]), grad_nx=int(g[1]),
-                     grad_ny=int(g[2]), grad_pad=0, grad_hx=float(g[3]), grad_hy=float(g[4]))
+                     grad_ny=int(g[2]), omega_cache=int(omega_cache), grad_hx=float(g[3]), grad_hy=float(g[4]))
 
 
 def workspace_bytes(params):
@@ -178,7 +179,7 @@ class Engine:
         if X.dim() != 2 or X.shape[0] != self.m_loc:
             raise ValueError(f"block must have shape (m_loc={self.m_loc}, ncols)")
         ncols = X.shape[1]
-        if self.m_loc > 1 and X.stride(0) != 1:
+        if ncols > 0 and self.m_loc > 1 and X.stride(0) != 1:
             raise ValueError("block must be column-major (X.stride(0) == 1); pass Xt.T for a (ncols, m) tensor")
         ld = X.stride(1) if ncols > 1 else self.m_loc
         return ctypes.c_void_p(X.data_ptr()), ld, ncols

@@ -881,6 +881,9 @@ inline bool k1p_call_ok(const K1TcArgs& a) {
   if (reinterpret_cast<uintptr_t>(a.X) % 16 != 0) return false;
   if (a.row_end - a.row_begin >= (int64_t(1) << 31)) return false;
   if (a.num_sms > k1p::kMaxSms) return false;
+  // two stages of X and digit planes must fit beside the static shared state (f64, 33..64
+  // columns on one CTA does not)
+  if (k1p::make_geom(a.ell, a.ncols, a.row_end - a.row_begin, a.f64, a.num_sms).smem > 200 * 1024) return false;
   return k1tc_encoder() != nullptr;
 }
 
@@ -889,7 +892,10 @@ inline cudaError_t k1p_launch_t(const CUtensorMap& map, const K1TcArgs& a, const
                                  double* part, double* npart, double* cpart) {
   auto fn = k1p::k1_tc_kernel<T, BPAD, TM, NC>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem);
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();   // consumed here: a later call must not report it again
+    return e;
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(g.nslabs * g.nh * NC));
   cfg.blockDim = dim3(32 * k1p::kWarpsK1);

@@ -47,6 +47,8 @@ struct K1TcArgs {
   int num_sms;
   uint32_t t0, t1;   // Gauss-16 magnitudes m_0..m_3, m_4..m_7 as bytes (reading R2)
   long long* dbg;     // diagnostics (may be null): per-tile role timestamps of CTA 0
+  const uint4* omega; // stored sketch entries (NEXT-3, may be null): the Philox words of every
+                      // (32-row group g of the shard, sketch row r) at omega[g * ell + r]
 };
 
 namespace k1tc {
@@ -80,6 +82,8 @@ struct Geom {
   int64_t rows_per_slab;
   long long* dbg;  // [5][kDbgTiles] clock64 of CTA 0: A ready, B ready, MMA start, MMA issued, TMA issue
   int exp;         // diagnostics only (OID_K1_EXP): 1 = skip the Philox generation, 2 = skip the digit conversion
+  const uint4* omega;   // stored Philox words (NEXT-3) or null: generate in registers
+  int64_t g0;           // first 32-row group of the shard
 };
 constexpr int kDbgTiles = 4096;
 constexpr int kDbgRows = 10;
@@ -181,7 +185,7 @@ __device__ __forceinline__ void load_half(const uint8_t* xs, int j, int c16, int
   }
 }
 
-template <typename T, int BPAD, int TM>
+template <typename T, int BPAD, int TM, bool OMEGA>
 __global__ void __launch_bounds__(kThreads, 1)
 k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_begin, int64_t m_loc, int ell,
              uint32_t key0, uint32_t key1, uint32_t t0, uint32_t t1, Geom g, double* __restrict__ part,
@@ -568,7 +572,22 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
         }
       uint32_t kk0 = key0, kk1 = key1;
       asm volatile("" : "+r"(kk0), "+r"(kk1));   // keep the key schedule in-loop (register budget)
-      const int nrnd = g.exp == 1 ? 0 : 10;
+      const int nrnd = (g.exp == 1 || OMEGA) ? 0 : 10;
+      if constexpr (OMEGA) {
+        // stored sketch entries (NEXT-3): the same Philox words, streamed from HBM (one 16-byte
+        // load per 32 entries, consecutive lanes = consecutive sketch rows)
+#pragma unroll
+        for (int ci = 0; ci < NC; ++ci) {
+          // rows r >= ell (the padded half) read row ell - 1: their products are discarded
+          const int64_t gi = static_cast<int64_t>(c0[ci]) - g.g0;
+          c1[ci] = min(c1[ci], static_cast<uint32_t>(ell - 1));
+          uint4 v;
+          asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                       : "l"(g.omega + gi * ell + c1[ci]));
+          c0[ci] = v.x; c1[ci] = v.y; c2[ci] = v.z; c3[ci] = v.w;
+        }
+      }
 #pragma unroll
       for (int rnd = 0; rnd < 10; ++rnd) {
         if (rnd >= nrnd) break;
@@ -621,6 +640,20 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+// NEXT-3: store the Philox words of the shard's sketch entries, omega[g * ell + r] = Philox4x32-10
+// at counter (g0 + g, r, 0, 0) (reading R2), so K1 streams them instead of generating them
+__global__ void omega_fill_kernel(uint4* __restrict__ omega, int64_t ngroups, int64_t g0, int ell, uint32_t key0,
+                                  uint32_t key1) {
+  const int64_t n = ngroups * ell;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t gq = i / ell;
+    const int r = static_cast<int>(i - gq * ell);
+    const U4 w = philox4x32_10(static_cast<uint32_t>(g0 + gq), static_cast<uint32_t>(r), 0u, 0u, key0, key1);
+    omega[i] = make_uint4(w.x, w.y, w.z, w.w);
   }
 }
 
@@ -694,9 +727,12 @@ inline bool k1tc_call_ok(const K1TcArgs& a) {
 template <typename T, int BPAD, int TM>
 inline cudaError_t k1tc_launch_t(const CUtensorMap& map, const K1TcArgs& a, const k1tc::Geom& g, cudaStream_t st,
                                  double* part, double* npart, double* cpart) {
-  auto fn = k1tc::k1_tc_kernel<T, BPAD, TM>;
+  auto fn = g.omega ? k1tc::k1_tc_kernel<T, BPAD, TM, true> : k1tc::k1_tc_kernel<T, BPAD, TM, false>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem);
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();   // consumed here: a later call must not report it again
+    return e;
+  }
   fn<<<g.nslabs * g.nhalves, k1tc::kThreads, g.smem, st>>>(map, a.ncols, a.row_begin, a.row_end - a.row_begin, a.ell,
                                                            a.key0, a.key1, a.t0, a.t1, g, part, npart, cpart);
   return cudaGetLastError();
@@ -717,6 +753,8 @@ inline cudaError_t k1tc_launch(const K1TcArgs& a, cudaStream_t st, int* nlaunch)
   const int64_t m_loc = a.row_end - a.row_begin;
   k1tc::Geom g = k1tc::make_geom(a.ell, a.ncols, m_loc, a.f64, a.num_sms);
   g.dbg = a.dbg;
+  g.omega = a.omega;
+  g.g0 = a.row_begin / 32;
   g.exp = getenv("OID_K1_EXP") ? atoi(getenv("OID_K1_EXP")) : 0;
   CUtensorMap map;
   const int es = a.f64 ? 8 : 4;

@@ -110,7 +110,7 @@ struct Bump {
 struct Layout {
   size_t S, gram, Ypart, k1part, k1npart, gB, gV, mu, mu_sorted, Yc, Tsc, tau, scal, J, tau_old, admit, counts,
       flags, counters, C, SJ, sjB, sjV, sjsig, sjw, sjZ, Sjpinv, Pexp, AJP, G, Gsum, Gpart, cB, cV, csig, cw, cZ, M,
-      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, wyT, sjG, cG, cBt, cZ2, dbg, Jsnap, Dsnap, gcnt, S1, S2, YpG, GX, OGO, gH, gHV, gHs, gHw, gHZ, gHp, gR, gCm, gE, gLst, gLV, gLs, gLw, gLZ, gLp, gRhs, gscal, td2, te2, Vh2, tauv2, wyT2, ldl2, mu2, cum, elog, eslog, total;
+      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, wyT, sjG, cG, cBt, cZ2, dbg, Jsnap, Dsnap, gcnt, S1, S2, YpG, GX, OGO, gH, gHV, gHs, gHw, gHZ, gHp, gR, gCm, gE, gLst, gLV, gLs, gLw, gLZ, gLp, gRhs, gscal, td2, te2, Vh2, tauv2, wyT2, ldl2, mu2, cum, elog, eslog, omega, total;
 };
 
 int64_t m_local(const oid_params& p) { return p.row_end - p.row_begin; }
@@ -241,6 +241,11 @@ Layout make_layout(const oid_params& p) {
     L.gRhs = b.take(3 * ell * n * d);
     L.gscal = b.take(8 * d);
   }
+  if (p.omega_cache == 1) {   // omega_cache (NEXT-3): Philox words of ell x m_loc sketch entries
+    // + 1 group: the last 64-row K1 tile may run one 32-row group past the shard (zero rows of X)
+    const int64_t ng = (p.row_end + 31) / 32 - p.row_begin / 32 + 1;
+    L.omega = b.take(static_cast<size_t>(ng) * ell * 16);
+  }
   L.tc = b.take(std::max(k1tc_workspace_bytes(p.ell, p.b_max, m_local(p), p.dtype == OID_F64),
                          k1p_workspace_bytes(p.ell, p.b_max, m_local(p), p.dtype == OID_F64)));
   L.total = b.off;
@@ -265,6 +270,7 @@ const char* validate(const oid_params* p) {
   if (p->k1_mode < 0 || p->k1_mode > 3) return "bad k1_mode";
   if (p->m / 32 >= (int64_t(1) << 32)) return "m too large for the 32-bit Philox row counter";
   if (p->grad_nfields < 0) return "grad_nfields must be >= 0";
+  if (p->omega_cache != 0 && p->omega_cache != 1) return "omega_cache must be 0 or 1";
   if (p->grad_nfields > 0) {
     if (p->grad_nx < 1 || p->grad_ny < 1 || int64_t(p->grad_nfields) * p->grad_nx * p->grad_ny != p->m)
       return "gradient variant: grad_nfields * grad_nx * grad_ny must equal m";
@@ -581,6 +587,7 @@ oid_status sketch_one(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream
          (static_cast<uint32_t>(ctx->qmag[6]) << 16) | (static_cast<uint32_t>(ctx->qmag[7]) << 24);
   a.num_sms = std::max(2, ctx->num_sms - ctx->k1_free_sms);
   a.dbg = ctx->k1_debug ? ctx->ptr<long long>(ctx->L.dbg) : nullptr;
+  a.omega = (p.omega_cache == 1 && strict_mode) ? reinterpret_cast<const uint4*>(ctx->ws + ctx->L.omega) : nullptr;
   const bool tc_call = want_tc && ctx->tc_ok && (want_pair ? k1p_call_ok(a) : k1tc_call_ok(a));
   if (strict_mode && (p.k1_mode == OID_K1_TC_INT8 || want_pair) && !tc_call)
     return ctx->fail(OID_EINVAL, "tensor-core K1 unavailable for this device/shape/alignment");
@@ -1185,6 +1192,12 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
     const int64_t RL = 128 / static_cast<int64_t>(dsize(*p));
     const size_t cb = static_cast<size_t>((ctx->m_loc + RL - 1) / RL * RL) * ctx->t * dsize(*p);
     if ((e = cudaMemsetAsync(ctx->ws + L.C, 0, cb, st)) != cudaSuccess) return bad(e);
+  }
+  if (p->omega_cache == 1) {
+    const int64_t g0 = p->row_begin / 32, ng = (p->row_end + 31) / 32 - g0 + 1;
+    k1tc::omega_fill_kernel<<<static_cast<unsigned>(ctx->num_sms * 8), 256, 0, st>>>(
+        reinterpret_cast<uint4*>(ctx->ws + L.omega), ng, g0, p->ell, ctx->key0, ctx->key1);
+    if ((e = cudaGetLastError()) != cudaSuccess) return bad(e);
   }
   if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return bad(e);   // host arrays above go out of scope
   *out = ctx;

@@ -54,7 +54,14 @@ class ShardedIngest:
         self.world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
 
     def _reduce(self, t):
-        if self.world > 1:
+        if self.world <= 1:
+            return
+        if t.is_cuda and dist.get_backend(self.group) == "gloo":
+            # gloo (CPU tests, single-GPU runs) reduces host copies; staged on the current stream
+            h = t.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=self.group)
+            t.copy_(h)
+        else:
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
 
     def ingest(self, X):

@@ -13,12 +13,14 @@ ap.add_argument("--grid", default="192,129,192")
 ap.add_argument("--b", type=int, default=32)
 ap.add_argument("--ell", type=int, default=512)
 ap.add_argument("--mode", type=int, default=0)
+ap.add_argument("--omega-cache", type=int, default=0)
 a = ap.parse_args()
 grid = tuple(int(x) for x in a.grid.split(","))
 gen = ChannelFlow(*grid, seed=1003)
 dev = torch.device("cuda", 0)
 X = gen.block_torch(0, a.b, dev).T
-p = oid.make_params(m=gen.m, k=200, ell=a.ell, b_max=a.b, n_cap=64 * a.b, lam=-1.0, seed=0, profile=True, k1_mode=a.mode)
+p = oid.make_params(m=gen.m, k=200, ell=a.ell, b_max=a.b, n_cap=64 * a.b, lam=-1.0, seed=0, profile=True, k1_mode=a.mode,
+                    omega_cache=bool(a.omega_cache))
 eng = oid.Engine(p)
 for r in range(a.reps):
     eng.ingest_sketch(X)          # repeated sketches without commit are allowed (pending block replaced)

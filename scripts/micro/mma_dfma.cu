@@ -105,6 +105,21 @@ __global__ void __launch_bounds__(288, 1) k(int tiles, int iters, long long* out
 #pragma unroll
       for (int i = 0; i < 8; ++i) s += a[i];
       sink[blockIdx.x * blockDim.x + threadIdx.x] = s;
+    } else if (KIND == 5 || (KIND == 6 && (warp & 1))) {
+      // DMMA m8n8k4 chains (4 independent accumulators)
+      double acc[4][2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { acc[i][0] = 0.0; acc[i][1] = 0.0; }
+      const double a = threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-4;
+      for (int it = 0; it < iters / 4; ++it)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                       : "+d"(acc[i][0]), "+d"(acc[i][1]) : "d"(a), "d"(b));
+      double s = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) s += acc[i][0] + acc[i][1];
+      sink[blockIdx.x * blockDim.x + threadIdx.x] = s;
     } else {
       uint32_t a[8];
 #pragma unroll
@@ -122,7 +137,8 @@ __global__ void __launch_bounds__(288, 1) k(int tiles, int iters, long long* out
       sink[blockIdx.x * blockDim.x + threadIdx.x] = s;
     }
     long long t1 = clock64();
-    if (threadIdx.x == 32 && blockIdx.x == 0) out[0] = t1 - t0;
+    if (threadIdx.x == 32 && blockIdx.x == 0) out[0] = t1 - t0;   // warp 1 (DMMA in KIND 6)
+    if (threadIdx.x == 64 && blockIdx.x == 0) out[1] = t1 - t0;   // warp 2 (ALU in KIND 6)
   }
   if (threadIdx.x == 0 && MODE == 1)
     asm volatile("{.reg .pred p; W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0; @!p bra W;}" ::"r"(smem_u32(&bar)) : "memory");
@@ -153,5 +169,11 @@ int main() {
   printf("IMAD.WIDE + MMA   %lld cycles\n", run<1, 3>(out, sink, tiles, iters));
   printf("IDP4A alone       %lld cycles\n", run<0, 4>(out, sink, tiles, iters));
   printf("IDP4A + MMA       %lld cycles\n", run<1, 4>(out, sink, tiles, iters));
+  printf("DMMA alone        %lld cycles\n", run<0, 5>(out, sink, tiles, iters));
+  printf("DMMA + int8 MMA   %lld cycles\n", run<1, 5>(out, sink, tiles, iters));
+  long long d0 = run<0, 6>(out, sink, tiles, iters); long long a0 = out[1];
+  printf("DMMA|ALU mix      DMMA warps %lld, ALU warps %lld cycles\n", d0, a0);
+  long long d1 = run<1, 6>(out, sink, tiles, iters); long long a1 = out[1];
+  printf("DMMA|ALU + MMA    DMMA warps %lld, ALU warps %lld cycles\n", d1, a1);
   printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
 }

@@ -43,7 +43,9 @@ C1 = Config("C1", 4096, 512, 16, 20, 48, (16, 16, 16), "f64", math.nan, 1001)
 C2 = Config("C2", 64 * 80, 20000, 64, 100, 256, hutch_split(256), "f32", -1.0, 1002)
 C3 = Config("C3", 3 * 192 * 129 * 192, 1000, 32, 200, 512, hutch_split(512), "f64", -1.0, 1003)
 C3R = Config("C3r", 3 * 48 * 33 * 48, 1000, 32, 200, 512, hutch_split(512), "f64", -1.0, 1003)
-CONFIGS = {c.name: c for c in (C1, C2, C3, C3R)}
+C5 = Config("C5", 1 << 27, 4096, 64, 400, 1024, hutch_split(1024), "f32", -1.0, 1005)
+C5R = Config("C5r", 1 << 18, 4096, 64, 400, 1024, hutch_split(1024), "f32", -1.0, 1005)
+CONFIGS = {c.name: c for c in (C1, C2, C3, C3R, C5, C5R)}
 
 
 # --------------------------------------------------------------------------- C1
@@ -208,4 +210,65 @@ class ChannelFlow:
         for j, t in enumerate(range(t0, t1)):
             gen.manual_seed((self.seed * 1_000_003 + t) & 0x7FFFFFFFFFFFFFFF)
             out[j].add_(torch.randn(m_loc, generator=gen, device=device, dtype=torch.float64), alpha=self.noise)
+        return out
+
+
+# --------------------------------------------------------------------------- C5
+
+class LowRankStream:
+    """BASELINE config 4 (scaling sweep): X = U diag(sigma) V^T + 1e-5 N(0, 1), rank 500 with
+    sigma_i = i^-1.5, U (m x 500) and V (n x 500) with unnormalized N(0, 1) entries (SURVEY Q20:
+    signal entry variance ~zeta(3) ~ 1.2, noise 1e-5 relative), fp32, m = 2^27 rows (Q16) split
+    into contiguous slabs; C5r keeps n, b, k, l and reduces m to 2^18 for parity.
+
+    Host blocks (numpy, parity sizes): U rows from PCG64 keyed on (seed, 1, row chunk of 2^16), V
+    from (seed, 2), noise of column t from (seed, 3, t).  Device blocks (torch, throughput sizes)
+    follow the same formula with torch's generator (U in row chunks keyed on (seed, chunk)), so
+    they have the same structure but not the host's values.
+    """
+
+    RANK = 500
+    CHUNK = 1 << 16
+
+    def __init__(self, m=1 << 27, n=4096, seed=1005, noise=1e-5):
+        self.m, self.n, self.seed, self.noise = m, n, seed, noise
+        self.sigma = np.arange(1, self.RANK + 1, dtype=np.float64) ** -1.5
+        self.V = np.random.default_rng([seed, 2]).standard_normal((n, self.RANK))
+
+    def _u_rows(self, r0, r1):
+        out = np.empty((r1 - r0, self.RANK))
+        c0, c1 = r0 // self.CHUNK, (r1 + self.CHUNK - 1) // self.CHUNK
+        for c in range(c0, c1):
+            u = np.random.default_rng([self.seed, 1, c]).standard_normal((self.CHUNK, self.RANK))
+            a, b = max(r0, c * self.CHUNK), min(r1, (c + 1) * self.CHUNK)
+            out[a - r0:b - r0] = u[a - c * self.CHUNK:b - c * self.CHUNK]
+        return out
+
+    def block(self, t0, t1, row_begin=0, row_end=None):
+        """Host (numpy) block, rows [row_begin, row_end) x snapshots [t0, t1), fp32."""
+        row_end = self.m if row_end is None else row_end
+        U = self._u_rows(row_begin, row_end)
+        X = (U * self.sigma) @ self.V[t0:t1].T
+        for j, t in enumerate(range(t0, t1)):
+            nz = np.random.default_rng([self.seed, 3, t]).standard_normal(self.m)
+            X[:, j] += self.noise * nz[row_begin:row_end]
+        return X.astype(np.float32)
+
+    def block_torch(self, t0, t1, device, row_begin=0, row_end=None, chunk=1 << 21):
+        """Device (torch) block (t1 - t0, m_loc) fp32 (row j = snapshot t0 + j, rows contiguous), as
+        a GEMM over row chunks with U generated on the device; outside any timed region."""
+        import torch
+        row_end = self.m if row_end is None else row_end
+        m_loc = row_end - row_begin
+        out = torch.empty((t1 - t0, m_loc), dtype=torch.float32, device=device)
+        W = torch.from_numpy(self.sigma[:, None] * self.V[t0:t1].T).to(device=device, dtype=torch.float32)  # [R, T]
+        gen = torch.Generator(device=device)
+        for r in range(row_begin, row_end, chunk):
+            r1 = min(row_end, r + chunk)
+            gen.manual_seed((self.seed * 1_000_003 + r // chunk) & 0x7FFFFFFFFFFFFFFF)
+            U = torch.randn((r1 - r, self.RANK), generator=gen, device=device, dtype=torch.float32)
+            out[:, r - row_begin:r1 - row_begin] = (U @ W).T
+        for j, t in enumerate(range(t0, t1)):
+            gen.manual_seed((self.seed * 7_000_003 + t) & 0x7FFFFFFFFFFFFFFF)
+            out[j].add_(torch.randn(m_loc, generator=gen, device=device, dtype=torch.float32), alpha=self.noise)
         return out

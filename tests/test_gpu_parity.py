@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 
 from oracle import OracleParams, OracleOID                      # noqa: E402
 from oracle.oid import sketch as oracle_sketch                   # noqa: E402
-from synth import c1_matrix, low_rank_matrix, ImageStream, ChannelFlow, C2, C3R   # noqa: E402
+from synth import c1_matrix, low_rank_matrix, ImageStream, ChannelFlow, LowRankStream, C2, C3R, C5R   # noqa: E402
 
 
 @pytest.fixture(scope="module")
@@ -84,7 +84,12 @@ def test_sketch_parity(oid, m, nc, ell, dtype, k1_mode):
     X[rng.integers(0, m, 5), 0] *= 1e5          # late large values force accumulator flushes in the TC kernel
     eng, o = _pair(oid, m, min(8, ell), ell, 64, 256, 0.0, seed=12345, dtype="f64" if dtype == np.float64 else "f32",
                    k1_mode=k1_mode)
-    eng.ingest_sketch(_dev(X, dtype))
+    try:
+        eng.ingest_sketch(_dev(X, dtype))
+    except oid.OidError as err:
+        if k1_mode == 3 and "unavailable" in str(err):
+            pytest.skip(f"pair kernel does not take this shape: {err}")
+        raise
     part = eng.partials(0).cpu().numpy()
     Yg = part[:ell * nc].reshape(nc, ell).T
     ng = part[ell * nc:ell * nc + nc]
@@ -100,11 +105,34 @@ def test_sketch_parity(oid, m, nc, ell, dtype, k1_mode):
         xmax = np.max(np.abs(X.astype(np.float64)), axis=0)
         u = 2.0 ** (np.ceil(np.log2(xmax)) + 1 + 6 - 46)
         assert np.all(np.abs(Yg - Y) <= 1e-13 * scale + 6 * u * np.sqrt(m / 3))
-    assert np.allclose(ng, nrm, rtol=1e-13)
+        # the norms are exact sums of the rounded values x~ (|x~ - x| <= u):
+        # |sum x~^2 - sum x^2| <= 2 u sum|x| + m u^2
+        sabs = np.sum(np.abs(X.astype(np.float64)), axis=0)
+        assert np.all(np.abs(ng - nrm) <= 1e-13 * nrm + 2 * u * sabs + m * u * u)
+    else:
+        assert np.allclose(ng, nrm, rtol=1e-13)
     if k1_mode == 0:
         mode = eng.stats()["k1_mode_used"]
         aligned = (m % (2 if dtype == np.float64 else 4) == 0)
         assert mode == (oid.K1_TC_INT8 if aligned else oid.K1_SIMT_F64), mode
+
+
+@pytest.mark.parametrize("m,nc,ell,rb,dtype", [(100_000, 64, 512, 0, np.float64), (70_004, 40, 300, 32_768, np.float32),
+                                                 (5000, 16, 1024, 96, np.float64)])
+def test_omega_cache_bitwise(oid, m, nc, ell, rb, dtype):
+    """NEXT-3: streaming the stored sketch entries (omega_cache = 1) gives bitwise the partials of
+    generating them in registers -- same Philox words, same exact int8 contraction."""
+    X = np.random.default_rng(m).standard_normal((m - rb, nc)).astype(dtype)
+    outs = []
+    for cache in (False, True):
+        p = oid.make_params(m=m, k=8, ell=ell, b_max=64, n_cap=256, lam=0.0, split=_split(ell), seed=77,
+                            dtype="f64" if dtype == np.float64 else "f32", k1_mode=oid.K1_TC_INT8, row_begin=rb,
+                            omega_cache=cache)
+        eng = oid.Engine(p)
+        eng.ingest_sketch(_dev(X, dtype))
+        outs.append(eng.partials(0).cpu())
+        eng.close()
+    assert torch.equal(outs[0], outs[1])
 
 
 def test_sketch_shard_additivity(oid):
@@ -240,6 +268,41 @@ def test_c3r_whole_stream(oid):
             P = eng.finalize()["P"].cpu().numpy()
             assert np.linalg.norm(P - o.P) / np.linalg.norm(o.P) < 1e-5, e
     assert o.min_margin() >= 1e-6
+
+
+def test_c5r_prefix_parity(oid):
+    """BASELINE config 4 with m = 2^18 (C5r: fp32, b = 64, k = 400, l = 1024, rank-500 + 1e-5 noise,
+    paper surrogate lambda), first 8 blocks: J every epoch, tau_old, lambda and E_k; then P to 1e-5
+    and the NA-Hutch++ components to 1e-5 of ||A||^2."""
+    cfg = C5R
+    nb = 8
+    A = LowRankStream(m=cfg.m, n=cfg.n, seed=cfg.data_seed).block(0, nb * cfg.b)
+    eng, o = _pair(oid, cfg.m, cfg.k, cfg.ell, cfg.b, nb * cfg.b, -1.0, seed=0, dtype="f32")
+    o2 = OracleOID(o.p, cache_limit=300_000_000)
+    Ad = _dev(A, np.float32)
+    for e, j in enumerate(range(0, nb * cfg.b, cfg.b)):
+        eng.ingest_block(Ad[:, j:j + cfg.b])
+        lg = o2.ingest_block(A[:, j:j + cfg.b])
+        low = [d for d in lg.decisions if d[5] < 1e-6]
+        if low:
+            pytest.skip(f"oracle decision margin {min(d[5] for d in low):.2e} < 1e-6 at epoch {e}")
+        assert np.array_equal(eng.J(), o2.J), e
+        sc = eng.scalars()
+        assert abs(sc["lam"] - lg.lam_eff) <= 1e-9 * max(abs(lg.lam_eff), 1e-300), (e, sc["lam"], lg.lam_eff)
+        assert abs(sc["Ek"] - lg.Ek) <= 1e-10 * abs(lg.Ek)
+        # scores in the pseudo-inverse regime (n_obs < l, lambda_s clamped to 0): each eigen-term
+        # (w^T y)^2 / mu of the fp64 eigen-decomposition carries a relative error ~ eps * mu_max / mu,
+        # so the bar is 1e-8 + 64 eps kappa over the spectrum kept by the R9 cutoff
+        mu = np.linalg.eigvalsh(o2.gram)
+        kept = mu[mu > 1e-12 * mu[-1]]
+        rtol = 1e-8 + 64 * np.finfo(float).eps * mu[-1] / kept[0] if lg.lam_eff == 0 else 1e-8
+        assert np.allclose(eng.get(1), o2.tau_old, rtol=rtol, atol=0), (e, rtol)
+    P = eng.finalize()["P"].cpu().numpy()
+    assert np.linalg.norm(P - o2.P) / np.linalg.norm(o2.P) < 1e-5
+    est, ref = eng.error_estimate(), o2.error_estimate()
+    fro = o2.frob2
+    for key in ("e2", "T", "gpp"):
+        assert abs(est[key] - ref[key]) / fro < 1e-5, (key, est[key], ref[key])
 
 
 # ----------------------------------------------------------------------------- ragged / edge cases
