@@ -110,7 +110,7 @@ struct Bump {
 struct Layout {
   size_t S, gram, Ypart, k1part, k1npart, gB, gV, mu, mu_sorted, Yc, Tsc, tau, scal, J, tau_old, admit, counts,
       flags, counters, C, SJ, sjB, sjV, sjsig, sjw, sjZ, Sjpinv, Pexp, AJP, G, Gsum, Gpart, cB, cV, csig, cw, cZ, M,
-      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, wyT, sjG, cG, cBt, cZ2, dbg, Jsnap, Dsnap, gcnt, S1, S2, YpG, GX, OGO, gH, gHV, gHs, gHw, gHZ, gHp, gR, gCm, gE, gLst, gLV, gLs, gLw, gLZ, gLp, gRhs, gscal, td2, te2, Vh2, tauv2, wyT2, ldl2, mu2, cum, elog, eslog, omega, total;
+      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, wyT, sjG, cG, cBt, cZ2, dbg, Jsnap, Dsnap, gcnt, S1, S2, YpG, GX, OGO, gH, gHV, gHs, gHw, gHZ, gHp, gR, gCm, gE, gLst, gLV, gLs, gLw, gLZ, gLp, gRhs, gscal, td2, te2, Vh2, tauv2, wyT2, ldl2, mu2, cum, elog, eslog, omega, trA, trW, total;
 };
 
 int64_t m_local(const oid_params& p) { return p.row_end - p.row_begin; }
@@ -204,7 +204,12 @@ Layout make_layout(const oid_params& p) {
   L.cZ2 = b.take(std::max<size_t>(1, l1 * l2) * d);
   L.cG = b.take(std::max<size_t>(1, std::min(l1, l2) * std::min(l1, l2)) * d);
   L.ldl = b.take(2 * ellg * d);
-  L.wyT = b.take(static_cast<size_t>(kMaxRefChunks) * kRefChunk * kRefChunk * d);
+  L.wyT = b.take(static_cast<size_t>(kMaxRefChunksG) * kRefChunk * kRefChunk * d);
+  if (ellg > kTriMaxN && ellg <= kTriMaxG) {
+    // panel reduction of Gram orders 512 < n <= 1024: working copy of the Gram and the panel's W
+    L.trA = b.take(ellg * ellg * d);
+    L.trW = b.take(ellg * kPanNb * d);
+  }
   // second tridiagonal workspace: the Alg 4 SPD solve (side stream) runs beside A4 of the next block
   L.td2 = b.take(ell * d);
   L.te2 = b.take(ell * d);
@@ -439,7 +444,7 @@ oid_status spd_solve(oid_ctx ctx, cudaStream_t st, const double* A, int n, const
                      int nrhs, double* X, int64_t ldx, bool out_t, double kmax2, int* gate, double* kappa_out) {
   const Layout& L = ctx->L;   // second tridiagonal workspace (td2 ...)
   const size_t smem = sizeof(double) * static_cast<size_t>(n) * tri_rows(n);
-  tridiag_cluster_kernel<<<kTriCtas, 256, smem, st>>>(A, n, ctx->d(L.td2), ctx->d(L.te2), ctx->d(L.Vh2), ctx->d(L.tauv2),
+  tridiag_cluster_kernel<<<kTriCtas, 256, smem, st>>>(A, n, n, ctx->d(L.td2), ctx->d(L.te2), ctx->d(L.Vh2), tri_ldv(n), ctx->d(L.tauv2),
                                                       nullptr, ctx->d(L.wyT2));
   CKL();
   // the SPD gate needs only the extreme eigenvalues
@@ -451,6 +456,42 @@ oid_status spd_solve(oid_ctx ctx, cudaStream_t st, const double* A, int n, const
   CKL();
   tri_solve_kernel<<<nrhs, 256, sizeof(double) * kQStages * kRefChunk * tri_ldv(n), st>>>(R, ldr, in_t ? 1 : 0, n, nrhs, ctx->d(L.Vh2), ctx->d(L.wyT2), ctx->d(L.ldl2), gate, X, ldx,
                                          out_t ? 1 : 0);
+  CKL();
+  return OID_OK;
+}
+
+// Householder tridiagonalisation of the Gram (order 512 < n <= kTriMaxG) into (td, te, Vh, tauv,
+// wyT): panels of kPanNb columns (tridiag_panel_kernel + the two-GEMM trailing update) down to
+// the last 512 columns, which the register-resident cluster kernel finishes (tri.cuh).
+oid_status tridiag_big(oid_ctx ctx, cudaStream_t st, int n, long long* dbg) {
+  const Layout& L = ctx->L;
+  const int ldv = tri_ldv(n);
+  double* A = ctx->d(L.trA);
+  double* Vh = ctx->d(L.Vh);
+  double* Wp = ctx->d(L.trW);
+  CK(cudaMemcpyAsync(A, ctx->d(L.gram), sizeof(double) * n * n, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemsetAsync(Vh, 0, sizeof(double) * static_cast<size_t>(ldv) * n, st));   // rows no reflector writes
+  const int n0 = n - kTriMaxN;
+  for (int k0 = 0; k0 < n0; k0 += kPanNb) {
+    const int nb = std::min(kPanNb, n0 - k0);
+    tridiag_panel_kernel<<<kTriCtas, 256, kPanSmem, st>>>(A, n, k0, nb, ctx->d(L.td), ctx->d(L.te), Vh, ldv,
+                                                          ctx->d(L.tauv), Wp);
+    CKL();
+    // A(k1:, k1:) -= V W^T + W V^T over the panel's reflectors (k1 = k0 + nb)
+    const int k1 = k0 + nb, m = n - k1;
+    double* C = A + k1 + static_cast<int64_t>(k1) * n;
+    const double* V = Vh + k1 + static_cast<int64_t>(k0) * ldv;
+    oid_status s = gemm(ctx, st, false, true, m, m, nb, -1.0, V, ldv, Wp + k1, n, 1.0, C, n);
+    if (s != OID_OK) return s;
+    s = gemm(ctx, st, false, true, m, m, nb, -1.0, Wp + k1, n, V, ldv, 1.0, C, n);
+    if (s != OID_OK) return s;
+  }
+  const size_t smem = sizeof(double) * static_cast<size_t>(kTriMaxN) * tri_rows(kTriMaxN);
+  tridiag_cluster_kernel<<<kTriCtas, 256, smem, st>>>(A + n0 + static_cast<int64_t>(n0) * n, n, kTriMaxN, ctx->d(L.td) + n0,
+                                                      ctx->d(L.te) + n0, Vh + n0 + static_cast<int64_t>(n0) * ldv, ldv,
+                                                      ctx->d(L.tauv) + n0, dbg, nullptr);
+  CKL();
+  wy_t_kernel<<<(n - 2 + kRefChunk - 1) / kRefChunk, 256, 0, st>>>(Vh, ctx->d(L.tauv), n, ctx->d(L.wyT));
   CKL();
   return OID_OK;
 }
@@ -667,13 +708,19 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
     CKL();
   }
   int* gate = ctx->ptr<int>(L.gate);
-  if (ng <= kTriMaxN && !ctx->cold_jacobi) {
+  if (ng <= kTriMaxG && !ctx->cold_jacobi) {
     // tridiagonal fast path (tri.cuh); the eigenvector path below runs only when gate[1] is set
-    const size_t smem = sizeof(double) * static_cast<size_t>(ng) * tri_rows(ng);
-    tridiag_cluster_kernel<<<kTriCtas, 256, smem, st>>>(ctx->d(L.gram), ng, ctx->d(L.td), ctx->d(L.te), ctx->d(L.Vh),
-                                                        ctx->d(L.tauv), ctx->k1_debug ? ctx->ptr<long long>(L.dbg) + k1p::kDbgRows * k1tc::kDbgTiles : nullptr,
-                                                        ctx->d(L.wyT));   // the compact-WY T factors too
-    CKL();
+    long long* tdbg = ctx->k1_debug ? ctx->ptr<long long>(L.dbg) + k1p::kDbgRows * k1tc::kDbgTiles : nullptr;
+    if (ng <= kTriMaxN) {
+      const size_t smem = sizeof(double) * static_cast<size_t>(ng) * tri_rows(ng);
+      tridiag_cluster_kernel<<<kTriCtas, 256, smem, st>>>(ctx->d(L.gram), ng, ng, ctx->d(L.td), ctx->d(L.te), ctx->d(L.Vh),
+                                                          tri_ldv(ng), ctx->d(L.tauv), tdbg,
+                                                          ctx->d(L.wyT));   // the compact-WY T factors too
+      CKL();
+    } else {
+      s = tridiag_big(ctx, st, ng, tdbg);
+      if (s != OID_OK) return s;
+    }
     tl_mark(ctx, st, 15);
     // the spectrum -> lambda -> LDL^T chain on side stream 3, beside z = Q^T y for all scored columns
     cudaStream_t s3 = ctx->use_side ? ctx->side3 : st;
@@ -687,9 +734,17 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
     lambda_sorted_kernel<<<1, 256, 0, s3>>>(ctx->d(L.mu), ng, p.k, ctx->d(L.gram), p.lambda, ell, scal, gate,
                                             ctx->d(L.td), ctx->d(L.te), ctx->d(L.ldl), 1, frob_idx);
     CKL();
-    tri_scores_multi_kernel<<<(ns + kQV - 1) / kQV, 256, sizeof(double) * kQStages * kRefChunk * tri_ldv(ng), st>>>(
-        ctx->d(L.Yc), ng, ns, ctx->d(L.Vh), ctx->d(L.wyT), ctx->d(L.ldl), gate, ctx->d(L.tau), ctx->d(L.Tsc));
-    CKL();
+    {
+      const size_t qsm = sizeof(double) * kQStages * kRefChunk * tri_ldv(ng);
+      const unsigned qg = (ns + kQV - 1) / kQV;
+      if (ng <= 512)
+        tri_scores_multi_kernel<2><<<qg, 256, qsm, st>>>(ctx->d(L.Yc), ng, ns, ctx->d(L.Vh), ctx->d(L.wyT), ctx->d(L.ldl),
+                                                          gate, ctx->d(L.tau), ctx->d(L.Tsc));
+      else
+        tri_scores_multi_kernel<4><<<qg, 256, qsm, st>>>(ctx->d(L.Yc), ng, ns, ctx->d(L.Vh), ctx->d(L.wyT), ctx->d(L.ldl),
+                                                          gate, ctx->d(L.tau), ctx->d(L.Tsc));
+      CKL();
+    }
     s = join_from(ctx, st, s3);
     if (s != OID_OK) return s;
     tri_scores_chain_kernel<<<(ns + kQV - 1) / kQV, 128, 0, st>>>(ctx->d(L.Tsc), ng, ns, ctx->d(L.ldl), gate,
@@ -1069,9 +1124,9 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
     if ((e = cudaFuncSetAttribute(bjacobi_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big)) != cudaSuccess) return bad(e);
     if ((e = cudaFuncSetAttribute(bjacobi_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big)) != cudaSuccess) return bad(e);
   }
-  if (std::min(ng, p->k) <= kTriMaxN) {
-    // the cluster tridiagonalisation serves A4 (order ell, or 3 ell with gradients, when <= 512)
-    // and the A8 SPD solve (order k, when k <= 512)
+  if (std::min(ng, p->k) <= kTriMaxG) {
+    // the cluster tridiagonalisation serves A4 (order ell, or 3 ell with gradients: alone up to
+    // 512, as the last 512 columns up to 1024) and the A8 SPD solve (order k, when k <= 512)
     const int ntri = std::min(std::max(ng, p->k), kTriMaxN);
     if ((e = cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
       return bad(e);
@@ -1080,7 +1135,14 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
         cudaSuccess)
       return bad(e);
     const int ref_smem = static_cast<int>(sizeof(double) * kQStages * kRefChunk * tri_ldv(kTriMaxN));
-    if ((e = cudaFuncSetAttribute(tri_scores_multi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ref_smem)) != cudaSuccess)
+    const int ref_smem_g = static_cast<int>(sizeof(double) * kQStages * kRefChunk * tri_ldv(kTriMaxG));
+    if ((e = cudaFuncSetAttribute(tri_scores_multi_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ref_smem)) != cudaSuccess)
+      return bad(e);
+    if ((e = cudaFuncSetAttribute(tri_scores_multi_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, ref_smem_g)) != cudaSuccess)
+      return bad(e);
+    if ((e = cudaFuncSetAttribute(tridiag_panel_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
+      return bad(e);
+    if ((e = cudaFuncSetAttribute(tridiag_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPanSmem)) != cudaSuccess)
       return bad(e);
     if ((e = cudaFuncSetAttribute(tri_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ref_smem)) != cudaSuccess)
       return bad(e);

@@ -16,6 +16,7 @@ namespace cg2 = cooperative_groups;
 
 constexpr int kTriCtas = 16;
 constexpr int kTriMaxN = 512;
+constexpr int kTriMaxG = 1024;   // largest Gram order on the tridiagonal A4/A5 path (panels + cluster)
 constexpr int kTriRows = kTriMaxN / kTriCtas;   // 32 rows per CTA at the maximum size
 
 // Householder tridiagonalisation of the symmetric n x n matrix A (col-major), n <= 512.
@@ -106,6 +107,7 @@ __device__ __forceinline__ void tri_mbar_wait(uint64_t* bar, uint32_t parity) {
 // chunk; T_b row-major in wyT[64 b ..].  Reflectors with tau = 0 give zero rows/columns.
 constexpr int kRefChunk = 8;
 constexpr int kMaxRefChunks = (kTriMaxN + kRefChunk - 1) / kRefChunk;
+constexpr int kMaxRefChunksG = (kTriMaxG + kRefChunk - 1) / kRefChunk;
 constexpr int kQStages = 3;
 // T factor of reflector chunk b (256 threads; G: 8 x 8 shared scratch); tau from tau_src.
 __device__ __forceinline__ void wy_t_chunk(int b, const double* __restrict__ Vh, const double* tau_src, int n,
@@ -158,8 +160,8 @@ __device__ __forceinline__ void wy_t_chunk(int b, const double* __restrict__ Vh,
 }
 
 __global__ void __cluster_dims__(kTriCtas, 1, 1) __launch_bounds__(256, 1)
-tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__ d, double* __restrict__ e,
-                       double* __restrict__ Vh, double* __restrict__ tauv, long long* __restrict__ dbg,
+tridiag_cluster_kernel(const double* __restrict__ A, int lda, int n, double* __restrict__ d, double* __restrict__ e,
+                       double* __restrict__ Vh, int ldv_out, double* __restrict__ tauv, long long* __restrict__ dbg,
                        double* __restrict__ wyT) {
   cg2::cluster_group cluster = cg2::this_cluster();
   const int c = static_cast<int>(cluster.block_rank());
@@ -190,7 +192,7 @@ tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__
 #pragma unroll
     for (int q = 0; q < kTriCL; ++q) {
       const int j = lane + 32 * q;
-      a[r][q] = (gi[r] >= 0 && j < n) ? A[j + static_cast<int64_t>(gi[r]) * n] : 0.0;   // row i = column i
+      a[r][q] = (gi[r] >= 0 && j < n) ? A[j + static_cast<int64_t>(gi[r]) * lda] : 0.0;   // row i = column i
     }
   }
   // sender roles: thread -> (target CTA, pair of rows)
@@ -350,12 +352,13 @@ tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__
   __syncthreads();
   // bulk writes: reflector rows of this CTA (Vh(i, k) for i in [r0, r1), k < n - 2; leading
   // dimension tri_ldv(n), the pad row of odd n written as zero by the last CTA), tau/d/e
-  const int ldv = tri_ldv(n);
+  // (ldv_out > tri_ldv(n): the trailing block of a larger reduction, whose Vh the caller zeroed)
+  const int ldv = ldv_out;
   for (int idx = tid; idx < (r1 - r0) * (n - 2); idx += 256) {
     const int k = idx / (r1 - r0), il = idx - k * (r1 - r0);
     Vh[(r0 + il) + static_cast<int64_t>(k) * ldv] = vh_s[k * R + il];
   }
-  if (ldv > n && r0 <= n - 1 && n - 1 < r0 + R)
+  if (ldv == tri_ldv(n) && ldv > n && r0 <= n - 1 && n - 1 < r0 + R)
     for (int k = tid; k < n - 2; k += 256) Vh[n + static_cast<int64_t>(k) * ldv] = 0.0;
   for (int k = tid; k < n; k += 256) {
     if (c == 0 && k < n - 2) tauv[k] = tau_s[k];
@@ -370,6 +373,236 @@ tridiag_cluster_kernel(const double* __restrict__ A, int n, double* __restrict__
   }
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// Gram orders 512 < n <= kTriMaxG (l = 1024 on C5): the first n - 512 columns are reduced in
+// panels of kPanNb by tridiag_panel_kernel, the LAPACK sytrd/latrd blocking restated for one
+// 16-CTA cluster: within a panel the trailing matrix is not touched; column k and the product
+// p = tau A v are corrected for the panel's earlier reflectors through their (v, w) pairs,
+//   A_cur = A - V W^T - W V^T,
+// and after the panel two GEMMs apply A <- A - V W^T - W V^T to the trailing block.  The
+// remaining 512 x 512 block goes to tridiag_cluster_kernel.  The reflectors are those of the
+// unblocked reduction (same H_k = I - tau_k v_k v_k^T, same d, e), only summed in another order.
+// A lives in global memory (L2-resident: 8 MB at n = 1024); CTA c owns rows [c R, c R + R).
+// Per column, three distributed-shared-memory exchanges (st.async onto the receivers'
+// mbarriers, buffers alternating by step parity as in the cluster kernel):
+//   A: the corrected column k below the diagonal (= x, slices of every CTA) and its partial norms
+//   B: partial V^T v, W^T v over each CTA's rows
+//   C: partial v^T p, and from the owner of row k + 1 that row of V and W (and p_{k+1}), which
+//      the next column's correction needs.
+constexpr int kPanNb = 32;
+constexpr int kPanMaxR = kTriMaxG / kTriCtas;   // 64
+__host__ __device__ constexpr int pan_rows(int n) { return 2 * ((n + 2 * kTriCtas - 1) / (2 * kTriCtas)); }
+constexpr int kPanSmem = 2 * kPanMaxR * (kPanNb + 1) * static_cast<int>(sizeof(double));
+
+__global__ void __cluster_dims__(kTriCtas, 1, 1) __launch_bounds__(256, 1)
+tridiag_panel_kernel(const double* __restrict__ A, int n, int k0, int nb, double* __restrict__ d,
+                     double* __restrict__ e, double* __restrict__ Vh, int ldv, double* __restrict__ tauv,
+                     double* __restrict__ W) {
+  cg2::cluster_group cluster = cg2::this_cluster();
+  const int c = static_cast<int>(cluster.block_rank());
+  const int R = pan_rows(n);
+  const int r0 = c * R;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // V, W rows of this CTA (dynamic: 2 kPanMaxR (kPanNb + 1) doubles)
+  extern __shared__ double pan_smem[];
+  double (*Vs)[kPanNb + 1] = reinterpret_cast<double (*)[kPanNb + 1]>(pan_smem);
+  double (*Ws)[kPanNb + 1] = reinterpret_cast<double (*)[kPanNb + 1]>(pan_smem + kPanMaxR * (kPanNb + 1));
+  __shared__ __align__(16) double xb[2][kTriCtas * kPanMaxR];
+  __shared__ double ssb[2][kTriCtas];
+  __shared__ double vtb[2][kTriCtas][2 * kPanNb];
+  __shared__ double kb[2][kTriCtas];
+  __shared__ double rowb[2][1 + 2 * kPanNb];
+  __shared__ double rowV[kPanNb], rowW[kPanNb];
+  __shared__ __align__(16) double locx[kPanMaxR];
+  __shared__ double locs[kPanMaxR], locp[kPanMaxR];
+  __shared__ double vtot[2 * kPanNb];
+  __shared__ double wred[8];
+  __shared__ double tau_s[kPanNb], e_s[kPanNb];
+  __shared__ __align__(8) uint64_t barA[2], barB[2], barC[2];
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) { tri_mbar_init(&barA[b], 1); tri_mbar_init(&barB[b], 1); tri_mbar_init(&barC[b], 1); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = tid; i < kTriCtas * kPanMaxR; i += blockDim.x) { xb[0][i] = 0.0; xb[1][i] = 0.0; }
+  cluster.sync();
+  const uint32_t bytesA = static_cast<uint32_t>(kTriCtas) * (R + 1) * 8u;
+  const uint32_t bytesB = static_cast<uint32_t>(kTriCtas) * 2 * kPanNb * 8u;
+  const uint32_t bytesC = static_cast<uint32_t>(kTriCtas) * 8u + (1 + 2 * kPanNb) * 8u;
+  const int hp = R >> 1;                          // v2 stores per slice
+  for (int j = 0; j < nb; ++j) {
+    const int k = k0 + j;
+    const int buf = j & 1;
+    const uint32_t par = (j >> 1) & 1;
+    if (tid == 0) {
+      tri_mbar_expect(&barA[buf], bytesA);
+      tri_mbar_expect(&barB[buf], bytesB);
+      tri_mbar_expect(&barC[buf], bytesC);
+    }
+    // ---- phase A: column k of A_cur on my rows (x_i for i > k, d_k on its owner)
+    double ssw = 0.0;
+    if (tid < R) {
+      const int i = r0 + tid;
+      double a = 0.0;
+      if (i < n && i >= k) {
+        a = A[i + static_cast<int64_t>(k) * n];
+        for (int q = 0; q < j; ++q) a -= Vs[tid][q] * rowW[q] + Ws[tid][q] * rowV[q];
+      }
+      if (i == k) d[k] = a;
+      const double xi = (i < n && i > k) ? a : 0.0;
+      locx[tid] = xi;
+      ssw = xi * xi;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ssw += __shfl_xor_sync(0xffffffffu, ssw, o);
+    if (lane == 0) wred[warp] = ssw;
+    __syncthreads();
+    for (int idx = tid; idx < kTriCtas * hp; idx += blockDim.x) {
+      const int tq = idx / hp, tu = idx - tq * hp;   // (target CTA, pair of rows)
+      const uint32_t la = tri_saddr(&xb[buf][r0 + 2 * tu]);
+      tri_st_async2(tri_mapa(la, tq), locx[2 * tu], locx[2 * tu + 1], tri_mapa(tri_saddr(&barA[buf]), tq));
+    }
+    if (tid < kTriCtas) {
+      double ss = 0.0;
+      for (int w = 0; w < 8; ++w) ss += wred[w];
+      tri_st_async1(tri_mapa(tri_saddr(&ssb[buf][c]), tid), ss, tri_mapa(tri_saddr(&barA[buf]), tid));
+    }
+    tri_mbar_wait(&barA[buf], par);
+    // ---- reflector (redundant in every CTA), as in the unblocked reduction
+    double ss = 0.0;
+    for (int q = 0; q < kTriCtas; ++q) ss += ssb[buf][q];
+    const double* xk = xb[buf];
+    const double x0 = xk[k + 1];
+    const double tail = ss - x0 * x0;
+    double alpha, tau = 0.0, v0 = 0.0;
+    if (tail > 0.0) {
+      alpha = -copysign(sqrt(ss), x0);
+      v0 = x0 - alpha;
+      tau = 2.0 * rcp_nr(tail + v0 * v0);
+    } else {
+      alpha = x0;
+    }
+    if (tid == 0) { tau_s[j] = tau; e_s[j] = alpha; }
+    // ---- phase B: s = A v on my rows (column i of the symmetric A = row i), V^T v, W^T v partials
+    // warp w: rows w, w + 8, ... of this CTA (8 at R = 64), lanes over the columns j' > k
+    {
+      constexpr int RW = kPanMaxR / 8;
+      double acc[RW];
+#pragma unroll
+      for (int r = 0; r < RW; ++r) acc[r] = 0.0;
+      if (tau != 0.0) {
+        for (int jj = k + 1 + lane; jj < n; jj += 32) {
+          const double vj = jj == k + 1 ? v0 : xk[jj];
+#pragma unroll
+          for (int r = 0; r < RW; ++r) {
+            const int il = warp + 8 * r, i = r0 + il;
+            if (il < R && i < n && i > k) acc[r] = fma(__ldcg(A + jj + static_cast<int64_t>(i) * n), vj, acc[r]);
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < RW; ++r) {
+        double t = acc[r];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0 && warp + 8 * r < R) locs[warp + 8 * r] = t;
+      }
+    }
+    if (tid < 2 * kPanNb) {
+      const int q = tid & (kPanNb - 1);
+      const bool isw = tid >= kPanNb;
+      double t = 0.0;
+      if (q < j && tau != 0.0)
+        for (int il = 0; il < R; ++il) {
+          const int i = r0 + il;
+          if (i > k && i < n) {
+            const double vi = i == k + 1 ? v0 : xk[i];
+            t = fma(isw ? Ws[il][q] : Vs[il][q], vi, t);
+          }
+        }
+      vtot[tid] = t;   // staging of this CTA's partials
+    }
+    __syncthreads();
+    for (int idx = tid; idx < kTriCtas * 2 * kPanNb; idx += blockDim.x) {
+      const int dst = idx / (2 * kPanNb), q = idx - dst * (2 * kPanNb);
+      tri_st_async1(tri_mapa(tri_saddr(&vtb[buf][c][q]), dst), vtot[q], tri_mapa(tri_saddr(&barB[buf]), dst));
+    }
+    tri_mbar_wait(&barB[buf], par);
+    __syncthreads();   // vtot (staging) is rewritten below
+    if (tid < 2 * kPanNb) {
+      double t = 0.0;
+      for (int q = 0; q < kTriCtas; ++q) t += vtb[buf][q][tid];
+      vtot[tid] = t;    // [0, nb): V^T v, [nb, 2 nb): W^T v
+    }
+    __syncthreads();
+    // ---- phase C: p = tau (A v - V (W^T v) - W (V^T v)) on my rows; K = v^T p
+    double kw = 0.0;
+    if (tid < R) {
+      const int i = r0 + tid;
+      double p = 0.0, vi = 0.0;
+      if (i < n && i > k && tau != 0.0) {
+        p = locs[tid];
+        for (int q = 0; q < j; ++q) p -= Vs[tid][q] * vtot[kPanNb + q] + Ws[tid][q] * vtot[q];
+        p *= tau;
+        vi = i == k + 1 ? v0 : xk[i];
+      }
+      locp[tid] = p;
+      kw = vi * p;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) kw += __shfl_xor_sync(0xffffffffu, kw, o);
+    if (lane == 0) wred[warp] = kw;
+    __syncthreads();
+    if (tid < kTriCtas) {
+      double kp = 0.0;
+      for (int w = 0; w < 8; ++w) kp += wred[w];
+      tri_st_async1(tri_mapa(tri_saddr(&kb[buf][c]), tid), kp, tri_mapa(tri_saddr(&barC[buf]), tid));
+    }
+    // the owner of row k + 1 (k + 1 < n: panels stop 512 columns before the end): p_{k+1} and
+    // that row of V, W (columns < j) for every CTA
+    const int own = (k + 1) / R;
+    if (c == own) {
+      const int il = k + 1 - r0;
+      for (int idx = tid; idx < kTriCtas * (1 + 2 * kPanNb); idx += blockDim.x) {
+        const int dst = idx / (1 + 2 * kPanNb), q = idx - dst * (1 + 2 * kPanNb);
+        double val;
+        if (q == 0) val = locp[il];
+        else if (q <= kPanNb) val = (q - 1 < j) ? Vs[il][q - 1] : 0.0;
+        else val = (q - 1 - kPanNb < j) ? Ws[il][q - 1 - kPanNb] : 0.0;
+        tri_st_async1(tri_mapa(tri_saddr(&rowb[buf][q]), dst), val, tri_mapa(tri_saddr(&barC[buf]), dst));
+      }
+    }
+    tri_mbar_wait(&barC[buf], par);
+    double K = 0.0;
+    for (int q = 0; q < kTriCtas; ++q) K += kb[buf][q];
+    const double h = 0.5 * tau * K;
+    if (tid < R) {
+      const int i = r0 + tid;
+      const bool act = i < n && i > k && tau != 0.0;
+      const double vi = act ? (i == k + 1 ? v0 : xk[i]) : 0.0;
+      Vs[tid][j] = vi;
+      Ws[tid][j] = act ? locp[tid] - h * vi : 0.0;
+    }
+    if (tid < kPanNb) {
+      // row k + 1 of V and W for the next column's correction
+      const int q = tid;
+      if (q < j) { rowV[q] = rowb[buf][1 + q]; rowW[q] = rowb[buf][1 + kPanNb + q]; }
+      else if (q == j) { rowV[q] = tau != 0.0 ? v0 : 0.0; rowW[q] = tau != 0.0 ? rowb[buf][0] - h * v0 : 0.0; }
+    }
+    __syncthreads();
+  }
+  // panel outputs: reflector columns (all rows of this CTA), W rows, tau / e
+  for (int idx = tid; idx < R * nb; idx += blockDim.x) {
+    const int q = idx / R, il = idx - q * R, i = r0 + il;
+    if (i < n) {
+      Vh[i + static_cast<int64_t>(k0 + q) * ldv] = Vs[il][q];
+      W[i + static_cast<int64_t>(q) * n] = Ws[il][q];
+    }
+  }
+  if (c == 0)
+    for (int q = tid; q < nb; q += blockDim.x) { tauv[k0 + q] = tau_s[q]; e[k0 + q] = e_s[q]; }
+  cluster.sync();
+}
 
 // Number of eigenvalues >= x of the symmetric tridiagonal (d, e2 = e^2): n minus the number of
 // sign changes of the Sturm sequence p_{-1} = 1, p_j = (d_j - x) p_{j-1} - e_{j-1}^2 p_{j-2}
@@ -475,7 +708,7 @@ __global__ void lambda_sorted_kernel(const double* __restrict__ mu, int n, int k
                                      const double* __restrict__ d, const double* __restrict__ e,
                                      double* __restrict__ ldl, int tri_ok, int frob_idx) {
   __shared__ double red[8];
-  __shared__ double mus[kTriMaxN], ds[kTriMaxN], es[kTriMaxN];   // the serial loops read shared memory
+  __shared__ double mus[kTriMaxG], ds[kTriMaxG], es[kTriMaxG];   // the serial loops read shared memory
   double tr = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     tr += gram[static_cast<int64_t>(i) * n + i];   // Gram order n
@@ -649,7 +882,8 @@ __device__ __forceinline__ void cta_apply_q(double (&z)[2], int n, const double*
 // every thread applies z -= V u.
 constexpr int kQV = 4;   // vectors per CTA (kQV * kRefChunk == 32: one reduced value per lane)
 static_assert(kQV * kRefChunk == 32, "one reduced value per lane");
-__device__ __forceinline__ void cta_apply_qt_multi(double (&z)[kQV][2], int n, const double* __restrict__ Vh,
+template <int NS>   // vector entries per thread: n <= 256 NS
+__device__ __forceinline__ void cta_apply_qt_multi(double (&z)[kQV][NS], int n, const double* __restrict__ Vh,
                                                    const double* __restrict__ wyT, double* vring, double* tring,
                                                    uint64_t* full, double (*redm)[8][32], double* us) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -677,11 +911,11 @@ __device__ __forceinline__ void cta_apply_qt_multi(double (&z)[kQV][2], int n, c
     const int st = it % kQStages;
     tri_mbar_wait(&full[st], (it / kQStages) & 1);
     const double* vb = vring + static_cast<size_t>(st) * kRefChunk * ldv;
-    double v[kRefChunk][2];
+    double v[kRefChunk][NS];
 #pragma unroll
     for (int r = 0; r < kRefChunk; ++r)
 #pragma unroll
-      for (int s = 0; s < 2; ++s) {
+      for (int s = 0; s < NS; ++s) {
         const int i = tid + 256 * s;
         v[r][s] = (r < nr && i > k0 && i < n) ? vb[r * ldv + i] : 0.0;   // rows <= k0 are zero in V
       }
@@ -689,7 +923,12 @@ __device__ __forceinline__ void cta_apply_qt_multi(double (&z)[kQV][2], int n, c
 #pragma unroll
     for (int q = 0; q < kQV; ++q)
 #pragma unroll
-      for (int r = 0; r < kRefChunk; ++r) val[q * kRefChunk + r] = fma(v[r][1], z[q][1], v[r][0] * z[q][0]);
+      for (int r = 0; r < kRefChunk; ++r) {
+        double acc = v[r][0] * z[q][0];
+#pragma unroll
+        for (int s = 1; s < NS; ++s) acc = fma(v[r][s], z[q][s], acc);
+        val[q * kRefChunk + r] = acc;
+      }
 #pragma unroll
     for (int half = 16; half > 0; half >>= 1) {
       const bool hi = (lane & half) != 0;
@@ -721,7 +960,7 @@ __device__ __forceinline__ void cta_apply_qt_multi(double (&z)[kQV][2], int n, c
 #pragma unroll
     for (int q = 0; q < kQV; ++q)
 #pragma unroll
-      for (int s = 0; s < 2; ++s) {
+      for (int s = 0; s < NS; ++s) {
         double zi = z[q][s];
 #pragma unroll
         for (int r = 0; r < kRefChunk; ++r) zi = fma(-v[r][s], us[(it & 1) * 32 + q * kRefChunk + r], zi);
@@ -733,6 +972,7 @@ __device__ __forceinline__ void cta_apply_qt_multi(double (&z)[kQV][2], int n, c
 
 // A5 fast path: tau(y) = z^T (T + sI)^-1 z with z = Q^T y = H_{n-3} ... H_0 y, y = column j of Yc
 // (ell x ncol), for kQV columns per CTA; the LDL^T chains run on kQV threads.  Runs when gate[0] != 0.
+template <int NS>
 __global__ void __launch_bounds__(256) tri_scores_multi_kernel(const double* __restrict__ Yc, int n, int ncol,
                                                                const double* __restrict__ Vh, const double* __restrict__ wyT,
                                                                const double* __restrict__ ldl, const int* __restrict__ gate,
@@ -745,41 +985,43 @@ __global__ void __launch_bounds__(256) tri_scores_multi_kernel(const double* __r
   __shared__ __align__(8) uint64_t full[kQStages];
   __shared__ double redm[2][8][32];
   __shared__ double us[64];
-  __shared__ double zs[kQV][kTriMaxN];
-  __shared__ double ls[2 * kTriMaxN];
   const int tid = threadIdx.x, j0 = blockIdx.x * kQV;
   if (tid == 0) {
     for (int q = 0; q < kQStages; ++q) tri_mbar_init(&full[q], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  double z[kQV][2];
+  double z[kQV][NS];
 #pragma unroll
   for (int q = 0; q < kQV; ++q)
 #pragma unroll
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NS; ++s) {
       const int i = tid + 256 * s;
       z[q][s] = (i < n && j0 + q < ncol) ? Yc[static_cast<int64_t>(j0 + q) * n + i] : 0.0;
     }
   __syncthreads();
-  cta_apply_qt_multi(z, n, Vh, wyT, ref_smem, tsm, full, redm, us);
+  cta_apply_qt_multi<NS>(z, n, Vh, wyT, ref_smem, tsm, full, redm, us);
   if (zout != nullptr) {
 #pragma unroll
     for (int q = 0; q < kQV; ++q)
 #pragma unroll
-      for (int s = 0; s < 2; ++s) {
+      for (int s = 0; s < NS; ++s) {
         const int i = tid + 256 * s;
         if (i < n && j0 + q < ncol) zout[static_cast<int64_t>(j0 + q) * n + i] = z[q][s];
       }
     return;
   }
+  // the reflector ring is free again (cta_apply_qt_multi ends with a barrier): z and the LDL^T
+  // factors go to the start of the dynamic shared memory (kQV n + 2 n doubles <= the ring)
+  double* zs = ref_smem;
+  double* ls = ref_smem + kQV * n;
 #pragma unroll
   for (int q = 0; q < kQV; ++q)
 #pragma unroll
-    for (int s = 0; s < 2; ++s) if (tid + 256 * s < n) zs[q][tid + 256 * s] = z[q][s];
+    for (int s = 0; s < NS; ++s) if (tid + 256 * s < n) zs[q * n + tid + 256 * s] = z[q][s];
   for (int i = tid; i < 2 * n - 1; i += blockDim.x) ls[i] = ldl[i];
   __syncthreads();
   if (tid < kQV && j0 + tid < ncol) {
-    const double* zq = zs[tid];
+    const double* zq = zs + tid * n;
     double y = zq[0];
     double acc = y * y * ls[0];
     for (int i = 1; i < n; ++i) {
@@ -796,8 +1038,8 @@ __global__ void __launch_bounds__(128) tri_scores_chain_kernel(const double* __r
                                                                const double* __restrict__ ldl, const int* __restrict__ gate,
                                                                double* __restrict__ tau_out) {
   if (gate[0] == 0) return;
-  __shared__ double zs[kQV][kTriMaxN];
-  __shared__ double ls[2 * kTriMaxN];
+  __shared__ double zs[kQV][kTriMaxG];
+  __shared__ double ls[2 * kTriMaxG];
   const int tid = threadIdx.x, j0 = blockIdx.x * kQV;
   for (int e = tid; e < kQV * n; e += blockDim.x) {
     const int q = e / n, i = e - q * n;

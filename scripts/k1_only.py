@@ -5,7 +5,7 @@ import torch
 from __graft_entry__ import build
 build()
 import paper_2405_16076_b200 as oid
-from synth import ChannelFlow
+from synth import ChannelFlow, LowRankStream
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--reps", type=int, default=5)
@@ -14,12 +14,18 @@ ap.add_argument("--b", type=int, default=32)
 ap.add_argument("--ell", type=int, default=512)
 ap.add_argument("--mode", type=int, default=0)
 ap.add_argument("--omega-cache", type=int, default=0)
+ap.add_argument("--lowrank-m", type=int, default=0, help="C5-shaped slab: m rows of the fp32 low-rank stream")
 a = ap.parse_args()
 grid = tuple(int(x) for x in a.grid.split(","))
-gen = ChannelFlow(*grid, seed=1003)
 dev = torch.device("cuda", 0)
-X = gen.block_torch(0, a.b, dev).T
-p = oid.make_params(m=gen.m, k=200, ell=a.ell, b_max=a.b, n_cap=64 * a.b, lam=-1.0, seed=0, profile=True, k1_mode=a.mode,
+if a.lowrank_m:
+    gen = LowRankStream(m=a.lowrank_m, seed=1005)
+    X = gen.block_torch(0, a.b, dev).T
+else:
+    gen = ChannelFlow(*grid, seed=1003)
+    X = gen.block_torch(0, a.b, dev).T
+p = oid.make_params(m=gen.m, k=200, ell=a.ell, b_max=a.b, n_cap=64 * a.b, lam=-1.0, seed=0, profile=True,
+                    dtype="f32" if X.dtype == torch.float32 else "f64", k1_mode=a.mode,
                     omega_cache=bool(a.omega_cache))
 eng = oid.Engine(p)
 for r in range(a.reps):

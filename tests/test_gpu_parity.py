@@ -378,6 +378,33 @@ def test_maximum_sizes(oid, dtype):
         pytest.skip(f"decision margin < 1e-6 at epoch {low}")
 
 
+@pytest.mark.parametrize("ell", [520, 600, 1000, 1024])
+def test_panel_tridiagonal_spectrum_and_scores(oid, ell):
+    """Gram orders 512 < n <= 1024: blocked panel reduction + cluster kernel on the last 512
+    (tri.cuh).  The k largest eigenvalues against LAPACK eigvalsh of the same Gram (field 3) and
+    the ridge scores y^T (Gram + l lambda I)^-1 y against a dense solve, on the engine's own
+    sketch (so the check is of A4/A5 alone): Sturm bisection resolves each eigenvalue to
+    ~4 eps ||T||, the LDL^T scores are backward stable in the shifted (well-conditioned) system."""
+    m, k, b, lam = 4096, 200, 64, 0.05
+    A = c1_matrix(seed=ell, m=m, n=3 * b, rank=150, noise=1e-3)
+    eng, _ = _pair(oid, m, k, ell, b, 3 * b, lam, seed=7)
+    for j in range(0, 3 * b, b):
+        J = eng.J()                      # the slots scored by this block's A5
+        eng.ingest_block(_dev(A[:, j:j + b], np.float64))
+    G = eng.get(3)
+    mu = np.linalg.eigvalsh(G)[::-1]
+    mu_gpu = eng.get(6)[:k]
+    assert np.max(np.abs(mu_gpu - mu[:k])) <= 1e-12 * mu[0], np.max(np.abs(mu_gpu - mu[:k])) / mu[0]
+    sc = eng.scalars()
+    assert abs(sc["lam"] - lam) == 0
+    S = eng.get(2)
+    Yc = np.concatenate([np.where(J[None, :] >= 0, S[:, np.maximum(J, 0)], 0.0), S[:, -b:]], axis=1)
+    tau_ref = np.einsum("ij,ij->j", Yc, np.linalg.solve(G + ell * lam * np.eye(ell), Yc))
+    tau = eng.get(5)[:k + b]
+    occ = np.concatenate([J >= 0, np.ones(b, bool)])
+    assert np.allclose(tau[occ], tau_ref[occ], rtol=1e-9, atol=0)
+
+
 def test_nonfinite_input_flagged(oid):
     A = np.random.default_rng(5).standard_normal((320, 8))
     A[7, 3] = np.nan
