@@ -230,6 +230,21 @@ oid_status oid_stats_reset(oid_ctx ctx);
    Errors: OID_EINVAL on NULL pointers. */
 oid_status oid_sketch_table(int32_t q[16], double* scale);
 
+/* Diagnostics and tuning knobs (environment variables read at oid_init; none changes a result:
+   every one only moves work between streams / SMs or records timings, and the tests compare
+   the affected paths bitwise or against the oracle):
+     OID_K1_DEBUG=1     record K1 role timestamps (oid_get field 10) and the tridiagonalisation
+                        phase timestamps (field 12)
+     OID_K1_EXP=bits    K1 ablations for timing only (1: no Philox, 2: no digit conversion; the
+                        pair kernel: 4 no TMEM store, 32 no fence, 64 no dp4a, 128 no conversion,
+                        256 no MMA, 512 no TMA) - results are WRONG with any bit set
+     OID_K1_FREE=n      SMs the persistent K1 grid leaves free (default 0)
+     OID_TIMELINE=1     per-stream timeline marks (oid_get field 13)
+     OID_NO_SIDE=1      run every kernel on the caller's stream (race check of the event graph)
+     OID_JACOBI_COLD=1  A4/A5 always by cold-started Jacobi (reference path for tests)
+     OID_SIDE_PRIO, OID_SIDE2_PRIO, OID_GS_PRIO   stream priorities of the side / A9 streams
+     OID_BG_FREE, OID_BG_WAVES, OID_BG_CLUSTER, OID_BG_SMEM, OID_GS_GATE   A9 launch shape
+                        (SMs left free, waves per SM, cluster size, ring KB, gate behind A8) */
 void oid_destroy(oid_ctx ctx);
 const char* oid_last_error(oid_ctx ctx);   /* ctx == NULL: last oid_init failure (this thread) */
 const char* oid_version(void);

@@ -44,8 +44,8 @@ constexpr int kNumJacobiUses = 3;
 constexpr int kSymMaxPairs = 33;   // ceil(1024 / 16) / 2 + 1
 constexpr size_t kSmallSvdSmem = 200 * 1024;
 
-// ------------------------------------------------------------------ Gauss-256 (reading R2)
-// Inverse normal CDF: Acklam's rational approximation refined by one Halley step on erfc.
+// ------------------------------------------------------------------ Gauss-16 table (reading R2)
+// Inverse normal CDF (for the bin centroids of the 16-level law): Acklam's rational approximation refined by one Halley step on erfc.
 double inv_norm_cdf(double p) {
   static const double a[] = {-3.969683028665376e+01, 2.209460984245205e+02, -2.759285104469687e+02,
                              1.383577518672690e+02, -3.066479806614716e+01, 2.506628277459239e+00};

@@ -90,8 +90,10 @@ __global__ void scores_kernel(const double* __restrict__ T, const double* __rest
 
 constexpr int kSelMaxT = 416;   // validated maximum of k
 
-// Alg 3 steps 15-27, readings R4-R7, R14.  Single thread (sequential by nature:
-// slot i+1 sees the candidates consumed by slot i).
+// Alg 3 steps 15-27, readings R4-R7, R14.  The t evictions are independent (one
+// thread per slot); the vacant slots are then filled in slot order (sequential by nature: slot
+// i+1 sees the candidates consumed by slot i), each by one warp testing its candidates at once
+// (the first success in candidate order is the sequential scan's admission).
 // tau: [t slot scores | nc candidate scores]; nrm: candidate norms (zero columns skipped).
 // Outputs: admit list (slot, r) pairs, count; zero list (slots vacated, not refilled).
 __global__ void __launch_bounds__(256) select_kernel(int64_t* __restrict__ J, double* __restrict__ tau_old,
