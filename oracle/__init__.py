@@ -29,9 +29,11 @@ Parity-pin status per function:
 
 from .philox import philox4x32_10, uniform24
 from .gauss16 import gauss16_magnitudes, gauss16_levels, gauss16_scale, omega_rows
-from .oid import OracleParams, OracleOID, ridge_scores, hutchpp_estimate, alg4_coefficients
+from .oid import (OracleParams, OracleOID, ridge_scores, hutchpp_estimate, alg4_coefficients, alg5_coefficients,
+                  alg6_coefficients, alg7_coefficients, extend_prev, sketch_pinv, pinv_psd)
 
 __all__ = [
     "philox4x32_10", "uniform24", "gauss16_magnitudes", "gauss16_levels", "gauss16_scale", "omega_rows",
-    "OracleParams", "OracleOID", "ridge_scores", "hutchpp_estimate", "alg4_coefficients",
+    "OracleParams", "OracleOID", "ridge_scores", "hutchpp_estimate", "alg4_coefficients", "alg5_coefficients",
+    "alg6_coefficients", "alg7_coefficients", "extend_prev", "sketch_pinv", "pinv_psd",
 ]

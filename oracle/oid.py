@@ -9,6 +9,8 @@ Follows the paper step by step in its notation:
   * eviction with probability 1 - tau_i/tau_old_i          (Alg 3 step 20)
   * admission with probability tau_r^D c (k log k + k log(1/delta)/eps)/t  (Alg 3 step 24)
   * coefficients P = (Omega A_J)^+ (Omega A_obs)           (Alg 4, eq:coeff_rID_fullsketch)
+  * optionally (coeff="argmin") Algs 5-7 beside Alg 4 and the per-epoch choice of the candidate
+    with the smallest NA-Hutch++ estimate                  (Alg 3 steps 28-32)
   * NA-Hutch++ estimate of ||A_obs - A_J P||_F             (Alg 8, eq:NAhutchPP_expansion P:589,
                                                             eq:NAhutchPP_2nd_term P:595-597)
 with the readings R1-R14 of DESIGN.md section 3 (one ingest block = one epoch,
@@ -47,6 +49,8 @@ class OracleParams:
     row_end: int = -1
     omega_law: str = "gauss16"   # "gauss16" (reading R2, the build's law) or "gaussian" (the paper's
                                  # randn; numpy draws, for the R2 ablation only - not the GPU's)
+    coeff: str = "alg4"          # "alg4": Alg 4 every epoch (the hot path); "argmin": Algs 4-7 and the
+                                 # NA-Hutch++ argmin every epoch (NEXT-1)
 
     @property
     def t(self):
@@ -221,6 +225,80 @@ def alg4_coefficients(S_obs, J):
     return P, float(sig[0] / sig[keep][-1])
 
 
+def pinv_psd(G):
+    """G^+ of a symmetric positive semi-definite matrix by its eigen-decomposition, eigenvalues
+    below 1e-12 * max dropped (reading R9).  Used for the paper's G^-1 (Alg 5)."""
+    if G.size == 0:
+        return np.zeros_like(G)
+    mu, W = np.linalg.eigh(G)
+    mmax = float(np.max(mu))
+    if mmax <= 0.0:
+        return np.zeros_like(G)
+    keep = mu > PINV_RCOND * mmax
+    return (W[:, keep] / mu[keep]) @ W[:, keep].T
+
+
+def alg5_coefficients(S_obs, J, G):
+    """Alg 5: P = G^-1 Y, G = A_J^T A_J (exact, t x t), Y = (Omega A_J)^T (Omega A_obs)
+    "approximates A_J^T A_obs using sketched data".  The paper's Omega there is the JL-scaled
+    one (E[Omega^T Omega] = I); S stores the unit-variance Z A (reading R3, E[Z^T Z] = l I), so
+    Y = S_J^T S / l.  G^-1 read as the pseudo-inverse of the occupied block (R9); rows of vacant
+    slots zero (R10)."""
+    t, n_obs = J.size, S_obs.shape[1]
+    ell = S_obs.shape[0]
+    P = np.zeros((t, n_obs))
+    occ = np.nonzero(J >= 0)[0]
+    if occ.size == 0:
+        return P
+    SJ = S_obs[:, J[occ]]
+    P[occ] = pinv_psd(G[np.ix_(occ, occ)]) @ ((SJ.T @ S_obs) / ell)
+    return P
+
+
+def sketch_pinv(SJ_full, J):
+    """(Omega A_J)^+ (t x l) with R9's cutoff on the singular values, vacant rows zero."""
+    t, ell = J.size, SJ_full.shape[0]
+    Z = np.zeros((t, ell))
+    occ = np.nonzero(J >= 0)[0]
+    if occ.size:
+        Z[occ] = np.linalg.pinv(SJ_full[:, occ], rcond=PINV_RCOND)
+    return Z
+
+
+def extend_prev(P_prev, Z_prev, S_new):
+    """Reading R15: P_prev (t x n_prev, the previous epoch's chosen coefficients) has no columns for
+    the epoch's new block; Algs 6 and 7 take them as the new columns' coefficients in the PREVIOUS
+    basis, (Omega A_Jprev)^+ (Omega A_new) (Alg 4 with J_prev), so that every candidate covers A_obs."""
+    return np.concatenate([P_prev, Z_prev @ S_new], axis=1)
+
+
+def alg6_coefficients(S_obs, J, J_prev, P_prev_ext):
+    """Alg 6: zero the rows of P_prev whose basis column changed
+    (eq:coeff_update_residual_zeroout), r_A = Omega A_obs - Omega A_J P_prev,
+    dP = argmin_X ||Omega A_J X - r_A|| (the box: the whole Omega A_J, min-norm, R9),
+    P = P_prev + dP."""
+    t, ell = J.size, S_obs.shape[0]
+    Pp = P_prev_ext.copy()
+    Pp[J != J_prev] = 0.0
+    SJ = np.zeros((ell, t))
+    occ = J >= 0
+    SJ[:, occ] = S_obs[:, J[occ]]
+    r = S_obs - SJ @ Pp
+    return Pp + sketch_pinv(SJ, J) @ r
+
+
+def alg7_coefficients(C, C_prev, J, P_prev_ext):
+    """Alg 7: A_J = QR (occupied columns), T = R^+ Q^T A_Jprev (R9 cutoff), P = T P_prev.
+    C, C_prev: the basis before / after this epoch's replacements (vacant columns zero)."""
+    t = J.size
+    T = np.zeros((t, t))
+    occ = np.nonzero(J >= 0)[0]
+    if occ.size:
+        Q, R = np.linalg.qr(C[:, occ])
+        T[occ] = np.linalg.pinv(R, rcond=PINV_RCOND) @ (Q.T @ C_prev)
+    return T @ P_prev_ext
+
+
 def hutchpp_estimate(S_obs, SJ, P, G, frob2, ell1, ell2, ell3):
     """Alg 8: NA-Hutch++ estimate of ||A_obs - A_J P||_F^2.
 
@@ -266,6 +344,8 @@ class EpochLog:
     admits: list
     decisions: list = field(repr=False)
     kappa: float = 1.0
+    qstar: int = 4                 # coeff="argmin": the chosen algorithm
+    e2q: tuple = ()                # its candidates' unclamped NA-Hutch++ estimates, Algs 4..7
 
 
 class OracleOID:
@@ -284,7 +364,9 @@ class OracleOID:
         self.tau_old = np.ones(t)
         self.C = np.zeros((params.m_loc, t))                         # basis
         self.P = np.zeros((t, 0))
+        self.Z = np.zeros((t, ell))                                  # (Omega A_J)^+ of the last epoch
         self.kappa = 1.0
+        self.qstar = 4
         self.log = []
         self._Q = None
         if cache_omega and params.omega_law == "gauss16" and ell * params.m_loc <= cache_limit:
@@ -315,15 +397,32 @@ class OracleOID:
         cand_zero = nrm == 0.0
         J, tau_old, admits, decisions = select(p.seed, self.epoch, self.J, self.tau_old, tau_slot,
                                                tau_cand, cand_zero, p.admission_factor(), base)
+        C_prev, J_prev, P_prev, Z_prev = self.C.copy(), self.J.copy(), self.P, self.Z
         for (i, r) in admits:                                          # c_i = d_r
             self.C[:, i] = X[:, r]
         for i in range(p.t):                                           # evicted and not refilled
             if J[i] < 0:
                 self.C[:, i] = 0.0
         self.J, self.tau_old = J, tau_old
-        self.P, self.kappa = alg4_coefficients(self.S, self.J)        # Alg 4
+        P4, self.kappa = alg4_coefficients(self.S, self.J)            # Alg 4
+        SJ = np.zeros((p.ell, p.t))
+        SJ[:, J >= 0] = self.S[:, J[J >= 0]]
+        self.Z = sketch_pinv(SJ, J)
+        qstar, e2q = 4, ()
+        if p.coeff == "argmin":
+            # Alg 3 steps 28-32: all four candidates, NA-Hutch++ on each, argmin
+            G = self.basis_gram()
+            Pext = extend_prev(P_prev, Z_prev, Y)
+            cands = [P4, alg5_coefficients(self.S, J, G), alg6_coefficients(self.S, J, J_prev, Pext),
+                     alg7_coefficients(self.C, C_prev, J, Pext)]
+            e2q = tuple(hutchpp_estimate(self.S, SJ, Pq, G, self.frob2, p.ell1, p.ell2, p.ell3)["e2"] for Pq in cands)
+            qi = int(np.argmin(e2q))                                   # first minimum: lowest algorithm number
+            qstar, self.P = 4 + qi, cands[qi]
+        else:
+            self.P = P4
+        self.qstar = qstar
         self.log.append(EpochLog(self.epoch, lam_eff, Ek, tau_slot, tau_cand, J.copy(), tau_old.copy(),
-                                 admits, decisions, self.kappa))
+                                 admits, decisions, self.kappa, qstar, e2q))
         self.epoch += 1
         return self.log[-1]
 

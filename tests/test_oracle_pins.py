@@ -13,7 +13,8 @@ import pytest
 from oracle import philox4x32_10, uniform24, gauss16_magnitudes, gauss16_levels, gauss16_scale, omega_rows
 from oracle.gauss16 import omega_nibbles
 from oracle.oid import (OracleParams, OracleOID, ridge_scores, ridge_lambda, eig_gram, select,
-                        alg4_coefficients, hutchpp_estimate, sketch)
+                        alg4_coefficients, hutchpp_estimate, sketch, alg5_coefficients, alg6_coefficients,
+                        alg7_coefficients, extend_prev, sketch_pinv)
 from synth import c1_matrix, low_rank_matrix
 
 
@@ -471,3 +472,133 @@ def test_exact_rank_stream_selects_full_rank_basis():
         o = _stream(A, _params(120, 8, 24, -1.0, seed=seed), 8)
         good += np.linalg.matrix_rank(o.C, tol=1e-8 * np.linalg.norm(A)) == 5
     assert good >= 18
+
+
+# ------------------------------------------------------------------ Algs 5-7 and the argmin (NEXT-1)
+
+def test_alg5_identity_sketch_is_exact_least_squares():
+    """Alg 5 with the identity sketch (the JL-scaled Omega = I, i.e. the unit-variance Z = sqrt(l) I
+    of reading R3 with l = m, so Y = A_J^T A_obs exactly) is the exact least-squares solution
+    A_J^+ A_obs (eq:coeff_ID1), including a vacant slot (R10)."""
+    rng = np.random.default_rng(31)
+    A = rng.standard_normal((40, 25))
+    J = np.array([2, -1, 11, 17, 20])
+    occ = J >= 0
+    G = np.zeros((5, 5))
+    G[np.ix_(occ, occ)] = A[:, J[occ]].T @ A[:, J[occ]]
+    P = alg5_coefficients(math.sqrt(40) * A, J, G)
+    X, *_ = np.linalg.lstsq(A[:, J[occ]], A, rcond=None)
+    assert np.allclose(P[occ], X, atol=1e-11)
+    assert np.all(P[~occ] == 0.0)
+
+
+def test_alg5_differs_from_alg4_under_a_real_sketch():
+    """With a genuine (l < m) sketch, Alg 5's exact Gram makes it a different estimator from Alg 4
+    (it 'uses both original and sketched column bases'), but it still reproduces the
+    basis columns' own coefficients up to the sketch's distortion of A_J^T A_J."""
+    p = _params(300, 6, 24, 0.0, seed=4)
+    A = np.random.default_rng(32).standard_normal((300, 30))
+    S = sketch(p, A)
+    J = np.array([1, 4, 9, 15, 22, 28])
+    G = A[:, J].T @ A[:, J]
+    P4, _ = alg4_coefficients(S, J)
+    P5 = alg5_coefficients(S, J, G)
+    assert np.linalg.norm(P5 - P4) > 1e-3 * np.linalg.norm(P4)
+    # the normal equations of P:468 with the unit-variance sketch: G P5 = S_J^T S / l
+    Y = S[:, J].T @ S / 24
+    assert np.allclose(G @ P5, Y, rtol=1e-10, atol=1e-9 * np.abs(Y).max())
+    # and Y is an unbiased estimate of A_J^T A (E[Z^T Z] = l I): the mean over 200 sketch seeds
+    Ym = np.mean([sketch(_params(300, 6, 24, 0.0, seed=s_), A[:, J]).T @ sketch(_params(300, 6, 24, 0.0, seed=s_), A)
+                  for s_ in range(200)], axis=0) / 24
+    assert np.linalg.norm(Ym - A[:, J].T @ A) < 0.1 * np.linalg.norm(A[:, J].T @ A)
+
+
+def test_alg6_box_reading_equals_alg4_for_full_rank_sketch():
+    """Alg 6 as its box writes it (dP = argmin ||Omega A_J X - r_A|| over the whole Omega A_J):
+    P_prev + S_J^+ (S - S_J P_prev) = S_J^+ S when S_J has full column rank, whatever P_prev
+    (a sign error in the residual or the zero-out applied to the wrong rows fails)."""
+    rng = np.random.default_rng(33)
+    S = rng.standard_normal((20, 30))
+    J = np.array([0, 5, 9, -1, 14])
+    J_prev = np.array([0, 6, 9, 3, -1])
+    Pp = rng.standard_normal((5, 30))
+    P6 = alg6_coefficients(S, J, J_prev, Pp)
+    P4, _ = alg4_coefficients(S, J)
+    assert np.allclose(P6, P4, atol=1e-11)
+
+
+def test_alg6_rank_deficient_keeps_unchanged_prev_rows():
+    """Rank-deficient S_J (a duplicated basis column): the min-norm dP leaves the null-space part of
+    P_prev, so Alg 6 = Alg 4 + (I - S_J^+ S_J) P_prev(zeroed rows) - the case where it differs."""
+    rng = np.random.default_rng(34)
+    S = rng.standard_normal((12, 20))
+    S[:, 7] = S[:, 3]
+    J = np.array([3, 7, 10])
+    J_prev = np.array([3, 7, 11])
+    Pp = rng.standard_normal((3, 20))
+    P6 = alg6_coefficients(S, J, J_prev, Pp)
+    P4, _ = alg4_coefficients(S, J)
+    Z = sketch_pinv(S[:, J], J)
+    Pz = Pp.copy()
+    Pz[2] = 0.0                                        # slot 2 changed: its row is zeroed (P:487-494)
+    assert np.allclose(P6, P4 + (np.eye(3) - Z @ S[:, J]) @ Pz, atol=1e-11)
+    assert np.linalg.norm(P6 - P4) > 1e-3
+
+
+def test_alg7_transform_exact_when_old_basis_in_new_span():
+    """Alg 7: A_Jprev = A_J B exactly => T = R^+ Q^T A_Jprev = B (P:530-533), so A_J P7 = A_Jprev P_prev;
+    unchanged basis => T = I and P7 = P_prev."""
+    rng = np.random.default_rng(35)
+    C = rng.standard_normal((50, 4))
+    B = rng.standard_normal((4, 4))
+    Pp = rng.standard_normal((4, 9))
+    J = np.array([1, 2, 3, 4])
+    P7 = alg7_coefficients(C, C @ B, J, Pp)
+    assert np.allclose(P7, B @ Pp, atol=1e-11)
+    assert np.allclose(alg7_coefficients(C, C, J, Pp), Pp, atol=1e-12)
+
+
+def test_extend_prev_uses_previous_basis_sketch_pinv():
+    """Reading R15: the new block's columns of P_prev are (Omega A_Jprev)^+ (Omega A_new)."""
+    rng = np.random.default_rng(36)
+    S = rng.standard_normal((16, 12))
+    Jp = np.array([0, 2, -1, 5])
+    Zp = sketch_pinv(S[:, np.maximum(Jp, 0)] * (Jp >= 0), Jp)
+    Pprev = rng.standard_normal((4, 8))
+    Pe = extend_prev(Pprev, Zp, S[:, 8:])
+    assert np.array_equal(Pe[:, :8], Pprev)
+    X, *_ = np.linalg.lstsq(S[:, [0, 2, 5]], S[:, 8:], rcond=None)
+    assert np.allclose(Pe[[0, 1, 3], 8:], X, atol=1e-11) and np.all(Pe[2, 8:] == 0.0)
+
+
+def test_argmin_mode_picks_the_smallest_estimate_and_exact_rank_recovers():
+    """Alg 3 steps 28-32: every epoch the chosen P is the candidate with the smallest
+    unclamped NA-Hutch++ estimate (ties to the lowest algorithm number); on exactly rank-5 data
+    with k = 8 the chosen P reconstructs A_obs exactly once the basis has rank 5."""
+    A = low_rank_matrix(41, 160, 48, 5)
+    p = _params(160, 8, 24, 0.0, seed=5, coeff="argmin")
+    o = OracleOID(p)
+    for j in range(0, 48, 8):
+        lg = o.ingest_block(A[:, j:j + 8])
+        assert len(lg.e2q) == 4
+        assert lg.qstar == 4 + int(np.argmin(lg.e2q))
+    n = o.n_obs
+    assert np.linalg.matrix_rank(o.C) == 5
+    assert np.linalg.norm(A[:, :n] - o.C @ o.P) / np.linalg.norm(A[:, :n]) < 1e-10
+
+
+def test_argmin_mode_not_worse_than_alg4_on_c1():
+    """On C1-like data (rank 10 + noise) the argmin's chosen P is, at the last epoch, no worse by the
+    true error than 1.05x Alg 4's (the estimate is what it minimises; a wrong choice rule - argmax,
+    or a stale P_prev - typically fails by far)."""
+    A = c1_matrix(seed=43, m=512, n=96, rank=10, noise=1e-3)
+    p4 = _params(512, 12, 36, 0.0, seed=6)
+    pa = _params(512, 12, 36, 0.0, seed=6, coeff="argmin")
+    o4, oa = OracleOID(p4), OracleOID(pa)
+    for j in range(0, 96, 12):
+        o4.ingest_block(A[:, j:j + 12])
+        oa.ingest_block(A[:, j:j + 12])
+    assert np.array_equal(o4.J, oa.J)                   # selection does not depend on P
+    e4 = np.linalg.norm(A - o4.C @ o4.P)
+    ea = np.linalg.norm(A - oa.C @ oa.P)
+    assert ea <= 1.05 * e4, (ea, e4, [lg.qstar for lg in oa.log])
