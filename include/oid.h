@@ -96,6 +96,15 @@ typedef struct {
                           into the tensor-core K1 instead of generating them; 0 = generate in
                           registers (the default).  Same entries, bitwise-identical results.   */
   double grad_hx, grad_hy;
+  /* Coefficients (NEXT-1, Alg 3 steps 28-32).  0: Alg 4 every epoch, P kept implicit
+     (the hot path).  1: every epoch also Algs 5-7 (readings R15-R17 of DESIGN.md) and
+     the NA-Hutch++ estimate of each of the four candidates (A9 every epoch); P = the candidate
+     with the smallest unclamped estimate (lowest algorithm number on ties), kept explicit
+     (t x n_cap) as the next epoch's P_prev.  oid_finalize then returns that P and
+     oid_error_estimate the chosen candidate's estimate; oid_get field 14 logs the choices.
+     Requires a single shard (row_begin = 0, row_end = m) and ell1, ell2 > 0.                  */
+  int32_t coeff_mode;
+  int32_t reserved0;
 } oid_params;
 
 typedef struct {
@@ -207,7 +216,9 @@ oid_status oid_gradient_finalize(oid_ctx ctx, double lo, double hi, double tol, 
           11 basis Gram G = A_J^T A_J of the last estimate (k x k; rows/columns of vacant
              slots zero),
           12 tridiagonalisation phase timestamps of the last ingest (4 x 1024 int64 clock64 of
-             cluster CTA 0; recorded with OID_K1_DEBUG=1). */
+             cluster CTA 0; recorded with OID_K1_DEBUG=1),
+          14 coefficient choices (coeff_mode = 1): per epoch [epoch, q*, e2 of Algs 4, 5, 6, 7]
+             (epochs x 6 doubles). */
 oid_status oid_get(oid_ctx ctx, int32_t field, void* host_dst, size_t bytes, void* stream);
 
 /* Counters and CUDA-event timings (synchronizes the context's recorded events).

@@ -42,7 +42,8 @@ class OidParams(ctypes.Structure):
                 ("seed", ctypes.c_uint64), ("dtype", ctypes.c_int32), ("k1_mode", ctypes.c_int32),
                 ("profile", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("grad_nfields", ctypes.c_int32), ("grad_nx", ctypes.c_int32), ("grad_ny", ctypes.c_int32),
-                ("omega_cache", ctypes.c_int32), ("grad_hx", ctypes.c_double), ("grad_hy", ctypes.c_double)]
+                ("omega_cache", ctypes.c_int32), ("grad_hx", ctypes.c_double), ("grad_hy", ctypes.c_double),
+                ("coeff_mode", ctypes.c_int32), ("reserved0", ctypes.c_int32)]
 
 
 class OidStats(ctypes.Structure):
@@ -117,15 +118,19 @@ def hutch_split(ell):
 
 def make_params(m, k, ell, b_max, n_cap, lam, split=None, eps=0.5, delta=0.05, c=1.0, seed=0, dtype="f64",
                 row_begin=0, row_end=None, k1_mode=K1_AUTO, profile=False, device=0, grad=None,
-                omega_cache=False):
-    """grad: None, or (nfields, nx, ny[, hx, hy]) for the gradient-enhanced variant (A11)."""
+                omega_cache=False, coeff="alg4"):
+    """grad: None, or (nfields, nx, ny[, hx, hy]) for the gradient-enhanced variant (A11).
+    coeff: "alg4" (Alg 4 every epoch, the hot path) or "argmin" (Algs 4-7 + NA-Hutch++ argmin, NEXT-1)."""
+    if coeff not in ("alg4", "argmin"):
+        raise ValueError("coeff must be 'alg4' or 'argmin'")
     split = hutch_split(ell) if split is None else split
     g = tuple(grad) + (0.0, 0.0)[len(grad) - 3:] if grad is not None else (0, 0, 0, 0.0, 0.0)
     return OidParams(m=m, row_begin=row_begin, row_end=m if row_end is None else row_end, n_cap=n_cap, k=k, ell=ell,
                      b_max=b_max, ell1=split[0], ell2=split[1], ell3=split[2], lam=lam, eps=eps, delta=delta, c=c,
                      seed=seed, dtype=OID_F64 if dtype in ("f64", "float64") else OID_F32, k1_mode=k1_mode,
                      profile=int(bool(profile)), device=device, grad_nfields=int(g[0]), grad_nx=int(g[1]),
-                     grad_ny=int(g[2]), omega_cache=int(omega_cache), grad_hx=float(g[3]), grad_hy=float(g[4]))
+                     grad_ny=int(g[2]), omega_cache=int(omega_cache), grad_hx=float(g[3]), grad_hy=float(g[4]),
+                     coeff_mode=1 if coeff == "argmin" else 0)
 
 
 def workspace_bytes(params):
@@ -260,10 +265,12 @@ class Engine:
         ell, t, bm = self.p.ell, self.p.k, self.p.b_max
         ga = 3 if self.p.grad_nfields > 0 else 1
         n_obs = self.stats()["n_obs"] if field == 2 else 0
+        epochs = self.stats()["epochs"] if field == 14 else 0
         shapes = {0: ((t,), np.int64), 1: ((t,), np.float64), 2: ((n_obs, ell), np.float64),
                   3: ((ga * ell, ga * ell), np.float64), 4: ((8,), np.float64), 5: ((t + bm,), np.float64),
                   6: ((ga * ell,), np.float64), 7: (((ell + 1) * bm,), np.float64), 8: ((ell, t), np.float64),
-                  9: ((3, 48), np.int32), 10: ((12, 4096), np.int64), 11: ((t, t), np.float64), 12: ((1024, 4), np.int64), 13: ((4096, 2), np.float64)}
+                  9: ((3, 48), np.int32), 10: ((12, 4096), np.int64), 11: ((t, t), np.float64), 12: ((1024, 4), np.int64), 13: ((4096, 2), np.float64),
+                  14: ((epochs, 6), np.float64)}
         shape, dt = shapes[field]
         a = np.empty(shape, dtype=dt)
         self._check(_lib.oid_get(self.h, field, ctypes.c_void_p(a.ctypes.data), a.nbytes, self._st()), "oid_get")

@@ -22,6 +22,7 @@
 #include "k1_simt.cuh"
 #include "k1_tc.cuh"
 #include "k1_pair.cuh"
+#include "coeff.cuh"
 #include "gram_tc.cuh"
 #include "grad.cuh"
 #include "path.cuh"
@@ -43,6 +44,7 @@ constexpr int kMaxSweeps = 48;
 constexpr int kNumJacobiUses = 3;
 constexpr int kSymMaxPairs = 33;   // ceil(1024 / 16) / 2 + 1
 constexpr size_t kSmallSvdSmem = 200 * 1024;
+constexpr int kCrossChunks = 64;    // row chunks of the NEXT-1 cross dots (fixed-order sum)
 
 // ------------------------------------------------------------------ Gauss-16 table (reading R2)
 // Inverse normal CDF (for the bin centroids of the 16-level law): Acklam's rational approximation refined by one Halley step on erfc.
@@ -110,7 +112,7 @@ struct Bump {
 struct Layout {
   size_t S, gram, Ypart, k1part, k1npart, gB, gV, mu, mu_sorted, Yc, Tsc, tau, scal, J, tau_old, admit, counts,
       flags, counters, C, SJ, sjB, sjV, sjsig, sjw, sjZ, Sjpinv, Pexp, AJP, G, Gsum, Gpart, cB, cV, csig, cw, cZ, M,
-      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, wyT, sjG, cG, cBt, cZ2, dbg, Jsnap, Dsnap, gcnt, S1, S2, YpG, GX, OGO, gH, gHV, gHs, gHw, gHZ, gHp, gR, gCm, gE, gLst, gLV, gLs, gLw, gLZ, gLp, gRhs, gscal, td2, te2, Vh2, tauv2, wyT2, ldl2, mu2, cum, elog, eslog, omega, trA, trW, total;
+      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, wyT, sjG, cG, cBt, cZ2, dbg, Jsnap, Dsnap, gcnt, S1, S2, YpG, GX, OGO, gH, gHV, gHs, gHw, gHZ, gHp, gR, gCm, gE, gLst, gLV, gLs, gLw, gLZ, gLp, gRhs, gscal, td2, te2, Vh2, tauv2, wyT2, ldl2, mu2, cum, elog, eslog, omega, trA, trW, Pcand, Pchosen, Pext, Rres, Gprev, gpH, gpV, gpMu, gpW, Gpinv, Xc, Dx, Dxp, Tm, cest, est_ch, est4, qlog, Jprev, olds, nold, qsel, total;
 };
 
 int64_t m_local(const oid_params& p) { return p.row_end - p.row_begin; }
@@ -246,6 +248,32 @@ Layout make_layout(const oid_params& p) {
     L.gRhs = b.take(3 * ell * n * d);
     L.gscal = b.take(8 * d);
   }
+  if (p.coeff_mode == 1) {
+    // NEXT-1: candidates of Algs 5-7, the chosen P (= next P_prev), P_prev extended, a residual,
+    // G_prev, G^+ and its eigen-decomposition, the cross Gram, cross dots and their chunk partials
+    L.Pcand = b.take(3 * t * n * d);
+    L.Pchosen = b.take(t * n * d);
+    L.Pext = b.take(t * n * d);
+    L.Rres = b.take(ell * n * d);
+    L.Gprev = b.take(t * t * d);
+    L.gpH = b.take(t * t * d);
+    L.gpV = b.take(t * t * d);
+    L.gpMu = b.take(t * d);
+    L.gpW = b.take(t * d);
+    L.Gpinv = b.take(t * t * d);
+    L.Xc = b.take(t * t * d);
+    L.Dx = b.take(t * t * d);
+    L.Dxp = b.take(static_cast<size_t>(kCrossChunks) * t * t * d);
+    L.Tm = b.take(t * t * d);
+    L.cest = b.take(3 * 8 * d);
+    L.est_ch = b.take(8 * d);
+    L.est4 = b.take(8 * d);
+    L.qlog = b.take(n * 6 * d);
+    L.Jprev = b.take(t * sizeof(int64_t));
+    L.olds = b.take(t * sizeof(int));
+    L.nold = b.take(4 * sizeof(int));
+    L.qsel = b.take(4 * sizeof(int));
+  }
   if (p.omega_cache == 1) {   // omega_cache (NEXT-3): Philox words of ell x m_loc sketch entries
     // + 1 group: the last 64-row K1 tile may run one 32-row group past the shard (zero rows of X)
     const int64_t ng = (p.row_end + 31) / 32 - p.row_begin / 32 + 1;
@@ -276,6 +304,11 @@ const char* validate(const oid_params* p) {
   if (p->m / 32 >= (int64_t(1) << 32)) return "m too large for the 32-bit Philox row counter";
   if (p->grad_nfields < 0) return "grad_nfields must be >= 0";
   if (p->omega_cache != 0 && p->omega_cache != 1) return "omega_cache must be 0 or 1";
+  if (p->coeff_mode != 0 && p->coeff_mode != 1) return "coeff_mode must be 0 or 1";
+  if (p->coeff_mode == 1 && (p->row_begin != 0 || p->row_end != p->m))
+    return "coeff_mode = 1 needs a single shard (row_begin = 0, row_end = m)";
+  if (p->coeff_mode == 1 && (p->ell1 <= 0 || p->ell2 <= 0)) return "coeff_mode = 1 needs ell1, ell2 > 0";
+  if (p->coeff_mode == 1 && p->grad_nfields > 0) return "coeff_mode = 1 is not combined with the gradient variant";
   if (p->grad_nfields > 0) {
     if (p->grad_nx < 1 || p->grad_ny < 1 || int64_t(p->grad_nfields) * p->grad_nx * p->grad_ny != p->m)
       return "gradient variant: grad_nfields * grad_nx * grad_ny must equal m";
@@ -342,6 +375,7 @@ struct oid_ctx_s {
   int gs_gate = 0;            // A9 also waits for the epoch's A8 chain (diagnostics: OID_GS_GATE)
   bool use_side = true;       // diagnostics: OID_NO_SIDE=1 runs everything on the caller's stream
   int k1_free_sms = 0;        // SMs the persistent K1 grid leaves to concurrent streams (OID_K1_FREE)
+  int last_nc = 0;            // columns of the last committed epoch (NEXT-1's P_prev extension)
   bool timeline = false;      // diagnostics: OID_TIMELINE=1 records tagged events (oid_get 13)
   std::vector<std::pair<int, cudaEvent_t>> tl;
   char err[512] = {0};
@@ -674,6 +708,8 @@ oid_status do_sketch(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   return sketch_one(ctx, GX1, m, nc, st, Y2, true, false);
 }
 
+oid_status coeff_argmin(oid_ctx ctx, cudaStream_t st);   // NEXT-1, after the extern "C" block
+
 oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_t st) {
   const oid_params& p = ctx->p;
   const Layout& L = ctx->L;
@@ -780,6 +816,8 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   }
   // A6: selection / replacement; the previous block's Alg 4 chain reads J first
   tl_mark(ctx, st, 4);
+  if (p.coeff_mode == 1)   // NEXT-1: J_prev of Algs 6 and 7
+    CK(cudaMemcpyAsync(ctx->ws + L.Jprev, ctx->ws + L.J, sizeof(int64_t) * t, cudaMemcpyDeviceToDevice, st));
   CK(cudaStreamWaitEvent(st, ctx->ev_sj_j, 0));
   select_kernel<<<1, 256, 0, st>>>(ctx->ptr<int64_t>(L.J), ctx->d(L.tau_old), ctx->d(L.tau), Yp + int64_t(ell) * nc, t, nc,
                                   ctx->factor, static_cast<uint32_t>(ctx->epoch), ctx->n_obs, ctx->key0, ctx->key1,
@@ -792,6 +830,26 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   if (s != OID_OK) return s;
   // A7: basis copy of this shard's rows, after the last estimate's basis reads
   CK(cudaStreamWaitEvent(st, ctx->ev_gram_done, 0));
+  if (p.coeff_mode == 1) {
+    // NEXT-1: <x_r, c_old_i> for the admitted columns and the columns about to be replaced or
+    // vacated, before the copy overwrites them (Alg 7's A_J^T A_Jprev)
+    changed_slots_kernel<<<1, 32, 0, st>>>(ctx->ptr<int64_t>(L.J), ctx->ptr<int64_t>(L.Jprev), t, ctx->ptr<int>(L.olds),
+                                           ctx->ptr<int>(L.nold));
+    CKL();
+    const int64_t per = (ctx->m_loc + kCrossChunks - 1) / kCrossChunks;
+    const dim3 grid(static_cast<unsigned>((nc * t + 7) / 8 < 64 ? (nc * t + 7) / 8 : 64), kCrossChunks);
+    if (p.dtype == OID_F64)
+      cross_dots_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(X), ld, ctx->ptr<double>(L.C), ctx->m_loc, t,
+                                                      ctx->ptr<int>(L.admit), ctx->ptr<int>(L.counts), ctx->ptr<int>(L.olds),
+                                                      ctx->ptr<int>(L.nold), per, ctx->d(L.Dxp));
+    else
+      cross_dots_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(X), ld, ctx->ptr<float>(L.C), ctx->m_loc, t,
+                                                     ctx->ptr<int>(L.admit), ctx->ptr<int>(L.counts), ctx->ptr<int>(L.olds),
+                                                     ctx->ptr<int>(L.nold), per, ctx->d(L.Dxp));
+    CKL();
+    cross_dots_sum_kernel<<<blocks_for(int64_t(t) * t), 256, 0, st>>>(ctx->d(L.Dxp), kCrossChunks, t, ctx->d(L.Dx));
+    CKL();
+  }
   tl_mark(ctx, st, 5);
   {
     dim3 grid(std::max(1u, std::min(blocks_for(ctx->m_loc), static_cast<unsigned>(8 * ctx->num_sms))));
@@ -805,6 +863,7 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   }
   tl_mark(ctx, st, 6);
   ctx->n_obs += nc;
+  ctx->last_nc = nc;
   cudaStream_t cs = ctx->use_side ? ctx->side : st;
   const int par = static_cast<int>(ctx->epoch & 1);
   double* SJp = ctx->d(L.SJ) + static_cast<size_t>(par) * ell * t;
@@ -855,6 +914,7 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   CK(cudaEventRecord(ctx->ev_committed, st));
   ctx->epoch += 1;
   ctx->estimate_ready = true;
+  if (p.coeff_mode == 1) return coeff_argmin(ctx, st);
   return OID_OK;
 }
 
@@ -879,21 +939,28 @@ oid_status explicit_P(oid_ctx ctx, cudaStream_t st) {
 
 // Alg 8 factors that do not involve the basis Gram G (A10): P = S_J^+ S, Omega A_J P, the core
 // pseudo-inverse M, Omega_k A P^T, the third-block trace terms and P P^T; enqueued on stream cs.
+// The G-independent factors of Alg 8 for an explicit t x n_obs coefficient matrix P (ld t) and the
+// sketched basis SJ (l x t): Omega A_J P, the core pseudo-inverse M, Omega_k A P^T, the third-block
+// traces and P P^T; sc[0..3] = [T1 (set later with G), t3a, t3b, tr(G P P^T) (later)].
+oid_status hutch_pre(oid_ctx ctx, cudaStream_t st, const double* P, const double* SJ, double* sc);
+
 oid_status estimate_pre(oid_ctx ctx, cudaStream_t st, int par) {
+  oid_status s = explicit_P(ctx, st);                                                 // P = S_J^+ S
+  if (s != OID_OK) return s;
+  return hutch_pre(ctx, st, ctx->d(ctx->L.Pexp), ctx->d(ctx->L.SJ) + static_cast<size_t>(par) * ctx->p.ell * ctx->t,
+                   ctx->d(ctx->L.scal) + SC_T1);
+}
+
+oid_status hutch_pre(oid_ctx ctx, cudaStream_t st, const double* P, const double* SJ, double* sc) {
   const Layout& L = ctx->L;
   const oid_params& p = ctx->p;
   const int t = ctx->t, ell = p.ell, l1 = p.ell1, l2 = p.ell2, l3 = p.ell3;
   const int n = static_cast<int>(ctx->n_obs);
   double* S = ctx->d(L.S);
-  double* scal = ctx->d(L.scal);
-  oid_status s = explicit_P(ctx, st);                                                 // P = S_J^+ S
-  if (s != OID_OK) return s;
-  double* P = ctx->d(L.Pexp);
   double* AJP = ctx->d(L.AJP);
-  s = gemm(ctx, st, false, false, ell, n, t, 1.0, ctx->d(L.SJ) + static_cast<size_t>(par) * ell * t, ell, P, t, 0.0, AJP,
-           ell);   // Omega A_J P
+  oid_status s = gemm(ctx, st, false, false, ell, n, t, 1.0, SJ, ell, P, t, 0.0, AJP, ell);   // Omega A_J P
   if (s != OID_OK) return s;
-  CK(cudaMemsetAsync(scal + SC_T1, 0, 4 * sizeof(double), st));
+  CK(cudaMemsetAsync(sc, 0, 4 * sizeof(double), st));
   if (l1 > 0 && l2 > 0) {
     // M = (Omega1 A (Omega2 A_J P)^T)^+   
     s = gemm(ctx, st, false, true, l1, l2, n, 1.0, S, ell, AJP + l1, ell, 0.0, ctx->d(L.cB), l1);
@@ -945,7 +1012,7 @@ oid_status estimate_pre(oid_ctx ctx, cudaStream_t st, int par) {
   }
   if (l3 > 0) {
     // t3a = tr((Omega3 A)(Omega3 A_J P)^T)
-    frob_dot_kernel<<<1, 256, 0, st>>>(S + l1 + l2, ell, AJP + l1 + l2, ell, l3, n, scal + SC_T3A);
+    frob_dot_kernel<<<1, 256, 0, st>>>(S + l1 + l2, ell, AJP + l1 + l2, ell, l3, n, sc + 1);
     CKL();
     if (l1 > 0 && l2 > 0) {
       // t3b = tr((Omega3 A_J P)(Omega2 A)^T M (Omega1 A)(Omega3 A_J P)^T)
@@ -955,7 +1022,7 @@ oid_status estimate_pre(oid_ctx ctx, cudaStream_t st, int par) {
       if (s != OID_OK) return s;
       s = gemm(ctx, st, false, false, l3, l1, l2, 1.0, ctx->d(L.R1), l3, ctx->d(L.M), l2, 0.0, ctx->d(L.R3), l3);
       if (s != OID_OK) return s;
-      frob_dot_kernel<<<1, 256, 0, st>>>(ctx->d(L.R3), l3, ctx->d(L.R2t), l3, l3, l1, scal + SC_T3B);
+      frob_dot_kernel<<<1, 256, 0, st>>>(ctx->d(L.R3), l3, ctx->d(L.R2t), l3, l3, l1, sc + 2);
       CKL();
     }
   }
@@ -1309,7 +1376,7 @@ oid_status oid_partials(oid_ctx ctx, int32_t which, double** dev_ptr, int64_t* c
   return OID_OK;
 }
 
-oid_status oid_estimate_begin(oid_ctx ctx, void* stream) {
+static oid_status estimate_begin_impl(oid_ctx ctx, void* stream) {
   if (!ctx) return OID_EINVAL;
   if (!ctx->estimate_ready) return ctx->fail(OID_ESTATE, "no block ingested yet");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1413,7 +1480,7 @@ oid_status oid_estimate_begin(oid_ctx ctx, void* stream) {
   return OID_OK;
 }
 
-oid_status oid_estimate_end(oid_ctx ctx, double* out_dev, void* stream) {
+static oid_status estimate_end_impl(oid_ctx ctx, double* out_dev, void* stream) {
   if (!ctx) return OID_EINVAL;
   if (!ctx->estimate_ready) return ctx->fail(OID_ESTATE, "no block ingested yet");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1463,6 +1530,27 @@ oid_status oid_estimate_end(oid_ctx ctx, double* out_dev, void* stream) {
   if (s != OID_OK) return s;
   CK(cudaEventRecord(ctx->ev_est_done, st));
   tl_mark(ctx, st, 10);
+  return OID_OK;
+}
+
+// With coeff_mode = 1 every commit already ran the estimate of all four candidates (coeff_argmin):
+// these return the chosen candidate's estimate, ordered after that work.
+oid_status oid_estimate_begin(oid_ctx ctx, void* stream) {
+  if (!ctx) return OID_EINVAL;
+  if (ctx->p.coeff_mode != 1) return estimate_begin_impl(ctx, stream);
+  if (!ctx->estimate_ready) return ctx->fail(OID_ESTATE, "no block ingested yet");
+  CK(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), ctx->ev_est_done, 0));
+  return OID_OK;
+}
+
+oid_status oid_estimate_end(oid_ctx ctx, double* out_dev, void* stream) {
+  if (!ctx) return OID_EINVAL;
+  if (ctx->p.coeff_mode != 1) return estimate_end_impl(ctx, out_dev, stream);
+  if (!ctx->estimate_ready) return ctx->fail(OID_ESTATE, "no block ingested yet");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CK(cudaStreamWaitEvent(st, ctx->ev_est_done, 0));
+  CK(cudaMemcpyAsync(ctx->d(ctx->L.est), ctx->d(ctx->L.est_ch), 8 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  if (out_dev) CK(cudaMemcpyAsync(out_dev, ctx->d(ctx->L.est_ch), 8 * sizeof(double), cudaMemcpyDeviceToDevice, st));
   return OID_OK;
 }
 
@@ -1552,10 +1640,15 @@ oid_status oid_finalize(oid_ctx ctx, int64_t* J_host, double* P, int32_t P_on_de
   if (sj != OID_OK) return sj;
   CK(cudaStreamWaitEvent(st, ctx->ev_est_done, 0));
   if (ctx->n_obs > 0 && P) {
-    oid_status s = explicit_P(ctx, st);
-    if (s != OID_OK) return s;
-    CK(cudaMemcpyAsync(P, ctx->d(L.Pexp), sizeof(double) * t * ctx->n_obs,
-                       P_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    if (ctx->p.coeff_mode == 1) {   // NEXT-1: the chosen candidate of the last epoch
+      CK(cudaMemcpyAsync(P, ctx->d(L.Pchosen), sizeof(double) * t * ctx->n_obs,
+                         P_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    } else {
+      oid_status s = explicit_P(ctx, st);
+      if (s != OID_OK) return s;
+      CK(cudaMemcpyAsync(P, ctx->d(L.Pexp), sizeof(double) * t * ctx->n_obs,
+                         P_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    }
   }
   if (J_host) CK(cudaMemcpyAsync(J_host, ctx->ws + L.J, sizeof(int64_t) * t, cudaMemcpyDeviceToHost, st));
   if (basis_dev)
@@ -1591,6 +1684,9 @@ oid_status oid_get(oid_ctx ctx, int32_t field, void* host_dst, size_t bytes, voi
     case 10: off = L.dbg; need = k1p::kDbgRows * k1tc::kDbgTiles * sizeof(long long); break;
     case 11: off = L.G; need = sizeof(double) * ctx->t * ctx->t; break;
     case 12: off = L.dbg + k1p::kDbgRows * k1tc::kDbgTiles * sizeof(long long); need = k1tc::kDbgTiles * sizeof(long long); break;
+    case 14:
+      if (p.coeff_mode != 1) return ctx->fail(OID_ESTATE, "field 14 needs coeff_mode = 1");
+      off = L.qlog; need = sizeof(double) * 6 * ctx->epoch; break;
     case 13: {   // timeline: up to 4096 (tag, ms since the first mark) pairs, then cleared
       if (bytes < 2 * 4096 * sizeof(double)) return ctx->fail(OID_ESHAPE, "field 13 needs %zu bytes", 2 * 4096 * sizeof(double));
       CK(cudaDeviceSynchronize());
@@ -1764,3 +1860,107 @@ void oid_destroy(oid_ctx ctx) {
 }
 
 }  // extern "C"
+
+namespace {
+// NEXT-1 (Alg 3 steps 28-32) at the end of a commit: the Alg 4 candidate and its
+// estimate through the standard A9/A10 machinery (so G is the exact basis Gram of this epoch),
+// then Algs 5-7 (readings R15-R17) by GEMMs on the stream, their estimates, the device-side argmin
+// and P <- P_{q*} (kept explicit as the next epoch's P_prev).
+oid_status coeff_argmin(oid_ctx ctx, cudaStream_t st) {
+  const Layout& L = ctx->L;
+  const oid_params& p = ctx->p;
+  const int t = ctx->t, ell = p.ell, l1 = p.ell1, l2 = p.ell2;
+  const int nn = static_cast<int>(ctx->n_obs);
+  const int nc = ctx->last_nc, nprev = nn - nc;
+  oid_status s = estimate_begin_impl(ctx, st);
+  if (s != OID_OK) return s;
+  s = estimate_end_impl(ctx, ctx->d(L.est4), st);
+  if (s != OID_OK) return s;
+  CK(cudaStreamWaitEvent(st, ctx->ev_est_done, 0));
+  const int par = static_cast<int>((ctx->epoch + 1) & 1);   // parity of the epoch just committed
+  const double* S = ctx->d(L.S);
+  const double* SJ = ctx->d(L.SJ) + static_cast<size_t>(par) * ell * t;
+  const double* Z = ctx->d(L.Sjpinv) + static_cast<size_t>(par) * ell * t;
+  const double* Zprev = ctx->d(L.Sjpinv) + static_cast<size_t>(par ^ 1) * ell * t;
+  const double* G = ctx->d(L.G);
+  const int64_t* J = ctx->ptr<int64_t>(L.J);
+  const int64_t* Jp = ctx->ptr<int64_t>(L.Jprev);
+  const size_t cs = static_cast<size_t>(t) * p.n_cap;
+  double* P5 = ctx->d(L.Pcand);
+  double* P6 = P5 + cs;
+  double* P7 = P6 + cs;
+  double* Gp = ctx->d(L.Gpinv);
+  double* Pext = ctx->d(L.Pext);
+  double* Rres = ctx->d(L.Rres);
+  // G^+ (P:468's G^-1, reading R9 on G's eigenvalues; vacant slots are zero rows / columns of G)
+  CK(cudaMemcpyAsync(ctx->d(L.gpH), G, sizeof(double) * t * t, cudaMemcpyDeviceToDevice, st));
+  s = sym_eig(ctx, st, ctx->d(L.gpH), t, ctx->d(L.gpV), ctx->d(L.gpMu), 0, false);
+  if (s != OID_OK) return s;
+  psd_pinv_weights_kernel<<<1, 256, 0, st>>>(ctx->d(L.gpMu), t, ctx->d(L.gpW));
+  CKL();
+  scale_cols_kernel<<<blocks_for(int64_t(t) * t), 256, 0, st>>>(ctx->d(L.gpV), t, ctx->d(L.gpW), ctx->d(L.Tm));
+  CKL();
+  s = gemm(ctx, st, false, true, t, t, t, 1.0, ctx->d(L.Tm), t, ctx->d(L.gpV), t, 0.0, Gp, t);
+  if (s != OID_OK) return s;
+  // Alg 5: P5 = G^+ (S_J^T S) / l (reading R16: the 1/l of the JL-scaled Omega)
+  s = gemm(ctx, st, true, false, t, nn, ell, 1.0, SJ, ell, S, ell, 0.0, Rres, t);
+  if (s != OID_OK) return s;
+  s = gemm(ctx, st, false, false, t, nn, t, 1.0 / ell, Gp, t, Rres, t, 0.0, P5, t);
+  if (s != OID_OK) return s;
+  // P_prev extended to this epoch's block (reading R15): (Omega A_Jprev)^+ Omega A_new
+  if (nprev > 0) CK(cudaMemcpyAsync(Pext, ctx->d(L.Pchosen), sizeof(double) * t * nprev, cudaMemcpyDeviceToDevice, st));
+  if (ctx->epoch == 1) {
+    CK(cudaMemsetAsync(Pext + static_cast<size_t>(t) * nprev, 0, sizeof(double) * t * nc, st));
+  } else {
+    s = gemm(ctx, st, false, false, t, nc, ell, 1.0, Zprev, t, S + static_cast<size_t>(ell) * nprev, ell, 0.0,
+             Pext + static_cast<size_t>(t) * nprev, t);
+    if (s != OID_OK) return s;
+  }
+  // Alg 6 (the box's full Omega A_J, reading R17): P6 = Pz + S_J^+ (S - S_J Pz)
+  CK(cudaMemcpyAsync(P6, Pext, sizeof(double) * t * nn, cudaMemcpyDeviceToDevice, st));
+  zero_changed_rows_kernel<<<blocks_for(int64_t(t) * nn), 256, 0, st>>>(P6, t, nn, J, Jp);
+  CKL();
+  CK(cudaMemcpyAsync(Rres, S, sizeof(double) * ell * nn, cudaMemcpyDeviceToDevice, st));
+  s = gemm(ctx, st, false, false, ell, nn, t, -1.0, SJ, ell, P6, t, 1.0, Rres, ell);
+  if (s != OID_OK) return s;
+  s = gemm(ctx, st, false, false, t, nn, ell, 1.0, Z, t, Rres, ell, 1.0, P6, t);
+  if (s != OID_OK) return s;
+  // Alg 7: T = A_J^+ A_Jprev = G^+ (A_J^T A_Jprev) (the QR transform R^+ Q^T written
+  // with the exact Gram), P7 = T P_prev
+  cross_gram_kernel<<<blocks_for(int64_t(t) * t), 256, 0, st>>>(G, ctx->d(L.Gprev), ctx->d(L.Dx), J, Jp, t, ctx->d(L.Xc));
+  CKL();
+  s = gemm(ctx, st, false, false, t, t, t, 1.0, Gp, t, ctx->d(L.Xc), t, 0.0, ctx->d(L.Tm), t);
+  if (s != OID_OK) return s;
+  s = gemm(ctx, st, false, false, t, nn, t, 1.0, ctx->d(L.Tm), t, Pext, t, 0.0, P7, t);
+  if (s != OID_OK) return s;
+  // NA-Hutch++ of each candidate (Alg 8 with the exact G of this epoch)
+  double* cest = ctx->d(L.cest);
+  for (int q = 0; q < 3; ++q) {
+    double* sc = cest + 8 * q;
+    s = hutch_pre(ctx, st, P5 + static_cast<size_t>(q) * cs, SJ, sc);
+    if (s != OID_OK) return s;
+    s = gemm(ctx, st, false, false, l2, t, t, 1.0, ctx->d(L.Q1), l2, G, t, 0.0, ctx->d(L.Q2), l2);
+    if (s != OID_OK) return s;
+    frob_dot_kernel<<<1, 256, 0, st>>>(ctx->d(L.Q2), l2, ctx->d(L.X2), l2, l2, t, sc);
+    CKL();
+    frob_dot_kernel<<<1, 256, 0, st>>>(G, t, ctx->d(L.PPt), t, t, t, sc + 3);
+    CKL();
+    cand_e2_kernel<<<1, 32, 0, st>>>(sc, p.ell3, ctx->d(L.scal) + SC_FROB2_EST);
+    CKL();
+  }
+  (void)l1;
+  // argmin over the unclamped estimates (first minimum), P <- P_{q*}
+  argmin_pick_kernel<<<1, 32, 0, st>>>(ctx->d(L.est4), cest + 4, 8, static_cast<double>(ctx->epoch - 1),
+                                       ctx->d(L.qlog) + static_cast<size_t>(ctx->epoch - 1) * 6, ctx->ptr<int>(L.qsel));
+  CKL();
+  copy_chosen_kernel<<<std::max(1u, std::min(blocks_for(int64_t(t) * nn), 1024u)), 256, 0, st>>>(
+      ctx->d(L.Pexp), P5, static_cast<int64_t>(cs), ctx->ptr<int>(L.qsel), static_cast<int64_t>(t) * nn, ctx->d(L.Pchosen));
+  CKL();
+  chosen_estimate_kernel<<<1, 32, 0, st>>>(ctx->d(L.est4), cest, 8, ctx->ptr<int>(L.qsel), p.ell3,
+                                           ctx->d(L.scal) + SC_FROB2_EST, ctx->d(L.est_ch));
+  CKL();
+  CK(cudaMemcpyAsync(ctx->d(L.Gprev), G, sizeof(double) * t * t, cudaMemcpyDeviceToDevice, st));
+  CK(cudaEventRecord(ctx->ev_est_done, st));
+  return OID_OK;
+}
+}  // namespace

@@ -66,9 +66,28 @@ def test_workspace_query_validates(oid):
 
 def test_struct_layout_matches_header(oid):
     # oid_params: 4 int64 + 6 int32 + 4 double + uint64 + 4 int32 = 32 + 24 + 32 + 8 + 16 = 112 bytes,
-    # then the gradient-variant block: 4 int32 + 2 double = 32 bytes
-    assert ctypes.sizeof(oid.OidParams) == 144
+    # then the gradient-variant block: 4 int32 + 2 double = 32 bytes, then coeff_mode + reserved0
+    assert ctypes.sizeof(oid.OidParams) == 152
     assert oid.OidParams.grad_nfields.offset == 112 and oid.OidParams.grad_hx.offset == 128
+    assert oid.OidParams.coeff_mode.offset == 144
     # oid_stats_t: 4 int64 + 3 double + uint32 + int32, then a9_ms, 4 int64, 3 double
     assert ctypes.sizeof(oid.OidStats) == 4 * 8 + 3 * 8 + 8 + 8 + 4 * 8 + 3 * 8
     assert oid.OidStats.a9_ms.offset == 64 and oid.OidStats.lat_max_ms.offset == 120
+
+
+def test_struct_layout_matches_compiled_header(oid, tmp_path):
+    """The ctypes structs against the C compiler's view of include/oid.h (sizes and key offsets)."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "oid.h"\n'
+                   'int main(void){printf("%zu %zu %zu %zu %zu\\n", sizeof(oid_params), offsetof(oid_params, coeff_mode),'
+                   ' offsetof(oid_params, grad_hx), sizeof(oid_stats_t), offsetof(oid_stats_t, lat_max_ms)); return 0;}\n')
+    exe = tmp_path / "sz"
+    inc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include")
+    subprocess.run(["gcc", "-I", inc, str(src), "-o", str(exe)], check=True)
+    vals = [int(v) for v in subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split()]
+    assert vals == [ctypes.sizeof(oid.OidParams), oid.OidParams.coeff_mode.offset, oid.OidParams.grad_hx.offset,
+                    ctypes.sizeof(oid.OidStats), oid.OidStats.lat_max_ms.offset]

@@ -405,6 +405,44 @@ def test_panel_tridiagonal_spectrum_and_scores(oid, ell):
     assert np.allclose(tau[occ], tau_ref[occ], rtol=1e-9, atol=0)
 
 
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_argmin_coefficients_match_oracle(oid, dtype):
+    """NEXT-1 (coeff = "argmin"): Algs 4-7 and the NA-Hutch++ argmin every epoch against
+    the oracle: J bit-exact, the four candidates' unclamped estimates within 1e-5 ||A_obs||^2
+    (oid_get field 14), q* equal whenever the oracle's best two estimates are more than 1e-5
+    ||A_obs||^2 apart (Algs 4 and 6 tie for a full-rank S_J: equal P up to rounding, either
+    choice), and the chosen P within 1e-5 of the oracle's at the end."""
+    m, n, b, k, ell = 2000, 160, 16, 12, 36
+    A = c1_matrix(seed=51, m=m, n=n, rank=14, noise=1e-3).astype(dtype)
+    split = (6, 12, 18)
+    p = oid.make_params(m=m, k=k, ell=ell, b_max=b, n_cap=n, lam=0.0, split=split, seed=8,
+                        dtype="f64" if dtype == np.float64 else "f32", coeff="argmin")
+    eng = oid.Engine(p)
+    o = OracleOID(OracleParams(m=m, k=k, ell=ell, ell1=split[0], ell2=split[1], ell3=split[2], lam=0.0, seed=8,
+                               coeff="argmin"))
+    Ad = _dev(A, dtype)
+    chosen = []
+    for e, j in enumerate(range(0, n, b)):
+        eng.ingest_block(Ad[:, j:j + b])
+        lg = o.ingest_block(A[:, j:j + b])
+        if any(d[5] < 1e-6 for d in lg.decisions):
+            pytest.skip(f"oracle decision margin < 1e-6 at epoch {e}")
+        assert np.array_equal(eng.J(), o.J), e
+        row = eng.get(14)[e]
+        assert row[0] == e
+        fro = o.frob2
+        assert np.all(np.abs(row[2:6] - np.array(lg.e2q)) <= 1e-5 * fro), (e, row[2:6], lg.e2q)
+        srt = np.sort(lg.e2q)
+        if srt[1] - srt[0] > 1e-5 * fro:
+            assert int(row[1]) == lg.qstar, (e, row, lg.e2q)
+        chosen.append((int(row[1]), lg.qstar))
+    P = eng.finalize()["P"].cpu().numpy()
+    assert np.linalg.norm(P - o.P) / np.linalg.norm(o.P) < 1e-5, chosen
+    est = eng.error_estimate()
+    qi = chosen[-1][0] - 4
+    assert abs(est["e2"] - eng.get(14)[-1][2 + qi]) <= 1e-12 * o.frob2   # the chosen candidate's estimate
+
+
 def test_nonfinite_input_flagged(oid):
     A = np.random.default_rng(5).standard_normal((320, 8))
     A[7, 3] = np.nan
