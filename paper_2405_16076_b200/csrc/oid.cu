@@ -1790,6 +1790,11 @@ oid_status oid_report(oid_ctx ctx, char* buf, size_t cap, size_t* needed, void* 
       es(static_cast<size_t>(std::max<int64_t>(1, nest)) * kElogCols);
   if (ne) CK(cudaMemcpy(el.data(), ctx->ws + ctx->L.elog, sizeof(double) * kElogCols * ne, cudaMemcpyDeviceToHost));
   if (nest) CK(cudaMemcpy(es.data(), ctx->ws + ctx->L.eslog, sizeof(double) * kElogCols * nest, cudaMemcpyDeviceToHost));
+  std::vector<double> ql;
+  if (ctx->p.coeff_mode == 1 && ne) {
+    ql.resize(static_cast<size_t>(ne) * 6);
+    CK(cudaMemcpy(ql.data(), ctx->ws + ctx->L.qlog, sizeof(double) * 6 * ne, cudaMemcpyDeviceToHost));
+  }
   unsigned f = 0;
   CK(cudaMemcpy(&f, ctx->ws + ctx->L.flags, sizeof(unsigned), cudaMemcpyDeviceToHost));
   unsigned long long cum[4] = {0, 0, 0, 0};
@@ -1814,7 +1819,13 @@ oid_status oid_report(oid_ctx ctx, char* buf, size_t cap, size_t* needed, void* 
     j += e ? ", " : "";
     j += "{\"epoch\": " + num(r[0]) + ", \"n_obs\": " + num(r[1]) + ", \"admissions\": " + num(r[2]) +
          ", \"evictions\": " + num(r[3]) + ", \"lambda_eff\": " + num(r[4]) + ", \"E_k\": " + num(r[5]) +
-         ", \"min_margin\": " + num(r[6]) + ", \"kappa_SJ\": " + num(r[7]) + "}";
+         ", \"min_margin\": " + num(r[6]) + ", \"kappa_SJ\": " + num(r[7]);
+    if (!ql.empty()) {   // NEXT-1: the chosen algorithm and the four candidates' estimates
+      const double* q = ql.data() + e * 6;
+      j += ", \"coeff_alg\": " + num(q[1]) + ", \"e2_alg4_7\": [" + num(q[2]) + ", " + num(q[3]) + ", " + num(q[4]) +
+           ", " + num(q[5]) + "]";
+    }
+    j += "}";
   }
   j += "], \"estimate_log\": [";
   for (int64_t q = 0; q < nest; ++q) {

@@ -438,6 +438,8 @@ def test_argmin_coefficients_match_oracle(oid, dtype):
         chosen.append((int(row[1]), lg.qstar))
     P = eng.finalize()["P"].cpu().numpy()
     assert np.linalg.norm(P - o.P) / np.linalg.norm(o.P) < 1e-5, chosen
+    rep = eng.report()
+    assert [int(r["coeff_alg"]) for r in rep["epoch_log"]] == [c[0] for c in chosen]
     est = eng.error_estimate()
     qi = chosen[-1][0] - 4
     assert abs(est["e2"] - eng.get(14)[-1][2 + qi]) <= 1e-12 * o.frob2   # the chosen candidate's estimate
