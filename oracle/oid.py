@@ -51,6 +51,9 @@ class OracleParams:
                                  # randn; numpy draws, for the R2 ablation only - not the GPU's)
     coeff: str = "alg4"          # "alg4": Alg 4 every epoch (the hot path); "argmin": Algs 4-7 and the
                                  # NA-Hutch++ argmin every epoch (NEXT-1)
+    epochs: str = "block"        # "block": one ingest block = one epoch (reading R4, the hot path);
+                                 # "t": the paper's buffer - an epoch whenever t columns have been
+                                 # buffered in D, across block boundaries (NEXT-2)
 
     @property
     def t(self):
@@ -364,6 +367,7 @@ class OracleOID:
         self.tau_old = np.ones(t)
         self.C = np.zeros((params.m_loc, t))                         # basis
         self.P = np.zeros((t, 0))
+        self._D = []                                                 # buffered (index, a, s, ||a||^2), epochs="t"
         self.Z = np.zeros((t, ell))                                  # (Omega A_J)^+ of the last epoch
         self.kappa = 1.0
         self.qstar = 4
@@ -374,18 +378,41 @@ class OracleOID:
             self._Q = omega_rows(params.seed, np.arange(ell), rb, rb + params.m_loc)
 
     def ingest_block(self, X, partial_sketch=None, partial_norms=None):
-        """One epoch.  partial_sketch/norms: already all-reduced [Y; n] (multi-shard runs)."""
+        """One block.  epochs="block": one epoch over the block's columns (R4); epochs="t": the
+        columns are buffered in D and an epoch runs each time D holds t of them.
+        Returns the last epoch's log (None if no epoch ran).  partial_sketch/norms: already
+        all-reduced [Y; n] (multi-shard runs)."""
         p = self.p
         X = np.asarray(X, dtype=np.float64)
         ncols = X.shape[1]
         Y = sketch(p, X, self._Q) if partial_sketch is None else np.asarray(partial_sketch, np.float64)
         nrm = column_norms2(X) if partial_norms is None else np.asarray(partial_norms, np.float64)
-        base = self.n_obs
+        if p.epochs == "block":
+            self._observe(Y, nrm)
+            return self._epoch(X, Y, nrm, self.n_obs - ncols)
+        last = None
+        for c in range(ncols):
+            self._observe(Y[:, c:c + 1], nrm[c:c + 1])                # every column sketched and counted
+            self._D.append((self.n_obs - 1, X[:, c], Y[:, c], nrm[c]))   # d_count = a_j (P:372)
+            if len(self._D) == p.t:                                    # count = t: epoch (P:374)
+                base = self._D[0][0]
+                Xd = np.stack([d[1] for d in self._D], axis=1)
+                Yd = np.stack([d[2] for d in self._D], axis=1)
+                nd = np.array([d[3] for d in self._D])
+                self._D = []
+                last = self._epoch(Xd, Yd, nd, base)
+        return last
+
+    def _observe(self, Y, nrm):
         self.S = np.concatenate([self.S, Y], axis=1)                  # S <- [S, s_j]   (P:368)
         self.gram = self.gram + Y @ Y.T                               # SS^T += s s^T   (P:369)
         self.frob2 += float(np.sum(nrm))                              # ||A_obs||^2     (P:372)
-        self.n_obs += ncols
+        self.n_obs += Y.shape[1]
 
+    def _epoch(self, X, Y, nrm, base):
+        """Alg 3 steps 15-32 over the candidate columns X (sketches Y, squared norms nrm), whose
+        global indices are base, base + 1, ...."""
+        p = self.p
         mu, W = eig_gram(self.gram)
         lam_eff, Ek = ridge_lambda(p, mu, self.frob2, float(np.trace(self.gram)))
         shift = p.ell * lam_eff
@@ -412,7 +439,7 @@ class OracleOID:
         if p.coeff == "argmin":
             # Alg 3 steps 28-32: all four candidates, NA-Hutch++ on each, argmin
             G = self.basis_gram()
-            Pext = extend_prev(P_prev, Z_prev, Y)
+            Pext = extend_prev(P_prev, Z_prev, self.S[:, P_prev.shape[1]:])
             cands = [P4, alg5_coefficients(self.S, J, G), alg6_coefficients(self.S, J, J_prev, Pext),
                      alg7_coefficients(self.C, C_prev, J, Pext)]
             e2q = tuple(hutchpp_estimate(self.S, SJ, Pq, G, self.frob2, p.ell1, p.ell2, p.ell3)["e2"] for Pq in cands)
@@ -430,13 +457,18 @@ class OracleOID:
         """G = A_J^T A_J from the stored basis; vacant columns are zero."""
         return self.C.T @ self.C
 
+    def current_P(self):
+        """Coefficients of every observed column: the last epoch's P, extended to columns observed
+        since by the current basis' sketched LS (Alg 4 with the current J; = S_J^+ S in Alg 4 mode)."""
+        return extend_prev(self.P, self.Z, self.S[:, self.P.shape[1]:])
+
     def error_estimate(self, G=None):
         p = self.p
         SJ = np.zeros((p.ell, p.t))
         occ = self.J >= 0
         SJ[:, occ] = self.S[:, self.J[occ]]
         G = self.basis_gram() if G is None else G
-        return hutchpp_estimate(self.S, SJ, self.P, G, self.frob2, p.ell1, p.ell2, p.ell3)
+        return hutchpp_estimate(self.S, SJ, self.current_P(), G, self.frob2, p.ell1, p.ell2, p.ell3)
 
     def min_margin(self):
         return min((d[5] for lg in self.log for d in lg.decisions), default=math.inf)

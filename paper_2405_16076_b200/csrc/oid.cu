@@ -15,6 +15,7 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: named ranges per API call for nsys / ncu --nvtx
 
 #include "../../include/oid.h"
 #include "common.cuh"
@@ -29,6 +30,14 @@
 #include "tri.cuh"
 
 using namespace oid;
+
+namespace {
+// one NVTX range per public call (the step structure in a profiler timeline)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 namespace {
 
@@ -1334,6 +1343,7 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
 }
 
 oid_status oid_ingest_sketch(oid_ctx ctx, const void* X, int64_t ld, int32_t ncols, void* stream) {
+  NvtxRange nvtx_range("oid_ingest_sketch");
   if (!ctx) return OID_EINVAL;
   oid_status s = check_block(ctx, X, ld, ncols);
   if (s != OID_OK) return s;
@@ -1343,6 +1353,7 @@ oid_status oid_ingest_sketch(oid_ctx ctx, const void* X, int64_t ld, int32_t nco
 }
 
 oid_status oid_ingest_commit(oid_ctx ctx, const void* X, int64_t ld, int32_t ncols, void* stream) {
+  NvtxRange nvtx_range("oid_ingest_commit");
   if (!ctx) return OID_EINVAL;
   if (ctx->pending_nc < 0 || ctx->pending_nc != ncols)
     return ctx->fail(OID_ESTATE, "commit without a matching sketch (pending ncols %d, got %d)", ctx->pending_nc, ncols);
@@ -1536,6 +1547,7 @@ static oid_status estimate_end_impl(oid_ctx ctx, double* out_dev, void* stream) 
 // With coeff_mode = 1 every commit already ran the estimate of all four candidates (coeff_argmin):
 // these return the chosen candidate's estimate, ordered after that work.
 oid_status oid_estimate_begin(oid_ctx ctx, void* stream) {
+  NvtxRange nvtx_range("oid_estimate_begin");
   if (!ctx) return OID_EINVAL;
   if (ctx->p.coeff_mode != 1) return estimate_begin_impl(ctx, stream);
   if (!ctx->estimate_ready) return ctx->fail(OID_ESTATE, "no block ingested yet");
@@ -1544,6 +1556,7 @@ oid_status oid_estimate_begin(oid_ctx ctx, void* stream) {
 }
 
 oid_status oid_estimate_end(oid_ctx ctx, double* out_dev, void* stream) {
+  NvtxRange nvtx_range("oid_estimate_end");
   if (!ctx) return OID_EINVAL;
   if (ctx->p.coeff_mode != 1) return estimate_end_impl(ctx, out_dev, stream);
   if (!ctx->estimate_ready) return ctx->fail(OID_ESTATE, "no block ingested yet");
@@ -1631,6 +1644,7 @@ oid_status oid_gradient_finalize(oid_ctx ctx, double lo, double hi, double tol, 
 }
 
 oid_status oid_finalize(oid_ctx ctx, int64_t* J_host, double* P, int32_t P_on_device, void* basis_dev, void* stream) {
+  NvtxRange nvtx_range("oid_finalize");
   if (!ctx) return OID_EINVAL;
   if (ctx->pending_nc >= 0) return ctx->fail(OID_ESTATE, "a sketch is pending commit");
   cudaStream_t st = static_cast<cudaStream_t>(stream);

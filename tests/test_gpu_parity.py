@@ -530,7 +530,7 @@ def test_two_stream_estimates_match_one_stream(oid):
         two.estimate_end(out2[e])
     torch.cuda.synchronize()
     diff = (out1 != out2).any(dim=1).cpu().numpy()
-    assert not diff.any(), (np.flatnonzero(diff), out1[diff].cpu().numpy(), out2[diff].cpu().numpy())
+    assert not diff.any(), (np.flatnonzero(diff), out1[diff].cpu().numpy().tolist(), out2[diff].cpu().numpy().tolist())
     assert np.array_equal(one.J(), two.J())
     P1 = one.finalize()["P"]
     P2 = two.finalize()["P"]
@@ -570,7 +570,7 @@ def test_internal_side_streams_match_serial(oid, monkeypatch):
         par.estimate_end(out2[e])
     torch.cuda.synchronize()
     diff = (out1 != out2).any(dim=1).cpu().numpy()
-    assert not diff.any(), (np.flatnonzero(diff), out1[diff].cpu().numpy(), out2[diff].cpu().numpy())
+    assert not diff.any(), (np.flatnonzero(diff), out1[diff].cpu().numpy().tolist(), out2[diff].cpu().numpy().tolist())
     assert np.array_equal(serial.J(), par.J())
     r1, r2 = serial.finalize(basis=True), par.finalize(basis=True)
     torch.cuda.synchronize()

@@ -605,3 +605,50 @@ def test_argmin_mode_not_worse_than_alg4_on_c1():
     e4 = np.linalg.norm(A - o4.C @ o4.P)
     ea = np.linalg.norm(A - oa.C @ oa.P)
     assert ea <= 1.05 * e4, (ea, e4, [lg.qstar for lg in oa.log])
+
+
+# ------------------------------------------------------------------ paper-literal t-column epochs (NEXT-2)
+
+def test_t_epochs_equal_block_epochs_when_b_equals_t():
+    """With blocks of exactly t columns the buffer fills once per block: the t-column epochs are the
+    block epochs (same J, tau_old, P after every block)."""
+    A = c1_matrix(seed=61, m=300, n=48, rank=8, noise=1e-3)
+    ob = OracleOID(_params(300, 8, 24, 0.0, seed=3))
+    ot = OracleOID(_params(300, 8, 24, 0.0, seed=3, epochs="t"))
+    for j in range(0, 48, 8):
+        ob.ingest_block(A[:, j:j + 8])
+        ot.ingest_block(A[:, j:j + 8])
+        # (the Gram is accumulated per column in "t" mode: equal up to rounding)
+        assert np.array_equal(ob.J, ot.J) and np.allclose(ob.tau_old, ot.tau_old, rtol=1e-12)
+        assert np.allclose(ob.P, ot.P, atol=1e-11)
+
+
+def test_t_epochs_cross_block_boundaries():
+    """t = 8, blocks of 5: an epoch after every 8th column (columns 8, 16, ..., 40 of 42), its
+    candidates exactly the 8 buffered columns (global indices [8e, 8e + 8)), even when they span two
+    blocks; the 2 leftover columns stay buffered (sketched and counted, no epoch yet)."""
+    A = c1_matrix(seed=62, m=300, n=42, rank=8, noise=1e-3)
+    o = OracleOID(_params(300, 8, 24, 0.0, seed=4, epochs="t"))
+    for j in range(0, 42, 5):
+        o.ingest_block(A[:, j:j + 5])
+    assert o.epoch == 5 and len(o._D) == 2 and o.n_obs == 42
+    assert abs(o.frob2 - np.sum(A * A)) <= 1e-12 * np.sum(A * A)
+    for lg in o.log:
+        for (_, _, r, *_rest) in [d for d in lg.decisions if d[0] == "admit"]:
+            assert 0 <= r < 8
+        Jnew = set(lg.J[lg.J >= 0].tolist())
+        assert all(0 <= ji < 8 * (lg.epoch + 1) for ji in Jnew)
+    # the estimate covers all 42 observed columns (current basis' LS for the 2 buffered ones)
+    assert o.current_P().shape == (8, 42)
+
+
+def test_t_epochs_first_epoch_forced_admissions():
+    """the first t columns only fill D; at the first epoch every slot is vacant and the
+    first t columns are the candidates (C1 first-block argument with D = the first t columns)."""
+    A = c1_matrix(seed=63, m=400, n=20, rank=10, noise=1e-6)
+    o = OracleOID(_params(400, 10, 30, 0.0, seed=5, epochs="t"))
+    o.ingest_block(A[:, :7])
+    assert o.epoch == 0 and np.all(o.J == -1)
+    o.ingest_block(A[:, 7:14])
+    assert o.epoch == 1
+    assert np.all((o.J == -1) | (o.J < 10))
