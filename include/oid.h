@@ -104,7 +104,12 @@ typedef struct {
      oid_error_estimate the chosen candidate's estimate; oid_get field 14 logs the choices.
      Requires a single shard (row_begin = 0, row_end = m) and ell1, ell2 > 0.                  */
   int32_t coeff_mode;
-  int32_t reserved0;
+  /* Epochs (NEXT-2).  0: one ingest block = one epoch (reading R4, the hot path).  1: the paper's
+     buffer: every column is sketched, counted and copied into a device buffer
+     D (m_loc x k in the data dtype, part of the workspace); an epoch over D's k columns runs
+     whenever k are buffered, across block boundaries.  Not combined with coeff_mode = 1 or the
+     gradient variant.  oid_error_estimate is available once the first epoch has run.           */
+  int32_t epoch_mode;
 } oid_params;
 
 typedef struct {

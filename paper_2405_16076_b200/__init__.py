@@ -43,7 +43,7 @@ class OidParams(ctypes.Structure):
                 ("profile", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("grad_nfields", ctypes.c_int32), ("grad_nx", ctypes.c_int32), ("grad_ny", ctypes.c_int32),
                 ("omega_cache", ctypes.c_int32), ("grad_hx", ctypes.c_double), ("grad_hy", ctypes.c_double),
-                ("coeff_mode", ctypes.c_int32), ("reserved0", ctypes.c_int32)]
+                ("coeff_mode", ctypes.c_int32), ("epoch_mode", ctypes.c_int32)]
 
 
 class OidStats(ctypes.Structure):
@@ -118,11 +118,14 @@ def hutch_split(ell):
 
 def make_params(m, k, ell, b_max, n_cap, lam, split=None, eps=0.5, delta=0.05, c=1.0, seed=0, dtype="f64",
                 row_begin=0, row_end=None, k1_mode=K1_AUTO, profile=False, device=0, grad=None,
-                omega_cache=False, coeff="alg4"):
+                omega_cache=False, coeff="alg4", epochs="block"):
     """grad: None, or (nfields, nx, ny[, hx, hy]) for the gradient-enhanced variant (A11).
-    coeff: "alg4" (Alg 4 every epoch, the hot path) or "argmin" (Algs 4-7 + NA-Hutch++ argmin, NEXT-1)."""
+    coeff: "alg4" (Alg 4 every epoch, the hot path) or "argmin" (Algs 4-7 + NA-Hutch++ argmin, NEXT-1).
+    epochs: "block" (one block = one epoch, R4) or "t" (the paper's t-column buffer, NEXT-2)."""
     if coeff not in ("alg4", "argmin"):
         raise ValueError("coeff must be 'alg4' or 'argmin'")
+    if epochs not in ("block", "t"):
+        raise ValueError("epochs must be 'block' or 't'")
     split = hutch_split(ell) if split is None else split
     g = tuple(grad) + (0.0, 0.0)[len(grad) - 3:] if grad is not None else (0, 0, 0, 0.0, 0.0)
     return OidParams(m=m, row_begin=row_begin, row_end=m if row_end is None else row_end, n_cap=n_cap, k=k, ell=ell,
@@ -130,7 +133,7 @@ def make_params(m, k, ell, b_max, n_cap, lam, split=None, eps=0.5, delta=0.05, c
                      seed=seed, dtype=OID_F64 if dtype in ("f64", "float64") else OID_F32, k1_mode=k1_mode,
                      profile=int(bool(profile)), device=device, grad_nfields=int(g[0]), grad_nx=int(g[1]),
                      grad_ny=int(g[2]), omega_cache=int(omega_cache), grad_hx=float(g[3]), grad_hy=float(g[4]),
-                     coeff_mode=1 if coeff == "argmin" else 0)
+                     coeff_mode=1 if coeff == "argmin" else 0, epoch_mode=1 if epochs == "t" else 0)
 
 
 def workspace_bytes(params):

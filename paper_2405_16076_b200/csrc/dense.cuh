@@ -71,8 +71,10 @@ __global__ void __launch_bounds__(256) dgemm_kernel(int M, int N, int K, double 
 }
 
 // Gram += Y Y^T (ell x ell), S(:, n0:n0+nc) = Y, frob2 += sum n_j  (Alg 3 steps 10-13).
-__global__ void gram_update_kernel(const double* __restrict__ Yp, int ell, int nc, double* __restrict__ gram,
-                                   double* __restrict__ S, int64_t n0, double* __restrict__ scal) {
+// Y: ell x nc sketches (ld ell), nrm: their nc squared column norms
+__global__ void gram_update_kernel(const double* __restrict__ Yp, const double* __restrict__ nrm, int ell, int nc,
+                                   double* __restrict__ gram, double* __restrict__ S, int64_t n0,
+                                   double* __restrict__ scal) {
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t nn = static_cast<int64_t>(ell) * ell;
   if (idx < nn) {
@@ -85,8 +87,19 @@ __global__ void gram_update_kernel(const double* __restrict__ Yp, int ell, int n
   if (idx < ny) S[n0 * ell + idx] = Yp[idx];
   if (idx == 0) {
     double f = scal[0];
-    for (int j = 0; j < nc; ++j) f += Yp[ny + j];
+    for (int j = 0; j < nc; ++j) f += nrm[j];
     scal[0] = f;
+  }
+}
+
+// dst(:, j) = src(:, j), j < ncols, rows < m (column-major, leading dimensions lds / ldd)
+template <typename T>
+__global__ void copy_cols_kernel(const T* __restrict__ src, int64_t lds, T* __restrict__ dst, int64_t ldd, int64_t m,
+                                 int ncols) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < m * ncols;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = i / m, r = i - j * m;
+    dst[j * ldd + r] = src[j * lds + r];
   }
 }
 

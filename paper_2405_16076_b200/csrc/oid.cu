@@ -121,7 +121,7 @@ struct Bump {
 struct Layout {
   size_t S, gram, Ypart, k1part, k1npart, gB, gV, mu, mu_sorted, Yc, Tsc, tau, scal, J, tau_old, admit, counts,
       flags, counters, C, SJ, sjB, sjV, sjsig, sjw, sjZ, Sjpinv, Pexp, AJP, G, Gsum, Gpart, cB, cV, csig, cw, cZ, M,
-      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, wyT, sjG, cG, cBt, cZ2, dbg, Jsnap, Dsnap, gcnt, S1, S2, YpG, GX, OGO, gH, gHV, gHs, gHw, gHZ, gHp, gR, gCm, gE, gLst, gLV, gLs, gLw, gLZ, gLp, gRhs, gscal, td2, te2, Vh2, tauv2, wyT2, ldl2, mu2, cum, elog, eslog, omega, trA, trW, Pcand, Pchosen, Pext, Rres, Gprev, gpH, gpV, gpMu, gpW, Gpinv, Xc, Dx, Dxp, Tm, cest, est_ch, est4, qlog, Jprev, olds, nold, qsel, total;
+      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, wyT, sjG, cG, cBt, cZ2, dbg, Jsnap, Dsnap, gcnt, S1, S2, YpG, GX, OGO, gH, gHV, gHs, gHw, gHZ, gHp, gR, gCm, gE, gLst, gLV, gLs, gLw, gLZ, gLp, gRhs, gscal, td2, te2, Vh2, tauv2, wyT2, ldl2, mu2, cum, elog, eslog, omega, trA, trW, Pcand, Pchosen, Pext, Rres, Gprev, gpH, gpV, gpMu, gpW, Gpinv, Xc, Dx, Dxp, Tm, cest, est_ch, est4, qlog, Jprev, olds, nold, qsel, Dpool, Dnorm, total;
 };
 
 int64_t m_local(const oid_params& p) { return p.row_end - p.row_begin; }
@@ -134,13 +134,15 @@ Layout make_layout(const oid_params& p) {
   Layout L{};
   Bump b;
   const size_t d = sizeof(double);
-  const size_t ell = p.ell, t = p.k, bm = p.b_max, n = p.n_cap;
+  const size_t ell = p.ell, t = p.k, n = p.n_cap;
+  // candidates per epoch: the block (b_max) or, with paper-literal epochs, the t buffered columns
+  const size_t bm = p.epoch_mode == 1 ? std::max<size_t>(p.b_max, p.k) : p.b_max;
   const size_t ncb = 64;
   const size_t ga = p.grad_nfields > 0 ? 3 : 1;   // augmented sketch [Y; Y1; Y2] (A11)
   const size_t ellg = ga * ell;                     // order of the Gram whose spectrum A4/A5 use
   L.S = b.take(ell * n * d);
   L.gram = b.take(ellg * ellg * d);
-  L.Ypart = b.take((ell + 1) * bm * d);
+  L.Ypart = b.take((ell + 1) * p.b_max * d);
   L.k1part = b.take(static_cast<size_t>(kK1MaxCtas) * ell * ncb * d);
   L.k1npart = b.take(static_cast<size_t>(kK1MaxCtas) * ncb * d);
   L.gB = b.take(ellg * ellg * d);
@@ -257,6 +259,10 @@ Layout make_layout(const oid_params& p) {
     L.gRhs = b.take(3 * ell * n * d);
     L.gscal = b.take(8 * d);
   }
+  if (p.epoch_mode == 1) {   // NEXT-2: the buffer D (m_loc x t, data dtype) and its squared norms
+    L.Dpool = b.take(static_cast<size_t>(m_local(p)) * t * dsize(p));
+    L.Dnorm = b.take(t * d);
+  }
   if (p.coeff_mode == 1) {
     // NEXT-1: candidates of Algs 5-7, the chosen P (= next P_prev), P_prev extended, a residual,
     // G_prev, G^+ and its eigen-decomposition, the cross Gram, cross dots and their chunk partials
@@ -318,6 +324,9 @@ const char* validate(const oid_params* p) {
     return "coeff_mode = 1 needs a single shard (row_begin = 0, row_end = m)";
   if (p->coeff_mode == 1 && (p->ell1 <= 0 || p->ell2 <= 0)) return "coeff_mode = 1 needs ell1, ell2 > 0";
   if (p->coeff_mode == 1 && p->grad_nfields > 0) return "coeff_mode = 1 is not combined with the gradient variant";
+  if (p->epoch_mode != 0 && p->epoch_mode != 1) return "epoch_mode must be 0 or 1";
+  if (p->epoch_mode == 1 && (p->coeff_mode != 0 || p->grad_nfields > 0))
+    return "epoch_mode = 1 (t-column epochs) is not combined with coeff_mode = 1 or the gradient variant";
   if (p->grad_nfields > 0) {
     if (p->grad_nx < 1 || p->grad_ny < 1 || int64_t(p->grad_nfields) * p->grad_nx * p->grad_ny != p->m)
       return "gradient variant: grad_nfields * grad_nx * grad_ny must equal m";
@@ -385,6 +394,8 @@ struct oid_ctx_s {
   bool use_side = true;       // diagnostics: OID_NO_SIDE=1 runs everything on the caller's stream
   int k1_free_sms = 0;        // SMs the persistent K1 grid leaves to concurrent streams (OID_K1_FREE)
   int last_nc = 0;            // columns of the last committed epoch (NEXT-1's P_prev extension)
+  int dcount = 0;             // NEXT-2: columns buffered in D since the last epoch
+  int64_t dbase = 0;          //         global index of D's first column
   bool timeline = false;      // diagnostics: OID_TIMELINE=1 records tagged events (oid_get 13)
   std::vector<std::pair<int, cudaEvent_t>> tl;
   char err[512] = {0};
@@ -719,7 +730,12 @@ oid_status do_sketch(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
 
 oid_status coeff_argmin(oid_ctx ctx, cudaStream_t st);   // NEXT-1, after the extern "C" block
 
-oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_t st) {
+// One epoch of Alg 3 (steps 15-27 + Alg 4) over nc candidate columns X (ld), whose
+// sketches are Ycand (ell x nc, ld ell), squared norms nrm and global indices base, base + 1, ...
+// do_a3: the block mode, where the candidates are the block itself and A3 (S, Gram, ||A_obs||^2)
+// runs here first; the t-column mode runs A3 per column segment itself (commit_tcols).
+oid_status post_epoch(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_t st, const double* Ycand,
+                      const double* nrm, int64_t base, bool do_a3) {
   const oid_params& p = ctx->p;
   const Layout& L = ctx->L;
   const int ell = p.ell, t = ctx->t;
@@ -733,12 +749,14 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   const int frob_idx = ctx->ga > 1 ? SC_FROB2_AUG : SC_FROB2;
   if (ctx->ga == 1) {
     // A3: S <- [S, Y], SS^T += YY^T, ||A_obs||^2 += sum n_j
-    gram_update_kernel<<<blocks_for(int64_t(ell) * ell), 256, 0, st>>>(Yp, ell, nc, ctx->d(L.gram), ctx->d(L.S), ctx->n_obs,
-                                                                      scal);
-    CKL();
+    if (do_a3) {
+      gram_update_kernel<<<blocks_for(int64_t(ell) * ell), 256, 0, st>>>(Yp, Yp + static_cast<int64_t>(ell) * nc, ell, nc,
+                                                                        ctx->d(L.gram), ctx->d(L.S), ctx->n_obs, scal);
+      CKL();
+    }
     // A4: spectrum of the Gram and lambda; A5: ridge scores
-    gather_scored_kernel<<<blocks_for(int64_t(ell) * ns), 256, 0, st>>>(ctx->d(L.S), ctx->ptr<int64_t>(L.J), t, Yp, nc, ell,
-                                                                        ctx->d(L.Yc));
+    gather_scored_kernel<<<blocks_for(int64_t(ell) * ns), 256, 0, st>>>(ctx->d(L.S), ctx->ptr<int64_t>(L.J), t, Ycand, nc,
+                                                                        ell, ctx->d(L.Yc));
     CKL();
   } else {
     // A11: augmented sketch [Y; Y1; Y2], its (3 ell)^2 Gram and energy
@@ -828,8 +846,8 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   if (p.coeff_mode == 1)   // NEXT-1: J_prev of Algs 6 and 7
     CK(cudaMemcpyAsync(ctx->ws + L.Jprev, ctx->ws + L.J, sizeof(int64_t) * t, cudaMemcpyDeviceToDevice, st));
   CK(cudaStreamWaitEvent(st, ctx->ev_sj_j, 0));
-  select_kernel<<<1, 256, 0, st>>>(ctx->ptr<int64_t>(L.J), ctx->d(L.tau_old), ctx->d(L.tau), Yp + int64_t(ell) * nc, t, nc,
-                                  ctx->factor, static_cast<uint32_t>(ctx->epoch), ctx->n_obs, ctx->key0, ctx->key1,
+  select_kernel<<<1, 256, 0, st>>>(ctx->ptr<int64_t>(L.J), ctx->d(L.tau_old), ctx->d(L.tau), nrm, t, nc,
+                                  ctx->factor, static_cast<uint32_t>(ctx->epoch), base, ctx->key0, ctx->key1,
                                   ctx->ptr<int>(L.admit), ctx->ptr<int>(L.counts), scal, ctx->ptr<int>(L.dirty),
                                   static_cast<int>(ctx->epoch + 1), ctx->ptr<unsigned long long>(L.cum),
                                   ctx->d(L.elog) + static_cast<size_t>(ctx->epoch) * kElogCols);
@@ -871,7 +889,7 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
     CKL();
   }
   tl_mark(ctx, st, 6);
-  ctx->n_obs += nc;
+  if (do_a3) ctx->n_obs += nc;
   ctx->last_nc = nc;
   cudaStream_t cs = ctx->use_side ? ctx->side : st;
   const int par = static_cast<int>(ctx->epoch & 1);
@@ -925,6 +943,64 @@ oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   ctx->estimate_ready = true;
   if (p.coeff_mode == 1) return coeff_argmin(ctx, st);
   return OID_OK;
+}
+
+// NEXT-2, paper-literal epochs: every column is sketched and counted and goes
+// into the buffer D (a device copy: the caller's block is gone by the time D fills); an epoch runs
+// over D's t columns whenever t are buffered, at the exact column where that happens.  A commit
+// that completes no epoch only moves the estimate's snapshot on (||A_obs||^2; J, S_J^+ unchanged).
+oid_status commit_tcols(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_t st) {
+  const oid_params& p = ctx->p;
+  const Layout& L = ctx->L;
+  const int ell = p.ell, t = ctx->t;
+  const int64_t m = ctx->m_loc;
+  double* Yp = ctx->d(L.Ypart);
+  const double* nrm_blk = Yp + static_cast<int64_t>(ell) * nc;
+  const size_t es = p.dtype == OID_F64 ? 8 : 4;
+  bool epoch_done = false;
+  for (int c0 = 0; c0 < nc;) {
+    const int q = std::min(nc - c0, t - ctx->dcount);
+    gram_update_kernel<<<blocks_for(int64_t(ell) * ell), 256, 0, st>>>(Yp + static_cast<int64_t>(ell) * c0, nrm_blk + c0, ell,
+                                                                      q, ctx->d(L.gram), ctx->d(L.S), ctx->n_obs,
+                                                                      ctx->d(L.scal));
+    CKL();
+    const unsigned g = static_cast<unsigned>(std::min<int64_t>(blocks_for(m * q), 8 * ctx->num_sms));
+    const uint8_t* src = static_cast<const uint8_t*>(X) + static_cast<size_t>(c0) * ld * es;
+    uint8_t* dst = reinterpret_cast<uint8_t*>(ctx->ws + L.Dpool) + static_cast<size_t>(ctx->dcount) * m * es;
+    if (p.dtype == OID_F64)
+      copy_cols_kernel<double><<<g, 256, 0, st>>>(reinterpret_cast<const double*>(src), ld, reinterpret_cast<double*>(dst), m, m, q);
+    else
+      copy_cols_kernel<float><<<g, 256, 0, st>>>(reinterpret_cast<const float*>(src), ld, reinterpret_cast<float*>(dst), m, m, q);
+    CKL();
+    CK(cudaMemcpyAsync(ctx->d(L.Dnorm) + ctx->dcount, nrm_blk + c0, sizeof(double) * q, cudaMemcpyDeviceToDevice, st));
+    ctx->n_obs += q;
+    ctx->dcount += q;
+    c0 += q;
+    if (ctx->dcount == t) {
+      oid_status s = post_epoch(ctx, ctx->ws + L.Dpool, m, t, st, ctx->d(L.S) + static_cast<int64_t>(ell) * ctx->dbase,
+                                ctx->d(L.Dnorm), ctx->dbase, false);
+      if (s != OID_OK) return s;
+      ctx->dbase += t;
+      ctx->dcount = 0;
+      epoch_done = true;
+    }
+  }
+  if (!epoch_done && ctx->epoch > 0) {
+    const int par = static_cast<int>((ctx->epoch + 1) & 1);   // the last epoch's parity
+    CK(cudaStreamWaitEvent(st, ctx->ev_snap_free[par], 0));
+    commit_snapshot_kernel<<<1, 256, 0, st>>>(ctx->ptr<int64_t>(L.J), ctx->ptr<int>(L.dirty), t,
+                                              ctx->ptr<int64_t>(L.Jsnap) + static_cast<size_t>(par) * t,
+                                              ctx->ptr<int>(L.Dsnap) + static_cast<size_t>(par) * t, ctx->d(L.scal), par);
+    CKL();
+    CK(cudaEventRecord(ctx->ev_committed, st));
+  }
+  return OID_OK;
+}
+
+oid_status do_commit(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_t st) {
+  if (ctx->p.epoch_mode == 1) return commit_tcols(ctx, X, ld, nc, st);
+  double* Yp = ctx->d(ctx->L.Ypart);
+  return post_epoch(ctx, X, ld, nc, st, Yp, Yp + static_cast<int64_t>(ctx->p.ell) * nc, ctx->n_obs, true);
 }
 
 oid_status check_block(oid_ctx ctx, const void* X, int64_t ld, int32_t nc) {

@@ -89,6 +89,7 @@ __global__ void scores_kernel(const double* __restrict__ T, const double* __rest
 }
 
 constexpr int kSelMaxT = 416;   // validated maximum of k
+constexpr int kSelH = 14;       // candidate chunks of 32 per selection (448 >= max(b_max, k))
 
 // Alg 3 steps 15-27, readings R4-R7, R14.  The t evictions are independent (one
 // thread per slot); the vacant slots are then filled in slot order (sequential by nature: slot
@@ -132,36 +133,40 @@ __global__ void __launch_bounds__(256) select_kernel(int64_t* __restrict__ J, do
   __syncthreads();
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
-    // candidate r's probability (float copies only index the smem; the tests use fp64)
-    double praw[2], pr[2];
-    bool ok[2];
+    // candidate r = lane + 32 h (h < kSelH: up to 448 candidates - a block of b_max <= 64, or
+    // the t buffered columns of a paper-literal epoch); fp64 probabilities
+    double praw[kSelH], pr[kSelH];
+    bool ok[kSelH];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < kSelH; ++h) {
       const int r = lane + 32 * h;
       ok[h] = r < nc && nrm[r] != 0.0;
       praw[h] = r < nc ? tau[t + r] * factor : 0.0;
       pr[h] = fmin(1.0, praw[h]);
     }
+    const int nh = (nc + 31) >> 5;
     int na = 0, nz = 0;
     for (int i0 = 0; i0 < t; i0 += 32) {
       uint32_t vm = __ballot_sync(0xffffffffu, i0 + lane < t && s_vac[i0 + lane]);
       while (vm) {
         const int i = i0 + __ffs(vm) - 1;
         vm &= vm - 1;
-        bool hit[2];
-        double u[2];
+        // first success in candidate order: chunks of 32 in order, the lowest hit of the first
+        // chunk that has one (the sequential scan's admission); draws past it are not evaluated
+        int rs = kSelH * 32;   // no admission
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          u[h] = ok[h] ? select_uniform(epoch, static_cast<uint32_t>(i), static_cast<uint32_t>(lane + 32 * h), key0, key1)
-                       : 1.0;
-          hit[h] = ok[h] && u[h] < pr[h];
+        for (int h = 0; h < kSelH; ++h) {
+          if (h >= nh) break;
+          const double u = ok[h] ? select_uniform(epoch, static_cast<uint32_t>(i), static_cast<uint32_t>(lane + 32 * h),
+                                                  key0, key1)
+                                 : 1.0;
+          const bool hit = ok[h] && u < pr[h];
+          const uint32_t bh = __ballot_sync(0xffffffffu, hit);
+          const int rh = bh ? 32 * h + __ffs(bh) - 1 : kSelH * 32;
+          if (ok[h] && lane + 32 * h <= rh) mm = fmin(mm, fabs(u - praw[h]) / fmax(praw[h], 0x1p-24));
+          if (bh) { rs = rh; break; }
         }
-        const uint32_t b0 = __ballot_sync(0xffffffffu, hit[0]), b1 = __ballot_sync(0xffffffffu, hit[1]);
-        const int rs = b0 ? __ffs(b0) - 1 : (b1 ? 32 + __ffs(b1) - 1 : 64);   // 64: no admission
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-          if (ok[h] && lane + 32 * h <= rs) mm = fmin(mm, fabs(u[h] - praw[h]) / fmax(praw[h], 0x1p-24));
-        if (rs < 64) {
+        if (rs < kSelH * 32) {
           if (lane == 0) {
             J[i] = base + rs;
             tau_old[i] = tau[t + rs];
@@ -169,7 +174,9 @@ __global__ void __launch_bounds__(256) select_kernel(int64_t* __restrict__ J, do
             admit[2 * na + 1] = rs;
             dirty[i] = dtag;   // epoch tag of the admission (estimates pick tags newer than theirs)
           }
-          if (lane == (rs & 31)) ok[rs >> 5] = false;   // consumed
+#pragma unroll
+          for (int h = 0; h < kSelH; ++h)
+            if (lane == (rs & 31) && h == (rs >> 5)) ok[h] = false;   // consumed
           ++na;
         } else if (s_ev[i]) {
           if (lane == 0) admit[2 * (nc + t) - 2 - 2 * nz] = i;

@@ -66,7 +66,7 @@ def test_workspace_query_validates(oid):
 
 def test_struct_layout_matches_header(oid):
     # oid_params: 4 int64 + 6 int32 + 4 double + uint64 + 4 int32 = 32 + 24 + 32 + 8 + 16 = 112 bytes,
-    # then the gradient-variant block: 4 int32 + 2 double = 32 bytes, then coeff_mode + reserved0
+    # then the gradient-variant block: 4 int32 + 2 double = 32 bytes, then coeff_mode + epoch_mode
     assert ctypes.sizeof(oid.OidParams) == 152
     assert oid.OidParams.grad_nfields.offset == 112 and oid.OidParams.grad_hx.offset == 128
     assert oid.OidParams.coeff_mode.offset == 144

@@ -445,6 +445,38 @@ def test_argmin_coefficients_match_oracle(oid, dtype):
     assert abs(est["e2"] - eng.get(14)[-1][2 + qi]) <= 1e-12 * o.frob2   # the chosen candidate's estimate
 
 
+@pytest.mark.parametrize("b,lam", [(5, 0.0), (8, -1.0), (13, 0.05)])
+def test_t_column_epochs_match_oracle(oid, b, lam):
+    """NEXT-2 (epochs = "t"): the t = k buffered columns are copied into the device
+    buffer D and an epoch runs at the exact column where D fills, across block boundaries
+    (b = 5, 13 do not divide t = 12; b = 8 straddles every other block).  Against the oracle's
+    t-column epochs: J bit-exact and tau_old to 1e-8 after every block, the epoch count, P and the
+    NA-Hutch++ estimate (every column covered) within 1e-5."""
+    m, n, k, ell = 1500, 120, 12, 36
+    A = c1_matrix(seed=70 + b, m=m, n=n, rank=12, noise=1e-3)
+    split = (6, 12, 18)
+    p = oid.make_params(m=m, k=k, ell=ell, b_max=b, n_cap=n, lam=lam, split=split, seed=9, epochs="t")
+    eng = oid.Engine(p)
+    o = OracleOID(OracleParams(m=m, k=k, ell=ell, ell1=6, ell2=12, ell3=18, lam=lam, seed=9, epochs="t"))
+    Ad = _dev(A, np.float64)
+    for j in range(0, n, b):
+        eng.ingest_block(Ad[:, j:j + b])
+        o.ingest_block(A[:, j:j + b])
+        assert eng.stats()["epochs"] == o.epoch
+        low = o.first_low_margin_epoch()
+        if low is not None:
+            pytest.skip(f"oracle decision margin < 1e-6 at epoch {low}")
+        assert np.array_equal(eng.J(), o.J), (j, eng.J(), o.J)
+        assert np.allclose(eng.get(1), o.tau_old, rtol=1e-8, atol=0), j
+    assert eng.stats()["n_obs"] == n
+    P = eng.finalize()["P"].cpu().numpy()
+    Pref = o.current_P()
+    assert np.linalg.norm(P - Pref) / np.linalg.norm(Pref) < 1e-5
+    est, ref = eng.error_estimate(), o.error_estimate()
+    for key in ("e2", "T", "gpp"):
+        assert abs(est[key] - ref[key]) <= 1e-5 * o.frob2, (key, est[key], ref[key])
+
+
 def test_nonfinite_input_flagged(oid):
     A = np.random.default_rng(5).standard_normal((320, 8))
     A[7, 3] = np.nan
