@@ -1502,7 +1502,9 @@ static oid_status estimate_begin_impl(oid_ctx ctx, void* stream) {
   tl_mark(ctx, cs2, 13);
   s0 = estimate_pre(ctx, cs2, par);
   if (s0 != OID_OK) return s0;
-  CK(cudaEventRecord(ctx->ev_sj_free[par], cs2));   // S_J, S_J^+ of this parity are free again
+  est_kappa_kernel<<<1, 1, 0, cs2>>>(ctx->d(L.scal), par);
+  CKL();
+  CK(cudaEventRecord(ctx->ev_sj_free[par], cs2));   // S_J, S_J^+ (and kappa) of this parity are free again
   tl_mark(ctx, cs2, 14);
   tl_mark(ctx, gs, 8);
   // A9: exact basis Gram G = A_J^T A_J, incremental: only the rows/columns of

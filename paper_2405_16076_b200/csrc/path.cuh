@@ -324,9 +324,14 @@ __global__ void commit_snapshot_kernel(const int64_t* __restrict__ J, const int*
   if (threadIdx.x == 0) scal[SC_FROB2_SNAP + par] = scal[SC_FROB2];
 }
 
-// Scalars of the estimated epoch (parity par) for hutch_final_kernel.
+// Scalars of the estimated epoch (parity par) for hutch_final_kernel: ||A_obs||^2 of the
+// snapshot (protected by ev_snap_free until the estimate ends) ...
 __global__ void est_scalars_kernel(double* __restrict__ scal, int par) {
   scal[SC_FROB2_EST] = scal[SC_FROB2_SNAP + par];
+}
+// ... and kappa(S_J) of that epoch's Alg 4, taken in estimate_begin BEFORE ev_sj_free releases the
+// parity: the A8 chain of the commit two epochs later rewrites SC_KAPPA_SNAP + par after that event
+__global__ void est_kappa_kernel(double* __restrict__ scal, int par) {
   scal[SC_KAPPA_EST] = scal[SC_KAPPA_SNAP + par];
 }
 

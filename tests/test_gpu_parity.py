@@ -536,9 +536,13 @@ def test_virtual_shards_match_single(oid):
     assert abs(out[5].item() - ref["est_rel"]) < 1e-8
 
 
-def test_two_stream_estimates_match_one_stream(oid):
+@pytest.mark.parametrize("delay_cycles", [0, 4_000_000])
+def test_two_stream_estimates_match_one_stream(oid, delay_cycles):
     """Estimates on a second stream (overlapping the next block's ingest)
-    give bitwise the same J, estimates and P as the single-stream engine."""
+    give bitwise the same J, estimates and P as the single-stream engine.  delay_cycles > 0 holds
+    the estimate stream back (~2 ms spin before each estimate), so the ingest runs epochs ahead
+    of the estimates and every event guarding a parity buffer is exercised (this caught kappa(S_J)
+    being read after its parity had been released)."""
     cfg = C3R
     gen = ChannelFlow(48, 33, 48, seed=cfg.data_seed)
     A = gen.block(0, 8 * cfg.b)
@@ -558,6 +562,9 @@ def test_two_stream_estimates_match_one_stream(oid):
         one.estimate_end(out1[e])
         with torch.cuda.stream(hi):
             two.ingest_block(Ad[:, j:j + cfg.b])
+        if delay_cycles:
+            with torch.cuda.stream(lo):
+                torch.cuda._sleep(delay_cycles)
         two.estimate_begin()
         two.estimate_end(out2[e])
     torch.cuda.synchronize()
