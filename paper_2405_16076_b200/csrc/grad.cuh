@@ -154,6 +154,28 @@ __global__ void omega_g_omega_kernel(int ell, int64_t m, GradGrid g, uint32_t ke
   OGO[static_cast<int64_t>(p) * ell * ell + idx] = acc;
 }
 
+// W(:, j) = G^p omega_{s0 + j} (m x ns, ld m): the stencil applied to sketch row s0 + j, so that
+// Omega W = (Omega G^p Omega^T)(:, s0 .. s0 + ns) comes out of the tensor-core K1 (grad_ogo)
+__global__ void omega_g_cols_kernel(int s0, int ns, int64_t m, GradGrid g, int p, uint32_t key0, uint32_t key1,
+                                    double scale, double* __restrict__ W) {
+  __shared__ double qd[16];
+  if (threadIdx.x < 16) qd[threadIdx.x] = c_qtab_f64[threadIdx.x];
+  __syncthreads();
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < m * ns;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int j = static_cast<int>(idx / m);
+    const int64_t q = idx - static_cast<int64_t>(j) * m;
+    const int64_t local = q % (static_cast<int64_t>(g.nx) * g.ny);
+    const int i = static_cast<int>(local / g.ny), jj = static_cast<int>(local % g.ny);
+    int64_t op, om;
+    double w;
+    grad_axis(g, i, jj, p, op, om, w);
+    W[idx] = (w == 0.0) ? 0.0
+                        : (omega_entry(s0 + j, q + op, key0, key1, qd, scale) -
+                           omega_entry(s0 + j, q + om, key0, key1, qd, scale)) * w;
+  }
+}
+
 // out (rows x ncol) = [A0; c A1; c A2] stacked by rows (each A_p rows_p = ell x ncol, ld ell);
 // with J != nullptr, column j of A_p is A_p(:, J[j]) (zero for vacant slots)
 __global__ void stack3_kernel(const double* __restrict__ A0, const double* __restrict__ A1, const double* __restrict__ A2,

@@ -51,7 +51,7 @@ inline int gram_tc_chunks(int t) {           // short CTAs (several waves) so hi
 }
 constexpr int kMaxSweeps = 48;
 constexpr int kNumJacobiUses = 3;
-constexpr int kSymMaxPairs = 33;   // ceil(1024 / 16) / 2 + 1
+constexpr int kSymMaxPairs = 65;   // ceil(2048 / 16) / 2 + 1
 constexpr size_t kSmallSvdSmem = 200 * 1024;
 constexpr int kCrossChunks = 64;    // row chunks of the NEXT-1 cross dots (fixed-order sum)
 
@@ -331,7 +331,7 @@ const char* validate(const oid_params* p) {
     if (p->grad_nx < 1 || p->grad_ny < 1 || int64_t(p->grad_nfields) * p->grad_nx * p->grad_ny != p->m)
       return "gradient variant: grad_nfields * grad_nx * grad_ny must equal m";
     if (p->row_begin != 0 || p->row_end != p->m) return "gradient variant: single shard only (row_begin = 0, row_end = m)";
-    if (3 * p->ell > 1024) return "gradient variant: 3 ell must be <= 1024";
+    if (3 * p->ell > 2048) return "gradient variant: 3 ell must be <= 2048";
     if (!(p->grad_hx >= 0.0) || !(p->grad_hy >= 0.0)) return "gradient variant: spacings must be >= 0 (0 = 1/(N-1))";
   }
   return nullptr;
@@ -794,24 +794,28 @@ oid_status post_epoch(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream
     multisect_kernel<<<(nev * 32 + 255) / 256, 256, sizeof(double) * multisect_smem_doubles(ng), s3>>>(
         ctx->d(L.td), ctx->d(L.te), ng, ctx->d(L.mu), nev, 0);
     CKL();
-    lambda_sorted_kernel<<<1, 256, 0, s3>>>(ctx->d(L.mu), ng, p.k, ctx->d(L.gram), p.lambda, ell, scal, gate,
-                                            ctx->d(L.td), ctx->d(L.te), ctx->d(L.ldl), 1, frob_idx);
+    lambda_sorted_kernel<<<1, 256, sizeof(double) * 3 * ng, s3>>>(ctx->d(L.mu), ng, p.k, ctx->d(L.gram), p.lambda, ell,
+                                                                  scal, gate, ctx->d(L.td), ctx->d(L.te), ctx->d(L.ldl), 1,
+                                                                  frob_idx);
     CKL();
     {
-      const size_t qsm = sizeof(double) * kQStages * kRefChunk * tri_ldv(ng);
       const unsigned qg = (ns + kQV - 1) / kQV;
+      const size_t ring = sizeof(double) * kRefChunk * tri_ldv(ng);   // one stage
       if (ng <= 512)
-        tri_scores_multi_kernel<2><<<qg, 256, qsm, st>>>(ctx->d(L.Yc), ng, ns, ctx->d(L.Vh), ctx->d(L.wyT), ctx->d(L.ldl),
-                                                          gate, ctx->d(L.tau), ctx->d(L.Tsc));
-      else
-        tri_scores_multi_kernel<4><<<qg, 256, qsm, st>>>(ctx->d(L.Yc), ng, ns, ctx->d(L.Vh), ctx->d(L.wyT), ctx->d(L.ldl),
-                                                          gate, ctx->d(L.tau), ctx->d(L.Tsc));
+        tri_scores_multi_kernel<2, 256, kQStages><<<qg, 256, kQStages * ring, st>>>(
+            ctx->d(L.Yc), ng, ns, ctx->d(L.Vh), ctx->d(L.wyT), ctx->d(L.ldl), gate, ctx->d(L.tau), ctx->d(L.Tsc));
+      else if (ng <= 1024)
+        tri_scores_multi_kernel<4, 256, kQStages><<<qg, 256, kQStages * ring, st>>>(
+            ctx->d(L.Yc), ng, ns, ctx->d(L.Vh), ctx->d(L.wyT), ctx->d(L.ldl), gate, ctx->d(L.tau), ctx->d(L.Tsc));
+      else   // n <= 2048: 512 threads, one ring stage (a stage is 128 KB)
+        tri_scores_multi_kernel<4, 512, 1><<<qg, 512, ring, st>>>(
+            ctx->d(L.Yc), ng, ns, ctx->d(L.Vh), ctx->d(L.wyT), ctx->d(L.ldl), gate, ctx->d(L.tau), ctx->d(L.Tsc));
       CKL();
     }
     s = join_from(ctx, st, s3);
     if (s != OID_OK) return s;
-    tri_scores_chain_kernel<<<(ns + kQV - 1) / kQV, 128, 0, st>>>(ctx->d(L.Tsc), ng, ns, ctx->d(L.ldl), gate,
-                                                                  ctx->d(L.tau));
+    tri_scores_chain_kernel<<<(ns + kQV - 1) / kQV, 128, sizeof(double) * (kQV + 2) * ng, st>>>(
+        ctx->d(L.Tsc), ng, ns, ctx->d(L.ldl), gate, ctx->d(L.tau));
     CKL();
     tl_mark(ctx, st, 16);
     const int* g1 = gate + 1;
@@ -1119,12 +1123,28 @@ oid_status hutch_pre(oid_ctx ctx, cudaStream_t st, const double* P, const double
 
 // ---------------------------------------------------------------- gradient variant (A11)
 // Omega G^p Omega^T (l x l, p = 0, 1), regenerated once per context (finalize-time only)
+// Omega G^p Omega^T (l x l, p = 0, 1), once per context: for chunks of sketch rows s, W = G^p
+// Omega(s, :)^T (the stencil applied to the generated rows, m x chunk), then Omega W through the
+// tensor-core K1 like any block (O(l m) generation + l/chunk K1 passes instead of O(l^2 m) Philox)
 oid_status grad_ogo(oid_ctx ctx, cudaStream_t st) {
   if (ctx->ogo_ready) return OID_OK;
+  const Layout& L = ctx->L;
   const int ell = ctx->p.ell;
-  dim3 grid(blocks_for(int64_t(ell) * ell), 1, 2);
-  omega_g_omega_kernel<<<grid, 256, 0, st>>>(ell, ctx->m_loc, ctx->grid, ctx->key0, ctx->key1, ctx->qscale, ctx->d(ctx->L.OGO));
-  CKL();
+  const int64_t m = ctx->m_loc;
+  const int chunk = std::min(64, 2 * ctx->p.b_max);   // W lives in L.GX (2 m b_max doubles)
+  double* W = ctx->d(L.GX);
+  double* Y = ctx->d(L.YpG);                             // (l + 1) x chunk K1 output
+  for (int p = 0; p < 2; ++p)
+    for (int s0 = 0; s0 < ell; s0 += chunk) {
+      const int ns = std::min(chunk, ell - s0);
+      const unsigned g = static_cast<unsigned>(std::min<int64_t>(blocks_for(m * ns), 8 * ctx->num_sms));
+      omega_g_cols_kernel<<<g, 256, 0, st>>>(s0, ns, m, ctx->grid, p, ctx->key0, ctx->key1, ctx->qscale, W);
+      CKL();
+      oid_status s = sketch_one(ctx, W, m, ns, st, Y, true, false);
+      if (s != OID_OK) return s;
+      CK(cudaMemcpyAsync(ctx->d(L.OGO) + static_cast<size_t>(p) * ell * ell + static_cast<size_t>(s0) * ell, Y,
+                         sizeof(double) * ell * ns, cudaMemcpyDeviceToDevice, st));
+    }
   ctx->ogo_ready = true;
   return OID_OK;
 }
@@ -1287,10 +1307,22 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
         cudaSuccess)
       return bad(e);
     const int ref_smem = static_cast<int>(sizeof(double) * kQStages * kRefChunk * tri_ldv(kTriMaxN));
-    const int ref_smem_g = static_cast<int>(sizeof(double) * kQStages * kRefChunk * tri_ldv(kTriMaxG));
-    if ((e = cudaFuncSetAttribute(tri_scores_multi_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ref_smem)) != cudaSuccess)
+    const int ref_smem_1k = static_cast<int>(sizeof(double) * kQStages * kRefChunk * tri_ldv(1024));
+    const int ref_smem_2k = static_cast<int>(sizeof(double) * kRefChunk * tri_ldv(kTriMaxG));
+    if ((e = cudaFuncSetAttribute(tri_scores_multi_kernel<2, 256, kQStages>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  ref_smem)) != cudaSuccess)
       return bad(e);
-    if ((e = cudaFuncSetAttribute(tri_scores_multi_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, ref_smem_g)) != cudaSuccess)
+    if ((e = cudaFuncSetAttribute(tri_scores_multi_kernel<4, 256, kQStages>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  ref_smem_1k)) != cudaSuccess)
+      return bad(e);
+    if ((e = cudaFuncSetAttribute(tri_scores_multi_kernel<4, 512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  ref_smem_2k)) != cudaSuccess)
+      return bad(e);
+    if ((e = cudaFuncSetAttribute(tri_scores_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sizeof(double) * (kQV + 2) * kTriMaxG))) != cudaSuccess)
+      return bad(e);
+    if ((e = cudaFuncSetAttribute(lambda_sorted_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sizeof(double) * 3 * kTriMaxG))) != cudaSuccess)
       return bad(e);
     if ((e = cudaFuncSetAttribute(tridiag_panel_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
       return bad(e);

@@ -16,7 +16,7 @@ namespace cg2 = cooperative_groups;
 
 constexpr int kTriCtas = 16;
 constexpr int kTriMaxN = 512;
-constexpr int kTriMaxG = 1024;   // largest Gram order on the tridiagonal A4/A5 path (panels + cluster)
+constexpr int kTriMaxG = 2048;   // largest Gram order on the tridiagonal A4/A5 path (panels + cluster)
 constexpr int kTriRows = kTriMaxN / kTriCtas;   // 32 rows per CTA at the maximum size
 
 // Householder tridiagonalisation of the symmetric n x n matrix A (col-major), n <= 512.
@@ -391,9 +391,11 @@ tridiag_cluster_kernel(const double* __restrict__ A, int lda, int n, double* __r
 //   C: partial v^T p, and from the owner of row k + 1 that row of V and W (and p_{k+1}), which
 //      the next column's correction needs.
 constexpr int kPanNb = 32;
-constexpr int kPanMaxR = kTriMaxG / kTriCtas;   // 64
+constexpr int kPanMaxR = kTriMaxG / kTriCtas;   // 128
 __host__ __device__ constexpr int pan_rows(int n) { return 2 * ((n + 2 * kTriCtas - 1) / (2 * kTriCtas)); }
-constexpr int kPanSmem = 2 * kPanMaxR * (kPanNb + 1) * static_cast<int>(sizeof(double));
+// dynamic shared memory: V, W rows of this CTA (2 kPanMaxR (kPanNb + 1)) + the column buffers
+// xb[2][kTriCtas kPanMaxR]
+constexpr int kPanSmem = (2 * kPanMaxR * (kPanNb + 1) + 2 * kTriCtas * kPanMaxR) * static_cast<int>(sizeof(double));
 
 __global__ void __cluster_dims__(kTriCtas, 1, 1) __launch_bounds__(256, 1)
 tridiag_panel_kernel(const double* __restrict__ A, int n, int k0, int nb, double* __restrict__ d,
@@ -404,11 +406,12 @@ tridiag_panel_kernel(const double* __restrict__ A, int n, int k0, int nb, double
   const int R = pan_rows(n);
   const int r0 = c * R;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // V, W rows of this CTA (dynamic: 2 kPanMaxR (kPanNb + 1) doubles)
-  extern __shared__ double pan_smem[];
+  // V, W rows of this CTA and the two column buffers (dynamic, kPanSmem bytes)
+  extern __shared__ __align__(16) double pan_smem[];
   double (*Vs)[kPanNb + 1] = reinterpret_cast<double (*)[kPanNb + 1]>(pan_smem);
   double (*Ws)[kPanNb + 1] = reinterpret_cast<double (*)[kPanNb + 1]>(pan_smem + kPanMaxR * (kPanNb + 1));
-  __shared__ __align__(16) double xb[2][kTriCtas * kPanMaxR];
+  double (*xb)[kTriCtas * kPanMaxR] =
+      reinterpret_cast<double (*)[kTriCtas * kPanMaxR]>(pan_smem + 2 * kPanMaxR * (kPanNb + 1));
   __shared__ double ssb[2][kTriCtas];
   __shared__ double vtb[2][kTriCtas][2 * kPanNb];
   __shared__ double kb[2][kTriCtas];
@@ -708,7 +711,10 @@ __global__ void lambda_sorted_kernel(const double* __restrict__ mu, int n, int k
                                      const double* __restrict__ d, const double* __restrict__ e,
                                      double* __restrict__ ldl, int tri_ok, int frob_idx) {
   __shared__ double red[8];
-  __shared__ double mus[kTriMaxG], ds[kTriMaxG], es[kTriMaxG];   // the serial loops read shared memory
+  extern __shared__ double ls_smem[];   // mus, ds, es: 3 n doubles (the serial loops read shared memory)
+  double* mus = ls_smem;
+  double* ds = ls_smem + n;
+  double* es = ls_smem + 2 * n;
   double tr = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     tr += gram[static_cast<int64_t>(i) * n + i];   // Gram order n
@@ -882,10 +888,13 @@ __device__ __forceinline__ void cta_apply_q(double (&z)[2], int n, const double*
 // every thread applies z -= V u.
 constexpr int kQV = 4;   // vectors per CTA (kQV * kRefChunk == 32: one reduced value per lane)
 static_assert(kQV * kRefChunk == 32, "one reduced value per lane");
-template <int NS>   // vector entries per thread: n <= 256 NS
+// NS entries per thread, NT threads (n <= NT NS), QST ring stages (chunks 0 .. QST-1 issued up
+// front; chunk it + QST into stage it % QST once chunk it is fully consumed)
+template <int NS, int NT, int QST>
 __device__ __forceinline__ void cta_apply_qt_multi(double (&z)[kQV][NS], int n, const double* __restrict__ Vh,
                                                    const double* __restrict__ wyT, double* vring, double* tring,
-                                                   uint64_t* full, double (*redm)[8][32], double* us) {
+                                                   uint64_t* full, double (*redm)[NT / 32][32], double* us) {
+  constexpr int NW = NT / 32;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nk = n - 2, ldv = tri_ldv(n);
   if (nk <= 0) return;
@@ -893,7 +902,7 @@ __device__ __forceinline__ void cta_apply_qt_multi(double (&z)[kQV][NS], int n, 
   auto issue = [&](int b) {        // thread 0 only
     const int k0 = b * kRefChunk, k0e = k0 & ~1;
     const int nr = min(kRefChunk, nk - k0);
-    const int st = b % kQStages;
+    const int st = b % QST;
     const uint32_t row_bytes = static_cast<uint32_t>(ldv - k0e) * 8u;
     tri_mbar_expect(&full[st], static_cast<uint32_t>(nr) * row_bytes + 64u * 8u);
     q_bulk(tring + st * 64, wyT + b * 64, 64u * 8u, &full[st]);
@@ -901,22 +910,20 @@ __device__ __forceinline__ void cta_apply_qt_multi(double (&z)[kQV][NS], int n, 
       q_bulk(vring + (static_cast<size_t>(st) * kRefChunk + r) * ldv + k0e, Vh + static_cast<int64_t>(k0 + r) * ldv + k0e,
              row_bytes, &full[st]);
   };
-  if (tid == 0) {
-    issue(0);
-    if (nch > 1) issue(1);
-  }
+  if (tid == 0)
+    for (int b = 0; b < QST && b < nch; ++b) issue(b);
   for (int it = 0; it < nch; ++it) {
     const int k0 = it * kRefChunk;
     const int nr = min(kRefChunk, nk - k0);
-    const int st = it % kQStages;
-    tri_mbar_wait(&full[st], (it / kQStages) & 1);
+    const int st = it % QST;
+    tri_mbar_wait(&full[st], (it / QST) & 1);
     const double* vb = vring + static_cast<size_t>(st) * kRefChunk * ldv;
     double v[kRefChunk][NS];
 #pragma unroll
     for (int r = 0; r < kRefChunk; ++r)
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
-        const int i = tid + 256 * s;
+        const int i = tid + NT * s;
         v[r][s] = (r < nr && i > k0 && i < n) ? vb[r * ldv + i] : 0.0;   // rows <= k0 are zero in V
       }
     double val[32];
@@ -940,12 +947,11 @@ __device__ __forceinline__ void cta_apply_qt_multi(double (&z)[kQV][NS], int n, 
       }
     }
     redm[it & 1][warp][lane] = val[0];   // warp sum of value `lane` = (vector lane / 8, row lane % 8)
-    __syncthreads();                     // V_it in registers, redm complete; stage (it - 1) % 3 free
-    if (tid == 0 && it + 2 < nch) issue(it + 2);
+    __syncthreads();                     // V_it in registers, redm complete
     if (warp == 0) {
       double w = 0.0;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) w += redm[it & 1][q][lane];
+      for (int q = 0; q < NW; ++q) w += redm[it & 1][q][lane];
       const int c = lane & (kRefChunk - 1), base = lane & ~(kRefChunk - 1);
       const double* T = tring + st * 64;
       double u = 0.0;
@@ -956,7 +962,8 @@ __device__ __forceinline__ void cta_apply_qt_multi(double (&z)[kQV][NS], int n, 
       }
       us[(it & 1) * 32 + lane] = u;
     }
-    __syncthreads();
+    __syncthreads();                     // stage st (V and T) fully consumed
+    if (tid == 0 && it + QST < nch) issue(it + QST);
 #pragma unroll
     for (int q = 0; q < kQV; ++q)
 #pragma unroll
@@ -972,8 +979,8 @@ __device__ __forceinline__ void cta_apply_qt_multi(double (&z)[kQV][NS], int n, 
 
 // A5 fast path: tau(y) = z^T (T + sI)^-1 z with z = Q^T y = H_{n-3} ... H_0 y, y = column j of Yc
 // (ell x ncol), for kQV columns per CTA; the LDL^T chains run on kQV threads.  Runs when gate[0] != 0.
-template <int NS>
-__global__ void __launch_bounds__(256) tri_scores_multi_kernel(const double* __restrict__ Yc, int n, int ncol,
+template <int NS, int NT, int QST>
+__global__ void __launch_bounds__(NT) tri_scores_multi_kernel(const double* __restrict__ Yc, int n, int ncol,
                                                                const double* __restrict__ Vh, const double* __restrict__ wyT,
                                                                const double* __restrict__ ldl, const int* __restrict__ gate,
                                                                double* __restrict__ tau_out, double* __restrict__ zout) {
@@ -981,13 +988,13 @@ __global__ void __launch_bounds__(256) tri_scores_multi_kernel(const double* __r
   // exist (tri_scores_chain_kernel finishes); otherwise the whole score
   if (zout == nullptr && gate[0] == 0) return;
   extern __shared__ __align__(16) double ref_smem[];
-  __shared__ __align__(16) double tsm[kQStages * 64];
-  __shared__ __align__(8) uint64_t full[kQStages];
-  __shared__ double redm[2][8][32];
+  __shared__ __align__(16) double tsm[QST * 64];
+  __shared__ __align__(8) uint64_t full[QST];
+  __shared__ double redm[2][NT / 32][32];
   __shared__ double us[64];
   const int tid = threadIdx.x, j0 = blockIdx.x * kQV;
   if (tid == 0) {
-    for (int q = 0; q < kQStages; ++q) tri_mbar_init(&full[q], 1);
+    for (int q = 0; q < QST; ++q) tri_mbar_init(&full[q], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   double z[kQV][NS];
@@ -995,17 +1002,17 @@ __global__ void __launch_bounds__(256) tri_scores_multi_kernel(const double* __r
   for (int q = 0; q < kQV; ++q)
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
-      const int i = tid + 256 * s;
+      const int i = tid + NT * s;
       z[q][s] = (i < n && j0 + q < ncol) ? Yc[static_cast<int64_t>(j0 + q) * n + i] : 0.0;
     }
   __syncthreads();
-  cta_apply_qt_multi<NS>(z, n, Vh, wyT, ref_smem, tsm, full, redm, us);
+  cta_apply_qt_multi<NS, NT, QST>(z, n, Vh, wyT, ref_smem, tsm, full, redm, us);
   if (zout != nullptr) {
 #pragma unroll
     for (int q = 0; q < kQV; ++q)
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
-        const int i = tid + 256 * s;
+        const int i = tid + NT * s;
         if (i < n && j0 + q < ncol) zout[static_cast<int64_t>(j0 + q) * n + i] = z[q][s];
       }
     return;
@@ -1017,7 +1024,7 @@ __global__ void __launch_bounds__(256) tri_scores_multi_kernel(const double* __r
 #pragma unroll
   for (int q = 0; q < kQV; ++q)
 #pragma unroll
-    for (int s = 0; s < NS; ++s) if (tid + 256 * s < n) zs[q * n + tid + 256 * s] = z[q][s];
+    for (int s = 0; s < NS; ++s) if (tid + NT * s < n) zs[q * n + tid + NT * s] = z[q][s];
   for (int i = tid; i < 2 * n - 1; i += blockDim.x) ls[i] = ldl[i];
   __syncthreads();
   if (tid < kQV && j0 + tid < ncol) {
@@ -1038,17 +1045,18 @@ __global__ void __launch_bounds__(128) tri_scores_chain_kernel(const double* __r
                                                                const double* __restrict__ ldl, const int* __restrict__ gate,
                                                                double* __restrict__ tau_out) {
   if (gate[0] == 0) return;
-  __shared__ double zs[kQV][kTriMaxG];
-  __shared__ double ls[2 * kTriMaxG];
+  extern __shared__ double chain_smem[];   // zs[kQV][n], ls[2 n]: (kQV + 2) n doubles
+  double* zs = chain_smem;
+  double* ls = chain_smem + kQV * n;
   const int tid = threadIdx.x, j0 = blockIdx.x * kQV;
   for (int e = tid; e < kQV * n; e += blockDim.x) {
     const int q = e / n, i = e - q * n;
-    zs[q][i] = j0 + q < ncol ? Z[static_cast<int64_t>(j0 + q) * n + i] : 0.0;
+    zs[q * n + i] = j0 + q < ncol ? Z[static_cast<int64_t>(j0 + q) * n + i] : 0.0;
   }
   for (int i = tid; i < 2 * n - 1; i += blockDim.x) ls[i] = ldl[i];
   __syncthreads();
   if (tid < kQV && j0 + tid < ncol) {
-    const double* zq = zs[tid];
+    const double* zq = zs + tid * n;
     double y = zq[0];
     double acc = y * y * ls[0];
     for (int i = 1; i < n; ++i) {

@@ -43,9 +43,11 @@ C1 = Config("C1", 4096, 512, 16, 20, 48, (16, 16, 16), "f64", math.nan, 1001)
 C2 = Config("C2", 64 * 80, 20000, 64, 100, 256, hutch_split(256), "f32", -1.0, 1002)
 C3 = Config("C3", 3 * 192 * 129 * 192, 1000, 32, 200, 512, hutch_split(512), "f64", -1.0, 1003)
 C3R = Config("C3r", 3 * 48 * 33 * 48, 1000, 32, 200, 512, hutch_split(512), "f64", -1.0, 1003)
+C4 = Config("C4", 10 * 1024 * 1024, 2000, 32, 300, 640, hutch_split(640), "f64", -1.0, 1004)
+C4R = Config("C4r", 10 * 32 * 32, 2000, 32, 300, 640, hutch_split(640), "f64", -1.0, 1004)
 C5 = Config("C5", 1 << 27, 4096, 64, 400, 1024, hutch_split(1024), "f32", -1.0, 1005)
 C5R = Config("C5r", 1 << 18, 4096, 64, 400, 1024, hutch_split(1024), "f32", -1.0, 1005)
-CONFIGS = {c.name: c for c in (C1, C2, C3, C3R, C5, C5R)}
+CONFIGS = {c.name: c for c in (C1, C2, C3, C3R, C4, C4R, C5, C5R)}
 
 
 # --------------------------------------------------------------------------- C1
@@ -113,6 +115,51 @@ class ImageStream:
             noise = np.random.default_rng([self.seed, t]).standard_normal(x.size)
             out[:, jj] = (bg + blobs.sum(0)) * (1.0 + 0.01 * noise)
         return out.astype(dtype)
+
+
+# --------------------------------------------------------------------------- C4
+
+class ReactingFront:
+    """BASELINE config 3 (ignition stand-in), fp64: nf = 10 fields (temperature + 9 species)
+    on an N x N grid of the unit square, field f at rows [f N^2, (f+1) N^2), node (i, j) at
+    f N^2 + i N + j (reading Q17's layout).  Snapshot t: a tanh front of width 0.01 around a seeded
+    centre, radius r0 + v t with 20 sinusoidal wrinkle modes (amplitude ~1e-2, travelling),
+        T(x, t) = (1 + tanh((R(theta, t) - |x - c|) / 0.01)) / 2,
+    species f = s_f (T shifted by a seeded offset of the front, or its complement), s_f log-spaced
+    on [1e-6, 1] - the fields span six decades, as in the paper's ignition data.
+    """
+
+    def __init__(self, N=1024, nf=10, n=2000, seed=1004):
+        rng = np.random.default_rng(seed)
+        self.N, self.nf, self.n, self.seed = N, nf, n, seed
+        self.m = nf * N * N
+        self.c = 0.5 + 0.05 * rng.standard_normal(2)
+        self.r0 = 0.05
+        self.v = rng.uniform(0.15, 0.2) / n            # radius grows by ~0.15-0.2 over the stream
+        self.amp = 0.01 * rng.uniform(0.2, 1.0, 20) / np.arange(1, 21) ** 0.5
+        self.mode = np.arange(1, 21) + rng.integers(0, 3, 20)
+        self.phi = rng.uniform(0, 2 * np.pi, 20)
+        self.omega = rng.uniform(-0.01, 0.01, 20)
+        self.scale = np.logspace(0, -6, nf)             # temperature O(1) ... species down to 1e-6
+        self.shift = np.concatenate([[0.0], 0.01 * rng.standard_normal(nf - 1)])
+        self.sign = np.concatenate([[1.0], rng.choice([-1.0, 1.0], nf - 1)])
+
+    def block(self, t0, t1, row_begin=0, row_end=None):
+        N = self.N
+        row_end = self.m if row_end is None else row_end
+        i, j = np.meshgrid(np.arange(N), np.arange(N), indexing="ij")
+        x, y = (i / (N - 1)).ravel() - self.c[0], (j / (N - 1)).ravel() - self.c[1]
+        r, th = np.hypot(x, y), np.arctan2(y, x)
+        out = np.empty((self.m, t1 - t0))
+        for jj, t in enumerate(range(t0, t1)):
+            R = (self.r0 + self.v * t) * (1.0 + np.sum(self.amp[:, None] * np.sin(
+                self.mode[:, None] * th[None, :] + self.phi[:, None] + self.omega[:, None] * t), axis=0))
+            for f in range(self.nf):
+                T = 0.5 * (1.0 + np.tanh((R + self.shift[f] - r) / 0.01))
+                if self.sign[f] < 0:
+                    T = 1.0 - T
+                out[f * N * N:(f + 1) * N * N, jj] = self.scale[f] * T
+        return out[row_begin:row_end]
 
 
 # --------------------------------------------------------------------------- C3

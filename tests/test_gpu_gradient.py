@@ -78,3 +78,44 @@ def test_gradient_variant_parity(oid, nf, nx, ny, k, ell, b, dtype):
     mu_o, P_o = o.finalize(-3.0, 3.0, 1e-3)
     assert abs(np.log10(mu_g) - np.log10(mu_o)) <= 2e-3
     assert np.linalg.norm(P_g.cpu().numpy() - P_o) <= 1e-4 * np.linalg.norm(P_o)
+
+
+def test_gradient_variant_c4r_parity(oid):
+    """BASELINE config 3 at reduced grid (C4r: 10 reacting-front fields on 32 x 32, k = 300, l = 640,
+    so the augmented Gram is 3 l = 1920: the panel tridiagonalisation to 2048 and, when lambda_s
+    clamps to 0, the two-sided Jacobi at that order), 4 blocks of 32: J every epoch, the augmented
+    Gram, the sketched GCV at fixed mu and P(mu) (the reconstruction A_J P(mu) of SURVEY Q27 is then
+    the same up to that tolerance, the basis being bit-exact) against the oracle (P:625-719);
+    Omega G^p Omega^T through the tensor-core K1 (grad_ogo)."""
+    from synth import ReactingFront, C4R
+    nf, N, k, ell, b = 10, 32, C4R.k, C4R.ell, C4R.b
+    n = 4 * b
+    gen = ReactingFront(N=N, nf=nf, seed=C4R.data_seed)
+    A = gen.block(0, n)
+    m = A.shape[0]
+    split = C4R.split
+    p = oid.make_params(m=m, k=k, ell=ell, b_max=b, n_cap=n, lam=-1.0, split=split, seed=4, grad=(nf, N, N))
+    eng = oid.Engine(p)
+    o = OracleGradOID(OracleParams(m=m, k=k, ell=ell, ell1=split[0], ell2=split[1], ell3=split[2], lam=-1.0, seed=4),
+                      grid_gradient_operators(nf, N, N))
+    Ad = torch.from_numpy(np.asfortranarray(A)).to("cuda:0")
+    low = None
+    for e, j in enumerate(range(0, n, b)):
+        eng.ingest_block(Ad[:, j:j + b])
+        lg = o.ingest_block(A[:, j:j + b])
+        if low is None and any(d[5] < 1e-6 for d in lg.decisions):
+            low = e
+        if low is None:
+            assert np.array_equal(eng.J(), o.J), (e, eng.J(), o.J)
+    G = eng.get(3)
+    assert G.shape == (3 * ell, 3 * ell)
+    assert np.linalg.norm(G - o.gram) <= 1e-10 * np.linalg.norm(o.gram)
+    if low is not None:
+        pytest.skip(f"decision margin < 1e-6 at epoch {low}")
+    OGO = o.omega_g_omega()
+    for mu in (1e-2, 1.0):
+        g_gpu, g_ref = eng.gradient_gcv(mu), o.gcv(mu, OGO)
+        assert abs(g_gpu - g_ref) <= 1e-6 * abs(g_ref), (mu, g_gpu, g_ref)
+        P = eng.gradient_coefficients(mu).cpu().numpy()
+        Pr = o.coefficients(mu)
+        assert np.linalg.norm(P - Pr) <= 1e-5 * np.linalg.norm(Pr), mu
