@@ -114,8 +114,14 @@ def test_gradient_variant_c4r_parity(oid):
         pytest.skip(f"decision margin < 1e-6 at epoch {low}")
     OGO = o.omega_g_omega()
     for mu in (1e-2, 1.0):
+        # the fields span six decades (species down to 1e-6): the stacked sketched LS behind GCV has
+        # kappa ~ 1e6-1e7 here, so the bar is the north_star's 1e-5 (the small cases above hold 1e-7)
         g_gpu, g_ref = eng.gradient_gcv(mu), o.gcv(mu, OGO)
-        assert abs(g_gpu - g_ref) <= 1e-6 * abs(g_ref), (mu, g_gpu, g_ref)
+        assert abs(g_gpu - g_ref) <= 1e-5 * abs(g_ref), (mu, g_gpu, g_ref)
+        # with k = 300 slots on a numerically rank ~15 stream the basis is rank-deficient, so P(mu) is
+        # the min-norm solution and not well determined at the cutoff; the reconstruction is (SURVEY
+        # Q27): A_J P(mu) against the oracle's, the basis columns being bit-identical copies
         P = eng.gradient_coefficients(mu).cpu().numpy()
         Pr = o.coefficients(mu)
-        assert np.linalg.norm(P - Pr) <= 1e-5 * np.linalg.norm(Pr), mu
+        R, Rr = o.C @ P, o.C @ Pr
+        assert np.linalg.norm(R - Rr) <= 1e-5 * np.linalg.norm(Rr), (mu, np.linalg.norm(R - Rr) / np.linalg.norm(Rr))
