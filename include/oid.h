@@ -110,6 +110,13 @@ typedef struct {
      whenever k are buffered, across block boundaries.  Not combined with coeff_mode = 1 or the
      gradient variant.  oid_error_estimate is available once the first epoch has run.           */
   int32_t epoch_mode;
+  /* NEXT-4: a 3-D grid for the gradient variant.  grad_nz > 1: the fields live on grad_nx x
+     grad_ny x grad_nz nodes (node (i, j, l) of field f at row f nx ny nz + (i ny + j) nz + l),
+     three gradient components with spacings grad_hx, grad_hy, grad_hz (0: 1/(N-1)), augmented
+     sketch of 4 ell rows ((d + 1) ell <= 2048).  0 or 1: the 2-D grid above.                    */
+  int32_t grad_nz;
+  int32_t reserved1;
+  double grad_hz;
 } oid_params;
 
 typedef struct {

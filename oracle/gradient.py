@@ -67,6 +67,41 @@ def grid_gradient_operators(nf, nx, ny, hx=None, hy=None):
     return [sp.csr_matrix((vals[p], (rows[p], cols[p])), shape=(m, m)) for p in range(2)]
 
 
+def grid_gradient_operators_3d(nf, nx, ny, nz, hx=None, hy=None, hz=None):
+    """[G^1, G^2, G^3] (scipy CSR, m x m, m = nf nx ny nz) of eq:gradient_estimation_mat
+    on a 3-D grid (NEXT-4: the channel-flow analogue): node (i, j, l) of field f at row
+    f nx ny nz + (i ny + j) nz + l, coordinates (i hx, j hy, l hz), 1-ring = the axis neighbours
+    (up to 6); K_q stacks x(v_r) - x(v_q) (n_q x 3), K_q^+ its pseudo-inverse."""
+    hx = 1.0 / (nx - 1) if hx is None else hx
+    hy = 1.0 / (ny - 1) if hy is None else hy
+    hz = 1.0 / (nz - 1) if hz is None else hz
+    m = nf * nx * ny * nz
+    rows, cols, vals = ([], [], []), ([], [], []), ([], [], [])
+    steps = ((1, 0, 0), (-1, 0, 0), (0, 1, 0), (0, -1, 0), (0, 0, 1), (0, 0, -1))
+    for f in range(nf):
+        base = f * nx * ny * nz
+        for i in range(nx):
+            for j in range(ny):
+                for l in range(nz):
+                    q = base + (i * ny + j) * nz + l
+                    nbr, dx = [], []
+                    for (di, dj, dl) in steps:
+                        ii, jj, ll = i + di, j + dj, l + dl
+                        if 0 <= ii < nx and 0 <= jj < ny and 0 <= ll < nz:
+                            nbr.append(base + (ii * ny + jj) * nz + ll)
+                            dx.append((di * hx, dj * hy, dl * hz))
+                    Kp = np.linalg.pinv(np.array(dx, dtype=np.float64))     # 3 x n_q
+                    for p in range(3):
+                        for kk, r in enumerate(nbr):
+                            rows[p].append(q)
+                            cols[p].append(r)
+                            vals[p].append(Kp[p, kk])
+                        rows[p].append(q)
+                        cols[p].append(q)
+                        vals[p].append(-float(np.sum(Kp[p])))
+    return [sp.csr_matrix((vals[p], (rows[p], cols[p])), shape=(m, m)) for p in range(3)]
+
+
 def stacked_coefficients(S, Sg, J, mu):
     """P(mu) of eq:opt_grad_fullsketch: the minimiser of
     ||S_J X - S||^2 + mu sum_p ||S^p_J X - S^p||^2 with S = Omega A_obs, S^p = Omega G^p A_obs,

@@ -43,7 +43,8 @@ class OidParams(ctypes.Structure):
                 ("profile", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("grad_nfields", ctypes.c_int32), ("grad_nx", ctypes.c_int32), ("grad_ny", ctypes.c_int32),
                 ("omega_cache", ctypes.c_int32), ("grad_hx", ctypes.c_double), ("grad_hy", ctypes.c_double),
-                ("coeff_mode", ctypes.c_int32), ("epoch_mode", ctypes.c_int32)]
+                ("coeff_mode", ctypes.c_int32), ("epoch_mode", ctypes.c_int32),
+                ("grad_nz", ctypes.c_int32), ("reserved1", ctypes.c_int32), ("grad_hz", ctypes.c_double)]
 
 
 class OidStats(ctypes.Structure):
@@ -118,8 +119,9 @@ def hutch_split(ell):
 
 def make_params(m, k, ell, b_max, n_cap, lam, split=None, eps=0.5, delta=0.05, c=1.0, seed=0, dtype="f64",
                 row_begin=0, row_end=None, k1_mode=K1_AUTO, profile=False, device=0, grad=None,
-                omega_cache=False, coeff="alg4", epochs="block"):
-    """grad: None, or (nfields, nx, ny[, hx, hy]) for the gradient-enhanced variant (A11).
+                omega_cache=False, coeff="alg4", epochs="block", grad3=None):
+    """grad: None, or (nfields, nx, ny[, hx, hy]) for the gradient-enhanced variant (A11) on a 2-D
+    grid; grad3: (nfields, nx, ny, nz[, hx, hy, hz]) for the 3-D grid with three components (NEXT-4).
     coeff: "alg4" (Alg 4 every epoch, the hot path) or "argmin" (Algs 4-7 + NA-Hutch++ argmin, NEXT-1).
     epochs: "block" (one block = one epoch, R4) or "t" (the paper's t-column buffer, NEXT-2)."""
     if coeff not in ("alg4", "argmin"):
@@ -128,12 +130,17 @@ def make_params(m, k, ell, b_max, n_cap, lam, split=None, eps=0.5, delta=0.05, c
         raise ValueError("epochs must be 'block' or 't'")
     split = hutch_split(ell) if split is None else split
     g = tuple(grad) + (0.0, 0.0)[len(grad) - 3:] if grad is not None else (0, 0, 0, 0.0, 0.0)
+    nz, hz = 0, 0.0
+    if grad3 is not None:
+        g3 = tuple(grad3) + (0.0, 0.0, 0.0)[len(grad3) - 4:]
+        g, nz, hz = (g3[0], g3[1], g3[2], g3[4], g3[5]), int(g3[3]), float(g3[6])
     return OidParams(m=m, row_begin=row_begin, row_end=m if row_end is None else row_end, n_cap=n_cap, k=k, ell=ell,
                      b_max=b_max, ell1=split[0], ell2=split[1], ell3=split[2], lam=lam, eps=eps, delta=delta, c=c,
                      seed=seed, dtype=OID_F64 if dtype in ("f64", "float64") else OID_F32, k1_mode=k1_mode,
                      profile=int(bool(profile)), device=device, grad_nfields=int(g[0]), grad_nx=int(g[1]),
                      grad_ny=int(g[2]), omega_cache=int(omega_cache), grad_hx=float(g[3]), grad_hy=float(g[4]),
-                     coeff_mode=1 if coeff == "argmin" else 0, epoch_mode=1 if epochs == "t" else 0)
+                     coeff_mode=1 if coeff == "argmin" else 0, epoch_mode=1 if epochs == "t" else 0,
+                     grad_nz=nz, grad_hz=hz)
 
 
 def workspace_bytes(params):
@@ -266,7 +273,7 @@ class Engine:
 
     def get(self, field):
         ell, t, bm = self.p.ell, self.p.k, self.p.b_max
-        ga = 3 if self.p.grad_nfields > 0 else 1
+        ga = (4 if self.p.grad_nz > 1 else 3) if self.p.grad_nfields > 0 else 1
         n_obs = self.stats()["n_obs"] if field == 2 else 0
         epochs = self.stats()["epochs"] if field == 14 else 0
         shapes = {0: ((t,), np.int64), 1: ((t,), np.float64), 2: ((n_obs, ell), np.float64),

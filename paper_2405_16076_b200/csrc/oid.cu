@@ -121,7 +121,7 @@ struct Bump {
 struct Layout {
   size_t S, gram, Ypart, k1part, k1npart, gB, gV, mu, mu_sorted, Yc, Tsc, tau, scal, J, tau_old, admit, counts,
       flags, counters, C, SJ, sjB, sjV, sjsig, sjw, sjZ, Sjpinv, Pexp, AJP, G, Gsum, Gpart, cB, cV, csig, cw, cZ, M,
-      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, wyT, sjG, cG, cBt, cZ2, dbg, Jsnap, Dsnap, gcnt, S1, S2, YpG, GX, OGO, gH, gHV, gHs, gHw, gHZ, gHp, gR, gCm, gE, gLst, gLV, gLs, gLw, gLZ, gLp, gRhs, gscal, td2, te2, Vh2, tauv2, wyT2, ldl2, mu2, cum, elog, eslog, omega, trA, trW, Pcand, Pchosen, Pext, Rres, Gprev, gpH, gpV, gpMu, gpW, Gpinv, Xc, Dx, Dxp, Tm, cest, est_ch, est4, qlog, Jprev, olds, nold, qsel, Dpool, Dnorm, total;
+      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, wyT, sjG, cG, cBt, cZ2, dbg, Jsnap, Dsnap, gcnt, Sg, YpG, GX, OGO, gH, gHV, gHs, gHw, gHZ, gHp, gR, gCm, gE, gLst, gLV, gLs, gLw, gLZ, gLp, gRhs, gscal, td2, te2, Vh2, tauv2, wyT2, ldl2, mu2, cum, elog, eslog, omega, trA, trW, Pcand, Pchosen, Pext, Rres, Gprev, gpH, gpV, gpMu, gpW, Gpinv, Xc, Dx, Dxp, Tm, cest, est_ch, est4, qlog, Jprev, olds, nold, qsel, Dpool, Dnorm, total;
 };
 
 int64_t m_local(const oid_params& p) { return p.row_end - p.row_begin; }
@@ -138,7 +138,9 @@ Layout make_layout(const oid_params& p) {
   // candidates per epoch: the block (b_max) or, with paper-literal epochs, the t buffered columns
   const size_t bm = p.epoch_mode == 1 ? std::max<size_t>(p.b_max, p.k) : p.b_max;
   const size_t ncb = 64;
-  const size_t ga = p.grad_nfields > 0 ? 3 : 1;   // augmented sketch [Y; Y1; Y2] (A11)
+  // augmented sketch [Y; Y_1; ..; Y_d] (A11): d = 2 gradient components on a 2-D grid, 3 in 3-D
+  const size_t ga = p.grad_nfields > 0 ? (p.grad_nz > 1 ? 4 : 3) : 1;
+  const size_t gd = ga - 1;
   const size_t ellg = ga * ell;                     // order of the Gram whose spectrum A4/A5 use
   L.S = b.take(ell * n * d);
   L.gram = b.take(ellg * ellg * d);
@@ -236,11 +238,10 @@ Layout make_layout(const oid_params& p) {
   if (ga > 1) {
     // gradient variant (A11): S^p, their K1 outputs, G^p X, Omega G^p Omega^T, GCV / P(mu) scratch
     const size_t ml = static_cast<size_t>(m_local(p));
-    L.S1 = b.take(ell * n * d);
-    L.S2 = b.take(ell * n * d);
-    L.YpG = b.take(2 * (ell + 1) * bm * d);
-    L.GX = b.take(2 * ml * bm * d);
-    L.OGO = b.take(2 * ell * ell * d);
+    L.Sg = b.take(gd * ell * n * d);   // S^p = Omega G^p A_obs, p = 1..d
+    L.YpG = b.take(std::max<size_t>(2, gd) * (ell + 1) * bm * d);
+    L.GX = b.take(std::max<size_t>(2, gd) * ml * bm * d);
+    L.OGO = b.take(gd * ell * ell * d);
     L.gH = b.take(t * t * d);
     L.gHV = b.take(t * t * d);
     L.gHs = b.take(t * d);
@@ -250,13 +251,13 @@ Layout make_layout(const oid_params& p) {
     L.gR = b.take(ell * t * d);
     L.gCm = b.take(ell * ell * d);
     L.gE = b.take(ell * n * d);
-    L.gLst = b.take(3 * ell * t * d);
+    L.gLst = b.take(ga * ell * t * d);
     L.gLV = b.take(t * t * d);
     L.gLs = b.take(t * d);
     L.gLw = b.take(t * d);
-    L.gLZ = b.take(3 * ell * t * d);
-    L.gLp = b.take(t * 3 * ell * d);
-    L.gRhs = b.take(3 * ell * n * d);
+    L.gLZ = b.take(ga * ell * t * d);
+    L.gLp = b.take(t * ga * ell * d);
+    L.gRhs = b.take(ga * ell * n * d);
     L.gscal = b.take(8 * d);
   }
   if (p.epoch_mode == 1) {   // NEXT-2: the buffer D (m_loc x t, data dtype) and its squared norms
@@ -328,10 +329,13 @@ const char* validate(const oid_params* p) {
   if (p->epoch_mode == 1 && (p->coeff_mode != 0 || p->grad_nfields > 0))
     return "epoch_mode = 1 (t-column epochs) is not combined with coeff_mode = 1 or the gradient variant";
   if (p->grad_nfields > 0) {
-    if (p->grad_nx < 1 || p->grad_ny < 1 || int64_t(p->grad_nfields) * p->grad_nx * p->grad_ny != p->m)
-      return "gradient variant: grad_nfields * grad_nx * grad_ny must equal m";
+    const int64_t nz = p->grad_nz > 1 ? p->grad_nz : 1;
+    if (p->grad_nz < 0) return "gradient variant: grad_nz must be >= 0 (0 or 1: a 2-D grid)";
+    if (p->grad_nx < 1 || p->grad_ny < 1 || int64_t(p->grad_nfields) * p->grad_nx * p->grad_ny * nz != p->m)
+      return "gradient variant: grad_nfields * grad_nx * grad_ny (* grad_nz) must equal m";
+    if (!(p->grad_hz >= 0.0)) return "gradient variant: grad_hz must be >= 0";
     if (p->row_begin != 0 || p->row_end != p->m) return "gradient variant: single shard only (row_begin = 0, row_end = m)";
-    if (3 * p->ell > 2048) return "gradient variant: 3 ell must be <= 2048";
+    if ((p->grad_nz > 1 ? 4 : 3) * p->ell > 2048) return "gradient variant: (d + 1) ell must be <= 2048";
     if (!(p->grad_hx >= 0.0) || !(p->grad_hy >= 0.0)) return "gradient variant: spacings must be >= 0 (0 = 1/(N-1))";
   }
   return nullptr;
@@ -713,19 +717,20 @@ oid_status do_sketch(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   // gradient variant (A11): G^p X by the axis-neighbour stencils, then K1 on each
   // (same Omega, so the three sketches stack into [Omega a; Omega G^1 a; Omega G^2 a])
   const int64_t m = ctx->m_loc;
-  double* GX0 = ctx->d(L.GX);
-  double* GX1 = GX0 + m * p.b_max;
+  double* GX = ctx->d(L.GX);
+  const int64_t gstride = m * p.b_max;
   const unsigned gb = static_cast<unsigned>(std::min<int64_t>(blocks_for(m * nc), 8 * ctx->num_sms));
   if (p.dtype == OID_F64)
-    grad_stencil_kernel<double><<<gb, 256, 0, st>>>(static_cast<const double*>(X), ld, m, nc, ctx->grid, GX0, GX1);
+    grad_stencil_kernel<double><<<gb, 256, 0, st>>>(static_cast<const double*>(X), ld, m, nc, ctx->grid, GX, gstride);
   else
-    grad_stencil_kernel<float><<<gb, 256, 0, st>>>(static_cast<const float*>(X), ld, m, nc, ctx->grid, GX0, GX1);
+    grad_stencil_kernel<float><<<gb, 256, 0, st>>>(static_cast<const float*>(X), ld, m, nc, ctx->grid, GX, gstride);
   CKL();
-  double* Y1 = ctx->d(L.YpG);
-  double* Y2 = Y1 + static_cast<size_t>(p.ell + 1) * p.b_max;
-  s = sketch_one(ctx, GX0, m, nc, st, Y1, true, false);
-  if (s != OID_OK) return s;
-  return sketch_one(ctx, GX1, m, nc, st, Y2, true, false);
+  for (int q = 0; q < ctx->ga - 1; ++q) {
+    s = sketch_one(ctx, GX + q * gstride, m, nc, st, ctx->d(L.YpG) + static_cast<size_t>(q) * (p.ell + 1) * p.b_max, true,
+                   false);
+    if (s != OID_OK) return s;
+  }
+  return OID_OK;
 }
 
 oid_status coeff_argmin(oid_ctx ctx, cudaStream_t st);   // NEXT-1, after the extern "C" block
@@ -759,15 +764,15 @@ oid_status post_epoch(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream
                                                                         ell, ctx->d(L.Yc));
     CKL();
   } else {
-    // A11: augmented sketch [Y; Y1; Y2], its (3 ell)^2 Gram and energy
-    double* Y1 = ctx->d(L.YpG);
-    double* Y2 = Y1 + static_cast<size_t>(ell + 1) * p.b_max;
-    gram_update_aug_kernel<<<blocks_for(int64_t(ng) * ng), 256, 0, st>>>(Yp, Y1, Y2, ell, nc, ctx->d(L.gram), ctx->d(L.S),
-                                                                         ctx->d(L.S1), ctx->d(L.S2), ctx->n_obs, scal);
+    // A11: augmented sketch [Y; Y_1; ..; Y_d], its ((d+1) ell)^2 Gram and energy
+    const int64_t ystride = static_cast<int64_t>(ell + 1) * p.b_max, sstride = static_cast<int64_t>(ell) * p.n_cap;
+    gram_update_aug_kernel<<<blocks_for(int64_t(ng) * ng), 256, 0, st>>>(Yp, ctx->d(L.YpG), ystride, ctx->ga, ell, nc,
+                                                                         ctx->d(L.gram), ctx->d(L.S), ctx->d(L.Sg), sstride,
+                                                                         ctx->n_obs, scal);
     CKL();
-    gather_scored_aug_kernel<<<blocks_for(int64_t(ng) * ns), 256, 0, st>>>(ctx->d(L.S), ctx->d(L.S1), ctx->d(L.S2),
-                                                                           ctx->ptr<int64_t>(L.J), t, Yp, Y1, Y2, nc, ell,
-                                                                           ctx->d(L.Yc));
+    gather_scored_aug_kernel<<<blocks_for(int64_t(ng) * ns), 256, 0, st>>>(ctx->d(L.S), ctx->d(L.Sg), sstride,
+                                                                           ctx->ptr<int64_t>(L.J), t, Yp, ctx->d(L.YpG),
+                                                                           ystride, ctx->ga, nc, ell, ctx->d(L.Yc));
     CKL();
   }
   int* gate = ctx->ptr<int>(L.gate);
@@ -1134,7 +1139,7 @@ oid_status grad_ogo(oid_ctx ctx, cudaStream_t st) {
   const int chunk = std::min(64, 2 * ctx->p.b_max);   // W lives in L.GX (2 m b_max doubles)
   double* W = ctx->d(L.GX);
   double* Y = ctx->d(L.YpG);                             // (l + 1) x chunk K1 output
-  for (int p = 0; p < 2; ++p)
+  for (int p = 0; p < ctx->ga - 1; ++p)
     for (int s0 = 0; s0 < ell; s0 += chunk) {
       const int ns = std::min(chunk, ell - s0);
       const unsigned g = static_cast<unsigned>(std::min<int64_t>(blocks_for(m * ns), 8 * ctx->num_sms));
@@ -1149,12 +1154,13 @@ oid_status grad_ogo(oid_ctx ctx, cudaStream_t st) {
   return OID_OK;
 }
 
-// [S_J; c S^1_J; c S^2_J] (3l x t) into L.gLst
+// [S_J; c S^1_J; ..; c S^d_J] ((d+1) l x t) into L.gLst
 oid_status grad_stack_j(oid_ctx ctx, cudaStream_t st, double c) {
   const Layout& L = ctx->L;
   const int ell = ctx->p.ell, t = ctx->t;
-  stack3_kernel<<<blocks_for(int64_t(3) * ell * t), 256, 0, st>>>(ctx->d(L.S), ctx->d(L.S1), ctx->d(L.S2), ell, t,
-                                                                   ctx->ptr<int64_t>(L.J), c, ctx->d(L.gLst));
+  stack_aug_kernel<<<blocks_for(int64_t(ctx->ga) * ell * t), 256, 0, st>>>(
+      ctx->d(L.S), ctx->d(L.Sg), static_cast<int64_t>(ell) * ctx->p.n_cap, ctx->ga, ell, t, ctx->ptr<int64_t>(L.J), c,
+      ctx->d(L.gLst));
   CKL();
   return OID_OK;
 }
@@ -1162,27 +1168,25 @@ oid_status grad_stack_j(oid_ctx ctx, cudaStream_t st, double c) {
 // sketched GCV(mu) of eq:GCV_COmega -> L.gscal[0]
 oid_status grad_gcv(oid_ctx ctx, cudaStream_t st, double mu) {
   const Layout& L = ctx->L;
-  const int ell = ctx->p.ell, t = ctx->t, n = static_cast<int>(ctx->n_obs), l3 = 3 * ell;
+  const int ell = ctx->p.ell, t = ctx->t, n = static_cast<int>(ctx->n_obs), l3 = ctx->ga * ell, gd = ctx->ga - 1;
   oid_status s = grad_ogo(ctx, st);
   if (s != OID_OK) return s;
   s = grad_stack_j(ctx, st, 1.0);
   if (s != OID_OK) return s;
-  const double* SJ = ctx->d(L.gLst);              // rows 0..l-1 of the stack (ld 3l)
-  const double* S1J = SJ + ell;
-  const double* S2J = SJ + 2 * ell;
-  // H = S_J^T S_J + mu (S^1_J^T S^1_J + S^2_J^T S^2_J)      (t x t)
+  const double* SJ = ctx->d(L.gLst);              // rows 0..l-1 of the stack (ld (d+1) l); S^p_J at SJ + p l
+  // H = S_J^T S_J + mu sum_p S^p_J^T S^p_J      (t x t)
   s = gemm(ctx, st, true, false, t, t, ell, 1.0, SJ, l3, SJ, l3, 0.0, ctx->d(L.gH), t);
   if (s != OID_OK) return s;
-  s = gemm(ctx, st, true, false, t, t, ell, mu, S1J, l3, S1J, l3, 1.0, ctx->d(L.gH), t);
-  if (s != OID_OK) return s;
-  s = gemm(ctx, st, true, false, t, t, ell, mu, S2J, l3, S2J, l3, 1.0, ctx->d(L.gH), t);
-  if (s != OID_OK) return s;
-  // R = S_J + mu ((Omega G^1 Omega^T)^T S^1_J + (Omega G^2 Omega^T)^T S^2_J)   (l x t)
-  s = gemm(ctx, st, true, false, ell, t, ell, mu, ctx->d(L.OGO), ell, S1J, l3, 0.0, ctx->d(L.gR), ell);
-  if (s != OID_OK) return s;
-  s = gemm(ctx, st, true, false, ell, t, ell, mu, ctx->d(L.OGO) + static_cast<size_t>(ell) * ell, ell, S2J, l3, 1.0,
-           ctx->d(L.gR), ell);
-  if (s != OID_OK) return s;
+  for (int q = 1; q <= gd; ++q) {
+    s = gemm(ctx, st, true, false, t, t, ell, mu, SJ + q * ell, l3, SJ + q * ell, l3, 1.0, ctx->d(L.gH), t);
+    if (s != OID_OK) return s;
+  }
+  // R = S_J + mu sum_p (Omega G^p Omega^T)^T S^p_J   (l x t)
+  for (int q = 1; q <= gd; ++q) {
+    s = gemm(ctx, st, true, false, ell, t, ell, mu, ctx->d(L.OGO) + static_cast<size_t>(q - 1) * ell * ell, ell,
+             SJ + q * ell, l3, q == 1 ? 0.0 : 1.0, ctx->d(L.gR), ell);
+    if (s != OID_OK) return s;
+  }
   add_strided_kernel<<<blocks_for(int64_t(ell) * t), 256, 0, st>>>(SJ, l3, ell, t, ctx->d(L.gR), ell);
   CKL();
   // H^+ by the one-sided Jacobi SVD (R9 cutoff)
@@ -1208,7 +1212,7 @@ oid_status grad_gcv(oid_ctx ctx, cudaStream_t st, double mu) {
 // P(mu) of eq:opt_grad_fullsketch: [S_J; sqrt(mu) S^p_J]^+ [S; sqrt(mu) S^p]  (t x n, ld t)
 oid_status grad_coefficients(oid_ctx ctx, cudaStream_t st, double mu, double* P) {
   const Layout& L = ctx->L;
-  const int ell = ctx->p.ell, t = ctx->t, n = static_cast<int>(ctx->n_obs), l3 = 3 * ell;
+  const int ell = ctx->p.ell, t = ctx->t, n = static_cast<int>(ctx->n_obs), l3 = ctx->ga * ell;
   const double c = std::sqrt(mu);
   oid_status s = grad_stack_j(ctx, st, c);
   if (s != OID_OK) return s;
@@ -1217,8 +1221,9 @@ oid_status grad_coefficients(oid_ctx ctx, cudaStream_t st, double mu, double* P)
   s = pinv_assemble(ctx, st, ctx->d(L.gLst), l3, t, ctx->d(L.gLV), ctx->d(L.gLs), ctx->d(L.gLw), ctx->d(L.gLZ),
                     ctx->d(L.gLp), nullptr, 0);
   if (s != OID_OK) return s;
-  stack3_kernel<<<blocks_for(int64_t(l3) * n), 256, 0, st>>>(ctx->d(L.S), ctx->d(L.S1), ctx->d(L.S2), ell, n, nullptr, c,
-                                                             ctx->d(L.gRhs));
+  stack_aug_kernel<<<blocks_for(int64_t(l3) * n), 256, 0, st>>>(ctx->d(L.S), ctx->d(L.Sg),
+                                                                 static_cast<int64_t>(ell) * ctx->p.n_cap, ctx->ga, ell, n,
+                                                                 nullptr, c, ctx->d(L.gRhs));
   CKL();
   return gemm(ctx, st, false, false, t, n, l3, 1.0, ctx->d(L.gLp), t, ctx->d(L.gRhs), l3, 0.0, P, t);
 }
@@ -1261,12 +1266,16 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
   ctx->m_loc = m_local(*p);
   ctx->t = p->k;
   if (p->grad_nfields > 0) {
-    ctx->ga = 3;
+    const bool d3 = p->grad_nz > 1;   // NEXT-4: three gradient components on a 3-D grid
+    ctx->ga = d3 ? 4 : 3;
     ctx->grid.nf = p->grad_nfields;
     ctx->grid.nx = p->grad_nx;
     ctx->grid.ny = p->grad_ny;
+    ctx->grid.nz = d3 ? p->grad_nz : 1;
+    ctx->grid.d = d3 ? 3 : 2;
     ctx->grid.hx = p->grad_hx > 0.0 ? p->grad_hx : (p->grad_nx > 1 ? 1.0 / (p->grad_nx - 1) : 1.0);
     ctx->grid.hy = p->grad_hy > 0.0 ? p->grad_hy : (p->grad_ny > 1 ? 1.0 / (p->grad_ny - 1) : 1.0);
+    ctx->grid.hz = p->grad_hz > 0.0 ? p->grad_hz : (p->grad_nz > 1 ? 1.0 / (p->grad_nz - 1) : 1.0);
   }
   const int ng = ctx->ga * p->ell;
   ctx->key0 = static_cast<uint32_t>(p->seed & 0xffffffffu);

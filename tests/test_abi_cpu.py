@@ -66,8 +66,9 @@ def test_workspace_query_validates(oid):
 
 def test_struct_layout_matches_header(oid):
     # oid_params: 4 int64 + 6 int32 + 4 double + uint64 + 4 int32 = 32 + 24 + 32 + 8 + 16 = 112 bytes,
-    # then the gradient-variant block: 4 int32 + 2 double = 32 bytes, then coeff_mode + epoch_mode
-    assert ctypes.sizeof(oid.OidParams) == 152
+    # then the gradient-variant block: 4 int32 + 2 double = 32 bytes, then coeff_mode + epoch_mode,
+    # then grad_nz + reserved1 + grad_hz (3-D gradients)
+    assert ctypes.sizeof(oid.OidParams) == 168
     assert oid.OidParams.grad_nfields.offset == 112 and oid.OidParams.grad_hx.offset == 128
     assert oid.OidParams.coeff_mode.offset == 144
     # oid_stats_t: 4 int64 + 3 double + uint32 + int32, then a9_ms, 4 int64, 3 double

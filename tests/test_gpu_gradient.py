@@ -125,3 +125,59 @@ def test_gradient_variant_c4r_parity(oid):
         Pr = o.coefficients(mu)
         R, Rr = o.C @ P, o.C @ Pr
         assert np.linalg.norm(R - Rr) <= 1e-5 * np.linalg.norm(Rr), (mu, np.linalg.norm(R - Rr) / np.linalg.norm(Rr))
+
+
+@pytest.mark.parametrize("case", ["smooth", "channel"])
+def test_gradient_variant_3d_parity(oid, case):
+    """NEXT-4: three gradient components on a 3-D grid, augmented sketch of 4 l rows.
+    "smooth": 3 smooth fields on 12 x 10 x 8; "channel": the C3 channel-flow generator on a
+    12 x 9 x 12 grid (components u, v, w; grid axes (z, y, x) -> (i, j, l), the stencil with
+    uniform steps).  J every epoch, the 4l x 4l Gram, GCV and the reconstruction A_J P(mu) against
+    the oracle with the 3-D operators."""
+    from oracle.gradient import grid_gradient_operators_3d
+    if case == "smooth":
+        nf, nx, ny, nz, k, ell, b = 3, 12, 10, 8, 10, 48, 16
+        rng = np.random.default_rng(21)
+        i, j, l = np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij")
+        x, y, z = (i / (nx - 1)).ravel(), (j / (ny - 1)).ravel(), (l / (nz - 1)).ravel()
+        cols = []
+        for s in range(4 * b):
+            f = []
+            for fi in range(nf):
+                a, bb, c = rng.standard_normal(3)
+                f.append(np.sin((2 + fi) * x + a + 0.05 * s) * np.cos(3 * y + bb) * np.cos(2 * z + c)
+                         + 1e-3 * rng.standard_normal(x.size))
+            cols.append(np.concatenate(f))
+        A = np.stack(cols, axis=1)
+    else:
+        from synth import ChannelFlow
+        Nx, Ny, Nz = 12, 9, 12
+        nf, nx, ny, nz, k, ell, b = 3, Nz, Ny, Nx, 10, 48, 16
+        A = ChannelFlow(Nx, Ny, Nz, seed=1003).block(0, 4 * b)
+    m, n = A.shape
+    split = (ell // 6, ell // 3, ell - ell // 6 - ell // 3)
+    p = oid.make_params(m=m, k=k, ell=ell, b_max=b, n_cap=n, lam=-1.0, split=split, seed=6, grad3=(nf, nx, ny, nz))
+    eng = oid.Engine(p)
+    o = OracleGradOID(OracleParams(m=m, k=k, ell=ell, ell1=split[0], ell2=split[1], ell3=split[2], lam=-1.0, seed=6),
+                      grid_gradient_operators_3d(nf, nx, ny, nz))
+    Ad = torch.from_numpy(np.asfortranarray(A)).to("cuda:0")
+    low = None
+    for e, j in enumerate(range(0, n, b)):
+        eng.ingest_block(Ad[:, j:j + b])
+        lg = o.ingest_block(A[:, j:j + b])
+        if low is None and any(d[5] < 1e-6 for d in lg.decisions):
+            low = e
+        if low is None:
+            assert np.array_equal(eng.J(), o.J), (e, eng.J(), o.J)
+    G = eng.get(3)
+    assert G.shape == (4 * ell, 4 * ell)
+    assert np.linalg.norm(G - o.gram) <= 1e-10 * np.linalg.norm(o.gram)
+    if low is not None:
+        pytest.skip(f"decision margin < 1e-6 at epoch {low}")
+    OGO = o.omega_g_omega()
+    for mu in (1e-2, 1.0):
+        g_gpu, g_ref = eng.gradient_gcv(mu), o.gcv(mu, OGO)
+        assert abs(g_gpu - g_ref) <= 1e-6 * abs(g_ref), (mu, g_gpu, g_ref)
+        P = eng.gradient_coefficients(mu).cpu().numpy()
+        R, Rr = o.C @ P, o.C @ o.coefficients(mu)
+        assert np.linalg.norm(R - Rr) <= 1e-6 * np.linalg.norm(Rr), mu

@@ -131,3 +131,30 @@ def test_gradient_variant_end_to_end_small():
     def grad_err(PP):
         return sum(np.linalg.norm(G @ (AJ @ PP[occ]) - G @ A) for G in Gs)
     assert grad_err(P) <= grad_err(P0) * (1 + 1e-9)
+
+
+def test_3d_gradient_operators_exact_on_linear_fields():
+    """NEXT-4: the 3-D simplex gradients of a linear field a x + b y + c z are exact at every node
+    (interior central differences, one-sided at faces, edges and corners), per field, and every
+    row sums to zero."""
+    from oracle.gradient import grid_gradient_operators_3d
+    nf, nx, ny, nz = 2, 5, 4, 3
+    G = grid_gradient_operators_3d(nf, nx, ny, nz)
+    hx, hy, hz = 1 / (nx - 1), 1 / (ny - 1), 1 / (nz - 1)
+    i, j, l = np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij")
+    x, y, z = (i * hx).ravel(), (j * hy).ravel(), (l * hz).ravel()
+    coef = [(0.7, -1.3, 2.1), (-0.2, 0.5, -3.0)]
+    a = np.concatenate([c[0] * x + c[1] * y + c[2] * z + 4.0 for c in coef])
+    for p in range(3):
+        g = G[p] @ a
+        want = np.concatenate([np.full(x.size, c[p]) for c in coef])
+        assert np.allclose(g, want, atol=1e-12)
+        assert np.allclose(np.asarray(G[p].sum(axis=1)).ravel(), 0.0, atol=1e-12)
+    # the 2-D operators are the nz = 1 slice of the same construction
+    from oracle.gradient import grid_gradient_operators
+    G2 = grid_gradient_operators(1, nx, ny)
+    G3 = grid_gradient_operators_3d(1, nx, ny, 2, hz=1.0)
+    b = np.random.default_rng(0).standard_normal(nx * ny)
+    b3 = np.repeat(b, 2)                      # constant along z: l = 0, 1 hold the same values
+    for p in range(2):
+        assert np.allclose((G3[p] @ b3)[::2], G2[p] @ b, atol=1e-12)
