@@ -270,7 +270,7 @@ def main():
     m_loc = re - rb
     W, K, E = args.warmup, args.steps, args.e2e_steps
     nblk = W + K + E
-    n_cap = max(1000, nblk * b)
+    n_cap = max(1000, (nblk + 8) * b)   # + the ingest-only blocks
     # distinct device-resident blocks: the whole stream when it fits (C3: 31 blocks of 3.65 GB),
     # else a ring cycled in order (stated in config.blocks)
     dsz = 8 if dt == "f64" else 4
@@ -356,6 +356,36 @@ def main():
     block_bytes = m * b * dsz                       # all ranks together
     value = K * block_bytes / (ms * 1e-3) / 1e9
     est_val = est_out.cpu().tolist()
+
+    # ingest GB/s alone (K1 -> AR1 -> K2-K7, no estimate), on the next blocks of
+    # the stream after the timed region (reported beside the step metric, not instead of it)
+    ingest_only = None
+    KI = min(8, K)
+    if not args.no_estimate and KI > 0:
+        torch.cuda.synchronize()
+        if sharded:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        with torch.cuda.stream(stream):
+            for s in range(W + K, W + K + KI):
+                X = blocks[s % ring]
+                if flush is not None:
+                    flush.fill_(1)
+                if sharded:
+                    drv.ingest(X)
+                else:
+                    eng.ingest_block(X)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ims = e0.elapsed_time(e1)
+        if sharded:
+            t = torch.tensor([ims], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ims = t.item()
+        ingest_only = {"ms_per_block": ims / KI, "value": KI * block_bytes / (ims * 1e-3) / 1e9, "unit": "GB/s",
+                       "blocks": KI, "definition": "SURVEY 8(d) D(1): ingest_block only (no estimate), the "
+                                                   f"{KI} blocks after the timed region"}
 
     # roofline of the dominant kernel (K1, fused ingest) on this rank, as SURVEY.md section 8(d)
     # defines it: t_roof = max(HBM read of the block, 2 l m b sketch flops at the chosen pipe's peak),
@@ -496,6 +526,7 @@ def main():
             "clocks": clocks,
             "gpu_launches": st["launches"],
             "breakdown_ms_per_step": {"k1": st["k1_ms"] / K, "post": st["post_ms"] / K, "estimate": st["est_ms"] / K},
+            "ingest_only": ingest_only,
             "last_estimate": {"est_rel": est_val[5], "e2": est_val[0], "flags": int(est_val[6])},
             "k1_mode": "tc_int8" if mode == oid.K1_TC_INT8 else "simt_f64",
         }
