@@ -48,15 +48,22 @@ typedef enum {
 
 typedef enum { OID_F32 = 0, OID_F64 = 1 } oid_dtype;
 
-/* K1 (fused ingest) implementation.  Both are exact to fp64 rounding. */
+/* K1 (fused ingest) implementation.  Modes 0-3 are exact to fp64 rounding. */
 typedef enum {
   OID_K1_AUTO = 0,      /* tensor-core path when available for the shape, else SIMT       */
   OID_K1_SIMT_F64 = 1,  /* CUDA-core DFMA, Omega generated in registers                    */
   OID_K1_TC_INT8 = 2,   /* tcgen05 kind::i8, Omega generated into TMEM (A operand), data
                            split into exact int8 digit planes in shared memory (sm_100a);
                            needs row_begin % 32 == 0, 16-byte aligned X and ld            */
-  OID_K1_TC_PAIR = 3    /* experimental: 2-CTA (cta_group::2) variant of OID_K1_TC_INT8 with
+  OID_K1_TC_PAIR = 3,   /* experimental: 2-CTA (cta_group::2) variant of OID_K1_TC_INT8 with
                            48-bit digit planes converted by integer arithmetic            */
+  OID_K1_TC_FAST = 4    /* K1F: tcgen05 kind::i8 with the data quantised to a 31-bit per-column
+                           fixed point (4 signed digit planes stacked in M, Omega^T generated
+                           into shared memory as the B operand, each X element converted once
+                           for ell <= 512).  Not exact: |x - x_q| <= 2^-26 max_i |x_ij| per
+                           element, within north_star's 1e-5 tolerance.
+                           Used for the snapshot blocks; the gradient passes stay exact.  Same
+                           alignment needs as OID_K1_TC_INT8, else the exact kernels run.  */
 } oid_k1_mode;
 
 /* flag bits (oid_stats.flags, estimate out[6]) */

@@ -25,7 +25,7 @@ OID_OK, OID_EINVAL, OID_ESHAPE, OID_ENOMEM, OID_ECUDA, OID_ENCCL, OID_ENUMERIC, 
 _STATUS = {0: "OID_OK", -1: "OID_EINVAL", -2: "OID_ESHAPE", -3: "OID_ENOMEM", -4: "OID_ECUDA", -5: "OID_ENCCL",
            -6: "OID_ENUMERIC", -7: "OID_ESTATE"}
 OID_F32, OID_F64 = 0, 1
-K1_AUTO, K1_SIMT_F64, K1_TC_INT8, K1_TC_PAIR = 0, 1, 2, 3
+K1_AUTO, K1_SIMT_F64, K1_TC_INT8, K1_TC_PAIR, K1_TC_FAST = 0, 1, 2, 3, 4
 FLAG_NONFINITE_INPUT, FLAG_SJ_RANK_DEFICIENT, FLAG_E2_NEGATIVE, FLAG_K1_RECOMPUTED = 1, 2, 4, 8
 
 EXPORTED = ["oid_workspace_query", "oid_init", "oid_ingest_block", "oid_ingest_sketch", "oid_ingest_commit",

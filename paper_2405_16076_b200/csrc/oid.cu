@@ -23,6 +23,7 @@
 #include "k1_simt.cuh"
 #include "k1_tc.cuh"
 #include "k1_pair.cuh"
+#include "k1_fast.cuh"
 #include "coeff.cuh"
 #include "gram_tc.cuh"
 #include "grad.cuh"
@@ -121,7 +122,7 @@ struct Bump {
 struct Layout {
   size_t S, gram, Ypart, k1part, k1npart, gB, gV, mu, mu_sorted, Yc, Tsc, tau, scal, J, tau_old, admit, counts,
       flags, counters, C, SJ, sjB, sjV, sjsig, sjw, sjZ, Sjpinv, Pexp, AJP, G, Gsum, Gpart, cB, cV, csig, cw, cZ, M,
-      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, wyT, sjG, cG, cBt, cZ2, dbg, Jsnap, Dsnap, gcnt, Sg, YpG, GX, OGO, gH, gHV, gHs, gHw, gHZ, gHp, gR, gCm, gE, gLst, gLV, gLs, gLw, gLZ, gLp, gRhs, gscal, td2, te2, Vh2, tauv2, wyT2, ldl2, mu2, cum, elog, eslog, omega, trA, trW, Pcand, Pchosen, Pext, Rres, Gprev, gpH, gpV, gpMu, gpW, Gpinv, Xc, Dx, Dxp, Tm, cest, est_ch, est4, qlog, Jprev, olds, nold, qsel, Dpool, Dnorm, total;
+      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, k1g, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, wyT, sjG, cG, cBt, cZ2, dbg, Jsnap, Dsnap, gcnt, Sg, YpG, GX, OGO, gH, gHV, gHs, gHw, gHZ, gHp, gR, gCm, gE, gLst, gLV, gLs, gLw, gLZ, gLp, gRhs, gscal, td2, te2, Vh2, tauv2, wyT2, ldl2, mu2, cum, elog, eslog, omega, trA, trW, Pcand, Pchosen, Pext, Rres, Gprev, gpH, gpV, gpMu, gpW, Gpinv, Xc, Dx, Dxp, Tm, cest, est_ch, est4, qlog, Jprev, olds, nold, qsel, Dpool, Dnorm, total;
 };
 
 int64_t m_local(const oid_params& p) { return p.row_end - p.row_begin; }
@@ -295,8 +296,10 @@ Layout make_layout(const oid_params& p) {
     const int64_t ng = (p.row_end + 31) / 32 - p.row_begin / 32 + 1;
     L.omega = b.take(static_cast<size_t>(ng) * ell * 16);
   }
-  L.tc = b.take(std::max(k1tc_workspace_bytes(p.ell, p.b_max, m_local(p), p.dtype == OID_F64),
-                         k1p_workspace_bytes(p.ell, p.b_max, m_local(p), p.dtype == OID_F64)));
+  L.tc = b.take(std::max(std::max(k1tc_workspace_bytes(p.ell, p.b_max, m_local(p), p.dtype == OID_F64),
+                                  k1p_workspace_bytes(p.ell, p.b_max, m_local(p), p.dtype == OID_F64)),
+                         k1f_workspace_bytes()));
+  L.k1g = b.take(static_cast<size_t>(k1f::kMaxUnits) * 32 * sizeof(int));   // K1F exponent guesses
   L.total = b.off;
   return L;
 }
@@ -316,7 +319,7 @@ const char* validate(const oid_params* p) {
   if (!(p->lambda >= 0.0 || p->lambda == -1.0 || p->lambda == -2.0)) return "lambda must be >= 0, -1 or -2";
   if (!(p->eps > 0.0) || !(p->delta > 0.0 && p->delta < 1.0) || !(p->c > 0.0)) return "need eps > 0, 0 < delta < 1, c > 0";
   if (p->dtype != OID_F32 && p->dtype != OID_F64) return "dtype must be OID_F32 or OID_F64";
-  if (p->k1_mode < 0 || p->k1_mode > 3) return "bad k1_mode";
+  if (p->k1_mode < 0 || p->k1_mode > 4) return "bad k1_mode";
   if (p->m / 32 >= (int64_t(1) << 32)) return "m too large for the 32-bit Philox row counter";
   if (p->grad_nfields < 0) return "grad_nfields must be >= 0";
   if (p->omega_cache != 0 && p->omega_cache != 1) return "omega_cache must be 0 or 1";
@@ -672,10 +675,11 @@ oid_status launch_k1_simt(oid_ctx ctx, cudaStream_t st, const T* X, int64_t ld, 
 
 // K1 on one block (X of dtype f64 / f32) into out = [Y (ell x nc); n (nc)]
 oid_status sketch_one(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_t st, double* out, bool f64,
-                      bool strict_mode) {
+                      bool strict_mode, bool main_x = false) {
   const oid_params& p = ctx->p;
   const bool want_pair = p.k1_mode == OID_K1_TC_PAIR;
-  const bool want_tc = (p.k1_mode == OID_K1_TC_INT8) || want_pair || (p.k1_mode == OID_K1_AUTO && ctx->tc_ok);
+  const bool want_tc = (p.k1_mode == OID_K1_TC_INT8) || want_pair || p.k1_mode == OID_K1_TC_FAST ||
+                       (p.k1_mode == OID_K1_AUTO && ctx->tc_ok);
   K1TcArgs a{};
   a.X = X; a.ld = ld; a.ncols = nc; a.row_begin = p.row_begin; a.row_end = p.row_end; a.ell = p.ell;
   a.key0 = ctx->key0; a.key1 = ctx->key1; a.scale = ctx->qscale; a.f64 = f64;
@@ -687,6 +691,23 @@ oid_status sketch_one(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream
   a.num_sms = std::max(2, ctx->num_sms - ctx->k1_free_sms);
   a.dbg = ctx->k1_debug ? ctx->ptr<long long>(ctx->L.dbg) : nullptr;
   a.omega = (p.omega_cache == 1 && strict_mode) ? reinterpret_cast<const uint4*>(ctx->ws + ctx->L.omega) : nullptr;
+  // K1F (OID_K1_TC_FAST): the snapshot blocks themselves (its exponent guesses follow one data
+  // stream); the gradient / Omega G Omega^T passes keep the exact kernel
+  if (p.k1_mode == OID_K1_TC_FAST && main_x && ctx->tc_ok && k1f_call_ok(a)) {
+    int nl = 0;
+    cudaError_t e;
+    {
+      EvScope ev(ctx, st, &ctx->ev_k1);
+      tl_mark(ctx, st, 1);
+      e = k1f_launch(a, ctx->ptr<int>(ctx->L.k1g), st, &nl);
+      tl_mark(ctx, st, 2);
+    }
+    ctx->launches += nl;
+    ctx->k1_launches += 1;
+    if (e != cudaSuccess) return ctx->fail(OID_ECUDA, "k1 fast: %s", cudaGetErrorString(e));
+    ctx->k1_mode_used = OID_K1_TC_FAST;
+    return OID_OK;
+  }
   const bool tc_call = want_tc && ctx->tc_ok && (want_pair ? k1p_call_ok(a) : k1tc_call_ok(a));
   if (strict_mode && (p.k1_mode == OID_K1_TC_INT8 || want_pair) && !tc_call)
     return ctx->fail(OID_EINVAL, "tensor-core K1 unavailable for this device/shape/alignment");
@@ -712,7 +733,7 @@ oid_status sketch_one(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream
 oid_status do_sketch(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_t st) {
   const oid_params& p = ctx->p;
   const Layout& L = ctx->L;
-  oid_status s = sketch_one(ctx, X, ld, nc, st, ctx->d(L.Ypart), p.dtype == OID_F64, true);
+  oid_status s = sketch_one(ctx, X, ld, nc, st, ctx->d(L.Ypart), p.dtype == OID_F64, true, true);
   if (s != OID_OK || ctx->ga == 1) return s;
   // gradient variant (A11): G^p X by the axis-neighbour stencils, then K1 on each
   // (same Omega, so the three sketches stack into [Omega a; Omega G^1 a; Omega G^2 a])
@@ -1443,6 +1464,9 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
   if ((e = cudaMemsetAsync(ctx->ws + L.elog, 0, sizeof(double) * kElogCols * p->n_cap, st)) != cudaSuccess) return bad(e);
   if ((e = cudaMemsetAsync(ctx->ws + L.eslog, 0, sizeof(double) * kElogCols * p->n_cap, st)) != cudaSuccess) return bad(e);
   if ((e = cudaMemsetAsync(ctx->ws + L.gcnt, 0, 8 * sizeof(int), st)) != cudaSuccess) return bad(e);
+  k1f::fill_int_kernel<<<(k1f::kMaxUnits * 32 + 255) / 256, 256, 0, st>>>(ctx->ptr<int>(L.k1g), k1f::kMaxUnits * 32,
+                                                                        k1f::kNoGuess);
+  if ((e = cudaGetLastError()) != cudaSuccess) return bad(e);
   {
     const int64_t RL = 128 / static_cast<int64_t>(dsize(*p));
     const size_t cb = static_cast<size_t>((ctx->m_loc + RL - 1) / RL * RL) * ctx->t * dsize(*p);

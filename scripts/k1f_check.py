@@ -1,0 +1,103 @@
+"""K1F (OID_K1_TC_FAST) against the exact tensor-core K1 (OID_K1_TC_INT8) on the same blocks:
+error of the partial sketch [Y; n] relative to the per-element quantisation bound, plus timing."""
+import argparse, os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+from __graft_entry__ import build
+build()
+import paper_2405_16076_b200 as oid
+from synth import ChannelFlow
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--full", action="store_true", help="C3 full size timing")
+a = ap.parse_args()
+dev = torch.device("cuda", 0)
+
+
+def partials(X, ell, mode, dtype, reps=1, scales=(1.0,)):
+    m, b = X.shape
+    p = oid.make_params(m=m, k=min(ell, 8), ell=ell, b_max=64, n_cap=64 * 64, lam=-1.0, seed=5, profile=True,
+                        dtype=dtype, k1_mode=mode)
+    eng = oid.Engine(p)
+    outs = []
+    for sc in scales:
+        Xs = (X.T * sc).contiguous().T if sc != 1.0 else X
+        for _ in range(reps):
+            eng.ingest_sketch(Xs)
+        torch.cuda.synchronize()
+        outs.append(eng.partials(0)[: (ell + 1) * b].clone().cpu().numpy())
+    st = eng.stats()
+    eng.close()
+    return outs, st
+
+
+def check(m, b, ell, dtype="f64", seed=0, scales=(1.0,), kind="gauss"):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    if kind == "gauss":
+        Xh = torch.randn(b, m, generator=g, dtype=torch.float64)
+        Xh *= torch.logspace(-3, 3, b, dtype=torch.float64)[:, None]       # column scales 1e-3 .. 1e3
+    else:
+        t = torch.linspace(0, 1, m, dtype=torch.float64)
+        Xh = torch.stack([torch.sin(7 * t * (i + 1)) * (1 + 1e3 * t) for i in range(b)])  # growing magnitude
+    X = Xh.to(tdt).to(dev).T          # (m, b) column-major
+    ex, _ = partials(X, ell, oid.K1_TC_INT8, dtype, scales=scales)
+    fa, st = partials(X, ell, oid.K1_TC_FAST, dtype, scales=scales)
+    res = []
+    for e, f, sc in zip(ex, fa, scales):
+        Y = e[: ell * b].reshape(b, ell).T
+        Yf = f[: ell * b].reshape(b, ell).T
+        n, nf = e[ell * b:], f[ell * b:]
+        colmax = (X.abs().amax(0).double() * sc).cpu().numpy()
+        # per-element quantisation error <= 2^-26 colmax; |dY_rj| <= s sum_i |L_ri| 2^-26 colmax_j
+        # (s sum |L_ri| ~ m E|Z| = 0.8 m); the RMS expectation is ~ sqrt(m) 2^-29 colmax
+        dY = np.abs(Y - Yf)
+        bound = 0.8 * m * 2.0 ** -26 * colmax[None, :]
+        ratio = (dY / bound).max()
+        rms = np.sqrt((dY ** 2).mean(0)) / (np.sqrt(m) * colmax)
+        relY = np.linalg.norm(Y - Yf) / np.linalg.norm(Y)
+        reln = np.abs(n - nf).max() / np.abs(n).max()
+        res.append((sc, ratio, rms.max(), relY, reln))
+    print(f"m={m} b={b} ell={ell} {dtype} {kind} mode_used={st['k1_mode_used']}: " +
+          "; ".join(f"x{sc:g}: max/bound {r:.2e} rms/(sqrt(m)max) {q:.2e} relY {y:.2e} reln {nn:.2e}"
+                    for sc, r, q, y, nn in res), flush=True)
+    return res
+
+
+ok = True
+for (m, b, ell, dt) in [(4096, 16, 48, "f64"), (5000, 32, 256, "f64"), (33000, 32, 512, "f64"), (33000, 17, 100, "f64"),
+                        (70000, 64, 640, "f64"), (20000, 64, 1024, "f32"), (5120, 64, 256, "f32"), (100000, 32, 512, "f64")]:
+    r = check(m, b, ell, dt)
+    ok &= all(x[1] < 1.0 for x in r)
+r = check(200000, 32, 512, "f64", kind="ramp")
+ok &= all(x[1] < 1.0 for x in r)
+r = check(300000, 32, 512, "f64", scales=(1.0, 1.0, 1024.0, 1.0 / 4096, 3.0))
+ok &= all(x[1] < 1.0 for x in r)
+print("BOUND_OK" if ok else "BOUND_FAIL", flush=True)
+
+if a.full:
+    gen = ChannelFlow(192, 129, 192, seed=1003)
+    X = gen.block_torch(0, 32, dev).T
+    for mode in (oid.K1_TC_INT8, oid.K1_TC_FAST):
+        p = oid.make_params(m=gen.m, k=200, ell=512, b_max=32, n_cap=64 * 32, lam=-1.0, seed=0, profile=True,
+                            dtype="f64", k1_mode=mode)
+        eng = oid.Engine(p)
+        eng.ingest_sketch(X)
+        torch.cuda.synchronize()
+        eng.stats_reset()
+        for r in range(a.reps):
+            eng.ingest_sketch(X)
+        torch.cuda.synchronize()
+        st = eng.stats()
+        ms = st['k1_ms'] / st['k1_launches']
+        print(f"C3 mode {mode} (used {st['k1_mode_used']}): K1 {ms:.3f} ms/launch, "
+              f"{gen.m * 32 * 8 / (ms * 1e-3) / 1e9:.1f} GB/s", flush=True)
+        if mode == oid.K1_TC_FAST:
+            fa = eng.partials(0)[: 513 * 32].clone().cpu().numpy()
+        else:
+            ex = eng.partials(0)[: 513 * 32].clone().cpu().numpy()
+        eng.close()
+    print(f"C3 relY {np.linalg.norm(ex[:512*32]-fa[:512*32])/np.linalg.norm(ex[:512*32]):.3e} "
+          f"reln {np.abs(ex[512*32:]-fa[512*32:]).max()/np.abs(ex[512*32:]).max():.3e}")
