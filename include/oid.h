@@ -237,7 +237,11 @@ oid_status oid_gradient_finalize(oid_ctx ctx, double lo, double hi, double tol, 
           12 tridiagonalisation phase timestamps of the last ingest (4 x 1024 int64 clock64 of
              cluster CTA 0; recorded with OID_K1_DEBUG=1),
           14 coefficient choices (coeff_mode = 1): per epoch [epoch, q*, e2 of Algs 4, 5, 6, 7]
-             (epochs x 6 doubles). */
+             (epochs x 6 doubles),
+          15 K1F exponent state (OID_K1_TC_FAST): 256 units x 32 columns of observed maximum
+             biased exponents (INT_MIN before the first block), then 8 int32 counters summed over
+             launches: [first-tile raises, mid-stream raises (accumulator drains), reruns of a
+             unit after a precision loss, int32-overflow epochs, 0, 0, 0, 0]. */
 oid_status oid_get(oid_ctx ctx, int32_t field, void* host_dst, size_t bytes, void* stream);
 
 /* Counters and CUDA-event timings (synchronizes the context's recorded events).

@@ -280,7 +280,7 @@ class Engine:
                   3: ((ga * ell, ga * ell), np.float64), 4: ((8,), np.float64), 5: ((t + bm,), np.float64),
                   6: ((ga * ell,), np.float64), 7: (((ell + 1) * bm,), np.float64), 8: ((ell, t), np.float64),
                   9: ((3, 48), np.int32), 10: ((12, 4096), np.int64), 11: ((t, t), np.float64), 12: ((1024, 4), np.int64), 13: ((4096, 2), np.float64),
-                  14: ((epochs, 6), np.float64)}
+                  14: ((epochs, 6), np.float64), 15: ((256 * 32 + 8,), np.int32)}
         shape, dt = shapes[field]
         a = np.empty(shape, dtype=dt)
         self._check(_lib.oid_get(self.h, field, ctypes.c_void_p(a.ctypes.data), a.nbytes, self._st()), "oid_get")

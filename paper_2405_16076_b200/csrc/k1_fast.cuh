@@ -11,7 +11,7 @@
 // column's maximum per element, see kH / kShrink) and the final fp64 assembly.
 //
 // Shape of the contraction (B200-first): the four planes of the 32 block columns are stacked into the
-// M = 128 rows of the A operand (row 32 p + j = plane p of column j), so one unit holds up to 512
+// M = 128 rows of the A operand (row 32 (j / 8) + 8 p + j % 8 = plane p of column j), so one unit holds up to 512
 // sketch rows in the 512 TMEM columns (D = 128 lanes x nu columns, two N = 256 MMAs per K step) and
 // every X element is converted ONCE per launch when ell <= 512 (C3) instead of once per 256 sketch
 // rows.  The sketch tile Z^T (nu x 64 rows of int8, K-major) is the B operand, generated straight into
@@ -20,11 +20,12 @@
 //
 // CTA (one per SM, 16 warps, persistent over one unit = contiguous row range x 32 columns x nu
 // sketch rows):
-//   warp 0       TMA producer: 2-D boxes of X (128 B of rows x 32 columns, 128-byte swizzle)
+//   warp 0       TMA producer: one box per tile, every column one contiguous 528-byte line
 //   warp 1       TMEM allocator + single-thread tcgen05.mma issuer (A and B from shared memory)
-//   warps 4-7    digit slicer (warp 4 + p may read TMEM lane quarter p = plane p): 16 rows of one
-//                column per thread and tile; per-column exponent check; the A operand; exact int32
-//                dp4a column sums and norm terms; drains the accumulators at epoch ends
+//   warps 4-7    digit slicer: 16 rows of one column per thread and tile; per-column exponent
+//                check; the A operand (row 32 (j/8) + 8 p + j%8 = plane p of column j); int32 dp4a column
+//                sums and norm terms; drains the accumulators at epoch ends (a warp reads TMEM lane
+//                quarter warp % 4, where the four planes of 8 columns sit in adjacent lanes)
 //   warps 8-15   sketch generator: Philox4x32-10 (rounds 1-2 and half of round 3 factored into a
 //                row part and a group part), Gauss-16 nibbles -> int8 by PRMT, st.shared into B
 // Exponents.  F_j starts from a guess (the unit's observed column maximum of the previous launch,
@@ -50,27 +51,30 @@ using k1tc::smem_u32;
 constexpr int kWarps = 16;
 constexpr int kThreads = 32 * kWarps;
 constexpr int kKT = 64;            // data rows per tile (K of one pipeline stage)
-constexpr int kNSX = 4;            // X stages
-constexpr int kNS = 3;             // A / B stages
-constexpr int kSl0 = 4;            // first slicer warp
-constexpr int kGen0 = 8;           // first generator warp
-constexpr int kGenT = 256;         // generator threads
+constexpr int kNSX = 6;            // X stages (~100 KB of fp64 in flight per SM)
+constexpr int kNSA = 3;            // A stages (digit planes, 8 KB)
+constexpr int kNSB = 3;            // B stages (sketch tile, 256 / 512 rows x 64 bytes)
+constexpr int kSl0 = 4, kSlW = 4;  // slicer warps 4..7 (TMEM lane quarter = warp % 4)
+constexpr int kSlE = kKT / kSlW;   // rows per slicer thread and tile (16)
+constexpr int kGen0 = 8, kGenW = 8;    // generator warps 8..15
 constexpr int kEpochTiles = 2048;  // int32 bound: 2048 * 64 rows * 128 * 111 < 2^31
 constexpr int kH = 1;              // exponent headroom over the guess (bits)
 constexpr int kShrink = 1;         // tolerated excess of the guess over the observed maximum (bits)
 constexpr int kHFirst = 8;         // headroom over the first tile when there is no guess
 constexpr int kNoGuess = INT_MIN;
 constexpr int kMaxUnits = 256;
-constexpr int kScratch = 4 * 32 * 32 * 8;   // drain staging: 4 planes x 32 sketch rows x 32 columns
 
 struct Keys { uint32_t k0[10], k1[10]; };   // Philox key schedule (reading R1)
 
 struct Geom {
   int nu;            // sketch rows per unit (multiple of 16, <= 512)
   int nsg, ncg;      // sketch-row groups, 32-column groups
-  int nranges;
-  int64_t rows_per_range;   // multiple of kKT
-  int x_bytes, b_bytes, smem;
+  int nranges;       // CTAs sharing the tiles of one (column group, sketch group), round-robin
+  int xline, x_bytes, b_bytes, smem;
+  int brows;         // rows of a B stage (256 or 512; rows past nu are generated and ignored)
+  // multipliers passed at run time so that ptxas keeps them as IMAD / IMAD.HI (FMA pipe)
+  // instead of strength-reducing them to ALU shifts (the pipes are balanced by hand)
+  uint32_t k16, k65536, k2p31;
   int nunits() const { return nranges * ncg * nsg; }
 };
 
@@ -82,31 +86,31 @@ inline Geom make_geom(int ell, int ncols, int64_t m_loc, bool f64, int num_sms) 
   const int per_range_units = g.nsg * g.ncg;
   int nr = std::max(1, num_sms / per_range_units);
   const int64_t tiles = (m_loc + kKT - 1) / kKT;
-  nr = static_cast<int>(std::min<int64_t>(nr, tiles));
-  int64_t per = (tiles + nr - 1) / nr * kKT;
-  g.rows_per_range = per;
-  g.nranges = static_cast<int>((m_loc + per - 1) / per);
-  g.x_bytes = kKT * 32 * (f64 ? 8 : 4);
-  g.b_bytes = g.nu * kKT;
-  g.smem = 1024 + kNSX * g.x_bytes + kNS * (128 * kKT) + kNS * g.b_bytes + kScratch;
+  g.nranges = static_cast<int>(std::min<int64_t>(nr, tiles));   // CTAs per (column, sketch) group
+  g.xline = kKT * (f64 ? 8 : 4) + 16;   // one column's tile rows + 16 B pad (conflict-free reads)
+  g.x_bytes = 32 * g.xline;
+  g.brows = g.nu > 256 ? 512 : 256;
+  g.b_bytes = g.brows * kKT;
+  g.k16 = 16; g.k65536 = 65536; g.k2p31 = 0x80000000u;
+  g.smem = 1024 + kNSX * g.x_bytes + kNSA * (128 * kKT) + kNSB * g.b_bytes;
   return g;
 }
 
 struct Shared {
   uint64_t x_full[kNSX], x_empty[kNSX];
-  uint64_t a_full[kNS], a_empty[kNS];
-  uint64_t b_full[kNS], b_empty[kNS];
+  uint64_t a_full[kNSA], a_empty[kNSA];
+  uint64_t b_full[kNSB], b_empty[kNSB];
   uint64_t d_full, d_empty;
   uint32_t tmem_base;
-  int aflag[kNS];
-  int cexp[2][32];        // C_j of the current / next accumulation epoch (a = E - C_j <= 31)
-  int tmx[4][32];         // per slicer warp: tile maximum of E (raise path), then the observed max
-  double cs[4][32], nr[4][32];
+  int aflag[kNSA];
+  int cold[32];           // C_j of the epoch being drained
+  int tmx[kSlW][32];      // per slicer warp: tile maximum of E (raise path), then the observed max
+  double cs[kSlW][32], nr[kSlW][32];
   int redo;
 };
 
-// mad.hi.u32 / mul.lo.u32 with a register operand the compiler cannot see as a constant, so they
-// stay IMAD (FMA pipe) instead of being strength-reduced to shifts (ALU pipe)
+// mad.hi.u32 / mul.lo.u32 / mad.lo.s32 as written (the multiplier comes from a kernel parameter
+// where the FMA pipe is wanted, see Geom)
 __device__ __forceinline__ uint32_t madhi(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t d;
   asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
@@ -126,10 +130,6 @@ __device__ __forceinline__ int mulhi_s(int a, int b) {
   int d;
   asm("mul.hi.s32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
   return d;
-}
-__device__ __forceinline__ uint32_t launder(uint32_t v) {
-  asm volatile("" : "+r"(v));
-  return v;
 }
 __device__ __forceinline__ uint32_t shl_clamp(uint32_t a, uint32_t s) {   // a << s, 0 for s >= 32
   uint32_t d;
@@ -162,9 +162,9 @@ template <> struct Fmt<float> {
   static constexpr int kEmax = 255;
 };
 
-template <typename TD>
+template <typename TD, int NROW>
 __global__ void __launch_bounds__(kThreads, 1)
-k1f_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Keys keys, int64_t row_begin,
+k1f_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, const __grid_constant__ Keys keys, int64_t row_begin,
            int64_t m_loc, Geom g, uint32_t t0, uint32_t t1, double* __restrict__ part, double* __restrict__ npart,
            double* __restrict__ cpart, int* __restrict__ gE, unsigned* __restrict__ flags) {
   extern __shared__ uint8_t smem_raw[];
@@ -176,31 +176,35 @@ k1f_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Key
   const int sg = unit % g.nsg;
   const int cg = (unit / g.nsg) % g.ncg;
   const int range = unit / (g.nsg * g.ncg);
-  const int64_t r0 = static_cast<int64_t>(range) * g.rows_per_range;
-  const int64_t r1 = min(m_loc, r0 + g.rows_per_range);
-  const int ntiles = static_cast<int>((r1 - r0 + kKT - 1) / kKT);
+  // tiles are dealt round-robin (tile gt = range + k nranges): at any moment the whole grid reads
+  // a narrow window of rows of each column (few 2 MB pages, DRAM row locality), instead of 148
+  // distant row ranges x 32 columns
+  const int64_t total_tiles = (m_loc + kKT - 1) / kKT;
+  const int ntiles = static_cast<int>((total_tiles - range + g.nranges - 1) / g.nranges);
   const int nu = g.nu;
   const int nh = nu > 256 ? 2 : 1;                 // N halves of the unit (MMA N <= 256)
+  static_assert(NROW == 1 || NROW == 2, "generator rows per thread");
 
   uint8_t* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-  uint8_t* xbuf = base;                                    // kNSX x x_bytes (1024-aligned)
-  uint8_t* abuf = xbuf + kNSX * g.x_bytes;                 // kNS x 8 KB
-  uint8_t* bbuf = abuf + kNS * 128 * kKT;                  // kNS x b_bytes
-  double* scr = reinterpret_cast<double*>(bbuf + kNS * g.b_bytes);   // drain staging
+  uint8_t* xbuf = base;                                    // kNSX x x_bytes: [column][xline]
+  uint8_t* abuf = xbuf + kNSX * g.x_bytes;                 // kNSA x 8 KB
+  uint8_t* bbuf = abuf + kNSA * 128 * kKT;                 // kNSB x b_bytes
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kNSX; ++s) {
       k1tc::mbar_init(&sh.x_full[s], 1);
-      k1tc::mbar_init(&sh.x_empty[s], 4);
+      k1tc::mbar_init(&sh.x_empty[s], kSlW);
     }
-    for (int s = 0; s < kNS; ++s) {
-      k1tc::mbar_init(&sh.a_full[s], 4);
+    for (int s = 0; s < kNSA; ++s) {
+      k1tc::mbar_init(&sh.a_full[s], kSlW);
       k1tc::mbar_init(&sh.a_empty[s], 1);
-      k1tc::mbar_init(&sh.b_full[s], 8);
+    }
+    for (int s = 0; s < kNSB; ++s) {
+      k1tc::mbar_init(&sh.b_full[s], kGenW);
       k1tc::mbar_init(&sh.b_empty[s], 1);
     }
     k1tc::mbar_init(&sh.d_full, 1);
-    k1tc::mbar_init(&sh.d_empty, 4);
+    k1tc::mbar_init(&sh.d_empty, kSlW);
     sh.redo = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -217,38 +221,38 @@ k1f_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Key
   for (int pass = 0; pass < 2; ++pass) {
     if (warp == 0) {
       // ------------------------------------------------------------ TMA producer
+      // one 2-D box per tile: kKT + pad rows x 32 columns, no swizzle, so every column is one
+      // contiguous line of xline bytes (512-byte lines stream at HBM speed; 128-byte lines cap
+      // near 4.6 TB/s, scripts/micro/xstream.cu).  The pad rows (16 bytes, the next tile's first
+      // rows, hit in L2) offset the lines so the slicer's reads are bank-conflict-free.  Rows past
+      // m_loc and columns past ncols are zero-filled by the TMA unit.
       for (int t = 0; t < ntiles; ++t) {
         const int T = T0 + t, s = T % kNSX;
         if (T >= kNSX) k1tc::mbar_wait(&sh.x_empty[s], ((T / kNSX) - 1) & 1);
         k1tc::mbar_arrive_expect_tx_e(&sh.x_full[s], g.x_bytes);
-        uint8_t* dst = xbuf + s * g.x_bytes;
-        constexpr int kBoxRows = 128 / sizeof(TD);
-#pragma unroll
-        for (int bx = 0; bx < kKT / kBoxRows; ++bx)
-          k1tc::tma_load_2d_e(dst + bx * 4096, &tmap, &sh.x_full[s], static_cast<int>(r0 + int64_t(t) * kKT + bx * kBoxRows),
-                              32 * cg);
+        k1tc::tma_load_2d_e(xbuf + s * g.x_bytes, &tmap, &sh.x_full[s], static_cast<int>((range + int64_t(t) * g.nranges) * kKT),
+                            32 * cg);
       }
     } else if (warp == 1) {
       // ------------------------------------------------------------ MMA issuer
       const uint32_t abase = smem_u32(abuf), bbase = smem_u32(bbuf);
       const uint32_t id0 = k1tc::idesc_i8m(128, nh == 2 ? 256 : nu, true);
       const uint32_t id1 = k1tc::idesc_i8m(128, nh == 2 ? nu - 256 : 16, true);
-      const uint32_t bchunk = static_cast<uint32_t>(nu) * 16;     // bytes per 16-byte K chunk of B
+      const uint32_t bchunk = static_cast<uint32_t>(g.brows) * 16;   // bytes per 16-byte K chunk of B
       bool first = true;
       for (int t = 0; t < ntiles; ++t) {
-        const int T = T0 + t, s = T % kNS;
-        const uint32_t ph = (T / kNS) & 1;
-        k1tc::mbar_wait(&sh.a_full[s], ph);
-        k1tc::mbar_wait(&sh.b_full[s], ph);
+        const int T = T0 + t, sa = T % kNSA, sb = T % kNSB;
+        k1tc::mbar_wait(&sh.a_full[sa], (T / kNSA) & 1);
+        k1tc::mbar_wait(&sh.b_full[sb], (T / kNSB) & 1);
         k1tc::tc_fence_after();
-        if (sh.aflag[s] && t > 0) {        // close the accumulation epoch: drain D first
+        if (sh.aflag[sa] && t > 0) {       // close the accumulation epoch: drain D first
           k1tc::mma_commit_e(&sh.d_full);
           k1tc::mbar_wait(&sh.d_empty, ndrain & 1);
           ++ndrain;
           k1tc::tc_fence_after();
           first = true;
         }
-        const uint32_t a0 = abase + s * (128 * kKT), b0 = bbase + s * g.b_bytes;
+        const uint32_t a0 = abase + sa * (128 * kKT), b0 = bbase + sb * g.b_bytes;
 #pragma unroll
         for (int ks = 0; ks < kKT / 32; ++ks) {
           const uint32_t acc = (first && ks == 0) ? 0u : 1u;
@@ -257,175 +261,186 @@ k1f_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Key
           if (nh == 2) k1tc::mma_i8_ss_e(tmem + 256, ad, k1tc::umma_desc(b0 + ks * 2 * bchunk + 4096, bchunk, 128), id1, acc);
         }
         first = false;
-        k1tc::mma_commit_e(&sh.a_empty[s]);
-        k1tc::mma_commit_e(&sh.b_empty[s]);
+        k1tc::mma_commit_e(&sh.a_empty[sa]);
+        k1tc::mma_commit_e(&sh.b_empty[sb]);
       }
       k1tc::mma_commit_e(&sh.d_full);      // final epoch
       ++ndrain;
-    } else if (warp >= kSl0 && warp < kGen0) {
+    } else if (warp >= kSl0 && warp < kSl0 + kSlW) {
       // ------------------------------------------------------------ digit slicer + drains
-      const int c = warp - kSl0;           // 16-row chunk of the tile = TMEM lane quarter = plane
+      const int sw = warp - kSl0;          // 0 .. kSlW - 1
+      const int rs = sw * kSlE;            // first tile row of this thread (rows rs .. rs + kSlE - 1)
+      const int c = rs >> 4, h = (rs >> 3) & 1;   // K chunk (16 rows) and 8-row half of the rows
       const int j = lane;                  // column within the group
+      const int quarter = warp & 3;        // TMEM lane quarter this warp may read
+      constexpr int kDW = kSlW / 4;        // warps per TMEM lane quarter in a drain
+      const int dpair = sw >> 2;           // which of them (column chunks dealt round-robin)
       constexpr int kBarSl = 1;
+      constexpr int kSlT = 32 * kSlW;
       // exponent guess (first pass) or the observed maximum (second pass)
-      if (c == 0) {
-        int ge = gE[unit * 32 + j];
-        sh.cexp[0][j] = ge;
-      }
-      k1tc::named_bar(kBarSl, 128);
-      int ep = 0;                          // accumulation epoch of this pass
-      int Cj = sh.cexp[0][j];
+      int Cj = gE[unit * 32 + j];
       bool need_first = (Cj == kNoGuess);  // derive from the first tile
       if (!need_first) Cj = Cj - 31 + kH;  // guess = observed max E -> C
       int Cfirst = Cj;                     // C of the first epoch (the precision check)
-      int obs = INT_MIN;                   // observed max E of this thread's elements
+      int obs = 0;                         // observed max E of this thread's elements
       int cs[4] = {0, 0, 0, 0};
       int nq[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};   // digit-pair sums D_pq = sum_i d_p d_q, p <= q
       double csf = 0.0, nrf = 0.0;
       bool first_drain = true;
-      const uint32_t K2048 = launder(2048u), K4096 = launder(4096u), K2p31 = launder(0x80000000u);
-      const uint32_t K512 = launder(512u), K256 = launder(256u), K2 = launder(2u);
+      const uint32_t K2p31 = g.k2p31;
 
       // int32 digit sums of the closing epoch -> fp64, with that epoch's F = kFbase - C
       auto flush = [&](int Cep) {
         const int F = kFbase - Cep;
         const long long csi = static_cast<long long>(cs[0]) + (static_cast<long long>(cs[1]) << 8) +
                               (static_cast<long long>(cs[2]) << 16) + (static_cast<long long>(cs[3]) << 24);
-        {
-          csf += static_cast<double>(csi) * pow2(-F);
-          // ||v||^2 = sum_p,q 256^(p+q) D_pq (exact integers; fp64 sum, largest terms first)
-          double nn = static_cast<double>(nq[0]) * 0x1p48;                                      // (3,3)
-          nn += 2.0 * static_cast<double>(nq[1]) * 0x1p40;                                     // (2,3)
-          nn += static_cast<double>(nq[2]) * 0x1p32 + 2.0 * static_cast<double>(nq[3]) * 0x1p32;  // (2,2) (1,3)
-          nn += 2.0 * static_cast<double>(nq[4]) * 0x1p24 + 2.0 * static_cast<double>(nq[5]) * 0x1p24;  // (1,2) (0,3)
-          nn += static_cast<double>(nq[6]) * 0x1p16 + 2.0 * static_cast<double>(nq[7]) * 0x1p16;  // (1,1) (0,2)
-          nn += 2.0 * static_cast<double>(nq[8]) * 0x1p8 + static_cast<double>(nq[9]);          // (0,1) (0,0)
-          nrf += nn * pow2(-F) * pow2(-F);
-        }
+        csf += static_cast<double>(csi) * pow2(-F);
+        // ||v||^2 = sum_p,q 256^(p+q) D_pq (exact integers; fp64 sum, largest terms first)
+        double nn = static_cast<double>(nq[0]) * 0x1p48;                                      // (3,3)
+        nn += 2.0 * static_cast<double>(nq[1]) * 0x1p40;                                     // (2,3)
+        nn += static_cast<double>(nq[2]) * 0x1p32 + 2.0 * static_cast<double>(nq[3]) * 0x1p32;  // (2,2) (1,3)
+        nn += 2.0 * static_cast<double>(nq[4]) * 0x1p24 + 2.0 * static_cast<double>(nq[5]) * 0x1p24;  // (1,2) (0,3)
+        nn += static_cast<double>(nq[6]) * 0x1p16 + 2.0 * static_cast<double>(nq[7]) * 0x1p16;  // (1,1) (0,2)
+        nn += 2.0 * static_cast<double>(nq[8]) * 0x1p8 + static_cast<double>(nq[9]);          // (0,1) (0,0)
+        nrf += nn * pow2(-F) * pow2(-F);
+#pragma unroll
         for (int p = 0; p < 4; ++p) cs[p] = 0;
+#pragma unroll
         for (int q = 0; q < 10; ++q) nq[q] = 0;
       };
-      // D (TMEM, int32 per plane) of the closing epoch -> fp64 partials part[unit][r][j]
+      // D (TMEM, int32; lane 32 (j / 8) + 8 p + j % 8 = plane p of column j) of the closing epoch -> fp64 partials
+      // part[unit][r][j]: the four planes of a column sit in adjacent lanes of one warp, so they
+      // are combined by two shuffles in a fixed order; column chunks alternate between the two
+      // warps of a lane quarter.  sh.cold holds the epoch's C_j.
       auto drain = [&](int Cep) {
+        if (sw < 1) sh.cold[j] = Cep;
+        k1tc::named_bar(kBarSl, kSlT);
         k1tc::mbar_wait(&sh.d_full, ndrain & 1);
         ++ndrain;
         k1tc::tc_fence_after();
-        const int Fj = kFbase - Cep;
-        const double wgt = (Cep == kNoGuess) ? 0.0 : pow2(8 * c - Fj);
+        const int jd = 8 * quarter + (lane & 7), pd = lane >> 3;
+        const double wgt = pow2(8 * pd - (kFbase - sh.cold[jd]));
         double* dst = part + static_cast<int64_t>(unit) * nu * 32;
-        const int sl = threadIdx.x - 32 * kSl0;   // 0..127
+        const int nchunk = (nu + 31) / 32;
 #pragma unroll 1
-        for (int c0 = 0; c0 < nu; c0 += 32) {
+        for (int k = dpair; k < nchunk; k += kDW) {
+          const int c0 = 32 * k;
           uint32_t v[32];
-          K1F_TMEM_LD32(tmem + (static_cast<uint32_t>(32 * c) << 16) + c0, v);
+          K1F_TMEM_LD32(tmem + (static_cast<uint32_t>(32 * quarter) << 16) + c0, v);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          double out[8];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) scr[(c * 32 + i) * 32 + j] = static_cast<double>(static_cast<int>(v[i])) * wgt;
-          k1tc::named_bar(kBarSl, 128);
+          for (int i = 0; i < 32; ++i) {
+            double x = static_cast<double>(static_cast<int>(v[i])) * wgt;
+            x += __shfl_xor_sync(0xffffffffu, x, 8);
+            x += __shfl_xor_sync(0xffffffffu, x, 16);
+            if ((i >> 3) == pd) out[i & 7] = x;   // lane p keeps rows 8 p .. 8 p + 7 of the chunk
+          }
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int idx = sl + 128 * e;         // (i, jj) = (idx / 32, idx % 32)
-            const int i = idx >> 5, jj = idx & 31;
-            const double sum = ((scr[(3 * 32 + i) * 32 + jj] + scr[(2 * 32 + i) * 32 + jj]) + scr[(1 * 32 + i) * 32 + jj]) +
-                               scr[i * 32 + jj];
-            if (c0 + i < nu) {
-              double* q = dst + static_cast<int64_t>(c0 + i) * 32 + jj;
-              *q = first_drain ? sum : *q + sum;
+          for (int i = 0; i < 8; ++i) {
+            const int r = c0 + 8 * pd + i;
+            if (r < nu) {
+              double* q = dst + static_cast<int64_t>(r) * 32 + jd;
+              *q = first_drain ? out[i] : *q + out[i];
             }
           }
-          k1tc::named_bar(kBarSl, 128);
         }
         first_drain = false;
         k1tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) k1tc::mbar_arrive(&sh.d_empty);
+        k1tc::named_bar(kBarSl, kSlT);     // sh.cold is reused by the next drain
       };
 
 #pragma unroll 1
       for (int t = 0; t < ntiles; ++t) {
         const int T = T0 + t;
-        const int sx = T % kNSX, s = T % kNS;
+        const int sx = T % kNSX, sa = T % kNSA;
         k1tc::mbar_wait(&sh.x_full[sx], (T / kNSX) & 1);
-        uint32_t hi[16], lo[16];
+        uint32_t hi[kSlE], lo[kSlE];
         {
-          const uint8_t* xs = xbuf + sx * g.x_bytes;
+          const uint8_t* ln = xbuf + sx * g.x_bytes + j * g.xline;
           if constexpr (kF64) {
-            const uint8_t* ln = xs + c * 4096 + j * 128;
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const uint4 v = *reinterpret_cast<const uint4*>(ln + ((q ^ (j & 7)) << 4));
+            for (int q = 0; q < kSlE / 2; ++q) {
+              const uint4 v = *reinterpret_cast<const uint4*>(ln + (rs + 2 * q) * 8);
               lo[2 * q] = v.x; hi[2 * q] = v.y; lo[2 * q + 1] = v.z; hi[2 * q + 1] = v.w;
             }
           } else {
-            const uint8_t* ln = xs + (c >> 1) * 4096 + j * 128;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const uint4 v = *reinterpret_cast<const uint4*>(ln + (((4 * (c & 1) + q) ^ (j & 7)) << 4));
+            for (int q = 0; q < kSlE / 4; ++q) {
+              const uint4 v = *reinterpret_cast<const uint4*>(ln + (rs + 4 * q) * 4);
               hi[4 * q] = v.x; hi[4 * q + 1] = v.y; hi[4 * q + 2] = v.z; hi[4 * q + 3] = v.w;
             }
 #pragma unroll
-            for (int e = 0; e < 16; ++e) lo[e] = 0u;
+            for (int e = 0; e < kSlE; ++e) lo[e] = 0u;
           }
         }
-        __syncwarp();
-        if (lane == 0) k1tc::mbar_arrive(&sh.x_empty[sx]);
         // biased exponents E (FMA pipe): e2 = bits << 1 drops the sign, E = e2 >> 21 (f64) / >> 24
-        int Ee[16];
+        int Ee[kSlE];
         int emax = 0;
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const uint32_t e2 = mullo(hi[e], K2);
-          Ee[e] = static_cast<int>(madhi(e2, kF64 ? K2048 : K256, 0u));
+        for (int e = 0; e < kSlE; ++e) {
+          Ee[e] = static_cast<int>((hi[e] << 1) >> (kF64 ? 21 : 24));   // ALU shifts
           emax = max(emax, Ee[e]);
         }
         obs = max(obs, emax);
         if (need_first) {                    // no guess: C from the first tile's maximum + kHFirst
-          sh.tmx[c][j] = emax;
-          k1tc::named_bar(kBarSl, 128);
-          const int em = max(max(sh.tmx[0][j], sh.tmx[1][j]), max(sh.tmx[2][j], sh.tmx[3][j]));
+          sh.tmx[sw][j] = emax;
+          k1tc::named_bar(kBarSl, kSlT);
+          int em = 0;
+#pragma unroll
+          for (int q = 0; q < kSlW; ++q) em = max(em, sh.tmx[q][j]);
           Cj = em - 31 + kHFirst;
           Cfirst = Cj;
           need_first = false;
-          k1tc::named_bar(kBarSl, 128);
+          k1tc::named_bar(kBarSl, kSlT);
         }
         int newep = (t > 0 && (t % kEpochTiles) == 0) ? 1 : 0;
+        if (newep && threadIdx.x == 32 * kSl0) atomicAdd(gE + kMaxUnits * 32 + 3, 1);
         const int Cold = Cj;                 // exponents of the epoch that may close here
-        if (k1tc::named_bar_or(kBarSl, 128, (emax - Cj > 31) ? 1 : 0)) {
+        if (k1tc::named_bar_or(kBarSl, kSlT, (emax - Cj > 31) ? 1 : 0)) {
           // raise: C_j = (tile max E) - 31 + kH for the columns that overflow; a new epoch
-          sh.tmx[c][j] = emax;
-          k1tc::named_bar(kBarSl, 128);
-          const int em = max(max(sh.tmx[0][j], sh.tmx[1][j]), max(sh.tmx[2][j], sh.tmx[3][j]));
-          k1tc::named_bar(kBarSl, 128);
+          sh.tmx[sw][j] = emax;
+          k1tc::named_bar(kBarSl, kSlT);
+          int em = 0;
+#pragma unroll
+          for (int q = 0; q < kSlW; ++q) em = max(em, sh.tmx[q][j]);
+          k1tc::named_bar(kBarSl, kSlT);
           if (em - Cj > 31) Cj = em - 31 + kH;
           if (t > 0) newep = 1;
           else Cfirst = Cj;
+          if (threadIdx.x == 32 * kSl0) atomicAdd(gE + kMaxUnits * 32 + (t > 0 ? 1 : 0), 1);
         }
         if (newep) flush(Cold);              // before this tile's digits are added
-        // A stage free?
-        if (T >= kNS) k1tc::mbar_wait(&sh.a_empty[s], ((T / kNS) - 1) & 1);
         // ---- conversion: v = round(|x| 2^F) (31-bit), digits of v sg + 0x808080, 4x4 transposes
-        uint32_t w[16];
+        uint32_t w[kSlE];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
+        for (int e = 0; e < kSlE; ++e) {
           const uint32_t a = static_cast<uint32_t>(Ee[e] - Cj);   // <= 31; negative -> p = 0
           const uint32_t p = shl_clamp(1u, a);                   // 2^(33 - k)
           uint32_t tt;
+          // pipes balanced against the generator (ALU-heavy decode, FMA-heavy Philox): shifts on
+          // the ALU, the variable right shift and the sign on the FMA pipe
           if constexpr (kF64) {
-            const uint32_t h12 = mullo(hi[e], K4096);              // mantissa bits 51..32 at the top
-            const uint32_t b1 = madhi(h12, K2p31, K2p31);          // (h12 >> 1) + implicit bit
-            tt = madhi(lo[e], K2048, b1);                          // + lo >> 21: top 32 mantissa bits
+            // top 32 bits of the 53-bit mantissa: (1 << 31) | (mantissa 51..32 << 11) | (lo >> 21)
+            tt = __funnelshift_r(lo[e], (hi[e] & 0xFFFFFu) | 0x100000u, 21);
           } else {
-            const uint32_t h9 = mullo(hi[e], K512);
-            tt = madhi(h9, K2p31, K2p31);
+            tt = (hi[e] << 8) | 0x80000000u;
           }
           const uint32_t u = madhi(tt, p, 1u);                     // (t >> (k - 1)) + 1
           const int v = static_cast<int>(madhi(u, K2p31, 0u));     // round half up of t / 2^k
-          const int sgn = madlo_s(mulhi_s(static_cast<int>(hi[e]), 2), 2, 1);   // -1 or +1
-          w[e] = static_cast<uint32_t>(madlo_s(v, sgn, 0x808080));
+          const int sgn = static_cast<int>(hi[e]) >> 31;           // 0 or -1
+          w[e] = static_cast<uint32_t>(madlo_s(v, 2 * sgn + 1, 0x808080));
         }
-        uint32_t P[4][4];
+        // the stage is released only once its values have been consumed (the loads' results are
+        // in registers): an arrive right after issuing the loads let the next TMA load overwrite
+        // the first lines before slow loads had read them
+        __syncwarp();
+        if (lane == 0) k1tc::mbar_arrive(&sh.x_empty[sx]);
+        uint32_t P[4][kSlE / 4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < kSlE / 4; ++q) {
           const uint32_t x0 = k1tc::prmt(w[4 * q], w[4 * q + 1], 0x5140), x1 = k1tc::prmt(w[4 * q], w[4 * q + 1], 0x7362);
           const uint32_t y0 = k1tc::prmt(w[4 * q + 2], w[4 * q + 3], 0x5140), y1 = k1tc::prmt(w[4 * q + 2], w[4 * q + 3], 0x7362);
           P[0][q] = k1tc::prmt(x0, y0, 0x5410) ^ 0x80808080u;
@@ -433,19 +448,25 @@ k1f_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Key
           P[2][q] = k1tc::prmt(x1, y1, 0x5410) ^ 0x80808080u;
           P[3][q] = k1tc::prmt(x1, y1, 0x7632);
         }
-        uint8_t* as = abuf + s * (128 * kKT) + c * 2048;
+        // A stage free?
+        if (T >= kNSA) k1tc::mbar_wait(&sh.a_empty[sa], ((T / kNSA) - 1) & 1);
+        // A row 32 (j / 8) + 8 p + j % 8: the 8 lanes of a store phase hit 8 different 16-byte
+        // bank groups, and the four planes of a column share a TMEM lane quarter (lanes l + 8 p)
+        uint8_t* as = abuf + sa * (128 * kKT) + c * 2048 + (j >> 3) * 512 + (j & 7) * 16 + h * 8;
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
-          const int row = 32 * p + j;
-          *reinterpret_cast<uint4*>(as + (row >> 3) * 128 + (row & 7) * 16) = make_uint4(P[p][0], P[p][1], P[p][2], P[p][3]);
+          if constexpr (kSlE == 16)
+            *reinterpret_cast<uint4*>(as + p * 128) = make_uint4(P[p][0], P[p][1], P[p][2], P[p][3]);
+          else
+            *reinterpret_cast<uint2*>(as + p * 128) = make_uint2(P[p][0], P[p][1]);
         }
         k1tc::fence_proxy_async();
-        if (c == 0 && lane == 0) sh.aflag[s] = newep;
+        if (sw == 0 && lane == 0) sh.aflag[sa] = newep;
         __syncwarp();
-        if (lane == 0) k1tc::mbar_arrive(&sh.a_full[s]);
+        if (lane == 0) k1tc::mbar_arrive(&sh.a_full[sa]);
         // exact int32 column sums and norm terms of the digits (dp4a)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < kSlE / 4; ++q) {
 #pragma unroll
           for (int p = 0; p < 4; ++p) cs[p] = __dp4a(static_cast<int>(P[p][q]), 0x01010101, cs[p]);
           nq[0] = __dp4a(static_cast<int>(P[3][q]), static_cast<int>(P[3][q]), nq[0]);
@@ -459,35 +480,36 @@ k1f_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Key
           nq[8] = __dp4a(static_cast<int>(P[0][q]), static_cast<int>(P[1][q]), nq[8]);
           nq[9] = __dp4a(static_cast<int>(P[0][q]), static_cast<int>(P[0][q]), nq[9]);
         }
-        if (newep) {
-          // the MMA issuer commits the closed epoch when it reaches this tile; drain it
-          drain(Cold);
-          ++ep;
-        }
+        if (newep) drain(Cold);              // the MMA issuer commits the closed epoch at this tile
       }
       // final epoch of the pass
       flush(Cj);
       drain(Cj);
       // observed maxima, the precision check and the next launch's guess
-      sh.tmx[c][j] = obs;
-      sh.cs[c][j] = csf;
-      sh.nr[c][j] = nrf;
-      k1tc::named_bar(kBarSl, 128);
-      if (c == 0) {
-        const int em = max(max(sh.tmx[0][j], sh.tmx[1][j]), max(sh.tmx[2][j], sh.tmx[3][j]));
+      sh.tmx[sw][j] = obs;
+      sh.cs[sw][j] = csf;
+      sh.nr[sw][j] = nrf;
+      k1tc::named_bar(kBarSl, kSlT);
+      if (sw == 0) {
+        int em = 0;
+        double nsum = 0.0, csum = 0.0;
+#pragma unroll
+        for (int q = 0; q < kSlW; ++q) {
+          em = max(em, sh.tmx[q][j]);
+          nsum += sh.nr[q][j];
+          csum += sh.cs[q][j];
+        }
         gE[unit * 32 + j] = em;
         if (em >= Fmt<TD>::kEmax) atomicOr(flags, 1u);          // NaN / Inf in the block
         // the first epoch's C more than kH + kShrink above what the data needed: precision lost
         const bool lost = em > 0 && (em - Cfirst) < 31 - kH - kShrink;
-        if (lost && pass == 0) atomicOr(&sh.redo, 1);
-        npart[unit * 32 + j] = ((sh.nr[0][j] + sh.nr[1][j]) + sh.nr[2][j]) + sh.nr[3][j];
-        cpart[unit * 32 + j] = ((sh.cs[0][j] + sh.cs[1][j]) + sh.cs[2][j]) + sh.cs[3][j];
+        if (lost && pass == 0 && atomicOr(&sh.redo, 1) == 0) atomicAdd(gE + kMaxUnits * 32 + 2, 1);
+        npart[unit * 32 + j] = nsum;
+        cpart[unit * 32 + j] = csum;
       }
-      (void)ep;
     } else if (warp >= kGen0) {
       // ------------------------------------------------------------ sketch generator
       const int gt = threadIdx.x - 32 * kGen0;    // 0..255
-      const int nrow = nu > 256 ? 2 : 1;
       // per-row parts of rounds 1-3 (counter (g, R, 0, 0), key (k0, k1), reading R2)
       uint32_t A2[2], R2[2];
       int rr[2];
@@ -500,25 +522,20 @@ k1f_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Key
         A2[q] = hi ^ keys.k1[1];
         R2[q] = lo;
       }
-      const bool row1 = (nrow == 2) && (rr[1] < nu);
-      const bool row0 = rr[0] < nu;
-      const uint32_t bchunk = static_cast<uint32_t>(nu) * 16;
-      const uint32_t K16 = launder(16u), K65536 = launder(65536u);
+      const uint32_t bchunk = static_cast<uint32_t>(g.brows) * 16;
+      const uint32_t boff[2] = {static_cast<uint32_t>((rr[0] >> 3) * 128 + (rr[0] & 7) * 16),
+                                static_cast<uint32_t>((rr[1] >> 3) * 128 + (rr[1] & 7) * 16)};
+      const uint32_t K16 = g.k16, K65536 = g.k65536;
       for (int t = 0; t < ntiles; ++t) {
-        const int T = T0 + t, s = T % kNS;
-        if (T >= kNS) {
-          if (lane == 0) k1tc::mbar_wait(&sh.b_empty[s], ((T / kNS) - 1) & 1);
-          __syncwarp();
-        }
-        uint8_t* bs = bbuf + s * g.b_bytes;
-        const uint32_t g0 = static_cast<uint32_t>((row_begin + r0 + int64_t(t) * kKT) >> 5);
+        const int T = T0 + t, s = T % kNSB;
         // group parts (uniform): rounds 1-3
+        const uint32_t g0 = static_cast<uint32_t>((row_begin + (range + int64_t(t) * g.nranges) * kKT) >> 5);
         uint32_t G2[2], G3k[2], G5k[2], G5l[2];
 #pragma unroll
         for (int gi = 0; gi < 2; ++gi) {
-          uint32_t h, l;
-          mulhilo32(0xD2511F53u, g0 + gi, h, l);
-          const uint32_t G1 = h ^ keys.k1[0];
+          uint32_t hh, l;
+          mulhilo32(0xD2511F53u, g0 + gi, hh, l);
+          const uint32_t G1 = hh ^ keys.k1[0];
           G2[gi] = l;
           uint32_t h2, l2;
           mulhilo32(0xCD9E8D57u, G1, h2, l2);
@@ -530,10 +547,10 @@ k1f_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Key
           G5k[gi] = h3 ^ keys.k1[2];
           G5l[gi] = l3;
         }
-        // 4 streams: (row q, group gi)
+        // 2 NROW streams: (row q, group gi)
         uint32_t c0[4], c1[4], c2[4], c3[4];
 #pragma unroll
-        for (int q = 0; q < 2; ++q)
+        for (int q = 0; q < NROW; ++q)
 #pragma unroll
           for (int gi = 0; gi < 2; ++gi) {
             const int ci = 2 * q + gi;
@@ -548,8 +565,7 @@ k1f_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Key
 #pragma unroll
         for (int rnd = 3; rnd < 10; ++rnd) {
 #pragma unroll
-          for (int ci = 0; ci < 4; ++ci) {
-            if (ci >= 2 && nrow == 1) continue;
+          for (int ci = 0; ci < 2 * NROW; ++ci) {
             uint32_t hi0, lo0, hi1, lo1;
             mulhilo32(0xD2511F53u, c0[ci], hi0, lo0);
             mulhilo32(0xCD9E8D57u, c2[ci], hi1, lo1);
@@ -558,11 +574,14 @@ k1f_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Key
             c0[ci] = n0; c1[ci] = lo1; c2[ci] = n2; c3[ci] = lo0;
           }
         }
+        if (T >= kNSB) {
+          if (lane == 0) k1tc::mbar_wait(&sh.b_empty[s], ((T / kNSB) - 1) & 1);
+          __syncwarp();
+        }
+        uint8_t* bs = bbuf + s * g.b_bytes;
 #pragma unroll
-        for (int ci = 0; ci < 4; ++ci) {
+        for (int ci = 0; ci < 2 * NROW; ++ci) {
           const int q = ci >> 1, gi = ci & 1;
-          if (q == 1 && !row1) continue;
-          if (q == 0 && !row0) continue;
           const uint32_t ws[4] = {c0[ci], c1[ci], c2[ci], c3[ci]};
           uint32_t pk[8];
 #pragma unroll
@@ -576,8 +595,7 @@ k1f_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Key
             pk[2 * k] = mlo ^ slo;
             pk[2 * k + 1] = mhi ^ shi;
           }
-          const int r = rr[q];
-          uint8_t* d0 = bs + (2 * gi) * bchunk + (r >> 3) * 128 + (r & 7) * 16;
+          uint8_t* d0 = bs + (2 * gi) * bchunk + boff[q];
           *reinterpret_cast<uint4*>(d0) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           *reinterpret_cast<uint4*>(d0 + bchunk) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }
@@ -664,18 +682,7 @@ inline bool k1f_call_ok(const K1TcArgs& a) {
 inline cudaError_t k1f_launch(const K1TcArgs& a, int* gE, cudaStream_t st, int* nlaunch) {
   *nlaunch = 0;
   const int64_t m_loc = a.row_end - a.row_begin;
-  const k1f::Geom g = k1f::make_geom(a.ell, a.ncols, m_loc, a.f64, a.num_sms);
-  CUtensorMap map;
-  const int es = a.f64 ? 8 : 4;
-  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(m_loc), static_cast<cuuint64_t>(a.ncols)};
-  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.ld) * es};
-  const cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / es), 32u};
-  const cuuint32_t estr[2] = {1, 1};
-  CUresult cr = k1tc_encoder()(&map, a.f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
-                               const_cast<void*>(a.X), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  k1f::Geom g = k1f::make_geom(a.ell, a.ncols, m_loc, a.f64, a.num_sms);
   k1f::Keys keys;
   uint32_t k0 = a.key0, k1 = a.key1;
   for (int r = 0; r < 10; ++r) {
@@ -685,13 +692,27 @@ inline cudaError_t k1f_launch(const K1TcArgs& a, int* gE, cudaStream_t st, int* 
   double* part = reinterpret_cast<double*>(a.ws);
   double* npart = part + static_cast<size_t>(k1f::kMaxUnits) * 512 * 32;
   double* cpart = npart + static_cast<size_t>(k1f::kMaxUnits) * 32;
-  auto fn = a.f64 ? k1f::k1f_kernel<double> : k1f::k1f_kernel<float>;
+  CUtensorMap map;
+  const int es = a.f64 ? 8 : 4;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(m_loc), static_cast<cuuint64_t>(a.ncols)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.ld) * es};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(g.xline / es), 32u};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult cr = k1tc_encoder()(&map, a.f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                               const_cast<void*>(a.X), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  auto fn = a.f64 ? (g.brows == 512 ? k1f::k1f_kernel<double, 2> : k1f::k1f_kernel<double, 1>)
+                  : (g.brows == 512 ? k1f::k1f_kernel<float, 2> : k1f::k1f_kernel<float, 1>);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem);
+  if (e == cudaSuccess)
+    fn<<<g.nunits(), k1f::kThreads, g.smem, st>>>(map, a.ncols, keys, a.row_begin, m_loc, g, a.t0, a.t1, part, npart, cpart, gE,
+                                                  a.flags);
   if (e != cudaSuccess) {
     (void)cudaGetLastError();
     return e;
   }
-  fn<<<g.nunits(), k1f::kThreads, g.smem, st>>>(map, keys, a.row_begin, m_loc, g, a.t0, a.t1, part, npart, cpart, gE, a.flags);
   *nlaunch += 1;
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;

@@ -299,7 +299,7 @@ Layout make_layout(const oid_params& p) {
   L.tc = b.take(std::max(std::max(k1tc_workspace_bytes(p.ell, p.b_max, m_local(p), p.dtype == OID_F64),
                                   k1p_workspace_bytes(p.ell, p.b_max, m_local(p), p.dtype == OID_F64)),
                          k1f_workspace_bytes()));
-  L.k1g = b.take(static_cast<size_t>(k1f::kMaxUnits) * 32 * sizeof(int));   // K1F exponent guesses
+  L.k1g = b.take(static_cast<size_t>(k1f::kMaxUnits * 32 + 8) * sizeof(int));   // K1F exponent guesses + counters
   L.total = b.off;
   return L;
 }
@@ -1466,6 +1466,8 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
   if ((e = cudaMemsetAsync(ctx->ws + L.gcnt, 0, 8 * sizeof(int), st)) != cudaSuccess) return bad(e);
   k1f::fill_int_kernel<<<(k1f::kMaxUnits * 32 + 255) / 256, 256, 0, st>>>(ctx->ptr<int>(L.k1g), k1f::kMaxUnits * 32,
                                                                         k1f::kNoGuess);
+  if ((e = cudaMemsetAsync(ctx->ws + L.k1g + k1f::kMaxUnits * 32 * sizeof(int), 0, 8 * sizeof(int), st)) != cudaSuccess)
+    return bad(e);
   if ((e = cudaGetLastError()) != cudaSuccess) return bad(e);
   {
     const int64_t RL = 128 / static_cast<int64_t>(dsize(*p));
@@ -1841,6 +1843,7 @@ oid_status oid_get(oid_ctx ctx, int32_t field, void* host_dst, size_t bytes, voi
     case 10: off = L.dbg; need = k1p::kDbgRows * k1tc::kDbgTiles * sizeof(long long); break;
     case 11: off = L.G; need = sizeof(double) * ctx->t * ctx->t; break;
     case 12: off = L.dbg + k1p::kDbgRows * k1tc::kDbgTiles * sizeof(long long); need = k1tc::kDbgTiles * sizeof(long long); break;
+    case 15: off = L.k1g; need = sizeof(int) * (k1f::kMaxUnits * 32 + 8); break;
     case 14:
       if (p.coeff_mode != 1) return ctx->fail(OID_ESTATE, "field 14 needs coeff_mode = 1");
       off = L.qlog; need = sizeof(double) * 6 * ctx->epoch; break;

@@ -76,6 +76,8 @@ ok &= all(x[1] < 1.0 for x in r)
 r = check(300000, 32, 512, "f64", scales=(1.0, 1.0, 1024.0, 1.0 / 4096, 3.0))
 ok &= all(x[1] < 1.0 for x in r)
 print("BOUND_OK" if ok else "BOUND_FAIL", flush=True)
+for (sc, ratio, q, y, nn) in r:
+    print(f"  scale x{sc:g}: max/bound {ratio:.3e} relY {y:.3e}")
 
 if a.full:
     gen = ChannelFlow(192, 129, 192, seed=1003)
