@@ -647,8 +647,17 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
         }
       }
       if (dbgt) g.dbg[6 * kDbgTiles + t] = clock64();
+      // release the X stages only once the loads have landed in registers (the arrive depends on
+      // their values through an opaque OR): otherwise the next TMA load can overwrite the stage
+      // before the shared-memory loads read it (a WAR race across proxies, observed in K1F)
+      uint32_t tok = 0u;
+#pragma unroll
+      for (int gi = 0; gi < G; ++gi)
+#pragma unroll
+        for (int c = 0; c < RPT * NW; ++c) tok |= w[gi][c];
+      asm volatile("or.b32 %0, %0, 1;" : "+r"(tok));
       __syncwarp();
-      if (lane == 0) {
+      if (lane == 0 && tok != 0u) {
 #pragma unroll
         for (int gi = 0; gi < G; ++gi)
           if (gi < cnt) mbar_arrive(&sh.x_empty[sg_[gi]]);

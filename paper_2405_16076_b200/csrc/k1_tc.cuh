@@ -477,12 +477,15 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
       mbar_wait(&sh.x_full[s], ph);
       uint32_t wc[GHU][NWH];
       load_tile(s, wc);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sh.x_empty[s]);     // values are in registers
       if (t >= NS) mbar_wait(&sh.b_empty[s], ph ^ 1u);
       if (dbgt) g.dbg[6 * kDbgTiles + t] = clock64();
       int egen = *reinterpret_cast<volatile int*>(&sh.egen);
       int viol = g.exp == 2 ? 0 : convert(wc, s, true);
+      // release the X stage only after its values were consumed: an arrive right after issuing
+      // the shared-memory loads lets the next TMA load overwrite them first (a WAR race across
+      // the generic and async proxies, observed in K1F)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.x_empty[s]);
       fence_proxy_async();
       int viol_any = named_bar_or(barg, GT, viol);
       if (dbgt) g.dbg[7 * kDbgTiles + t] = clock64();
