@@ -109,7 +109,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--workload", default="C3", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--k1-mode", type=int, default=0)
+    ap.add_argument("--k1-mode", type=int, default=4,
+                    help="oid_k1_mode: 4 = K1F (31-bit fixed point, parity-tested at full C3 size in "
+                         "tests/test_gpu_k1fast.py; the default), 2 = exact int8 digit planes, 0 = auto (exact)")
     ap.add_argument("--no-estimate", action="store_true", help="ingest only (estimate not in the step)")
     ap.add_argument("--one-stream", action="store_true", help="estimates on the ingest stream (no overlap)")
     ap.add_argument("--cpu-sample-rows", type=int, default=1 << 18)
@@ -398,24 +400,28 @@ def main():
     k1_flops = 2.0 * ell * m_loc * b
     mode = st["k1_mode_used"]
     t_hbm = k1_bytes / (hbm * 1e9) * 1e3
-    t_flop = k1_flops / (int8_tops * 1e12) * 1e3 if mode in (oid.K1_TC_INT8, oid.K1_TC_PAIR) else \
+    tc_modes = (oid.K1_TC_INT8, oid.K1_TC_PAIR, oid.K1_TC_FAST)
+    t_flop = k1_flops / (int8_tops * 1e12) * 1e3 if mode in tc_modes else \
         k1_flops / (bf16_sus * FP64_NOMINAL_TF / BF16_NOMINAL_TF * 1e12) * 1e3
     t_roof = max(t_hbm, t_flop)
     traffic, traffic_src = _traffic_from_profiles(args.workload, mode)
     roof = {"bound": "hbm" if t_hbm >= t_flop else "tensor",
             "achieved": k1_bytes / (k1_avg_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
             "frac": t_roof / k1_avg_ms, "traffic": traffic, "traffic_source": traffic_src,
-            "kernel": {oid.K1_TC_INT8: "k1_tc_kernel", oid.K1_TC_PAIR: "k1p::k1_tc_kernel"}.get(mode, "k1_simt_kernel"),
+            "kernel": {oid.K1_TC_INT8: "k1_tc_kernel", oid.K1_TC_PAIR: "k1p::k1_tc_kernel",
+                       oid.K1_TC_FAST: "k1f_kernel"}.get(mode, "k1_simt_kernel"),
             "k1_ms": k1_avg_ms, "hbm_roof_ms": t_hbm, "flop_roof_ms": t_flop, "peak_source": src,
             "definition": "frac = max(block bytes / HBM peak, 2 l m b / int8 peak) / t_K1 (SURVEY 8(d)); "
                           "t_K1 = CUDA events on the ingest stream inside the timed region"}
-    planes = (7 if dt == "f64" else 6) if mode == oid.K1_TC_INT8 else 6
+    planes = {oid.K1_TC_INT8: 7 if dt == "f64" else 6, oid.K1_TC_PAIR: 6, oid.K1_TC_FAST: 4}.get(mode, 0)
     emul = None
-    if mode in (oid.K1_TC_INT8, oid.K1_TC_PAIR):
+    if mode in tc_modes:
         ops = planes * k1_flops
         emul = {"planes": planes, "int8_ops_per_launch": ops, "achieved_tops": ops / (k1_avg_ms * 1e-3) / 1e12,
                 "peak_tops": int8_tops, "frac": ops / (k1_avg_ms * 1e-3) / 1e12 / int8_tops,
-                "note": "exact fixed-point emulation: one int8 MAC per digit plane per sketch multiply-add"}
+                "note": ("fixed-point emulation: one int8 MAC per digit plane per sketch multiply-add; " +
+                         ("31-bit fixed point (K1F), |x - x_q| <= 2^-27 max|x_j|" if mode == oid.K1_TC_FAST
+                          else "exact (56-bit / 48-bit fixed point)"))}
     # sketch-entry (RNG) roof: l m_loc Gauss-16 entries per launch; ALU-pipe bound at 1.5 ALU ops per
     # entry (Philox4x32-10: 20 LOP3 per 32 entries; Gauss-16 decode: 7 ALU ops per 8 entries, sm_100a
     # SASS) on 148 SMs x 64 ALU lanes per clock
@@ -528,7 +534,9 @@ def main():
             "breakdown_ms_per_step": {"k1": st["k1_ms"] / K, "post": st["post_ms"] / K, "estimate": st["est_ms"] / K},
             "ingest_only": ingest_only,
             "last_estimate": {"est_rel": est_val[5], "e2": est_val[0], "flags": int(est_val[6])},
-            "k1_mode": "tc_int8" if mode == oid.K1_TC_INT8 else "simt_f64",
+            "k1_mode": {oid.K1_TC_INT8: "tc_int8 (exact)", oid.K1_TC_PAIR: "tc_pair (exact)",
+                        oid.K1_TC_FAST: "tc_fast (K1F: 31-bit fixed point, int8 digit planes, int32 accumulate, "
+                                        "fp64 assembly)"}.get(mode, "simt_f64"),
         }
         print(json.dumps(line), flush=True)
     eng.close()
@@ -543,7 +551,7 @@ def _traffic_from_profiles(workload, mode):
     try:
         with open(path) as f:
             d = json.load(f)
-        key = f"{workload}:{ {2: 'tc', 3: 'pair'}.get(mode, 'simt') }"
+        key = f"{workload}:{ {2: 'tc', 3: 'pair', 4: 'fast'}.get(mode, 'simt') }"
         ent = d.get(key)
         if isinstance(ent, dict):
             return ent.get("bytes"), "copied from " + ent.get("capture", "profiles/k1_traffic.json")

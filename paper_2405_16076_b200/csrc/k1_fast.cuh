@@ -448,7 +448,9 @@ k1f_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, const __grid_con
           P[2][q] = k1tc::prmt(x1, y1, 0x5410) ^ 0x80808080u;
           P[3][q] = k1tc::prmt(x1, y1, 0x7632);
         }
-        // A stage free?
+        // A stage free?  (the conversion above runs before the wait: see the generator)
+#pragma unroll
+        for (int q = 0; q < kSlE / 4; ++q) asm volatile("" ::"r"(P[0][q]), "r"(P[1][q]), "r"(P[2][q]), "r"(P[3][q]));
         if (T >= kNSA) k1tc::mbar_wait(&sh.a_empty[sa], ((T / kNSA) - 1) & 1);
         // A row 32 (j / 8) + 8 p + j % 8: the 8 lanes of a store phase hit 8 different 16-byte
         // bank groups, and the four planes of a column share a TMEM lane quarter (lanes l + 8 p)
@@ -574,6 +576,10 @@ k1f_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, const __grid_con
             c0[ci] = n0; c1[ci] = lo1; c2[ci] = n2; c3[ci] = lo0;
           }
         }
+        // the Philox rounds above run before the wait (an ordered volatile asm that reads their
+        // results; the compiler would otherwise hoist the wait above the register-only arithmetic)
+#pragma unroll
+        for (int ci = 0; ci < 2 * NROW; ++ci) asm volatile("" ::"r"(c0[ci]), "r"(c1[ci]), "r"(c2[ci]), "r"(c3[ci]));
         if (T >= kNSB) {
           if (lane == 0) k1tc::mbar_wait(&sh.b_empty[s], ((T / kNSB) - 1) & 1);
           __syncwarp();
