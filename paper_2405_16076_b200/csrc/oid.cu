@@ -24,6 +24,7 @@
 #include "k1_tc.cuh"
 #include "k1_pair.cuh"
 #include "k1_fast.cuh"
+#include "gram_q.cuh"
 #include "coeff.cuh"
 #include "gram_tc.cuh"
 #include "grad.cuh"
@@ -122,7 +123,7 @@ struct Bump {
 struct Layout {
   size_t S, gram, Ypart, k1part, k1npart, gB, gV, mu, mu_sorted, Yc, Tsc, tau, scal, J, tau_old, admit, counts,
       flags, counters, C, SJ, sjB, sjV, sjsig, sjw, sjZ, Sjpinv, Pexp, AJP, G, Gsum, Gpart, cB, cV, csig, cw, cZ, M,
-      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, k1g, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, wyT, sjG, cG, cBt, cZ2, dbg, Jsnap, Dsnap, gcnt, Sg, YpG, GX, OGO, gH, gHV, gHs, gHw, gHZ, gHp, gR, gCm, gE, gLst, gLV, gLs, gLw, gLZ, gLp, gRhs, gscal, td2, te2, Vh2, tauv2, wyT2, ldl2, mu2, cum, elog, eslog, omega, trA, trW, Pcand, Pchosen, Pext, Rres, Gprev, gpH, gpV, gpMu, gpW, Gpinv, Xc, Dx, Dxp, Tm, cest, est_ch, est4, qlog, Jprev, olds, nold, qsel, Dpool, Dnorm, total;
+      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, k1g, Cq, Fq, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, wyT, sjG, cG, cBt, cZ2, dbg, Jsnap, Dsnap, gcnt, Sg, YpG, GX, OGO, gH, gHV, gHs, gHw, gHZ, gHp, gR, gCm, gE, gLst, gLV, gLs, gLw, gLZ, gLp, gRhs, gscal, td2, te2, Vh2, tauv2, wyT2, ldl2, mu2, cum, elog, eslog, omega, trA, trW, Pcand, Pchosen, Pext, Rres, Gprev, gpH, gpV, gpMu, gpW, Gpinv, Xc, Dx, Dxp, Tm, cest, est_ch, est4, qlog, Jprev, olds, nold, qsel, Dpool, Dnorm, total;
 };
 
 int64_t m_local(const oid_params& p) { return p.row_end - p.row_begin; }
@@ -130,6 +131,14 @@ constexpr int kElogCols = 8;   // report row: epoch log [epoch, n_obs, admission
                                // min margin, kappa(S_J)]; estimate log [epoch, e2, T, gpp, frob2, est_rel,
                                // flags, kappa]
 size_t dsize(const oid_params& p) { return p.dtype == OID_F64 ? 8 : 4; }
+
+// A9Q (the basis Gram on int8 tensor cores from a quantised basis copy) needs K1F's per-column
+// exponents of the block the admitted columns come from: the snapshot-block path only (not the
+// t-column buffer, not the gradient variant); OID_A9Q=0 keeps the fp64 A9 (diagnostics)
+inline bool a9q_wanted(const oid_params& p) {
+  const char* env = getenv("OID_A9Q");
+  return p.k1_mode == OID_K1_TC_FAST && p.epoch_mode == 0 && p.grad_nfields == 0 && !(env && atoi(env) == 0);
+}
 
 Layout make_layout(const oid_params& p) {
   Layout L{};
@@ -291,6 +300,10 @@ Layout make_layout(const oid_params& p) {
     L.nold = b.take(4 * sizeof(int));
     L.qsel = b.take(4 * sizeof(int));
   }
+  if (a9q_wanted(p)) {   // A9Q: the quantised basis (4 digit planes per element) and its exponents
+    L.Cq = b.take(a9q::qbasis_bytes(m_local(p), static_cast<int>(t)));
+    L.Fq = b.take(t * sizeof(int));
+  }
   if (p.omega_cache == 1) {   // omega_cache (NEXT-3): Philox words of ell x m_loc sketch entries
     // + 1 group: the last 64-row K1 tile may run one 32-row group past the shard (zero rows of X)
     const int64_t ng = (p.row_end + 31) / 32 - p.row_begin / 32 + 1;
@@ -400,6 +413,7 @@ struct oid_ctx_s {
   int gs_gate = 0;            // A9 also waits for the epoch's A8 chain (diagnostics: OID_GS_GATE)
   bool use_side = true;       // diagnostics: OID_NO_SIDE=1 runs everything on the caller's stream
   int k1_free_sms = 0;        // SMs the persistent K1 grid leaves to concurrent streams (OID_K1_FREE)
+  bool a9q = false;           // A9 on the quantised basis (K1F mode; off for good once a block skips K1F)
   int last_nc = 0;            // columns of the last committed epoch (NEXT-1's P_prev extension)
   int dcount = 0;             // NEXT-2: columns buffered in D since the last epoch
   int64_t dbase = 0;          //         global index of D's first column
@@ -917,6 +931,21 @@ oid_status post_epoch(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream
       basis_copy_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(X), ld, ctx->ptr<float>(L.C), ctx->m_loc,
                                                      ctx->ptr<int>(L.admit), ctx->ptr<int>(L.counts), nc, t);
     CKL();
+    if (ctx->a9q && ctx->k1_mode_used != OID_K1_TC_FAST) ctx->a9q = false;   // no exponents for this block
+    if (ctx->a9q) {
+      const k1f::Geom kg = k1f::make_geom(p.ell, nc, ctx->m_loc, p.dtype == OID_F64, std::max(2, ctx->num_sms - ctx->k1_free_sms));
+      if (p.dtype == OID_F64)
+        a9q::basis_quant_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(X), ld, ctx->ptr<uint8_t>(L.Cq),
+                                                             ctx->ptr<int>(L.Fq), ctx->m_loc, t, ctx->ptr<int>(L.admit),
+                                                             ctx->ptr<int>(L.counts), nc, ctx->ptr<int>(L.k1g), kg.nunits(),
+                                                             kg.nsg);
+      else
+        a9q::basis_quant_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(X), ld, ctx->ptr<uint8_t>(L.Cq),
+                                                            ctx->ptr<int>(L.Fq), ctx->m_loc, t, ctx->ptr<int>(L.admit),
+                                                            ctx->ptr<int>(L.counts), nc, ctx->ptr<int>(L.k1g), kg.nunits(),
+                                                            kg.nsg);
+      CKL();
+    }
   }
   tl_mark(ctx, st, 6);
   if (do_a3) ctx->n_obs += nc;
@@ -1431,6 +1460,8 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
       return OID_ECUDA;
     }
     const int bgmax = 200 * 1024 + 1024;
+    if ((e = cudaFuncSetAttribute(a9q::gram_q_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(a9q::smem_bytes()))) != cudaSuccess) return bad(e);
     if ((e = cudaFuncSetAttribute(bgtc::basis_gram_tc_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, bgmax)) != cudaSuccess) return bad(e);
     if ((e = cudaFuncSetAttribute(bgtc::basis_gram_tc_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, bgmax)) != cudaSuccess) return bad(e);
     if ((e = cudaFuncSetAttribute(bgtc::basis_gram_tc_kernel<double>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess) return bad(e);
@@ -1473,6 +1504,11 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
     const int64_t RL = 128 / static_cast<int64_t>(dsize(*p));
     const size_t cb = static_cast<size_t>((ctx->m_loc + RL - 1) / RL * RL) * ctx->t * dsize(*p);
     if ((e = cudaMemsetAsync(ctx->ws + L.C, 0, cb, st)) != cudaSuccess) return bad(e);
+  }
+  ctx->a9q = a9q_wanted(*p) && ctx->tc_ok;
+  if (a9q_wanted(*p)) {
+    if ((e = cudaMemsetAsync(ctx->ws + L.Cq, 0, a9q::qbasis_bytes(ctx->m_loc, ctx->t), st)) != cudaSuccess) return bad(e);
+    if ((e = cudaMemsetAsync(ctx->ws + L.Fq, 0, sizeof(int) * ctx->t, st)) != cudaSuccess) return bad(e);
   }
   if (p->omega_cache == 1) {
     const int64_t g0 = p->row_begin / 32, ng = (p->row_end + 31) / 32 - g0 + 1;
@@ -1608,7 +1644,18 @@ static oid_status estimate_begin_impl(oid_ctx ctx, void* stream) {
       lc.attrs = la;
       lc.numAttrs = 1;
     }
-    {
+    if (ctx->a9q) {
+      // A9Q: (row-tile set, slot chunk) CTAs, one per SM, leaving SMs to the concurrent chain
+      const int nch = a9q::nchunks(t);
+      const int nr = std::max(1, (sms - 20) / nch);
+      grid = nr * nch;
+      EvScope eva9(ctx, gs, &ctx->ev_a9);
+      const int64_t nt128 = (ctx->m_loc + a9q::kTR - 1) / a9q::kTR;
+      a9q::gram_q_kernel<<<grid, a9q::kThreads, a9q::smem_bytes(), gs>>>(ctx->ptr<uint8_t>(L.Cq), ctx->ptr<int>(L.Fq),
+                                                                          nt128, t, nr, static_cast<const int*>(dl),
+                                                                          static_cast<const int*>(gc), ctx->d(L.Gpart));
+      CKL();
+    } else {
       EvScope eva9(ctx, gs, &ctx->ev_a9);
       if (f64)
         CK(cudaLaunchKernelEx(&lc, bgtc::basis_gram_tc_kernel<double>, ctx->bg_map, ntiles, t, per, nstage, stage_bytes,

@@ -222,3 +222,37 @@ def test_k1f_c3_fullsize_sampled(oid):
         assert np.all(np.abs(Yg[r] - yr) <= bound + 1e-12 * np.abs(yr)), r
         assert np.max(np.abs(Yg[r] - yr)) <= 1e-7 * np.max(np.abs(yr)), r
     eng.close()
+
+
+def test_a9q_gram_bound(oid):
+    """A9Q (K1F mode): the basis Gram on the int8 tensor cores from the quantised basis copy, after
+    each of several estimates, against fp64 dot products of the finalized (exact) basis columns.
+    A7 quantises a column with unit <= 2^-28 of its maximum (|a - a_q| <= 2^-27 M), so
+    |dG_ij| <= 2^-27 (M_j ||a_i||_1 + M_i ||a_j||_1) + m 2^-54 M_i M_j; rows of vacant slots are 0."""
+    cfg = C3R
+    gen = ChannelFlow(48, 33, 48, seed=cfg.data_seed)
+    m, b = cfg.m, cfg.b
+    eng, _ = _engine(oid, m, cfg.k, cfg.ell, b, 8 * b, -1.0, seed=0)
+    A = gen.block(0, 8 * b)
+    Ad = _dev(A, np.float64)
+    rng = np.random.default_rng(4)
+    for blk in range(8):
+        eng.ingest_block(Ad[:, blk * b:(blk + 1) * b])
+        if blk not in (0, 1, 3, 7):
+            continue
+        eng.error_estimate()
+        G = eng.get(11)
+        J = eng.J()
+        occ = np.flatnonzero(J >= 0)
+        basis = eng.finalize(basis=True)["basis"].cpu().numpy()
+        pick = rng.choice(occ, size=min(12, len(occ)), replace=False)
+        for i in pick:
+            for j in pick:
+                ai, aj = basis[:, i], basis[:, j]
+                ref = float(np.dot(ai, aj))
+                Mi, Mj = np.max(np.abs(ai)), np.max(np.abs(aj))
+                bnd = 2.0 ** -27 * (Mj * np.sum(np.abs(ai)) + Mi * np.sum(np.abs(aj))) + m * 2.0 ** -54 * Mi * Mj
+                assert abs(G[i, j] - ref) <= bnd + 1e-13 * abs(ref), (blk, i, j, G[i, j], ref, bnd)
+        vac = np.flatnonzero(J < 0)
+        assert np.all(G[vac, :] == 0) and np.all(G[:, vac] == 0)
+    eng.close()
