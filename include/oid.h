@@ -122,7 +122,14 @@ typedef struct {
      three gradient components with spacings grad_hx, grad_hy, grad_hz (0: 1/(N-1)), augmented
      sketch of 4 ell rows ((d + 1) ell <= 2048).  0 or 1: the 2-D grid above.                    */
   int32_t grad_nz;
-  int32_t reserved1;
+  /* Basis Gram (A9).  0: exact fp64 (DMMA) from the stored basis (the default).  1: A9Q - int8
+     tensor cores from a second copy of the basis quantised by A7 to a 31-bit per-column fixed
+     point (4 bytes per element, half the read, no DMMA bound; |dG_ij| <= 2^-27 (M_j ||a_i||_1 +
+     M_i ||a_j||_1) + m 2^-54 M_i M_j).  Needs k1_mode = OID_K1_TC_FAST,
+     epoch_mode = 0 and no gradient variant (else the exact A9 runs); NOT for ill-conditioned
+     bases: the NA-Hutch++ estimate amplifies G's error by about kappa(S_J)^2 (on C1 it misses the
+     1e-5 bar).                                                                                  */
+  int32_t a9_mode;
   double grad_hz;
 } oid_params;
 

@@ -44,7 +44,7 @@ class OidParams(ctypes.Structure):
                 ("grad_nfields", ctypes.c_int32), ("grad_nx", ctypes.c_int32), ("grad_ny", ctypes.c_int32),
                 ("omega_cache", ctypes.c_int32), ("grad_hx", ctypes.c_double), ("grad_hy", ctypes.c_double),
                 ("coeff_mode", ctypes.c_int32), ("epoch_mode", ctypes.c_int32),
-                ("grad_nz", ctypes.c_int32), ("reserved1", ctypes.c_int32), ("grad_hz", ctypes.c_double)]
+                ("grad_nz", ctypes.c_int32), ("a9_mode", ctypes.c_int32), ("grad_hz", ctypes.c_double)]
 
 
 class OidStats(ctypes.Structure):
@@ -119,11 +119,13 @@ def hutch_split(ell):
 
 def make_params(m, k, ell, b_max, n_cap, lam, split=None, eps=0.5, delta=0.05, c=1.0, seed=0, dtype="f64",
                 row_begin=0, row_end=None, k1_mode=K1_AUTO, profile=False, device=0, grad=None,
-                omega_cache=False, coeff="alg4", epochs="block", grad3=None):
+                omega_cache=False, coeff="alg4", epochs="block", grad3=None, a9q=False):
     """grad: None, or (nfields, nx, ny[, hx, hy]) for the gradient-enhanced variant (A11) on a 2-D
     grid; grad3: (nfields, nx, ny, nz[, hx, hy, hz]) for the 3-D grid with three components (NEXT-4).
     coeff: "alg4" (Alg 4 every epoch, the hot path) or "argmin" (Algs 4-7 + NA-Hutch++ argmin, NEXT-1).
-    epochs: "block" (one block = one epoch, R4) or "t" (the paper's t-column buffer, NEXT-2)."""
+    epochs: "block" (one block = one epoch, R4) or "t" (the paper's t-column buffer, NEXT-2).
+    a9q: the basis Gram on int8 tensor cores from a quantised basis copy (a9_mode = 1, oid.h;
+    k1_mode = K1_TC_FAST only; not for ill-conditioned bases)."""
     if coeff not in ("alg4", "argmin"):
         raise ValueError("coeff must be 'alg4' or 'argmin'")
     if epochs not in ("block", "t"):
@@ -140,7 +142,7 @@ def make_params(m, k, ell, b_max, n_cap, lam, split=None, eps=0.5, delta=0.05, c
                      profile=int(bool(profile)), device=device, grad_nfields=int(g[0]), grad_nx=int(g[1]),
                      grad_ny=int(g[2]), omega_cache=int(omega_cache), grad_hx=float(g[3]), grad_hy=float(g[4]),
                      coeff_mode=1 if coeff == "argmin" else 0, epoch_mode=1 if epochs == "t" else 0,
-                     grad_nz=nz, grad_hz=hz)
+                     grad_nz=nz, grad_hz=hz, a9_mode=1 if a9q else 0)
 
 
 def workspace_bytes(params):

@@ -206,6 +206,14 @@ gram_q_kernel(const uint8_t* __restrict__ Cq, const int* __restrict__ Fq, int64_
             }
           }
         }
+        if (first_drain) {
+          // the fixed-order reduction sums whole partial rows: zero the columns of the other
+          // slot chunks (computed by the other CTAs of this row-tile set)
+          for (int idx = gt; idx < ndg * t; idx += 128) {
+            const int qq = idx / t, j = idx - qq * t;
+            if (j < s0 || j >= s0 + tc) out[(q0 + qq) + static_cast<int64_t>(j) * t] = 0.0;
+          }
+        }
         first_drain = false;
         k1tc::tc_fence_before();
         __syncwarp();

@@ -134,10 +134,9 @@ size_t dsize(const oid_params& p) { return p.dtype == OID_F64 ? 8 : 4; }
 
 // A9Q (the basis Gram on int8 tensor cores from a quantised basis copy) needs K1F's per-column
 // exponents of the block the admitted columns come from: the snapshot-block path only (not the
-// t-column buffer, not the gradient variant); OID_A9Q=0 keeps the fp64 A9 (diagnostics)
+// t-column buffer, not the gradient variant); opt-in (a9_mode = 1, oid.h)
 inline bool a9q_wanted(const oid_params& p) {
-  const char* env = getenv("OID_A9Q");
-  return p.k1_mode == OID_K1_TC_FAST && p.epoch_mode == 0 && p.grad_nfields == 0 && !(env && atoi(env) == 0);
+  return p.a9_mode == 1 && p.k1_mode == OID_K1_TC_FAST && p.epoch_mode == 0 && p.grad_nfields == 0;
 }
 
 Layout make_layout(const oid_params& p) {

@@ -12,8 +12,8 @@ dev = torch.device("cuda", 0)
 gen = ChannelFlow(192, 129, 192, seed=C3.data_seed) if full else ChannelFlow(48, 33, 48, seed=C3R.data_seed)
 b, nblk = 32, (6 if full else 10)
 def run(a9q):
-    os.environ["OID_A9Q"] = "1" if a9q else "0"
-    p = oid.make_params(m=gen.m, k=200, ell=512, b_max=b, n_cap=nblk * b, lam=-1.0, seed=0, k1_mode=oid.K1_TC_FAST, profile=True)
+    p = oid.make_params(m=gen.m, k=200, ell=512, b_max=b, n_cap=nblk * b, lam=-1.0, seed=0, k1_mode=oid.K1_TC_FAST, profile=True,
+                        a9q=a9q)
     eng = oid.Engine(p)
     Gs, ts = [], []
     for blk in range(nblk):

@@ -49,10 +49,10 @@ def _split(ell):
     return (a, b, ell - a - b)
 
 
-def _engine(oid, m, k, ell, b_max, n_cap, lam, seed=0, dtype="f64", split=None):
+def _engine(oid, m, k, ell, b_max, n_cap, lam, seed=0, dtype="f64", split=None, a9q=False):
     split = _split(ell) if split is None else split
     p = oid.make_params(m=m, k=k, ell=ell, b_max=b_max, n_cap=n_cap, lam=lam, split=split, seed=seed, dtype=dtype,
-                        k1_mode=FAST)
+                        k1_mode=FAST, a9q=a9q)
     return oid.Engine(p), split
 
 
@@ -142,10 +142,10 @@ def test_k1f_exponent_paths(oid, monkeypatch):
     eng.close()
 
 
-def _stream(oid, A, b, k, ell, lam, seed, checks, dtype=np.float64, cache_limit=100_000_000, split=None):
+def _stream(oid, A, b, k, ell, lam, seed, checks, dtype=np.float64, cache_limit=100_000_000, split=None, a9q=False):
     m, n = A.shape
     eng, split = _engine(oid, m, k, ell, b, n, lam, seed=seed, dtype="f64" if dtype == np.float64 else "f32",
-                         split=split)
+                         split=split, a9q=a9q)
     o = OracleOID(OracleParams(m=m, k=k, ell=ell, ell1=split[0], ell2=split[1], ell3=split[2], lam=lam, seed=seed),
                   cache_limit=cache_limit)
     Ad = _dev(A, dtype)
@@ -193,6 +193,16 @@ def test_k1f_c3r_whole_stream(oid):
     assert o.min_margin() >= 1e-6
 
 
+def test_a9q_c3r_whole_stream(oid):
+    """The same whole C3r stream with the opt-in A9Q basis Gram (a9_mode = 1): on this well-posed
+    channel-flow basis the quantised G keeps the NA-Hutch++ components within 1e-5 of the oracle.
+    (On C1's nearly rank-deficient basis it does not - the reason A9Q is opt-in.)"""
+    cfg = C3R
+    gen = ChannelFlow(48, 33, 48, seed=cfg.data_seed)
+    A = gen.block(0, cfg.n)
+    _stream(oid, A, cfg.b, cfg.k, cfg.ell, -1.0, seed=0, checks={8, 16, 25, 32}, cache_limit=200_000_000, a9q=True)
+
+
 def test_k1f_c3_fullsize_sampled(oid):
     """C3 at full size (m = 14,266,368 fp64, b = 32, l = 512) in the bench launch configuration:
     sampled sketch rows recomputed by the oracle row by row, and all column norms, within the bound."""
@@ -232,7 +242,7 @@ def test_a9q_gram_bound(oid):
     cfg = C3R
     gen = ChannelFlow(48, 33, 48, seed=cfg.data_seed)
     m, b = cfg.m, cfg.b
-    eng, _ = _engine(oid, m, cfg.k, cfg.ell, b, 8 * b, -1.0, seed=0)
+    eng, _ = _engine(oid, m, cfg.k, cfg.ell, b, 8 * b, -1.0, seed=0, a9q=True)
     A = gen.block(0, 8 * b)
     Ad = _dev(A, np.float64)
     rng = np.random.default_rng(4)
