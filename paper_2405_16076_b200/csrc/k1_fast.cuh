@@ -48,15 +48,15 @@ namespace k1f {
 
 using k1tc::smem_u32;
 
-constexpr int kWarps = 16;
+constexpr int kWarps = 18;
 constexpr int kThreads = 32 * kWarps;
 constexpr int kKT = 64;            // data rows per tile (K of one pipeline stage)
 constexpr int kNSX = 6;            // X stages (~100 KB of fp64 in flight per SM)
 constexpr int kNSA = 3;            // A stages (digit planes, 8 KB)
 constexpr int kNSB = 3;            // B stages (sketch tile, 256 / 512 rows x 64 bytes)
-constexpr int kSl0 = 4, kSlW = 4;  // slicer warps 4..7 (TMEM lane quarter = warp % 4)
+constexpr int kSl0 = 2, kSlW = 8;  // slicer warps 2..9 (each TMEM lane quarter twice)
 constexpr int kSlE = kKT / kSlW;   // rows per slicer thread and tile (16)
-constexpr int kGen0 = 8, kGenW = 8;    // generator warps 8..15
+constexpr int kGen0 = 10, kGenW = 8;   // generator warps 10..17
 constexpr int kEpochTiles = 2048;  // int32 bound: 2048 * 64 rows * 128 * 111 < 2^31
 constexpr int kH = 1;              // exponent headroom over the guess (bits)
 constexpr int kShrink = 1;         // tolerated excess of the guess over the observed maximum (bits)
@@ -528,8 +528,8 @@ k1f_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, const __grid_con
       const uint32_t boff[2] = {static_cast<uint32_t>((rr[0] >> 3) * 128 + (rr[0] & 7) * 16),
                                 static_cast<uint32_t>((rr[1] >> 3) * 128 + (rr[1] & 7) * 16)};
       const uint32_t K16 = g.k16, K65536 = g.k65536;
-      for (int t = 0; t < ntiles; ++t) {
-        const int T = T0 + t, s = T % kNSB;
+      // the 32 sketch entries of each (row q, group gi) stream of tile t: Philox4x32-10 words
+      auto philox = [&](int t, uint32_t (&c0)[4], uint32_t (&c1)[4], uint32_t (&c2)[4], uint32_t (&c3)[4]) {
         // group parts (uniform): rounds 1-3
         const uint32_t g0 = static_cast<uint32_t>((row_begin + (range + int64_t(t) * g.nranges) * kKT) >> 5);
         uint32_t G2[2], G3k[2], G5k[2], G5l[2];
@@ -549,8 +549,6 @@ k1f_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, const __grid_con
           G5k[gi] = h3 ^ keys.k1[2];
           G5l[gi] = l3;
         }
-        // 2 NROW streams: (row q, group gi)
-        uint32_t c0[4], c1[4], c2[4], c3[4];
 #pragma unroll
         for (int q = 0; q < NROW; ++q)
 #pragma unroll
@@ -576,19 +574,24 @@ k1f_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, const __grid_con
             c0[ci] = n0; c1[ci] = lo1; c2[ci] = n2; c3[ci] = lo0;
           }
         }
-        // the Philox rounds above run before the wait (an ordered volatile asm that reads their
-        // results; the compiler would otherwise hoist the wait above the register-only arithmetic)
-#pragma unroll
-        for (int ci = 0; ci < 2 * NROW; ++ci) asm volatile("" ::"r"(c0[ci]), "r"(c1[ci]), "r"(c2[ci]), "r"(c3[ci]));
+      };
+      // software pipeline: the Philox rounds of tile t + 1 (FMA-heavy pipe) and the Gauss-16 decode
+      // and stores of tile t (ALU pipe) are independent code in one block, so they interleave
+      uint32_t a0[4], a1[4], a2[4], a3[4];
+      philox(0, a0, a1, a2, a3);
+      for (int t = 0; t < ntiles; ++t) {
+        const int T = T0 + t, s = T % kNSB;
         if (T >= kNSB) {
           if (lane == 0) k1tc::mbar_wait(&sh.b_empty[s], ((T / kNSB) - 1) & 1);
           __syncwarp();
         }
+        uint32_t n0[4], n1[4], n2[4], n3[4];
+        philox(t + 1, n0, n1, n2, n3);             // (past the last tile: unused)
         uint8_t* bs = bbuf + s * g.b_bytes;
 #pragma unroll
         for (int ci = 0; ci < 2 * NROW; ++ci) {
           const int q = ci >> 1, gi = ci & 1;
-          const uint32_t ws[4] = {c0[ci], c1[ci], c2[ci], c3[ci]};
+          const uint32_t ws[4] = {a0[ci], a1[ci], a2[ci], a3[ci]};
           uint32_t pk[8];
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
@@ -608,6 +611,8 @@ k1f_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, const __grid_con
         k1tc::fence_proxy_async();
         __syncwarp();
         if (lane == 0) k1tc::mbar_arrive(&sh.b_full[s]);
+#pragma unroll
+        for (int ci = 0; ci < 4; ++ci) { a0[ci] = n0[ci]; a1[ci] = n1[ci]; a2[ci] = n2[ci]; a3[ci] = n3[ci]; }
       }
     }
     // ---- end of pass: everyone learns whether the unit runs again
