@@ -74,7 +74,7 @@ struct Geom {
   int brows;         // rows of a B stage (256 or 512; rows past nu are generated and ignored)
   // multipliers passed at run time so that ptxas keeps them as IMAD / IMAD.HI (FMA pipe)
   // instead of strength-reducing them to ALU shifts (the pipes are balanced by hand)
-  uint32_t k16, k65536, k2p31;
+  uint32_t k2, k16, k256, k2048, k65536, k2p31;
   int nunits() const { return nranges * ncg * nsg; }
 };
 
@@ -91,7 +91,7 @@ inline Geom make_geom(int ell, int ncols, int64_t m_loc, bool f64, int num_sms) 
   g.x_bytes = 32 * g.xline;
   g.brows = g.nu > 256 ? 512 : 256;
   g.b_bytes = g.brows * kKT;
-  g.k16 = 16; g.k65536 = 65536; g.k2p31 = 0x80000000u;
+  g.k2 = 2; g.k16 = 16; g.k256 = 256; g.k2048 = 2048; g.k65536 = 65536; g.k2p31 = 0x80000000u;
   g.smem = 1024 + kNSX * g.x_bytes + kNSA * (128 * kKT) + kNSB * g.b_bytes;
   return g;
 }
@@ -287,7 +287,7 @@ k1f_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, const __grid_con
       int nq[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};   // digit-pair sums D_pq = sum_i d_p d_q, p <= q
       double csf = 0.0, nrf = 0.0;
       bool first_drain = true;
-      const uint32_t K2p31 = g.k2p31;
+      const uint32_t K2p31 = g.k2p31, K2 = g.k2, K256 = g.k256, K2048 = g.k2048;
 
       // int32 digit sums of the closing epoch -> fp64, with that epoch's F = kFbase - C
       auto flush = [&](int Cep) {
@@ -381,7 +381,9 @@ k1f_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, const __grid_con
         int emax = 0;
 #pragma unroll
         for (int e = 0; e < kSlE; ++e) {
-          Ee[e] = static_cast<int>((hi[e] << 1) >> (kF64 ? 21 : 24));   // ALU shifts
+          // E = (bits << 1) >> 21 (f64) / >> 24 (f32) on the FMA pipe (IMAD, IMAD.HI): the ALU pipe
+          // carries the generator's decode
+          Ee[e] = static_cast<int>(madhi(mullo(hi[e], K2), kF64 ? K2048 : K256, 0u));
           emax = max(emax, Ee[e]);
         }
         obs = max(obs, emax);
@@ -430,8 +432,8 @@ k1f_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, const __grid_con
           }
           const uint32_t u = madhi(tt, p, 1u);                     // (t >> (k - 1)) + 1
           const int v = static_cast<int>(madhi(u, K2p31, 0u));     // round half up of t / 2^k
-          const int sgn = static_cast<int>(hi[e]) >> 31;           // 0 or -1
-          w[e] = static_cast<uint32_t>(madlo_s(v, 2 * sgn + 1, 0x808080));
+          const int sgn = madlo_s(mulhi_s(static_cast<int>(hi[e]), 2), 2, 1);   // -1 or +1 (FMA pipe)
+          w[e] = static_cast<uint32_t>(madlo_s(v, sgn, 0x808080));
         }
         // the stage is released only once its values have been consumed (the loads' results are
         // in registers): an arrive right after issuing the loads let the next TMA load overwrite
@@ -577,21 +579,20 @@ k1f_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, const __grid_con
       };
       // software pipeline: the Philox rounds of tile t + 1 (FMA-heavy pipe) and the Gauss-16 decode
       // and stores of tile t (ALU pipe) are independent code in one block, so they interleave
-      uint32_t a0[4], a1[4], a2[4], a3[4];
-      philox(0, a0, a1, a2, a3);
-      for (int t = 0; t < ntiles; ++t) {
+      // one tile: wait for the stage, Philox of tile t + 1 into (n*), decode and store (c*) of tile t
+      auto tile = [&](int t, const uint32_t (&c0)[4], const uint32_t (&c1)[4], const uint32_t (&c2)[4],
+                      const uint32_t (&c3)[4], uint32_t (&n0)[4], uint32_t (&n1)[4], uint32_t (&n2)[4], uint32_t (&n3)[4]) {
         const int T = T0 + t, s = T % kNSB;
         if (T >= kNSB) {
           if (lane == 0) k1tc::mbar_wait(&sh.b_empty[s], ((T / kNSB) - 1) & 1);
           __syncwarp();
         }
-        uint32_t n0[4], n1[4], n2[4], n3[4];
         philox(t + 1, n0, n1, n2, n3);             // (past the last tile: unused)
         uint8_t* bs = bbuf + s * g.b_bytes;
 #pragma unroll
         for (int ci = 0; ci < 2 * NROW; ++ci) {
           const int q = ci >> 1, gi = ci & 1;
-          const uint32_t ws[4] = {a0[ci], a1[ci], a2[ci], a3[ci]};
+          const uint32_t ws[4] = {c0[ci], c1[ci], c2[ci], c3[ci]};
           uint32_t pk[8];
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
@@ -611,9 +612,18 @@ k1f_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, const __grid_con
         k1tc::fence_proxy_async();
         __syncwarp();
         if (lane == 0) k1tc::mbar_arrive(&sh.b_full[s]);
-#pragma unroll
-        for (int ci = 0; ci < 4; ++ci) { a0[ci] = n0[ci]; a1[ci] = n1[ci]; a2[ci] = n2[ci]; a3[ci] = n3[ci]; }
+      };
+      // software pipeline over ping-pong register buffers (no copies between tiles): the Philox
+      // rounds of tile t + 1 (FMA-heavy pipe) and the decode / stores of tile t (ALU pipe) are
+      // independent code in one block, so they interleave
+      uint32_t a0[4], a1[4], a2[4], a3[4], b0[4], b1[4], b2[4], b3[4];
+      philox(0, a0, a1, a2, a3);
+      int t = 0;
+      for (; t + 1 < ntiles; t += 2) {
+        tile(t, a0, a1, a2, a3, b0, b1, b2, b3);
+        tile(t + 1, b0, b1, b2, b3, a0, a1, a2, a3);
       }
+      if (t < ntiles) tile(t, a0, a1, a2, a3, b0, b1, b2, b3);
     }
     // ---- end of pass: everyone learns whether the unit runs again
     k1tc::tc_fence_before();
