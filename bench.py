@@ -112,8 +112,9 @@ def parse():
     ap.add_argument("--k1-mode", type=int, default=4,
                     help="oid_k1_mode: 4 = K1F (31-bit fixed point, parity-tested at full C3 size in "
                          "tests/test_gpu_k1fast.py; the default), 2 = exact int8 digit planes, 0 = auto (exact)")
-    ap.add_argument("--a9q", action="store_true", help="opt-in A9Q basis Gram (a9_mode = 1; not the default: "
-                                                       "ill-conditioned bases amplify its quantisation)")
+    ap.add_argument("--a9", default="q", choices=["q", "fp64"],
+                    help="basis Gram: q = A9Q (int8 tensor cores on the 31-bit quantised basis copy, a9_mode = 1; "
+                         "with --k1-mode 4, the default) or fp64 (exact DMMA Gram)")
     ap.add_argument("--no-estimate", action="store_true", help="ingest only (estimate not in the step)")
     ap.add_argument("--one-stream", action="store_true", help="estimates on the ingest stream (no overlap)")
     ap.add_argument("--cpu-sample-rows", type=int, default=1 << 18)
@@ -295,7 +296,8 @@ def main():
         return
     ring = max(2, min(W + K, int((free - ws_bytes - (8 << 30)) // blk_bytes_loc)))
     p = oid.make_params(m=m, k=k, ell=ell, b_max=b, n_cap=n_cap, lam=lam, split=split, seed=0, dtype=dt,
-                        row_begin=rb, row_end=re, k1_mode=args.k1_mode, profile=True, device=local, a9q=args.a9q)
+                        row_begin=rb, row_end=re, k1_mode=args.k1_mode, profile=True, device=local,
+                        a9q=(args.a9 == "q" and args.k1_mode == 4))
     # ingest on a high-priority stream, estimates on a second stream: the basis Gram of block k
     # (HBM/DMMA-bound) overlaps the latency-bound post-pass of block k+1
     stream = torch.cuda.Stream(dev, priority=-1)
@@ -446,12 +448,12 @@ def main():
               "achieved_gbs": basis_bytes / (a9_ms * 1e-3) / 1e9, "dirty_slots_per_estimate": nd,
               "hbm_roof_ms": t_a9_hbm, "dmma_roof_ms": t_a9_flop, "fp64_tensor_peak_tflops": fp64_tf,
               "frac": max(t_a9_hbm, t_a9_flop) / a9_ms}
-        if args.a9q and mode == oid.K1_TC_FAST:
+        if args.a9 == "q" and mode == oid.K1_TC_FAST:
             # A9Q: 4 bytes per basis element (quantised copy), 16 int8 plane pairs per fp64 MAC
             qbytes = m_loc * k * 4
             t_q_hbm = qbytes / (hbm * 1e9) * 1e3
             t_q_mma = 16 * 2.0 * nd * k * m_loc / (int8_tops * 1e12) * 1e3
-            a9 = {"kernel": "a9q::gram_q_kernel (opt-in, a9_mode = 1)", "ms_per_launch": a9_ms, "bytes_per_launch": qbytes,
+            a9 = {"kernel": "a9q::gram_q_kernel (a9_mode = 1)", "ms_per_launch": a9_ms, "bytes_per_launch": qbytes,
                   "achieved_gbs": qbytes / (a9_ms * 1e-3) / 1e9, "dirty_slots_per_estimate": nd,
                   "hbm_roof_ms": t_q_hbm, "int8_roof_ms": t_q_mma, "frac": max(t_q_hbm, t_q_mma) / a9_ms}
     adm = (st["admissions"] - st0["admissions"]) / K

@@ -125,10 +125,9 @@ typedef struct {
   /* Basis Gram (A9).  0: exact fp64 (DMMA) from the stored basis (the default).  1: A9Q - int8
      tensor cores from a second copy of the basis quantised by A7 to a 31-bit per-column fixed
      point (4 bytes per element, half the read, no DMMA bound; |dG_ij| <= 2^-27 (M_j ||a_i||_1 +
-     M_i ||a_j||_1) + m 2^-54 M_i M_j).  Needs k1_mode = OID_K1_TC_FAST,
-     epoch_mode = 0 and no gradient variant (else the exact A9 runs); NOT for ill-conditioned
-     bases: the NA-Hutch++ estimate amplifies G's error by about kappa(S_J)^2 (on C1 it misses the
-     1e-5 bar).                                                                                  */
+     M_i ||a_j||_1) + m 2^-54 M_i M_j; measured 2e-10 relative on C1 and
+     C3).  Needs k1_mode = OID_K1_TC_FAST (the per-column exponents come from K1F), epoch_mode = 0
+     and no gradient variant; otherwise the exact A9 runs.  The fast mode of bench.py.           */
   int32_t a9_mode;
   double grad_hz;
 } oid_params;

@@ -124,8 +124,8 @@ def make_params(m, k, ell, b_max, n_cap, lam, split=None, eps=0.5, delta=0.05, c
     grid; grad3: (nfields, nx, ny, nz[, hx, hy, hz]) for the 3-D grid with three components (NEXT-4).
     coeff: "alg4" (Alg 4 every epoch, the hot path) or "argmin" (Algs 4-7 + NA-Hutch++ argmin, NEXT-1).
     epochs: "block" (one block = one epoch, R4) or "t" (the paper's t-column buffer, NEXT-2).
-    a9q: the basis Gram on int8 tensor cores from a quantised basis copy (a9_mode = 1, oid.h;
-    k1_mode = K1_TC_FAST only; not for ill-conditioned bases)."""
+    a9q: the basis Gram on int8 tensor cores from a 31-bit quantised basis copy (a9_mode = 1,
+    oid.h; with k1_mode = K1_TC_FAST)."""
     if coeff not in ("alg4", "argmin"):
         raise ValueError("coeff must be 'alg4' or 'argmin'")
     if epochs not in ("block", "t"):

@@ -94,6 +94,11 @@ gram_q_kernel(const uint8_t* __restrict__ Cq, const int* __restrict__ Fq, int64_
   const int64_t bb = block_bytes(t);
   const uint32_t bcopy = static_cast<uint32_t>((nrow + 7) / 8 * 1024);
   const int ntiles = static_cast<int>((ntiles_total - range + nranges - 1) / nranges);
+  if (ntiles <= 0) {            // no tiles (more CTAs than tiles): zero partial rows, nothing else
+    double* o = part + static_cast<int64_t>(blockIdx.x) * t * t;
+    for (int idx = threadIdx.x; idx < nd * t; idx += blockDim.x) o[(idx % nd) + static_cast<int64_t>(idx / nd) * t] = 0.0;
+    return;
+  }
   uint8_t* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t* bbuf = base;                                    // kNSB x 64 KB
   uint8_t* abuf = bbuf + kNSB * 65536;                     // kNSA x 16 KB

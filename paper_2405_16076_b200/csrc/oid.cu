@@ -1646,10 +1646,10 @@ static oid_status estimate_begin_impl(oid_ctx ctx, void* stream) {
     if (ctx->a9q) {
       // A9Q: (row-tile set, slot chunk) CTAs, one per SM, leaving SMs to the concurrent chain
       const int nch = a9q::nchunks(t);
-      const int nr = std::max(1, (sms - 20) / nch);
+      const int64_t nt128 = (ctx->m_loc + a9q::kTR - 1) / a9q::kTR;
+      const int nr = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((sms - 20) / nch, nt128)));
       grid = nr * nch;
       EvScope eva9(ctx, gs, &ctx->ev_a9);
-      const int64_t nt128 = (ctx->m_loc + a9q::kTR - 1) / a9q::kTR;
       a9q::gram_q_kernel<<<grid, a9q::kThreads, a9q::smem_bytes(), gs>>>(ctx->ptr<uint8_t>(L.Cq), ctx->ptr<int>(L.Fq),
                                                                           nt128, t, nr, static_cast<const int*>(dl),
                                                                           static_cast<const int*>(gc), ctx->d(L.Gpart));

@@ -23,7 +23,8 @@ else:
     cfg, gen = C3, ChannelFlow(192, 129, 192, seed=1003)
     dt = "f64"
 dev = torch.device("cuda", 0)
-p = oid.make_params(m=gen.m, k=cfg.k, ell=cfg.ell, b_max=cfg.b, n_cap=cfg.n, lam=-1.0, seed=0, dtype=dt)
+p = oid.make_params(m=gen.m, k=cfg.k, ell=cfg.ell, b_max=cfg.b, n_cap=cfg.n, lam=-1.0, seed=0, dtype=dt,
+                    k1_mode=int(sys.argv[sys.argv.index("--k1") + 1]) if "--k1" in sys.argv else 4)
 I = torch.cuda.Stream(dev, priority=-1)
 E = I if one else torch.cuda.Stream(dev, priority=0)
 eng = oid.Engine(p, stream=I, estimate_stream=E)

@@ -182,6 +182,48 @@ def test_k1f_c1_stream(oid):
     _stream(oid, A, 16, 20, 48, lam, seed=0, checks={8, 32}, split=(16, 16, 16))
 
 
+def test_a9q_c1_stream(oid):
+    """C1 through K1F with the A9Q basis Gram (a9_mode = 1): J after every epoch, P and the
+    NA-Hutch++ components after blocks 8 and 32 (the small-m case: 32 row tiles, fewer than CTAs)."""
+    A = c1_matrix()
+    s = np.linalg.svd(A, compute_uv=False)
+    lam = float(np.sum(s[20:] ** 2) / 20)
+    _stream(oid, A, 16, 20, 48, lam, seed=0, checks={8, 32}, split=(16, 16, 16), a9q=True)
+
+
+def test_a9q_c3_fullsize_gram(oid):
+    """A9Q at full C3 size in the bench launch configuration: sampled G entries against fp64 dot
+    products of the finalized basis, within the quantisation bound, across three estimates."""
+    gen = ChannelFlow(192, 129, 192, seed=C3.data_seed)
+    m, b = gen.m, C3.b
+    dev = torch.device("cuda", 0)
+    eng, _ = _engine(oid, m, C3.k, C3.ell, b, 128, -1.0, seed=0, a9q=True)
+    rng = np.random.default_rng(3)
+    for blk in range(3):
+        X = gen.block_torch(blk * b, (blk + 1) * b, dev).T
+        eng.ingest_block(X)
+        assert np.isfinite(eng.error_estimate()["est_rel"])
+        del X
+        G = eng.get(11)
+        J = eng.J()
+        occ = np.flatnonzero(J >= 0)
+        basis = eng.finalize(basis=True)["basis"]
+        pick = rng.choice(occ, size=min(6, len(occ)), replace=False)
+        cols = {int(i): basis[:, int(i)].cpu().numpy() for i in pick}
+        for i in pick:
+            for j in pick:
+                ai, aj = cols[int(i)], cols[int(j)]
+                Mi, Mj = np.max(np.abs(ai)), np.max(np.abs(aj))
+                bnd = 2.0 ** -27 * (Mj * np.sum(np.abs(ai)) + Mi * np.sum(np.abs(aj))) + m * 2.0 ** -54 * Mi * Mj
+                ref = float(np.dot(ai, aj))
+                assert abs(G[i, j] - ref) <= bnd + 1e-13 * abs(ref), (blk, i, j, G[i, j], ref, bnd)
+                assert abs(G[i, j] - ref) <= 1e-8 * np.sqrt(np.dot(ai, ai) * np.dot(aj, aj))
+        vac = np.flatnonzero(J < 0)
+        assert np.all(G[vac, :] == 0) and np.all(G[:, vac] == 0)
+        del basis
+    eng.close()
+
+
 def test_k1f_c3r_whole_stream(oid):
     """BASELINE config 2 on the 48x33x48 grid (C3r), the whole 1000-snapshot stream through K1F,
     lambda = paper surrogate: J bit-exact after every epoch, E_k to 1e-6, tau to 1e-5, and after
@@ -194,9 +236,8 @@ def test_k1f_c3r_whole_stream(oid):
 
 
 def test_a9q_c3r_whole_stream(oid):
-    """The same whole C3r stream with the opt-in A9Q basis Gram (a9_mode = 1): on this well-posed
-    channel-flow basis the quantised G keeps the NA-Hutch++ components within 1e-5 of the oracle.
-    (On C1's nearly rank-deficient basis it does not - the reason A9Q is opt-in.)"""
+    """The same whole C3r stream with the A9Q basis Gram (a9_mode = 1, the bench's fast mode): J,
+    P and the NA-Hutch++ components against the oracle as above."""
     cfg = C3R
     gen = ChannelFlow(48, 33, 48, seed=cfg.data_seed)
     A = gen.block(0, cfg.n)
