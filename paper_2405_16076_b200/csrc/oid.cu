@@ -413,6 +413,7 @@ struct oid_ctx_s {
   bool use_side = true;       // diagnostics: OID_NO_SIDE=1 runs everything on the caller's stream
   int k1_free_sms = 0;        // SMs the persistent K1 grid leaves to concurrent streams (OID_K1_FREE)
   bool a9q = false;           // A9 on the quantised basis (K1F mode; off for good once a block skips K1F)
+  bool a9q_serial = false;    // K1 waits for the last A9Q (diagnostics: OID_A9Q_SERIAL=1)
   int last_nc = 0;            // columns of the last committed epoch (NEXT-1's P_prev extension)
   int dcount = 0;             // NEXT-2: columns buffered in D since the last epoch
   int64_t dbase = 0;          //         global index of D's first column
@@ -746,6 +747,9 @@ oid_status sketch_one(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream
 oid_status do_sketch(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_t st) {
   const oid_params& p = ctx->p;
   const Layout& L = ctx->L;
+  // diagnostics (OID_A9Q_SERIAL=1): K1 waits for the last A9Q instead of sharing the SMs with it
+  // (measured: 482 vs 513 GB/s on C3, the overlap wins although each kernel stretches)
+  if (ctx->a9q && ctx->a9q_serial && ctx->use_side) CK(cudaStreamWaitEvent(st, ctx->ev_gram_done, 0));
   oid_status s = sketch_one(ctx, X, ld, nc, st, ctx->d(L.Ypart), p.dtype == OID_F64, true, true);
   if (s != OID_OK || ctx->ga == 1) return s;
   // gradient variant (A11): G^p X by the axis-neighbour stencils, then K1 on each
@@ -1505,6 +1509,7 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
     if ((e = cudaMemsetAsync(ctx->ws + L.C, 0, cb, st)) != cudaSuccess) return bad(e);
   }
   ctx->a9q = a9q_wanted(*p) && ctx->tc_ok;
+  ctx->a9q_serial = getenv("OID_A9Q_SERIAL") && atoi(getenv("OID_A9Q_SERIAL")) != 0;
   if (a9q_wanted(*p)) {
     if ((e = cudaMemsetAsync(ctx->ws + L.Cq, 0, a9q::qbasis_bytes(ctx->m_loc, ctx->t), st)) != cudaSuccess) return bad(e);
     if ((e = cudaMemsetAsync(ctx->ws + L.Fq, 0, sizeof(int) * ctx->t, st)) != cudaSuccess) return bad(e);

@@ -24,7 +24,8 @@ else:
     dt = "f64"
 dev = torch.device("cuda", 0)
 p = oid.make_params(m=gen.m, k=cfg.k, ell=cfg.ell, b_max=cfg.b, n_cap=cfg.n, lam=-1.0, seed=0, dtype=dt,
-                    k1_mode=int(sys.argv[sys.argv.index("--k1") + 1]) if "--k1" in sys.argv else 4)
+                    k1_mode=int(sys.argv[sys.argv.index("--k1") + 1]) if "--k1" in sys.argv else 4,
+                    a9q="--a9fp64" not in sys.argv)
 I = torch.cuda.Stream(dev, priority=-1)
 E = I if one else torch.cuda.Stream(dev, priority=0)
 eng = oid.Engine(p, stream=I, estimate_stream=E)
