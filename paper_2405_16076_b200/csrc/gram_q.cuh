@@ -275,7 +275,10 @@ gram_q_kernel(const uint8_t* __restrict__ Cq, const int* __restrict__ Fq, int64_
 template <typename T>
 __global__ void basis_quant_kernel(const T* __restrict__ X, int64_t ld, uint8_t* __restrict__ Cq, int* __restrict__ Fq,
                                    int64_t m_loc, int t, const int* __restrict__ admit, const int* __restrict__ counts,
-                                   int nc, const int* __restrict__ gE, int nunits, int nsg) {
+                                   int nc, const int* __restrict__ gE, int nunits, int nsg, T* __restrict__ Cb) {
+  // A7 fused: every admitted column is read once and written twice - bit-exactly into the row-tiled
+  // fp64 / fp32 basis (lines of RL rows) and as the quantised planes
+  constexpr int RL = 128 / sizeof(T);
   constexpr bool kF64 = sizeof(T) == 8;
   constexpr int kFbase = kF64 ? 1021 : 125;
   const int na = counts[0], nz = counts[1];
@@ -303,21 +306,61 @@ __global__ void basis_quant_kernel(const T* __restrict__ X, int64_t ld, uint8_t*
     __syncthreads();                                         // s_em is rewritten for the next admission
     const int C = em - 30;                                   // |v| <= 2^29 for the largest element
     if (blockIdx.x == 0 && threadIdx.x == 0) Fq[slot] = r >= 0 ? kFbase - C : 0;
-    for (int64_t ch = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; ch < nchunk16;
-         ch += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    // a warp takes 512 consecutive rows (32 runs of 16): coalesced 16-byte loads into its shared
+    // buffer, each lane then converts its own run; the exact copy goes out 8 lanes per basis line
+    __shared__ uint4 s_x[8][32 * (16 * static_cast<int>(sizeof(T)) / 16) + 32];   // +1 uint4 pad per run
+    constexpr int kQ = 16 * static_cast<int>(sizeof(T)) / 16;                    // uint4 per run (8 / 4)
+    const int wl = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    uint4* sw = s_x[wl];
+    const int64_t nwork = (nchunk16 + 31) / 32;
+    const int64_t wstride = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t wk = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wl; wk < nwork; wk += wstride) {
+      const int64_t ch = wk * 32 + ln;                   // this lane's run
+      const int64_t base_row = wk * 512;
+      // coalesced load of the warp's 512 rows (zeros past m_loc and for vacated slots)
+      const T* col = r >= 0 ? X + static_cast<int64_t>(r) * ld : nullptr;
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) {
+        const int u = q * 32 + ln;                       // uint4 index within the warp's rows
+        const int64_t row = base_row + static_cast<int64_t>(u) * (16 / static_cast<int>(sizeof(T)));
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (col && row + (16 / static_cast<int>(sizeof(T))) <= m_loc) v = __ldg(reinterpret_cast<const uint4*>(col + row));
+        else if (col && row < m_loc) {
+          T tmp[16 / sizeof(T)];
+#pragma unroll
+          for (int e = 0; e < static_cast<int>(16 / sizeof(T)); ++e) tmp[e] = row + e < m_loc ? col[row + e] : T(0);
+          v = *reinterpret_cast<uint4*>(tmp);
+        }
+        sw[(u / kQ) * (kQ + 1) + (u % kQ)] = v;          // run u / kQ, padded
+      }
+      __syncwarp();
+      // exact copy: a run of 16 rows is one 128-byte basis line (f64, 8 lanes per line) or
+      // half of one (f32, 4 lanes)
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) {
+        const int u = q * 32 + ln;
+        const int run = u / kQ, part = u % kQ;
+        const int64_t i0r = base_row + static_cast<int64_t>(run) * 16;
+        if (i0r < m_loc) {
+          T* dst = Cb + ((i0r / RL) * t + slot) * RL + (i0r % RL);
+          __stcs(reinterpret_cast<uint4*>(dst) + part, sw[run * (kQ + 1) + part]);
+        }
+      }
+      const bool valid = ch < nchunk16;
       const int64_t i0 = ch * 16;
+      T xv[16];
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) reinterpret_cast<uint4*>(xv)[q] = sw[ln * (kQ + 1) + q];
+      __syncwarp();                                       // the buffer is reused by the next run set
       uint32_t w[16];
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
-        const int64_t i = i0 + e;
-        uint32_t hi = 0u, lo = 0u;
-        if (r >= 0 && i < m_loc) {
-          if constexpr (kF64) {
-            const uint64_t b = __double_as_longlong(X[static_cast<int64_t>(r) * ld + i]);
-            hi = static_cast<uint32_t>(b >> 32); lo = static_cast<uint32_t>(b);
-          } else {
-            hi = __float_as_uint(X[static_cast<int64_t>(r) * ld + i]);
-          }
+        uint32_t hi, lo;
+        if constexpr (kF64) {
+          const uint64_t bb2 = __double_as_longlong(xv[e]);
+          hi = static_cast<uint32_t>(bb2 >> 32); lo = static_cast<uint32_t>(bb2);
+        } else {
+          hi = __float_as_uint(xv[e]); lo = 0u;
         }
         const int E = static_cast<int>((hi << 1) >> (kF64 ? 21 : 24));
         const uint32_t pw = (E - C) < 0 || (E - C) > 31 ? 0u : (1u << (E - C));   // 2^(33 - k)
@@ -341,9 +384,11 @@ __global__ void basis_quant_kernel(const T* __restrict__ X, int64_t ld, uint8_t*
       const int64_t tile = i0 / kTR;
       const int c = static_cast<int>((i0 % kTR) / 16);
       uint8_t* blk = Cq + tile * bb;
+      if (valid) {
 #pragma unroll
-      for (int p = 0; p < 4; ++p)
-        *reinterpret_cast<uint4*>(blk + swz(4 * slot + p, c)) = make_uint4(P[p][0], P[p][1], P[p][2], P[p][3]);
+        for (int p = 0; p < 4; ++p)
+          *reinterpret_cast<uint4*>(blk + swz(4 * slot + p, c)) = make_uint4(P[p][0], P[p][1], P[p][2], P[p][3]);
+      }
     }
   }
 }

@@ -927,26 +927,29 @@ oid_status post_epoch(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream
   tl_mark(ctx, st, 5);
   {
     dim3 grid(std::max(1u, std::min(blocks_for(ctx->m_loc), static_cast<unsigned>(8 * ctx->num_sms))));
-    if (p.dtype == OID_F64)
-      basis_copy_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(X), ld, ctx->ptr<double>(L.C), ctx->m_loc,
-                                                      ctx->ptr<int>(L.admit), ctx->ptr<int>(L.counts), nc, t);
-    else
-      basis_copy_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(X), ld, ctx->ptr<float>(L.C), ctx->m_loc,
-                                                     ctx->ptr<int>(L.admit), ctx->ptr<int>(L.counts), nc, t);
-    CKL();
     if (ctx->a9q && ctx->k1_mode_used != OID_K1_TC_FAST) ctx->a9q = false;   // no exponents for this block
-    if (ctx->a9q) {
+    if (!ctx->a9q) {
+      if (p.dtype == OID_F64)
+        basis_copy_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(X), ld, ctx->ptr<double>(L.C), ctx->m_loc,
+                                                        ctx->ptr<int>(L.admit), ctx->ptr<int>(L.counts), nc, t);
+      else
+        basis_copy_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(X), ld, ctx->ptr<float>(L.C), ctx->m_loc,
+                                                       ctx->ptr<int>(L.admit), ctx->ptr<int>(L.counts), nc, t);
+      CKL();
+    } else {
+      // A7 + the quantised copy in one pass over the admitted columns (a9q::basis_quant_kernel)
+      grid = dim3(std::max(1u, std::min(static_cast<unsigned>((ctx->m_loc + 4095) / 4096), static_cast<unsigned>(8 * ctx->num_sms))));
       const k1f::Geom kg = k1f::make_geom(p.ell, nc, ctx->m_loc, p.dtype == OID_F64, std::max(2, ctx->num_sms - ctx->k1_free_sms));
       if (p.dtype == OID_F64)
         a9q::basis_quant_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(X), ld, ctx->ptr<uint8_t>(L.Cq),
                                                              ctx->ptr<int>(L.Fq), ctx->m_loc, t, ctx->ptr<int>(L.admit),
                                                              ctx->ptr<int>(L.counts), nc, ctx->ptr<int>(L.k1g), kg.nunits(),
-                                                             kg.nsg);
+                                                             kg.nsg, ctx->ptr<double>(L.C));
       else
         a9q::basis_quant_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(X), ld, ctx->ptr<uint8_t>(L.Cq),
                                                             ctx->ptr<int>(L.Fq), ctx->m_loc, t, ctx->ptr<int>(L.admit),
                                                             ctx->ptr<int>(L.counts), nc, ctx->ptr<int>(L.k1g), kg.nunits(),
-                                                            kg.nsg);
+                                                            kg.nsg, ctx->ptr<float>(L.C));
       CKL();
     }
   }

@@ -296,6 +296,9 @@ def test_a9q_gram_bound(oid):
         J = eng.J()
         occ = np.flatnonzero(J >= 0)
         basis = eng.finalize(basis=True)["basis"].cpu().numpy()
+        # A7 fused with the quantised copy: the basis still holds the admitted columns bit-exactly
+        assert np.array_equal(basis[:, occ], A[:, J[occ]]), blk
+        assert np.all(basis[:, J < 0] == 0)
         pick = rng.choice(occ, size=min(12, len(occ)), replace=False)
         for i in pick:
             for j in pick:
