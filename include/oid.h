@@ -280,6 +280,8 @@ oid_status oid_sketch_table(int32_t q[16], double* scale);
                         256 no MMA, 512 no TMA) - results are WRONG with any bit set
      OID_K1_FREE=n      SMs the persistent K1 grid leaves free (default 0)
      OID_A9Q_SERIAL=1   K1 waits for the previous A9Q instead of sharing the SMs with it
+     OID_A9_DEFER=0     single-shard contexts launch an estimate's basis Gram in oid_estimate_begin
+                        (default: after the next block's K1, or when anything needs it)
      OID_TIMELINE=1     per-stream timeline marks (oid_get field 13)
      OID_NO_SIDE=1      run every kernel on the caller's stream (race check of the event graph)
      OID_JACOBI_COLD=1  A4/A5 always by cold-started Jacobi (reference path for tests)

@@ -414,6 +414,11 @@ struct oid_ctx_s {
   int k1_free_sms = 0;        // SMs the persistent K1 grid leaves to concurrent streams (OID_K1_FREE)
   bool a9q = false;           // A9 on the quantised basis (K1F mode; off for good once a block skips K1F)
   bool a9q_serial = false;    // K1 waits for the last A9Q (diagnostics: OID_A9Q_SERIAL=1)
+  bool a9_defer = false;      // single shard: A9 launched after the next block's K1 (OID_A9_DEFER=0: at once)
+  bool a9_pending = false;    // an estimate's A9 queued but not launched
+  int a9_gp = 0;
+  cudaStream_t a9_gs = nullptr;
+  cudaEvent_t ev_k1_end = nullptr;
   int last_nc = 0;            // columns of the last committed epoch (NEXT-1's P_prev extension)
   int dcount = 0;             // NEXT-2: columns buffered in D since the last epoch
   int64_t dbase = 0;          //         global index of D's first column
@@ -744,6 +749,109 @@ oid_status sketch_one(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream
   return launch_k1_simt<float>(ctx, st, static_cast<const float*>(X), ld, nc, out);
 }
 
+// A9 of the pending estimate: exact basis Gram (or A9Q) of parity ctx->a9_gp on the A9 stream, then
+// the fixed-order sums; records ev_gram_done (the next basis copy waits for it) and ev_gs_done.
+static oid_status launch_a9(oid_ctx ctx) {
+  if (!ctx->a9_pending) return OID_OK;
+  ctx->a9_pending = false;
+  const Layout& L = ctx->L;
+  const int t = ctx->t;
+  const int gp = ctx->a9_gp;
+  cudaStream_t gs = ctx->a9_gs;
+  int* dl = ctx->ptr<int>(L.dlist) + static_cast<size_t>(gp) * t;
+  int* gc = ctx->ptr<int>(L.gcnt) + 4 * gp;
+  double* Gs = ctx->d(L.Gsum) + static_cast<size_t>(gp) * t * t;
+  tl_mark(ctx, gs, 8);
+  // A9: exact basis Gram G = A_J^T A_J (P:468, P:614), incremental: only the rows/columns of
+  // slots admitted since the last estimate are recomputed, over this shard's rows.
+  {
+    const bool f64 = ctx->p.dtype == OID_F64;
+    const int64_t RL = f64 ? 16 : 32;
+    const int64_t ntiles = (ctx->m_loc + RL - 1) / RL;
+    // many short CTAs (waves of num_sms - bg_free_sms): kernels of higher-priority streams (the next
+    // block's K1 and post-pass, the side stream) are scheduled as they retire
+    const int sms = std::max(1, ctx->num_sms - ctx->bg_free_sms);
+    const int cl = ctx->bg_cluster;   // CTAs per cluster (1: plain launch)
+    int want = std::min(gram_tc_chunks(t), sms * ctx->bg_waves);
+    want = std::max(cl, want / cl * cl);
+    int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, (ntiles + 7) / 8)));
+    const int64_t per = (ntiles + grid - 1) / grid;
+    grid = static_cast<int>((ntiles + per - 1) / per);
+    grid = (grid + cl - 1) / cl * cl;   // CTAs past the last tile contribute zero partials
+    const int nbox = (t + 255) / 256;
+    const int stage_bytes = (nbox * std::min(t, 256) * 128 + 1023) / 1024 * 1024;
+    const int nstage = std::max(2, std::min(bgtc::kMaxStages, (ctx->bg_smem_kb * 1024) / stage_bytes));
+    const size_t smem = static_cast<size_t>(nstage) * stage_bytes + 1024;
+    cudaLaunchConfig_t lc = {};
+    cudaLaunchAttribute la[1];
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(32 * (bgtc::kCW + 1));
+    lc.dynamicSmemBytes = smem;
+    lc.stream = gs;
+    if (cl > 1) {
+      la[0].id = cudaLaunchAttributeClusterDimension;
+      la[0].val.clusterDim.x = cl;
+      la[0].val.clusterDim.y = 1;
+      la[0].val.clusterDim.z = 1;
+      lc.attrs = la;
+      lc.numAttrs = 1;
+    }
+    if (ctx->a9q) {
+      // A9Q: (row-tile set, slot chunk) CTAs, one per SM, launched as 16-CTA clusters (at most 7,
+      // so each occupies one GPC and at least one GPC stays free: the A4 tridiagonalisation's
+      // 16-CTA cluster, which runs concurrently, can always be placed)
+      const int nch = a9q::nchunks(t);
+      const int64_t nt128 = (ctx->m_loc + a9q::kTR - 1) / a9q::kTR;
+      int ncl = std::min(7, (sms - 20) / 16);
+      while (ncl > 0 && (16 * ncl) % nch != 0) --ncl;
+      const bool clustered = ncl > 0 && (16 * ncl) / nch <= nt128;
+      const int nr = clustered ? (16 * ncl) / nch
+                               : static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((sms - 20) / nch, nt128)));
+      grid = nr * nch;
+      EvScope eva9(ctx, gs, &ctx->ev_a9);
+      cudaLaunchConfig_t qc = {};
+      cudaLaunchAttribute qa[1];
+      qc.gridDim = dim3(grid);
+      qc.blockDim = dim3(a9q::kThreads);
+      qc.dynamicSmemBytes = a9q::smem_bytes();
+      qc.stream = gs;
+      if (clustered) {
+        qa[0].id = cudaLaunchAttributeClusterDimension;
+        qa[0].val.clusterDim.x = 16;
+        qa[0].val.clusterDim.y = 1;
+        qa[0].val.clusterDim.z = 1;
+        qc.attrs = qa;
+        qc.numAttrs = 1;
+      }
+      CK(cudaLaunchKernelEx(&qc, a9q::gram_q_kernel, static_cast<const uint8_t*>(ctx->ptr<uint8_t>(L.Cq)),
+                            static_cast<const int*>(ctx->ptr<int>(L.Fq)), nt128, t, nr, static_cast<const int*>(dl),
+                            static_cast<const int*>(gc), ctx->d(L.Gpart)));
+      CKL();
+    } else {
+      EvScope eva9(ctx, gs, &ctx->ev_a9);
+      if (f64)
+        CK(cudaLaunchKernelEx(&lc, bgtc::basis_gram_tc_kernel<double>, ctx->bg_map, ntiles, t, per, nstage, stage_bytes,
+                              nbox, static_cast<const int*>(dl), static_cast<const int*>(gc), ctx->d(L.Gpart)));
+      else
+        CK(cudaLaunchKernelEx(&lc, bgtc::basis_gram_tc_kernel<float>, ctx->bg_map, ntiles, t, per, nstage, stage_bytes,
+                              nbox, static_cast<const int*>(dl), static_cast<const int*>(gc), ctx->d(L.Gpart)));
+      CKL();
+    }
+    CK(cudaEventRecord(ctx->ev_gram_done, gs));
+    tl_mark(ctx, gs, 9);
+    // two-level fixed-order sum: up to 64 segment sums into the tail of Gpart, then one
+    const int nseg = std::min(64, std::max(1, grid / 16));
+    double* seg = ctx->d(L.Gpart) + static_cast<size_t>(grid) * t * t;
+    sum_dirty_chunks_kernel<<<dim3(blocks_for(int64_t(t) * t), nseg), 256, 0, gs>>>(ctx->d(L.Gpart), grid, t, gc, seg);
+    CKL();
+    sum_dirty_chunks_kernel<<<dim3(blocks_for(int64_t(t) * t), 1), 256, 0, gs>>>(seg, nseg, t, gc, Gs);
+    CKL();
+  }
+
+  CK(cudaEventRecord(ctx->ev_gs_done, gs));
+  return OID_OK;
+}
+
 oid_status do_sketch(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_t st) {
   const oid_params& p = ctx->p;
   const Layout& L = ctx->L;
@@ -751,6 +859,7 @@ oid_status do_sketch(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   // (measured: 482 vs 513 GB/s on C3, the overlap wins although each kernel stretches)
   if (ctx->a9q && ctx->a9q_serial && ctx->use_side) CK(cudaStreamWaitEvent(st, ctx->ev_gram_done, 0));
   oid_status s = sketch_one(ctx, X, ld, nc, st, ctx->d(L.Ypart), p.dtype == OID_F64, true, true);
+
   if (s != OID_OK || ctx->ga == 1) return s;
   // gradient variant (A11): G^p X by the axis-neighbour stencils, then K1 on each
   // (same Omega, so the three sketches stack into [Omega a; Omega G^1 a; Omega G^2 a])
@@ -814,11 +923,24 @@ oid_status post_epoch(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream
     CKL();
   }
   int* gate = ctx->ptr<int>(L.gate);
+  // the deferred A9 of the last estimate (estimate_begin) starts once the work before this point is
+  // done, i.e. after this block's K1: queued behind the tridiagonalisation below on the block
+  // scheduler (the cluster kernel on the higher-priority stream is placed first and keeps its 16
+  // SMs; the Gram then takes the rest), so the Gram overlaps the latency-bound A4-A6 chain
+  auto launch_deferred_a9 = [&]() -> oid_status {
+    if (!(ctx->a9_pending && ctx->use_side)) return OID_OK;
+    CK(cudaEventRecord(ctx->ev_k1_end, st));
+    CK(cudaStreamWaitEvent(ctx->a9_gs, ctx->ev_k1_end, 0));
+    return launch_a9(ctx);
+  };
   if (ng <= kTriMaxG && !ctx->cold_jacobi) {
     // tridiagonal fast path (tri.cuh); the eigenvector path below runs only when gate[1] is set
     long long* tdbg = ctx->k1_debug ? ctx->ptr<long long>(L.dbg) + k1p::kDbgRows * k1tc::kDbgTiles : nullptr;
     if (ng <= kTriMaxN) {
       const size_t smem = sizeof(double) * static_cast<size_t>(ng) * tri_rows(ng);
+      // (event before the cluster launch: the Gram becomes ready together with the cluster kernel)
+      s = launch_deferred_a9();
+      if (s != OID_OK) return s;
       tridiag_cluster_kernel<<<kTriCtas, 256, smem, st>>>(ctx->d(L.gram), ng, ng, ctx->d(L.td), ctx->d(L.te), ctx->d(L.Vh),
                                                           tri_ldv(ng), ctx->d(L.tauv), tdbg,
                                                           ctx->d(L.wyT));   // the compact-WY T factors too
@@ -1468,6 +1590,8 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
     const int bgmax = 200 * 1024 + 1024;
     if ((e = cudaFuncSetAttribute(a9q::gram_q_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(a9q::smem_bytes()))) != cudaSuccess) return bad(e);
+    if ((e = cudaFuncSetAttribute(a9q::gram_q_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
+      return bad(e);
     if ((e = cudaFuncSetAttribute(bgtc::basis_gram_tc_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, bgmax)) != cudaSuccess) return bad(e);
     if ((e = cudaFuncSetAttribute(bgtc::basis_gram_tc_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, bgmax)) != cudaSuccess) return bad(e);
     if ((e = cudaFuncSetAttribute(bgtc::basis_gram_tc_kernel<double>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess) return bad(e);
@@ -1513,6 +1637,8 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
   }
   ctx->a9q = a9q_wanted(*p) && ctx->tc_ok;
   ctx->a9q_serial = getenv("OID_A9Q_SERIAL") && atoi(getenv("OID_A9Q_SERIAL")) != 0;
+  ctx->a9_defer = p->row_begin == 0 && p->row_end == p->m && !(getenv("OID_A9_DEFER") && atoi(getenv("OID_A9_DEFER")) == 0);
+  if ((e = cudaEventCreateWithFlags(&ctx->ev_k1_end, cudaEventDisableTiming)) != cudaSuccess) return bad(e);
   if (a9q_wanted(*p)) {
     if ((e = cudaMemsetAsync(ctx->ws + L.Cq, 0, a9q::qbasis_bytes(ctx->m_loc, ctx->t), st)) != cudaSuccess) return bad(e);
     if ((e = cudaMemsetAsync(ctx->ws + L.Fq, 0, sizeof(int) * ctx->t, st)) != cudaSuccess) return bad(e);
@@ -1560,6 +1686,10 @@ oid_status oid_ingest_block(oid_ctx ctx, const void* X, int64_t ld, int32_t ncol
 }
 
 oid_status oid_partials(oid_ctx ctx, int32_t which, double** dev_ptr, int64_t* count) {
+  if (ctx && ctx->a9_pending) {   // a deferred A9 (estimate_begin) is launched before anything reads state
+    oid_status sp = launch_a9(ctx);
+    if (sp != OID_OK) return sp;
+  }
   if (!ctx || !dev_ptr || !count) return OID_EINVAL;
   if (which == 0) {
     *dev_ptr = ctx->d(ctx->L.Ypart);
@@ -1577,6 +1707,8 @@ static oid_status estimate_begin_impl(oid_ctx ctx, void* stream) {
   if (!ctx) return OID_EINVAL;
   if (!ctx->estimate_ready) return ctx->fail(OID_ESTATE, "no block ingested yet");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  oid_status sp = launch_a9(ctx);   // an estimate begun but never ended
+  if (sp != OID_OK) return sp;
   const Layout& L = ctx->L;
   const int t = ctx->t;
   EvScope ev(ctx, st, &ctx->ev_est);
@@ -1616,77 +1748,17 @@ static oid_status estimate_begin_impl(oid_ctx ctx, void* stream) {
   CKL();
   CK(cudaEventRecord(ctx->ev_sj_free[par], cs2));   // S_J, S_J^+ (and kappa) of this parity are free again
   tl_mark(ctx, cs2, 14);
-  tl_mark(ctx, gs, 8);
-  // A9: exact basis Gram G = A_J^T A_J (P:468, P:614), incremental: only the rows/columns of
-  // slots admitted since the last estimate are recomputed, over this shard's rows.
-  {
-    const bool f64 = ctx->p.dtype == OID_F64;
-    const int64_t RL = f64 ? 16 : 32;
-    const int64_t ntiles = (ctx->m_loc + RL - 1) / RL;
-    // many short CTAs (waves of num_sms - bg_free_sms): kernels of higher-priority streams (the next
-    // block's K1 and post-pass, the side stream) are scheduled as they retire
-    const int sms = std::max(1, ctx->num_sms - ctx->bg_free_sms);
-    const int cl = ctx->bg_cluster;   // CTAs per cluster (1: plain launch)
-    int want = std::min(gram_tc_chunks(t), sms * ctx->bg_waves);
-    want = std::max(cl, want / cl * cl);
-    int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, (ntiles + 7) / 8)));
-    const int64_t per = (ntiles + grid - 1) / grid;
-    grid = static_cast<int>((ntiles + per - 1) / per);
-    grid = (grid + cl - 1) / cl * cl;   // CTAs past the last tile contribute zero partials
-    const int nbox = (t + 255) / 256;
-    const int stage_bytes = (nbox * std::min(t, 256) * 128 + 1023) / 1024 * 1024;
-    const int nstage = std::max(2, std::min(bgtc::kMaxStages, (ctx->bg_smem_kb * 1024) / stage_bytes));
-    const size_t smem = static_cast<size_t>(nstage) * stage_bytes + 1024;
-    cudaLaunchConfig_t lc = {};
-    cudaLaunchAttribute la[1];
-    lc.gridDim = dim3(grid);
-    lc.blockDim = dim3(32 * (bgtc::kCW + 1));
-    lc.dynamicSmemBytes = smem;
-    lc.stream = gs;
-    if (cl > 1) {
-      la[0].id = cudaLaunchAttributeClusterDimension;
-      la[0].val.clusterDim.x = cl;
-      la[0].val.clusterDim.y = 1;
-      la[0].val.clusterDim.z = 1;
-      lc.attrs = la;
-      lc.numAttrs = 1;
-    }
-    if (ctx->a9q) {
-      // A9Q: (row-tile set, slot chunk) CTAs, one per SM, leaving SMs to the concurrent chain
-      const int nch = a9q::nchunks(t);
-      const int64_t nt128 = (ctx->m_loc + a9q::kTR - 1) / a9q::kTR;
-      const int nr = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((sms - 20) / nch, nt128)));
-      grid = nr * nch;
-      EvScope eva9(ctx, gs, &ctx->ev_a9);
-      a9q::gram_q_kernel<<<grid, a9q::kThreads, a9q::smem_bytes(), gs>>>(ctx->ptr<uint8_t>(L.Cq), ctx->ptr<int>(L.Fq),
-                                                                          nt128, t, nr, static_cast<const int*>(dl),
-                                                                          static_cast<const int*>(gc), ctx->d(L.Gpart));
-      CKL();
-    } else {
-      EvScope eva9(ctx, gs, &ctx->ev_a9);
-      if (f64)
-        CK(cudaLaunchKernelEx(&lc, bgtc::basis_gram_tc_kernel<double>, ctx->bg_map, ntiles, t, per, nstage, stage_bytes,
-                              nbox, static_cast<const int*>(dl), static_cast<const int*>(gc), ctx->d(L.Gpart)));
-      else
-        CK(cudaLaunchKernelEx(&lc, bgtc::basis_gram_tc_kernel<float>, ctx->bg_map, ntiles, t, per, nstage, stage_bytes,
-                              nbox, static_cast<const int*>(dl), static_cast<const int*>(gc), ctx->d(L.Gpart)));
-      CKL();
-    }
-    CK(cudaEventRecord(ctx->ev_gram_done, gs));
-    tl_mark(ctx, gs, 9);
-    // two-level fixed-order sum: up to 64 segment sums into the tail of Gpart, then one
-    const int nseg = std::min(64, std::max(1, grid / 16));
-    double* seg = ctx->d(L.Gpart) + static_cast<size_t>(grid) * t * t;
-    sum_dirty_chunks_kernel<<<dim3(blocks_for(int64_t(t) * t), nseg), 256, 0, gs>>>(ctx->d(L.Gpart), grid, t, gc, seg);
-    CKL();
-    sum_dirty_chunks_kernel<<<dim3(blocks_for(int64_t(t) * t), 1), 256, 0, gs>>>(seg, nseg, t, gc, Gs);
-    CKL();
-  }
+  // A9 (below, launch_a9) reads what this call has queued on gs; single-shard contexts defer its
+  // launch until the next ingest has launched its K1 (or until anything needs the Gram): the two
+  // full-GPU kernels then run back to back and A9 overlaps the latency-bound post-pass instead
+  ctx->a9_gs = gs;
+  ctx->a9_gp = gp;
+  ctx->a9_pending = true;
+  if (ctx->a9_defer && ctx->use_side) return OID_OK;
+  oid_status sa = launch_a9(ctx);
+  if (sa != OID_OK) return sa;
   // the caller's stream sees the partial sums (the sharded path reduces them on it)
-  if (ctx->use_side) {
-    CK(cudaEventRecord(ctx->ev_gs_done, gs));
-    CK(cudaStreamWaitEvent(st, ctx->ev_gs_done, 0));
-  }
+  if (ctx->use_side) CK(cudaStreamWaitEvent(st, ctx->ev_gs_done, 0));
   return OID_OK;
 }
 
@@ -1694,6 +1766,11 @@ static oid_status estimate_end_impl(oid_ctx ctx, double* out_dev, void* stream) 
   if (!ctx) return OID_EINVAL;
   if (!ctx->estimate_ready) return ctx->fail(OID_ESTATE, "no block ingested yet");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  {
+    oid_status sp = launch_a9(ctx);   // deferred and not yet launched by an ingest
+    if (sp != OID_OK) return sp;
+    if (ctx->use_side) CK(cudaStreamWaitEvent(st, ctx->ev_gs_done, 0));
+  }
   const Layout& L = ctx->L;
   const oid_params& p = ctx->p;
   const int t = ctx->t, l1 = p.ell1, l2 = p.ell2;
@@ -1843,6 +1920,10 @@ oid_status oid_gradient_finalize(oid_ctx ctx, double lo, double hi, double tol, 
 }
 
 oid_status oid_finalize(oid_ctx ctx, int64_t* J_host, double* P, int32_t P_on_device, void* basis_dev, void* stream) {
+  if (ctx && ctx->a9_pending) {   // a deferred A9 (estimate_begin) is launched before anything reads state
+    oid_status sp = launch_a9(ctx);
+    if (sp != OID_OK) return sp;
+  }
   NvtxRange nvtx_range("oid_finalize");
   if (!ctx) return OID_EINVAL;
   if (ctx->pending_nc >= 0) return ctx->fail(OID_ESTATE, "a sketch is pending commit");
@@ -1878,6 +1959,10 @@ oid_status oid_finalize(oid_ctx ctx, int64_t* J_host, double* P, int32_t P_on_de
 }
 
 oid_status oid_get(oid_ctx ctx, int32_t field, void* host_dst, size_t bytes, void* stream) {
+  if (ctx && ctx->a9_pending) {   // a deferred A9 (estimate_begin) is launched before anything reads state
+    oid_status sp = launch_a9(ctx);
+    if (sp != OID_OK) return sp;
+  }
   if (!ctx || !host_dst) return OID_EINVAL;
   const Layout& L = ctx->L;
   const oid_params& p = ctx->p;
@@ -1929,6 +2014,10 @@ oid_status oid_get(oid_ctx ctx, int32_t field, void* host_dst, size_t bytes, voi
 }
 
 oid_status oid_stats(oid_ctx ctx, oid_stats_t* out) {
+  if (ctx && ctx->a9_pending) {   // a deferred A9 (estimate_begin) is launched before anything reads state
+    oid_status sp = launch_a9(ctx);
+    if (sp != OID_OK) return sp;
+  }
   if (!ctx || !out) return OID_EINVAL;
   std::memset(out, 0, sizeof(*out));
   out->n_obs = ctx->n_obs;
@@ -1992,6 +2081,10 @@ oid_status oid_stats(oid_ctx ctx, oid_stats_t* out) {
 }
 
 oid_status oid_report(oid_ctx ctx, char* buf, size_t cap, size_t* needed, void* stream) {
+  if (ctx && ctx->a9_pending) {   // a deferred A9 (estimate_begin) is launched before anything reads state
+    oid_status sp = launch_a9(ctx);
+    if (sp != OID_OK) return sp;
+  }
   if (!ctx) return OID_EINVAL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   CK(cudaStreamSynchronize(st));
@@ -2075,6 +2168,7 @@ void oid_destroy(oid_ctx ctx) {
       cudaStreamDestroy(*sp);
     }
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_k1_end) cudaEventDestroy(ctx->ev_k1_end);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   for (cudaEvent_t ev : {ctx->ev_committed, ctx->ev_gram_done, ctx->ev_sj_j, ctx->ev_est_done, ctx->ev_sj_done[0],
                          ctx->ev_sj_done[1], ctx->ev_sj_free[0], ctx->ev_sj_free[1], ctx->ev_snap_free[0], ctx->ev_snap_free[1],

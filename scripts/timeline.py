@@ -39,9 +39,17 @@ for s in range(start):
 torch.cuda.synchronize()
 eng.get(13)   # drop the warm-up marks
 blocks = blocks[start:]
+pipe = "--pipeline" in sys.argv
 for s in range(steps):
     eng.ingest_block(blocks[s])
-    eng.estimate_begin()
+    if pipe:
+        if s > 0:
+            eng.estimate_end(out)
+        eng.estimate_begin()
+    else:
+        eng.estimate_begin()
+        eng.estimate_end(out)
+if pipe:
     eng.estimate_end(out)
 torch.cuda.synchronize()
 tl = eng.get(13)
