@@ -284,7 +284,10 @@ __global__ void basis_quant_kernel(const T* __restrict__ X, int64_t ld, uint8_t*
   const int na = counts[0], nz = counts[1];
   const int64_t bb = block_bytes(t);
   const int64_t nchunk16 = (m_loc + 15) / 16;
-  for (int a = 0; a < na + nz; ++a) {
+  // one admission (or vacated slot) per blockIdx.y: all columns stream concurrently
+  {
+    const int a = blockIdx.y;
+    if (a >= na + nz) return;
     int slot, r = -1;
     if (a < na) { slot = admit[2 * a]; r = admit[2 * a + 1]; }
     else slot = admit[2 * (nc + t) - 2 - 2 * (a - na)];
@@ -303,7 +306,6 @@ __global__ void basis_quant_kernel(const T* __restrict__ X, int64_t ld, uint8_t*
     }
     __syncthreads();
     const int em = s_em;
-    __syncthreads();                                         // s_em is rewritten for the next admission
     const int C = em - 30;                                   // |v| <= 2^29 for the largest element
     if (blockIdx.x == 0 && threadIdx.x == 0) Fq[slot] = r >= 0 ? kFbase - C : 0;
     // a warp takes 512 consecutive rows (32 runs of 16): coalesced 16-byte loads into its shared

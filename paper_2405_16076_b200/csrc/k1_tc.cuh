@@ -158,6 +158,7 @@ struct Shared {
   int ehist[4][64];
   uint64_t tok[2];
   int egen, qsh;
+  int epi_done;      // epilogue warps finished (4 per accumulation epoch, in epoch order)
   int emax[2][4][2][64];
   double nrm[kSlT];
   double csum[kSlT];
@@ -231,6 +232,7 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
     mbar_init(&sh.tok[1], 1);
     sh.egen = 0;
     sh.qsh = 0;
+    sh.epi_done = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -323,7 +325,16 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
     constexpr int chB = NTOT / 8 * 128;
     const int quarter = warp & 3;                    // TMEM lane quarter this warp may access
     // epilogue of accumulation epoch qe: D (int32, TMEM) -> fp64 partial sums, one group
+    // Epilogues run in epoch order.  Each group drains only the epochs its own tiles open, so it
+    // may skip d_full phases; with the MMA two flushes behind, the parity of epoch qe would match
+    // the completed phase qe - 2 and the drain would read D mid-accumulation.  Waiting for the
+    // epilogue of epoch qe - 1 first (which itself waited for phase qe - 1) makes the parity wait
+    // unambiguous and orders the read-modify-write of `part` after the previous epoch's stores.
     auto epilogue = [&](int qe) {
+      if (lane == 0)
+        while (*reinterpret_cast<volatile int*>(&sh.epi_done) < 4 * qe) __nanosleep(32);
+      __syncwarp();
+      __threadfence_block();
       mbar_wait(&sh.d_full, qe & 1);
       tc_fence_after();
 #pragma unroll
@@ -360,8 +371,12 @@ k1_tc_kernel(const __grid_constant__ CUtensorMap tmap, int ncols, int64_t row_be
         }
       }
       tc_fence_before();
+      __threadfence_block();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sh.d_empty);
+      if (lane == 0) {
+        mbar_arrive(&sh.d_empty);
+        atomicAdd(&sh.epi_done, 1);
+      }
     };
     auto keymax = [&](const uint32_t (&w)[NWH]) -> uint32_t {
       uint32_t km = 0;

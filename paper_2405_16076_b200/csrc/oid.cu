@@ -1060,7 +1060,11 @@ oid_status post_epoch(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream
       CKL();
     } else {
       // A7 + the quantised copy in one pass over the admitted columns (a9q::basis_quant_kernel)
-      grid = dim3(std::max(1u, std::min(static_cast<unsigned>((ctx->m_loc + 4095) / 4096), static_cast<unsigned>(8 * ctx->num_sms))));
+      // x: row blocks of 4096 rows (8 warps x 512), y: one admission or vacated slot each (blocks past
+      // the device-side count exit at once)
+      grid = dim3(std::max(1u, std::min(static_cast<unsigned>((ctx->m_loc + 4095) / 4096),
+                                        static_cast<unsigned>(std::max(1, 8 * ctx->num_sms / std::max(1, nc))))),
+                  static_cast<unsigned>(nc + t));
       const k1f::Geom kg = k1f::make_geom(p.ell, nc, ctx->m_loc, p.dtype == OID_F64, std::max(2, ctx->num_sms - ctx->k1_free_sms));
       if (p.dtype == OID_F64)
         a9q::basis_quant_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(X), ld, ctx->ptr<uint8_t>(L.Cq),

@@ -1,6 +1,6 @@
 """Per-kernel totals of an ncu launch list (--metrics gpu__time_duration.sum --csv).
 usage: launch_summary.py LIST.csv [TOP] [--ours]   (--ours: only this library's kernels, i.e. the
-oid / k1tc / k1p / bgtc namespaces; block generation and torch glue outside the timed region dropped)"""
+oid / k1tc / k1p / k1f / a9q / bgtc namespaces; block generation and torch glue outside the timed region dropped)"""
 import csv, collections, sys
 args = [a for a in sys.argv[1:] if not a.startswith("--")]
 ours = "--ours" in sys.argv
@@ -11,7 +11,7 @@ for r in rows[1:]:
     try: v = float(r[vi].replace(',', ''))
     except ValueError: continue
     name = r[ki]
-    if ours and not any(t in name for t in ("oid::", "k1tc::", "k1p::", "bgtc::")): continue
+    if ours and not any(t in name for t in ("oid::", "k1tc::", "k1p::", "k1f::", "a9q::", "bgtc::")): continue
     name = name[:70]; tot[name] += v; cnt[name] += 1
 T = sum(tot.values())
 for n, v in sorted(tot.items(), key=lambda x: -x[1])[:int(args[1]) if len(args) > 1 else 22]:

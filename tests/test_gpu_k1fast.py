@@ -310,3 +310,35 @@ def test_a9q_gram_bound(oid):
         vac = np.flatnonzero(J < 0)
         assert np.all(G[vac, :] == 0) and np.all(G[:, vac] == 0)
     eng.close()
+
+
+def test_a9q_fp32_large_basis(oid):
+    """A9Q on fp32 data with C5's shape of the basis and sketch (k = 400: four 128-slot chunks;
+    l = 1024: two K1F sketch-row groups; b = 64: two column groups), on the C5 low-rank stream law
+    (C5r rows): the Gram against fp64 dot products of the exact fp32 basis within the bound, the basis
+    bit-exact."""
+    from synth import LowRankStream
+    gen = LowRankStream(m=1 << 18, seed=1005)
+    m, b, k, ell = gen.m, 64, 400, 1024
+    eng, _ = _engine(oid, m, k, ell, b, 16 * b, -1.0, seed=0, dtype="f32", a9q=True)
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(9)
+    for blk in range(9):
+        X = gen.block_torch(blk * b, (blk + 1) * b, dev).T
+        eng.ingest_block(X)
+        if blk in (0, 4, 8):
+            assert np.isfinite(eng.error_estimate()["est_rel"])
+            G = eng.get(11)
+            J = eng.J()
+            occ = np.flatnonzero(J >= 0)
+            basis = eng.finalize(basis=True)["basis"].cpu().numpy().astype(np.float64)
+            pick = rng.choice(occ, size=min(10, len(occ)), replace=False)
+            for i in pick:
+                for j in pick:
+                    ai, aj = basis[:, i], basis[:, j]
+                    Mi, Mj = np.max(np.abs(ai)), np.max(np.abs(aj))
+                    bnd = 2.0 ** -27 * (Mj * np.sum(np.abs(ai)) + Mi * np.sum(np.abs(aj))) + m * 2.0 ** -54 * Mi * Mj
+                    ref = float(np.dot(ai, aj))
+                    assert abs(G[i, j] - ref) <= bnd + 1e-12 * abs(ref), (blk, i, j, G[i, j], ref, bnd)
+        del X
+    eng.close()

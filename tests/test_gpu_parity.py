@@ -615,3 +615,51 @@ def test_internal_side_streams_match_serial(oid, monkeypatch):
     torch.cuda.synchronize()
     assert torch.equal(r1["P"], r2["P"])
     assert torch.equal(r1["basis"], r2["basis"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k1_mode", [2, 3])
+def test_k1_sketch_under_concurrent_estimates(oid, k1_mode):
+    """The exact tensor-core K1 gives bitwise the solo sketch while the same engine's estimates
+    (low-priority stream, held back by a device spin) and another engine's work on the default
+    stream share the SMs.  Regression for the k1_tc epilogue ordering: each slicer group drains
+    only the accumulation epochs its own tiles open, so with the MMA warp two flushes behind, the
+    d_full parity of epoch q matched the completed phase q - 2 and a drain read D mid-epoch
+    (whole-block sketches off by up to 30 %, about half of such runs before the fix)."""
+    cfg = C3R
+    nblk = 8
+    A = ChannelFlow(48, 33, 48, seed=cfg.data_seed).block(0, nblk * cfg.b)
+    Ad = _dev(A, np.float64)
+    X = [Ad[:, j:j + cfg.b] for j in range(0, nblk * cfg.b, cfg.b)]
+    p = oid.make_params(m=cfg.m, k=cfg.k, ell=cfg.ell, b_max=cfg.b, n_cap=nblk * cfg.b, lam=-1.0,
+                        split=_split(cfg.ell), seed=0, k1_mode=k1_mode)
+    hs = torch.cuda.Stream(priority=-1)
+    solo = oid.Engine(p, stream=hs)
+    ref = []
+    for e in range(nblk):
+        with torch.cuda.stream(hs):
+            solo.ingest_sketch(X[e])
+            ref.append(solo.partials(0).clone())
+    torch.cuda.synchronize()
+    for rep in range(4):
+        other = oid.Engine(p)                       # default stream
+        hi = torch.cuda.Stream(priority=-1)
+        lo = torch.cuda.Stream(priority=0)
+        eng = oid.Engine(p, stream=hi, estimate_stream=lo)
+        got = []
+        torch.cuda.synchronize()
+        for e in range(nblk):
+            other.ingest_block(X[e])
+            other.estimate_begin()
+            other.estimate_end()
+            with torch.cuda.stream(hi):
+                eng.ingest_sketch(X[e])
+                got.append(eng.partials(0).clone())
+                eng.ingest_commit(X[e])
+            with torch.cuda.stream(lo):
+                torch.cuda._sleep(4_000_000)
+            eng.estimate_begin()
+            eng.estimate_end()
+        torch.cuda.synchronize()
+        bad = [e for e in range(nblk) if not torch.equal(got[e], ref[e])]
+        assert not bad, f"rep {rep}: sketches of blocks {bad} differ from the solo sketches"
