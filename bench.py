@@ -392,6 +392,11 @@ def main():
     ingest_only = None
     KI = min(8, K)
     if not args.no_estimate and KI > 0:
+        # the next KI snapshots blocks of the stream, generated into ring slots the timed region is
+        # done with (cycling back to block 0 would feed the engine columns it has already seen)
+        for s in range(W + K, W + K + KI):
+            blocks[s % ring] = None
+            blocks[s % ring] = gen.block_torch(s * b, (s + 1) * b, dev, row_begin=rb, row_end=re).T
         torch.cuda.synchronize()
         if sharded:
             dist.barrier()
@@ -494,7 +499,7 @@ def main():
     if E > 0:
         host = []
         for s in range(E):
-            t0_ = (W + K + s) * b
+            t0_ = (W + K + (KI if ingest_only is not None else 0) + s) * b
             hb = torch.empty((b, m_loc), dtype=blocks[0].dtype, pin_memory=True)
             hb.copy_(gen.block_torch(t0_, t0_ + b, dev, row_begin=rb, row_end=re).cpu())
             host.append(hb)
