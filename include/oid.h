@@ -278,8 +278,11 @@ oid_status oid_sketch_table(int32_t q[16], double* scale);
      OID_K1_EXP=bits    K1 ablations for timing only (1: no Philox, 2: no digit conversion; the
                         pair kernel: 4 no TMEM store, 32 no fence, 64 no dp4a, 128 no conversion,
                         256 no MMA, 512 no TMA) - results are WRONG with any bit set
-     OID_K1_FREE=n      SMs the persistent K1 grid leaves free (default 0)
+     OID_K1_FREE=n      SMs the persistent K1 grid leaves free (default 2: the estimate's single-SM
+                        core SVD and side kernels hold no K1 CTA back)
      OID_A9Q_SERIAL=1   K1 waits for the previous A9Q instead of sharing the SMs with it
+     OID_A9Q_CL=n       A9Q launched as at most n 16-CTA clusters (default 6, two GPCs stay free
+                        for the A4 and A8 tridiagonalisation clusters)
      OID_A9_DEFER=0     single-shard contexts launch an estimate's basis Gram in oid_estimate_begin
                         (default: after the next block's K1, or when anything needs it)
      OID_TIMELINE=1     per-stream timeline marks (oid_get field 13)

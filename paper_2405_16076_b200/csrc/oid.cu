@@ -411,9 +411,13 @@ struct oid_ctx_s {
   int bg_cluster = 1;         // A9 CTAs per cluster: whole groups of SMs retire together (OID_BG_CLUSTER)
   int gs_gate = 0;            // A9 also waits for the epoch's A8 chain (diagnostics: OID_GS_GATE)
   bool use_side = true;       // diagnostics: OID_NO_SIDE=1 runs everything on the caller's stream
-  int k1_free_sms = 0;        // SMs the persistent K1 grid leaves to concurrent streams (OID_K1_FREE)
+  int k1_free_sms = 2;        // SMs the persistent K1 grid leaves to concurrent streams (OID_K1_FREE):
+                              // the estimate's single-SM core SVD and side-stream kernels then hold no
+                              // K1 CTA back (C3 pipelined: 623 vs 605 GB/s with 0)
   bool a9q = false;           // A9 on the quantised basis (K1F mode; off for good once a block skips K1F)
   bool a9q_serial = false;    // K1 waits for the last A9Q (diagnostics: OID_A9Q_SERIAL=1)
+  int a9q_cl = 6;             // A9Q 16-CTA clusters at most (OID_A9Q_CL): two GPCs stay free for the
+                              // A4 and A8 tridiagonalisation clusters (C3: 587 vs 547 GB/s with 7)
   bool a9_defer = false;      // single shard: A9 launched after the next block's K1 (OID_A9_DEFER=0: at once)
   bool a9_pending = false;    // an estimate's A9 queued but not launched
   int a9_gp = 0;
@@ -802,7 +806,7 @@ static oid_status launch_a9(oid_ctx ctx) {
       // 16-CTA cluster, which runs concurrently, can always be placed)
       const int nch = a9q::nchunks(t);
       const int64_t nt128 = (ctx->m_loc + a9q::kTR - 1) / a9q::kTR;
-      int ncl = std::min(7, (sms - 20) / 16);
+      int ncl = std::min(ctx->a9q_cl, (sms - 20) / 16);
       while (ncl > 0 && (16 * ncl) % nch != 0) --ncl;
       const bool clustered = ncl > 0 && (16 * ncl) / nch <= nt128;
       const int nr = clustered ? (16 * ncl) / nch
@@ -1641,6 +1645,7 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
   }
   ctx->a9q = a9q_wanted(*p) && ctx->tc_ok;
   ctx->a9q_serial = getenv("OID_A9Q_SERIAL") && atoi(getenv("OID_A9Q_SERIAL")) != 0;
+  if (getenv("OID_A9Q_CL")) ctx->a9q_cl = std::max(1, std::min(7, atoi(getenv("OID_A9Q_CL"))));
   ctx->a9_defer = p->row_begin == 0 && p->row_end == p->m && !(getenv("OID_A9_DEFER") && atoi(getenv("OID_A9_DEFER")) == 0);
   if ((e = cudaEventCreateWithFlags(&ctx->ev_k1_end, cudaEventDisableTiming)) != cudaSuccess) return bad(e);
   if (a9q_wanted(*p)) {
