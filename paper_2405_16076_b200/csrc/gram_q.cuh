@@ -269,128 +269,147 @@ gram_q_kernel(const uint8_t* __restrict__ Cq, const int* __restrict__ Fq, int64_
   }
 }
 
-// A7 for the quantised copy: planes of v = round(x 2^F_s) for every admission, zero planes for
-// vacated slots, F_s from the column's maximum biased exponent over the K1F units (gE, this block);
-// one thread = 16 consecutive rows of one admitted column (one 16-byte chunk per plane)
+// A7 for the quantised copy, step 1: per admission (or vacated slot) a = 0 .. na + nz - 1 of this
+// commit, its slot, column r (-1: vacated) and C = (the column's maximum biased exponent over the
+// K1F units that saw it) - 30, so |v| <= 2^29 for its largest element; F_s = kFbase - C -> Fq.
+// One warp per admission.
+__global__ void quant_adm_kernel(const int* __restrict__ admit, const int* __restrict__ counts, int nc, int t,
+                                 const int* __restrict__ gE, int nunits, int nsg, int kFbase, int* __restrict__ Fq,
+                                 int4* __restrict__ qadm) {
+  const int na = counts[0], nz = counts[1];
+  const int a = static_cast<int>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5), ln = threadIdx.x & 31;
+  if (a >= na + nz) return;
+  int slot, r = -1;
+  if (a < na) { slot = admit[2 * a]; r = admit[2 * a + 1]; }
+  else slot = admit[2 * (nc + t) - 2 - 2 * (a - na)];
+  int em = 0;
+  if (r >= 0) {
+    const int cg = r >> 5, jl = r & 31, ncg = (nc + 31) / 32;
+    for (int u = ln; u < nunits; u += 32)
+      if (((u / nsg) % ncg) == cg && (u % nsg) == 0) em = max(em, gE[u * 32 + jl]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) em = max(em, __shfl_xor_sync(0xffffffffu, em, o));
+  }
+  const int C = em - 30;
+  if (ln == 0) {
+    Fq[slot] = r >= 0 ? kFbase - C : 0;
+    qadm[a] = make_int4(slot, r, C, 0);
+  }
+}
+
+// A7 for the quantised copy, step 2: every admitted column is read once and written twice -
+// bit-exactly into the row-tiled fp64 / fp32 basis (lines of RL rows)
+// and as the digit planes of v = round(x 2^F_s) (zero lines and planes for vacated slots).  Work
+// items are (admission, 512 rows); a warp takes items with a grid stride over all admissions (the
+// grid fills the GPU whatever the device-side admission count) and loads the next item's rows into
+// registers while it converts and stores the current one from its shared buffer.
 template <typename T>
-__global__ void basis_quant_kernel(const T* __restrict__ X, int64_t ld, uint8_t* __restrict__ Cq, int* __restrict__ Fq,
-                                   int64_t m_loc, int t, const int* __restrict__ admit, const int* __restrict__ counts,
-                                   int nc, const int* __restrict__ gE, int nunits, int nsg, T* __restrict__ Cb) {
-  // A7 fused: every admitted column is read once and written twice - bit-exactly into the row-tiled
-  // fp64 / fp32 basis (lines of RL rows) and as the quantised planes
+__global__ void __launch_bounds__(256, 3)
+basis_quant_kernel(const T* __restrict__ X, int64_t ld, uint8_t* __restrict__ Cq, int64_t m_loc, int t,
+                   const int* __restrict__ counts, const int4* __restrict__ qadm, T* __restrict__ Cb) {
   constexpr int RL = 128 / sizeof(T);
   constexpr bool kF64 = sizeof(T) == 8;
-  constexpr int kFbase = kF64 ? 1021 : 125;
-  const int na = counts[0], nz = counts[1];
+  constexpr int kQ = 16 * static_cast<int>(sizeof(T)) / 16;   // uint4 per 16-row run (8 / 4)
+  constexpr int kE = 16 / static_cast<int>(sizeof(T));        // elements per uint4
+  const int nadm = counts[0] + counts[1];
   const int64_t bb = block_bytes(t);
   const int64_t nchunk16 = (m_loc + 15) / 16;
-  // one admission (or vacated slot) per blockIdx.y: all columns stream concurrently
-  {
-    const int a = blockIdx.y;
-    if (a >= na + nz) return;
-    int slot, r = -1;
-    if (a < na) { slot = admit[2 * a]; r = admit[2 * a + 1]; }
-    else slot = admit[2 * (nc + t) - 2 - 2 * (a - na)];
-    // column maximum biased exponent over the units that saw column r (all ranges, sketch group 0),
-    // one block-wide max per admission
-    __shared__ int s_em;
-    if (threadIdx.x == 0) s_em = 0;
-    __syncthreads();
-    if (r >= 0) {
-      const int cg = r >> 5, jl = r & 31;
-      const int ncg = (nc + 31) / 32;
-      int em_t = 0;
-      for (int u = threadIdx.x; u < nunits; u += blockDim.x)
-        if (((u / nsg) % ncg) == cg && (u % nsg) == 0) em_t = max(em_t, gE[u * 32 + jl]);
-      atomicMax(&s_em, em_t);
+  const int nwork = static_cast<int>((nchunk16 + 31) / 32);      // items per admission
+  const int total = nadm * nwork;                                 // < 2^31 (m_loc < 2^31, nadm <= 2 b + t)
+  __shared__ uint4 s_x[8][32 * kQ + 32];                        // +1 uint4 pad per run
+  const int wl = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  uint4* sw = s_x[wl];
+  const int wstride = static_cast<int>(gridDim.x) * (blockDim.x >> 5);
+  uint4 nx[kQ];
+  // coalesced loads of item wi's 512 rows (zeros past m_loc and for vacated slots)
+  auto fetch = [&](int wi) {
+    const int a = wi / nwork;
+    const int64_t base_row = static_cast<int64_t>(wi - a * nwork) * 512;
+    const int r = __ldg(&qadm[a].y);
+    const T* col = r >= 0 ? X + static_cast<int64_t>(r) * ld : nullptr;
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+      const int64_t row = base_row + static_cast<int64_t>(q * 32 + ln) * kE;
+      uint4 v = make_uint4(0u, 0u, 0u, 0u);
+      if (col && row + kE <= m_loc) v = __ldcs(reinterpret_cast<const uint4*>(col + row));
+      else if (col && row < m_loc) {
+        T tmp[kE];
+#pragma unroll
+        for (int e = 0; e < kE; ++e) tmp[e] = row + e < m_loc ? col[row + e] : T(0);
+        v = *reinterpret_cast<uint4*>(tmp);
+      }
+      nx[q] = v;
     }
-    __syncthreads();
-    const int em = s_em;
-    const int C = em - 30;                                   // |v| <= 2^29 for the largest element
-    if (blockIdx.x == 0 && threadIdx.x == 0) Fq[slot] = r >= 0 ? kFbase - C : 0;
-    // a warp takes 512 consecutive rows (32 runs of 16): coalesced 16-byte loads into its shared
-    // buffer, each lane then converts its own run; the exact copy goes out 8 lanes per basis line
-    __shared__ uint4 s_x[8][32 * (16 * static_cast<int>(sizeof(T)) / 16) + 32];   // +1 uint4 pad per run
-    constexpr int kQ = 16 * static_cast<int>(sizeof(T)) / 16;                    // uint4 per run (8 / 4)
-    const int wl = threadIdx.x >> 5, ln = threadIdx.x & 31;
-    uint4* sw = s_x[wl];
-    const int64_t nwork = (nchunk16 + 31) / 32;
-    const int64_t wstride = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-    for (int64_t wk = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wl; wk < nwork; wk += wstride) {
-      const int64_t ch = wk * 32 + ln;                   // this lane's run
-      const int64_t base_row = wk * 512;
-      // coalesced load of the warp's 512 rows (zeros past m_loc and for vacated slots)
-      const T* col = r >= 0 ? X + static_cast<int64_t>(r) * ld : nullptr;
+  };
+  int w = static_cast<int>(blockIdx.x) * (blockDim.x >> 5) + wl;
+  if (w < total) fetch(w);
+  for (; w < total; w += wstride) {
+    const int a = w / nwork;
+    const int64_t wk = w - a * nwork;
+    const int4 qa = __ldg(&qadm[a]);
+    const int slot = qa.x, C = qa.z;
+    const int64_t base_row = wk * 512;
 #pragma unroll
-      for (int q = 0; q < kQ; ++q) {
-        const int u = q * 32 + ln;                       // uint4 index within the warp's rows
-        const int64_t row = base_row + static_cast<int64_t>(u) * (16 / static_cast<int>(sizeof(T)));
-        uint4 v = make_uint4(0u, 0u, 0u, 0u);
-        if (col && row + (16 / static_cast<int>(sizeof(T))) <= m_loc) v = __ldg(reinterpret_cast<const uint4*>(col + row));
-        else if (col && row < m_loc) {
-          T tmp[16 / sizeof(T)];
+    for (int q = 0; q < kQ; ++q) {
+      const int u = q * 32 + ln;
+      sw[(u / kQ) * (kQ + 1) + (u % kQ)] = nx[q];                // run u / kQ, padded
+    }
+    __syncwarp();
+    if (w + wstride < total) fetch(w + wstride);                   // in flight during the work below
+    // exact copy: a run of 16 rows is one 128-byte basis line (f64, 8 lanes per line) or
+    // half of one (f32, 4 lanes)
 #pragma unroll
-          for (int e = 0; e < static_cast<int>(16 / sizeof(T)); ++e) tmp[e] = row + e < m_loc ? col[row + e] : T(0);
-          v = *reinterpret_cast<uint4*>(tmp);
-        }
-        sw[(u / kQ) * (kQ + 1) + (u % kQ)] = v;          // run u / kQ, padded
+    for (int q = 0; q < kQ; ++q) {
+      const int u = q * 32 + ln;
+      const int run = u / kQ, part = u % kQ;
+      const int64_t i0r = base_row + static_cast<int64_t>(run) * 16;
+      if (i0r < m_loc) {
+        T* dst = Cb + ((i0r / RL) * t + slot) * RL + (i0r % RL);
+        __stcs(reinterpret_cast<uint4*>(dst) + part, sw[run * (kQ + 1) + part]);
       }
-      __syncwarp();
-      // exact copy: a run of 16 rows is one 128-byte basis line (f64, 8 lanes per line) or
-      // half of one (f32, 4 lanes)
+    }
+    const int64_t ch = wk * 32 + ln;                               // this lane's run
+    const bool valid = ch < nchunk16;
+    const int64_t i0 = ch * 16;
+    uint32_t wv[16];
 #pragma unroll
-      for (int q = 0; q < kQ; ++q) {
-        const int u = q * 32 + ln;
-        const int run = u / kQ, part = u % kQ;
-        const int64_t i0r = base_row + static_cast<int64_t>(run) * 16;
-        if (i0r < m_loc) {
-          T* dst = Cb + ((i0r / RL) * t + slot) * RL + (i0r % RL);
-          __stcs(reinterpret_cast<uint4*>(dst) + part, sw[run * (kQ + 1) + part]);
-        }
+    for (int e = 0; e < 16; ++e) {
+      // one 16-byte shared load per kE elements (conflict-free: runs are 9 / 5 uint4 apart)
+      uint32_t hi, lo;
+      if constexpr (kF64) {
+        const uint4 q4 = sw[ln * (kQ + 1) + e / 2];
+        hi = (e & 1) ? q4.w : q4.y; lo = (e & 1) ? q4.z : q4.x;
+      } else {
+        const uint4 q4 = sw[ln * (kQ + 1) + e / 4];
+        hi = (e & 3) == 0 ? q4.x : (e & 3) == 1 ? q4.y : (e & 3) == 2 ? q4.z : q4.w; lo = 0u;
       }
-      const bool valid = ch < nchunk16;
-      const int64_t i0 = ch * 16;
-      T xv[16];
+      const int E = static_cast<int>((hi << 1) >> (kF64 ? 21 : 24));
+      const uint32_t pw = (E - C) < 0 || (E - C) > 31 ? 0u : (1u << (E - C));   // 2^(33 - k)
+      const uint32_t tt = kF64 ? __funnelshift_r(lo, (hi & 0xFFFFFu) | 0x100000u, 21) : ((hi << 8) | 0x80000000u);
+      const uint32_t u = __umulhi(tt, pw) + 1u;
+      const int v = static_cast<int>(u >> 1);
+      const int sg = static_cast<int>(hi) >> 31;
+      wv[e] = static_cast<uint32_t>(v * (2 * sg + 1) + 0x808080);
+    }
+    __syncwarp();                                                  // the buffer is reused by the next item
+    // 4x4 byte transposes -> plane words (rows i0 .. i0 + 15 of plane p)
+    uint32_t P[4][4];
 #pragma unroll
-      for (int q = 0; q < kQ; ++q) reinterpret_cast<uint4*>(xv)[q] = sw[ln * (kQ + 1) + q];
-      __syncwarp();                                       // the buffer is reused by the next run set
-      uint32_t w[16];
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t x0 = __byte_perm(wv[4 * q], wv[4 * q + 1], 0x5140), x1 = __byte_perm(wv[4 * q], wv[4 * q + 1], 0x7362);
+      const uint32_t y0 = __byte_perm(wv[4 * q + 2], wv[4 * q + 3], 0x5140), y1 = __byte_perm(wv[4 * q + 2], wv[4 * q + 3], 0x7362);
+      P[0][q] = __byte_perm(x0, y0, 0x5410) ^ 0x80808080u;
+      P[1][q] = __byte_perm(x0, y0, 0x7632) ^ 0x80808080u;
+      P[2][q] = __byte_perm(x1, y1, 0x5410) ^ 0x80808080u;
+      P[3][q] = __byte_perm(x1, y1, 0x7632);
+    }
+    const int64_t tile = i0 / kTR;
+    const int c = static_cast<int>((i0 % kTR) / 16);
+    uint8_t* blk = Cq + tile * bb;
+    if (valid) {
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        uint32_t hi, lo;
-        if constexpr (kF64) {
-          const uint64_t bb2 = __double_as_longlong(xv[e]);
-          hi = static_cast<uint32_t>(bb2 >> 32); lo = static_cast<uint32_t>(bb2);
-        } else {
-          hi = __float_as_uint(xv[e]); lo = 0u;
-        }
-        const int E = static_cast<int>((hi << 1) >> (kF64 ? 21 : 24));
-        const uint32_t pw = (E - C) < 0 || (E - C) > 31 ? 0u : (1u << (E - C));   // 2^(33 - k)
-        const uint32_t tt = kF64 ? __funnelshift_r(lo, (hi & 0xFFFFFu) | 0x100000u, 21) : ((hi << 8) | 0x80000000u);
-        const uint32_t u = __umulhi(tt, pw) + 1u;
-        const int v = static_cast<int>(u >> 1);
-        const int sg = static_cast<int>(hi) >> 31;
-        w[e] = static_cast<uint32_t>(v * (2 * sg + 1) + 0x808080);
-      }
-      // 4x4 byte transposes -> plane words (rows i0 .. i0 + 15 of plane p)
-      uint32_t P[4][4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t x0 = __byte_perm(w[4 * q], w[4 * q + 1], 0x5140), x1 = __byte_perm(w[4 * q], w[4 * q + 1], 0x7362);
-        const uint32_t y0 = __byte_perm(w[4 * q + 2], w[4 * q + 3], 0x5140), y1 = __byte_perm(w[4 * q + 2], w[4 * q + 3], 0x7362);
-        P[0][q] = __byte_perm(x0, y0, 0x5410) ^ 0x80808080u;
-        P[1][q] = __byte_perm(x0, y0, 0x7632) ^ 0x80808080u;
-        P[2][q] = __byte_perm(x1, y1, 0x5410) ^ 0x80808080u;
-        P[3][q] = __byte_perm(x1, y1, 0x7632);
-      }
-      const int64_t tile = i0 / kTR;
-      const int c = static_cast<int>((i0 % kTR) / 16);
-      uint8_t* blk = Cq + tile * bb;
-      if (valid) {
-#pragma unroll
-        for (int p = 0; p < 4; ++p)
-          *reinterpret_cast<uint4*>(blk + swz(4 * slot + p, c)) = make_uint4(P[p][0], P[p][1], P[p][2], P[p][3]);
-      }
+      for (int p = 0; p < 4; ++p)
+        *reinterpret_cast<uint4*>(blk + swz(4 * slot + p, c)) = make_uint4(P[p][0], P[p][1], P[p][2], P[p][3]);
     }
   }
 }

@@ -123,7 +123,7 @@ struct Bump {
 struct Layout {
   size_t S, gram, Ypart, k1part, k1npart, gB, gV, mu, mu_sorted, Yc, Tsc, tau, scal, J, tau_old, admit, counts,
       flags, counters, C, SJ, sjB, sjV, sjsig, sjw, sjZ, Sjpinv, Pexp, AJP, G, Gsum, Gpart, cB, cV, csig, cw, cZ, M,
-      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, k1g, Cq, Fq, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, wyT, sjG, cG, cBt, cZ2, dbg, Jsnap, Dsnap, gcnt, Sg, YpG, GX, OGO, gH, gHV, gHs, gHw, gHZ, gHp, gR, gCm, gE, gLst, gLV, gLs, gLw, gLZ, gLp, gRhs, gscal, td2, te2, Vh2, tauv2, wyT2, ldl2, mu2, cum, elog, eslog, omega, trA, trW, Pcand, Pchosen, Pext, Rres, Gprev, gpH, gpV, gpMu, gpW, Gpinv, Xc, Dx, Dxp, Tm, cest, est_ch, est4, qlog, Jprev, olds, nold, qsel, Dpool, Dnorm, total;
+      X1, X2, Q1, Q2, R1, R2t, R3, PPt, est, tc, k1g, Cq, Fq, qadm, Gfull, dirty, dlist, jfro2, symU, symF, symTol, gT, td, te, Vh, tauv, gv, gp, gate, ldl, wyT, sjG, cG, cBt, cZ2, dbg, Jsnap, Dsnap, gcnt, Sg, YpG, GX, OGO, gH, gHV, gHs, gHw, gHZ, gHp, gR, gCm, gE, gLst, gLV, gLs, gLw, gLZ, gLp, gRhs, gscal, td2, te2, Vh2, tauv2, wyT2, ldl2, mu2, cum, elog, eslog, omega, trA, trW, Pcand, Pchosen, Pext, Rres, Gprev, gpH, gpV, gpMu, gpW, Gpinv, Xc, Dx, Dxp, Tm, cest, est_ch, est4, qlog, Jprev, olds, nold, qsel, Dpool, Dnorm, total;
 };
 
 int64_t m_local(const oid_params& p) { return p.row_end - p.row_begin; }
@@ -302,6 +302,7 @@ Layout make_layout(const oid_params& p) {
   if (a9q_wanted(p)) {   // A9Q: the quantised basis (4 digit planes per element) and its exponents
     L.Cq = b.take(a9q::qbasis_bytes(m_local(p), static_cast<int>(t)));
     L.Fq = b.take(t * sizeof(int));
+    L.qadm = b.take((static_cast<size_t>(p.b_max) + t) * 4 * sizeof(int));   // (slot, column, C, -) per admission
   }
   if (p.omega_cache == 1) {   // omega_cache (NEXT-3): Philox words of ell x m_loc sketch entries
     // + 1 group: the last 64-row K1 tile may run one 32-row group past the shard (zero rows of X)
@@ -1063,23 +1064,27 @@ oid_status post_epoch(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream
                                                        ctx->ptr<int>(L.admit), ctx->ptr<int>(L.counts), nc, t);
       CKL();
     } else {
-      // A7 + the quantised copy in one pass over the admitted columns (a9q::basis_quant_kernel)
-      // x: row blocks of 4096 rows (8 warps x 512), y: one admission or vacated slot each (blocks past
-      // the device-side count exit at once)
-      grid = dim3(std::max(1u, std::min(static_cast<unsigned>((ctx->m_loc + 4095) / 4096),
-                                        static_cast<unsigned>(std::max(1, 8 * ctx->num_sms / std::max(1, nc))))),
-                  static_cast<unsigned>(nc + t));
+      // A7 + the quantised copy in one pass over the admitted columns: per-admission exponents
+      // (one warp each, blocks past the device-side count exit at once), then a GPU-filling
+      // grid-stride pass over (admission, 512-row) items
       const k1f::Geom kg = k1f::make_geom(p.ell, nc, ctx->m_loc, p.dtype == OID_F64, std::max(2, ctx->num_sms - ctx->k1_free_sms));
+      a9q::quant_adm_kernel<<<static_cast<unsigned>((nc + t + 7) / 8), 256, 0, st>>>(
+          ctx->ptr<int>(L.admit), ctx->ptr<int>(L.counts), nc, t, ctx->ptr<int>(L.k1g), kg.nunits(), kg.nsg,
+          p.dtype == OID_F64 ? 1021 : 125, ctx->ptr<int>(L.Fq), reinterpret_cast<int4*>(ctx->ptr<int>(L.qadm)));
+      CKL();
+      if (static_cast<int64_t>(nc + t) * ((ctx->m_loc + 511) / 512) >= (int64_t(1) << 31))
+        return ctx->fail(OID_ESHAPE, "quantised copy: %lld rows per shard too many", (long long)ctx->m_loc);
+      grid = dim3(static_cast<unsigned>(3 * ctx->num_sms));
       if (p.dtype == OID_F64)
         a9q::basis_quant_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(X), ld, ctx->ptr<uint8_t>(L.Cq),
-                                                             ctx->ptr<int>(L.Fq), ctx->m_loc, t, ctx->ptr<int>(L.admit),
-                                                             ctx->ptr<int>(L.counts), nc, ctx->ptr<int>(L.k1g), kg.nunits(),
-                                                             kg.nsg, ctx->ptr<double>(L.C));
+                                                             ctx->m_loc, t, ctx->ptr<int>(L.counts),
+                                                             reinterpret_cast<const int4*>(ctx->ptr<int>(L.qadm)),
+                                                             ctx->ptr<double>(L.C));
       else
         a9q::basis_quant_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(X), ld, ctx->ptr<uint8_t>(L.Cq),
-                                                            ctx->ptr<int>(L.Fq), ctx->m_loc, t, ctx->ptr<int>(L.admit),
-                                                            ctx->ptr<int>(L.counts), nc, ctx->ptr<int>(L.k1g), kg.nunits(),
-                                                            kg.nsg, ctx->ptr<float>(L.C));
+                                                            ctx->m_loc, t, ctx->ptr<int>(L.counts),
+                                                            reinterpret_cast<const int4*>(ctx->ptr<int>(L.qadm)),
+                                                            ctx->ptr<float>(L.C));
       CKL();
     }
   }
