@@ -95,8 +95,12 @@ typedef struct {
      [f nx ny, (f+1) nx ny), node (i, j) at f nx ny + i ny + j); simplex gradients over the axis
      neighbours with spacings grad_hx, grad_hy (0: 1/(N-1)).  The ridge scores then use the
      augmented sketch [Omega a; Omega G^1 a; Omega G^2 a] and the augmented energy; the
-     estimate keeps Alg 4's P; oid_gradient_* give P(mu) and the sketched GCV.  Requires a single
-     shard (row_begin = 0, row_end = m), grad_nfields grad_nx grad_ny = m and 3 ell <= 1024.  */
+     estimate keeps Alg 4's P; oid_gradient_* give P(mu) and the sketched GCV.  Requires
+     grad_nfields grad_nx grad_ny (grad_nz) = m and (d + 1) ell <= 2048.  Row-sharded contexts
+     (route (ii) for G^p X): each block comes with its stencil halos
+     (oid_ingest_sketch_halo, widths from oid_grad_halo), the gradient sketches are summed with
+     oid_partials(2) beside oid_partials(0), and Omega G^p Omega^T (route (i): Omega generated at
+     the neighbouring global rows, no exchange) with oid_gradient_ogo + oid_partials(3).  */
   int32_t grad_nfields, grad_nx, grad_ny;
   int32_t omega_cache; /* NEXT-3 ablation: 1 = store the sketch entries (their Philox words,
                           ell * m_loc / 2 bytes of workspace, filled at oid_init) and stream them
@@ -180,8 +184,26 @@ oid_status oid_ingest_commit(oid_ctx ctx, const void* X, int64_t ld, int32_t nco
 
 /* Device pointer and element count (fp64) of a partial buffer to be summed over shards:
    which = 0: ingest partials ((ell + 1) * ncols of the last sketch);
-   which = 1: basis-Gram partials (k * k) of the last oid_estimate_begin. */
+   which = 1: basis-Gram partials (k * k) of the last oid_estimate_begin;
+   which = 2: gradient variant, the gradient sketches of the last sketch: d buffers
+              [Y_p (ell x ncols); n_p (ncols)], buffer p - 1 at offset (p - 1)(ell + 1) b_max
+              (count = d (ell + 1) b_max: summing the whole range is allowed, entries past
+              (ell + 1) ncols of a buffer are never read);
+   which = 3: gradient variant, Omega G^p Omega^T (d ell x ell, p = 1..d) after oid_gradient_ogo.
+   Errors: OID_EINVAL (unknown which, or 2/3 without the gradient variant). */
 oid_status oid_partials(oid_ctx ctx, int32_t which, double** dev_ptr, int64_t* count);
+
+/* Sharded gradient variant (P:684 stencils G^p X across row slabs, SURVEY 8(e) route (ii)):
+   oid_ingest_sketch with the block's stencil halos.  X_lo: device, rows_lo x ncols (ld_lo >=
+   rows_lo), the global rows [row_begin - rows_lo, row_begin) of the same block; X_hi: rows_hi x
+   ncols (ld_hi >= rows_hi), the rows [row_end, row_end + rows_hi); dtype p->dtype; both read by
+   kernels on `stream` and borrowed like X.  rows_lo / rows_hi = oid_grad_halo (grad_ny grad_nz
+   rows, clipped at 0 and m; 0 without the gradient variant, when the pointers may be NULL).
+   oid_ingest_sketch = this call with NULL halos.  Errors: those of oid_ingest_sketch, and
+   OID_EINVAL when a needed halo is NULL or its ld too small. */
+oid_status oid_ingest_sketch_halo(oid_ctx ctx, const void* X, int64_t ld, int32_t ncols, const void* X_lo,
+                                  int64_t ld_lo, const void* X_hi, int64_t ld_hi, void* stream);
+oid_status oid_grad_halo(oid_ctx ctx, int64_t* rows_lo, int64_t* rows_hi);
 
 /* NA-Hutch++ estimate of ||A_obs - A_J P||_F for the current J and P (Alg 8).
    _begin computes this shard's part of G = A_J^T A_J; after the caller's reduction
@@ -220,8 +242,12 @@ oid_status oid_finalize(oid_ctx ctx, int64_t* J_host, double* P, int32_t P_on_de
    oid_gradient_finalize  mu* by golden-section search of GCV over log10(mu) in [lo, hi] to
                           tolerance tol (the paper: [-3, 3]); P(mu*) into P_dev when not
                           NULL; synchronizes.
-   Errors: OID_ESTATE (variant off, nothing ingested, sketch pending), OID_EINVAL (mu < 0,
-   lo >= hi, tol <= 0). */
+   oid_gradient_ogo       this shard's part of Omega G^p Omega^T, into oid_partials(3);
+                          sharded contexts call it once and sum the partials over the shards
+                          before the first GCV (single shard: optional, done on first use).
+   Errors: OID_ESTATE (variant off, nothing ingested, sketch pending; sharded GCV before
+   oid_gradient_ogo), OID_EINVAL (mu < 0, lo >= hi, tol <= 0). */
+oid_status oid_gradient_ogo(oid_ctx ctx, void* stream);
 oid_status oid_gradient_gcv(oid_ctx ctx, double mu, double* gcv, void* stream);
 oid_status oid_gradient_coefficients(oid_ctx ctx, double mu, double* P_dev, void* stream);
 oid_status oid_gradient_finalize(oid_ctx ctx, double lo, double hi, double tol, double* mu_star, double* P_dev,

@@ -31,7 +31,8 @@ FLAG_NONFINITE_INPUT, FLAG_SJ_RANK_DEFICIENT, FLAG_E2_NEGATIVE, FLAG_K1_RECOMPUT
 EXPORTED = ["oid_workspace_query", "oid_init", "oid_ingest_block", "oid_ingest_sketch", "oid_ingest_commit",
             "oid_partials", "oid_estimate_begin", "oid_estimate_end", "oid_error_estimate", "oid_finalize", "oid_get",
             "oid_stats", "oid_stats_reset", "oid_sketch_table", "oid_destroy", "oid_last_error", "oid_version",
-            "oid_gradient_gcv", "oid_gradient_coefficients", "oid_gradient_finalize", "oid_report"]
+            "oid_gradient_gcv", "oid_gradient_coefficients", "oid_gradient_finalize", "oid_report",
+            "oid_ingest_sketch_halo", "oid_grad_halo", "oid_gradient_ogo"]
 
 
 class OidParams(ctypes.Structure):
@@ -63,6 +64,9 @@ _sig = {
     "oid_ingest_block": [_vp, _vp, _i64, _i32, _vp],
     "oid_ingest_sketch": [_vp, _vp, _i64, _i32, _vp],
     "oid_ingest_commit": [_vp, _vp, _i64, _i32, _vp],
+    "oid_ingest_sketch_halo": [_vp, _vp, _i64, _i32, _vp, _i64, _vp, _i64, _vp],
+    "oid_grad_halo": [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)],
+    "oid_gradient_ogo": [_vp, _vp],
     "oid_partials": [_vp, _i32, ctypes.POINTER(_dp), ctypes.POINTER(_i64)],
     "oid_estimate_begin": [_vp, _vp],
     "oid_estimate_end": [_vp, _vp, _vp],
@@ -205,9 +209,35 @@ class Engine:
         ptr, ld, nc = self._block(X)
         self._check(_lib.oid_ingest_block(self.h, ptr, ld, nc, self._st()), "oid_ingest_block")
 
-    def ingest_sketch(self, X):
+    def ingest_sketch(self, X, halo_lo=None, halo_hi=None):
+        """halo_lo / halo_hi: the block's stencil halos ((rows, ncols) device tensors, column-major)
+        of a sharded gradient-variant context (grad_halo() rows below / above the slab)."""
         ptr, ld, nc = self._block(X)
-        self._check(_lib.oid_ingest_sketch(self.h, ptr, ld, nc, self._st()), "oid_ingest_sketch")
+        if halo_lo is None and halo_hi is None:
+            self._check(_lib.oid_ingest_sketch(self.h, ptr, ld, nc, self._st()), "oid_ingest_sketch")
+            return
+        hp = []
+        for H in (halo_lo, halo_hi):
+            if H is None or H.shape[0] == 0:
+                hp += [ctypes.c_void_p(), 0]
+                continue
+            if H.device != self.device or H.dtype != self.dtype or H.dim() != 2 or H.shape[1] != nc:
+                raise ValueError(f"halo must be a (rows, {nc}) {self.dtype} tensor on {self.device}")
+            if H.shape[0] > 1 and H.stride(0) != 1:
+                raise ValueError("halo must be column-major (stride(0) == 1)")
+            hp += [ctypes.c_void_p(H.data_ptr()), H.stride(1) if nc > 1 else H.shape[0]]
+        self._check(_lib.oid_ingest_sketch_halo(self.h, ptr, ld, nc, hp[0], hp[1], hp[2], hp[3], self._st()),
+                    "oid_ingest_sketch_halo")
+
+    def grad_halo(self):
+        """(rows below, rows above) of stencil halo this shard's blocks need (0, 0 when none)."""
+        lo, hi = _i64(), _i64()
+        self._check(_lib.oid_grad_halo(self.h, ctypes.byref(lo), ctypes.byref(hi)), "oid_grad_halo")
+        return lo.value, hi.value
+
+    def gradient_ogo(self):
+        """This shard's part of Omega G^p Omega^T into partials(3) (sum over shards before the GCV)."""
+        self._check(_lib.oid_gradient_ogo(self.h, self._st()), "oid_gradient_ogo")
 
     def ingest_commit(self, X):
         ptr, ld, nc = self._block(X)

@@ -45,24 +45,33 @@ __device__ __forceinline__ void grad_axis(const GradGrid& g, int i, int j, int l
   w = n ? 1.0 / (n * h) : 0.0;
 }
 
-// GX + p gstride (m x nc, ld m, fp64) = G^p X for p < d (the block's rows are the whole grid:
-// single shard)
+// GX + p gstride (m x nc, ld m, fp64) = G^p X for p < d on this shard's rows: local row q is
+// global row row0 + q (its grid node); a neighbour outside [0, m) is read from the halos (SURVEY
+// 8(e) route (ii)): Xlo holds the hlo global rows [row0 - hlo, row0) (ld ldlo), Xhi the hhi rows
+// [row0 + m, row0 + m + hhi) (ld ldhi).  Single shard: row0 = 0, no halo is ever read.
 template <typename T>
 __global__ void grad_stencil_kernel(const T* __restrict__ X, int64_t ld, int64_t m, int nc, GradGrid g,
-                                    double* __restrict__ GX, int64_t gstride) {
+                                    double* __restrict__ GX, int64_t gstride, int64_t row0,
+                                    const T* __restrict__ Xlo, int64_t ldlo, int64_t hlo,
+                                    const T* __restrict__ Xhi, int64_t ldhi) {
   const int64_t total = m * nc;
   for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int c = static_cast<int>(e / m);
     const int64_t q = e - static_cast<int64_t>(c) * m;
     int i, j, l;
-    grad_node(g, q, i, j, l);
+    grad_node(g, row0 + q, i, j, l);
     const T* col = X + static_cast<int64_t>(c) * ld;
+    auto at = [&](int64_t r) -> double {   // local row r (possibly in a halo)
+      if (r < 0) return static_cast<double>(Xlo[static_cast<int64_t>(c) * ldlo + (hlo + r)]);
+      if (r >= m) return static_cast<double>(Xhi[static_cast<int64_t>(c) * ldhi + (r - m)]);
+      return static_cast<double>(col[r]);
+    };
     for (int p = 0; p < g.d; ++p) {
       int64_t op, om;
       double w;
       grad_axis(g, i, j, l, p, op, om, w);
-      GX[p * gstride + e] = (static_cast<double>(col[q + op]) - static_cast<double>(col[q + om])) * w;
+      GX[p * gstride + e] = (at(q + op) - at(q + om)) * w;
     }
   }
 }
@@ -132,18 +141,19 @@ __device__ __forceinline__ double omega_entry(int r, int64_t i, uint32_t key0, u
   return scale * qd[(words[rr >> 3] >> (4 * (rr & 7))) & 15u];
 }
 
-// W(:, j) = G^p omega_{s0 + j} (m x ns, ld m): the stencil applied to sketch row s0 + j, so that
+// W(:, j) = G^p omega_{s0 + j} (m x ns, ld m, this shard's rows row0 ..): the stencil applied to
+// sketch row s0 + j (neighbours of a slab-edge row are generated, not exchanged), so that
 // Omega W = (Omega G^p Omega^T)(:, s0 .. s0 + ns) comes out of the tensor-core K1 (grad_ogo)
 __global__ void omega_g_cols_kernel(int s0, int ns, int64_t m, GradGrid g, int p, uint32_t key0, uint32_t key1,
-                                    double scale, double* __restrict__ W) {
+                                    double scale, double* __restrict__ W, int64_t row0) {
   __shared__ double qd[16];
   if (threadIdx.x < 16) qd[threadIdx.x] = c_qtab_f64[threadIdx.x];
   __syncthreads();
   for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < m * ns;
        idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int j = static_cast<int>(idx / m);
-    const int64_t q = idx - static_cast<int64_t>(j) * m;
-    int i, jj, l;
+    const int64_t q = row0 + (idx - static_cast<int64_t>(j) * m);   // global row: Omega is keyed on it (8(e)
+    int i, jj, l;                                                     // route (i), no halo needed)
     grad_node(g, q, i, jj, l);
     int64_t op, om;
     double w;

@@ -350,7 +350,6 @@ const char* validate(const oid_params* p) {
     if (p->grad_nx < 1 || p->grad_ny < 1 || int64_t(p->grad_nfields) * p->grad_nx * p->grad_ny * nz != p->m)
       return "gradient variant: grad_nfields * grad_nx * grad_ny (* grad_nz) must equal m";
     if (!(p->grad_hz >= 0.0)) return "gradient variant: grad_hz must be >= 0";
-    if (p->row_begin != 0 || p->row_end != p->m) return "gradient variant: single shard only (row_begin = 0, row_end = m)";
     if ((p->grad_nz > 1 ? 4 : 3) * p->ell > 2048) return "gradient variant: (d + 1) ell must be <= 2048";
     if (!(p->grad_hx >= 0.0) || !(p->grad_hy >= 0.0)) return "gradient variant: spacings must be >= 0 (0 = 1/(N-1))";
   }
@@ -401,7 +400,12 @@ struct oid_ctx_s {
   int last_est_tag = 0;       // admission tag of the last estimated epoch (dirty = newer tags)
   int ga = 1;                 // 3 with the gradient variant (augmented sketch), else 1
   GradGrid grid{};
-  bool ogo_ready = false;     // Omega G^p Omega^T formed (gradient variant)
+  bool ogo_ready = false;     // Omega G^p Omega^T formed (gradient variant; sharded: this shard's
+                              // partial until the caller's reduction of oid_partials(3))
+  // stencil halos of the pending sketch (sharded gradient variant, oid_ingest_sketch_halo)
+  const void* halo_lo = nullptr;
+  const void* halo_hi = nullptr;
+  int64_t halo_ld_lo = 0, halo_ld_hi = 0;
   // cross-stream hazards when estimates run on another stream than the ingests:
   // committed = end of a commit (its snapshot taken); gram_done = estimate's basis reads
   // finished; sj_j = Alg 4 chain finished reading J; est_done = end of an estimate.
@@ -857,6 +861,14 @@ static oid_status launch_a9(oid_ctx ctx) {
   return OID_OK;
 }
 
+// rows of the stencil halo below (lo) / above this shard: an axis-0 neighbour is ny nz rows
+// away and no stencil reaches further (grad.cuh); 0 at the ends of the row range
+int64_t grad_halo_rows(oid_ctx ctx, bool lo) {
+  if (ctx->ga == 1) return 0;
+  const int64_t reach = static_cast<int64_t>(ctx->grid.ny) * ctx->grid.nz;
+  return lo ? std::min<int64_t>(ctx->p.row_begin, reach) : std::min<int64_t>(ctx->p.m - ctx->p.row_end, reach);
+}
+
 oid_status do_sketch(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_t st) {
   const oid_params& p = ctx->p;
   const Layout& L = ctx->L;
@@ -872,10 +884,15 @@ oid_status do_sketch(oid_ctx ctx, const void* X, int64_t ld, int nc, cudaStream_
   double* GX = ctx->d(L.GX);
   const int64_t gstride = m * p.b_max;
   const unsigned gb = static_cast<unsigned>(std::min<int64_t>(blocks_for(m * nc), 8 * ctx->num_sms));
+  const int64_t hlo = grad_halo_rows(ctx, true);
   if (p.dtype == OID_F64)
-    grad_stencil_kernel<double><<<gb, 256, 0, st>>>(static_cast<const double*>(X), ld, m, nc, ctx->grid, GX, gstride);
+    grad_stencil_kernel<double><<<gb, 256, 0, st>>>(static_cast<const double*>(X), ld, m, nc, ctx->grid, GX, gstride,
+                                                    p.row_begin, static_cast<const double*>(ctx->halo_lo), ctx->halo_ld_lo,
+                                                    hlo, static_cast<const double*>(ctx->halo_hi), ctx->halo_ld_hi);
   else
-    grad_stencil_kernel<float><<<gb, 256, 0, st>>>(static_cast<const float*>(X), ld, m, nc, ctx->grid, GX, gstride);
+    grad_stencil_kernel<float><<<gb, 256, 0, st>>>(static_cast<const float*>(X), ld, m, nc, ctx->grid, GX, gstride,
+                                                   p.row_begin, static_cast<const float*>(ctx->halo_lo), ctx->halo_ld_lo,
+                                                   hlo, static_cast<const float*>(ctx->halo_hi), ctx->halo_ld_hi);
   CKL();
   for (int q = 0; q < ctx->ga - 1; ++q) {
     s = sketch_one(ctx, GX + q * gstride, m, nc, st, ctx->d(L.YpG) + static_cast<size_t>(q) * (p.ell + 1) * p.b_max, true,
@@ -1322,8 +1339,11 @@ oid_status hutch_pre(oid_ctx ctx, cudaStream_t st, const double* P, const double
 // Omega G^p Omega^T (l x l, p = 0, 1), once per context: for chunks of sketch rows s, W = G^p
 // Omega(s, :)^T (the stencil applied to the generated rows, m x chunk), then Omega W through the
 // tensor-core K1 like any block (O(l m) generation + l/chunk K1 passes instead of O(l^2 m) Philox)
-oid_status grad_ogo(oid_ctx ctx, cudaStream_t st) {
+oid_status grad_ogo(oid_ctx ctx, cudaStream_t st, bool explicit_call = false) {
   if (ctx->ogo_ready) return OID_OK;
+  if (!explicit_call && (ctx->p.row_begin != 0 || ctx->p.row_end != ctx->p.m))
+    return ctx->fail(OID_ESTATE, "sharded gradient variant: call oid_gradient_ogo and sum oid_partials(3) over the "
+                     "shards before the GCV");
   const Layout& L = ctx->L;
   const int ell = ctx->p.ell;
   const int64_t m = ctx->m_loc;
@@ -1334,7 +1354,8 @@ oid_status grad_ogo(oid_ctx ctx, cudaStream_t st) {
     for (int s0 = 0; s0 < ell; s0 += chunk) {
       const int ns = std::min(chunk, ell - s0);
       const unsigned g = static_cast<unsigned>(std::min<int64_t>(blocks_for(m * ns), 8 * ctx->num_sms));
-      omega_g_cols_kernel<<<g, 256, 0, st>>>(s0, ns, m, ctx->grid, p, ctx->key0, ctx->key1, ctx->qscale, W);
+      omega_g_cols_kernel<<<g, 256, 0, st>>>(s0, ns, m, ctx->grid, p, ctx->key0, ctx->key1, ctx->qscale, W,
+                                             ctx->p.row_begin);
       CKL();
       oid_status s = sketch_one(ctx, W, m, ns, st, Y, true, false);
       if (s != OID_OK) return s;
@@ -1669,13 +1690,35 @@ oid_status oid_init(const oid_params* p, void* workspace, size_t bytes, void* st
 }
 
 oid_status oid_ingest_sketch(oid_ctx ctx, const void* X, int64_t ld, int32_t ncols, void* stream) {
+  return oid_ingest_sketch_halo(ctx, X, ld, ncols, nullptr, 0, nullptr, 0, stream);
+}
+
+oid_status oid_ingest_sketch_halo(oid_ctx ctx, const void* X, int64_t ld, int32_t ncols, const void* X_lo,
+                                  int64_t ld_lo, const void* X_hi, int64_t ld_hi, void* stream) {
   NvtxRange nvtx_range("oid_ingest_sketch");
   if (!ctx) return OID_EINVAL;
   oid_status s = check_block(ctx, X, ld, ncols);
   if (s != OID_OK) return s;
+  const int64_t hlo = grad_halo_rows(ctx, true), hhi = grad_halo_rows(ctx, false);
+  if (ncols > 0 && ((hlo > 0 && (!X_lo || ld_lo < hlo)) || (hhi > 0 && (!X_hi || ld_hi < hhi))))
+    return ctx->fail(OID_EINVAL, "sharded gradient variant: the block needs stencil halos of %lld rows below and %lld "
+                     "above (oid_grad_halo; got %p ld %lld, %p ld %lld)", static_cast<long long>(hlo),
+                     static_cast<long long>(hhi), X_lo, static_cast<long long>(ld_lo), X_hi,
+                     static_cast<long long>(ld_hi));
+  ctx->halo_lo = X_lo;
+  ctx->halo_hi = X_hi;
+  ctx->halo_ld_lo = ld_lo;
+  ctx->halo_ld_hi = ld_hi;
   ctx->pending_nc = ncols;
   if (ncols == 0) return OID_OK;
   return do_sketch(ctx, X, ld, ncols, static_cast<cudaStream_t>(stream));
+}
+
+oid_status oid_grad_halo(oid_ctx ctx, int64_t* rows_lo, int64_t* rows_hi) {
+  if (!ctx || !rows_lo || !rows_hi) return OID_EINVAL;
+  *rows_lo = grad_halo_rows(ctx, true);
+  *rows_hi = grad_halo_rows(ctx, false);
+  return OID_OK;
 }
 
 oid_status oid_ingest_commit(oid_ctx ctx, const void* X, int64_t ld, int32_t ncols, void* stream) {
@@ -1711,6 +1754,12 @@ oid_status oid_partials(oid_ctx ctx, int32_t which, double** dev_ptr, int64_t* c
   } else if (which == 1) {
     *dev_ptr = ctx->d(ctx->L.Gsum) + static_cast<size_t>(ctx->est_par) * ctx->t * ctx->t;
     *count = int64_t(ctx->t) * ctx->t;
+  } else if (which == 2 && ctx->ga > 1) {   // [Y_p; n_p], p = 1..d, each (ell + 1) b_max apart
+    *dev_ptr = ctx->d(ctx->L.YpG);
+    *count = int64_t(ctx->ga - 1) * (ctx->p.ell + 1) * ctx->p.b_max;
+  } else if (which == 3 && ctx->ga > 1) {   // Omega G^p Omega^T, p = 1..d (ell x ell each)
+    *dev_ptr = ctx->d(ctx->L.OGO);
+    *count = int64_t(ctx->ga - 1) * ctx->p.ell * ctx->p.ell;
   } else {
     return OID_EINVAL;
   }
@@ -1867,6 +1916,16 @@ oid_status oid_error_estimate(oid_ctx ctx, double* out_host, void* stream) {
   CK(cudaMemcpyAsync(out_host, ctx->d(ctx->L.est), 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   return OID_OK;
+}
+
+oid_status oid_gradient_ogo(oid_ctx ctx, void* stream) {
+  if (!ctx) return OID_EINVAL;
+  if (ctx->ga == 1) return ctx->fail(OID_ESTATE, "gradient variant not enabled (grad_nfields = 0)");
+  if (ctx->ogo_ready) return OID_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  oid_status s = join_side(ctx, st);
+  if (s != OID_OK) return s;
+  return grad_ogo(ctx, st, true);
 }
 
 oid_status oid_gradient_gcv(oid_ctx ctx, double mu, double* gcv_out, void* stream) {

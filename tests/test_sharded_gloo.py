@@ -123,3 +123,96 @@ def test_two_rank_gloo_matches_single():
         assert np.array_equal(J, ref.J), (rank, J, ref.J)
         assert np.linalg.norm(P - ref.P) / np.linalg.norm(ref.P) < 1e-10
         assert abs(est_rel - ref_est["est_rel"]) < 1e-10
+
+
+# ---------------------------------------------------------------- gradient variant across slabs
+# SURVEY 8(e) route (ii): each block's stencil halos come from the neighbouring ranks, so the
+# shards' parts Omega[:, slab] (G^p X)[slab] of the gradient sketches sum to Omega G^p X.
+GNF, GNX, GNY, GNC = 2, 10, 12, 5
+
+
+class HaloShardEngine:
+    """Test double of the engine's sharded gradient interface: (G^p X)[slab] from the halo-extended
+    slab with the oracle's stencil matrices, sketched by a test-local dense Omega on global rows."""
+
+    def __init__(self, rb, re, m, Om):
+        from oracle.gradient import grid_gradient_operators
+        self.rb, self.re, self.m, self.Om = rb, re, m, Om
+        self.G = grid_gradient_operators(GNF, GNX, GNY)
+        self.reach = GNY                         # one axis-0 neighbour = ny rows (2-D grid)
+        self.halos = None
+        self._p0 = self._p2 = None
+
+    def grad_halo(self):
+        return min(self.rb, self.reach), min(self.m - self.re, self.reach)
+
+    def ingest_sketch(self, X, lo=None, hi=None):
+        hlo, hhi = self.grad_halo()
+        assert (0 if lo is None else lo.shape[0]) == hlo and (0 if hi is None else hi.shape[0]) == hhi
+        parts = [t.numpy() for t in (lo, X, hi) if t is not None]
+        ext = np.vstack(parts)
+        self.halos = (None if lo is None else lo.numpy().copy(), None if hi is None else hi.numpy().copy())
+        Om = self.Om[:, self.rb:self.re]
+        self._p0 = torch.from_numpy(np.ascontiguousarray(Om @ X.numpy()).ravel())
+        gx = [Gp[self.rb:self.re, self.rb - hlo:self.re + hhi] @ ext for Gp in self.G]
+        self._p2 = torch.from_numpy(np.concatenate([(Om @ g).ravel() for g in gx]))
+
+    def partials(self, which):
+        return {0: self._p0, 2: self._p2}[which]
+
+    def ingest_commit(self, X):
+        self.committed = (self._p0.numpy().copy(), self._p2.numpy().copy())
+
+
+def _halo_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2405_16076_b200.sharded import ShardedIngest
+        m = GNF * GNX * GNY
+        rng = np.random.default_rng(3)
+        A = rng.standard_normal((m, GNC))
+        Om = rng.standard_normal((7, m))
+        cuts = [0, 64, 160, m][: world + 1] if world == 3 else [0, 128, m]
+        rb, re = cuts[rank], cuts[rank + 1]
+        eng = HaloShardEngine(rb, re, m, Om)
+        drv = ShardedIngest(eng)
+        drv.ingest(torch.from_numpy(np.asfortranarray(A[rb:re])))
+        q.put((rank, (rb, re), eng.halos, eng.committed))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gradient_halo_exchange_gloo(world):
+    from oracle.gradient import grid_gradient_operators
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_halo_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=600) for _ in range(world)], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    m = GNF * GNX * GNY
+    rng = np.random.default_rng(3)
+    A = rng.standard_normal((m, GNC))
+    Om = rng.standard_normal((7, m))
+    G = grid_gradient_operators(GNF, GNX, GNY)
+    for rank, (rb, re), (lo, hi), (p0, p2) in res:
+        # halos are exactly the neighbouring global rows (clipped at the ends of the row range)
+        if rb == 0:
+            assert lo is None
+        else:
+            assert np.array_equal(lo, A[rb - min(rb, GNY):rb])
+        if re == m:
+            assert hi is None
+        else:
+            assert np.array_equal(hi, A[re:re + min(m - re, GNY)])
+        # the reduced partials equal the unsharded sketches [Omega X] and [Omega G^p X]
+        assert np.allclose(p0, (Om @ A).ravel(), rtol=0, atol=1e-12)
+        ref2 = np.concatenate([(Om @ (Gp @ A)).ravel() for Gp in G])
+        assert np.allclose(p2, ref2, rtol=0, atol=1e-10)
